@@ -1,0 +1,276 @@
+"""Pins for oracle/mlp.py, energy.py, losses.py, adam.py, critic.py (contracts C2-C8), CPU.
+
+Every pin is independent of the function it checks: hand values and closed forms from the
+paper's definitions (tests/golden/closed_forms.txt), invariants (shift invariance, row /
+column sums of the softmax gradient, sign and range of the energies), and central finite
+differences in fp64 of the scalar loss through the whole path."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import adam, critic, energy, losses, mlp
+
+ENERGIES = ["l2", "dot", "cos"]
+KINDS = ["fwd", "bwd", "sym"]
+
+
+def fd_grad(f, x, h=1e-6):
+    x = np.array(x, np.float64)
+    g = np.zeros_like(x)
+    flat, gf = x.ravel(), g.ravel()
+    for i in range(flat.size):
+        old = flat[i]
+        flat[i] = old + h; fp = f(x)
+        flat[i] = old - h; fm = f(x)
+        flat[i] = old
+        gf[i] = (fp - fm) / (2 * h)
+    return g
+
+
+def rel_err(a, b):
+    return np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-30)
+
+
+# ------------------------------------------------------------------------------ energies
+
+def test_energy_hand_values(closed_forms):
+    z, p = np.array([[0.0, 0.0]]), np.array([[3.0, 4.0]])
+    assert abs(energy.logits("l2", z, p)[0, 0] - closed_forms["l2_345"]) < 1e-12
+    assert energy.logits("dot", np.array([[1.0, 2.0]]), np.array([[3.0, 4.0]]))[0, 0] == closed_forms["dot_12_34"]
+    u = np.array([[0.3, -1.2, 2.0]])
+    assert abs(energy.logits("cos", u, u)[0, 0] - closed_forms["cos_identical"]) < 1e-15
+    assert abs(energy.logits("cos", np.array([[1.0, 0]]), np.array([[0, 2.0]]))[0, 0]
+               - closed_forms["cos_orthogonal"]) < 1e-15
+
+
+def test_energy_ranges_and_diag():
+    rng = np.random.default_rng(0)
+    phi, psi = rng.standard_normal((9, 5)), rng.standard_normal((9, 5))
+    l2 = energy.logits("l2", phi, psi)
+    assert np.all(l2 < 0)
+    assert abs(energy.logits("l2", phi, phi)[3, 3] + 1e-6) < 1e-12       # -sqrt(eps2)
+    c = energy.logits("cos", phi, psi)
+    assert np.all(np.abs(c) <= 1 + 1e-12)
+    for k in ENERGIES:
+        assert np.allclose(np.diag(energy.logits(k, phi, psi)), energy.diag_logits(k, phi, psi))
+    # L2 logits are symmetric in their two arguments
+    assert np.allclose(energy.logits("l2", phi, psi), energy.logits("l2", psi, phi).T)
+
+
+@pytest.mark.parametrize("kind", ENERGIES)
+def test_energy_vjp_finite_differences(kind):
+    rng = np.random.default_rng(1)
+    N, D = 5, 4
+    phi, psi = rng.standard_normal((N, D)), rng.standard_normal((N, D))
+    G = rng.standard_normal((N, N))
+    dphi, dpsi = energy.vjp(kind, phi, psi, G)
+    fphi = fd_grad(lambda x: (energy.logits(kind, x, psi) * G).sum(), phi)
+    fpsi = fd_grad(lambda x: (energy.logits(kind, phi, x) * G).sum(), psi)
+    assert rel_err(dphi, fphi) < 1e-7
+    assert rel_err(dpsi, fpsi) < 1e-7
+
+
+# ------------------------------------------------------------------------------ losses
+
+def test_loss_closed_forms(closed_forms):
+    z = np.zeros((2, 2))
+    c, _ = losses.loss_and_grad(z, "fwd", 0.1)
+    assert abs(c["L_fwd"] - closed_forms["infonce_fwd_zero2x2"]) < 1e-15
+    assert abs(c["penalty"] - closed_forms["penalty_zero2x2_b01"]) < 1e-15
+    c, _ = losses.loss_and_grad(z, "sym", 0.0)
+    assert abs(c["total"] - closed_forms["infonce_sym_zero2x2"]) < 1e-15
+    c, _ = losses.loss_and_grad(np.eye(2), "fwd", 0.0)
+    assert abs(c["total"] - closed_forms["infonce_fwd_eye2"]) < 1e-15
+    I4 = np.eye(4)
+    c, _ = losses.loss_and_grad(energy.logits("dot", I4, I4), "fwd", 0.0)
+    assert abs(c["total"] - closed_forms["infonce_fwd_onehot4"]) < 1e-14
+    c, _ = losses.loss_and_grad(energy.logits("l2", I4, I4), "fwd", 0.0)
+    assert abs(c["total"] - closed_forms["infonce_fwd_orthl2_4"]) < 1e-5   # eps2 = 1e-12 perturbs
+
+
+@pytest.mark.parametrize("N", [3, 8])
+def test_loss_all_equal_logits(N):
+    cval, beta = -2.5, 0.1
+    comps, _ = losses.loss_and_grad(np.full((N, N), cval), "sym", beta)
+    assert abs(comps["L_fwd"] - math.log(N)) < 1e-13
+    assert abs(comps["L_bwd"] - math.log(N)) < 1e-13
+    assert abs(comps["penalty"] - beta * (cval + math.log(N)) ** 2) < 1e-13
+
+
+def test_loss_shift_invariance_and_gradient_sums():
+    rng = np.random.default_rng(2)
+    l = rng.standard_normal((6, 6))
+    a, _ = losses.loss_and_grad(l, "sym", 0.1)
+    b, _ = losses.loss_and_grad(l + 3.7, "sym", 0.1)
+    assert abs(a["L_fwd"] - b["L_fwd"]) < 1e-13 and abs(a["L_bwd"] - b["L_bwd"]) < 1e-13
+    assert abs(a["penalty"] - b["penalty"]) > 1e-3                     # penalty is not invariant
+    assert np.allclose(b["lse_row"], a["lse_row"] + 3.7)
+    _, Gf = losses.loss_and_grad(l, "fwd", 0.0)
+    _, Gb = losses.loss_and_grad(l, "bwd", 0.0)
+    assert np.allclose(Gf.sum(1), 0, atol=1e-15)                        # softmax rows sum to 1
+    assert np.allclose(Gb.sum(0), 0, atol=1e-15)
+    _, Gs = losses.loss_and_grad(l, "sym", 0.0)
+    assert np.allclose(Gs, Gf + Gb, rtol=0, atol=1e-16)
+    cs, _ = losses.loss_and_grad(l, "sym", 0.0)
+    cf, _ = losses.loss_and_grad(l, "fwd", 0.0)
+    cb, _ = losses.loss_and_grad(l, "bwd", 0.0)
+    assert cs["total"] == cf["total"] + cb["total"]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("beta", [0.0, 0.1])
+def test_loss_gradient_finite_differences(kind, beta):
+    rng = np.random.default_rng(3)
+    l = rng.standard_normal((5, 5)) * 2
+    _, G = losses.loss_and_grad(l, kind, beta)
+    fd = fd_grad(lambda x: losses.loss_and_grad(x, kind, beta)[0]["total"], l)
+    assert rel_err(G, fd) < 1e-8
+
+
+def test_loss_increasing_diagonal_lowers_loss():
+    rng = np.random.default_rng(4)
+    l = rng.standard_normal((7, 7))
+    for k in KINDS:
+        a, _ = losses.loss_and_grad(l, k, 0.0)
+        b, _ = losses.loss_and_grad(l + 0.5 * np.eye(7), k, 0.0)
+        assert b["total"] < a["total"]
+
+
+# ------------------------------------------------------------------------------ MLP
+
+def test_mlp_zero_weights_gives_output_bias():
+    rng = np.random.default_rng(5)
+    dims = mlp.layer_dims(4, 2, 6, 3)
+    layers = [(np.zeros(d), rng.standard_normal(d[1]) if i == len(dims) - 1 else rng.standard_normal(d[1]))
+              for i, d in enumerate(dims)]
+    layers = [(np.zeros((fi, fo)), b) for (fi, fo), (_, b) in zip(dims, layers)]
+    y, _ = mlp.forward(layers, rng.standard_normal((5, 4)), "silu")
+    assert np.allclose(y, layers[-1][1][None, :])
+
+
+def test_mlp_linear_layer_closed_form():
+    rng = np.random.default_rng(6)
+    W, b = rng.standard_normal((4, 3)), rng.standard_normal(3)
+    X, dY = rng.standard_normal((6, 4)), rng.standard_normal((6, 3))
+    y, cache = mlp.forward([(W, b)], X)
+    assert np.allclose(y, X @ W + b)
+    (gw, gb), = mlp.backward([(W, b)], cache, dY)[0]
+    assert np.allclose(gw, sum(np.outer(X[i], dY[i]) for i in range(6)))
+    assert np.allclose(gb, dY.sum(0))
+
+
+@pytest.mark.parametrize("act", ["silu", "relu"])
+def test_mlp_backward_finite_differences(act):
+    rng = np.random.default_rng(7)
+    layers = [(rng.standard_normal((fi, fo)) * 0.7, rng.standard_normal(fo) * 0.3)
+              for fi, fo in mlp.layer_dims(3, 2, 5, 4)]
+    X, C = rng.standard_normal((6, 3)), rng.standard_normal((6, 4))
+    flat = mlp.pack(layers)
+
+    def f(p):
+        ls, _ = mlp.unpack(p, 3, 2, 5, 4)
+        return (mlp.forward(ls, X, act)[0] * C).sum()
+
+    _, cache = mlp.forward(layers, X, act)
+    grads, _ = mlp.backward(layers, cache, C, act)
+    assert rel_err(mlp.pack(grads), fd_grad(f, flat)) < 1e-7
+
+
+def test_activation_values():
+    z = np.array([-2.0, 0.0, 1.5])
+    assert np.allclose(mlp.act_fn(z, "silu"), z / (1 + np.exp(-z)))
+    assert mlp.act_fn(np.array([0.0]), "silu")[0] == 0.0
+    assert mlp.act_grad(np.array([0.0]), "relu")[0] == 0.0
+    assert abs(mlp.act_grad(np.array([0.0]), "silu")[0] - 0.5) < 1e-15
+
+
+# ------------------------------------------------------------------------------ Adam
+
+def test_adam_zero_gradient_is_identity():
+    p = np.array([1.0, -2.0, 3.0])
+    p2, m2, v2, t2 = adam.adam_step(p, np.zeros(3), np.zeros(3), np.zeros(3), 0)
+    assert np.array_equal(p2, p) and t2 == 1
+
+
+def test_adam_first_step_closed_form():
+    g = np.array([1e-3, -2.0, 5e-9, 0.3])
+    p2, *_ = adam.adam_step(np.zeros(4), g, np.zeros(4), np.zeros(4), 0, lr=0.01)
+    assert np.allclose(p2, -0.01 * g / (np.abs(g) + 1e-8), rtol=1e-12, atol=0)
+
+
+def test_adam_quadratic_recurrence():
+    th, m, v, t = np.array([1.0]), np.zeros(1), np.zeros(1), 0
+    for _ in range(100):
+        th, m, v, t = adam.adam_step(th, 2 * th, m, v, t, lr=0.1)
+    assert abs(th[0]) < 0.1
+
+
+def test_adam_rejects_non_finite():
+    with pytest.raises(FloatingPointError):
+        adam.adam_step(np.zeros(2), np.array([np.nan, 0]), np.zeros(2), np.zeros(2), 0)
+
+
+# ------------------------------------------------------------------------------ whole step
+
+TINY = dict(obs_dim=3, act_dim=2, goal_dim=2, depth=2, width=5, repr_dim=4)
+
+
+def _tiny_problem(seed, N=6):
+    rng = np.random.default_rng(seed)
+    n_phi = sum(i * o + o for i, o in mlp.layer_dims(5, 2, 5, 4))
+    n_psi = sum(i * o + o for i, o in mlp.layer_dims(2, 2, 5, 4))
+    params = rng.standard_normal(n_phi + n_psi) * 0.6
+    s, a, g = rng.standard_normal((N, 3)), rng.uniform(-1, 1, (N, 2)), rng.standard_normal((N, 2))
+    return params, s, a, g
+
+
+@pytest.mark.parametrize("kind", ENERGIES)
+@pytest.mark.parametrize("loss_kind", KINDS)
+@pytest.mark.parametrize("act", ["silu", "relu"])
+def test_critic_gradient_end_to_end_finite_differences(kind, loss_kind, act):
+    params, s, a, g = _tiny_problem(8)
+    kw = dict(TINY, energy_kind=kind, loss_kind=loss_kind, beta=0.1, activation=act)
+    out = critic.critic_forward_backward(params, s, a, g, **kw)
+    fd = fd_grad(lambda p: critic.critic_forward_backward(p, s, a, g, **kw)["total"], params)
+    assert rel_err(out["grads"], fd) < 1e-6
+
+
+def test_critic_step_applies_adam_to_the_gradient():
+    params, s, a, g = _tiny_problem(9)
+    z = np.zeros_like(params)
+    out = critic.critic_step(params, z, z, 0, s, a, g, lr=1e-3, **TINY)
+    gr = out["grads"]
+    assert np.allclose(out["params_new"], params - 1e-3 * gr / (np.abs(gr) + 1e-8))
+    assert out["t_new"] == 1
+
+
+def test_critic_step_descends():
+    params, s, a, g = _tiny_problem(10, N=8)
+    p, m, v, t = params, np.zeros_like(params), np.zeros_like(params), 0
+    l0 = critic.critic_forward_backward(p, s, a, g, **TINY)["total"]
+    for _ in range(5):
+        o = critic.critic_step(p, m, v, t, s, a, g, lr=1e-2, **TINY)
+        p, m, v, t = o["params_new"], o["m_new"], o["v_new"], o["t_new"]
+    assert critic.critic_forward_backward(p, s, a, g, **TINY)["total"] < l0
+
+
+@pytest.mark.parametrize("kind", ENERGIES)
+def test_actor_loss_finite_differences(kind):
+    rng = np.random.default_rng(11)
+    N = 5
+    params, s, _, g = _tiny_problem(12, N=N)
+    n_pi = sum(i * o + o for i, o in mlp.layer_dims(5, 2, 6, 4))
+    pi = rng.standard_normal(n_pi) * 0.5
+    eps = rng.standard_normal((N, 2))
+    kw = dict(TINY, actor_depth=2, actor_width=6, energy_kind=kind, alpha_ent=0.2)
+    out = critic.actor_loss(pi, params, s, g, eps, **kw)
+    fd = fd_grad(lambda p: critic.actor_loss(p, params, s, g, eps, **kw)["loss"], pi)
+    assert rel_err(out["grads"], fd) < 1e-6
+    assert np.all(np.abs(out["a_new"]) < 1)
+
+
+def test_bf16_round_is_round_to_nearest_even():
+    x = np.array([1.0, 1.0 + 2**-8, 1.0 + 3 * 2**-8, -3.14159], np.float32)
+    r = critic.bf16_round(x)
+    assert r[0] == 1.0 and r[1] == 1.0 and r[2] == 1.0 + 2**-6 and abs(r[3] + 3.140625) < 1e-12
