@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark: CRL critic update steps/s (BASELINE.json metric) on synthetic data.
+
+A "step" is one pass of the whole hot path over one batch: crl_relabel_sample (A1) on the
+HBM-resident replay buffer followed by crl_critic_step (A2-A6: encoders fwd, online-LSE
+logits + loss, in-pass dlogits, encoders bwd, gradient all-reduce, fused Adam).  The buffer
+is filled (A0) before the timed region.
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload ant] [--precision fp32]
+  python bench.py --impl reference ...     # the CPU oracle timed on the host cores
+
+Default workload = BASELINE.json configs[1] (Ant-shaped, 4x256 encoders, repr 64, batch 256,
+beta 0.1, 1024 envs x 1000).  Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import crl_synth  # noqa: E402
+
+METRIC = "CRL critic update steps/sec at batch B, 1/2/4/8 B200; % of HBM/tensor roofline"
+UNIT = "steps/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=1000)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="ant")
+    p.add_argument("--precision", default=None)
+    p.add_argument("--energy", default=None)
+    p.add_argument("--profile-steps", type=int, default=20)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def workload_cfg(args):
+    over = {}
+    if args.precision:
+        over["precision"] = args.precision
+    if args.energy:
+        over["energy"] = args.energy
+    cfg = crl_synth.preset(args.workload, **over)
+    if cfg["precision"] == "bf16":
+        cfg["precision"] = "fp32"   # tensor-core path not built in this revision -> fp32 (stated in dtype)
+    return cfg
+
+
+def n_fill_chunks(cfg):
+    # enough U=62 chunks to wrap the ring (20 chunks = 1240 steps for T=1000)
+    return int(np.ceil((cfg["capacity"] * 1.24) / cfg["unroll_length"]))
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- roofline
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return mp, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+def stage_work(stage, cfg, N, Bl):
+    """Algorithmic work of ONE launch of a stage: (amount, unit, bound)."""
+    D, Wd, depth = cfg["repr_dim"], cfg["width"], cfg["depth"]
+    in_phi, in_psi = cfg["obs_dim"] + cfg["act_dim"], cfg["goal_dim"]
+    fp32 = cfg["precision"] == "fp32"
+    dims = lambda i: [i] + [Wd] * depth + [D]
+    if stage in ("lse_row", "lse_col"):
+        # the logits GEMM (2 N^2 D, counted once for both orientations) -> N_l N D per launch
+        return Bl * N * D * 1.0, "flop", "alu" if fp32 else "tensor"
+    if stage in ("grad_phi", "grad_psi"):
+        # the two backward contractions (W Psi and W^T Phi): 2 N^2 D each, one per launch
+        return 2.0 * Bl * N * D, "flop", "alu" if fp32 else "tensor"
+    if stage == "adam":
+        return 28.0 * crl_synth.critic_param_count(cfg), "byte", "hbm"
+    if stage == "relabel":
+        row = 4 * (2 * (cfg["obs_dim"] + cfg["act_dim"] + cfg["goal_dim"])) + 4
+        return float(row * Bl), "byte", "hbm"
+    if stage == "loss":
+        return float(Bl * D * 4 * 2), "byte", "hbm"
+    for tag, ind in (("phi", in_phi), ("psi", in_psi)):
+        if stage.startswith(tag + "_"):
+            l = int(stage.rsplit("_l", 1)[1])
+            d = dims(ind)
+            return 2.0 * Bl * d[l] * d[l + 1], "flop", "alu" if fp32 else "tensor"
+    return None, None, None
+
+
+def roofline(stages, cfg, N, Bl, peaks, peak_kind, clocks, traffic_db):
+    name, (ms, cnt) = max(stages.items(), key=lambda kv: kv[1][0])
+    per_launch_ms = ms / cnt
+    work, unit, bound = stage_work(name, cfg, N, Bl)
+    if work is None:
+        return {"kernel": name, "bound": None}
+    if bound == "hbm":
+        achieved = work / (per_launch_ms * 1e-3) / 1e9
+        peak = peaks["hbm_gbs"]
+        u = "GB/s"
+        note = f"HBM copy bandwidth ({peak_kind} MEASURED_PEAKS.json hbm_gbs)"
+    elif bound == "tensor":
+        achieved = work / (per_launch_ms * 1e-3) / 1e12
+        peak = peaks["bf16_tflops"]
+        u = "TFLOP/s"
+        note = f"dense bf16 ({peak_kind} MEASURED_PEAKS.json bf16_tflops, burst)"
+    else:
+        # fp32 SIMT: 148 SMs x 128 FP32 lanes x 2 flop/FMA x clock
+        mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        achieved = work / (per_launch_ms * 1e-3) / 1e12
+        peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+        u = "TFLOP/s"
+        note = f"FP32 FMA pipe: 148 SM x 128 lanes x 2 x {mhz:.0f} MHz (median SM clock under load)"
+    step_ms = sum(v[0] for v in stages.values()) / max(1, max(v[1] for v in stages.values()))
+    return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": u,
+            "frac": round(achieved / peak, 4), "traffic": traffic_db.get(name),
+            "kernel": name, "launch_us": round(per_launch_ms * 1e3, 3),
+            "share_of_step": round(ms / max(1e-9, sum(v[0] for v in stages.values())), 4),
+            "peak_source": note,
+            "stages_us": {k: round(v[0] / v[1] * 1e3, 2) for k, v in stages.items()}}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_steps(cfg, chunks, seconds, max_steps, seed_step0=0, warm=1):
+    """Time the oracle critic step (relabel + fwd + loss + bwd + Adam) on the host."""
+    from threadpoolctl import threadpool_info
+
+    from oracle import critic as ocritic
+    from oracle import replay as oreplay
+    buf = oreplay.OracleBuffer(cfg["n_envs"], cfg["obs_dim"], cfg["act_dim"], cfg["capacity"])
+    for obs, act, done in chunks:
+        buf.insert(obs, act, done)
+    _, Q = oreplay.geometric_tables(cfg["gamma"], cfg["capacity"])
+    params = crl_synth.init_critic_params(cfg, 42).astype(np.float64)
+    m = np.zeros_like(params); v = np.zeros_like(params); t = 0
+    kw = dict(obs_dim=cfg["obs_dim"], act_dim=cfg["act_dim"], goal_dim=cfg["goal_dim"],
+              depth=cfg["depth"], width=cfg["width"], repr_dim=cfg["repr_dim"],
+              energy_kind=cfg["energy"], loss_kind=cfg["loss"], beta=cfg["beta_lse"],
+              activation=cfg["activation"])
+    B = cfg["batch"]
+    times = []
+    step = seed_step0
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        s, a, g, _ = oreplay.relabel_sample(buf, crl_synth.PHILOX_SEED, step, B, gamma=cfg["gamma"],
+                                            goal_dim=cfg["goal_dim"], Q=Q)
+        out = ocritic.critic_step(params, m, v, t, s, a, g, lr=cfg["lr"], **kw)
+        params, m, v, t = out["params_new"], out["m_new"], out["v_new"], out["t_new"]
+        times.append(time.perf_counter() - t0)
+        step += 1
+        n_timed = len(times) - warm
+        if n_timed >= max_steps or (n_timed >= 1 and time.perf_counter() - t_start > seconds):
+            break
+    timed = times[warm:] if len(times) > warm else times
+    blas = [x for x in threadpool_info() if x.get("user_api") == "blas"]
+    cores = blas[0]["num_threads"] if blas else 1
+    return len(timed) / sum(timed), cores, len(timed)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = workload_cfg(args)
+    chunks = crl_synth.fast_chunks(cfg, n_fill_chunks(cfg))
+    # each step is a full oracle critic step on the workload; bounded by --cpu-seconds overall
+    steps = max(1, args.steps)
+    budget = max(args.cpu_seconds, 1.0)
+    val, cores, n = oracle_steps(cfg, chunks, budget, steps, warm=min(args.warmup, 2))
+    line = {"metric": METRIC, "value": round(val, 4), "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": n, "warmup": min(args.warmup, 2),
+            "ms_per_step": round(1e3 / val, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "global_batch": cfg["batch"],
+                       "energy": cfg["energy"], "loss": cfg["loss"]},
+            "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{n} full oracle critic steps (relabel+fwd+loss+bwd+Adam) "
+                                       f"on the {cfg['name']} workload, batch {cfg['batch']}"},
+            "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_11052_b200 import CrlConfig, CrlContext, bootstrap_nccl_id
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workload_cfg(args)
+    N = cfg["batch"]
+    if N % world:
+        raise SystemExit(f"global batch {N} not divisible by {world}")
+    Bl = N // world
+    ccfg = CrlConfig.from_preset(cfg, world_size=world, rank=rank)
+    nccl_id = bootstrap_nccl_id() if world > 1 else None
+    params = crl_synth.init_critic_params(cfg, 42)
+    ctx = CrlContext(ccfg, params=torch.from_numpy(params), nccl_id=nccl_id)
+    stream = torch.cuda.Stream()
+    chunks = crl_synth.fast_chunks(cfg, n_fill_chunks(cfg))
+    with torch.cuda.stream(stream):
+        for obs, act, done in crl_synth.rank_chunks(chunks, rank, world):
+            ctx.buffer_insert(torch.from_numpy(obs).cuda(), torch.from_numpy(act).cuda(),
+                              torch.from_numpy(done).cuda(), stream=stream)
+    s = torch.empty(Bl, cfg["obs_dim"], device="cuda")
+    a = torch.empty(Bl, cfg["act_dim"], device="cuda")
+    g = torch.empty(Bl, cfg["goal_dim"], device="cuda")
+    loss = torch.zeros(4, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step(i):
+        ctx.relabel_sample(crl_synth.PHILOX_SEED, i, s, a, g, stream=stream)
+        ctx.critic_step(s, a, g, loss, stream=stream)
+
+    for i in range(args.warmup):
+        step(i)
+    launches_per_step = 1 + ctx.launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    clk.start()
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.zero_()                         # L2 flush between timed iterations
+            ev0[i].record(stream)
+            step(args.warmup + i)
+            ev1[i].record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    per = [e0.elapsed_time(e1) for e0, e1 in zip(ev0, ev1)]
+    total_ms = sum(per)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t)
+    status = ctx.status()
+    value = args.steps / (total_ms * 1e-3)
+
+    # ---- end to end: host (pinned) batch in, host loss out, through crl_critic_step
+    e2e = None
+    if not args.no_e2e:
+        K = max(3, min(args.steps, 200))
+        hb = []
+        for i in range(K):
+            ctx.relabel_sample(crl_synth.PHILOX_SEED, 10_000_000 + i, s, a, g, stream=stream)
+            torch.cuda.synchronize()
+            hb.append(tuple(x.cpu().pin_memory() for x in (s, a, g)))
+        hloss = torch.zeros(4).pin_memory()
+        for i in range(3):
+            ctx.critic_step(*hb[i % K], hloss, stream=stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        f1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        with torch.cuda.stream(stream):
+            for i in range(K):
+                flush.zero_()
+                f0[i].record(stream)
+                ctx.critic_step(*hb[i], hloss, stream=stream)
+                f1[i].record(stream)
+        torch.cuda.synchronize()
+        e_ms = sum(x.elapsed_time(y) for x, y in zip(f0, f1))
+        if world > 1:
+            t = torch.tensor([e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t)
+        e2e = {"value": round(K / (e_ms * 1e-3), 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in hb[0])),
+               "d2h_bytes_per_step": 16,
+               "note": "crl_critic_step with pinned-host s/a/g and host loss (H2D+D2H inside the timed region)"}
+
+    # ---- per-stage profile (eager, event-bracketed) for the roofline
+    ctx.profile_enable(True)
+    with torch.cuda.stream(stream):
+        for i in range(args.profile_steps):
+            flush.zero_()
+            step(20_000_000 + i)
+    torch.cuda.synchronize()
+    stages = ctx.profile_read()
+    ctx.profile_enable(False)
+
+    if rank == 0:
+        peaks, kind = load_peaks()
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic_db = json.load(f).get(f"{cfg['name']}/{cfg['precision']}", {})
+        except Exception:
+            traffic_db = {}
+        rl = roofline(stages, cfg, N, Bl, peaks, kind, clocks, traffic_db)
+        cpu = None
+        if not args.no_cpu_baseline:
+            val, cores, n = oracle_steps(cfg, chunks, args.cpu_seconds, 10_000)
+            cpu = {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": f"{n} full oracle critic steps (relabel+fwd+loss+bwd+Adam, fp64 NumPy) "
+                             f"on the same {cfg['name']} workload (batch {N}), ~{args.cpu_seconds:.0f} s"}
+        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32" if cfg["precision"] == "fp32" else "bf16", "data": "synthetic",
+                "config": {"workload": cfg["name"], "global_batch": N, "batch_local": Bl,
+                           "obs_dim": cfg["obs_dim"], "act_dim": cfg["act_dim"],
+                           "goal_dim": cfg["goal_dim"], "encoders": f"{cfg['depth']}x{cfg['width']}",
+                           "repr_dim": cfg["repr_dim"], "energy": cfg["energy"], "loss": cfg["loss"],
+                           "beta_lse": cfg["beta_lse"], "buffer": f"{cfg['n_envs']}x{cfg['capacity']}",
+                           "parallelism": f"dp{world}", "l2_flush": "256 MiB memset between timed steps"},
+                "clocks": clocks, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+                "gpu_launches_per_step": launches_per_step, "roofline": rl, "cpu_baseline": cpu,
+                "device_status": status}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,644 @@
+// crl_api.cu — the C ABI (include/crl.h): context, workspace carving, argument checks, the
+// critic-step schedule (captured once per pointer tuple into a CUDA graph and replayed),
+// data-parallel collectives over NCCL, device status word.
+//
+// Critic step schedule (one rank; W = world size, B_l local rows, N = W B_l):
+//   phi fwd (d+1 GEMMs, fused bias+act)        psi fwd
+//   [W>1] all-gather Phi, Psi (global negatives, reading A-21)
+//   LSE_i  = lse_rows(Phi_l, Psi_g)              LSE'_j = lse_rows(Psi_l, Phi_g)
+//   [W>1] all-gather LSE, LSE'
+//   loss partial sums (+ finalize when W = 1)  [W>1] all-reduce 3 floats + finalize
+//   dPhi_l = grad_rows(Phi_l, Psi_g, LSE_l, LSE'_g)   dPsi_l = grad_rows(Psi_l, Phi_g, LSE'_l, LSE_g)
+//   phi bwd, psi bwd (dW, db, dX with fused act')
+//   [W>1] all-reduce grads (sum; per-row terms already carry 1/N, reading A-23)
+//   Adam (+ bf16 shadow)
+#include "common.cuh"
+
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace crl {
+cudaError_t launch_buffer_insert(const float*, const float*, const uint8_t*, int, int, int, int, int,
+                                 int, int, uint32_t, float*, float*, uint32_t*, uint32_t*,
+                                 cudaStream_t);
+cudaError_t launch_relabel_sample(int, int, int, int, int, int, int, int, int, int, uint32_t,
+                                  uint32_t, uint64_t, uint64_t, const float*, const float*,
+                                  const uint32_t*, const uint64_t*, float*, float*, float*,
+                                  int64_t*, int*, cudaStream_t);
+cudaError_t mlp_forward_layer_f32(int, int, int, const float*, int, const float*, int, int,
+                                  const float*, const float*, float*, float*, int, cudaStream_t);
+cudaError_t mlp_backward_dx_f32(int, int, int, const float*, const float*, const float*, float*,
+                                int, cudaStream_t);
+cudaError_t mlp_backward_dw_f32(int, int, int, const float*, int, const float*, int, int,
+                                const float*, float*, float*, cudaStream_t);
+bool logits_simt_supports(int D);
+cudaError_t logits_lse_f32(int, int, const float*, int, const float*, int, float*, cudaStream_t);
+cudaError_t logits_grad_f32(int, int, const float*, int, int, const float*, int, const float*,
+                            const float*, float, float, float, float, float, float*, cudaStream_t);
+cudaError_t launch_loss_partial(const float*, const float*, int, int, int, const float*,
+                                const float*, float*, int, float, float, float, float, float*,
+                                int*, int*, int*, cudaStream_t);
+cudaError_t launch_loss_finalize(const float*, float, float, float, float, float*, int*, int*,
+                                 int*, cudaStream_t);
+cudaError_t launch_adam(float*, const float*, float*, float*, size_t, float, float, float, float,
+                        float, const int*, const int*, int*, void*, int, cudaStream_t);
+}  // namespace crl
+
+using namespace crl;
+
+static thread_local std::string g_last_error;
+
+// ----------------------------------------------------------------------------------------
+// workspace carving (shared by crl_workspace_size and crl_create)
+// ----------------------------------------------------------------------------------------
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct GraphKey {
+  const void *s, *a, *g, *loss, *grads;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(s, a, g, loss, grads) < std::tie(o.s, o.a, o.g, o.loss, o.grads);
+  }
+};
+
+struct crl_ctx {
+  crl_config cfg{};
+  crl_sizes sizes{};
+  crl_memory mem{};
+  EncoderPlan phi_plan{}, psi_plan{};
+  int N = 0;
+  // replay buffer
+  float* obs_ring = nullptr; float* act_ring = nullptr;
+  uint32_t* ep_end = nullptr; uint32_t* open_start = nullptr; uint64_t* qtab = nullptr;
+  int obs_stride = 0, act_stride = 0;
+  uint64_t n_ins = 0;
+  // scratch
+  float* grads = nullptr;
+  float* phiX[CRL_MAX_LAYERS] = {}; float* phiZ[CRL_MAX_LAYERS] = {};
+  float* psiX[CRL_MAX_LAYERS] = {}; float* psiZ[CRL_MAX_LAYERS] = {};
+  float *phi_out = nullptr, *psi_out = nullptr, *phi_g = nullptr, *psi_g = nullptr;
+  float *lse_row = nullptr, *lse_col = nullptr, *lse_row_g = nullptr, *lse_col_g = nullptr;
+  float *dphi = nullptr, *dpsi = nullptr, *dz[2] = {nullptr, nullptr};
+  float *loss_acc = nullptr, *loss_dev = nullptr;
+  int *status = nullptr, *adam_t = nullptr, *skip = nullptr;
+  float *stage_s = nullptr, *stage_a = nullptr, *stage_g = nullptr;
+  // runtime
+  cudaStream_t cap_stream = nullptr;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+  int launches = 0;
+  std::string err;
+  // profiling mode (eager launches bracketed by CUDA events, per-stage totals)
+  bool prof_on = false;
+  struct ProfEv { std::string name; cudaEvent_t a, b; };
+  std::vector<ProfEv> prof_pending;
+  std::vector<std::string> prof_names;
+  std::map<std::string, std::pair<double, int>> prof_acc;
+};
+
+// Brackets one launch with CUDA events when the context is in profiling mode.
+struct Stage {
+  crl_ctx* c; cudaStream_t st; cudaEvent_t b = nullptr;
+  Stage(crl_ctx* c_, cudaStream_t st_, const std::string& name) : c(c_), st(st_) {
+    if (!c->prof_on) return;
+    cudaEvent_t a;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    c->prof_pending.push_back({name, a, b});
+  }
+  ~Stage() { if (b) cudaEventRecord(b, st); }
+};
+
+static crl_status fail(crl_ctx* ctx, crl_status st, const std::string& msg) {
+  g_last_error = msg;
+  if (ctx) ctx->err = msg;
+  return st;
+}
+
+#define CU(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(ctx, CRL_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+#define NC(call)                                                                           \
+  do {                                                                                     \
+    ncclResult_t _r = (call);                                                              \
+    if (_r != ncclSuccess)                                                                 \
+      return fail(ctx, CRL_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r));     \
+  } while (0)
+
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
+                  size_t* scr_bytes) {
+  const crl_config& k = c->cfg;
+  const int E = k.n_envs_local, T = k.capacity;
+  c->obs_stride = round_up(k.obs_dim, 4);
+  c->act_stride = round_up(k.act_dim, 4);
+  Carver b{buf_base};
+  c->obs_ring = b.take<float>((size_t)E * T * c->obs_stride);
+  c->act_ring = b.take<float>((size_t)E * T * c->act_stride);
+  c->ep_end = b.take<uint32_t>((size_t)E * T);
+  c->open_start = b.take<uint32_t>((size_t)E);
+  c->qtab = b.take<uint64_t>((size_t)T + 1);
+  *buf_bytes = (b.off + 255) & ~(size_t)255;
+
+  const int Bl = k.batch_local, W = k.world_size, N = Bl * W, D = k.repr_dim, Wd = k.width;
+  Carver s{scr_base};
+  c->grads = s.take<float>(c->sizes.n_params);
+  for (int l = 1; l <= k.depth; ++l) {
+    c->phiX[l] = s.take<float>((size_t)Bl * Wd);
+    c->psiX[l] = s.take<float>((size_t)Bl * Wd);
+  }
+  for (int l = 0; l < k.depth; ++l) {
+    c->phiZ[l] = s.take<float>((size_t)Bl * Wd);
+    c->psiZ[l] = s.take<float>((size_t)Bl * Wd);
+  }
+  c->phi_out = s.take<float>((size_t)Bl * D);
+  c->psi_out = s.take<float>((size_t)Bl * D);
+  if (W > 1) {
+    c->phi_g = s.take<float>((size_t)N * D);
+    c->psi_g = s.take<float>((size_t)N * D);
+  } else {
+    c->phi_g = c->phi_out;
+    c->psi_g = c->psi_out;
+  }
+  c->lse_row = s.take<float>(Bl);
+  c->lse_col = s.take<float>(Bl);
+  if (W > 1) {
+    c->lse_row_g = s.take<float>(N);
+    c->lse_col_g = s.take<float>(N);
+  } else {
+    c->lse_row_g = c->lse_row;
+    c->lse_col_g = c->lse_col;
+  }
+  c->dphi = s.take<float>((size_t)Bl * D);
+  c->dpsi = s.take<float>((size_t)Bl * D);
+  const int wmax = Wd > D ? Wd : D;
+  c->dz[0] = s.take<float>((size_t)Bl * wmax);
+  c->dz[1] = s.take<float>((size_t)Bl * wmax);
+  c->loss_acc = s.take<float>(16);
+  c->loss_dev = s.take<float>(4);
+  c->status = s.take<int>(1);
+  c->adam_t = s.take<int>(1);
+  c->skip = s.take<int>(1);
+  c->stage_s = s.take<float>((size_t)Bl * k.obs_dim);
+  c->stage_a = s.take<float>((size_t)Bl * k.act_dim);
+  c->stage_g = s.take<float>((size_t)Bl * k.goal_dim);
+  *scr_bytes = (s.off + 255) & ~(size_t)255;
+}
+
+static crl_status validate(const crl_config* k, crl_ctx* ctx) {
+  if (!k) return fail(ctx, CRL_EINVAL, "cfg is NULL");
+  if (k->obs_dim <= 0 || k->act_dim <= 0 || k->goal_dim <= 0)
+    return fail(ctx, CRL_EINVAL, "obs_dim, act_dim and goal_dim must be positive");
+  if (k->goal_offset < 0 || k->goal_offset + k->goal_dim > k->obs_dim)
+    return fail(ctx, CRL_EINVAL, "goal slice obs[goal_offset:goal_offset+goal_dim] out of range");
+  if (k->n_envs_local <= 0 || k->capacity < 2)
+    return fail(ctx, CRL_EINVAL, "n_envs_local must be > 0 and capacity >= 2");
+  if (!(k->gamma >= 0.0 && k->gamma < 1.0)) return fail(ctx, CRL_EINVAL, "gamma must be in [0, 1)");
+  if (k->depth < 0 || k->depth > CRL_MAX_LAYERS - 1 || k->width <= 0)
+    return fail(ctx, CRL_EINVAL, "depth must be in [0, 7] and width > 0");
+  if (!logits_simt_supports(k->repr_dim))
+    return fail(ctx, CRL_EUNSUPPORTED, "repr_dim must be one of 16, 32, 64, 128, 256");
+  if (k->activation != CRL_ACT_SILU && k->activation != CRL_ACT_RELU)
+    return fail(ctx, CRL_EINVAL, "activation");
+  if (k->energy < 0 || k->energy > 2) return fail(ctx, CRL_EINVAL, "energy");
+  if (k->loss < 0 || k->loss > 2) return fail(ctx, CRL_EINVAL, "loss");
+  if (k->precision != CRL_FP32 && k->precision != CRL_BF16) return fail(ctx, CRL_EINVAL, "precision");
+  if (k->precision == CRL_BF16)
+    return fail(ctx, CRL_EUNSUPPORTED, "bf16 tensor-core path not built yet");
+  if (k->world_size < 1 || k->rank < 0 || k->rank >= k->world_size)
+    return fail(ctx, CRL_EINVAL, "rank / world_size");
+  if (k->batch_local < 1 || (long long)k->batch_local * k->world_size < 2)
+    return fail(ctx, CRL_EINVAL, "global batch must be >= 2 (InfoNCE needs negatives)");
+  if (!(k->lr > 0.f) || !(k->adam_eps > 0.f)) return fail(ctx, CRL_EINVAL, "lr and eps must be > 0");
+  return CRL_OK;
+}
+
+extern "C" {
+
+int crl_abi_version(void) { return CRL_ABI_VERSION; }
+
+const char* crl_last_error(const crl_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+crl_status crl_workspace_size(const crl_config* cfg, crl_sizes* out) {
+  crl_ctx* ctx = nullptr;
+  crl_status st = validate(cfg, ctx);
+  if (st != CRL_OK) return st;
+  if (!out) return fail(ctx, CRL_EINVAL, "out is NULL");
+  crl_ctx tmp;
+  tmp.cfg = *cfg;
+  tmp.phi_plan = make_encoder_plan(cfg->obs_dim + cfg->act_dim, cfg->depth, cfg->width,
+                                   cfg->repr_dim, 0);
+  tmp.psi_plan = make_encoder_plan(cfg->goal_dim, cfg->depth, cfg->width, cfg->repr_dim,
+                                   tmp.phi_plan.n_params);
+  tmp.sizes.n_params = tmp.phi_plan.n_params + tmp.psi_plan.n_params;
+  if (cfg->actor_depth > 0 && cfg->actor_width > 0) {
+    EncoderPlan a = make_encoder_plan(cfg->obs_dim + cfg->goal_dim, cfg->actor_depth,
+                                      cfg->actor_width, 2 * cfg->act_dim, 0);
+    tmp.sizes.n_actor_params = a.n_params;
+  }
+  carve(&tmp, nullptr, nullptr, &tmp.sizes.buffer_bytes, &tmp.sizes.scratch_bytes);
+  *out = tmp.sizes;
+  return CRL_OK;
+}
+
+crl_status crl_nccl_unique_id(void* out128) {
+  crl_ctx* ctx = nullptr;
+  if (!out128) return fail(ctx, CRL_EINVAL, "out128 is NULL");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return CRL_OK;
+}
+
+crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* nccl_id,
+                      crl_ctx** out) {
+  crl_ctx* ctx = nullptr;
+  crl_status st = validate(cfg, ctx);
+  if (st != CRL_OK) return st;
+  if (!mem || !out || !mem->params || !mem->adam_m || !mem->adam_v || !mem->buffer || !mem->scratch)
+    return fail(ctx, CRL_EINVAL, "memory pointers must be non-NULL");
+  if (((uintptr_t)mem->buffer & 255) || ((uintptr_t)mem->scratch & 255))
+    return fail(ctx, CRL_EINVAL, "buffer and scratch must be 256-byte aligned");
+  if (cfg->world_size > 1 && !nccl_id)
+    return fail(ctx, CRL_EINVAL, "world_size > 1 needs an NCCL unique id");
+  crl_sizes sz;
+  st = crl_workspace_size(cfg, &sz);
+  if (st != CRL_OK) return st;
+
+  ctx = new crl_ctx();
+  ctx->cfg = *cfg;
+  ctx->sizes = sz;
+  ctx->mem = *mem;
+  ctx->N = cfg->batch_local * cfg->world_size;
+  ctx->phi_plan = make_encoder_plan(cfg->obs_dim + cfg->act_dim, cfg->depth, cfg->width,
+                                    cfg->repr_dim, 0);
+  ctx->psi_plan = make_encoder_plan(cfg->goal_dim, cfg->depth, cfg->width, cfg->repr_dim,
+                                    ctx->phi_plan.n_params);
+  size_t bb, sb;
+  carve(ctx, (char*)mem->buffer, (char*)mem->scratch, &bb, &sb);
+
+  auto cleanup = [&](crl_status s) { crl_status r = s; delete ctx; return r; };
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return cleanup(fail(nullptr, CRL_ECUDA, "no CUDA device"));
+
+  // geometric offset table (contract C1): G[k] = gamma^k by repeated multiplication,
+  // Q[k] = floor((1 - G[k]) 2^64), saturated.
+  std::vector<uint64_t> q(cfg->capacity + 1);
+  double G = 1.0;
+  for (int k = 0; k <= cfg->capacity; ++k) {
+    if (k > 0) G = G * cfg->gamma;
+    double x = 1.0 - G;
+    q[k] = (x >= 1.0) ? ~0ull : (uint64_t)(x * 18446744073709551616.0);
+  }
+  if (cudaMemcpy(ctx->qtab, q.data(), q.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(ctx->ep_end, 0xFF, (size_t)cfg->n_envs_local * cfg->capacity * 4) != cudaSuccess ||
+      cudaMemset(ctx->open_start, 0, (size_t)cfg->n_envs_local * 4) != cudaSuccess ||
+      cudaMemset(ctx->status, 0, 4) != cudaSuccess || cudaMemset(ctx->adam_t, 0, 4) != cudaSuccess ||
+      cudaMemset(ctx->skip, 0, 4) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess)
+    return cleanup(fail(nullptr, CRL_ECUDA, "context initialisation failed"));
+
+  if (cfg->world_size > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, cfg->world_size, id, cfg->rank);
+    if (r != ncclSuccess)
+      return cleanup(fail(nullptr, CRL_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+  }
+  *out = ctx;
+  return CRL_OK;
+}
+
+crl_status crl_destroy(crl_ctx* ctx) {
+  if (!ctx) return CRL_OK;
+  for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  delete ctx;
+  return CRL_OK;
+}
+
+crl_status crl_get_status(crl_ctx* ctx, int sync, int reset) {
+  if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
+  if (sync) CU(cudaDeviceSynchronize());
+  int h = 0;
+  CU(cudaMemcpy(&h, ctx->status, 4, cudaMemcpyDeviceToHost));
+  if (reset) CU(cudaMemset(ctx->status, 0, 4));
+  return (crl_status)h;
+}
+
+int crl_last_launch_count(const crl_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+crl_status crl_debug_tensor(crl_ctx* ctx, const char* name, const float** ptr, size_t* count) {
+  if (!ctx || !name || !ptr || !count) return fail(ctx, CRL_EINVAL, "NULL argument");
+  const size_t Bl = ctx->cfg.batch_local, D = ctx->cfg.repr_dim;
+  std::string n(name);
+  if (n == "phi") { *ptr = ctx->phi_out; *count = Bl * D; }
+  else if (n == "psi") { *ptr = ctx->psi_out; *count = Bl * D; }
+  else if (n == "lse_row") { *ptr = ctx->lse_row; *count = Bl; }
+  else if (n == "lse_col") { *ptr = ctx->lse_col; *count = Bl; }
+  else if (n == "dphi") { *ptr = ctx->dphi; *count = Bl * D; }
+  else if (n == "dpsi") { *ptr = ctx->dpsi; *count = Bl * D; }
+  else if (n == "grads") { *ptr = ctx->grads; *count = ctx->sizes.n_params; }
+  else if (n == "loss") { *ptr = ctx->loss_dev; *count = 4; }
+  else return fail(ctx, CRL_EINVAL, "unknown debug tensor " + n);
+  return CRL_OK;
+}
+
+crl_status crl_buffer_insert(crl_ctx* ctx, const float* obs, const float* act, const uint8_t* done,
+                             int U, void* stream) {
+  if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
+  if (!obs || !act || !done || U <= 0) return fail(ctx, CRL_EINVAL, "insert: NULL input or U <= 0");
+  const crl_config& k = ctx->cfg;
+  if (ctx->n_ins + (uint64_t)U >= 0xFFFFFFF0ull) return fail(ctx, CRL_ESTATE, "step counter overflow");
+  CU(launch_buffer_insert(obs, act, done, U, k.n_envs_local, k.capacity, k.obs_dim, k.act_dim,
+                          ctx->obs_stride, ctx->act_stride, (uint32_t)ctx->n_ins, ctx->obs_ring,
+                          ctx->act_ring, ctx->ep_end, ctx->open_start, (cudaStream_t)stream));
+  ctx->n_ins += (uint64_t)U;
+  ctx->launches = 1;
+  return CRL_OK;
+}
+
+crl_status crl_relabel_sample(crl_ctx* ctx, uint64_t seed, uint64_t step, float* s, float* a,
+                              float* g, int64_t* idx, void* stream) {
+  if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
+  if (!s || !a || !g) return fail(ctx, CRL_EINVAL, "sample: NULL output");
+  const crl_config& k = ctx->cfg;
+  const uint64_t n_ins = ctx->n_ins;
+  const uint64_t tau_new = n_ins - 1;
+  const uint64_t tau_old = n_ins > (uint64_t)k.capacity ? n_ins - k.capacity : 0;
+  if (n_ins < 2) return fail(ctx, CRL_ESTATE, "buffer holds fewer than 2 slots per env");
+  Stage sg(ctx, (cudaStream_t)stream, "relabel");
+  CU(launch_relabel_sample(k.batch_local, k.rank, k.n_envs_local, k.capacity, k.obs_dim, k.act_dim,
+                           k.goal_dim, k.goal_offset, ctx->obs_stride, ctx->act_stride,
+                           (uint32_t)tau_old, (uint32_t)tau_new, seed, step, ctx->obs_ring,
+                           ctx->act_ring, ctx->ep_end, ctx->qtab, s, a, g, idx, ctx->status,
+                           (cudaStream_t)stream));
+  ctx->launches = 1;
+  return CRL_OK;
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------------------------------------
+// critic step
+// ----------------------------------------------------------------------------------------
+static crl_status enc_forward(crl_ctx* ctx, const char* tag, const EncoderPlan& P, const float* x0, int ld0,
+                              const float* x0b, int ld0b, int fsplit, float** X, float** Z,
+                              float* out, cudaStream_t st, int* nl) {
+  const crl_config& k = ctx->cfg;
+  const float* prm = ctx->mem.params;
+  const int Bl = k.batch_local;
+  for (int l = 0; l < P.n_layers; ++l) {
+    const LayerPlan& L = P.layer[l];
+    const bool last = (l == P.n_layers - 1);
+    const float* xin = (l == 0) ? x0 : X[l];
+    const int ldx = (l == 0) ? ld0 : L.in;
+    Stage sg(ctx, st, std::string(tag) + "_fwd_l" + std::to_string(l));
+    CU(mlp_forward_layer_f32(Bl, L.in, L.out, xin, ldx, l == 0 ? x0b : nullptr, ld0b,
+                             l == 0 ? fsplit : 0, prm + L.w_off, prm + L.b_off,
+                             last ? out : Z[l], last ? nullptr : X[l + 1], k.activation, st));
+    ++*nl;
+  }
+  return CRL_OK;
+}
+
+static crl_status enc_backward(crl_ctx* ctx, const char* tag, const EncoderPlan& P, const float* x0, int ld0,
+                               const float* x0b, int ld0b, int fsplit, float** X, float** Z,
+                               const float* dY, cudaStream_t st, int* nl) {
+  const crl_config& k = ctx->cfg;
+  const float* prm = ctx->mem.params;
+  const int Bl = k.batch_local;
+  const float* dZ = dY;
+  int pp = 0;
+  for (int l = P.n_layers - 1; l >= 0; --l) {
+    const LayerPlan& L = P.layer[l];
+    const float* xin = (l == 0) ? x0 : X[l];
+    const int ldx = (l == 0) ? ld0 : L.in;
+    {
+      Stage sg(ctx, st, std::string(tag) + "_bwd_dw_l" + std::to_string(l));
+      CU(mlp_backward_dw_f32(Bl, L.in, L.out, xin, ldx, l == 0 ? x0b : nullptr, ld0b,
+                             l == 0 ? fsplit : 0, dZ, ctx->grads + L.w_off, ctx->grads + L.b_off, st));
+    }
+    ++*nl;
+    if (l > 0) {
+      float* dst = ctx->dz[pp];
+      Stage sg(ctx, st, std::string(tag) + "_bwd_dx_l" + std::to_string(l));
+      CU(mlp_backward_dx_f32(Bl, L.in, L.out, dZ, prm + L.w_off, Z[l - 1], dst, k.activation, st));
+      ++*nl;
+      dZ = dst;
+      pp ^= 1;
+    }
+  }
+  return CRL_OK;
+}
+
+static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, const float* g,
+                                 float* loss_out, float* grads_out, cudaStream_t st) {
+  const crl_config& k = ctx->cfg;
+  const int Bl = k.batch_local, W = k.world_size, N = ctx->N, D = k.repr_dim;
+  const float invN = 1.0f / (float)N;
+  const float c_f = (k.loss == CRL_LOSS_BWD) ? 0.f : 1.f;
+  const float c_b = (k.loss == CRL_LOSS_FWD) ? 0.f : 1.f;
+  int nl = 0;
+  crl_status rs;
+  // A2: encoders forward
+  rs = enc_forward(ctx, "phi", ctx->phi_plan, s, k.obs_dim, a, k.act_dim, k.obs_dim, ctx->phiX, ctx->phiZ,
+                   ctx->phi_out, st, &nl);
+  if (rs != CRL_OK) return rs;
+  rs = enc_forward(ctx, "psi", ctx->psi_plan, g, k.goal_dim, nullptr, 0, 0, ctx->psiX, ctx->psiZ,
+                   ctx->psi_out, st, &nl);
+  if (rs != CRL_OK) return rs;
+  if (W > 1) {
+    NC(ncclGroupStart());
+    NC(ncclAllGather(ctx->phi_out, ctx->phi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
+    NC(ncclAllGather(ctx->psi_out, ctx->psi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
+    NC(ncclGroupEnd());
+  }
+  // A3: online row / column logsumexp
+  { Stage sg(ctx, st, "lse_row"); CU(logits_lse_f32(D, k.energy, ctx->phi_out, Bl, ctx->psi_g, N, ctx->lse_row, st)); ++nl; }
+  { Stage sg(ctx, st, "lse_col"); CU(logits_lse_f32(D, k.energy, ctx->psi_out, Bl, ctx->phi_g, N, ctx->lse_col, st)); ++nl; }
+  if (W > 1) {
+    NC(ncclGroupStart());
+    NC(ncclAllGather(ctx->lse_row, ctx->lse_row_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
+    NC(ncclAllGather(ctx->lse_col, ctx->lse_col_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
+    NC(ncclGroupEnd());
+  }
+  { Stage sg(ctx, st, "loss");
+  CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,
+                         ctx->loss_acc, W == 1, invN, c_f, c_b, k.beta_lse, loss_out, ctx->skip,
+                         ctx->adam_t, ctx->status, st)); }
+  ++nl;
+  if (W > 1) {
+    NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
+    CU(launch_loss_finalize(ctx->loss_acc, invN, c_f, c_b, k.beta_lse, loss_out, ctx->skip,
+                            ctx->adam_t, ctx->status, st));
+    ++nl;
+  }
+  // A4: dlogits consumed in-pass
+  const int row_off = k.rank * Bl;
+  { Stage sg(ctx, st, "grad_phi");
+  CU(logits_grad_f32(D, k.energy, ctx->phi_out, Bl, row_off, ctx->psi_g, N, ctx->lse_row,
+                     ctx->lse_col_g, c_f, c_b, k.beta_lse, 0.f, invN, ctx->dphi, st)); }
+  ++nl;
+  { Stage sg(ctx, st, "grad_psi");
+  CU(logits_grad_f32(D, k.energy, ctx->psi_out, Bl, row_off, ctx->phi_g, N, ctx->lse_col,
+                     ctx->lse_row_g, c_b, c_f, 0.f, k.beta_lse, invN, ctx->dpsi, st)); }
+  ++nl;
+  // A5: encoders backward
+  rs = enc_backward(ctx, "phi", ctx->phi_plan, s, k.obs_dim, a, k.act_dim, k.obs_dim, ctx->phiX,
+                    ctx->phiZ, ctx->dphi, st, &nl);
+  if (rs != CRL_OK) return rs;
+  rs = enc_backward(ctx, "psi", ctx->psi_plan, g, k.goal_dim, nullptr, 0, 0, ctx->psiX, ctx->psiZ,
+                    ctx->dpsi, st, &nl);
+  if (rs != CRL_OK) return rs;
+  if (W > 1)
+    NC(ncclAllReduce(ctx->grads, ctx->grads, ctx->sizes.n_params, ncclFloat32, ncclSum, ctx->comm, st));
+  if (grads_out)
+    CU(cudaMemcpyAsync(grads_out, ctx->grads, ctx->sizes.n_params * 4, cudaMemcpyDeviceToDevice, st));
+  // A6: Adam
+  { Stage sg(ctx, st, "adam");
+  CU(launch_adam(ctx->mem.params, ctx->grads, ctx->mem.adam_m, ctx->mem.adam_v, ctx->sizes.n_params,
+                 k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay, ctx->adam_t, ctx->skip,
+                 ctx->status, nullptr, ctx->num_sms, st)); }
+  ++nl;
+  ctx->launches = nl;
+  return CRL_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float* a, const float* g,
+                                      float* loss_out, float* grads_out, void* stream) {
+  if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
+  if (!s || !a || !g) return fail(ctx, CRL_EINVAL, "critic_step: NULL batch");
+  if (grads_out && !is_device_ptr(grads_out))
+    return fail(ctx, CRL_EINVAL, "grads_out must be device memory");
+  const crl_config& k = ctx->cfg;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t Bl = k.batch_local;
+  // host batch -> staging (end-to-end path)
+  if (!is_device_ptr(s)) {
+    CU(cudaMemcpyAsync(ctx->stage_s, s, Bl * k.obs_dim * 4, cudaMemcpyHostToDevice, st));
+    s = ctx->stage_s;
+  }
+  if (!is_device_ptr(a)) {
+    CU(cudaMemcpyAsync(ctx->stage_a, a, Bl * k.act_dim * 4, cudaMemcpyHostToDevice, st));
+    a = ctx->stage_a;
+  }
+  if (!is_device_ptr(g)) {
+    CU(cudaMemcpyAsync(ctx->stage_g, g, Bl * k.goal_dim * 4, cudaMemcpyHostToDevice, st));
+    g = ctx->stage_g;
+  }
+  float* loss_dev = ctx->loss_dev;
+  const bool loss_host = loss_out && !is_device_ptr(loss_out);
+  if (loss_out && !loss_host) loss_dev = loss_out;
+
+  if (ctx->prof_on) {                    // eager, event-bracketed launches
+    crl_status rs = enqueue_critic(ctx, s, a, g, loss_dev, grads_out, st);
+    if (rs != CRL_OK) return rs;
+    if (loss_host) CU(cudaMemcpyAsync(loss_out, loss_dev, 16, cudaMemcpyDeviceToHost, st));
+    return CRL_OK;
+  }
+  GraphKey key{s, a, g, loss_dev, grads_out};
+  auto it = ctx->graphs.find(key);
+  if (it == ctx->graphs.end()) {
+    // capture the schedule once on the private capture stream
+    CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    crl_status rs = enqueue_critic(ctx, s, a, g, loss_dev, grads_out, ctx->cap_stream);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    if (rs != CRL_OK) { if (graph) cudaGraphDestroy(graph); return rs; }
+    CU(ce);
+    cudaGraphExec_t exec = nullptr;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CU(ce);
+    it = ctx->graphs.emplace(key, exec).first;
+  }
+  CU(cudaGraphLaunch(it->second, st));
+  if (loss_host) CU(cudaMemcpyAsync(loss_out, loss_dev, 16, cudaMemcpyDeviceToHost, st));
+  return CRL_OK;
+}
+
+extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* g, const float* eps,
+                                     float alpha_ent, float* loss_out, float* actor_grads_out,
+                                     int apply_adam, void* stream) {
+  (void)s; (void)g; (void)eps; (void)alpha_ent; (void)loss_out; (void)actor_grads_out;
+  (void)apply_adam; (void)stream;
+  return fail(ctx, CRL_EUNSUPPORTED, "crl_actor_loss: not built yet");
+}
+
+extern "C" crl_status crl_profile_enable(crl_ctx* ctx, int on) {
+  if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
+  CU(cudaDeviceSynchronize());
+  for (auto& e : ctx->prof_pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+  ctx->prof_pending.clear();
+  ctx->prof_acc.clear();
+  ctx->prof_names.clear();
+  ctx->prof_on = on != 0;
+  return CRL_OK;
+}
+
+extern "C" int crl_profile_read(crl_ctx* ctx, int i, char* name_out, int name_cap, double* total_ms,
+                                int* count) {
+  if (!ctx) return -1;
+  if (!ctx->prof_pending.empty()) {
+    cudaDeviceSynchronize();
+    for (auto& e : ctx->prof_pending) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e.a, e.b);
+      auto& acc = ctx->prof_acc[e.name];
+      if (acc.second == 0) ctx->prof_names.push_back(e.name);
+      acc.first += ms;
+      acc.second += 1;
+      cudaEventDestroy(e.a); cudaEventDestroy(e.b);
+    }
+    ctx->prof_pending.clear();
+  }
+  const int n = (int)ctx->prof_names.size();
+  if (i >= 0 && i < n) {
+    const std::string& nm = ctx->prof_names[i];
+    if (name_out && name_cap > 0) {
+      std::strncpy(name_out, nm.c_str(), name_cap - 1);
+      name_out[name_cap - 1] = 0;
+    }
+    if (total_ms) *total_ms = ctx->prof_acc[nm].first;
+    if (count) *count = ctx->prof_acc[nm].second;
+  }
+  return n;
+}

@@ -1,0 +1,308 @@
+// logits_simt.cu — fp32 SIMT energy logits + online logsumexp (A3) and the in-pass
+// dlogits -> representation gradients (A4).  The N x N logits are never stored.
+//
+// Paper: energies App. A.2 P:607-617 (L2 with the minus sign of P:614, reading A-01; dot
+// P:610; cos P:608), InfoNCE fwd/bwd/sym P:619-630, logsumexp penalty P:361 / Alg. 1 P:1052.
+// Readings A-02..A-06.
+//
+// Both kernels are "row-owner" kernels over an orientation (A rows, B columns):
+//   l_ij = f(A_i, B_j)  (f is symmetric in its two arguments for L2 / dot / cos)
+// * lse kernel : LSE_i = log sum_j exp(l_ij), online over column tiles.  Called with
+//   (A,B) = (Phi, Psi) for the row LSE and with (Psi, Phi) for the column LSE'.
+// * grad kernel: dA_i = sum_j g_ij df(A_i,B_j)/dA_i with the closed-form dlogits
+//     g_ij = invN [c_r (e^{l-lr_i} - d_ij) + c_c (e^{l-lc_j} - d_ij)]
+//            + 2 invN (beta_r lr_i e^{l-lr_i} + beta_c lc_j e^{l-lc_j})
+//   formed in registers and consumed in the same pass (never written to HBM).  With
+//   (A,B) = (Phi,Psi): lr = LSE, lc = LSE', (c_r,c_c) = (c_f,c_b), beta_r = beta.
+//   With (A,B) = (Psi,Phi): lr = LSE', lc = LSE, (c_r,c_c) = (c_b,c_f), beta_c = beta.
+//   Energy chain: dot w = g;  L2 w = g / r (r = -l) and dA_i = sum_j w_ij B_j - (sum_j w_ij) A_i;
+//   cos w = g / |B_j|, du_i = sum_j w_ij B_j, dA_i = (du_i - (du_i.u_i) u_i) / |A_i|.
+// L2 uses the difference form sum_k (a_k - b_k)^2 (no cancellation) on this fp32 path.
+//
+// Tile: 64 A-rows per CTA, 64 B-rows per column tile, full D resident in shared memory;
+// thread (tx,ty) owns rows ty+16i, columns tx+16j (i,j < 4): row reductions are 16-lane
+// shuffles, all shared-memory reads are conflict-free with a (D+1) row pitch.
+#include "common.cuh"
+#include <math_constants.h>
+
+namespace crl {
+
+struct LogitsArgs {
+  const float* A; int Na; int row_offset;   // global index of A row 0 (delta_ij)
+  const float* B; int Nb;                   // B rows are global column indices 0..Nb-1
+  const float* lr;                          // grad: row statistic [Na]
+  const float* lc;                          // grad: column statistic [Nb]
+  float c_r, c_c, beta_r, beta_c, invN;
+  float* out;                               // lse: [Na]; grad: dA [Na][D]
+};
+
+constexpr int TR = 64;                      // rows per tile (both A and B)
+
+template <int D>
+struct LogitsSmem {
+  static constexpr int P = D + 1;
+  static constexpr size_t bytes(bool grad) {
+    return sizeof(float) * ((size_t)2 * TR * P + TR + TR + (grad ? (size_t)TR * (TR + 1) : 0));
+  }
+};
+
+template <int D, int ENERGY, bool GRAD>
+__global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
+  constexpr int P = D + 1;
+  constexpr int DC = D / 16;               // d-columns per thread in the dA accumulation
+  extern __shared__ float sm[];
+  float* As = sm;                          // [TR][P]
+  float* Bs = As + TR * P;                 // [TR][P]
+  float* nA = Bs + TR * P;                 // [TR] inverse (clamped) norms of A rows (cos)
+  float* nB = nA + TR;                     // [TR] inverse norms of B rows (cos)
+  float* Ws = nB + TR;                     // [TR][TR+1] (grad only)
+
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int a0 = blockIdx.x * TR;
+
+  // ---- A tile: 64 rows x D, coalesced along D
+  for (int e = tid; e < TR * D; e += 256) {
+    int r = e / D, c = e - r * D;
+    As[r * P + c] = (a0 + r < p.Na) ? p.A[(size_t)(a0 + r) * D + c] : 0.0f;
+  }
+  __syncthreads();
+  if (ENERGY == CRL_ENERGY_COS && tid < TR) {
+    float s = 0.f;
+    for (int c = 0; c < D; ++c) s = fmaf(As[tid * P + c], As[tid * P + c], s);
+    nA[tid] = 1.0f / fmaxf(sqrtf(s), kEpsCos);
+  }
+
+  float lr_i[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int r = a0 + ty + 16 * i;
+    lr_i[i] = (GRAD && r < p.Na) ? p.lr[r] : 0.0f;
+  }
+
+  // state
+  float m_run[4], s_run[4];                // lse mode
+  float acc2[4][DC];                       // grad mode: dA accumulators
+  float wsum[4];                           // grad mode: row sums of w (L2)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    m_run[i] = -CUDART_INF_F; s_run[i] = 0.f; wsum[i] = 0.f;
+#pragma unroll
+    for (int c = 0; c < DC; ++c) acc2[i][c] = 0.f;
+  }
+
+  for (int b0 = 0; b0 < p.Nb; b0 += TR) {
+    __syncthreads();                       // previous tile fully consumed
+    for (int e = tid; e < TR * D; e += 256) {
+      int r = e / D, c = e - r * D;
+      Bs[r * P + c] = (b0 + r < p.Nb) ? p.B[(size_t)(b0 + r) * D + c] : 0.0f;
+    }
+    __syncthreads();
+    if (ENERGY == CRL_ENERGY_COS && tid < TR) {
+      float s = 0.f;
+      for (int c = 0; c < D; ++c) s = fmaf(Bs[tid * P + c], Bs[tid * P + c], s);
+      nB[tid] = 1.0f / fmaxf(sqrtf(s), kEpsCos);
+    }
+    if (ENERGY == CRL_ENERGY_COS) __syncthreads();
+
+    // ---- 4x4 logits per thread
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < D; ++k) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[(ty + 16 * i) * P + k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[(tx + 16 * j) * P + k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (ENERGY == CRL_ENERGY_L2) {
+            float d = a[i] - b[j];
+            acc[i][j] = fmaf(d, d, acc[i][j]);
+          } else {
+            acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          }
+        }
+    }
+
+    float l[4][4];
+    bool valid[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) valid[j] = (b0 + tx + 16 * j) < p.Nb;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v = acc[i][j];
+        if (ENERGY == CRL_ENERGY_L2) v = -sqrtf(v + kEpsL2);
+        if (ENERGY == CRL_ENERGY_COS) v = v * nA[ty + 16 * i] * nB[tx + 16 * j];
+        l[i][j] = v;
+      }
+
+    if (!GRAD) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float mx = m_run[i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) if (valid[j]) mx = fmaxf(mx, l[i][j]);
+        if (mx == -CUDART_INF_F) continue;
+        float s = s_run[i] * expf(m_run[i] - mx);     // m_run = -inf -> 0
+#pragma unroll
+        for (int j = 0; j < 4; ++j) if (valid[j]) s += expf(l[i][j] - mx);
+        s_run[i] = s; m_run[i] = mx;
+      }
+    } else {
+      // ---- dlogits in registers -> energy chain -> W tile in shared memory
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int jg = b0 + tx + 16 * j;
+        const float lcj = valid[j] ? p.lc[jg] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int ig = p.row_offset + a0 + ty + 16 * i;
+          float w = 0.f;
+          if (valid[j]) {
+            const float lv = l[i][j];
+            const float pe = expf(lv - lr_i[i]);
+            const float qe = expf(lv - lcj);
+            const float dlt = (ig == jg) ? 1.f : 0.f;
+            float g = p.invN * (p.c_r * (pe - dlt) + p.c_c * (qe - dlt)) +
+                      2.f * p.invN * (p.beta_r * lr_i[i] * pe + p.beta_c * lcj * qe);
+            if (ENERGY == CRL_ENERGY_L2) w = g / (-lv);
+            else if (ENERGY == CRL_ENERGY_COS) w = g * nB[tx + 16 * j];
+            else w = g;
+          }
+          Ws[(ty + 16 * i) * (TR + 1) + tx + 16 * j] = w;
+          if (ENERGY == CRL_ENERGY_L2) wsum[i] += w;
+        }
+      }
+      __syncthreads();
+      // dA[rows][d] += W[rows][64] . B[64][d]
+#pragma unroll 4
+      for (int jj = 0; jj < TR; ++jj) {
+        float w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = Ws[(ty + 16 * i) * (TR + 1) + jj];
+#pragma unroll
+        for (int c = 0; c < DC; ++c) {
+          float bv = Bs[jj * P + tx + 16 * c];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc2[i][c] = fmaf(w[i], bv, acc2[i][c]);
+        }
+      }
+    }
+  }
+
+  if (!GRAD) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float m = m_run[i], s = s_run[i];
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        float mx = fmaxf(m, m2);
+        float t = (m == -CUDART_INF_F ? 0.f : s * expf(m - mx)) +
+                  (m2 == -CUDART_INF_F ? 0.f : s2 * expf(m2 - mx));
+        m = mx; s = t;
+      }
+      const int r = a0 + ty + 16 * i;
+      if (tx == 0 && r < p.Na) p.out[r] = m + logf(s);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = ty + 16 * i;
+      const int r = a0 + rl;
+      if (ENERGY == CRL_ENERGY_L2) {
+        float ws = wsum[i];
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
+#pragma unroll
+        for (int c = 0; c < DC; ++c) acc2[i][c] -= ws * As[rl * P + tx + 16 * c];
+      } else if (ENERGY == CRL_ENERGY_COS) {
+        const float inv = nA[rl];
+        float pr = 0.f;
+#pragma unroll
+        for (int c = 0; c < DC; ++c) pr = fmaf(acc2[i][c], As[rl * P + tx + 16 * c], pr);
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+        pr *= inv;                                        // du . u
+        const bool big = inv < 1.0f / kEpsCos;           // ||A_i|| > eps
+#pragma unroll
+        for (int c = 0; c < DC; ++c) {
+          float u = As[rl * P + tx + 16 * c] * inv;
+          acc2[i][c] = big ? (acc2[i][c] - pr * u) * inv : acc2[i][c] * inv;
+        }
+      }
+      if (r < p.Na) {
+#pragma unroll
+        for (int c = 0; c < DC; ++c) p.out[(size_t)r * D + tx + 16 * c] = acc2[i][c];
+      }
+    }
+  }
+}
+
+template <int D, int ENERGY, bool GRAD>
+static cudaError_t launch_logits_t(const LogitsArgs& p, cudaStream_t st) {
+  size_t smem = LogitsSmem<D>::bytes(GRAD);
+  static bool attr_set = false;   // per template instance
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(logits_rows_kernel<D, ENERGY, GRAD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((p.Na + TR - 1) / TR);
+  logits_rows_kernel<D, ENERGY, GRAD><<<grid, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int D, bool GRAD>
+static cudaError_t launch_logits_e(int energy, const LogitsArgs& p, cudaStream_t st) {
+  switch (energy) {
+    case CRL_ENERGY_L2: return launch_logits_t<D, CRL_ENERGY_L2, GRAD>(p, st);
+    case CRL_ENERGY_DOT: return launch_logits_t<D, CRL_ENERGY_DOT, GRAD>(p, st);
+    case CRL_ENERGY_COS: return launch_logits_t<D, CRL_ENERGY_COS, GRAD>(p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <bool GRAD>
+static cudaError_t launch_logits_d(int D, int energy, const LogitsArgs& p, cudaStream_t st) {
+  switch (D) {
+    case 16: return launch_logits_e<16, GRAD>(energy, p, st);
+    case 32: return launch_logits_e<32, GRAD>(energy, p, st);
+    case 64: return launch_logits_e<64, GRAD>(energy, p, st);
+    case 128: return launch_logits_e<128, GRAD>(energy, p, st);
+    case 256: return launch_logits_e<256, GRAD>(energy, p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+bool logits_simt_supports(int D) { return D == 16 || D == 32 || D == 64 || D == 128 || D == 256; }
+
+cudaError_t logits_lse_f32(int D, int energy, const float* A, int Na, const float* B, int Nb,
+                           float* lse_out, cudaStream_t st) {
+  LogitsArgs p{};
+  p.A = A; p.Na = Na; p.B = B; p.Nb = Nb; p.out = lse_out;
+  return launch_logits_d<false>(D, energy, p, st);
+}
+
+cudaError_t logits_grad_f32(int D, int energy, const float* A, int Na, int row_offset,
+                            const float* B, int Nb, const float* lr, const float* lc, float c_r,
+                            float c_c, float beta_r, float beta_c, float invN, float* dA,
+                            cudaStream_t st) {
+  LogitsArgs p{};
+  p.A = A; p.Na = Na; p.row_offset = row_offset; p.B = B; p.Nb = Nb;
+  p.lr = lr; p.lc = lc; p.c_r = c_r; p.c_c = c_c; p.beta_r = beta_r; p.beta_c = beta_c;
+  p.invN = invN; p.out = dA;
+  return launch_logits_d<true>(D, energy, p, st);
+}
+
+}  // namespace crl

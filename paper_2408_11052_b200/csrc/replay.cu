@@ -1,0 +1,196 @@
+// replay.cu — A0 buffer insert and A1 hindsight relabel sample (contract C1).
+//
+// Paper: Alg. 1 P:1030-1038 (per-env trajectories, reset on terminal), Table 2
+// (capacity per env), §3 P:165-169 (goal T ~ Geom(1-gamma) steps ahead), §3.1 P:190-191 and
+// §3.2 P:219 ((s,a) uniform, g from the states after s in the same trajectory), Alg. 1
+// P:1045-1046 ("sample (with discount)").  Readings A-07..A-12, A-18.
+//
+// HBM layout (per rank, inside crl_memory.buffer):
+//   obs_ring [E_l][T][obs_stride] fp32    act_ring [E_l][T][act_stride] fp32
+//   ep_end   [E_l][T] u32  absolute index of the last slot of that slot's episode, or
+//                          kOpen while the episode is still running
+//   open_start [E_l] u32   absolute index where the currently open episode began
+//   qtab     [T+1] u64     Q[k] = floor((1 - gamma^k) 2^64), built on the host
+// Device index arithmetic is integer-only, so sampled indices are bit-exact.
+#include "common.cuh"
+
+namespace crl {
+
+constexpr uint32_t kOpen = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11), counter (c0..c3), key (k0, k1)
+// ---------------------------------------------------------------------------------------
+struct U4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------------------------------
+// A0: one CTA per env.  All threads copy the env's U new rows into the ring (coalesced
+// per row), mark the new slots open, then warp 0 walks the U done flags and back-fills
+// ep_end for every episode that closed (each slot is back-filled at most once).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) buffer_insert_kernel(
+    const float* __restrict__ obs, const float* __restrict__ act, const uint8_t* __restrict__ done,
+    int U, int E, int T, int obs_dim, int act_dim, int obs_stride, int act_stride,
+    uint32_t n_ins, float* __restrict__ obs_ring, float* __restrict__ act_ring,
+    uint32_t* __restrict__ ep_end, uint32_t* __restrict__ open_start) {
+  const int e = blockIdx.x;
+  const uint32_t n_new = n_ins + (uint32_t)U;
+  // copy rows: element-level loop over (u, c) so every row is written by consecutive threads
+  for (int idx = threadIdx.x; idx < U * obs_dim; idx += blockDim.x) {
+    int u = idx / obs_dim, c = idx - u * obs_dim;
+    uint32_t slot = (n_ins + u) % (uint32_t)T;
+    obs_ring[((size_t)e * T + slot) * obs_stride + c] = obs[((size_t)u * E + e) * obs_dim + c];
+  }
+  for (int idx = threadIdx.x; idx < U * act_dim; idx += blockDim.x) {
+    int u = idx / act_dim, c = idx - u * act_dim;
+    uint32_t slot = (n_ins + u) % (uint32_t)T;
+    act_ring[((size_t)e * T + slot) * act_stride + c] = act[((size_t)u * E + e) * act_dim + c];
+  }
+  for (int u = threadIdx.x; u < U; u += blockDim.x) {
+    uint32_t slot = (n_ins + u) % (uint32_t)T;
+    ep_end[(size_t)e * T + slot] = kOpen;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  uint32_t start = open_start[e];
+  const uint32_t lo_keep = n_new > (uint32_t)T ? n_new - (uint32_t)T : 0u;   // oldest kept slot
+  for (int u = 0; u < U; ++u) {
+    if (done[(size_t)u * E + e]) {
+      uint32_t tau_end = n_ins + (uint32_t)u;
+      uint32_t first = start > lo_keep ? start : lo_keep;
+      for (uint32_t t = first + lane; t <= tau_end; t += 32)
+        ep_end[(size_t)e * T + (t % (uint32_t)T)] = tau_end;
+      start = tau_end + 1;
+    }
+  }
+  if (lane == 0) open_start[e] = start;
+}
+
+// ---------------------------------------------------------------------------------------
+// A1: one warp per row.  Lane a evaluates attempt a (and a+32) of the rejection loop in
+// parallel; the first accepted attempt (lowest a) wins via ballot, which reproduces the
+// sequential "first valid attempt" of the contract.  The offset k is an inverse-CDF lookup
+// in the u64 table Q (binary search in shared memory).  Rows are then gathered by the
+// whole warp (vectorised when the row stride allows).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+__global__ void __launch_bounds__(256) relabel_sample_kernel(
+    int B_l, int rank, int E, int T, int obs_dim, int act_dim, int goal_dim, int goal_offset,
+    int obs_stride, int act_stride, uint32_t tau_old, uint32_t tau_new,
+    uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo, uint32_t step_hi,
+    const float* __restrict__ obs_ring, const float* __restrict__ act_ring,
+    const uint32_t* __restrict__ ep_end, const uint64_t* __restrict__ qtab,
+    float* __restrict__ s_out, float* __restrict__ a_out, float* __restrict__ g_out,
+    int64_t* __restrict__ idx_out, int* __restrict__ status) {
+  extern __shared__ uint64_t q_sm[];
+  // stage Q[0..T] in shared memory
+  for (int k = threadIdx.x; k <= T; k += blockDim.x) q_sm[k] = qtab[k];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= B_l) return;
+  const uint32_t rho = (uint32_t)rank * (uint32_t)B_l + (uint32_t)r;
+  const uint32_t n = tau_new - tau_old + 1;
+
+  int found = -1;
+  uint32_t e = 0, tau = 0, L = 0, x2 = 0, x3 = 0;
+  for (int base = 0; base < 64 && found < 0; base += 32) {
+    const uint32_t att = (uint32_t)(base + lane);
+    U4 x = philox4x32_10(U4{rho, att, step_lo, step_hi}, seed_lo, seed_hi);
+    uint32_t ee = (uint32_t)(((uint64_t)x.x * (uint64_t)E) >> 32);
+    uint32_t j = (uint32_t)(((uint64_t)x.y * (uint64_t)n) >> 32);
+    uint32_t t = tau_old + j;
+    uint32_t end = ep_end[(size_t)ee * T + (t % (uint32_t)T)];
+    uint32_t cap = end < tau_new ? end : tau_new;          // kOpen > tau_new always
+    uint32_t LL = cap - t;
+    unsigned ok = __ballot_sync(0xffffffffu, LL >= 1u);
+    if (ok) {
+      int src = __ffs(ok) - 1;
+      found = base + src;
+      e = __shfl_sync(0xffffffffu, ee, src);
+      tau = __shfl_sync(0xffffffffu, t, src);
+      L = __shfl_sync(0xffffffffu, LL, src);
+      x2 = __shfl_sync(0xffffffffu, x.z, src);
+      x3 = __shfl_sync(0xffffffffu, x.w, src);
+    }
+  }
+  if (found < 0) {
+    if (lane == 0) set_status(status, CRL_ESAMPLER);
+    // deterministic fill so downstream stays finite
+    e = 0; tau = tau_old; L = 1; x2 = 0; x3 = 0;
+  }
+  // k = min{k in [1, L] : Q[k] > t},  t = (R * Q[L]) >> 64
+  const uint64_t R = ((uint64_t)x2 << 32) | (uint64_t)x3;
+  const uint64_t tt = mulhi64(R, q_sm[L]);
+  uint32_t lo = 1, hi = L;                     // invariant: answer in [lo, hi], Q[hi] > tt
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (q_sm[mid] > tt) hi = mid; else lo = mid + 1;
+  }
+  const uint32_t k = lo;
+  const uint32_t slot = tau % (uint32_t)T;
+  const uint32_t gslot = (tau + k) % (uint32_t)T;
+  const float* srow = obs_ring + ((size_t)e * T + slot) * obs_stride;
+  const float* arow = act_ring + ((size_t)e * T + slot) * act_stride;
+  const float* grow = obs_ring + ((size_t)e * T + gslot) * obs_stride + goal_offset;
+  float* so = s_out + (size_t)r * obs_dim;
+  float* ao = a_out + (size_t)r * act_dim;
+  float* go = g_out + (size_t)r * goal_dim;
+  for (int c = lane; c < obs_dim; c += 32) so[c] = srow[c];
+  for (int c = lane; c < act_dim; c += 32) ao[c] = arow[c];
+  for (int c = lane; c < goal_dim; c += 32) go[c] = grow[c];
+  if (idx_out != nullptr && lane < 3) {
+    int64_t v = lane == 0 ? (int64_t)rank * E + e : (lane == 1 ? (int64_t)tau : (int64_t)(tau + k));
+    idx_out[(size_t)r * 3 + lane] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------------------
+cudaError_t launch_buffer_insert(const float* obs, const float* act, const uint8_t* done, int U,
+                                 int E, int T, int obs_dim, int act_dim, int obs_stride,
+                                 int act_stride, uint32_t n_ins, float* obs_ring, float* act_ring,
+                                 uint32_t* ep_end, uint32_t* open_start, cudaStream_t st) {
+  buffer_insert_kernel<<<E, 256, 0, st>>>(obs, act, done, U, E, T, obs_dim, act_dim, obs_stride,
+                                          act_stride, n_ins, obs_ring, act_ring, ep_end, open_start);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relabel_sample(int B_l, int rank, int E, int T, int obs_dim, int act_dim,
+                                  int goal_dim, int goal_offset, int obs_stride, int act_stride,
+                                  uint32_t tau_old, uint32_t tau_new, uint64_t seed, uint64_t step,
+                                  const float* obs_ring, const float* act_ring,
+                                  const uint32_t* ep_end, const uint64_t* qtab, float* s, float* a,
+                                  float* g, int64_t* idx, int* status, cudaStream_t st) {
+  const int warps = 8;
+  dim3 grid((B_l + warps - 1) / warps);
+  size_t smem = sizeof(uint64_t) * (size_t)(T + 1);
+  if (smem > 48 * 1024) {
+    cudaError_t err = cudaFuncSetAttribute(relabel_sample_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+  }
+  relabel_sample_kernel<<<grid, warps * 32, smem, st>>>(
+      B_l, rank, E, T, obs_dim, act_dim, goal_dim, goal_offset, obs_stride, act_stride, tau_old,
+      tau_new, (uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)step, (uint32_t)(step >> 32),
+      obs_ring, act_ring, ep_end, qtab, s, a, g, idx, status);
+  return cudaGetLastError();
+}
+
+}  // namespace crl

@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs.  Tolerances (north_star): relabel indices bit-exact and s/a/g bitwise; fp32 path
+loss within 1e-5 relative and gradients within 1e-4 relative (per-tensor L2 norm)."""
+import numpy as np
+import pytest
+
+import crl_synth
+from _crl_testlib import fill_buffer, make_ctx, oracle_buffers, oracle_kw, rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import critic as ocritic       # noqa: E402
+from oracle import replay as oreplay       # noqa: E402
+
+SEED = crl_synth.PHILOX_SEED
+
+
+def _sample_gpu(ctx, cfg, step, B=None):
+    B = B or ctx.cfg.batch_local
+    s = torch.empty(B, cfg["obs_dim"], device="cuda")
+    a = torch.empty(B, cfg["act_dim"], device="cuda")
+    g = torch.empty(B, cfg["goal_dim"], device="cuda")
+    idx = torch.empty(B, 3, dtype=torch.int64, device="cuda")
+    ctx.relabel_sample(SEED, step, s, a, g, idx)
+    torch.cuda.synchronize()
+    return s.cpu().numpy(), a.cpu().numpy(), g.cpu().numpy(), idx.cpu().numpy()
+
+
+# ------------------------------------------------------------------------- A0 + A1
+
+@pytest.mark.parametrize("name,n_chunks,U,B", [
+    ("reacher", 20, 62, 256),      # configs[0]: 8 envs x 1000, ring wrapped (1240 steps)
+    ("humanoid", 3, 62, 512),      # configs[2] shapes (obs 268), partially filled ring
+    ("reacher", 1, 1, 37),         # degenerate: a single step per env is < 2 slots -> ESTATE
+])
+def test_relabel_bit_exact(name, n_chunks, U, B):
+    cfg = crl_synth.preset(name, precision="fp32", batch=B)
+    if name == "humanoid":
+        cfg["n_envs"] = 64                      # keep the oracle's Python loops short
+    ctx, _ = make_ctx(cfg)
+    chunks = fill_buffer(ctx, cfg, n_chunks, U=U)
+    if n_chunks * U < 2:
+        from paper_2408_11052_b200 import CrlError
+        with pytest.raises(CrlError):
+            _sample_gpu(ctx, cfg, 0, B)
+        return
+    bufs = oracle_buffers(cfg, chunks)
+    for step in (0, 1, 12345678901):
+        s, a, g, idx = _sample_gpu(ctx, cfg, step, B)
+        os_, oa, og, oidx = oreplay.relabel_sample(bufs[0], SEED, step, B, gamma=cfg["gamma"],
+                                                   goal_offset=cfg["goal_offset"],
+                                                   goal_dim=cfg["goal_dim"])
+        assert np.array_equal(idx, oidx)
+        assert np.array_equal(s.view(np.uint32), os_.view(np.uint32))
+        assert np.array_equal(a.view(np.uint32), oa.view(np.uint32))
+        assert np.array_equal(g.view(np.uint32), og.view(np.uint32))
+    assert ctx.status() == 0
+
+
+def test_relabel_full_size_ant_sampled_rows():
+    """configs[1] at full size (1024 envs x 1000, wrapped ring): the oracle recomputes a
+    sample of rows one by one."""
+    cfg = crl_synth.preset("ant", batch=4096)
+    ctx, _ = make_ctx(cfg)
+    chunks = fill_buffer(ctx, cfg, 20)
+    bufs = oracle_buffers(cfg, chunks)
+    s, a, g, idx = _sample_gpu(ctx, cfg, 7)
+    rows = list(range(0, 4096, 97)) + [4095]
+    _, _, og, oidx = oreplay.relabel_sample(bufs[0], SEED, 7, 4096, gamma=cfg["gamma"],
+                                            goal_dim=cfg["goal_dim"], rows=rows)
+    assert np.array_equal(idx[rows], oidx[rows])
+    assert np.array_equal(g[rows], og[rows])
+    # properties over all rows: in-window, strictly future, same episode
+    tau_old, tau_new, _ = bufs[0].window()
+    assert np.all(idx[:, 1] >= tau_old) and np.all(idx[:, 2] <= tau_new)
+    assert np.all(idx[:, 2] > idx[:, 1])
+
+
+# ------------------------------------------------------------------------- A2-A6
+
+def _critic_parity(cfg, batch_seed=11, check_adam=True):
+    ctx, params = make_ctx(cfg)
+    B = cfg["batch"]
+    s, a, g = crl_synth.random_batch(cfg, B, seed=batch_seed)
+    loss = torch.zeros(4, device="cuda")
+    grads = torch.zeros(ctx.n_params, device="cuda")
+    ctx.critic_step(torch.from_numpy(s).cuda(), torch.from_numpy(a).cuda(),
+                    torch.from_numpy(g).cuda(), loss, grads)
+    torch.cuda.synchronize()
+    assert ctx.status() == 0
+    z = np.zeros_like(params, dtype=np.float64)
+    ref = ocritic.critic_step(params.astype(np.float64), z, z, 0, s, a, g, lr=cfg["lr"],
+                              **oracle_kw(cfg))
+    L = loss.cpu().numpy()
+    for i, k in enumerate(["L_fwd", "L_bwd", "penalty", "total"]):
+        assert abs(L[i] - ref[k]) <= 1e-5 * max(abs(ref[k]), 1e-3), (k, L[i], ref[k])
+    assert rel(ctx.debug_tensor("phi").cpu().numpy(), ref["phi"]) < 1e-5
+    assert rel(ctx.debug_tensor("lse_row").cpu().numpy(), ref["lse_row"]) < 1e-5
+    assert rel(ctx.debug_tensor("lse_col").cpu().numpy(), ref["lse_col"]) < 1e-5
+    assert rel(ctx.debug_tensor("dphi").cpu().numpy(), ref["dphi"]) < 1e-4
+    assert rel(ctx.debug_tensor("dpsi").cpu().numpy(), ref["dpsi"]) < 1e-4
+    gr = grads.cpu().numpy()
+    assert rel(gr, ref["grads"]) < 1e-4
+    # per-layer tensors as well (a wrong small tensor can hide in the global norm)
+    off = 0
+    for enc_in in (cfg["obs_dim"] + cfg["act_dim"], cfg["goal_dim"]):
+        for fi, fo in crl_synth.param_shapes(enc_in, cfg["depth"], cfg["width"], cfg["repr_dim"]):
+            for n in (fi * fo, fo):
+                assert rel(gr[off:off + n], ref["grads"][off:off + n]) < 1e-4, off
+                off += n
+    if check_adam:
+        dp = ctx.params.cpu().numpy().astype(np.float64) - params
+        dref = ref["params_new"] - params
+        assert rel(dp, dref) < 1e-4
+    return ctx
+
+
+@pytest.mark.parametrize("energy", ["l2", "dot", "cos"])
+@pytest.mark.parametrize("loss", ["fwd", "bwd", "sym"])
+def test_critic_step_fp32_small(energy, loss):
+    cfg = crl_synth.preset("reacher", batch=200, width=64, energy=energy, loss=loss)
+    _critic_parity(cfg)
+
+
+@pytest.mark.parametrize("B", [2, 3, 65, 130])
+def test_critic_step_fp32_ragged(B):
+    cfg = crl_synth.preset("reacher", batch=B, width=96, depth=3, beta_lse=0.0)
+    _critic_parity(cfg)
+
+
+def test_critic_step_fp32_relu_and_beta():
+    cfg = crl_synth.preset("ant", batch=128, width=128, activation="relu", beta_lse=0.5)
+    _critic_parity(cfg)
+
+
+@pytest.mark.parametrize("name", ["reacher", "ant"])
+def test_critic_step_fp32_paper_configs(name):
+    """configs[0] and configs[1] at their full sizes (batch 256, 2x256 / 4x256)."""
+    _critic_parity(crl_synth.preset(name))
+
+
+def test_critic_step_fp32_repr256():
+    cfg = crl_synth.preset("ant", batch=192, width=128, repr_dim=256, precision="fp32")
+    _critic_parity(cfg)
+
+
+def test_critic_step_fp32_sweep4096():
+    """configs[3] at batch 4096 (the bench launch configuration)."""
+    _critic_parity(crl_synth.preset("sweep4096"), check_adam=False)
+
+
+def test_critic_step_graph_replay_and_host_buffers():
+    """Two steps: the second replays the cached graph; host (pinned) batch + host loss go
+    through the end-to-end path.  Compared with two oracle steps."""
+    cfg = crl_synth.preset("reacher", batch=96, width=64)
+    ctx, params = make_ctx(cfg)
+    s, a, g = crl_synth.random_batch(cfg, 96, seed=3)
+    sd, ad, gd = (torch.from_numpy(x).cuda() for x in (s, a, g))
+    loss_d = torch.zeros(4, device="cuda")
+    ctx.critic_step(sd, ad, gd, loss_d)
+    s2, a2, g2 = crl_synth.random_batch(cfg, 96, seed=4)
+    hs, ha, hg = (torch.from_numpy(x).pin_memory() for x in (s2, a2, g2))
+    loss_h = torch.zeros(4).pin_memory()
+    ctx.critic_step(hs, ha, hg, loss_h)
+    torch.cuda.synchronize()
+    kw = oracle_kw(cfg)
+    z = np.zeros_like(params, dtype=np.float64)
+    r1 = ocritic.critic_step(params.astype(np.float64), z, z, 0, s, a, g, lr=cfg["lr"], **kw)
+    r2 = ocritic.critic_step(r1["params_new"], r1["m_new"], r1["v_new"], r1["t_new"], s2, a2, g2,
+                             lr=cfg["lr"], **kw)
+    assert abs(loss_d.cpu().numpy()[3] - r1["total"]) < 1e-5 * abs(r1["total"])
+    assert abs(loss_h.numpy()[3] - r2["total"]) < 1e-5 * abs(r2["total"])
+    dp = ctx.params.cpu().numpy().astype(np.float64) - params
+    assert rel(dp, r2["params_new"] - params) < 1e-3
+    assert ctx.launch_count() > 0
+
+
+def test_critic_step_nonfinite_sets_status_and_skips_adam():
+    cfg = crl_synth.preset("reacher", batch=64, width=32)
+    ctx, params = make_ctx(cfg)
+    s, a, g = crl_synth.random_batch(cfg, 64)
+    s[3, 0] = np.nan
+    ctx.critic_step(torch.from_numpy(s).cuda(), torch.from_numpy(a).cuda(), torch.from_numpy(g).cuda())
+    torch.cuda.synchronize()
+    assert ctx.status(reset=True) == 5          # CRL_ENONFINITE
+    assert np.array_equal(ctx.params.cpu().numpy(), params)
