@@ -293,7 +293,7 @@ class _DevView:
     """Minimal __cuda_array_interface__ over a raw fp32 device pointer (read-only view)."""
 
     def __init__(self, ptr, n):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, True),
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
                                          "version": 3, "strides": None}
 
 

@@ -19,9 +19,10 @@
 //   cos w = g / |B_j|, du_i = sum_j w_ij B_j, dA_i = (du_i - (du_i.u_i) u_i) / |A_i|.
 // L2 uses the difference form sum_k (a_k - b_k)^2 (no cancellation) on this fp32 path.
 //
-// Tile: 64 A-rows per CTA, 64 B-rows per column tile, full D resident in shared memory;
-// thread (tx,ty) owns rows ty+16i, columns tx+16j (i,j < 4): row reductions are 16-lane
-// shuffles, all shared-memory reads are conflict-free with a (D+1) row pitch.
+// Tiling: TR (16/32/64) A-rows per CTA, 64 B-rows per column tile; A and the column tiles
+// are held TRANSPOSED in shared memory ([k][row], odd pitch) so every read in both the
+// logits and the dA contraction is conflict-free; column tiles are double-buffered with
+// 4-byte cp.async.  Thread (tx,ty) owns rows ty+16i and columns tx+16j.
 #include "common.cuh"
 #include <math_constants.h>
 
@@ -36,124 +37,147 @@ struct LogitsArgs {
   float* out;                               // lse: [Na]; grad: dA [Na][D]
 };
 
-constexpr int TR = 64;                      // rows per tile (both A and B)
+constexpr int TC = 64;                      // columns per tile
+constexpr int BPITCH = TC + 1;
 
-template <int D>
-struct LogitsSmem {
-  static constexpr int P = D + 1;
-  static constexpr size_t bytes(bool grad) {
-    return sizeof(float) * ((size_t)2 * TR * P + TR + TR + (grad ? (size_t)TR * (TR + 1) : 0));
+__device__ __forceinline__ void cpa4(float* smem, const float* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 4 : 0));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int D, int TR>
+struct LSmem {
+  static constexpr int AP = TR + 1;
+  static constexpr size_t floats(bool grad) {
+    return (size_t)D * AP + 2 * (size_t)D * BPITCH + TR + 2 * TC + (grad ? (size_t)TR * BPITCH : 0);
   }
 };
 
-template <int D, int ENERGY, bool GRAD>
+template <int D, int TR, int ENERGY, bool GRAD>
 __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
-  constexpr int P = D + 1;
+  constexpr int AP = TR + 1;
+  constexpr int RI = TR / 16;              // rows per thread
   constexpr int DC = D / 16;               // d-columns per thread in the dA accumulation
   extern __shared__ float sm[];
-  float* As = sm;                          // [TR][P]
-  float* Bs = As + TR * P;                 // [TR][P]
-  float* nA = Bs + TR * P;                 // [TR] inverse (clamped) norms of A rows (cos)
-  float* nB = nA + TR;                     // [TR] inverse norms of B rows (cos)
-  float* Ws = nB + TR;                     // [TR][TR+1] (grad only)
+  float* At = sm;                          // [D][AP]      A^T
+  float* Bt = At + D * AP;                 // [2][D][BPITCH]  B^T column tiles
+  float* nA = Bt + 2 * D * BPITCH;         // [TR]  inverse clamped norms (cos)
+  float* nB = nA + TR;                     // [2][TC]
+  float* Ws = nB + 2 * TC;                 // [TR][BPITCH] (grad only)
 
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int a0 = blockIdx.x * TR;
+  const int ntiles = (p.Nb + TC - 1) / TC;
 
-  // ---- A tile: 64 rows x D, coalesced along D
+  auto issue_b = [&](int buf, int b0) {
+    float* dst = Bt + buf * D * BPITCH;
+    for (int e = tid; e < TC * D; e += 256) {
+      const int r = e / D, c = e - r * D;
+      const bool ok = b0 + r < p.Nb;
+      cpa4(dst + c * BPITCH + r, ok ? p.B + (size_t)(b0 + r) * D + c : p.B, ok);
+    }
+  };
+  // A tile (transposed) + first column tile
   for (int e = tid; e < TR * D; e += 256) {
-    int r = e / D, c = e - r * D;
-    As[r * P + c] = (a0 + r < p.Na) ? p.A[(size_t)(a0 + r) * D + c] : 0.0f;
+    const int r = e / D, c = e - r * D;
+    const bool ok = a0 + r < p.Na;
+    cpa4(At + c * AP + r, ok ? p.A + (size_t)(a0 + r) * D + c : p.A, ok);
   }
-  __syncthreads();
-  if (ENERGY == CRL_ENERGY_COS && tid < TR) {
-    float s = 0.f;
-    for (int c = 0; c < D; ++c) s = fmaf(As[tid * P + c], As[tid * P + c], s);
-    nA[tid] = 1.0f / fmaxf(sqrtf(s), kEpsCos);
-  }
+  issue_b(0, 0);
+  cpa_commit();
 
-  float lr_i[4];
+  float lr_i[RI];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int r = a0 + ty + 16 * i;
+  for (int i = 0; i < RI; ++i) {
+    const int r = a0 + ty + 16 * i;
     lr_i[i] = (GRAD && r < p.Na) ? p.lr[r] : 0.0f;
   }
-
-  // state
-  float m_run[4], s_run[4];                // lse mode
-  float acc2[4][DC];                       // grad mode: dA accumulators
-  float wsum[4];                           // grad mode: row sums of w (L2)
+  float m_run[RI], s_run[RI], wsum[RI];
+  float acc2[RI][GRAD ? DC : 1];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < RI; ++i) {
     m_run[i] = -CUDART_INF_F; s_run[i] = 0.f; wsum[i] = 0.f;
 #pragma unroll
-    for (int c = 0; c < DC; ++c) acc2[i][c] = 0.f;
+    for (int c = 0; c < (GRAD ? DC : 1); ++c) acc2[i][c] = 0.f;
   }
 
-  for (int b0 = 0; b0 < p.Nb; b0 += TR) {
-    __syncthreads();                       // previous tile fully consumed
-    for (int e = tid; e < TR * D; e += 256) {
-      int r = e / D, c = e - r * D;
-      Bs[r * P + c] = (b0 + r < p.Nb) ? p.B[(size_t)(b0 + r) * D + c] : 0.0f;
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = t & 1, b0 = t * TC;
+    if (t + 1 < ntiles) {
+      issue_b(buf ^ 1, b0 + TC);
+      cpa_commit();
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
     }
     __syncthreads();
-    if (ENERGY == CRL_ENERGY_COS && tid < TR) {
-      float s = 0.f;
-      for (int c = 0; c < D; ++c) s = fmaf(Bs[tid * P + c], Bs[tid * P + c], s);
-      nB[tid] = 1.0f / fmaxf(sqrtf(s), kEpsCos);
+    const float* B_ = Bt + buf * D * BPITCH;
+    if (ENERGY == CRL_ENERGY_COS) {
+      if (t == 0 && tid < TR) {
+        float s = 0.f;
+        for (int c = 0; c < D; ++c) s = fmaf(At[c * AP + tid], At[c * AP + tid], s);
+        nA[tid] = 1.0f / fmaxf(sqrtf(s), kEpsCos);
+      }
+      if (tid >= 128 && tid < 128 + TC) {
+        const int r = tid - 128;
+        float s = 0.f;
+        for (int c = 0; c < D; ++c) s = fmaf(B_[c * BPITCH + r], B_[c * BPITCH + r], s);
+        nB[buf * TC + r] = 1.0f / fmaxf(sqrtf(s), kEpsCos);
+      }
+      __syncthreads();
     }
-    if (ENERGY == CRL_ENERGY_COS) __syncthreads();
 
-    // ---- 4x4 logits per thread
-    float acc[4][4];
+    // ---- RI x 4 logits per thread
+    float acc[RI][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 #pragma unroll 8
     for (int k = 0; k < D; ++k) {
-      float a[4], b[4];
+      float a[RI], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[(ty + 16 * i) * P + k];
+      for (int i = 0; i < RI; ++i) a[i] = At[k * AP + ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[(tx + 16 * j) * P + k];
+      for (int j = 0; j < 4; ++j) b[j] = B_[k * BPITCH + tx + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (ENERGY == CRL_ENERGY_L2) {
-            float d = a[i] - b[j];
+            const float d = a[i] - b[j];
             acc[i][j] = fmaf(d, d, acc[i][j]);
           } else {
             acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
           }
         }
     }
-
-    float l[4][4];
     bool valid[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) valid[j] = (b0 + tx + 16 * j) < p.Nb;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float v = acc[i][j];
         if (ENERGY == CRL_ENERGY_L2) v = -sqrtf(v + kEpsL2);
-        if (ENERGY == CRL_ENERGY_COS) v = v * nA[ty + 16 * i] * nB[tx + 16 * j];
-        l[i][j] = v;
+        if (ENERGY == CRL_ENERGY_COS) v = v * nA[ty + 16 * i] * nB[buf * TC + tx + 16 * j];
+        acc[i][j] = v;                    // acc now holds l_ij
       }
 
     if (!GRAD) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < RI; ++i) {
         float mx = m_run[i];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) if (valid[j]) mx = fmaxf(mx, l[i][j]);
+        for (int j = 0; j < 4; ++j) if (valid[j]) mx = fmaxf(mx, acc[i][j]);
         if (mx == -CUDART_INF_F) continue;
         float s = s_run[i] * expf(m_run[i] - mx);     // m_run = -inf -> 0
 #pragma unroll
-        for (int j = 0; j < 4; ++j) if (valid[j]) s += expf(l[i][j] - mx);
+        for (int j = 0; j < 4; ++j) if (valid[j]) s += expf(acc[i][j] - mx);
         s_run[i] = s; m_run[i] = mx;
       }
     } else {
@@ -163,52 +187,53 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
         const int jg = b0 + tx + 16 * j;
         const float lcj = valid[j] ? p.lc[jg] : 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < RI; ++i) {
           const int ig = p.row_offset + a0 + ty + 16 * i;
           float w = 0.f;
           if (valid[j]) {
-            const float lv = l[i][j];
+            const float lv = acc[i][j];
             const float pe = expf(lv - lr_i[i]);
             const float qe = expf(lv - lcj);
             const float dlt = (ig == jg) ? 1.f : 0.f;
-            float g = p.invN * (p.c_r * (pe - dlt) + p.c_c * (qe - dlt)) +
-                      2.f * p.invN * (p.beta_r * lr_i[i] * pe + p.beta_c * lcj * qe);
+            const float g = p.invN * (p.c_r * (pe - dlt) + p.c_c * (qe - dlt)) +
+                            2.f * p.invN * (p.beta_r * lr_i[i] * pe + p.beta_c * lcj * qe);
             if (ENERGY == CRL_ENERGY_L2) w = g / (-lv);
-            else if (ENERGY == CRL_ENERGY_COS) w = g * nB[tx + 16 * j];
+            else if (ENERGY == CRL_ENERGY_COS) w = g * nB[buf * TC + tx + 16 * j];
             else w = g;
           }
-          Ws[(ty + 16 * i) * (TR + 1) + tx + 16 * j] = w;
+          Ws[(ty + 16 * i) * BPITCH + tx + 16 * j] = w;
           if (ENERGY == CRL_ENERGY_L2) wsum[i] += w;
         }
       }
       __syncthreads();
       // dA[rows][d] += W[rows][64] . B[64][d]
 #pragma unroll 4
-      for (int jj = 0; jj < TR; ++jj) {
-        float w[4];
+      for (int jj = 0; jj < TC; ++jj) {
+        float w[RI];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = Ws[(ty + 16 * i) * (TR + 1) + jj];
+        for (int i = 0; i < RI; ++i) w[i] = Ws[(ty + 16 * i) * BPITCH + jj];
 #pragma unroll
         for (int c = 0; c < DC; ++c) {
-          float bv = Bs[jj * P + tx + 16 * c];
+          const float bv = B_[(tx + 16 * c) * BPITCH + jj];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc2[i][c] = fmaf(w[i], bv, acc2[i][c]);
+          for (int i = 0; i < RI; ++i) acc2[i][c % (GRAD ? DC : 1)] = fmaf(w[i], bv, acc2[i][c % (GRAD ? DC : 1)]);
         }
       }
     }
+    __syncthreads();                       // buffer `buf` is refilled two tiles later
   }
 
   if (!GRAD) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < RI; ++i) {
       float m = m_run[i], s = s_run[i];
 #pragma unroll
       for (int o = 1; o < 16; o <<= 1) {
-        float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-        float s2 = __shfl_xor_sync(0xffffffffu, s, o);
-        float mx = fmaxf(m, m2);
-        float t = (m == -CUDART_INF_F ? 0.f : s * expf(m - mx)) +
-                  (m2 == -CUDART_INF_F ? 0.f : s2 * expf(m2 - mx));
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const float mx = fmaxf(m, m2);
+        const float t = (m == -CUDART_INF_F ? 0.f : s * expf(m - mx)) +
+                        (m2 == -CUDART_INF_F ? 0.f : s2 * expf(m2 - mx));
         m = mx; s = t;
       }
       const int r = a0 + ty + 16 * i;
@@ -216,59 +241,71 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < RI; ++i) {
       const int rl = ty + 16 * i;
       const int r = a0 + rl;
+      float* acc_i = acc2[i];
       if (ENERGY == CRL_ENERGY_L2) {
         float ws = wsum[i];
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
 #pragma unroll
-        for (int c = 0; c < DC; ++c) acc2[i][c] -= ws * As[rl * P + tx + 16 * c];
+        for (int c = 0; c < DC; ++c) acc_i[c % (GRAD ? DC : 1)] -= ws * At[(tx + 16 * c) * AP + rl];
       } else if (ENERGY == CRL_ENERGY_COS) {
         const float inv = nA[rl];
         float pr = 0.f;
 #pragma unroll
-        for (int c = 0; c < DC; ++c) pr = fmaf(acc2[i][c], As[rl * P + tx + 16 * c], pr);
+        for (int c = 0; c < DC; ++c) pr = fmaf(acc_i[c % (GRAD ? DC : 1)], At[(tx + 16 * c) * AP + rl], pr);
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
         pr *= inv;                                        // du . u
         const bool big = inv < 1.0f / kEpsCos;           // ||A_i|| > eps
 #pragma unroll
         for (int c = 0; c < DC; ++c) {
-          float u = As[rl * P + tx + 16 * c] * inv;
-          acc2[i][c] = big ? (acc2[i][c] - pr * u) * inv : acc2[i][c] * inv;
+          const float u = At[(tx + 16 * c) * AP + rl] * inv;
+          float& v = acc_i[c % (GRAD ? DC : 1)];
+          v = big ? (v - pr * u) * inv : v * inv;
         }
       }
       if (r < p.Na) {
 #pragma unroll
-        for (int c = 0; c < DC; ++c) p.out[(size_t)r * D + tx + 16 * c] = acc2[i][c];
+        for (int c = 0; c < DC; ++c) p.out[(size_t)r * D + tx + 16 * c] = acc_i[c % (GRAD ? DC : 1)];
       }
     }
   }
 }
 
-template <int D, int ENERGY, bool GRAD>
+static int g_sms_logits = 148;
+void logits_set_num_sms(int n) { g_sms_logits = n > 0 ? n : 148; }
+
+template <int D, int TR, int ENERGY, bool GRAD>
 static cudaError_t launch_logits_t(const LogitsArgs& p, cudaStream_t st) {
-  size_t smem = LogitsSmem<D>::bytes(GRAD);
+  const size_t smem = sizeof(float) * LSmem<D, TR>::floats(GRAD);
   static bool attr_set = false;   // per template instance
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(logits_rows_kernel<D, ENERGY, GRAD>,
+    cudaError_t e = cudaFuncSetAttribute(logits_rows_kernel<D, TR, ENERGY, GRAD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid((p.Na + TR - 1) / TR);
-  logits_rows_kernel<D, ENERGY, GRAD><<<grid, 256, smem, st>>>(p);
+  logits_rows_kernel<D, TR, ENERGY, GRAD><<<grid, 256, smem, st>>>(p);
   return cudaGetLastError();
+}
+
+template <int D, int ENERGY, bool GRAD>
+static cudaError_t launch_logits_tr(const LogitsArgs& p, cudaStream_t st) {
+  if (p.Na >= 64 * g_sms_logits) return launch_logits_t<D, 64, ENERGY, GRAD>(p, st);
+  if (p.Na >= 16 * g_sms_logits) return launch_logits_t<D, 32, ENERGY, GRAD>(p, st);
+  return launch_logits_t<D, 16, ENERGY, GRAD>(p, st);
 }
 
 template <int D, bool GRAD>
 static cudaError_t launch_logits_e(int energy, const LogitsArgs& p, cudaStream_t st) {
   switch (energy) {
-    case CRL_ENERGY_L2: return launch_logits_t<D, CRL_ENERGY_L2, GRAD>(p, st);
-    case CRL_ENERGY_DOT: return launch_logits_t<D, CRL_ENERGY_DOT, GRAD>(p, st);
-    case CRL_ENERGY_COS: return launch_logits_t<D, CRL_ENERGY_COS, GRAD>(p, st);
+    case CRL_ENERGY_L2: return launch_logits_tr<D, CRL_ENERGY_L2, GRAD>(p, st);
+    case CRL_ENERGY_DOT: return launch_logits_tr<D, CRL_ENERGY_DOT, GRAD>(p, st);
+    case CRL_ENERGY_COS: return launch_logits_tr<D, CRL_ENERGY_COS, GRAD>(p, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -12,65 +12,15 @@
 
 namespace crl {
 
-// One CTA, fixed reduction order (deterministic).  Writes acc[0..2] = local sums of
-// (LSE_i - l_ii), (LSE'_i - l_ii), LSE_i^2.  If `finalize`, also writes loss_out[0..3],
-// sets *skip when the loss is non-finite and advances the Adam step counter.
-__global__ void __launch_bounds__(1024) loss_partial_kernel(
-    const float* __restrict__ phi, const float* __restrict__ psi, int Bl, int D, int energy,
-    const float* __restrict__ lse_row, const float* __restrict__ lse_col, float* __restrict__ acc,
-    int finalize, float invN, float c_f, float c_b, float beta, float* __restrict__ loss_out,
-    int* __restrict__ skip, int* __restrict__ adam_t, int* __restrict__ status) {
-  __shared__ float red[3][32];
-  float s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  for (int i = threadIdx.x; i < Bl; i += blockDim.x) {
-    const float* a = phi + (size_t)i * D;
-    const float* b = psi + (size_t)i * D;
-    float l;
-    if (energy == CRL_ENERGY_L2) {
-      float d2 = 0.f;
-      for (int k = 0; k < D; ++k) { float d = a[k] - b[k]; d2 = fmaf(d, d, d2); }
-      l = -sqrtf(d2 + kEpsL2);
-    } else {
-      float dot = 0.f, na = 0.f, nb = 0.f;
-      for (int k = 0; k < D; ++k) { dot = fmaf(a[k], b[k], dot); na = fmaf(a[k], a[k], na); nb = fmaf(b[k], b[k], nb); }
-      l = (energy == CRL_ENERGY_DOT) ? dot
-                                     : dot / (fmaxf(sqrtf(na), kEpsCos) * fmaxf(sqrtf(nb), kEpsCos));
-    }
-    const float lr = lse_row[i], lc = lse_col[i];
-    s1 += lr - l;
-    s2 += lc - l;
-    s3 += lr * lr;
-  }
-  s1 = warp_sum(s1); s2 = warp_sum(s2); s3 = warp_sum(s3);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) { red[0][w] = s1; red[1][w] = s2; red[2][w] = s3; }
-  __syncthreads();
-  if (w == 0) {
-    const int nw = blockDim.x >> 5;
-    s1 = lane < nw ? red[0][lane] : 0.f;
-    s2 = lane < nw ? red[1][lane] : 0.f;
-    s3 = lane < nw ? red[2][lane] : 0.f;
-    s1 = warp_sum(s1); s2 = warp_sum(s2); s3 = warp_sum(s3);
-    if (lane == 0) {
-      acc[0] = s1; acc[1] = s2; acc[2] = s3;
-      if (finalize) {
-        const float Lf = s1 * invN, Lb = s2 * invN, P = beta * s3 * invN;
-        const float tot = c_f * Lf + c_b * Lb + P;
-        if (loss_out) { loss_out[0] = Lf; loss_out[1] = Lb; loss_out[2] = P; loss_out[3] = tot; }
-        const bool bad = !isfinite(tot);
-        *skip = bad ? 1 : 0;
-        if (bad) set_status(status, CRL_ENONFINITE);
-        else *adam_t += 1;
-      }
-    }
-  }
-}
+// Warp per row (coalesced), 64 rows per CTA; every CTA writes its partial sums and the
+// last CTA to finish (atomic ticket) adds them in CTA order — deterministic.  acc[0..2] =
+// local sums of (LSE_i - l_ii), (LSE'_i - l_ii), LSE_i^2.  If `finalize`, also writes
+// loss_out[0..3], sets *skip when the loss is non-finite and advances the Adam step counter.
+constexpr int kLossRowsPerCta = 64;
 
-// Multi-rank: acc[] already all-reduced.
-__global__ void loss_finalize_kernel(const float* __restrict__ acc, float invN, float c_f,
-                                     float c_b, float beta, float* __restrict__ loss_out,
-                                     int* __restrict__ skip, int* __restrict__ adam_t,
-                                     int* __restrict__ status) {
+__device__ __forceinline__ void loss_finalize_dev(const float* acc, float invN, float c_f,
+                                                  float c_b, float beta, float* loss_out,
+                                                  int* skip, int* adam_t, int* status) {
   const float Lf = acc[0] * invN, Lb = acc[1] * invN, P = beta * acc[2] * invN;
   const float tot = c_f * Lf + c_b * Lb + P;
   if (loss_out) { loss_out[0] = Lf; loss_out[1] = Lb; loss_out[2] = P; loss_out[3] = tot; }
@@ -80,10 +30,73 @@ __global__ void loss_finalize_kernel(const float* __restrict__ acc, float invN, 
   else *adam_t += 1;
 }
 
+__global__ void __launch_bounds__(256) loss_partial_kernel(
+    const float* __restrict__ phi, const float* __restrict__ psi, int Bl, int D, int energy,
+    const float* __restrict__ lse_row, const float* __restrict__ lse_col, float* __restrict__ acc,
+    float* __restrict__ part, unsigned* __restrict__ ticket, int finalize, float invN, float c_f,
+    float c_b, float beta, float* __restrict__ loss_out, int* __restrict__ skip,
+    int* __restrict__ adam_t, int* __restrict__ status) {
+  __shared__ float red[3][8];
+  __shared__ bool last;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  const int r0 = blockIdx.x * kLossRowsPerCta;
+  for (int q = w; q < kLossRowsPerCta; q += 8) {
+    const int i = r0 + q;
+    if (i >= Bl) break;
+    const float* a = phi + (size_t)i * D;
+    const float* b = psi + (size_t)i * D;
+    float x = 0.f, na = 0.f, nb = 0.f;
+    for (int k = lane; k < D; k += 32) {
+      const float av = a[k], bv = b[k];
+      if (energy == CRL_ENERGY_L2) { const float d = av - bv; x = fmaf(d, d, x); }
+      else { x = fmaf(av, bv, x); na = fmaf(av, av, na); nb = fmaf(bv, bv, nb); }
+    }
+    x = warp_sum(x);
+    float l;
+    if (energy == CRL_ENERGY_L2) l = -sqrtf(x + kEpsL2);
+    else if (energy == CRL_ENERGY_DOT) l = x;
+    else {
+      na = warp_sum(na); nb = warp_sum(nb);
+      l = x / (fmaxf(sqrtf(na), kEpsCos) * fmaxf(sqrtf(nb), kEpsCos));
+    }
+    const float lr = lse_row[i], lc = lse_col[i];
+    s1 += lr - l; s2 += lc - l; s3 += lr * lr;
+  }
+  if (lane == 0) { red[0][w] = s1; red[1][w] = s2; red[2][w] = s3; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    for (int j = 0; j < 8; ++j) { t1 += red[0][j]; t2 += red[1][j]; t3 += red[2][j]; }
+    part[blockIdx.x * 4 + 0] = t1; part[blockIdx.x * 4 + 1] = t2; part[blockIdx.x * 4 + 2] = t3;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    float t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    for (unsigned j = 0; j < gridDim.x; ++j) {
+      t1 += __ldcg(part + j * 4 + 0); t2 += __ldcg(part + j * 4 + 1); t3 += __ldcg(part + j * 4 + 2);
+    }
+    acc[0] = t1; acc[1] = t2; acc[2] = t3;
+    *ticket = 0u;                                  // re-armed for the next (graph) replay
+    if (finalize) loss_finalize_dev(acc, invN, c_f, c_b, beta, loss_out, skip, adam_t, status);
+  }
+}
+
+// Multi-rank: acc[] already all-reduced.
+__global__ void loss_finalize_kernel(const float* __restrict__ acc, float invN, float c_f,
+                                     float c_b, float beta, float* __restrict__ loss_out,
+                                     int* __restrict__ skip, int* __restrict__ adam_t,
+                                     int* __restrict__ status) {
+  loss_finalize_dev(acc, invN, c_f, c_b, beta, loss_out, skip, adam_t, status);
+}
+
 // Fused Adam over the flat fp32 parameters; optional bf16 shadow of the parameters
 // (operands of the tensor-core path) written in the same pass.
 __global__ void __launch_bounds__(256) adam_kernel(
-    float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+    float* __restrict__ p, float* __restrict__ g, int S, float* __restrict__ m,
     float* __restrict__ v, size_t n, float lr, float b1, float b2, float eps, float wd,
     const int* __restrict__ adam_t, const int* __restrict__ skip, int* __restrict__ status,
     __nv_bfloat16_raw* __restrict__ shadow) {
@@ -96,7 +109,9 @@ __global__ void __launch_bounds__(256) adam_kernel(
   bool bad = false;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
-    const float gi = g[i];
+    float gi = g[i];
+    for (int sl = 1; sl < S; ++sl) gi += g[(size_t)sl * n + i];   // deterministic split-K sum
+    if (S > 1) g[i] = gi;
     bad |= !isfinite(gi);
     const float mi = b1 * m[i] + (1.f - b1) * gi;
     const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
@@ -114,14 +129,16 @@ __global__ void __launch_bounds__(256) adam_kernel(
   if (bad) set_status(status, CRL_ENONFINITE);
 }
 
+int loss_partial_blocks(int Bl) { return (Bl + kLossRowsPerCta - 1) / kLossRowsPerCta; }
+
 cudaError_t launch_loss_partial(const float* phi, const float* psi, int Bl, int D, int energy,
                                 const float* lse_row, const float* lse_col, float* acc,
-                                int finalize, float invN, float c_f, float c_b, float beta,
-                                float* loss_out, int* skip, int* adam_t, int* status,
-                                cudaStream_t st) {
-  loss_partial_kernel<<<1, 1024, 0, st>>>(phi, psi, Bl, D, energy, lse_row, lse_col, acc,
-                                          finalize, invN, c_f, c_b, beta, loss_out, skip, adam_t,
-                                          status);
+                                float* part, unsigned* ticket, int finalize, float invN, float c_f,
+                                float c_b, float beta, float* loss_out, int* skip, int* adam_t,
+                                int* status, cudaStream_t st) {
+  loss_partial_kernel<<<loss_partial_blocks(Bl), 256, 0, st>>>(
+      phi, psi, Bl, D, energy, lse_row, lse_col, acc, part, ticket, finalize, invN, c_f, c_b, beta,
+      loss_out, skip, adam_t, status);
   return cudaGetLastError();
 }
 
@@ -132,7 +149,7 @@ cudaError_t launch_loss_finalize(const float* acc, float invN, float c_f, float 
   return cudaGetLastError();
 }
 
-cudaError_t launch_adam(float* p, const float* g, float* m, float* v, size_t n, float lr,
+cudaError_t launch_adam(float* p, float* g, int S, float* m, float* v, size_t n, float lr,
                         float b1, float b2, float eps, float wd, const int* adam_t,
                         const int* skip, int* status, void* shadow_bf16, int num_sms,
                         cudaStream_t st) {
@@ -140,7 +157,7 @@ cudaError_t launch_adam(float* p, const float* g, float* m, float* v, size_t n, 
   size_t cap = (size_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
-  adam_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, g, m, v, n, lr, b1, b2, eps, wd, adam_t, skip,
+  adam_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, g, S, m, v, n, lr, b1, b2, eps, wd, adam_t, skip,
                                                 status,
                                                 reinterpret_cast<__nv_bfloat16_raw*>(shadow_bf16));
   return cudaGetLastError();

@@ -113,9 +113,15 @@ def _critic_parity(cfg, batch_seed=11, check_adam=True):
                 assert rel(gr[off:off + n], ref["grads"][off:off + n]) < 1e-4, off
                 off += n
     if check_adam:
+        # The first Adam step maps g -> g/(|g|+eps) ~ sign(g): it magnifies tiny gradient
+        # differences near |g| ~ eps, so the optimiser kernel is checked on the GPU's own
+        # gradients (oracle Adam, fp64) and the end-to-end delta only loosely.
+        from oracle import adam as oadam
         dp = ctx.params.cpu().numpy().astype(np.float64) - params
-        dref = ref["params_new"] - params
-        assert rel(dp, dref) < 1e-4
+        p_ref, *_ = oadam.adam_step(params.astype(np.float64), gr.astype(np.float64), z, z, 0,
+                                    lr=cfg["lr"])
+        assert rel(dp, p_ref - params) < 1e-5
+        assert rel(dp, ref["params_new"] - params) < 1e-2
     return ctx
 
 
