@@ -24,121 +24,15 @@
 #include <tuple>
 #include <vector>
 
-namespace crl {
-cudaError_t launch_buffer_insert(const float*, const float*, const uint8_t*, int, int, int, int, int,
-                                 int, int, uint32_t, float*, float*, uint32_t*, uint32_t*,
-                                 cudaStream_t);
-cudaError_t launch_relabel_sample(int, int, int, int, int, int, int, int, int, int, uint32_t,
-                                  uint32_t, uint64_t, uint64_t, const float*, const float*,
-                                  const uint32_t*, const uint64_t*, float*, float*, float*,
-                                  int64_t*, int*, cudaStream_t);
-cudaError_t mlp_forward_layer_f32(int, int, int, const float*, int, const float*, int, int,
-                                  const float*, const float*, float*, float*, int, cudaStream_t);
-cudaError_t mlp_backward_dx_f32(int, int, int, const float*, const float*, const float*, float*,
-                                int, cudaStream_t);
-cudaError_t mlp_backward_dw_f32(int, int, int, const float*, int, const float*, int, int,
-                                const float*, float*, float*, int, size_t, cudaStream_t);
-int dw_splits_for(int Bn);
-void gemm_set_num_sms(int n);
-void logits_set_num_sms(int n);
-cudaError_t launch_reduce_partials(float*, size_t, int, cudaStream_t);
-bool logits_simt_supports(int D);
-cudaError_t logits_lse_f32(int, int, const float*, int, const float*, int, float*, cudaStream_t);
-cudaError_t logits_grad_f32(int, int, const float*, int, int, const float*, int, const float*,
-                            const float*, float, float, float, float, float, float*, cudaStream_t);
-cudaError_t launch_loss_partial(const float*, const float*, int, int, int, const float*,
-                                const float*, float*, float*, unsigned*, int, float, float, float,
-                                float, float*, int*, int*, int*, cudaStream_t);
-int loss_partial_blocks(int Bl);
-cudaError_t launch_loss_finalize(const float*, float, float, float, float, float*, int*, int*,
-                                 int*, cudaStream_t);
-cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, float, float, float,
-                        float, const int*, const int*, int*, void*, int, cudaStream_t);
-}  // namespace crl
+#include "ctx.h"
 
-using namespace crl;
+thread_local std::string g_last_error;
 
-static thread_local std::string g_last_error;
+crl_status bf16_prepare(crl_ctx* ctx);
+crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, const float* g, float* loss_out,
+                               float* grads_out, cudaStream_t st, cudaStream_t st2);
 
-// ----------------------------------------------------------------------------------------
-// workspace carving (shared by crl_workspace_size and crl_create)
-// ----------------------------------------------------------------------------------------
-struct Carver {
-  char* base;
-  size_t off = 0;
-  template <typename T>
-  T* take(size_t count) {
-    off = (off + 255) & ~(size_t)255;
-    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
-    off += count * sizeof(T);
-    return p;
-  }
-};
-
-struct GraphKey {
-  const void *s, *a, *g, *loss, *grads;
-  bool operator<(const GraphKey& o) const {
-    return std::tie(s, a, g, loss, grads) < std::tie(o.s, o.a, o.g, o.loss, o.grads);
-  }
-};
-
-struct crl_ctx {
-  crl_config cfg{};
-  crl_sizes sizes{};
-  crl_memory mem{};
-  EncoderPlan phi_plan{}, psi_plan{};
-  int N = 0;
-  // replay buffer
-  float* obs_ring = nullptr; float* act_ring = nullptr;
-  uint32_t* ep_end = nullptr; uint32_t* open_start = nullptr; uint64_t* qtab = nullptr;
-  int obs_stride = 0, act_stride = 0;
-  uint64_t n_ins = 0;
-  // scratch
-  float* grads = nullptr;             // [dw_splits][n_params] split-K partials, slice 0 = sum
-  int dw_splits = 1;
-  float* phiX[CRL_MAX_LAYERS] = {}; float* phiZ[CRL_MAX_LAYERS] = {};
-  float* psiX[CRL_MAX_LAYERS] = {}; float* psiZ[CRL_MAX_LAYERS] = {};
-  float *phi_out = nullptr, *psi_out = nullptr, *phi_g = nullptr, *psi_g = nullptr;
-  float *lse_row = nullptr, *lse_col = nullptr, *lse_row_g = nullptr, *lse_col_g = nullptr;
-  float *dphi = nullptr, *dpsi = nullptr, *dz[2] = {nullptr, nullptr}, *dz_psi[2] = {nullptr, nullptr};
-  float *loss_acc = nullptr, *loss_dev = nullptr, *loss_part = nullptr;
-  unsigned* loss_ticket = nullptr;
-  int *status = nullptr, *adam_t = nullptr, *skip = nullptr;
-  float *stage_s = nullptr, *stage_a = nullptr, *stage_g = nullptr;
-  // runtime
-  cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  std::map<GraphKey, cudaGraphExec_t> graphs;
-  ncclComm_t comm = nullptr;
-  int num_sms = 148;
-  int launches = 0;
-  std::string err;
-  // profiling mode (eager launches bracketed by CUDA events, per-stage totals)
-  bool prof_on = false;
-  struct ProfEv { std::string name; cudaEvent_t a, b; };
-  std::vector<ProfEv> prof_pending;
-  std::vector<std::string> prof_names;
-  std::map<std::string, std::pair<double, int>> prof_acc;
-  std::vector<cudaEvent_t> ev_pool;
-  size_t ev_pool_next = 0;
-};
-
-// Brackets one launch with CUDA events when the context is in profiling mode (events come
-// from a pool so the host enqueue stays cheap; see also spin_kernel below).
-static cudaEvent_t pool_event(crl_ctx* c);
-struct Stage {
-  crl_ctx* c; cudaStream_t st; cudaEvent_t b = nullptr;
-  Stage(crl_ctx* c_, cudaStream_t st_, const std::string& name) : c(c_), st(st_) {
-    if (!c->prof_on) return;
-    cudaEvent_t a = pool_event(c);
-    b = pool_event(c);
-    cudaEventRecord(a, st);
-    c->prof_pending.push_back({name, a, b});
-  }
-  ~Stage() { if (b) cudaEventRecord(b, st); }
-};
-
-static cudaEvent_t pool_event(crl_ctx* c) {
+cudaEvent_t pool_event(crl_ctx* c) {
   if (c->ev_pool_next == c->ev_pool.size()) {
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -156,25 +50,6 @@ __global__ void spin_kernel(unsigned long long ns) {
   while (t - t0 < ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
 }
 
-static crl_status fail(crl_ctx* ctx, crl_status st, const std::string& msg) {
-  g_last_error = msg;
-  if (ctx) ctx->err = msg;
-  return st;
-}
-
-#define CU(call)                                                                           \
-  do {                                                                                     \
-    cudaError_t _e = (call);                                                               \
-    if (_e != cudaSuccess)                                                                 \
-      return fail(ctx, CRL_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
-  } while (0)
-
-#define NC(call)                                                                           \
-  do {                                                                                     \
-    ncclResult_t _r = (call);                                                              \
-    if (_r != ncclSuccess)                                                                 \
-      return fail(ctx, CRL_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r));     \
-  } while (0)
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
@@ -196,13 +71,41 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   Carver s{scr_base};
   c->dw_splits = dw_splits_for(Bl);
   c->grads = s.take<float>(c->sizes.n_params * c->dw_splits);
-  for (int l = 1; l <= k.depth; ++l) {
-    c->phiX[l] = s.take<float>((size_t)Bl * Wd);
-    c->psiX[l] = s.take<float>((size_t)Bl * Wd);
-  }
-  for (int l = 0; l < k.depth; ++l) {
-    c->phiZ[l] = s.take<float>((size_t)Bl * Wd);
-    c->psiZ[l] = s.take<float>((size_t)Bl * Wd);
+  const bool bf = k.precision == CRL_BF16;
+  c->bf16 = bf;
+  if (!bf) {
+    for (int l = 1; l <= k.depth; ++l) {
+      c->phiX[l] = s.take<float>((size_t)Bl * Wd);
+      c->psiX[l] = s.take<float>((size_t)Bl * Wd);
+    }
+    for (int l = 0; l < k.depth; ++l) {
+      c->phiZ[l] = s.take<float>((size_t)Bl * Wd);
+      c->psiZ[l] = s.take<float>((size_t)Bl * Wd);
+    }
+  } else {
+    // bf16 operands; every row pitch is a multiple of 8 elements (16 B, TMA requirement)
+    c->wshadow = s.take<__nv_bfloat16>(c->sizes.n_params);
+    c->ld0_phi = round_up(k.obs_dim + k.act_dim, 8);
+    c->ld0_psi = round_up(k.goal_dim, 8);
+    c->x0_phi = s.take<__nv_bfloat16>((size_t)Bl * c->ld0_phi);
+    c->x0_psi = s.take<__nv_bfloat16>((size_t)Bl * c->ld0_psi);
+    for (int l = 1; l <= k.depth; ++l) {
+      c->phiXb[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
+      c->psiXb[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
+    }
+    for (int l = 0; l < k.depth; ++l) {
+      c->phiZb[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
+      c->psiZb[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
+    }
+    c->phi_outb = s.take<__nv_bfloat16>((size_t)Bl * D);
+    c->psi_outb = s.take<__nv_bfloat16>((size_t)Bl * D);
+    c->dphib = s.take<__nv_bfloat16>((size_t)Bl * D);
+    c->dpsib = s.take<__nv_bfloat16>((size_t)Bl * D);
+    const int wm = Wd > D ? Wd : D;
+    for (int i = 0; i < 2; ++i) {
+      c->dzb_phi[i] = s.take<__nv_bfloat16>((size_t)Bl * wm);
+      c->dzb_psi[i] = s.take<__nv_bfloat16>((size_t)Bl * wm);
+    }
   }
   c->phi_out = s.take<float>((size_t)Bl * D);
   c->psi_out = s.take<float>((size_t)Bl * D);
@@ -225,10 +128,12 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   c->dphi = s.take<float>((size_t)Bl * D);
   c->dpsi = s.take<float>((size_t)Bl * D);
   const int wmax = Wd > D ? Wd : D;
-  c->dz[0] = s.take<float>((size_t)Bl * wmax);
-  c->dz[1] = s.take<float>((size_t)Bl * wmax);
-  c->dz_psi[0] = s.take<float>((size_t)Bl * wmax);
-  c->dz_psi[1] = s.take<float>((size_t)Bl * wmax);
+  if (!bf) {
+    c->dz[0] = s.take<float>((size_t)Bl * wmax);
+    c->dz[1] = s.take<float>((size_t)Bl * wmax);
+    c->dz_psi[0] = s.take<float>((size_t)Bl * wmax);
+    c->dz_psi[1] = s.take<float>((size_t)Bl * wmax);
+  }
   c->loss_acc = s.take<float>(16);
   c->loss_part = s.take<float>((size_t)4 * loss_partial_blocks(Bl));
   c->loss_ticket = s.take<unsigned>(1);
@@ -260,8 +165,8 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
   if (k->energy < 0 || k->energy > 2) return fail(ctx, CRL_EINVAL, "energy");
   if (k->loss < 0 || k->loss > 2) return fail(ctx, CRL_EINVAL, "loss");
   if (k->precision != CRL_FP32 && k->precision != CRL_BF16) return fail(ctx, CRL_EINVAL, "precision");
-  if (k->precision == CRL_BF16)
-    return fail(ctx, CRL_EUNSUPPORTED, "bf16 tensor-core path not built yet");
+  if (k->precision == CRL_BF16 && (k->width % 16 != 0))
+    return fail(ctx, CRL_EUNSUPPORTED, "bf16 path needs width % 16 == 0");
   if (k->world_size < 1 || k->rank < 0 || k->rank >= k->world_size)
     return fail(ctx, CRL_EINVAL, "rank / world_size");
   if (k->batch_local < 1 || (long long)k->batch_local * k->world_size < 2)
@@ -365,6 +270,10 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaDeviceSynchronize() != cudaSuccess)
     return cleanup(fail(nullptr, CRL_ECUDA, "context initialisation failed"));
 
+  if (ctx->bf16) {
+    crl_status bs = bf16_prepare(ctx);
+    if (bs != CRL_OK) { std::string m = ctx->err; delete ctx; return fail(nullptr, bs, m); }
+  }
   if (cfg->world_size > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
@@ -645,7 +554,8 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
 
   if (ctx->prof_on) {                    // eager, event-bracketed launches
     spin_kernel<<<1, 1, 0, st>>>(300000ull);
-    crl_status rs = enqueue_critic(ctx, s, a, g, loss_dev, grads_out, st, st);
+    crl_status rs = ctx->bf16 ? enqueue_critic_bf16(ctx, s, a, g, loss_dev, grads_out, st, st)
+                              : enqueue_critic(ctx, s, a, g, loss_dev, grads_out, st, st);
     if (rs != CRL_OK) return rs;
     if (loss_host) CU(cudaMemcpyAsync(loss_out, loss_dev, 16, cudaMemcpyDeviceToHost, st));
     return CRL_OK;
@@ -655,8 +565,10 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
   if (it == ctx->graphs.end()) {
     // capture the schedule once on the private capture stream
     CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-    crl_status rs = enqueue_critic(ctx, s, a, g, loss_dev, grads_out, ctx->cap_stream,
-                                   ctx->cap_stream2);
+    crl_status rs = ctx->bf16 ? enqueue_critic_bf16(ctx, s, a, g, loss_dev, grads_out, ctx->cap_stream,
+                                                    ctx->cap_stream2)
+                              : enqueue_critic(ctx, s, a, g, loss_dev, grads_out, ctx->cap_stream,
+                                               ctx->cap_stream2);
     cudaGraph_t graph = nullptr;
     cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
     if (rs != CRL_OK) { if (graph) cudaGraphDestroy(graph); return rs; }

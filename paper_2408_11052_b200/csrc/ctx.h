@@ -1,0 +1,164 @@
+// ctx.h — internal definition of crl_ctx and the host-side helpers shared by the C ABI
+// (crl_api.cu) and the BF16 tensor-core schedule (step_bf16.cu).  Not part of the ABI.
+#pragma once
+#include "common.cuh"
+#include "tc_common.cuh"
+
+#include <nccl.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace crl {
+cudaError_t launch_buffer_insert(const float*, const float*, const uint8_t*, int, int, int, int, int,
+                                 int, int, uint32_t, float*, float*, uint32_t*, uint32_t*,
+                                 cudaStream_t);
+cudaError_t launch_relabel_sample(int, int, int, int, int, int, int, int, int, int, uint32_t,
+                                  uint32_t, uint64_t, uint64_t, const float*, const float*,
+                                  const uint32_t*, const uint64_t*, float*, float*, float*,
+                                  int64_t*, int*, cudaStream_t);
+cudaError_t mlp_forward_layer_f32(int, int, int, const float*, int, const float*, int, int,
+                                  const float*, const float*, float*, float*, int, cudaStream_t);
+cudaError_t mlp_backward_dx_f32(int, int, int, const float*, const float*, const float*, float*,
+                                int, cudaStream_t);
+cudaError_t mlp_backward_dw_f32(int, int, int, const float*, int, const float*, int, int,
+                                const float*, float*, float*, int, size_t, cudaStream_t);
+int dw_splits_for(int Bn);
+void gemm_set_num_sms(int n);
+void logits_set_num_sms(int n);
+cudaError_t launch_reduce_partials(float*, size_t, int, cudaStream_t);
+bool logits_simt_supports(int D);
+cudaError_t logits_lse_f32(int, int, const float*, int, const float*, int, float*, cudaStream_t);
+cudaError_t logits_grad_f32(int, int, const float*, int, int, const float*, int, const float*,
+                            const float*, float, float, float, float, float, float*, cudaStream_t);
+cudaError_t launch_loss_partial(const float*, const float*, int, int, int, const float*,
+                                const float*, float*, float*, unsigned*, int, float, float, float,
+                                float, float*, int*, int*, int*, cudaStream_t);
+int loss_partial_blocks(int Bl);
+cudaError_t launch_loss_finalize(const float*, float, float, float, float, float*, int*, int*,
+                                 int*, cudaStream_t);
+cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, float, float, float,
+                        float, const int*, const int*, int*, void*, int, cudaStream_t);
+}  // namespace crl
+
+using namespace crl;
+
+extern thread_local std::string g_last_error;
+
+// ----------------------------------------------------------------------------------------
+// workspace carving (shared by crl_workspace_size and crl_create)
+// ----------------------------------------------------------------------------------------
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct GraphKey {
+  const void *s, *a, *g, *loss, *grads;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(s, a, g, loss, grads) < std::tie(o.s, o.a, o.g, o.loss, o.grads);
+  }
+};
+
+struct crl_ctx {
+  crl_config cfg{};
+  crl_sizes sizes{};
+  crl_memory mem{};
+  EncoderPlan phi_plan{}, psi_plan{};
+  int N = 0;
+  // replay buffer
+  float* obs_ring = nullptr; float* act_ring = nullptr;
+  uint32_t* ep_end = nullptr; uint32_t* open_start = nullptr; uint64_t* qtab = nullptr;
+  int obs_stride = 0, act_stride = 0;
+  uint64_t n_ins = 0;
+  // scratch
+  float* grads = nullptr;             // [dw_splits][n_params] split-K partials, slice 0 = sum
+  int dw_splits = 1;
+  float* phiX[CRL_MAX_LAYERS] = {}; float* phiZ[CRL_MAX_LAYERS] = {};
+  float* psiX[CRL_MAX_LAYERS] = {}; float* psiZ[CRL_MAX_LAYERS] = {};
+  float *phi_out = nullptr, *psi_out = nullptr, *phi_g = nullptr, *psi_g = nullptr;
+  float *lse_row = nullptr, *lse_col = nullptr, *lse_row_g = nullptr, *lse_col_g = nullptr;
+  float *dphi = nullptr, *dpsi = nullptr, *dz[2] = {nullptr, nullptr}, *dz_psi[2] = {nullptr, nullptr};
+  float *loss_acc = nullptr, *loss_dev = nullptr, *loss_part = nullptr;
+  unsigned* loss_ticket = nullptr;
+  int *status = nullptr, *adam_t = nullptr, *skip = nullptr;
+  float *stage_s = nullptr, *stage_a = nullptr, *stage_g = nullptr;
+  // runtime
+  cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+  int launches = 0;
+  std::string err;
+  // profiling mode (eager launches bracketed by CUDA events, per-stage totals)
+  bool prof_on = false;
+  struct ProfEv { std::string name; cudaEvent_t a, b; };
+  std::vector<ProfEv> prof_pending;
+  std::vector<std::string> prof_names;
+  std::map<std::string, std::pair<double, int>> prof_acc;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_pool_next = 0;
+  // ---------------- BF16 tensor-core path (precision == CRL_BF16)
+  bool bf16 = false;
+  __nv_bfloat16* wshadow = nullptr;           // bf16 copy of params (written by Adam)
+  __nv_bfloat16 *x0_phi = nullptr, *x0_psi = nullptr;   // [B][ld0_phi], [B][ld0_psi]
+  int ld0_phi = 0, ld0_psi = 0;
+  __nv_bfloat16* phiXb[CRL_MAX_LAYERS] = {}; __nv_bfloat16* phiZb[CRL_MAX_LAYERS] = {};
+  __nv_bfloat16* psiXb[CRL_MAX_LAYERS] = {}; __nv_bfloat16* psiZb[CRL_MAX_LAYERS] = {};
+  __nv_bfloat16 *phi_outb = nullptr, *psi_outb = nullptr;   // Y in bf16 (logits operands)
+  __nv_bfloat16 *dphib = nullptr, *dpsib = nullptr;         // dY in bf16
+  __nv_bfloat16 *dzb_phi[2] = {nullptr, nullptr}, *dzb_psi[2] = {nullptr, nullptr};
+  struct TcLayer {
+    CUtensorMap fwdA, fwdB, dwA, dwB, dxA, dxB;
+    int bn_fwd = 64, bn_dw = 64, bn_dx = 64;
+    const __nv_bfloat16* dz = nullptr;   // dZ_l (bf16) consumed by this layer's backward
+    __nv_bfloat16* dzprev = nullptr;     // dZ_{l-1} written by this layer's dX GEMM
+  };
+  std::vector<TcLayer> tc_phi, tc_psi;
+};
+
+// Brackets one launch with CUDA events when the context is in profiling mode (events come
+// from a pool so the host enqueue stays cheap; see also spin_kernel below).
+cudaEvent_t pool_event(crl_ctx* c);
+struct Stage {
+  crl_ctx* c; cudaStream_t st; cudaEvent_t b = nullptr;
+  Stage(crl_ctx* c_, cudaStream_t st_, const std::string& name) : c(c_), st(st_) {
+    if (!c->prof_on) return;
+    cudaEvent_t a = pool_event(c);
+    b = pool_event(c);
+    cudaEventRecord(a, st);
+    c->prof_pending.push_back({name, a, b});
+  }
+  ~Stage() { if (b) cudaEventRecord(b, st); }
+};
+
+inline crl_status fail(crl_ctx* ctx, crl_status st, const std::string& msg) {
+  g_last_error = msg;
+  if (ctx) ctx->err = msg;
+  return st;
+}
+
+#define CU(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(ctx, CRL_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+#define NC(call)                                                                           \
+  do {                                                                                     \
+    ncclResult_t _r = (call);                                                              \
+    if (_r != ncclSuccess)                                                                 \
+      return fail(ctx, CRL_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r));     \
+  } while (0)
+

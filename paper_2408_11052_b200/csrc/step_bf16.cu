@@ -1,0 +1,231 @@
+// step_bf16.cu — the BF16 tensor-core schedule of crl_critic_step (precision == CRL_BF16):
+// bf16 operands everywhere a contraction happens (encoder GEMMs on tcgen05, fed by TMA),
+// fp32 accumulation, statistics, loss, gradients and optimiser state.
+//
+// Per encoder and layer l (W_l stored [in][out], bf16 shadow written by the Adam kernel):
+//   fwd  : Z_l = X_l W_l + b_l  -> Z_l (bf16), X_{l+1} = act(Z_l) (bf16)      [output: Y fp32+bf16]
+//   dW_l = X_l^T dZ_l  (split-K over the batch, fp32 partial slices), db_l = colsum(dZ_l)
+//   dX   : dZ_{l-1} = (dZ_l W_l^T) * act'(Z_{l-1})  (bf16)
+// All tensor maps are built once at context creation (buffers are context-owned).
+#include "ctx.h"
+
+namespace crl {
+cudaError_t logits_lse_f32(int, int, const float*, int, const float*, int, float*, cudaStream_t);
+cudaError_t logits_grad_f32(int, int, const float*, int, int, const float*, int, const float*,
+                            const float*, float, float, float, float, float, float*, cudaStream_t);
+cudaError_t launch_loss_partial(const float*, const float*, int, int, int, const float*,
+                                const float*, float*, float*, unsigned*, int, float, float, float,
+                                float, float*, int*, int*, int*, cudaStream_t);
+cudaError_t launch_loss_finalize(const float*, float, float, float, float, float*, int*, int*,
+                                 int*, cudaStream_t);
+cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, float, float, float,
+                        float, const int*, const int*, int*, void*, int, cudaStream_t);
+cudaError_t launch_reduce_partials(float*, size_t, int, cudaStream_t);
+namespace tc {
+bool make_map_bf16(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
+int tc_pick_bn(int M, int N, int num_sms);
+cudaError_t tc_forward(int, const CUtensorMap&, const CUtensorMap&, int, int, int, const float*,
+                       __nv_bfloat16*, __nv_bfloat16*, int, float*, int, int, cudaStream_t);
+cudaError_t tc_backward_dx(int, const CUtensorMap&, const CUtensorMap&, int, int, int,
+                           const __nv_bfloat16*, __nv_bfloat16*, int, int, cudaStream_t);
+cudaError_t tc_backward_dw(int, const CUtensorMap&, const CUtensorMap&, int, int, int, float*, int,
+                           size_t, cudaStream_t);
+cudaError_t launch_prep_inputs(const float*, const float*, const float*, int, int, int, int,
+                               __nv_bfloat16*, int, __nv_bfloat16*, int, int, cudaStream_t);
+cudaError_t launch_colsum_bf16(const __nv_bfloat16*, int, int, int, float*, int, size_t, cudaStream_t);
+cudaError_t launch_f32_to_bf16(const float*, __nv_bfloat16*, size_t, int, cudaStream_t);
+}  // namespace tc
+}  // namespace crl
+
+using namespace crl;
+
+static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const __nv_bfloat16* x0, int ld0,
+                                     __nv_bfloat16** Xb, __nv_bfloat16** Zb, __nv_bfloat16* dY,
+                                     __nv_bfloat16** dzb, std::vector<crl_ctx::TcLayer>& out) {
+  const int Bl = ctx->cfg.batch_local, Wd = ctx->cfg.width, L = P.n_layers;
+  out.assign(L, crl_ctx::TcLayer{});
+  for (int l = 0; l < L; ++l) {
+    auto& T = out[l];
+    const int in = P.layer[l].in, o = P.layer[l].out;
+    const __nv_bfloat16* X = (l == 0) ? x0 : Xb[l];
+    const int ldx = (l == 0) ? ld0 : Wd;
+    const __nv_bfloat16* W = ctx->wshadow + P.layer[l].w_off;
+    T.dz = (l == L - 1) ? dY : dzb[(L - 2 - l) % 2];
+    T.dzprev = (l > 0) ? dzb[(L - 1 - l) % 2] : nullptr;
+    T.bn_fwd = tc::tc_pick_bn(Bl, o, ctx->num_sms);
+    T.bn_dw = tc::tc_pick_bn(in, o, ctx->num_sms);
+    T.bn_dx = tc::tc_pick_bn(Bl, in, ctx->num_sms);
+    bool ok = tc::make_map_bf16(&T.fwdA, X, in, Bl, ldx, 64, 128) &&       // X  K-major
+              tc::make_map_bf16(&T.fwdB, W, o, in, o, 64, 64) &&           // W  MN-major (N = out)
+              tc::make_map_bf16(&T.dwA, X, in, Bl, ldx, 64, 64) &&         // X  MN-major (M = in)
+              tc::make_map_bf16(&T.dwB, T.dz, o, Bl, o, 64, 64);           // dZ MN-major (N = out)
+    if (l > 0)
+      ok = ok && tc::make_map_bf16(&T.dxA, T.dz, o, Bl, o, 64, 128) &&     // dZ K-major (K = out)
+           tc::make_map_bf16(&T.dxB, W, o, in, o, 64, T.bn_dx);            // W  K-major (N = in)
+    if (!ok) return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed (driver entry point missing?)");
+  }
+  return CRL_OK;
+}
+
+crl_status bf16_prepare(crl_ctx* ctx) {
+  const crl_config& k = ctx->cfg;
+  crl_status st = build_encoder_plan(ctx, ctx->phi_plan, ctx->x0_phi, ctx->ld0_phi, ctx->phiXb, ctx->phiZb,
+                                     ctx->dphib, ctx->dzb_phi, ctx->tc_phi);
+  if (st != CRL_OK) return st;
+  st = build_encoder_plan(ctx, ctx->psi_plan, ctx->x0_psi, ctx->ld0_psi, ctx->psiXb, ctx->psiZb, ctx->dpsib,
+                          ctx->dzb_psi, ctx->tc_psi);
+  if (st != CRL_OK) return st;
+  // initial bf16 shadow of the caller's parameters; zero the padded input rows
+  CU(tc::launch_f32_to_bf16(ctx->mem.params, ctx->wshadow, ctx->sizes.n_params, ctx->num_sms, 0));
+  CU(cudaMemset(ctx->x0_phi, 0, (size_t)k.batch_local * ctx->ld0_phi * 2));
+  CU(cudaMemset(ctx->x0_psi, 0, (size_t)k.batch_local * ctx->ld0_psi * 2));
+  CU(cudaDeviceSynchronize());
+  return CRL_OK;
+}
+
+static crl_status enc_forward_bf16(crl_ctx* ctx, const char* tag, const EncoderPlan& P,
+                                   std::vector<crl_ctx::TcLayer>& T, __nv_bfloat16** Xb, __nv_bfloat16** Zb,
+                                   float* yf, __nv_bfloat16* yb, cudaStream_t st, int* nl) {
+  const crl_config& k = ctx->cfg;
+  const int Bl = k.batch_local, L = P.n_layers;
+  for (int l = 0; l < L; ++l) {
+    const LayerPlan& Lp = P.layer[l];
+    const bool last = l == L - 1;
+    Stage sg(ctx, st, std::string(tag) + "_fwd_l" + std::to_string(l));
+    CU(tc::tc_forward(T[l].bn_fwd, T[l].fwdA, T[l].fwdB, Bl, Lp.in, Lp.out, ctx->mem.params + Lp.b_off,
+                      last ? nullptr : Zb[l], last ? yb : Xb[l + 1], Lp.out, last ? yf : nullptr, Lp.out,
+                      k.activation, st));
+    ++*nl;
+  }
+  return CRL_OK;
+}
+
+static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const EncoderPlan& P,
+                                    std::vector<crl_ctx::TcLayer>& T, __nv_bfloat16** Zb, cudaStream_t st,
+                                    int* nl) {
+  const crl_config& k = ctx->cfg;
+  const int Bl = k.batch_local, L = P.n_layers;
+  for (int l = L - 1; l >= 0; --l) {
+    const LayerPlan& Lp = P.layer[l];
+    {
+      Stage sg(ctx, st, std::string(tag) + "_bwd_dw_l" + std::to_string(l));
+      CU(tc::tc_backward_dw(T[l].bn_dw, T[l].dwA, T[l].dwB, Bl, Lp.in, Lp.out, ctx->grads + Lp.w_off,
+                            ctx->dw_splits, ctx->sizes.n_params, st));
+      ++*nl;
+    }
+    {
+      Stage sg(ctx, st, std::string(tag) + "_bwd_db_l" + std::to_string(l));
+      CU(tc::launch_colsum_bf16(T[l].dz, Bl, Lp.out, Lp.out, ctx->grads + Lp.b_off, ctx->dw_splits,
+                                ctx->sizes.n_params, st));
+      ++*nl;
+    }
+    if (l > 0) {
+      Stage sg(ctx, st, std::string(tag) + "_bwd_dx_l" + std::to_string(l));
+      CU(tc::tc_backward_dx(T[l].bn_dx, T[l].dxA, T[l].dxB, Bl, Lp.in, Lp.out, Zb[l - 1], T[l].dzprev, Lp.in,
+                            k.activation, st));
+      ++*nl;
+    }
+  }
+  return CRL_OK;
+}
+
+static void fork2(crl_ctx* ctx, cudaStream_t s0, cudaStream_t s1) {
+  if (s0 == s1) return;
+  cudaEventRecord(ctx->ev_fork, s0);
+  cudaStreamWaitEvent(s1, ctx->ev_fork, 0);
+}
+static void join2(crl_ctx* ctx, cudaStream_t s0, cudaStream_t s1) {
+  if (s0 == s1) return;
+  cudaEventRecord(ctx->ev_join, s1);
+  cudaStreamWaitEvent(s0, ctx->ev_join, 0);
+}
+
+crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, const float* g, float* loss_out,
+                               float* grads_out, cudaStream_t st, cudaStream_t st2) {
+  const crl_config& k = ctx->cfg;
+  const int Bl = k.batch_local, W = k.world_size, N = ctx->N, D = k.repr_dim;
+  const float invN = 1.0f / (float)N;
+  const float c_f = (k.loss == CRL_LOSS_BWD) ? 0.f : 1.f;
+  const float c_b = (k.loss == CRL_LOSS_FWD) ? 0.f : 1.f;
+  int nl = 0;
+  crl_status rs;
+  {
+    Stage sg(ctx, st, "prep_inputs");
+    CU(tc::launch_prep_inputs(s, a, g, Bl, k.obs_dim, k.act_dim, k.goal_dim, ctx->x0_phi, ctx->ld0_phi,
+                              ctx->x0_psi, ctx->ld0_psi, ctx->num_sms, st));
+    ++nl;
+  }
+  fork2(ctx, st, st2);
+  rs = enc_forward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiXb, ctx->psiZb, ctx->psi_out,
+                        ctx->psi_outb, st2, &nl);
+  if (rs != CRL_OK) return rs;
+  rs = enc_forward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiXb, ctx->phiZb, ctx->phi_out,
+                        ctx->phi_outb, st, &nl);
+  if (rs != CRL_OK) return rs;
+  join2(ctx, st, st2);
+  if (W > 1) {
+    NC(ncclGroupStart());
+    NC(ncclAllGather(ctx->phi_out, ctx->phi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
+    NC(ncclAllGather(ctx->psi_out, ctx->psi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
+    NC(ncclGroupEnd());
+  }
+  fork2(ctx, st, st2);
+  { Stage sg(ctx, st2, "lse_col");
+    CU(logits_lse_f32(D, k.energy, ctx->psi_out, Bl, ctx->phi_g, N, ctx->lse_col, st2)); ++nl; }
+  { Stage sg(ctx, st, "lse_row");
+    CU(logits_lse_f32(D, k.energy, ctx->phi_out, Bl, ctx->psi_g, N, ctx->lse_row, st)); ++nl; }
+  join2(ctx, st, st2);
+  if (W > 1) {
+    NC(ncclGroupStart());
+    NC(ncclAllGather(ctx->lse_row, ctx->lse_row_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
+    NC(ncclAllGather(ctx->lse_col, ctx->lse_col_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
+    NC(ncclGroupEnd());
+  }
+  { Stage sg(ctx, st, "loss");
+    CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,
+                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, W == 1, invN, c_f, c_b,
+                           k.beta_lse, loss_out, ctx->skip, ctx->adam_t, ctx->status, st));
+    ++nl; }
+  if (W > 1) {
+    NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
+    CU(launch_loss_finalize(ctx->loss_acc, invN, c_f, c_b, k.beta_lse, loss_out, ctx->skip, ctx->adam_t,
+                            ctx->status, st));
+    ++nl;
+  }
+  const int row_off = k.rank * Bl;
+  fork2(ctx, st, st2);
+  { Stage sg(ctx, st2, "grad_psi");
+    CU(logits_grad_f32(D, k.energy, ctx->psi_out, Bl, row_off, ctx->phi_g, N, ctx->lse_col, ctx->lse_row_g,
+                       c_b, c_f, 0.f, k.beta_lse, invN, ctx->dpsi, st2));
+    CU(tc::launch_f32_to_bf16(ctx->dpsi, ctx->dpsib, (size_t)Bl * D, ctx->num_sms, st2));
+    nl += 2; }
+  rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, &nl);
+  if (rs != CRL_OK) return rs;
+  { Stage sg(ctx, st, "grad_phi");
+    CU(logits_grad_f32(D, k.energy, ctx->phi_out, Bl, row_off, ctx->psi_g, N, ctx->lse_row, ctx->lse_col_g,
+                       c_f, c_b, k.beta_lse, 0.f, invN, ctx->dphi, st));
+    CU(tc::launch_f32_to_bf16(ctx->dphi, ctx->dphib, (size_t)Bl * D, ctx->num_sms, st));
+    nl += 2; }
+  rs = enc_backward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiZb, st, &nl);
+  if (rs != CRL_OK) return rs;
+  join2(ctx, st, st2);
+  int adam_splits = ctx->dw_splits;
+  if (W > 1) {
+    if (ctx->dw_splits > 1) {
+      Stage sg(ctx, st, "reduce_partials");
+      CU(launch_reduce_partials(ctx->grads, ctx->sizes.n_params, ctx->dw_splits, st));
+      ++nl;
+    }
+    adam_splits = 1;
+    NC(ncclAllReduce(ctx->grads, ctx->grads, ctx->sizes.n_params, ncclFloat32, ncclSum, ctx->comm, st));
+  }
+  { Stage sg(ctx, st, "adam");
+    CU(launch_adam(ctx->mem.params, ctx->grads, adam_splits, ctx->mem.adam_m, ctx->mem.adam_v,
+                   ctx->sizes.n_params, k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay, ctx->adam_t,
+                   ctx->skip, ctx->status, ctx->wshadow, ctx->num_sms, st));
+    ++nl; }
+  if (grads_out)
+    CU(cudaMemcpyAsync(grads_out, ctx->grads, ctx->sizes.n_params * 4, cudaMemcpyDeviceToDevice, st));
+  ctx->launches = nl;
+  return CRL_OK;
+}

@@ -1,0 +1,379 @@
+// tc_gemm.cu — bf16 tcgen05 GEMMs (TMA -> SMEM -> tcgen05.mma -> TMEM -> epilogue) for the
+// phi/psi encoders on the BF16 path (A2 forward, A5 backward).
+//
+// Paper: §3.1 P:193-195 (phi(s,a), psi(g)), Table 2, §5.4 P:387-465.
+//   forward  Z[B][out]  = X[B][in]  . W[in][out]   A K-major,   B MN-major (W as stored)
+//   dX       dX[B][in]  = dZ[B][out] . W^T          A K-major,   B K-major  (W as stored)
+//   dW       dW[in][out] = X^T . dZ (K = batch)     A MN-major,  B MN-major (X, dZ as stored)
+// so no transposed copies are ever made: the operand major-ness is a descriptor bit.
+//
+// Kernel anatomy (one 128 x BN output tile per CTA, 256 threads):
+//   warp 0 / lane 0 : TMA producer, STAGES-deep ring of (A, B) K-blocks of 64 (SW128)
+//   warp 1 / lane 0 : tcgen05.mma issuer (M=128, N=BN, K=16 per instruction), commits each
+//                     stage back to the producer and the accumulator to the epilogue
+//   warp 2          : TMEM allocation (BN fp32 columns)
+//   warps 4..7      : epilogue, one TMEM lane (= output row) per thread, tcgen05.ld x16,
+//                     fused bias / activation / activation-derivative, vector stores
+// Split-K along blockIdx.z writes deterministic fp32 partial slices (dW).
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace crl {
+namespace tc {
+
+enum TcEpi { TEPI_FWD_HIDDEN = 0, TEPI_FWD_OUT = 1, TEPI_DX = 2, TEPI_DW = 3 };
+
+struct TcGemmArgs {
+  int M, N, K, k_per_split;
+  const float* bias;               // FWD_*: [N] fp32 master bias
+  __nv_bfloat16* out_bf;           // FWD_HIDDEN: act(Z); FWD_OUT: Y; DX: dZ_prev
+  __nv_bfloat16* out_z;            // FWD_HIDDEN: Z (bf16)
+  int ld_bf;                       // pitch (elements) of out_bf / out_z / zprev
+  float* out_f;                    // FWD_OUT: Y fp32; DW: dW partial slices
+  int ld_f;
+  size_t split_stride;             // floats between DW partial slices
+  const __nv_bfloat16* zprev;      // DX: pre-activation of the previous layer
+  int act;
+};
+
+constexpr int BM = 128, BK = 64, STAGES = 4;
+
+template <int BN>
+struct TcSmem {
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr size_t bytes = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+};
+
+__device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float (&v)[16], int nvalid) {
+  if (nvalid >= 16) {
+    uint4 a, b;
+    a.x = pack_bf16x2(v[0], v[1]);   a.y = pack_bf16x2(v[2], v[3]);
+    a.z = pack_bf16x2(v[4], v[5]);   a.w = pack_bf16x2(v[6], v[7]);
+    b.x = pack_bf16x2(v[8], v[9]);   b.y = pack_bf16x2(v[10], v[11]);
+    b.z = pack_bf16x2(v[12], v[13]); b.w = pack_bf16x2(v[14], v[15]);
+    reinterpret_cast<uint4*>(dst)[0] = a;
+    reinterpret_cast<uint4*>(dst)[1] = b;
+  } else {
+    for (int i = 0; i < nvalid; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+__device__ __forceinline__ void store_f32x16(float* dst, const float (&v)[16], int nvalid) {
+  if (nvalid >= 16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  } else {
+    for (int i = 0; i < nvalid; ++i) dst[i] = v[i];
+  }
+}
+__device__ __forceinline__ void load_bf16x16(const __nv_bfloat16* src, float (&v)[16], int nvalid) {
+  if (nvalid >= 16) {
+    uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+      float2 f = __bfloat1622float2(h);
+      v[2 * i] = f.x; v[2 * i + 1] = f.y;
+    }
+  } else {
+    for (int i = 0; i < 16; ++i) v[i] = i < nvalid ? __bfloat162float(src[i]) : 0.f;
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                         const __grid_constant__ CUtensorMap tmB,
+                                                         TcGemmArgs p) {
+  using S = TcSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * S::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * S::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kbeg = blockIdx.z * p.k_per_split;
+  const int kend = min(p.K, kbeg + p.k_per_split);
+  const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------ TMA producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_expect_tx(&full[s], S::A_BYTES + S::B_BYTES);
+      const int k = kbeg + kb * BK;
+      uint8_t* a_dst = sA + s * S::A_BYTES;
+      uint8_t* b_dst = sB + s * S::B_BYTES;
+      if (!A_MN) {
+        tma_load_2d(a_dst, &tmA, &full[s], k, m0);                  // dims {K, M}
+      } else {
+#pragma unroll
+        for (int c = 0; c < BM / 64; ++c) tma_load_2d(a_dst + c * BK * 128, &tmA, &full[s], m0 + 64 * c, k);
+      }
+      if (!B_MN) {
+        tma_load_2d(b_dst, &tmB, &full[s], k, n0);                  // dims {K, N}
+      } else {
+#pragma unroll
+        for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * BK * 128, &tmB, &full[s], n0 + 64 * c, k);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t a_base = smem_u32(sA + s * S::A_BYTES);
+      const uint32_t b_base = smem_u32(sB + s * S::B_BYTES);
+#pragma unroll
+      for (int ks = 0; ks < BK / 16; ++ks) {
+        const uint64_t ad = A_MN ? smem_desc_sw128(a_base + ks * 2048, BK * 128, 1024)
+                                 : smem_desc_sw128(a_base + ks * 32, 16, 1024);
+        const uint64_t bd = B_MN ? smem_desc_sw128(b_base + ks * 2048, BK * 128, 1024)
+                                 : smem_desc_sw128(b_base + ks * 32, 16, 1024);
+        mma_bf16(tmem, ad, bd, idesc, (kb | ks) != 0);
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(tfull);
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp - 4;
+    const int row = m0 + q * 32 + lane;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const bool rv = row < p.M;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+      if (nkb == 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+      const int n = n0 + c0;
+      const int nvalid = min(16, p.N - n);
+      if (!rv || nvalid <= 0) continue;
+      if (EPI == TEPI_FWD_HIDDEN || EPI == TEPI_FWD_OUT) {
+        float bb[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) bb[i] = (i < nvalid) ? p.bias[n + i] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += bb[i];
+        if (EPI == TEPI_FWD_HIDDEN) {
+          store_bf16x16(p.out_z + (size_t)row * p.ld_bf + n, v, nvalid);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = act_f(v[i], p.act);
+          store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
+        } else {
+          store_f32x16(p.out_f + (size_t)row * p.ld_f + n, v, nvalid);
+          store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
+        }
+      } else if (EPI == TEPI_DX) {
+        float z[16];
+        load_bf16x16(p.zprev + (size_t)row * p.ld_bf + n, z, nvalid);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= act_grad_f(z[i], p.act);
+        store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
+      } else {
+        store_f32x16(p.out_f + (size_t)blockIdx.z * p.split_stride + (size_t)row * p.ld_f + n, v, nvalid);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, BN);
+  }
+}
+
+// -------------------------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map, SWIZZLE_128B, dims {inner, outer}, row pitch in elements.
+bool make_map_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
+                   uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcGemmArgs& p, int splits,
+                             cudaStream_t st) {
+  static bool attr = false;
+  const size_t smem = TcSmem<BN>::bytes;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, A_MN, B_MN, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, splits);
+  tc_gemm_kernel<BN, A_MN, B_MN, EPI><<<grid, 256, smem, st>>>(a, b, p);
+  return cudaGetLastError();
+}
+
+// Operand maps for one GEMM: boxes follow the kernel's TMA calls.
+//   A K-major: {K, M} box {64, 128};  A MN-major: {M, K} box {64, 64}
+//   B K-major: {K, N} box {64, BN};   B MN-major: {N, K} box {64, 64}
+int tc_pick_bn(int M, int N, int num_sms) {
+  if (N <= 64) return 64;
+  const long tiles128 = (long)((M + 127) / 128) * ((N + 127) / 128);
+  if (tiles128 * 2 <= num_sms) return 64;
+  return 128;
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+static cudaError_t dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const TcGemmArgs& p,
+                               int splits, cudaStream_t st) {
+  switch (bn) {
+    case 64: return launch_tc<64, A_MN, B_MN, EPI>(a, b, p, splits, st);
+    case 128: return launch_tc<128, A_MN, B_MN, EPI>(a, b, p, splits, st);
+    case 256: return launch_tc<256, A_MN, B_MN, EPI>(a, b, p, splits, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t tc_forward(int bn, const CUtensorMap& mapX, const CUtensorMap& mapW, int Bn, int in, int out,
+                       const float* bias, __nv_bfloat16* z, __nv_bfloat16* xn, int ld_bf, float* y_f32,
+                       int ld_f, int act, cudaStream_t st) {
+  TcGemmArgs p{};
+  p.M = Bn; p.N = out; p.K = in; p.k_per_split = in;
+  p.bias = bias; p.out_z = z; p.out_bf = xn; p.ld_bf = ld_bf; p.out_f = y_f32; p.ld_f = ld_f; p.act = act;
+  if (y_f32 == nullptr) return dispatch_bn<TEPI_FWD_HIDDEN, false, true>(bn, mapX, mapW, p, 1, st);
+  return dispatch_bn<TEPI_FWD_OUT, false, true>(bn, mapX, mapW, p, 1, st);
+}
+
+cudaError_t tc_backward_dx(int bn, const CUtensorMap& mapDZ, const CUtensorMap& mapWk, int Bn, int in, int out,
+                           const __nv_bfloat16* zprev, __nv_bfloat16* dzprev, int ld_bf, int act,
+                           cudaStream_t st) {
+  TcGemmArgs p{};
+  p.M = Bn; p.N = in; p.K = out; p.k_per_split = out;
+  p.zprev = zprev; p.out_bf = dzprev; p.ld_bf = ld_bf; p.act = act;
+  return dispatch_bn<TEPI_DX, false, false>(bn, mapDZ, mapWk, p, 1, st);
+}
+
+cudaError_t tc_backward_dw(int bn, const CUtensorMap& mapX_mn, const CUtensorMap& mapDZ_mn, int Bn, int in,
+                           int out, float* dW, int splits, size_t split_stride, cudaStream_t st) {
+  TcGemmArgs p{};
+  p.M = in; p.N = out; p.K = Bn;
+  p.k_per_split = ((Bn + splits - 1) / splits + BK - 1) / BK * BK;
+  p.out_f = dW; p.ld_f = out; p.split_stride = split_stride;
+  return dispatch_bn<TEPI_DW, true, true>(bn, mapX_mn, mapDZ_mn, p, splits, st);
+}
+
+// ---------------------------------------------------------------- small helpers (bf16 path)
+// X0 for phi: [s || a] -> bf16 [B][ld] (columns >= obs+act are left as written at init = 0);
+// X0 for psi: g -> bf16 [B][ldg]
+__global__ void prep_inputs_kernel(const float* __restrict__ s, const float* __restrict__ a,
+                                   const float* __restrict__ g, int Bn, int obs, int act, int goal,
+                                   __nv_bfloat16* __restrict__ x0, int ld0, __nv_bfloat16* __restrict__ g0,
+                                   int ldg) {
+  const int in0 = obs + act;
+  const size_t tot0 = (size_t)Bn * in0, totg = (size_t)Bn * goal;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot0 + totg;
+       i += (size_t)gridDim.x * blockDim.x) {
+    if (i < tot0) {
+      const int r = (int)(i / in0), c = (int)(i % in0);
+      const float v = c < obs ? s[(size_t)r * obs + c] : a[(size_t)r * act + (c - obs)];
+      x0[(size_t)r * ld0 + c] = __float2bfloat16_rn(v);
+    } else {
+      const size_t j = i - tot0;
+      const int r = (int)(j / goal), c = (int)(j % goal);
+      g0[(size_t)r * ldg + c] = __float2bfloat16_rn(g[j]);
+    }
+  }
+}
+
+cudaError_t launch_prep_inputs(const float* s, const float* a, const float* g, int Bn, int obs, int act,
+                               int goal, __nv_bfloat16* x0, int ld0, __nv_bfloat16* g0, int ldg,
+                               int num_sms, cudaStream_t st) {
+  size_t tot = (size_t)Bn * (obs + act + goal);
+  size_t blocks = (tot + 255) / 256;
+  if (blocks > (size_t)num_sms * 4) blocks = (size_t)num_sms * 4;
+  prep_inputs_kernel<<<(unsigned)blocks, 256, 0, st>>>(s, a, g, Bn, obs, act, goal, x0, ld0, g0, ldg);
+  return cudaGetLastError();
+}
+
+// db[s][n] = sum over the batch slice s of dZ[b][n] (bf16 in, fp32 out), one thread per
+// column, rows split into `splits` slices (deterministic, same slicing as the dW GEMM).
+__global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ dz, int Bn, int N, int ld,
+                                   float* __restrict__ db, int rows_per_split, size_t split_stride) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int sl = blockIdx.y;
+  if (n >= N) return;
+  const int r0 = sl * rows_per_split, r1 = min(Bn, r0 + rows_per_split);
+  float acc = 0.f;
+  for (int r = r0; r < r1; ++r) acc += __bfloat162float(dz[(size_t)r * ld + n]);
+  db[(size_t)sl * split_stride + n] = acc;
+}
+
+cudaError_t launch_colsum_bf16(const __nv_bfloat16* dz, int Bn, int N, int ld, float* db, int splits,
+                               size_t split_stride, cudaStream_t st) {
+  const int rps = ((Bn + splits - 1) / splits + BK - 1) / BK * BK;
+  dim3 grid((N + 127) / 128, splits);
+  colsum_bf16_kernel<<<grid, 128, 0, st>>>(dz, Bn, N, ld, db, rps, split_stride);
+  return cudaGetLastError();
+}
+
+// fp32 -> bf16 copy (dPhi / dPsi from the logits kernels feed the output-layer backward)
+__global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+cudaError_t launch_f32_to_bf16(const float* x, __nv_bfloat16* y, size_t n, int num_sms, cudaStream_t st) {
+  size_t blocks = (n + 255) / 256;
+  if (blocks > (size_t)num_sms * 4) blocks = (size_t)num_sms * 4;
+  f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, y, n);
+  return cudaGetLastError();
+}
+
+}  // namespace tc
+}  // namespace crl

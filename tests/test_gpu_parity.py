@@ -82,7 +82,7 @@ def test_relabel_full_size_ant_sampled_rows():
 
 # ------------------------------------------------------------------------- A2-A6
 
-def _critic_parity(cfg, batch_seed=11, check_adam=True):
+def _critic_parity(cfg, batch_seed=11, check_adam=True, tol_loss=1e-5, tol_grad=1e-4):
     ctx, params = make_ctx(cfg)
     B = cfg["batch"]
     s, a, g = crl_synth.random_batch(cfg, B, seed=batch_seed)
@@ -97,14 +97,14 @@ def _critic_parity(cfg, batch_seed=11, check_adam=True):
                               **oracle_kw(cfg))
     L = loss.cpu().numpy()
     for i, k in enumerate(["L_fwd", "L_bwd", "penalty", "total"]):
-        assert abs(L[i] - ref[k]) <= 1e-5 * max(abs(ref[k]), 1e-3), (k, L[i], ref[k])
-    assert rel(ctx.debug_tensor("phi").cpu().numpy(), ref["phi"]) < 1e-5
-    assert rel(ctx.debug_tensor("lse_row").cpu().numpy(), ref["lse_row"]) < 1e-5
-    assert rel(ctx.debug_tensor("lse_col").cpu().numpy(), ref["lse_col"]) < 1e-5
-    assert rel(ctx.debug_tensor("dphi").cpu().numpy(), ref["dphi"]) < 1e-4
-    assert rel(ctx.debug_tensor("dpsi").cpu().numpy(), ref["dpsi"]) < 1e-4
+        assert abs(L[i] - ref[k]) <= tol_loss * max(abs(ref[k]), 1e-3), (k, L[i], ref[k])
+    assert rel(ctx.debug_tensor("phi").cpu().numpy(), ref["phi"]) < tol_loss
+    assert rel(ctx.debug_tensor("lse_row").cpu().numpy(), ref["lse_row"]) < tol_loss
+    assert rel(ctx.debug_tensor("lse_col").cpu().numpy(), ref["lse_col"]) < tol_loss
+    assert rel(ctx.debug_tensor("dphi").cpu().numpy(), ref["dphi"]) < tol_grad
+    assert rel(ctx.debug_tensor("dpsi").cpu().numpy(), ref["dpsi"]) < tol_grad
     gr = grads.cpu().numpy()
-    assert rel(gr, ref["grads"]) < 1e-4
+    assert rel(gr, ref["grads"]) < tol_grad
     # per-layer tensors as well (a wrong small tensor can hide in the global norm)
     off = 0
     for enc_in in (cfg["obs_dim"] + cfg["act_dim"], cfg["goal_dim"]):
@@ -121,7 +121,8 @@ def _critic_parity(cfg, batch_seed=11, check_adam=True):
         p_ref, *_ = oadam.adam_step(params.astype(np.float64), gr.astype(np.float64), z, z, 0,
                                     lr=cfg["lr"])
         assert rel(dp, p_ref - params) < 1e-5
-        assert rel(dp, ref["params_new"] - params) < 1e-2
+        if tol_grad <= 1e-4:
+            assert rel(dp, ref["params_new"] - params) < 1e-2
     return ctx
 
 
@@ -194,3 +195,36 @@ def test_critic_step_nonfinite_sets_status_and_skips_adam():
     torch.cuda.synchronize()
     assert ctx.status(reset=True) == 5          # CRL_ENONFINITE
     assert np.array_equal(ctx.params.cpu().numpy(), params)
+
+
+# ------------------------------------------------------------------------- BF16 tensor-core path
+BF16_TOL = 2e-2          # north_star: bf16 path within 2e-2 relative of the oracle
+
+
+@pytest.mark.parametrize("energy", ["l2", "dot", "cos"])
+def test_critic_step_bf16_small(energy):
+    cfg = crl_synth.preset("ant", batch=256, width=128, energy=energy, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("B", [2, 130, 300])
+def test_critic_step_bf16_ragged(B):
+    cfg = crl_synth.preset("reacher", batch=B, width=64, depth=3, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+def test_critic_step_bf16_humanoid_config():
+    """configs[2] at full size: Humanoid shapes (obs 268 + act 17 = 285 inputs), 4x256,
+    batch 512, bf16 tensor-core path."""
+    _critic_parity(crl_synth.preset("humanoid"), tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+def test_critic_step_bf16_sweep4096():
+    _critic_parity(crl_synth.preset("sweep4096", precision="bf16"), check_adam=False,
+                   tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+def test_critic_step_bf16_repr256_width1024():
+    """configs[4] network shapes (4x1024, repr 256) at a batch the oracle finishes quickly."""
+    cfg = crl_synth.preset("netscale", batch=512)
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
