@@ -110,7 +110,7 @@ def _critic_parity(cfg, batch_seed=11, check_adam=True, tol_loss=1e-5, tol_grad=
     for enc_in in (cfg["obs_dim"] + cfg["act_dim"], cfg["goal_dim"]):
         for fi, fo in crl_synth.param_shapes(enc_in, cfg["depth"], cfg["width"], cfg["repr_dim"]):
             for n in (fi * fo, fo):
-                assert rel(gr[off:off + n], ref["grads"][off:off + n]) < 1e-4, off
+                assert rel(gr[off:off + n], ref["grads"][off:off + n]) < tol_grad, off
                 off += n
     if check_adam:
         # The first Adam step maps g -> g/(|g|+eps) ~ sign(g): it magnifies tiny gradient
