@@ -54,10 +54,7 @@ def workload_cfg(args):
         over["precision"] = args.precision
     if args.energy:
         over["energy"] = args.energy
-    cfg = crl_synth.preset(args.workload, **over)
-    if cfg["precision"] == "bf16":
-        cfg["precision"] = "fp32"   # tensor-core path not built in this revision -> fp32 (stated in dtype)
-    return cfg
+    return crl_synth.preset(args.workload, **over)
 
 
 def n_fill_chunks(cfg):

@@ -265,6 +265,8 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaMemset(ctx->skip, 0, 4) != cudaSuccess || cudaMemset(ctx->loss_ticket, 0, 4) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->cap_stream3, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess)
@@ -292,6 +294,8 @@ crl_status crl_destroy(crl_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
+  if (ctx->cap_stream3) cudaStreamDestroy(ctx->cap_stream3);
+  if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;

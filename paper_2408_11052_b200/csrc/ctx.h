@@ -93,8 +93,8 @@ struct crl_ctx {
   int *status = nullptr, *adam_t = nullptr, *skip = nullptr;
   float *stage_s = nullptr, *stage_a = nullptr, *stage_g = nullptr;
   // runtime
-  cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr, cap_stream3 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   ncclComm_t comm = nullptr;
   int num_sms = 148;

@@ -16,7 +16,7 @@ namespace crl {
 // last CTA to finish (atomic ticket) adds them in CTA order — deterministic.  acc[0..2] =
 // local sums of (LSE_i - l_ii), (LSE'_i - l_ii), LSE_i^2.  If `finalize`, also writes
 // loss_out[0..3], sets *skip when the loss is non-finite and advances the Adam step counter.
-constexpr int kLossRowsPerCta = 64;
+constexpr int kLossRowsPerCta = 16;    // 2 rows per warp: one DRAM round trip per CTA
 
 __device__ __forceinline__ void loss_finalize_dev(const float* acc, float invN, float c_f,
                                                   float c_b, float beta, float* loss_out,
@@ -26,8 +26,11 @@ __device__ __forceinline__ void loss_finalize_dev(const float* acc, float invN, 
   if (loss_out) { loss_out[0] = Lf; loss_out[1] = Lb; loss_out[2] = P; loss_out[3] = tot; }
   const bool bad = !isfinite(tot);
   *skip = bad ? 1 : 0;
-  if (bad) set_status(status, CRL_ENONFINITE);
-  else *adam_t += 1;
+  if (bad) {
+    set_status(status, CRL_ENONFINITE);
+  } else {
+    *adam_t += 1;
+  }
 }
 
 __global__ void __launch_bounds__(256) loss_partial_kernel(
@@ -107,20 +110,48 @@ __global__ void __launch_bounds__(256) adam_kernel(
   const float inv_bc1 = 1.0f / bc1;
   const float inv_sbc2 = 1.0f / sqrtf(bc2);
   bool bad = false;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
-    float gi = g[i];
-    for (int sl = 1; sl < S; ++sl) gi += g[(size_t)sl * n + i];   // deterministic split-K sum
-    if (S > 1) g[i] = gi;
+  auto upd = [&](float pi, float gi, float& mi, float& vi) -> float {
     bad |= !isfinite(gi);
-    const float mi = b1 * m[i] + (1.f - b1) * gi;
-    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
-    m[i] = mi; v[i] = vi;
-    const float mh = mi * inv_bc1;
+    mi = b1 * mi + (1.f - b1) * gi;
+    vi = b2 * vi + (1.f - b2) * gi * gi;
     const float denom = sqrtf(vi) * inv_sbc2 + eps;       // sqrt(v / bc2) + eps
-    const float pi = p[i];
-    const float pn = pi - lr * (mh / denom + wd * pi);
-    p[i] = pn;
+    return pi - lr * ((mi * inv_bc1) / denom + wd * pi);
+  };
+  const size_t n4 = (n % 4 == 0) ? n / 4 : 0;             // vector path (16-byte accesses)
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float4 gv = reinterpret_cast<const float4*>(g)[i];
+    for (int sl = 1; sl < S; ++sl) {                       // deterministic split-K sum
+      const float4 h = reinterpret_cast<const float4*>(g + (size_t)sl * n)[i];
+      gv.x += h.x; gv.y += h.y; gv.z += h.z; gv.w += h.w;
+    }
+    if (S > 1) reinterpret_cast<float4*>(g)[i] = gv;
+    float4 pv = reinterpret_cast<const float4*>(p)[i];
+    float4 mv = reinterpret_cast<const float4*>(m)[i];
+    float4 vv = reinterpret_cast<const float4*>(v)[i];
+    pv.x = upd(pv.x, gv.x, mv.x, vv.x);
+    pv.y = upd(pv.y, gv.y, mv.y, vv.y);
+    pv.z = upd(pv.z, gv.z, mv.z, vv.z);
+    pv.w = upd(pv.w, gv.w, mv.w, vv.w);
+    reinterpret_cast<float4*>(p)[i] = pv;
+    reinterpret_cast<float4*>(m)[i] = mv;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    if (shadow) {
+      uint2 hv;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(pv.x, pv.y), h1 = __floats2bfloat162_rn(pv.z, pv.w);
+      hv.x = *reinterpret_cast<uint32_t*>(&h0);
+      hv.y = *reinterpret_cast<uint32_t*>(&h1);
+      reinterpret_cast<uint2*>(shadow)[i] = hv;
+    }
+  }
+  for (size_t i = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {                // scalar path (n % 4 != 0)
+    float gi = g[i];
+    for (int sl = 1; sl < S; ++sl) gi += g[(size_t)sl * n + i];
+    if (S > 1) g[i] = gi;
+    float mi = m[i], vi = v[i];
+    const float pn = upd(p[i], gi, mi, vi);
+    m[i] = mi; v[i] = vi; p[i] = pn;
     if (shadow) {
       __nv_bfloat16 h = __float2bfloat16_rn(pn);
       shadow[i] = *reinterpret_cast<__nv_bfloat16_raw*>(&h);
@@ -153,7 +184,7 @@ cudaError_t launch_adam(float* p, float* g, int S, float* m, float* v, size_t n,
                         float b1, float b2, float eps, float wd, const int* adam_t,
                         const int* skip, int* status, void* shadow_bf16, int num_sms,
                         cudaStream_t st) {
-  size_t blocks = (n + 255) / 256;
+  size_t blocks = (n / 4 + 255) / 256 + 1;
   size_t cap = (size_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;

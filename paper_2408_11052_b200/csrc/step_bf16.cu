@@ -102,7 +102,7 @@ static crl_status enc_forward_bf16(crl_ctx* ctx, const char* tag, const EncoderP
 
 static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const EncoderPlan& P,
                                     std::vector<crl_ctx::TcLayer>& T, __nv_bfloat16** Zb, cudaStream_t st,
-                                    int* nl) {
+                                    cudaStream_t side, int* nl) {
   const crl_config& k = ctx->cfg;
   const int Bl = k.batch_local, L = P.n_layers;
   for (int l = L - 1; l >= 0; --l) {
@@ -114,9 +114,14 @@ static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const Encoder
       ++*nl;
     }
     {
-      Stage sg(ctx, st, std::string(tag) + "_bwd_db_l" + std::to_string(l));
+      // db_l = colsum(dZ_l) only feeds Adam: off the critical path on a side stream
+      if (side != st) {
+        cudaEventRecord(ctx->ev_side, st);
+        cudaStreamWaitEvent(side, ctx->ev_side, 0);
+      }
+      Stage sg(ctx, side, std::string(tag) + "_bwd_db_l" + std::to_string(l));
       CU(tc::launch_colsum_bf16(T[l].dz, Bl, Lp.out, Lp.out, ctx->grads + Lp.b_off, ctx->dw_splits,
-                                ctx->sizes.n_params, st));
+                                ctx->sizes.n_params, side));
       ++*nl;
     }
     if (l > 0) {
@@ -199,16 +204,21 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                        c_b, c_f, 0.f, k.beta_lse, invN, ctx->dpsi, st2));
     CU(tc::launch_f32_to_bf16(ctx->dpsi, ctx->dpsib, (size_t)Bl * D, ctx->num_sms, st2));
     nl += 2; }
-  rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, &nl);
+  cudaStream_t side = (st == st2) ? st : ctx->cap_stream3;
+  rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side, &nl);
   if (rs != CRL_OK) return rs;
   { Stage sg(ctx, st, "grad_phi");
     CU(logits_grad_f32(D, k.energy, ctx->phi_out, Bl, row_off, ctx->psi_g, N, ctx->lse_row, ctx->lse_col_g,
                        c_f, c_b, k.beta_lse, 0.f, invN, ctx->dphi, st));
     CU(tc::launch_f32_to_bf16(ctx->dphi, ctx->dphib, (size_t)Bl * D, ctx->num_sms, st));
     nl += 2; }
-  rs = enc_backward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiZb, st, &nl);
+  rs = enc_backward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiZb, st, side, &nl);
   if (rs != CRL_OK) return rs;
   join2(ctx, st, st2);
+  if (side != st) {
+    cudaEventRecord(ctx->ev_side, side);
+    cudaStreamWaitEvent(st, ctx->ev_side, 0);
+  }
   int adam_splits = ctx->dw_splits;
   if (W > 1) {
     if (ctx->dw_splits > 1) {

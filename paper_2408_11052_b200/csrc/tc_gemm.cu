@@ -42,7 +42,7 @@ template <int BN>
 struct TcSmem {
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BN * BK * 2;
-  static constexpr size_t bytes = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+  static constexpr size_t bytes = 1024 + STAGES * (A_BYTES + B_BYTES) + 256 + BN * 4;
 };
 
 __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float (&v)[16], int nvalid) {
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * S::B_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);   // followed by sbias[BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -163,10 +163,31 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
     // ------------------------------------------------------------ epilogue
     const int q = warp - 4;
     const int row = m0 + q * 32 + lane;
+    const bool rv = row < p.M;
+    // operands of the epilogue are fetched while the mainloop runs (one DRAM round trip,
+    // not one per 16-column chunk)
+    float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+    if (EPI == TEPI_FWD_HIDDEN || EPI == TEPI_FWD_OUT) {
+      for (int c = threadIdx.x - 128; c < BN; c += 128) sbias[c] = (n0 + c < p.N) ? p.bias[n0 + c] : 0.f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    uint4 zp[EPI == TEPI_DX ? BN / 8 : 1];
+    if (EPI == TEPI_DX && rv) {
+      const __nv_bfloat16* zrow = p.zprev + (size_t)row * p.ld_bf + n0;
+#pragma unroll
+      for (int j = 0; j < BN / 8; ++j) {
+        if (n0 + 8 * j + 8 <= p.N) {
+          zp[j] = reinterpret_cast<const uint4*>(zrow)[j];
+        } else {
+          __nv_bfloat16 t[8];
+          for (int i = 0; i < 8; ++i) t[i] = (n0 + 8 * j + i < p.N) ? zrow[8 * j + i] : __float2bfloat16_rn(0.f);
+          zp[j] = *reinterpret_cast<uint4*>(t);
+        }
+      }
+    }
     mbar_wait(tfull, 0);
     tc_fence_after();
-    const bool rv = row < p.M;
-#pragma unroll 1
+#pragma unroll
     for (int c0 = 0; c0 < BN; c0 += 16) {
       float v[16];
       tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
@@ -178,11 +199,8 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
       const int nvalid = min(16, p.N - n);
       if (!rv || nvalid <= 0) continue;
       if (EPI == TEPI_FWD_HIDDEN || EPI == TEPI_FWD_OUT) {
-        float bb[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) bb[i] = (i < nvalid) ? p.bias[n + i] : 0.f;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += bb[i];
+        for (int i = 0; i < 16; ++i) v[i] += sbias[c0 + i];
         if (EPI == TEPI_FWD_HIDDEN) {
           store_bf16x16(p.out_z + (size_t)row * p.ld_bf + n, v, nvalid);
 #pragma unroll
@@ -193,10 +211,14 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
           store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
         }
       } else if (EPI == TEPI_DX) {
-        float z[16];
-        load_bf16x16(p.zprev + (size_t)row * p.ld_bf + n, z, nvalid);
+        const uint32_t w[8] = {zp[c0 / 8].x, zp[c0 / 8].y, zp[c0 / 8].z, zp[c0 / 8].w,
+                               zp[c0 / 8 + 1].x, zp[c0 / 8 + 1].y, zp[c0 / 8 + 1].z, zp[c0 / 8 + 1].w};
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] *= act_grad_f(z[i], p.act);
+        for (int i = 0; i < 8; ++i) {
+          const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+          v[2 * i] *= act_grad_f(z.x, p.act);
+          v[2 * i + 1] *= act_grad_f(z.y, p.act);
+        }
         store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
       } else {
         store_f32x16(p.out_f + (size_t)blockIdx.z * p.split_stride + (size_t)row * p.ld_f + n, v, nvalid);
@@ -276,7 +298,6 @@ static cudaError_t dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& 
   switch (bn) {
     case 64: return launch_tc<64, A_MN, B_MN, EPI>(a, b, p, splits, st);
     case 128: return launch_tc<128, A_MN, B_MN, EPI>(a, b, p, splits, st);
-    case 256: return launch_tc<256, A_MN, B_MN, EPI>(a, b, p, splits, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -342,24 +363,56 @@ cudaError_t launch_prep_inputs(const float* s, const float* a, const float* g, i
   return cudaGetLastError();
 }
 
-// db[s][n] = sum over the batch slice s of dZ[b][n] (bf16 in, fp32 out), one thread per
-// column, rows split into `splits` slices (deterministic, same slicing as the dW GEMM).
-__global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ dz, int Bn, int N, int ld,
-                                   float* __restrict__ db, int rows_per_split, size_t split_stride) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+// db[s][n] = sum over the batch slice s of dZ[b][n] (bf16 in, fp32 out): 64 columns x one
+// slice per CTA; thread (tx, ty) sums column pair 2tx of rows ty, ty+8, ... with 8 loads in
+// flight, then the 8 row phases are added in a fixed order (deterministic).  Same slicing as
+// the dW GEMM so Adam can sum the partial slices.
+__global__ void __launch_bounds__(256) colsum_bf16_kernel(const __nv_bfloat16* __restrict__ dz, int Bn, int N,
+                                                          int ld, float* __restrict__ db, int rows_per_split,
+                                                          size_t split_stride) {
+  __shared__ float red[8][65];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int n = blockIdx.x * 64 + 2 * tx;
   const int sl = blockIdx.y;
-  if (n >= N) return;
   const int r0 = sl * rows_per_split, r1 = min(Bn, r0 + rows_per_split);
-  float acc = 0.f;
-  for (int r = r0; r < r1; ++r) acc += __bfloat162float(dz[(size_t)r * ld + n]);
-  db[(size_t)sl * split_stride + n] = acc;
+  float a0 = 0.f, a1 = 0.f;
+  if (n < N) {
+    const bool pair = n + 1 < N;
+    int r = r0 + ty;
+    for (; r + 56 < r1; r += 64) {
+      float2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const __nv_bfloat16* p = dz + (size_t)(r + 8 * u) * ld + n;
+        v[u] = pair ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p))
+                    : make_float2(__bfloat162float(*p), 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { a0 += v[u].x; a1 += v[u].y; }
+    }
+    for (; r < r1; r += 8) {
+      const __nv_bfloat16* p = dz + (size_t)r * ld + n;
+      a0 += __bfloat162float(p[0]);
+      if (pair) a1 += __bfloat162float(p[1]);
+    }
+  }
+  red[ty][2 * tx] = a0;
+  red[ty][2 * tx + 1] = a1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int c = blockIdx.x * 64 + threadIdx.x;
+    float t = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += red[j][threadIdx.x];
+    if (c < N) db[(size_t)sl * split_stride + c] = t;
+  }
 }
 
 cudaError_t launch_colsum_bf16(const __nv_bfloat16* dz, int Bn, int N, int ld, float* db, int splits,
                                size_t split_stride, cudaStream_t st) {
   const int rps = ((Bn + splits - 1) / splits + BK - 1) / BK * BK;
-  dim3 grid((N + 127) / 128, splits);
-  colsum_bf16_kernel<<<grid, 128, 0, st>>>(dz, Bn, N, ld, db, rps, split_stride);
+  dim3 grid((N + 63) / 64, splits);
+  colsum_bf16_kernel<<<grid, 256, 0, st>>>(dz, Bn, N, ld, db, rps, split_stride);
   return cudaGetLastError();
 }
 
