@@ -72,4 +72,30 @@ __device__ __forceinline__ void set_status(int* status, int code) {
 constexpr float kEpsL2 = 1e-12f;   // reading A-06
 constexpr float kEpsCos = 1e-8f;
 
+// ---------------------------------------------------------------------------------------
+// Programmatic dependent launch: every kernel of the step is launched with
+// programmaticStreamSerialization, waits for its predecessor's memory with
+// griddepcontrol.wait before touching predecessor-produced data, and lets its own
+// dependents start their prologue early (griddepcontrol.launch_dependents).  Without the
+// launch attribute both instructions are no-ops.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 }  // namespace crl

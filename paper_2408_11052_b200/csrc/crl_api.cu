@@ -101,10 +101,9 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     c->psi_outb = s.take<__nv_bfloat16>((size_t)Bl * D);
     c->dphib = s.take<__nv_bfloat16>((size_t)Bl * D);
     c->dpsib = s.take<__nv_bfloat16>((size_t)Bl * D);
-    const int wm = Wd > D ? Wd : D;
-    for (int i = 0; i < 2; ++i) {
-      c->dzb_phi[i] = s.take<__nv_bfloat16>((size_t)Bl * wm);
-      c->dzb_psi[i] = s.take<__nv_bfloat16>((size_t)Bl * wm);
+    for (int l = 0; l < k.depth; ++l) {          // dZ_l of hidden layer l: [B][width]
+      c->dzb_phi[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
+      c->dzb_psi[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
     }
   }
   c->phi_out = s.take<float>((size_t)Bl * D);

@@ -117,7 +117,10 @@ struct crl_ctx {
   __nv_bfloat16* psiXb[CRL_MAX_LAYERS] = {}; __nv_bfloat16* psiZb[CRL_MAX_LAYERS] = {};
   __nv_bfloat16 *phi_outb = nullptr, *psi_outb = nullptr;   // Y in bf16 (logits operands)
   __nv_bfloat16 *dphib = nullptr, *dpsib = nullptr;         // dY in bf16
-  __nv_bfloat16 *dzb_phi[2] = {nullptr, nullptr}, *dzb_psi[2] = {nullptr, nullptr};
+  // dZ_l of every hidden layer has its own buffer: db_l is reduced on a side stream, so a
+  // ping-pong buffer would be overwritten while the side stream still reads it
+  __nv_bfloat16* dzb_phi[CRL_MAX_LAYERS] = {};
+  __nv_bfloat16* dzb_psi[CRL_MAX_LAYERS] = {};
   struct TcLayer {
     CUtensorMap fwdA, fwdB, dwA, dwB, dxA, dxB;
     int bn_fwd = 64, bn_dw = 64, bn_dx = 64;

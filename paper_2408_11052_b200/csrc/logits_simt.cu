@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int a0 = blockIdx.x * TR;
   const int ntiles = (p.Nb + TC - 1) / TC;
+  pdl_wait();
+  pdl_launch();
 
   auto issue_b = [&](int buf, int b0) {
     float* dst = Bt + buf * D * BPITCH;
@@ -289,7 +291,7 @@ static cudaError_t launch_logits_t(const LogitsArgs& p, cudaStream_t st) {
     attr_set = true;
   }
   dim3 grid((p.Na + TR - 1) / TR);
-  logits_rows_kernel<D, TR, ENERGY, GRAD><<<grid, 256, smem, st>>>(p);
+  return launch_pdl(logits_rows_kernel<D, TR, ENERGY, GRAD>, grid, dim3(256), smem, st, p);
   return cudaGetLastError();
 }
 

@@ -80,6 +80,8 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(GemmArgs p) {
   const int kbeg = split * p.k_per_split;
   const int kend = min(p.K, kbeg + p.k_per_split);
   const bool do_colsum = (EPI == EPI_STORE_COLSUM) && blockIdx.y == 0;
+  pdl_wait();
+  pdl_launch();
 
   float acc[TM][TN];
 #pragma unroll
@@ -204,10 +206,10 @@ static cudaError_t launch_gemm(GemmArgs p, int splits, cudaStream_t st) {
   const long big = (long)((p.N + 63) / 64) * ((p.M + 63) / 64) * splits;
   if (big >= g_num_sms) {
     dim3 grid((p.N + 63) / 64, (p.M + 63) / 64, splits);
-    gemm_f32_kernel<A_T, B_T, EPI, 64, 64><<<grid, 256, 0, st>>>(p);
+    return launch_pdl(gemm_f32_kernel<A_T, B_T, EPI, 64, 64>, grid, dim3(256), 0, st, p);
   } else {
     dim3 grid((p.N + 31) / 32, (p.M + 31) / 32, splits);
-    gemm_f32_kernel<A_T, B_T, EPI, 32, 32><<<grid, 256, 0, st>>>(p);
+    return launch_pdl(gemm_f32_kernel<A_T, B_T, EPI, 32, 32>, grid, dim3(256), 0, st, p);
   }
   return cudaGetLastError();
 }
@@ -256,6 +258,8 @@ int dw_splits_for(int Bn) {
 
 // g[i] = sum_s part[s][i]  (in place into slice 0)
 __global__ void reduce_partials_kernel(float* part, size_t n, int S) {
+  pdl_wait();
+  pdl_launch();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     float v = part[i];
@@ -267,8 +271,7 @@ __global__ void reduce_partials_kernel(float* part, size_t n, int S) {
 cudaError_t launch_reduce_partials(float* part, size_t n, int S, cudaStream_t st) {
   size_t blocks = (n + 255) / 256;
   if (blocks > (size_t)g_num_sms * 8) blocks = (size_t)g_num_sms * 8;
-  reduce_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, n, S);
-  return cudaGetLastError();
+  return launch_pdl(reduce_partials_kernel, dim3((unsigned)blocks), dim3(256), 0, st, part, n, S);
 }
 
 }  // namespace crl

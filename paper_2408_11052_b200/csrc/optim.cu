@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(256) loss_partial_kernel(
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float s1 = 0.f, s2 = 0.f, s3 = 0.f;
   const int r0 = blockIdx.x * kLossRowsPerCta;
+  pdl_wait();
+  pdl_launch();
   for (int q = w; q < kLossRowsPerCta; q += 8) {
     const int i = r0 + q;
     if (i >= Bl) break;
@@ -93,6 +95,8 @@ __global__ void loss_finalize_kernel(const float* __restrict__ acc, float invN, 
                                      float c_b, float beta, float* __restrict__ loss_out,
                                      int* __restrict__ skip, int* __restrict__ adam_t,
                                      int* __restrict__ status) {
+  pdl_wait();
+  pdl_launch();
   loss_finalize_dev(acc, invN, c_f, c_b, beta, loss_out, skip, adam_t, status);
 }
 
@@ -103,6 +107,8 @@ __global__ void __launch_bounds__(256) adam_kernel(
     float* __restrict__ v, size_t n, float lr, float b1, float b2, float eps, float wd,
     const int* __restrict__ adam_t, const int* __restrict__ skip, int* __restrict__ status,
     __nv_bfloat16_raw* __restrict__ shadow) {
+  pdl_wait();
+  pdl_launch();
   if (*skip) return;
   const int t = *adam_t;
   const float bc1 = (float)(1.0 - pow((double)b1, (double)t));
@@ -167,17 +173,16 @@ cudaError_t launch_loss_partial(const float* phi, const float* psi, int Bl, int 
                                 float* part, unsigned* ticket, int finalize, float invN, float c_f,
                                 float c_b, float beta, float* loss_out, int* skip, int* adam_t,
                                 int* status, cudaStream_t st) {
-  loss_partial_kernel<<<loss_partial_blocks(Bl), 256, 0, st>>>(
-      phi, psi, Bl, D, energy, lse_row, lse_col, acc, part, ticket, finalize, invN, c_f, c_b, beta,
-      loss_out, skip, adam_t, status);
-  return cudaGetLastError();
+  return launch_pdl(loss_partial_kernel, dim3(loss_partial_blocks(Bl)), dim3(256), 0, st, phi, psi, Bl, D,
+                    energy, lse_row, lse_col, acc, part, ticket, finalize, invN, c_f, c_b, beta, loss_out,
+                    skip, adam_t, status);
 }
 
 cudaError_t launch_loss_finalize(const float* acc, float invN, float c_f, float c_b, float beta,
                                  float* loss_out, int* skip, int* adam_t, int* status,
                                  cudaStream_t st) {
-  loss_finalize_kernel<<<1, 1, 0, st>>>(acc, invN, c_f, c_b, beta, loss_out, skip, adam_t, status);
-  return cudaGetLastError();
+  return launch_pdl(loss_finalize_kernel, dim3(1), dim3(1), 0, st, acc, invN, c_f, c_b, beta, loss_out,
+                    skip, adam_t, status);
 }
 
 cudaError_t launch_adam(float* p, float* g, int S, float* m, float* v, size_t n, float lr,
@@ -188,10 +193,8 @@ cudaError_t launch_adam(float* p, float* g, int S, float* m, float* v, size_t n,
   size_t cap = (size_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
-  adam_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, g, S, m, v, n, lr, b1, b2, eps, wd, adam_t, skip,
-                                                status,
-                                                reinterpret_cast<__nv_bfloat16_raw*>(shadow_bf16));
-  return cudaGetLastError();
+  return launch_pdl(adam_kernel, dim3((unsigned)blocks), dim3(256), 0, st, p, g, S, m, v, n, lr, b1, b2, eps,
+                    wd, adam_t, skip, status, reinterpret_cast<__nv_bfloat16_raw*>(shadow_bf16));
 }
 
 }  // namespace crl

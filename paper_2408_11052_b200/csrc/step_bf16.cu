@@ -50,8 +50,8 @@ static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const _
     const __nv_bfloat16* X = (l == 0) ? x0 : Xb[l];
     const int ldx = (l == 0) ? ld0 : Wd;
     const __nv_bfloat16* W = ctx->wshadow + P.layer[l].w_off;
-    T.dz = (l == L - 1) ? dY : dzb[(L - 2 - l) % 2];
-    T.dzprev = (l > 0) ? dzb[(L - 1 - l) % 2] : nullptr;
+    T.dz = (l == L - 1) ? dY : dzb[l];
+    T.dzprev = (l > 0) ? dzb[l - 1] : nullptr;
     T.bn_fwd = tc::tc_pick_bn(Bl, o, ctx->num_sms);
     T.bn_dw = tc::tc_pick_bn(in, o, ctx->num_sms);
     T.bn_dx = tc::tc_pick_bn(Bl, in, ctx->num_sms);

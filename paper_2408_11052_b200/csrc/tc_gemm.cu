@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // prologue above (barriers, TMEM, descriptor prefetch) overlaps the predecessor's tail
+  pdl_wait();
+  pdl_launch();
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -278,8 +281,7 @@ static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const T
     attr = true;
   }
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, splits);
-  tc_gemm_kernel<BN, A_MN, B_MN, EPI><<<grid, 256, smem, st>>>(a, b, p);
-  return cudaGetLastError();
+  return launch_pdl(tc_gemm_kernel<BN, A_MN, B_MN, EPI>, grid, dim3(256), smem, st, a, b, p);
 }
 
 // Operand maps for one GEMM: boxes follow the kernel's TMA calls.
@@ -339,6 +341,8 @@ __global__ void prep_inputs_kernel(const float* __restrict__ s, const float* __r
                                    int ldg) {
   const int in0 = obs + act;
   const size_t tot0 = (size_t)Bn * in0, totg = (size_t)Bn * goal;
+  pdl_wait();
+  pdl_launch();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot0 + totg;
        i += (size_t)gridDim.x * blockDim.x) {
     if (i < tot0) {
@@ -359,8 +363,8 @@ cudaError_t launch_prep_inputs(const float* s, const float* a, const float* g, i
   size_t tot = (size_t)Bn * (obs + act + goal);
   size_t blocks = (tot + 255) / 256;
   if (blocks > (size_t)num_sms * 4) blocks = (size_t)num_sms * 4;
-  prep_inputs_kernel<<<(unsigned)blocks, 256, 0, st>>>(s, a, g, Bn, obs, act, goal, x0, ld0, g0, ldg);
-  return cudaGetLastError();
+  return launch_pdl(prep_inputs_kernel, dim3((unsigned)blocks), dim3(256), 0, st, s, a, g, Bn, obs, act, goal,
+                    x0, ld0, g0, ldg);
 }
 
 // db[s][n] = sum over the batch slice s of dZ[b][n] (bf16 in, fp32 out): 64 columns x one
@@ -376,6 +380,8 @@ __global__ void __launch_bounds__(256) colsum_bf16_kernel(const __nv_bfloat16* _
   const int sl = blockIdx.y;
   const int r0 = sl * rows_per_split, r1 = min(Bn, r0 + rows_per_split);
   float a0 = 0.f, a1 = 0.f;
+  pdl_wait();
+  pdl_launch();
   if (n < N) {
     const bool pair = n + 1 < N;
     int r = r0 + ty;
@@ -412,20 +418,20 @@ cudaError_t launch_colsum_bf16(const __nv_bfloat16* dz, int Bn, int N, int ld, f
                                size_t split_stride, cudaStream_t st) {
   const int rps = ((Bn + splits - 1) / splits + BK - 1) / BK * BK;
   dim3 grid((N + 63) / 64, splits);
-  colsum_bf16_kernel<<<grid, 256, 0, st>>>(dz, Bn, N, ld, db, rps, split_stride);
-  return cudaGetLastError();
+  return launch_pdl(colsum_bf16_kernel, grid, dim3(256), 0, st, dz, Bn, N, ld, db, rps, split_stride);
 }
 
 // fp32 -> bf16 copy (dPhi / dPsi from the logits kernels feed the output-layer backward)
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, size_t n) {
+  pdl_wait();
+  pdl_launch();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16_rn(x[i]);
 }
 cudaError_t launch_f32_to_bf16(const float* x, __nv_bfloat16* y, size_t n, int num_sms, cudaStream_t st) {
   size_t blocks = (n + 255) / 256;
   if (blocks > (size_t)num_sms * 4) blocks = (size_t)num_sms * 4;
-  f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, y, n);
-  return cudaGetLastError();
+  return launch_pdl(f32_to_bf16_kernel, dim3((unsigned)blocks), dim3(256), 0, st, x, y, n);
 }
 
 }  // namespace tc
