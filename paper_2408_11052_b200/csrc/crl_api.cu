@@ -105,6 +105,24 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       c->dzb_phi[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
       c->dzb_psi[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
     }
+    c->tc_logits = N >= kTcLogitsMinN && tc_logits_supports(D);
+    if (c->tc_logits) {
+      c->lg_splits = tc_logits_splits(Bl, N, D, 148);
+      if (W > 1) {
+        c->phi_outb_g = s.take<__nv_bfloat16>((size_t)N * D);
+        c->psi_outb_g = s.take<__nv_bfloat16>((size_t)N * D);
+      } else {
+        c->phi_outb_g = c->phi_outb;
+        c->psi_outb_g = c->psi_outb;
+      }
+      c->stat_phi = s.take<float>((size_t)N + kStatPad);
+      c->stat_psi = s.take<float>((size_t)N + kStatPad);
+      // two sets (row call on phi, column call on psi run concurrently)
+      c->lg_part_m = s.take<float>((size_t)2 * c->lg_splits * Bl);
+      c->lg_part_s = s.take<float>((size_t)2 * c->lg_splits * Bl);
+      c->lg_part_rs = s.take<float>((size_t)2 * c->lg_splits * Bl);
+      c->lg_part_da = s.take<float>((size_t)2 * c->lg_splits * Bl * D);
+    }
   }
   c->phi_out = s.take<float>((size_t)Bl * D);
   c->psi_out = s.take<float>((size_t)Bl * D);
@@ -115,11 +133,12 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     c->phi_g = c->phi_out;
     c->psi_g = c->psi_out;
   }
-  c->lse_row = s.take<float>(Bl);
-  c->lse_col = s.take<float>(Bl);
+  // padded: the tensor-core logits read column statistics with 1-D bulk copies of whole tiles
+  c->lse_row = s.take<float>((size_t)Bl + kStatPad);
+  c->lse_col = s.take<float>((size_t)Bl + kStatPad);
   if (W > 1) {
-    c->lse_row_g = s.take<float>(N);
-    c->lse_col_g = s.take<float>(N);
+    c->lse_row_g = s.take<float>((size_t)N + kStatPad);
+    c->lse_col_g = s.take<float>((size_t)N + kStatPad);
   } else {
     c->lse_row_g = c->lse_row;
     c->lse_col_g = c->lse_col;
@@ -265,6 +284,7 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream3, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->cap_stream4, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
@@ -294,6 +314,7 @@ crl_status crl_destroy(crl_ctx* ctx) {
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
   if (ctx->cap_stream3) cudaStreamDestroy(ctx->cap_stream3);
+  if (ctx->cap_stream4) cudaStreamDestroy(ctx->cap_stream4);
   if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);

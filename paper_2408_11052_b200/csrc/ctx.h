@@ -41,6 +41,12 @@ cudaError_t launch_loss_finalize(const float*, float, float, float, float, float
                                  int*, cudaStream_t);
 cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, float, float, float,
                         float, const int*, const int*, int*, void*, int, cudaStream_t);
+namespace tc {
+bool tc_logits_supports(int D);
+int tc_logits_splits(int Na, int Nb, int D, int num_sms);
+}  // namespace tc
+using tc::tc_logits_supports;
+using tc::tc_logits_splits;
 }  // namespace crl
 
 using namespace crl;
@@ -93,7 +99,7 @@ struct crl_ctx {
   int *status = nullptr, *adam_t = nullptr, *skip = nullptr;
   float *stage_s = nullptr, *stage_a = nullptr, *stage_g = nullptr;
   // runtime
-  cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr, cap_stream3 = nullptr;
+  cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr, cap_stream3 = nullptr, cap_stream4 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   ncclComm_t comm = nullptr;
@@ -128,7 +134,17 @@ struct crl_ctx {
     __nv_bfloat16* dzprev = nullptr;     // dZ_{l-1} written by this layer's dX GEMM
   };
   std::vector<TcLayer> tc_phi, tc_psi;
+  // tensor-core logits stage (bf16 path with N >= kTcLogitsMinN)
+  bool tc_logits = false;
+  int lg_splits = 1;
+  __nv_bfloat16 *phi_outb_g = nullptr, *psi_outb_g = nullptr;   // global (gathered) bf16 reps
+  float *stat_phi = nullptr, *stat_psi = nullptr;               // [N + pad] |x|^2 or 1/|x|
+  float *lg_part_m = nullptr, *lg_part_s = nullptr, *lg_part_da = nullptr, *lg_part_rs = nullptr;
+  CUtensorMap lg_row_A, lg_row_B, lg_col_A, lg_col_B;
 };
+
+constexpr int kTcLogitsMinN = 1024;      // below this the SIMT logits kernels have more CTAs
+constexpr int kStatPad = 256;            // padding of per-column arrays read by 1-D bulk copies
 
 // Brackets one launch with CUDA events when the context is in profiling mode (events come
 // from a pool so the host enqueue stays cheap; see also spin_kernel below).

@@ -34,6 +34,13 @@ cudaError_t launch_prep_inputs(const float*, const float*, const float*, int, in
                                __nv_bfloat16*, int, __nv_bfloat16*, int, int, cudaStream_t);
 cudaError_t launch_colsum_bf16(const __nv_bfloat16*, int, int, int, float*, int, size_t, cudaStream_t);
 cudaError_t launch_f32_to_bf16(const float*, __nv_bfloat16*, size_t, int, cudaStream_t);
+bool tc_logits_maps(CUtensorMap*, CUtensorMap*, const __nv_bfloat16*, int, const __nv_bfloat16*, int, int);
+cudaError_t tc_logits_lse(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*,
+                          int, float*, float*, float*, cudaStream_t);
+cudaError_t tc_logits_grad(int, int, const CUtensorMap&, const CUtensorMap&, int, int, int, const float*,
+                           const float*, const float*, const float*, float, float, float, float, float, int,
+                           float*, float*, const __nv_bfloat16*, float*, __nv_bfloat16*, cudaStream_t);
+cudaError_t launch_rowstat_bf16(const __nv_bfloat16*, int, int, int, float*, cudaStream_t);
 }  // namespace tc
 }  // namespace crl
 
@@ -75,6 +82,15 @@ crl_status bf16_prepare(crl_ctx* ctx) {
   st = build_encoder_plan(ctx, ctx->psi_plan, ctx->x0_psi, ctx->ld0_psi, ctx->psiXb, ctx->psiZb, ctx->dpsib,
                           ctx->dzb_psi, ctx->tc_psi);
   if (st != CRL_OK) return st;
+  if (ctx->tc_logits) {
+    ctx->lg_splits = std::min(ctx->lg_splits, tc::tc_logits_splits(k.batch_local, ctx->N, k.repr_dim,
+                                                                   ctx->num_sms));
+    if (!tc::tc_logits_maps(&ctx->lg_row_A, &ctx->lg_row_B, ctx->phi_outb, k.batch_local, ctx->psi_outb_g,
+                            ctx->N, k.repr_dim) ||
+        !tc::tc_logits_maps(&ctx->lg_col_A, &ctx->lg_col_B, ctx->psi_outb, k.batch_local, ctx->phi_outb_g,
+                            ctx->N, k.repr_dim))
+      return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the logits operands");
+  }
   // initial bf16 shadow of the caller's parameters; zero the padded input rows
   CU(tc::launch_f32_to_bf16(ctx->mem.params, ctx->wshadow, ctx->sizes.n_params, ctx->num_sms, 0));
   CU(cudaMemset(ctx->x0_phi, 0, (size_t)k.batch_local * ctx->ld0_phi * 2));
@@ -107,18 +123,18 @@ static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const Encoder
   const int Bl = k.batch_local, L = P.n_layers;
   for (int l = L - 1; l >= 0; --l) {
     const LayerPlan& Lp = P.layer[l];
+    // dW_l and db_l only feed Adam: they run on a side stream, off the dX critical path
+    if (side != st) {
+      cudaEventRecord(ctx->ev_side, st);
+      cudaStreamWaitEvent(side, ctx->ev_side, 0);
+    }
     {
-      Stage sg(ctx, st, std::string(tag) + "_bwd_dw_l" + std::to_string(l));
+      Stage sg(ctx, side, std::string(tag) + "_bwd_dw_l" + std::to_string(l));
       CU(tc::tc_backward_dw(T[l].bn_dw, T[l].dwA, T[l].dwB, Bl, Lp.in, Lp.out, ctx->grads + Lp.w_off,
-                            ctx->dw_splits, ctx->sizes.n_params, st));
+                            ctx->dw_splits, ctx->sizes.n_params, side));
       ++*nl;
     }
     {
-      // db_l = colsum(dZ_l) only feeds Adam: off the critical path on a side stream
-      if (side != st) {
-        cudaEventRecord(ctx->ev_side, st);
-        cudaStreamWaitEvent(side, ctx->ev_side, 0);
-      }
       Stage sg(ctx, side, std::string(tag) + "_bwd_db_l" + std::to_string(l));
       CU(tc::launch_colsum_bf16(T[l].dz, Bl, Lp.out, Lp.out, ctx->grads + Lp.b_off, ctx->dw_splits,
                                 ctx->sizes.n_params, side));
@@ -168,18 +184,47 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                         ctx->phi_outb, st, &nl);
   if (rs != CRL_OK) return rs;
   join2(ctx, st, st2);
-  if (W > 1) {
-    NC(ncclGroupStart());
-    NC(ncclAllGather(ctx->phi_out, ctx->phi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
-    NC(ncclAllGather(ctx->psi_out, ctx->psi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
-    NC(ncclGroupEnd());
+  const int row_off = k.rank * Bl;
+  const int S = ctx->lg_splits;
+  if (ctx->tc_logits) {
+    // per-row |x|^2 (L2) / 1/|x| (cos) of the bf16-rounded representations
+    { Stage sg(ctx, st, "rowstat");
+      CU(tc::launch_rowstat_bf16(ctx->phi_outb, Bl, D, k.energy, ctx->stat_phi + row_off, st));
+      CU(tc::launch_rowstat_bf16(ctx->psi_outb, Bl, D, k.energy, ctx->stat_psi + row_off, st));
+      nl += 2; }
+    if (W > 1) {   // global negatives: gather the bf16 representations and their statistics
+      NC(ncclGroupStart());
+      NC(ncclAllGather(ctx->phi_outb, ctx->phi_outb_g, (size_t)Bl * D, ncclBfloat16, ctx->comm, st));
+      NC(ncclAllGather(ctx->psi_outb, ctx->psi_outb_g, (size_t)Bl * D, ncclBfloat16, ctx->comm, st));
+      NC(ncclAllGather(ctx->stat_phi + row_off, ctx->stat_phi, (size_t)Bl, ncclFloat32, ctx->comm, st));
+      NC(ncclAllGather(ctx->stat_psi + row_off, ctx->stat_psi, (size_t)Bl, ncclFloat32, ctx->comm, st));
+      NC(ncclGroupEnd());
+    }
+    fork2(ctx, st, st2);
+    { Stage sg(ctx, st2, "lse_col");
+      CU(tc::tc_logits_lse(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, ctx->stat_psi + row_off,
+                           ctx->stat_phi, S, ctx->lg_part_m + (size_t)S * Bl, ctx->lg_part_s + (size_t)S * Bl,
+                           ctx->lse_col, st2));
+      nl += 2; }
+    { Stage sg(ctx, st, "lse_row");
+      CU(tc::tc_logits_lse(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off,
+                           ctx->stat_psi, S, ctx->lg_part_m, ctx->lg_part_s, ctx->lse_row, st));
+      nl += 2; }
+    join2(ctx, st, st2);
+  } else {
+    if (W > 1) {
+      NC(ncclGroupStart());
+      NC(ncclAllGather(ctx->phi_out, ctx->phi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
+      NC(ncclAllGather(ctx->psi_out, ctx->psi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
+      NC(ncclGroupEnd());
+    }
+    fork2(ctx, st, st2);
+    { Stage sg(ctx, st2, "lse_col");
+      CU(logits_lse_f32(D, k.energy, ctx->psi_out, Bl, ctx->phi_g, N, ctx->lse_col, st2)); ++nl; }
+    { Stage sg(ctx, st, "lse_row");
+      CU(logits_lse_f32(D, k.energy, ctx->phi_out, Bl, ctx->psi_g, N, ctx->lse_row, st)); ++nl; }
+    join2(ctx, st, st2);
   }
-  fork2(ctx, st, st2);
-  { Stage sg(ctx, st2, "lse_col");
-    CU(logits_lse_f32(D, k.energy, ctx->psi_out, Bl, ctx->phi_g, N, ctx->lse_col, st2)); ++nl; }
-  { Stage sg(ctx, st, "lse_row");
-    CU(logits_lse_f32(D, k.energy, ctx->phi_out, Bl, ctx->psi_g, N, ctx->lse_row, st)); ++nl; }
-  join2(ctx, st, st2);
   if (W > 1) {
     NC(ncclGroupStart());
     NC(ncclAllGather(ctx->lse_row, ctx->lse_row_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
@@ -197,26 +242,41 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                             ctx->status, st));
     ++nl;
   }
-  const int row_off = k.rank * Bl;
   fork2(ctx, st, st2);
   { Stage sg(ctx, st2, "grad_psi");
-    CU(logits_grad_f32(D, k.energy, ctx->psi_out, Bl, row_off, ctx->phi_g, N, ctx->lse_col, ctx->lse_row_g,
-                       c_b, c_f, 0.f, k.beta_lse, invN, ctx->dpsi, st2));
-    CU(tc::launch_f32_to_bf16(ctx->dpsi, ctx->dpsib, (size_t)Bl * D, ctx->num_sms, st2));
+    if (ctx->tc_logits) {
+      CU(tc::tc_logits_grad(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, row_off, ctx->stat_psi + row_off,
+                            ctx->stat_phi, ctx->lse_col, ctx->lse_row_g, c_b, c_f, 0.f, k.beta_lse, invN, S,
+                            ctx->lg_part_da + (size_t)S * Bl * D, ctx->lg_part_rs + (size_t)S * Bl,
+                            ctx->psi_outb, ctx->dpsi, ctx->dpsib, st2));
+    } else {
+      CU(logits_grad_f32(D, k.energy, ctx->psi_out, Bl, row_off, ctx->phi_g, N, ctx->lse_col, ctx->lse_row_g,
+                         c_b, c_f, 0.f, k.beta_lse, invN, ctx->dpsi, st2));
+      CU(tc::launch_f32_to_bf16(ctx->dpsi, ctx->dpsib, (size_t)Bl * D, ctx->num_sms, st2));
+    }
     nl += 2; }
-  cudaStream_t side = (st == st2) ? st : ctx->cap_stream3;
-  rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side, &nl);
+  cudaStream_t side = (st == st2) ? st : ctx->cap_stream3;      // phi weight gradients
+  cudaStream_t side2 = (st == st2) ? st : ctx->cap_stream4;     // psi weight gradients
+  rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side2, &nl);
   if (rs != CRL_OK) return rs;
   { Stage sg(ctx, st, "grad_phi");
-    CU(logits_grad_f32(D, k.energy, ctx->phi_out, Bl, row_off, ctx->psi_g, N, ctx->lse_row, ctx->lse_col_g,
-                       c_f, c_b, k.beta_lse, 0.f, invN, ctx->dphi, st));
-    CU(tc::launch_f32_to_bf16(ctx->dphi, ctx->dphib, (size_t)Bl * D, ctx->num_sms, st));
+    if (ctx->tc_logits) {
+      CU(tc::tc_logits_grad(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, row_off, ctx->stat_phi + row_off,
+                            ctx->stat_psi, ctx->lse_row, ctx->lse_col_g, c_f, c_b, k.beta_lse, 0.f, invN, S,
+                            ctx->lg_part_da, ctx->lg_part_rs, ctx->phi_outb, ctx->dphi, ctx->dphib, st));
+    } else {
+      CU(logits_grad_f32(D, k.energy, ctx->phi_out, Bl, row_off, ctx->psi_g, N, ctx->lse_row, ctx->lse_col_g,
+                         c_f, c_b, k.beta_lse, 0.f, invN, ctx->dphi, st));
+      CU(tc::launch_f32_to_bf16(ctx->dphi, ctx->dphib, (size_t)Bl * D, ctx->num_sms, st));
+    }
     nl += 2; }
   rs = enc_backward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiZb, st, side, &nl);
   if (rs != CRL_OK) return rs;
   join2(ctx, st, st2);
   if (side != st) {
     cudaEventRecord(ctx->ev_side, side);
+    cudaStreamWaitEvent(st, ctx->ev_side, 0);
+    cudaEventRecord(ctx->ev_side, side2);
     cudaStreamWaitEvent(st, ctx->ev_side, 0);
   }
   int adam_splits = ctx->dw_splits;

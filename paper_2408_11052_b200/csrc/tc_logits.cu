@@ -1,0 +1,501 @@
+// tc_logits.cu — bf16 tensor-core logits stage (A3 + A4) for the BF16 path.
+//
+// Paper: energies App. A.2 P:607-617 (L2 = -||phi-psi|| with the sign of P:614, reading A-01;
+// dot P:610; cos P:608); InfoNCE fwd/bwd/sym P:619-630; logsumexp penalty P:361, Alg. 1
+// P:1052.  Readings A-02..A-06.
+//
+// Row-owner orientation (A rows, B columns), l_ij = f(A_i, B_j); called with (Phi, Psi) and
+// with (Psi, Phi) exactly like the SIMT kernels (logits_simt.cu).  One CTA = 128 rows of A
+// x one column split of B.  The N x N logits never leave the SM:
+//   S = A . B^T              tcgen05.mma (M=128, N=BNT, K=D), S double-buffered in TMEM
+//   epilogue (row per thread, 2 warpgroups split the columns of a tile):
+//     LSE : l = f(S), online max / sum of exp2 -> per-split partial (m, s) per row
+//     GRAD: g = dL/dl (closed form, A-02..A-05) -> w (energy chain) -> bf16 W tile in SMEM
+//   dA += W . B               tcgen05.mma (M=128, N=D, K=BNT): the SMEM B tile that fed S is
+//                             re-used as an MN-major operand (same bytes, other descriptor)
+// Per-split partials are merged by lse_merge / grad_merge (grad_merge also applies the L2
+// "- (sum_j w_ij) A_i" term and the cosine projection, and emits fp32 + bf16 dA).
+//
+// L2 uses |a|^2 + |b|^2 - 2 a.b on the bf16-rounded vectors (norms of the same rounded
+// vectors, clamped at 0): the tolerance of this path is 2e-2 (north_star).
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace crl {
+namespace tc {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsq(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+struct TcLogitsArgs {
+  int Na, Nb, row_offset;
+  int cols_per_split;              // multiple of BNT
+  const float* a_stat;             // [Na]  L2: |a|^2, cos: 1/max(|a|,eps) (bf16-rounded vectors)
+  const float* b_stat;             // [Nb padded]  same for B
+  const float* lr;                 // GRAD: row statistic (natural log) [Na]
+  const float* lc;                 // GRAD: column statistic [Nb padded]
+  float c_r, c_c, beta_r, beta_c, invN;
+  float* part_m;                   // LSE: [S][Na] running max (log2 units)
+  float* part_s;                   // LSE: [S][Na] running sum
+  float* part_da;                  // GRAD: [S][Na][D]
+  float* part_rs;                  // GRAD: [S][Na] row sums of w (L2)
+};
+
+template <int D>
+struct LgCfg {
+  static constexpr int BNT = D <= 128 ? 128 : 64;         // columns per tile
+  static constexpr int STAGES = D <= 128 ? 3 : 2;
+  static constexpr int KC = D / 64;                       // 64-wide K chunks of A / B
+  static constexpr uint32_t A_BYTES = 128 * D * 2;
+  static constexpr uint32_t B_BYTES = BNT * D * 2;
+  static constexpr uint32_t W_BYTES = 128 * BNT * 2;
+  static constexpr uint32_t STAT_BYTES = BNT * 4;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr size_t smem(bool grad) {
+    return 1024 + A_BYTES + STAGES * B_BYTES + (grad ? 2 * W_BYTES : 0) + STAGES * 2 * STAT_BYTES +
+           2 * 128 * 4 * 3 + 512;
+  }
+};
+
+// byte offset of element (row r, k) inside a K-major SW128 tile chunk (rows at 128 B pitch)
+__device__ __forceinline__ uint32_t sw128_off(int r, int k) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2);
+}
+
+template <int D, int ENERGY, bool GRAD>
+__global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                           const __grid_constant__ CUtensorMap tmB,
+                                                           TcLogitsArgs p) {
+  using C = LgCfg<D>;
+  constexpr int BNT = C::BNT, STAGES = C::STAGES, KC = C::KC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::A_BYTES;
+  uint8_t* sW = sB + STAGES * C::B_BYTES;
+  float* sStat = reinterpret_cast<float*>(sW + (GRAD ? 2 * C::W_BYTES : 0));   // [STAGES][2][BNT]
+  float* sMerge = sStat + STAGES * 2 * BNT;                                     // [3][128] wg-1 partials
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + 3 * 128);
+  uint64_t* a_full = bars;
+  uint64_t* b_full = bars + 1;
+  uint64_t* b_empty = b_full + STAGES;
+  uint64_t* s_full = b_empty + STAGES;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* w_full = s_empty + 2;
+  uint64_t* w_empty = w_full + 2;
+  uint64_t* da_full = w_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a0 = blockIdx.x * 128;
+  const int split = blockIdx.y;
+  const int jbeg = split * p.cols_per_split;
+  const int jend = min(p.Nb, jbeg + p.cols_per_split);
+  const int ntiles = jend > jbeg ? (jend - jbeg + BNT - 1) / BNT : 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    mbar_init(a_full, 1);
+    // LSE mode: a B stage (and its column statistics) is free once S(t) is computed AND the
+    // 8 epilogue warps are done with the statistics; GRAD mode: once dA(t) is computed
+    // (which itself waits for the epilogue's W tile).
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], GRAD ? 1 : 9); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
+      mbar_init(&w_full[i], 8); mbar_init(&w_empty[i], 1);
+    }
+    mbar_init(da_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tm_s[2] = {tmem, tmem + BNT};
+  const uint32_t tm_da = tmem + 2 * BNT;
+  pdl_wait();
+  pdl_launch();
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    mbar_expect_tx(a_full, C::A_BYTES);
+#pragma unroll
+    for (int c = 0; c < KC; ++c) tma_load_2d(sA + c * 128 * 128, &tmA, a_full, 64 * c, a0);
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t % STAGES;
+      mbar_wait(&b_empty[s], ((t / STAGES) & 1) ^ 1);
+      const int j0 = jbeg + t * BNT;
+      mbar_expect_tx(&b_full[s], C::B_BYTES + (GRAD ? 2 : 1) * C::STAT_BYTES);
+      uint8_t* dst = sB + s * C::B_BYTES;
+#pragma unroll
+      for (int c = 0; c < KC; ++c) tma_load_2d(dst + c * BNT * 128, &tmB, &b_full[s], 64 * c, j0);
+      float* st = sStat + s * 2 * BNT;
+      bulk_g2s(st, p.b_stat + j0, C::STAT_BYTES, &b_full[s]);
+      if (GRAD) bulk_g2s(st + BNT, p.lc + j0, C::STAT_BYTES, &b_full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------------ MMA issuer
+    const uint32_t id_s = idesc_bf16_f32(128, BNT, false, false);
+    const uint32_t id_da = idesc_bf16_f32(128, D, false, true);
+    mbar_wait(a_full, 0);
+    const uint32_t a_base = smem_u32(sA);
+    auto issue_s = [&](int t) {
+      const int s = t % STAGES, b = t & 1;
+      mbar_wait(&b_full[s], (t / STAGES) & 1);
+      mbar_wait(&s_empty[b], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+      for (int c = 0; c < KC; ++c)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma_bf16(tm_s[b], smem_desc_sw128(a_base + c * 16384 + ks * 32, 16, 1024),
+                   smem_desc_sw128(b_base + c * BNT * 128 + ks * 32, 16, 1024), id_s, (c | ks) != 0);
+      mma_commit(&s_full[b]);
+      if (!GRAD) mma_commit(&b_empty[s]);
+    };
+    auto issue_da = [&](int t) {
+      const int s = t % STAGES, b = t & 1;
+      mbar_wait(&w_full[b], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
+      const uint32_t w_base = smem_u32(sW + b * C::W_BYTES);
+#pragma unroll
+      for (int c = 0; c < BNT / 64; ++c)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int j = 64 * c + 16 * ks;                  // K index (column of the tile)
+          mma_bf16(tm_da, smem_desc_sw128(w_base + c * 16384 + ks * 32, 16, 1024),
+                   smem_desc_sw128(b_base + j * 128, BNT * 128, 1024), id_da, (t | c | ks) != 0);
+        }
+      mma_commit(&w_empty[b]);
+      mma_commit(&b_empty[s]);
+    };
+    for (int t = 0; t < ntiles; ++t) {
+      issue_s(t);
+      if (GRAD && t > 0) issue_da(t - 1);
+    }
+    if (GRAD && ntiles > 0) issue_da(ntiles - 1);
+    mma_commit(da_full);
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ epilogue
+    const int wg = (warp - 4) >> 2;                       // column half of the tile
+    const int q = warp & 3;                               // TMEM lane quarter
+    const int r = q * 32 + lane;                          // row within the tile
+    const int row = a0 + r;
+    const bool rv = row < p.Na;
+    const float astat = rv ? p.a_stat[row] : 0.f;
+    const float lr2 = (GRAD && rv) ? p.lr[row] * kLog2e : 0.f;
+    const float lr_nat = (GRAD && rv) ? p.lr[row] : 0.f;
+    const int ig = p.row_offset + row;
+    float m2 = -INFINITY, ssum = 0.f, wsum = 0.f;
+    constexpr int HALF = BNT / 2;
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t % STAGES, b = t & 1;
+      const int j0 = jbeg + t * BNT;
+      mbar_wait(&s_full[b], (t >> 1) & 1);
+      tc_fence_after();
+      if (GRAD && t >= 2) mbar_wait(&w_empty[b], ((t >> 1) - 1) & 1);
+      const float* bst = sStat + s * 2 * BNT;
+#pragma unroll 1
+      for (int cc = 0; cc < HALF; cc += 16) {
+        const int c0 = wg * HALF + cc;                    // column within the tile
+        float v[16];
+        tmem_ld16(tm_s[b] + ((uint32_t)(q * 32) << 16) + c0, v);
+        float w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int jl = c0 + i;
+          const int jg = j0 + jl;
+          const bool valid = rv && jg < jend;
+          float l, rs = 0.f;
+          if (ENERGY == CRL_ENERGY_L2) {
+            const float d2 = fmaxf(astat + bst[jl] - 2.f * v[i], 0.f) + kEpsL2;
+            rs = rsq(d2);
+            l = -d2 * rs;
+          } else if (ENERGY == CRL_ENERGY_COS) {
+            l = v[i] * astat * bst[jl];
+          } else {
+            l = v[i];
+          }
+          const float t2 = l * kLog2e;
+          if (!GRAD) {
+            if (valid) {
+              if (t2 > m2) { ssum = ssum * ex2(m2 - t2) + 1.f; m2 = t2; }
+              else ssum += ex2(t2 - m2);
+            }
+          } else {
+            float wv = 0.f;
+            if (valid) {
+              const float lc = bst[BNT + jl];
+              const float pe = ex2(t2 - lr2);
+              const float qe = ex2(t2 - lc * kLog2e);
+              const float dl = (ig == jg) ? 1.f : 0.f;
+              const float g = p.invN * (p.c_r * (pe - dl) + p.c_c * (qe - dl)) +
+                              2.f * p.invN * (p.beta_r * lr_nat * pe + p.beta_c * lc * qe);
+              if (ENERGY == CRL_ENERGY_L2) wv = g * rs;
+              else if (ENERGY == CRL_ENERGY_COS) wv = g * bst[jl];
+              else wv = g;
+            }
+            w[i] = wv;
+            if (ENERGY == CRL_ENERGY_L2) wsum += wv;
+          }
+        }
+        if (GRAD) {
+          // 16 bf16 of row r, columns c0..c0+15 -> two 16-byte units of the swizzled W tile
+          uint8_t* wt = sW + b * C::W_BYTES + (c0 >> 6) * 16384;
+          const int k = c0 & 63;
+          uint4 u0, u1;
+          u0.x = pack_bf16x2(w[0], w[1]);   u0.y = pack_bf16x2(w[2], w[3]);
+          u0.z = pack_bf16x2(w[4], w[5]);   u0.w = pack_bf16x2(w[6], w[7]);
+          u1.x = pack_bf16x2(w[8], w[9]);   u1.y = pack_bf16x2(w[10], w[11]);
+          u1.z = pack_bf16x2(w[12], w[13]); u1.w = pack_bf16x2(w[14], w[15]);
+          *reinterpret_cast<uint4*>(wt + sw128_off(r, k)) = u0;
+          *reinterpret_cast<uint4*>(wt + sw128_off(r, k + 8)) = u1;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);
+      if (!GRAD && lane == 0) mbar_arrive(&b_empty[s]);
+      if (GRAD) {
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&w_full[b]);
+      }
+    }
+    // ---- per-row partial results: warpgroup 1 hands its half to warpgroup 0
+    if (wg == 1) {
+      sMerge[r] = m2; sMerge[128 + r] = ssum; sMerge[256 + r] = wsum;
+    }
+    named_sync(1, 256);
+    if (wg == 0 && rv) {
+      if (!GRAD) {
+        const float m2b = sMerge[r], sb = sMerge[128 + r];
+        const float mx = fmaxf(m2, m2b);
+        float st = 0.f;
+        if (m2 != -INFINITY) st += ssum * ex2(m2 - mx);
+        if (m2b != -INFINITY) st += sb * ex2(m2b - mx);
+        p.part_m[(size_t)split * p.Na + row] = mx;
+        p.part_s[(size_t)split * p.Na + row] = st;
+      } else {
+        if (ENERGY == CRL_ENERGY_L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[256 + r];
+      }
+    }
+    if (GRAD && wg == 0) {
+      mbar_wait(da_full, 0);
+      tc_fence_after();
+      float* out = p.part_da + ((size_t)split * p.Na + row) * D;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 16) {
+        float v[16];
+        tmem_ld16(tm_da + ((uint32_t)(q * 32) << 16) + c0, v);
+        if (ntiles == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (rv) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            reinterpret_cast<float4*>(out + c0)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// --------------------------------------------------------------------------- merges / prep
+// Row statistics of the bf16-rounded representations: L2 -> |x|^2, cos -> 1/max(|x|, eps),
+// dot -> 0.  One warp per row.
+__global__ void rowstat_bf16_kernel(const __nv_bfloat16* __restrict__ x, int N, int D, int energy,
+                                    float* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= N) return;
+  float s = 0.f;
+  for (int k = lane; k < D; k += 32) {
+    const float v = __bfloat162float(x[(size_t)w * D + k]);
+    s = fmaf(v, v, s);
+  }
+  s = warp_sum(s);
+  if (lane == 0) out[w] = energy == CRL_ENERGY_L2 ? s : (energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(s), kEpsCos) : 0.f);
+}
+
+// lse[i] = (max_s m + log2(sum_s s * 2^(m_s - max))) * ln 2
+__global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int Na, int S,
+                                 float* __restrict__ lse) {
+  pdl_wait();
+  pdl_launch();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Na) return;
+  float mx = -INFINITY;
+  for (int s = 0; s < S; ++s) mx = fmaxf(mx, pm[(size_t)s * Na + i]);
+  float t = 0.f;
+  for (int s = 0; s < S; ++s) {
+    const float m = pm[(size_t)s * Na + i];
+    if (m != -INFINITY) t += ps[(size_t)s * Na + i] * exp2f(m - mx);
+  }
+  lse[i] = (mx + log2f(t)) * kLn2;
+}
+
+// dA[i] = sum_s part[s][i]  (+ energy finalisation), fp32 and bf16 outputs.  One warp per row.
+template <int ENERGY>
+__global__ void grad_merge_kernel(const float* __restrict__ part, const float* __restrict__ prs,
+                                  const __nv_bfloat16* __restrict__ A, const float* __restrict__ a_stat, int Na,
+                                  int D, int S, float* __restrict__ out, __nv_bfloat16* __restrict__ outb) {
+  pdl_wait();
+  pdl_launch();
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= Na) return;
+  float rs = 0.f;
+  if (ENERGY == CRL_ENERGY_L2)
+    for (int s = 0; s < S; ++s) rs += prs[(size_t)s * Na + w];
+  float acc[8];                                          // D <= 256 -> 8 per lane
+  float pr = 0.f;
+  const float inv = ENERGY == CRL_ENERGY_COS ? a_stat[w] : 0.f;
+  for (int c = 0; c < D / 32; ++c) {
+    const int k = lane + 32 * c;
+    float v = 0.f;
+    for (int s = 0; s < S; ++s) v += part[((size_t)s * Na + w) * D + k];
+    const float a = __bfloat162float(A[(size_t)w * D + k]);
+    if (ENERGY == CRL_ENERGY_L2) v -= rs * a;
+    if (ENERGY == CRL_ENERGY_COS) pr = fmaf(v, a * inv, pr);
+    acc[c] = v;
+  }
+  if (ENERGY == CRL_ENERGY_COS) pr = warp_sum(pr);
+  for (int c = 0; c < D / 32; ++c) {
+    const int k = lane + 32 * c;
+    float v = acc[c];
+    if (ENERGY == CRL_ENERGY_COS) {
+      const float u = __bfloat162float(A[(size_t)w * D + k]) * inv;
+      v = inv < 1.f / kEpsCos ? (v - pr * u) * inv : v * inv;
+    }
+    out[(size_t)w * D + k] = v;
+    outb[(size_t)w * D + k] = __float2bfloat16_rn(v);
+  }
+}
+
+// ------------------------------------------------------------------------------- host side
+bool make_map_bf16(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
+
+bool tc_logits_supports(int D) { return D == 64 || D == 128 || D == 256; }
+
+int tc_logits_splits(int Na, int Nb, int D, int num_sms) {
+  const int rb = (Na + 127) / 128;
+  const int bnt = D <= 128 ? 128 : 64;
+  const int tiles = (Nb + bnt - 1) / bnt;
+  int s = (num_sms + rb - 1) / rb;
+  if (s > tiles) s = tiles;
+  return s < 1 ? 1 : s;
+}
+
+bool tc_logits_maps(CUtensorMap* mA, CUtensorMap* mB, const __nv_bfloat16* A, int Na, const __nv_bfloat16* B,
+                    int Nb, int D) {
+  const int bnt = D <= 128 ? 128 : 64;
+  return make_map_bf16(mA, A, D, Na, D, 64, 128) && make_map_bf16(mB, B, D, Nb, D, 64, bnt);
+}
+
+template <int D, int ENERGY, bool GRAD>
+static cudaError_t launch_lg(const CUtensorMap& a, const CUtensorMap& b, const TcLogitsArgs& p, int S,
+                             cudaStream_t st) {
+  static bool attr = false;
+  const size_t smem = LgCfg<D>::smem(GRAD);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_logits_kernel<D, ENERGY, GRAD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((p.Na + 127) / 128, S);
+  return launch_pdl(tc_logits_kernel<D, ENERGY, GRAD>, grid, dim3(384), smem, st, a, b, p);
+}
+
+template <bool GRAD>
+static cudaError_t dispatch_lg(int D, int energy, const CUtensorMap& a, const CUtensorMap& b,
+                               const TcLogitsArgs& p, int S, cudaStream_t st) {
+#define CRL_LG(DD)                                                                     \
+  if (D == DD) {                                                                       \
+    if (energy == CRL_ENERGY_L2) return launch_lg<DD, CRL_ENERGY_L2, GRAD>(a, b, p, S, st); \
+    if (energy == CRL_ENERGY_DOT) return launch_lg<DD, CRL_ENERGY_DOT, GRAD>(a, b, p, S, st); \
+    return launch_lg<DD, CRL_ENERGY_COS, GRAD>(a, b, p, S, st);                         \
+  }
+  CRL_LG(64)
+  CRL_LG(128)
+  CRL_LG(256)
+#undef CRL_LG
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
+                          const float* a_stat, const float* b_stat, int S, float* part_m, float* part_s,
+                          float* lse, cudaStream_t st) {
+  TcLogitsArgs p{};
+  p.Na = Na; p.Nb = Nb;
+  const int bnt = D <= 128 ? 128 : 64;
+  p.cols_per_split = ((Nb + S - 1) / S + bnt - 1) / bnt * bnt;
+  p.a_stat = a_stat; p.b_stat = b_stat; p.part_m = part_m; p.part_s = part_s;
+  cudaError_t e = dispatch_lg<false>(D, energy, mA, mB, p, S, st);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(lse_merge_kernel, dim3((Na + 255) / 256), dim3(256), 0, st, (const float*)part_m,
+                    (const float*)part_s, Na, S, lse);
+}
+
+cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
+                           int row_offset, const float* a_stat, const float* b_stat, const float* lr,
+                           const float* lc, float c_r, float c_c, float beta_r, float beta_c, float invN, int S,
+                           float* part_da, float* part_rs, const __nv_bfloat16* A, float* dA,
+                           __nv_bfloat16* dAb, cudaStream_t st) {
+  TcLogitsArgs p{};
+  p.Na = Na; p.Nb = Nb; p.row_offset = row_offset;
+  const int bnt = D <= 128 ? 128 : 64;
+  p.cols_per_split = ((Nb + S - 1) / S + bnt - 1) / bnt * bnt;
+  p.a_stat = a_stat; p.b_stat = b_stat; p.lr = lr; p.lc = lc;
+  p.c_r = c_r; p.c_c = c_c; p.beta_r = beta_r; p.beta_c = beta_c; p.invN = invN;
+  p.part_da = part_da; p.part_rs = part_rs;
+  cudaError_t e = dispatch_lg<true>(D, energy, mA, mB, p, S, st);
+  if (e != cudaSuccess) return e;
+  const dim3 g((Na * 32 + 255) / 256);
+  if (energy == CRL_ENERGY_L2)
+    return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2>, g, dim3(256), 0, st, (const float*)part_da,
+                      (const float*)part_rs, A, a_stat, Na, D, S, dA, dAb);
+  if (energy == CRL_ENERGY_COS)
+    return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, g, dim3(256), 0, st, (const float*)part_da,
+                      (const float*)part_rs, A, a_stat, Na, D, S, dA, dAb);
+  return launch_pdl(grad_merge_kernel<CRL_ENERGY_DOT>, g, dim3(256), 0, st, (const float*)part_da,
+                    (const float*)part_rs, A, a_stat, Na, D, S, dA, dAb);
+}
+
+cudaError_t launch_rowstat_bf16(const __nv_bfloat16* x, int N, int D, int energy, float* out, cudaStream_t st) {
+  return launch_pdl(rowstat_bf16_kernel, dim3((N * 32 + 255) / 256), dim3(256), 0, st, x, N, D, energy, out);
+}
+
+}  // namespace tc
+}  // namespace crl

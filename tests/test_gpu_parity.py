@@ -228,3 +228,17 @@ def test_critic_step_bf16_repr256_width1024():
     """configs[4] network shapes (4x1024, repr 256) at a batch the oracle finishes quickly."""
     cfg = crl_synth.preset("netscale", batch=512)
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+# tensor-core logits stage (bf16 path, N >= 1024): ragged N (not a multiple of the 128-row
+# tiles), every energy and loss kind, D = 64 and D = 256
+@pytest.mark.parametrize("energy", ["l2", "dot", "cos"])
+@pytest.mark.parametrize("loss", ["fwd", "bwd", "sym"])
+def test_critic_step_bf16_tc_logits(energy, loss):
+    cfg = crl_synth.preset("ant", batch=1100, width=128, energy=energy, loss=loss, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+def test_critic_step_bf16_tc_logits_repr256():
+    cfg = crl_synth.preset("ant", batch=1536, width=128, repr_dim=256, precision="bf16", beta_lse=0.3)
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
