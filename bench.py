@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="ant")
-    p.add_argument("--precision", default=None)
+    p.add_argument("--precision", default="bf16")
     p.add_argument("--energy", default=None)
     p.add_argument("--profile-steps", type=int, default=20)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -132,12 +132,21 @@ def stage_work(stage, cfg, N, Bl):
     in_phi, in_psi = cfg["obs_dim"] + cfg["act_dim"], cfg["goal_dim"]
     fp32 = cfg["precision"] == "fp32"
     dims = lambda i: [i] + [Wd] * depth + [D]
+    if stage in ("lse_row", "lse_col", "grad_phi", "grad_psi") and not fp32:
+        # bf16 path: the logits stage is bound by the MUFU/XU pipe: the
+        # algorithmic transcendental count of the WHOLE stage is 4 per logit for L2 (one exp +
+        # one sqrt per pass) and 2 for dot/cos; four launches share it -> 1/4 per launch.
+        per = (4.0 if cfg["energy"] == "l2" else 2.0) / 4.0
+        return Bl * N * per, "op", "xu"
     if stage in ("lse_row", "lse_col"):
-        # the logits GEMM (2 N^2 D, counted once for both orientations) -> N_l N D per launch
-        return Bl * N * D * 1.0, "flop", "alu" if fp32 else "tensor"
+        # fp32 path: the logits GEMM (2 N^2 D, counted once for both orientations) -> N_l N D
+        return Bl * N * D * 1.0, "flop", "alu"
     if stage in ("grad_phi", "grad_psi"):
         # the two backward contractions (W Psi and W^T Phi): 2 N^2 D each, one per launch
-        return 2.0 * Bl * N * D, "flop", "alu" if fp32 else "tensor"
+        return 2.0 * Bl * N * D, "flop", "alu"
+    if "_bwd_db_" in stage:
+        out = D if stage.endswith(f"_l{depth}") else Wd
+        return float(Bl * out * 2), "byte", "hbm"
     if stage == "adam":
         return 28.0 * crl_synth.critic_param_count(cfg), "byte", "hbm"
     if stage == "relabel":
@@ -169,6 +178,14 @@ def roofline(stages, cfg, N, Bl, peaks, peak_kind, clocks, traffic_db):
         peak = peaks["bf16_tflops"]
         u = "TFLOP/s"
         note = f"dense bf16 ({peak_kind} MEASURED_PEAKS.json bf16_tflops, burst)"
+    elif bound == "xu":
+        # MUFU/XU transcendental pipe: 148 SMs x 16 ops/clk x clock
+        mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        achieved = work / (per_launch_ms * 1e-3) / 1e9
+        peak = 148 * 16 * mhz * 1e6 / 1e9
+        u = "Gop/s"
+        bound = "alu"
+        note = f"MUFU/XU pipe: 148 SM x 16 op/clk x {mhz:.0f} MHz (median SM clock under load)"
     else:
         # fp32 SIMT: 148 SMs x 128 FP32 lanes x 2 flop/FMA x clock
         mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
@@ -176,7 +193,6 @@ def roofline(stages, cfg, N, Bl, peaks, peak_kind, clocks, traffic_db):
         peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
         u = "TFLOP/s"
         note = f"FP32 FMA pipe: 148 SM x 128 lanes x 2 x {mhz:.0f} MHz (median SM clock under load)"
-    step_ms = sum(v[0] for v in stages.values()) / max(1, max(v[1] for v in stages.values()))
     return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": u,
             "frac": round(achieved / peak, 4), "traffic": traffic_db.get(name),
             "kernel": name, "launch_us": round(per_launch_ms * 1e3, 3),

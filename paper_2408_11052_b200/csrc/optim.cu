@@ -78,13 +78,23 @@ __global__ void __launch_bounds__(256) loss_partial_kernel(
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    float t1 = 0.f, t2 = 0.f, t3 = 0.f;
-    for (unsigned j = 0; j < gridDim.x; ++j) {
-      t1 += __ldcg(part + j * 4 + 0); t2 += __ldcg(part + j * 4 + 1); t3 += __ldcg(part + j * 4 + 2);
-    }
-    acc[0] = t1; acc[1] = t2; acc[2] = t3;
+  if (!last) return;
+  // last CTA: all 256 threads add the CTA partials (strided, then a fixed-order tree)
+  __threadfence();
+  __shared__ float tr[3][256];
+  float t1 = 0.f, t2 = 0.f, t3 = 0.f;
+  for (unsigned j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
+    t1 += __ldcg(part + j * 4 + 0); t2 += __ldcg(part + j * 4 + 1); t3 += __ldcg(part + j * 4 + 2);
+  }
+  tr[0][threadIdx.x] = t1; tr[1][threadIdx.x] = t2; tr[2][threadIdx.x] = t3;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h)
+      for (int c = 0; c < 3; ++c) tr[c][threadIdx.x] += tr[c][threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    acc[0] = tr[0][0]; acc[1] = tr[1][0]; acc[2] = tr[2][0];
     *ticket = 0u;                                  // re-armed for the next (graph) replay
     if (finalize) loss_finalize_dev(acc, invN, c_f, c_b, beta, loss_out, skip, adam_t, status);
   }
