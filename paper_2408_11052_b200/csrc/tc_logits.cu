@@ -210,76 +210,95 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
     const float lr_nat = (GRAD && rv) ? p.lr[row] : 0.f;
     const int ig = p.row_offset + row;
     float m2 = -INFINITY, ssum = 0.f, wsum = 0.f;
-    constexpr int HALF = BNT / 2;
+    constexpr int HALF = BNT / 2;                         // columns per warpgroup per tile
+    constexpr int NCH = HALF / 32;                        // x32 TMEM loads per tile
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % STAGES, b = t & 1;
       const int j0 = jbeg + t * BNT;
+      const int nval = jend - j0;                         // valid columns in this tile
       mbar_wait(&s_full[b], (t >> 1) & 1);
       tc_fence_after();
-      if (GRAD && t >= 2) mbar_wait(&w_empty[b], ((t >> 1) - 1) & 1);
-      const float* bst = sStat + s * 2 * BNT;
-#pragma unroll 1
-      for (int cc = 0; cc < HALF; cc += 16) {
-        const int c0 = wg * HALF + cc;                    // column within the tile
-        float v[16];
-        tmem_ld16(tm_s[b] + ((uint32_t)(q * 32) << 16) + c0, v);
-        float w[16];
+      // the whole half-tile is pulled out of TMEM at once; the buffer is then handed back
+      // to the MMA warp before any arithmetic (overlaps S(t+2) with this epilogue)
+      uint32_t raw[NCH][32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int jl = c0 + i;
-          const int jg = j0 + jl;
-          const bool valid = rv && jg < jend;
-          float l, rs = 0.f;
-          if (ENERGY == CRL_ENERGY_L2) {
-            const float d2 = fmaxf(astat + bst[jl] - 2.f * v[i], 0.f) + kEpsL2;
-            rs = rsq(d2);
-            l = -d2 * rs;
-          } else if (ENERGY == CRL_ENERGY_COS) {
-            l = v[i] * astat * bst[jl];
-          } else {
-            l = v[i];
-          }
-          const float t2 = l * kLog2e;
-          if (!GRAD) {
-            if (valid) {
-              if (t2 > m2) { ssum = ssum * ex2(m2 - t2) + 1.f; m2 = t2; }
-              else ssum += ex2(t2 - m2);
-            }
-          } else {
-            float wv = 0.f;
-            if (valid) {
-              const float lc = bst[BNT + jl];
-              const float pe = ex2(t2 - lr2);
-              const float qe = ex2(t2 - lc * kLog2e);
-              const float dl = (ig == jg) ? 1.f : 0.f;
-              const float g = p.invN * (p.c_r * (pe - dl) + p.c_c * (qe - dl)) +
-                              2.f * p.invN * (p.beta_r * lr_nat * pe + p.beta_c * lc * qe);
-              if (ENERGY == CRL_ENERGY_L2) wv = g * rs;
-              else if (ENERGY == CRL_ENERGY_COS) wv = g * bst[jl];
-              else wv = g;
-            }
-            w[i] = wv;
-            if (ENERGY == CRL_ENERGY_L2) wsum += wv;
-          }
-        }
-        if (GRAD) {
-          // 16 bf16 of row r, columns c0..c0+15 -> two 16-byte units of the swizzled W tile
-          uint8_t* wt = sW + b * C::W_BYTES + (c0 >> 6) * 16384;
-          const int k = c0 & 63;
-          uint4 u0, u1;
-          u0.x = pack_bf16x2(w[0], w[1]);   u0.y = pack_bf16x2(w[2], w[3]);
-          u0.z = pack_bf16x2(w[4], w[5]);   u0.w = pack_bf16x2(w[6], w[7]);
-          u1.x = pack_bf16x2(w[8], w[9]);   u1.y = pack_bf16x2(w[10], w[11]);
-          u1.z = pack_bf16x2(w[12], w[13]); u1.w = pack_bf16x2(w[14], w[15]);
-          *reinterpret_cast<uint4*>(wt + sw128_off(r, k)) = u0;
-          *reinterpret_cast<uint4*>(wt + sw128_off(r, k + 8)) = u1;
-        }
-      }
+      for (int c = 0; c < NCH; ++c)
+        tmem_ld32_nowait(tm_s[b] + ((uint32_t)(q * 32) << 16) + wg * HALF + 32 * c, raw[c]);
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[b]);
-      if (!GRAD && lane == 0) mbar_arrive(&b_empty[s]);
-      if (GRAD) {
+      if (GRAD && t >= 2) mbar_wait(&w_empty[b], ((t >> 1) - 1) & 1);
+      const float* bst = sStat + s * 2 * BNT;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const int c0 = wg * HALF + 32 * c;                // column within the tile
+        float tv[32], rsv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int jl = c0 + i;
+          const float v = __uint_as_float(raw[c][i]);
+          float l;
+          if (ENERGY == CRL_ENERGY_L2) {
+            const float d2 = fmaxf(fmaf(-2.f, v, astat + bst[jl]), 0.f) + kEpsL2;
+            rsv[i] = rsq(d2);
+            l = -d2 * rsv[i];
+          } else if (ENERGY == CRL_ENERGY_COS) {
+            l = v * astat * bst[jl];
+          } else {
+            l = v;
+          }
+          tv[i] = (jl < nval) ? l * kLog2e : -INFINITY;
+        }
+        if (!GRAD) {
+          // chunk-wise online logsumexp: one rescale per 32 columns, no per-element branches
+          float cm = tv[0];
+#pragma unroll
+          for (int i = 1; i < 32; ++i) cm = fmaxf(cm, tv[i]);
+          if (cm > m2) { ssum *= ex2(m2 - cm); m2 = cm; }
+          if (m2 != -INFINITY) {
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc += ex2(tv[i] - m2);
+            ssum += acc;
+          }
+        } else {
+          float w[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int jl = c0 + i;
+            const int jg = j0 + jl;
+            const float lc = bst[BNT + jl];
+            const float pe = ex2(tv[i] - lr2);            // masked columns: 2^-inf = 0
+            const float qe = ex2(tv[i] - lc * kLog2e);
+            const float dl = (ig == jg) ? 1.f : 0.f;
+            const float g = p.invN * (p.c_r * (pe - dl) + p.c_c * (qe - dl)) +
+                            2.f * p.invN * (p.beta_r * lr_nat * pe + p.beta_c * lc * qe);
+            float wv;
+            if (ENERGY == CRL_ENERGY_L2) wv = g * rsv[i];
+            else if (ENERGY == CRL_ENERGY_COS) wv = g * bst[jl];
+            else wv = g;
+            wv = (jl < nval) ? wv : 0.f;
+            w[i] = wv;
+            if (ENERGY == CRL_ENERGY_L2) wsum += wv;
+          }
+          // 32 bf16 of row r -> four 16-byte units of the swizzled W tile
+          uint8_t* wt = sW + b * C::W_BYTES + (c0 >> 6) * 16384;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 pk;
+            pk.x = pack_bf16x2(w[8 * u + 0], w[8 * u + 1]);
+            pk.y = pack_bf16x2(w[8 * u + 2], w[8 * u + 3]);
+            pk.z = pack_bf16x2(w[8 * u + 4], w[8 * u + 5]);
+            pk.w = pack_bf16x2(w[8 * u + 6], w[8 * u + 7]);
+            *reinterpret_cast<uint4*>(wt + sw128_off(r, (c0 & 63) + 8 * u)) = pk;
+          }
+        }
+      }
+      if (!GRAD) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_empty[s]);
+      } else {
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&w_full[b]);
