@@ -117,6 +117,15 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       }
       c->stat_phi = s.take<float>((size_t)N + kStatPad);
       c->stat_psi = s.take<float>((size_t)N + kStatPad);
+      c->fac_row = s.take<float>((size_t)Bl + kStatPad);
+      c->fac_col = s.take<float>((size_t)Bl + kStatPad);
+      if (W > 1) {
+        c->fac_row_g = s.take<float>((size_t)N + kStatPad);
+        c->fac_col_g = s.take<float>((size_t)N + kStatPad);
+      } else {
+        c->fac_row_g = c->fac_row;
+        c->fac_col_g = c->fac_col;
+      }
       // two sets (row call on phi, column call on psi run concurrently)
       c->lg_part_m = s.take<float>((size_t)2 * c->lg_splits * Bl);
       c->lg_part_s = s.take<float>((size_t)2 * c->lg_splits * Bl);

@@ -53,6 +53,7 @@ struct TcLogitsArgs {
   const float* b_stat;             // [Nb padded]  same for B
   const float* lr;                 // GRAD: row statistic (natural log) [Na]
   const float* lc;                 // GRAD: column statistic [Nb padded]
+  const float* lcf;                // GRAD: column factor 2^(-lc log2 e), or -1 when out of range
   float c_r, c_c, beta_r, beta_c, invN;
   float* part_m;                   // LSE: [S][Na] running max (log2 units)
   float* part_s;                   // LSE: [S][Na] running sum
@@ -71,7 +72,7 @@ struct LgCfg {
   static constexpr uint32_t STAT_BYTES = BNT * 4;
   static constexpr int TMEM_COLS = 512;
   static constexpr size_t smem(bool grad) {
-    return 1024 + A_BYTES + STAGES * B_BYTES + (grad ? 2 * W_BYTES : 0) + STAGES * 2 * STAT_BYTES +
+    return 1024 + A_BYTES + STAGES * B_BYTES + (grad ? 2 * W_BYTES : 0) + STAGES * 3 * STAT_BYTES +
            2 * 128 * 4 * 3 + 512;
   }
 };
@@ -92,8 +93,8 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
   uint8_t* sA = smem;
   uint8_t* sB = sA + C::A_BYTES;
   uint8_t* sW = sB + STAGES * C::B_BYTES;
-  float* sStat = reinterpret_cast<float*>(sW + (GRAD ? 2 * C::W_BYTES : 0));   // [STAGES][2][BNT]
-  float* sMerge = sStat + STAGES * 2 * BNT;                                     // [3][128] wg-1 partials
+  float* sStat = reinterpret_cast<float*>(sW + (GRAD ? 2 * C::W_BYTES : 0));   // [STAGES][3][BNT]
+  float* sMerge = sStat + STAGES * 3 * BNT;                                     // [3][128] wg-1 partials
   uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + 3 * 128);
   uint64_t* a_full = bars;
   uint64_t* b_full = bars + 1;
@@ -146,13 +147,16 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
       const int s = t % STAGES;
       mbar_wait(&b_empty[s], ((t / STAGES) & 1) ^ 1);
       const int j0 = jbeg + t * BNT;
-      mbar_expect_tx(&b_full[s], C::B_BYTES + (GRAD ? 2 : 1) * C::STAT_BYTES);
+      mbar_expect_tx(&b_full[s], C::B_BYTES + (GRAD ? 3 : 1) * C::STAT_BYTES);
       uint8_t* dst = sB + s * C::B_BYTES;
 #pragma unroll
       for (int c = 0; c < KC; ++c) tma_load_2d(dst + c * BNT * 128, &tmB, &b_full[s], 64 * c, j0);
-      float* st = sStat + s * 2 * BNT;
+      float* st = sStat + s * 3 * BNT;
       bulk_g2s(st, p.b_stat + j0, C::STAT_BYTES, &b_full[s]);
-      if (GRAD) bulk_g2s(st + BNT, p.lc + j0, C::STAT_BYTES, &b_full[s]);
+      if (GRAD) {
+        bulk_g2s(st + BNT, p.lc + j0, C::STAT_BYTES, &b_full[s]);
+        bulk_g2s(st + 2 * BNT, p.lcf + j0, C::STAT_BYTES, &b_full[s]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ------------------------------------------------------------------ MMA issuer
@@ -208,6 +212,10 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
     const float astat = rv ? p.a_stat[row] : 0.f;
     const float lr2 = (GRAD && rv) ? p.lr[row] * kLog2e : 0.f;
     const float lr_nat = (GRAD && rv) ? p.lr[row] : 0.f;
+    // q_ij = p_ij * 2^(lr2_i) * 2^(-lc2_j): one MUFU op per logit instead of two, whenever
+    // both factors are normal fp32 numbers (else the exact second exp2 is used)
+    const bool row_fac_ok = GRAD && lr2 > -120.f && lr2 < 120.f;
+    const float Ei = row_fac_ok ? ex2(lr2) : 0.f;
     const int ig = p.row_offset + row;
     float m2 = -INFINITY, ssum = 0.f, wsum = 0.f;
     constexpr int HALF = BNT / 2;                         // columns per warpgroup per tile
@@ -229,7 +237,7 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[b]);
       if (GRAD && t >= 2) mbar_wait(&w_empty[b], ((t >> 1) - 1) & 1);
-      const float* bst = sStat + s * 2 * BNT;
+      const float* bst = sStat + s * 3 * BNT;
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
         const int c0 = wg * HALF + 32 * c;                // column within the tile
@@ -269,8 +277,11 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
             const int jl = c0 + i;
             const int jg = j0 + jl;
             const float lc = bst[BNT + jl];
+            const float Fj = bst[2 * BNT + jl];
             const float pe = ex2(tv[i] - lr2);            // masked columns: 2^-inf = 0
-            const float qe = ex2(tv[i] - lc * kLog2e);
+            float qe;
+            if (row_fac_ok && Fj > 0.f) qe = pe * Ei * Fj;
+            else qe = ex2(tv[i] - lc * kLog2e);
             const float dl = (ig == jg) ? 1.f : 0.f;
             const float g = p.invN * (p.c_r * (pe - dl) + p.c_c * (qe - dl)) +
                             2.f * p.invN * (p.beta_r * lr_nat * pe + p.beta_c * lc * qe);
@@ -370,7 +381,7 @@ __global__ void rowstat_bf16_kernel(const __nv_bfloat16* __restrict__ x, int N, 
 
 // lse[i] = (max_s m + log2(sum_s s * 2^(m_s - max))) * ln 2
 __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int Na, int S,
-                                 float* __restrict__ lse) {
+                                 float* __restrict__ lse, float* __restrict__ fac) {
   pdl_wait();
   pdl_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -382,7 +393,10 @@ __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __re
     const float m = pm[(size_t)s * Na + i];
     if (m != -INFINITY) t += ps[(size_t)s * Na + i] * exp2f(m - mx);
   }
-  lse[i] = (mx + log2f(t)) * kLn2;
+  const float l2 = mx + log2f(t);                        // LSE in log2 units
+  lse[i] = l2 * kLn2;
+  // column factor for the gradient pass: 2^(-LSE log2 e) when it is a normal float, else -1
+  fac[i] = (l2 > -120.f && l2 < 120.f) ? exp2f(-l2) : -1.f;
 }
 
 // dA[i] = sum_s part[s][i]  (+ energy finalisation), fp32 and bf16 outputs.  One warp per row.
@@ -431,7 +445,7 @@ int tc_logits_splits(int Na, int Nb, int D, int num_sms) {
   const int rb = (Na + 127) / 128;
   const int bnt = D <= 128 ? 128 : 64;
   const int tiles = (Nb + bnt - 1) / bnt;
-  int s = (num_sms + rb - 1) / rb;
+  int s = num_sms / rb;                        // one wave: rb * s <= #SMs
   if (s > tiles) s = tiles;
   return s < 1 ? 1 : s;
 }
@@ -475,7 +489,7 @@ static cudaError_t dispatch_lg(int D, int energy, const CUtensorMap& a, const CU
 
 cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                           const float* a_stat, const float* b_stat, int S, float* part_m, float* part_s,
-                          float* lse, cudaStream_t st) {
+                          float* lse, float* fac, cudaStream_t st) {
   TcLogitsArgs p{};
   p.Na = Na; p.Nb = Nb;
   const int bnt = D <= 128 ? 128 : 64;
@@ -484,19 +498,19 @@ cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtens
   cudaError_t e = dispatch_lg<false>(D, energy, mA, mB, p, S, st);
   if (e != cudaSuccess) return e;
   return launch_pdl(lse_merge_kernel, dim3((Na + 255) / 256), dim3(256), 0, st, (const float*)part_m,
-                    (const float*)part_s, Na, S, lse);
+                    (const float*)part_s, Na, S, lse, fac);
 }
 
 cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                            int row_offset, const float* a_stat, const float* b_stat, const float* lr,
-                           const float* lc, float c_r, float c_c, float beta_r, float beta_c, float invN, int S,
-                           float* part_da, float* part_rs, const __nv_bfloat16* A, float* dA,
+                           const float* lc, const float* lcf, float c_r, float c_c, float beta_r, float beta_c,
+                           float invN, int S, float* part_da, float* part_rs, const __nv_bfloat16* A, float* dA,
                            __nv_bfloat16* dAb, cudaStream_t st) {
   TcLogitsArgs p{};
   p.Na = Na; p.Nb = Nb; p.row_offset = row_offset;
   const int bnt = D <= 128 ? 128 : 64;
   p.cols_per_split = ((Nb + S - 1) / S + bnt - 1) / bnt * bnt;
-  p.a_stat = a_stat; p.b_stat = b_stat; p.lr = lr; p.lc = lc;
+  p.a_stat = a_stat; p.b_stat = b_stat; p.lr = lr; p.lc = lc; p.lcf = lcf;
   p.c_r = c_r; p.c_c = c_c; p.beta_r = beta_r; p.beta_c = beta_c; p.invN = invN;
   p.part_da = part_da; p.part_rs = part_rs;
   cudaError_t e = dispatch_lg<true>(D, energy, mA, mB, p, S, st);
