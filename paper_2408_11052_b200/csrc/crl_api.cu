@@ -117,6 +117,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       }
       c->stat_phi = s.take<float>((size_t)N + kStatPad);
       c->stat_psi = s.take<float>((size_t)N + kStatPad);
+      c->fac_ok = s.take<int>(4);
       c->fac_row = s.take<float>((size_t)Bl + kStatPad);
       c->fac_col = s.take<float>((size_t)Bl + kStatPad);
       if (W > 1) {

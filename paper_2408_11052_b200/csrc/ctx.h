@@ -141,6 +141,7 @@ struct crl_ctx {
   float *stat_phi = nullptr, *stat_psi = nullptr;               // [N + pad] |x|^2 or 1/|x|
   float *fac_row = nullptr, *fac_col = nullptr;                 // 2^(-LSE log2e) per local row / column
   float *fac_row_g = nullptr, *fac_col_g = nullptr;             // gathered (aliases when W = 1)
+  int* fac_ok = nullptr;                                        // all factors normal this step
   float *lg_part_m = nullptr, *lg_part_s = nullptr, *lg_part_da = nullptr, *lg_part_rs = nullptr;
   CUtensorMap lg_row_A, lg_row_B, lg_col_A, lg_col_B;
 };

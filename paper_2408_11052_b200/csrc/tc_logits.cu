@@ -54,6 +54,7 @@ struct TcLogitsArgs {
   const float* lr;                 // GRAD: row statistic (natural log) [Na]
   const float* lc;                 // GRAD: column statistic [Nb padded]
   const float* lcf;                // GRAD: column factor 2^(-lc log2 e), or -1 when out of range
+  const int* fac_ok;               // GRAD: 1 if all row / column factors of the step are normal
   float c_r, c_c, beta_r, beta_c, invN;
   float* part_m;                   // LSE: [S][Na] running max (log2 units)
   float* part_s;                   // LSE: [S][Na] running sum
@@ -214,8 +215,9 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
     const float lr_nat = (GRAD && rv) ? p.lr[row] : 0.f;
     // q_ij = p_ij * 2^(lr2_i) * 2^(-lc2_j): one MUFU op per logit instead of two, whenever
     // both factors are normal fp32 numbers (else the exact second exp2 is used)
-    const bool row_fac_ok = GRAD && lr2 > -120.f && lr2 < 120.f;
-    const float Ei = row_fac_ok ? ex2(lr2) : 0.f;
+    // fac_ok == 1 <=> every LSE / LSE' of the step gives a normal factor (lse_merge clears it)
+    const bool fac_fast = GRAD && *p.fac_ok != 0;
+    const float EiFj_row = fac_fast ? ex2(lr2) : 0.f;
     const int ig = p.row_offset + row;
     float m2 = -INFINITY, ssum = 0.f, wsum = 0.f;
     constexpr int HALF = BNT / 2;                         // columns per warpgroup per tile
@@ -272,16 +274,12 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
           }
         } else {
           float w[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          // kernel-uniform choice (fac_fast): q from the rank-1 factor (1 MUFU op / logit) or
+          // the exact second exp2; two separate loops so neither is predicated into the other
+          auto grad_elem = [&](int i, float qe, float pe) {
             const int jl = c0 + i;
             const int jg = j0 + jl;
             const float lc = bst[BNT + jl];
-            const float Fj = bst[2 * BNT + jl];
-            const float pe = ex2(tv[i] - lr2);            // masked columns: 2^-inf = 0
-            float qe;
-            if (row_fac_ok && Fj > 0.f) qe = pe * Ei * Fj;
-            else qe = ex2(tv[i] - lc * kLog2e);
             const float dl = (ig == jg) ? 1.f : 0.f;
             const float g = p.invN * (p.c_r * (pe - dl) + p.c_c * (qe - dl)) +
                             2.f * p.invN * (p.beta_r * lr_nat * pe + p.beta_c * lc * qe);
@@ -292,6 +290,19 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
             wv = (jl < nval) ? wv : 0.f;
             w[i] = wv;
             if (ENERGY == CRL_ENERGY_L2) wsum += wv;
+          };
+          if (fac_fast) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float pe = ex2(tv[i] - lr2);          // masked columns: 2^-inf = 0
+              grad_elem(i, pe * EiFj_row * bst[2 * BNT + c0 + i], pe);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float pe = ex2(tv[i] - lr2);
+              grad_elem(i, ex2(tv[i] - bst[BNT + c0 + i] * kLog2e), pe);
+            }
           }
           // 32 bf16 of row r -> four 16-byte units of the swizzled W tile
           uint8_t* wt = sW + b * C::W_BYTES + (c0 >> 6) * 16384;
@@ -365,9 +376,11 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
 // Row statistics of the bf16-rounded representations: L2 -> |x|^2, cos -> 1/max(|x|, eps),
 // dot -> 0.  One warp per row.
 __global__ void rowstat_bf16_kernel(const __nv_bfloat16* __restrict__ x, int N, int D, int energy,
-                                    float* __restrict__ out) {
+                                    float* __restrict__ out, int* __restrict__ fac_ok, int fac_init) {
   pdl_wait();
   pdl_launch();
+  // re-armed every step (fac_init = 0 forces the exact path: CRL_FORCE_EXACT_Q, for tests)
+  if (fac_ok != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *fac_ok = fac_init;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= N) return;
   float s = 0.f;
@@ -381,7 +394,7 @@ __global__ void rowstat_bf16_kernel(const __nv_bfloat16* __restrict__ x, int N, 
 
 // lse[i] = (max_s m + log2(sum_s s * 2^(m_s - max))) * ln 2
 __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int Na, int S,
-                                 float* __restrict__ lse, float* __restrict__ fac) {
+                                 float* __restrict__ lse, float* __restrict__ fac, int* __restrict__ fac_ok) {
   pdl_wait();
   pdl_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -396,7 +409,9 @@ __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __re
   const float l2 = mx + log2f(t);                        // LSE in log2 units
   lse[i] = l2 * kLn2;
   // column factor for the gradient pass: 2^(-LSE log2 e) when it is a normal float, else -1
-  fac[i] = (l2 > -120.f && l2 < 120.f) ? exp2f(-l2) : -1.f;
+  const bool ok = l2 > -120.f && l2 < 120.f;
+  fac[i] = ok ? exp2f(-l2) : -1.f;
+  if (!ok) *fac_ok = 0;
 }
 
 // dA[i] = sum_s part[s][i]  (+ energy finalisation), fp32 and bf16 outputs.  One warp per row.
@@ -489,7 +504,7 @@ static cudaError_t dispatch_lg(int D, int energy, const CUtensorMap& a, const CU
 
 cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                           const float* a_stat, const float* b_stat, int S, float* part_m, float* part_s,
-                          float* lse, float* fac, cudaStream_t st) {
+                          float* lse, float* fac, int* fac_ok, cudaStream_t st) {
   TcLogitsArgs p{};
   p.Na = Na; p.Nb = Nb;
   const int bnt = D <= 128 ? 128 : 64;
@@ -498,19 +513,19 @@ cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtens
   cudaError_t e = dispatch_lg<false>(D, energy, mA, mB, p, S, st);
   if (e != cudaSuccess) return e;
   return launch_pdl(lse_merge_kernel, dim3((Na + 255) / 256), dim3(256), 0, st, (const float*)part_m,
-                    (const float*)part_s, Na, S, lse, fac);
+                    (const float*)part_s, Na, S, lse, fac, fac_ok);
 }
 
 cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                            int row_offset, const float* a_stat, const float* b_stat, const float* lr,
                            const float* lc, const float* lcf, float c_r, float c_c, float beta_r, float beta_c,
                            float invN, int S, float* part_da, float* part_rs, const __nv_bfloat16* A, float* dA,
-                           __nv_bfloat16* dAb, cudaStream_t st) {
+                           __nv_bfloat16* dAb, const int* fac_ok, cudaStream_t st) {
   TcLogitsArgs p{};
   p.Na = Na; p.Nb = Nb; p.row_offset = row_offset;
   const int bnt = D <= 128 ? 128 : 64;
   p.cols_per_split = ((Nb + S - 1) / S + bnt - 1) / bnt * bnt;
-  p.a_stat = a_stat; p.b_stat = b_stat; p.lr = lr; p.lc = lc; p.lcf = lcf;
+  p.a_stat = a_stat; p.b_stat = b_stat; p.lr = lr; p.lc = lc; p.lcf = lcf; p.fac_ok = fac_ok;
   p.c_r = c_r; p.c_c = c_c; p.beta_r = beta_r; p.beta_c = beta_c; p.invN = invN;
   p.part_da = part_da; p.part_rs = part_rs;
   cudaError_t e = dispatch_lg<true>(D, energy, mA, mB, p, S, st);
@@ -526,8 +541,10 @@ cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUten
                     (const float*)part_rs, A, a_stat, Na, D, S, dA, dAb);
 }
 
-cudaError_t launch_rowstat_bf16(const __nv_bfloat16* x, int N, int D, int energy, float* out, cudaStream_t st) {
-  return launch_pdl(rowstat_bf16_kernel, dim3((N * 32 + 255) / 256), dim3(256), 0, st, x, N, D, energy, out);
+cudaError_t launch_rowstat_bf16(const __nv_bfloat16* x, int N, int D, int energy, float* out, int* fac_ok,
+                                int fac_init, cudaStream_t st) {
+  return launch_pdl(rowstat_bf16_kernel, dim3((N * 32 + 255) / 256), dim3(256), 0, st, x, N, D, energy, out,
+                    fac_ok, fac_init);
 }
 
 }  // namespace tc

@@ -242,3 +242,12 @@ def test_critic_step_bf16_tc_logits(energy, loss):
 def test_critic_step_bf16_tc_logits_repr256():
     cfg = crl_synth.preset("ant", batch=1536, width=128, repr_dim=256, precision="bf16", beta_lse=0.3)
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("energy", ["l2", "cos"])
+def test_critic_step_bf16_tc_logits_exact_q_path(energy, monkeypatch):
+    """The gradient pass normally forms q_ij = p_ij 2^lse2_i 2^-lse2'_j; the exact second-exp2
+    path (taken when a factor is not a normal float) is forced here and checked the same way."""
+    monkeypatch.setenv("CRL_FORCE_EXACT_Q", "1")
+    cfg = crl_synth.preset("ant", batch=1100, width=128, energy=energy, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
