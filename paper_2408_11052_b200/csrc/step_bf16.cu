@@ -38,11 +38,11 @@ cudaError_t launch_colsum_bf16(const __nv_bfloat16*, int, int, int, float*, int,
 cudaError_t launch_f32_to_bf16(const float*, __nv_bfloat16*, size_t, int, cudaStream_t);
 bool tc_logits_maps(CUtensorMap*, CUtensorMap*, const __nv_bfloat16*, int, const __nv_bfloat16*, int, int);
 cudaError_t tc_logits_lse(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*,
-                          int, float*, float*, float*, float*, int*, cudaStream_t);
+                          int, float*, float*, float*, float*, int*, float, float, cudaStream_t);
 cudaError_t tc_logits_grad(int, int, const CUtensorMap&, const CUtensorMap&, int, int, int, const float*,
                            const float*, const float*, const float*, const float*, float, float, float, float,
-                           float, int, float*, float*, const __nv_bfloat16*, float*, __nv_bfloat16*, const int*,
-                           cudaStream_t);
+                           float, int, float*, float*, const __nv_bfloat16*, const __nv_bfloat16*, float*,
+                           __nv_bfloat16*, const int*, cudaStream_t);
 cudaError_t launch_rowstat_bf16(const __nv_bfloat16*, int, int, int, float*, int*, int, cudaStream_t);
 }  // namespace tc
 }  // namespace crl
@@ -209,12 +209,12 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     { Stage sg(ctx, st2, "lse_col");
       CU(tc::tc_logits_lse(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, ctx->stat_psi + row_off,
                            ctx->stat_phi, S, ctx->lg_part_m + (size_t)S * Bl, ctx->lg_part_s + (size_t)S * Bl,
-                           ctx->lse_col, ctx->fac_col, ctx->fac_ok, st2));
+                           ctx->lse_col, ctx->fac_col, ctx->fac_ok, invN * c_b, 0.f, st2));
       nl += 2; }
     { Stage sg(ctx, st, "lse_row");
       CU(tc::tc_logits_lse(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off,
                            ctx->stat_psi, S, ctx->lg_part_m, ctx->lg_part_s, ctx->lse_row, ctx->fac_row,
-                           ctx->fac_ok, st));
+                           ctx->fac_ok, invN * c_f, 2.f * invN * k.beta_lse, st));
       nl += 2; }
     join2(ctx, st, st2);
   } else {
@@ -260,7 +260,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                             ctx->stat_phi, ctx->lse_col, ctx->lse_row_g, ctx->fac_row_g, c_b, c_f, 0.f,
                             k.beta_lse, invN, S,
                             ctx->lg_part_da + (size_t)S * Bl * D, ctx->lg_part_rs + (size_t)S * Bl,
-                            ctx->psi_outb, ctx->dpsi, ctx->dpsib, ctx->fac_ok, st2));
+                            ctx->psi_outb, ctx->phi_outb_g, ctx->dpsi, ctx->dpsib, ctx->fac_ok, st2));
     } else {
       CU(logits_grad_f32(D, k.energy, ctx->psi_out, Bl, row_off, ctx->phi_g, N, ctx->lse_col, ctx->lse_row_g,
                          c_b, c_f, 0.f, k.beta_lse, invN, ctx->dpsi, st2));
@@ -276,8 +276,8 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(tc::tc_logits_grad(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, row_off, ctx->stat_phi + row_off,
                             ctx->stat_psi, ctx->lse_row, ctx->lse_col_g, ctx->fac_col_g, c_f, c_b,
                             k.beta_lse, 0.f, invN, S,
-                            ctx->lg_part_da, ctx->lg_part_rs, ctx->phi_outb, ctx->dphi, ctx->dphib,
-                            ctx->fac_ok, st));
+                            ctx->lg_part_da, ctx->lg_part_rs, ctx->phi_outb, ctx->psi_outb_g, ctx->dphi,
+                            ctx->dphib, ctx->fac_ok, st));
     } else {
       CU(logits_grad_f32(D, k.energy, ctx->phi_out, Bl, row_off, ctx->psi_g, N, ctx->lse_row, ctx->lse_col_g,
                          c_f, c_b, k.beta_lse, 0.f, invN, ctx->dphi, st));

@@ -53,7 +53,7 @@ struct TcLogitsArgs {
   const float* b_stat;             // [Nb padded]  same for B
   const float* lr;                 // GRAD: row statistic (natural log) [Na]
   const float* lc;                 // GRAD: column statistic [Nb padded]
-  const float* lcf;                // GRAD: column factor 2^(-lc log2 e), or -1 when out of range
+  const float* lcf;                // GRAD: column coefficient 2^(-lc log2 e)(invN c_c + 2 invN beta_c lc)
   const int* fac_ok;               // GRAD: 1 if all row / column factors of the step are normal
   float c_r, c_c, beta_r, beta_c, invN;
   float* part_m;                   // LSE: [S][Na] running max (log2 units)
@@ -217,8 +217,9 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
     // both factors are normal fp32 numbers (else the exact second exp2 is used)
     // fac_ok == 1 <=> every LSE / LSE' of the step gives a normal factor (lse_merge clears it)
     const bool fac_fast = GRAD && *p.fac_ok != 0;
-    const float EiFj_row = fac_fast ? ex2(lr2) : 0.f;
-    const int ig = p.row_offset + row;
+    const float Ei = fac_fast ? ex2(lr2) : 0.f;
+    const float Arow = p.invN * p.c_r + 2.f * p.invN * p.beta_r * lr_nat;
+    const float cc0 = p.invN * p.c_c, cc1 = 2.f * p.invN * p.beta_c;
     float m2 = -INFINITY, ssum = 0.f, wsum = 0.f;
     constexpr int HALF = BNT / 2;                         // columns per warpgroup per tile
     constexpr int NCH = HALF / 32;                        // x32 TMEM loads per tile
@@ -274,34 +275,32 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
           }
         } else {
           float w[32];
-          // kernel-uniform choice (fac_fast): q from the rank-1 factor (1 MUFU op / logit) or
-          // the exact second exp2; two separate loops so neither is predicated into the other
-          auto grad_elem = [&](int i, float qe, float pe) {
-            const int jl = c0 + i;
-            const int jg = j0 + jl;
-            const float lc = bst[BNT + jl];
-            const float dl = (ig == jg) ? 1.f : 0.f;
-            const float g = p.invN * (p.c_r * (pe - dl) + p.c_c * (qe - dl)) +
-                            2.f * p.invN * (p.beta_r * lr_nat * pe + p.beta_c * lc * qe);
+          // g_ij without the delta_ij term (added exactly by grad_merge):
+          //   g = p (A_i + E_i cc_j),  A_i = invN c_r + 2 invN beta_r LSE_i,
+          //   cc_j = 2^-lse2'_j (invN c_c + 2 invN beta_c LSE'_j)  (precomputed by lse_merge)
+          // masked columns have p = 2^-inf = 0.  fac_fast is kernel-uniform; the exact path
+          // evaluates q = 2^(t - lse2'_j) with a second exp2 (two separate loops, no predication).
+          auto grad_w = [&](int i, float g) {
             float wv;
             if (ENERGY == CRL_ENERGY_L2) wv = g * rsv[i];
-            else if (ENERGY == CRL_ENERGY_COS) wv = g * bst[jl];
+            else if (ENERGY == CRL_ENERGY_COS) wv = g * bst[c0 + i];
             else wv = g;
-            wv = (jl < nval) ? wv : 0.f;
             w[i] = wv;
             if (ENERGY == CRL_ENERGY_L2) wsum += wv;
           };
           if (fac_fast) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              const float pe = ex2(tv[i] - lr2);          // masked columns: 2^-inf = 0
-              grad_elem(i, pe * EiFj_row * bst[2 * BNT + c0 + i], pe);
+              const float pe = ex2(tv[i] - lr2);
+              grad_w(i, pe * fmaf(Ei, bst[2 * BNT + c0 + i], Arow));
             }
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
+              const float lc = bst[BNT + c0 + i];
               const float pe = ex2(tv[i] - lr2);
-              grad_elem(i, ex2(tv[i] - bst[BNT + c0 + i] * kLog2e), pe);
+              const float qe = ex2(tv[i] - lc * kLog2e);
+              grad_w(i, fmaf(pe, Arow, qe * fmaf(cc1, lc, cc0)));
             }
           }
           // 32 bf16 of row r -> four 16-byte units of the swizzled W tile
@@ -394,7 +393,8 @@ __global__ void rowstat_bf16_kernel(const __nv_bfloat16* __restrict__ x, int N, 
 
 // lse[i] = (max_s m + log2(sum_s s * 2^(m_s - max))) * ln 2
 __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int Na, int S,
-                                 float* __restrict__ lse, float* __restrict__ fac, int* __restrict__ fac_ok) {
+                                 float* __restrict__ lse, float* __restrict__ fac, int* __restrict__ fac_ok,
+                                 float cc0, float cc1) {
   pdl_wait();
   pdl_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -408,34 +408,55 @@ __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __re
   }
   const float l2 = mx + log2f(t);                        // LSE in log2 units
   lse[i] = l2 * kLn2;
-  // column factor for the gradient pass: 2^(-LSE log2 e) when it is a normal float, else -1
+  // column coefficient for the gradient pass in which these rows are the columns:
+  // cc = 2^(-LSE log2 e) (cc0 + cc1 LSE); needs 2^(-LSE log2 e) to be a normal float
   const bool ok = l2 > -120.f && l2 < 120.f;
-  fac[i] = ok ? exp2f(-l2) : -1.f;
+  fac[i] = ok ? exp2f(-l2) * fmaf(cc1, l2 * kLn2, cc0) : 0.f;
   if (!ok) *fac_ok = 0;
 }
 
 // dA[i] = sum_s part[s][i]  (+ energy finalisation), fp32 and bf16 outputs.  One warp per row.
+// Also adds the positive-pair (delta_ii) term of dL/dl, -C delta_ij with C = invN (c_r + c_c),
+// which the tile epilogue leaves out: its energy chain uses the pair (A_i, B_{row_offset+i})
+// (L2: 1/r_ii from the difference form; cos: 1/|B_i|).
 template <int ENERGY>
 __global__ void grad_merge_kernel(const float* __restrict__ part, const float* __restrict__ prs,
-                                  const __nv_bfloat16* __restrict__ A, const float* __restrict__ a_stat, int Na,
-                                  int D, int S, float* __restrict__ out, __nv_bfloat16* __restrict__ outb) {
+                                  const __nv_bfloat16* __restrict__ A, const float* __restrict__ a_stat,
+                                  const __nv_bfloat16* __restrict__ Bg, const float* __restrict__ b_stat,
+                                  int row_offset, float Cdiag, int Na, int D, int S, float* __restrict__ out,
+                                  __nv_bfloat16* __restrict__ outb) {
   pdl_wait();
   pdl_launch();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= Na) return;
+  const size_t ib = (size_t)(row_offset + w) * D;
   float rs = 0.f;
   if (ENERGY == CRL_ENERGY_L2)
     for (int s = 0; s < S; ++s) rs += prs[(size_t)s * Na + w];
-  float acc[8];                                          // D <= 256 -> 8 per lane
-  float pr = 0.f;
+  float av[8], bv[8], acc[8];                            // D <= 256 -> 8 per lane
+  float d2 = 0.f;
+  for (int c = 0; c < D / 32; ++c) {
+    const int k = lane + 32 * c;
+    av[c] = __bfloat162float(A[(size_t)w * D + k]);
+    bv[c] = __bfloat162float(Bg[ib + k]);
+    const float d = av[c] - bv[c];
+    d2 = fmaf(d, d, d2);
+  }
+  float diag = 0.f;                                      // energy-chain weight of the delta term
+  if (ENERGY == CRL_ENERGY_L2) diag = Cdiag / sqrtf(warp_sum(d2) + kEpsL2);   // times (A_i - B_i)
+  const float invb = ENERGY == CRL_ENERGY_COS ? b_stat[row_offset + w] : 0.f;
   const float inv = ENERGY == CRL_ENERGY_COS ? a_stat[w] : 0.f;
+  float pr = 0.f;
   for (int c = 0; c < D / 32; ++c) {
     const int k = lane + 32 * c;
     float v = 0.f;
     for (int s = 0; s < S; ++s) v += part[((size_t)s * Na + w) * D + k];
-    const float a = __bfloat162float(A[(size_t)w * D + k]);
-    if (ENERGY == CRL_ENERGY_L2) v -= rs * a;
-    if (ENERGY == CRL_ENERGY_COS) pr = fmaf(v, a * inv, pr);
+    if (ENERGY == CRL_ENERGY_L2) v += diag * (av[c] - bv[c]) - rs * av[c];
+    if (ENERGY == CRL_ENERGY_DOT) v -= Cdiag * bv[c];
+    if (ENERGY == CRL_ENERGY_COS) {
+      v -= Cdiag * invb * bv[c];
+      pr = fmaf(v, av[c] * inv, pr);
+    }
     acc[c] = v;
   }
   if (ENERGY == CRL_ENERGY_COS) pr = warp_sum(pr);
@@ -443,7 +464,7 @@ __global__ void grad_merge_kernel(const float* __restrict__ part, const float* _
     const int k = lane + 32 * c;
     float v = acc[c];
     if (ENERGY == CRL_ENERGY_COS) {
-      const float u = __bfloat162float(A[(size_t)w * D + k]) * inv;
+      const float u = av[c] * inv;
       v = inv < 1.f / kEpsCos ? (v - pr * u) * inv : v * inv;
     }
     out[(size_t)w * D + k] = v;
@@ -460,9 +481,19 @@ int tc_logits_splits(int Na, int Nb, int D, int num_sms) {
   const int rb = (Na + 127) / 128;
   const int bnt = D <= 128 ? 128 : 64;
   const int tiles = (Nb + bnt - 1) / bnt;
-  int s = num_sms / rb;                        // one wave: rb * s <= #SMs
-  if (s > tiles) s = tiles;
-  return s < 1 ? 1 : s;
+  // choose the column split that minimises (waves x tiles per CTA), i.e. the makespan of a
+  // static grid of rb x S CTAs on num_sms SMs (<= 8 splits: partial buffers grow with S)
+  int best = 1;
+  long best_cost = -1;
+  for (int s = 1; s <= 8 && s <= tiles; ++s) {
+    const int cps = (tiles + s - 1) / s;
+    const int sp = (tiles + cps - 1) / cps;
+    const long ctas = (long)rb * sp;
+    const long waves = (ctas + num_sms - 1) / num_sms;
+    const long cost = waves * cps;
+    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = sp; }
+  }
+  return best;
 }
 
 bool tc_logits_maps(CUtensorMap* mA, CUtensorMap* mB, const __nv_bfloat16* A, int Na, const __nv_bfloat16* B,
@@ -504,7 +535,7 @@ static cudaError_t dispatch_lg(int D, int energy, const CUtensorMap& a, const CU
 
 cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                           const float* a_stat, const float* b_stat, int S, float* part_m, float* part_s,
-                          float* lse, float* fac, int* fac_ok, cudaStream_t st) {
+                          float* lse, float* fac, int* fac_ok, float cc0, float cc1, cudaStream_t st) {
   TcLogitsArgs p{};
   p.Na = Na; p.Nb = Nb;
   const int bnt = D <= 128 ? 128 : 64;
@@ -513,13 +544,14 @@ cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtens
   cudaError_t e = dispatch_lg<false>(D, energy, mA, mB, p, S, st);
   if (e != cudaSuccess) return e;
   return launch_pdl(lse_merge_kernel, dim3((Na + 255) / 256), dim3(256), 0, st, (const float*)part_m,
-                    (const float*)part_s, Na, S, lse, fac, fac_ok);
+                    (const float*)part_s, Na, S, lse, fac, fac_ok, cc0, cc1);
 }
 
 cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                            int row_offset, const float* a_stat, const float* b_stat, const float* lr,
                            const float* lc, const float* lcf, float c_r, float c_c, float beta_r, float beta_c,
-                           float invN, int S, float* part_da, float* part_rs, const __nv_bfloat16* A, float* dA,
+                           float invN, int S, float* part_da, float* part_rs, const __nv_bfloat16* A,
+                           const __nv_bfloat16* Bg, float* dA,
                            __nv_bfloat16* dAb, const int* fac_ok, cudaStream_t st) {
   TcLogitsArgs p{};
   p.Na = Na; p.Nb = Nb; p.row_offset = row_offset;
@@ -531,14 +563,15 @@ cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUten
   cudaError_t e = dispatch_lg<true>(D, energy, mA, mB, p, S, st);
   if (e != cudaSuccess) return e;
   const dim3 g((Na * 32 + 255) / 256);
+  const float Cdiag = invN * (c_r + c_c);
   if (energy == CRL_ENERGY_L2)
     return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2>, g, dim3(256), 0, st, (const float*)part_da,
-                      (const float*)part_rs, A, a_stat, Na, D, S, dA, dAb);
+                      (const float*)part_rs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, dA, dAb);
   if (energy == CRL_ENERGY_COS)
     return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, g, dim3(256), 0, st, (const float*)part_da,
-                      (const float*)part_rs, A, a_stat, Na, D, S, dA, dAb);
+                      (const float*)part_rs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, dA, dAb);
   return launch_pdl(grad_merge_kernel<CRL_ENERGY_DOT>, g, dim3(256), 0, st, (const float*)part_da,
-                    (const float*)part_rs, A, a_stat, Na, D, S, dA, dAb);
+                    (const float*)part_rs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, dA, dAb);
 }
 
 cudaError_t launch_rowstat_bf16(const __nv_bfloat16* x, int N, int D, int energy, float* out, int* fac_ok,
