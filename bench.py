@@ -132,7 +132,8 @@ def stage_work(stage, cfg, N, Bl):
     in_phi, in_psi = cfg["obs_dim"] + cfg["act_dim"], cfg["goal_dim"]
     fp32 = cfg["precision"] == "fp32"
     dims = lambda i: [i] + [Wd] * depth + [D]
-    if stage in ("lse_row", "lse_col", "grad_phi", "grad_psi") and not fp32:
+    tc_logits = (not fp32) and N >= 1024 and D in (64, 128, 256)   # csrc/ctx.h kTcLogitsMinN
+    if stage in ("lse_row", "lse_col", "grad_phi", "grad_psi") and tc_logits:
         # bf16 path: the logits stage is bound by the MUFU/XU pipe: the
         # algorithmic transcendental count of the WHOLE stage is 4 per logit for L2 (one exp +
         # one sqrt per pass) and 2 for dot/cos; four launches share it -> 1/4 per launch.

@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -105,7 +106,9 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       c->dzb_phi[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
       c->dzb_psi[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
     }
-    c->tc_logits = N >= kTcLogitsMinN && tc_logits_supports(D);
+    // CRL_TC_LOGITS_MIN_N overrides the SIMT/tensor-core crossover (measurement knob)
+    const char* mn = std::getenv("CRL_TC_LOGITS_MIN_N");
+    c->tc_logits = N >= (mn ? std::atoi(mn) : kTcLogitsMinN) && tc_logits_supports(D);
     if (c->tc_logits) {
       c->lg_splits = tc_logits_splits(Bl, N, D, 148);
       if (W > 1) {
@@ -612,8 +615,10 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
     cudaGraphDestroy(graph);
     CU(ce);
     it = ctx->graphs.emplace(key, exec).first;
+    ctx->graph_launches[key] = ctx->launches;
   }
   CU(cudaGraphLaunch(it->second, st));
+  ctx->launches = ctx->graph_launches[key];
   if (loss_host) CU(cudaMemcpyAsync(loss_out, loss_dev, 16, cudaMemcpyDeviceToHost, st));
   return CRL_OK;
 }

@@ -102,6 +102,7 @@ struct crl_ctx {
   cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr, cap_stream3 = nullptr, cap_stream4 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, int> graph_launches;     // kernels per replay of each cached graph
   ncclComm_t comm = nullptr;
   int num_sms = 148;
   int launches = 0;
