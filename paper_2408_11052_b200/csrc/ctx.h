@@ -3,6 +3,7 @@
 #pragma once
 #include "common.cuh"
 #include "tc_common.cuh"
+#include "tc_chain.h"
 
 #include <nccl.h>
 
@@ -143,11 +144,16 @@ struct crl_ctx {
   float *fac_row = nullptr, *fac_col = nullptr;                 // 2^(-LSE log2e) per local row / column
   float *fac_row_g = nullptr, *fac_col_g = nullptr;             // gathered (aliases when W = 1)
   int* fac_ok = nullptr;                                        // all factors normal this step
+  // fused per-row-block MLP chains (bf16 path, width <= 256): one launch for both encoders'
+  // forward, one for both encoders' dX chain
+  bool use_chain = false;
+  tc::ChainMaps chain_fwd[2], chain_bwd[2];
+  tc::ChainParams chain_fwd_p{}, chain_bwd_p{};
   float *lg_part_m = nullptr, *lg_part_s = nullptr, *lg_part_da = nullptr, *lg_part_rs = nullptr;
   CUtensorMap lg_row_A, lg_row_B, lg_col_A, lg_col_B;
 };
 
-constexpr int kTcLogitsMinN = 1024;      // below this the SIMT logits kernels have more CTAs
+constexpr int kTcLogitsMinN = 2;         // measured: tensor-core logits win down to N = 256
 constexpr int kStatPad = 256;            // padding of per-column arrays read by 1-D bulk copies
 
 // Brackets one launch with CUDA events when the context is in profiling mode (events come

@@ -94,6 +94,63 @@ crl_status bf16_prepare(crl_ctx* ctx) {
                             ctx->N, k.repr_dim))
       return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the logits operands");
   }
+  // fused MLP chains (activations resident in SMEM/TMEM across layers) when the shapes fit
+  ctx->use_chain = ctx->tc_logits && !std::getenv("CRL_NO_CHAIN") && k.depth >= 1 &&
+                   tc::tc_chain_supported(k.obs_dim + k.act_dim, k.width, k.repr_dim, k.depth) &&
+                   tc::tc_chain_supported(k.goal_dim, k.width, k.repr_dim, k.depth);
+  if (ctx->use_chain) {
+    const int row_off = k.rank * k.batch_local;
+    const EncoderPlan* plans[2] = {&ctx->phi_plan, &ctx->psi_plan};
+    std::vector<crl_ctx::TcLayer>* tcs[2] = {&ctx->tc_phi, &ctx->tc_psi};
+    __nv_bfloat16** Xb[2] = {ctx->phiXb, ctx->psiXb};
+    __nv_bfloat16** Zb[2] = {ctx->phiZb, ctx->psiZb};
+    __nv_bfloat16** dzb[2] = {ctx->dzb_phi, ctx->dzb_psi};
+    __nv_bfloat16* Yb[2] = {ctx->phi_outb, ctx->psi_outb};
+    float* Yf[2] = {ctx->phi_out, ctx->psi_out};
+    float* stat[2] = {ctx->stat_phi + row_off, ctx->stat_psi + row_off};
+    tc::ChainParams& F = ctx->chain_fwd_p;
+    tc::ChainParams& Bw = ctx->chain_bwd_p;
+    F.M = Bw.M = k.batch_local;
+    F.act = Bw.act = k.activation;
+    F.energy = Bw.energy = k.energy;
+    F.fac_ok = ctx->fac_ok;
+    F.fac_init = std::getenv("CRL_FORCE_EXACT_Q") ? 0 : 1;
+    Bw.fac_ok = nullptr;
+    for (int e = 0; e < 2; ++e) {
+      const EncoderPlan& P = *plans[e];
+      const int L = P.n_layers;
+      auto& T = *tcs[e];
+      tc::ChainEnc& fe = F.enc[e];
+      tc::ChainEnc& be = Bw.enc[e];
+      fe.L = L;
+      fe.out_stat = stat[e];
+      ctx->chain_fwd[e].a0 = T[0].fwdA;
+      for (int l = 0; l < L; ++l) {
+        const LayerPlan& Lp = P.layer[l];
+        tc::ChainLayer& cl = fe.layer[l];
+        cl.K = Lp.in; cl.N = Lp.out;
+        cl.bias = ctx->mem.params + Lp.b_off;
+        cl.out_act = (l < L - 1) ? Xb[e][l + 1] : Yb[e];
+        cl.out_z = (l < L - 1) ? Zb[e][l] : nullptr;
+        cl.out_f = (l == L - 1) ? Yf[e] : nullptr;
+        ctx->chain_fwd[e].w[l] = T[l].fwdB;
+      }
+      be.L = L - 1;
+      be.out_stat = nullptr;
+      ctx->chain_bwd[e].a0 = T[L - 1].dxA;                 // dY, K-major box {64, 128}
+      for (int s2 = 0; s2 < L - 1; ++s2) {
+        const int l = L - 1 - s2;
+        const LayerPlan& Lp = P.layer[l];
+        tc::ChainLayer& cl = be.layer[s2];
+        cl.K = Lp.out; cl.N = Lp.in;
+        cl.out_act = dzb[e][l - 1];
+        cl.zprev = Zb[e][l - 1];
+        if (!tc::make_map_bf16(&ctx->chain_bwd[e].w[s2], ctx->wshadow + Lp.w_off, Lp.out, Lp.in, Lp.out, 64,
+                               Lp.in))
+          return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the chain weights");
+      }
+    }
+  }
   // initial bf16 shadow of the caller's parameters; zero the padded input rows
   CU(tc::launch_f32_to_bf16(ctx->mem.params, ctx->wshadow, ctx->sizes.n_params, ctx->num_sms, 0));
   CU(cudaMemset(ctx->x0_phi, 0, (size_t)k.batch_local * ctx->ld0_phi * 2));
@@ -153,6 +210,28 @@ static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const Encoder
   return CRL_OK;
 }
 
+// dW_l and db_l of every layer (after the fused dX chain wrote all dZ_l), on one stream
+static crl_status enc_weight_grads_bf16(crl_ctx* ctx, const char* tag, const EncoderPlan& P,
+                                        std::vector<crl_ctx::TcLayer>& T, cudaStream_t st, int* nl) {
+  const int Bl = ctx->cfg.batch_local;
+  for (int l = P.n_layers - 1; l >= 0; --l) {
+    const LayerPlan& Lp = P.layer[l];
+    {
+      Stage sg(ctx, st, std::string(tag) + "_bwd_dw_l" + std::to_string(l));
+      CU(tc::tc_backward_dw(T[l].bn_dw, T[l].dwA, T[l].dwB, Bl, Lp.in, Lp.out, ctx->grads + Lp.w_off,
+                            ctx->dw_splits, ctx->sizes.n_params, st));
+      ++*nl;
+    }
+    {
+      Stage sg(ctx, st, std::string(tag) + "_bwd_db_l" + std::to_string(l));
+      CU(tc::launch_colsum_bf16(T[l].dz, Bl, Lp.out, Lp.out, ctx->grads + Lp.b_off, ctx->dw_splits,
+                                ctx->sizes.n_params, st));
+      ++*nl;
+    }
+  }
+  return CRL_OK;
+}
+
 static void fork2(crl_ctx* ctx, cudaStream_t s0, cudaStream_t s1) {
   if (s0 == s1) return;
   cudaEventRecord(ctx->ev_fork, s0);
@@ -179,19 +258,26 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                               ctx->x0_psi, ctx->ld0_psi, ctx->num_sms, st));
     ++nl;
   }
-  fork2(ctx, st, st2);
-  rs = enc_forward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiXb, ctx->psiZb, ctx->psi_out,
-                        ctx->psi_outb, st2, &nl);
-  if (rs != CRL_OK) return rs;
-  rs = enc_forward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiXb, ctx->phiZb, ctx->phi_out,
-                        ctx->phi_outb, st, &nl);
-  if (rs != CRL_OK) return rs;
-  join2(ctx, st, st2);
+  if (ctx->use_chain) {
+    // both encoders, every layer, one launch; also emits the row statistics of Y
+    Stage sg(ctx, st, "mlp_fwd_chain");
+    CU(tc::tc_chain_forward(ctx->chain_fwd[0], ctx->chain_fwd[1], ctx->chain_fwd_p, st));
+    ++nl;
+  } else {
+    fork2(ctx, st, st2);
+    rs = enc_forward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiXb, ctx->psiZb, ctx->psi_out,
+                          ctx->psi_outb, st2, &nl);
+    if (rs != CRL_OK) return rs;
+    rs = enc_forward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiXb, ctx->phiZb, ctx->phi_out,
+                          ctx->phi_outb, st, &nl);
+    if (rs != CRL_OK) return rs;
+    join2(ctx, st, st2);
+  }
   const int row_off = k.rank * Bl;
   const int S = ctx->lg_splits;
   if (ctx->tc_logits) {
     // per-row |x|^2 (L2) / 1/|x| (cos) of the bf16-rounded representations
-    { Stage sg(ctx, st, "rowstat");
+    if (!ctx->use_chain) { Stage sg(ctx, st, "rowstat");
       const int fac_init = std::getenv("CRL_FORCE_EXACT_Q") ? 0 : 1;
       CU(tc::launch_rowstat_bf16(ctx->phi_outb, Bl, D, k.energy, ctx->stat_phi + row_off, ctx->fac_ok, fac_init,
                                  st));
@@ -269,8 +355,10 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     nl += 2; }
   cudaStream_t side = (st == st2) ? st : ctx->cap_stream3;      // phi weight gradients
   cudaStream_t side2 = (st == st2) ? st : ctx->cap_stream4;     // psi weight gradients
-  rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side2, &nl);
-  if (rs != CRL_OK) return rs;
+  if (!ctx->use_chain) {
+    rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side2, &nl);
+    if (rs != CRL_OK) return rs;
+  }
   { Stage sg(ctx, st, "grad_phi");
     if (ctx->tc_logits) {
       CU(tc::tc_logits_grad(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, row_off, ctx->stat_phi + row_off,
@@ -284,9 +372,25 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(tc::launch_f32_to_bf16(ctx->dphi, ctx->dphib, (size_t)Bl * D, ctx->num_sms, st));
     }
     nl += 2; }
-  rs = enc_backward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiZb, st, side, &nl);
-  if (rs != CRL_OK) return rs;
-  join2(ctx, st, st2);
+  if (!ctx->use_chain) {
+    rs = enc_backward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiZb, st, side, &nl);
+    if (rs != CRL_OK) return rs;
+    join2(ctx, st, st2);
+  } else {
+    join2(ctx, st, st2);
+    { Stage sg(ctx, st, "mlp_bwd_chain");          // both encoders' dX chains, one launch
+      CU(tc::tc_chain_backward(ctx->chain_bwd[0], ctx->chain_bwd[1], ctx->chain_bwd_p, st));
+      ++nl; }
+    if (side != st) {
+      cudaEventRecord(ctx->ev_side, st);
+      cudaStreamWaitEvent(side, ctx->ev_side, 0);
+      cudaStreamWaitEvent(side2, ctx->ev_side, 0);
+    }
+    rs = enc_weight_grads_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, side, &nl);
+    if (rs != CRL_OK) return rs;
+    rs = enc_weight_grads_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, side2, &nl);
+    if (rs != CRL_OK) return rs;
+  }
   if (side != st) {
     cudaEventRecord(ctx->ev_side, side);
     cudaStreamWaitEvent(st, ctx->ev_side, 0);
