@@ -145,6 +145,18 @@ def stage_work(stage, cfg, N, Bl):
     if stage in ("grad_phi", "grad_psi"):
         # the two backward contractions (W Psi and W^T Phi): 2 N^2 D each, one per launch
         return 2.0 * Bl * N * D, "flop", "alu"
+    if stage in ("mlp_fwd_chain", "mlp_bwd_chain"):
+        # fused chains: every layer of both encoders (forward), every dX step (backward)
+        tot = 0.0
+        for ind in (in_phi, in_psi):
+            d = dims(ind)
+            rng = range(len(d) - 1) if stage == "mlp_fwd_chain" else range(1, len(d) - 1)
+            tot += sum(2.0 * Bl * d[l] * d[l + 1] for l in rng)
+        return tot, "flop", "tensor"
+    if stage == "rowstat":
+        return float(2 * Bl * D * 2), "byte", "hbm"
+    if stage == "prep_inputs":
+        return float(Bl * (in_phi + in_psi) * 6), "byte", "hbm"
     if "_bwd_db_" in stage:
         out = D if stage.endswith(f"_l{depth}") else Wd
         return float(Bl * out * 2), "byte", "hbm"
@@ -164,11 +176,10 @@ def stage_work(stage, cfg, N, Bl):
 
 
 def roofline(stages, cfg, N, Bl, peaks, peak_kind, clocks, traffic_db):
-    name, (ms, cnt) = max(stages.items(), key=lambda kv: kv[1][0])
+    known = {k: v for k, v in stages.items() if stage_work(k, cfg, N, Bl)[0] is not None}
+    name, (ms, cnt) = max(known.items(), key=lambda kv: kv[1][0])
     per_launch_ms = ms / cnt
     work, unit, bound = stage_work(name, cfg, N, Bl)
-    if work is None:
-        return {"kernel": name, "bound": None}
     if bound == "hbm":
         achieved = work / (per_launch_ms * 1e-3) / 1e9
         peak = peaks["hbm_gbs"]

@@ -6,8 +6,11 @@
 // One CTA owns 128 rows of the batch and runs EVERY layer of one encoder (blockIdx.y picks
 // phi or psi, so both encoders run in one launch).  Activations never leave the SM between
 // layers: layer l's epilogue writes its bf16 output straight into the SMEM operand buffer
-// (SW128 K-major) that layer l+1's tcgen05.mma reads; the accumulator lives in TMEM.  The
-// weights stream through a 3-stage TMA ring that runs ahead across layer boundaries.
+// (SW128 K-major, one 16 KB chunk per 64 features) that layer l+1's tcgen05.mma reads.
+// Pipelining: the TMEM accumulator is double-buffered and every 64-feature chunk is handed
+// to the MMA warp as soon as it is written (act_ready[c]), so layer l+1's MMAs overlap layer
+// l's epilogue; two epilogue warpgroups split the columns of each layer; the weights stream
+// through a 3-stage TMA ring that runs ahead across layer boundaries.
 //   FWD : Z_l = X_l W_l + b_l, X_{l+1} = SiLU(Z_l) (Z_l, X_{l+1} also stored for backward);
 //         output Y (fp32 + bf16) and the per-row statistic of the bf16 Y used by the logits
 //         stage (L2: |y|^2, cos: 1/max(|y|, eps)).
@@ -40,7 +43,7 @@ __device__ __forceinline__ uint32_t ch_sw128(int r, int k) {
 }
 
 template <int MODE>   // 0 = forward, 1 = backward dX chain
-__global__ void __launch_bounds__(256, 1) tc_chain_kernel(const __grid_constant__ ChainMaps maps0,
+__global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant__ ChainMaps maps0,
                                                           const __grid_constant__ ChainMaps maps1,
                                                           const ChainParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -52,9 +55,9 @@ __global__ void __launch_bounds__(256, 1) tc_chain_kernel(const __grid_constant_
   uint64_t* a0_full = bars;
   uint64_t* w_full = bars + 1;
   uint64_t* w_empty = w_full + CH_STAGES;
-  uint64_t* acc_full = w_empty + CH_STAGES;
-  uint64_t* act_ready = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + 1);
+  uint64_t* acc_full = w_empty + CH_STAGES;           // [2] per TMEM buffer
+  uint64_t* act_ready = acc_full + 2;                 // [CH_ACT_CHUNKS] per 64-feature chunk
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + CH_ACT_CHUNKS);
 
   const int enc = blockIdx.y;
   const ChainMaps& mp = enc ? maps1 : maps0;
@@ -67,11 +70,12 @@ __global__ void __launch_bounds__(256, 1) tc_chain_kernel(const __grid_constant_
     tma_prefetch_desc(&mp.a0);
     mbar_init(a0_full, 1);
     for (int s = 0; s < CH_STAGES; ++s) { mbar_init(&w_full[s], 1); mbar_init(&w_empty[s], 1); }
-    mbar_init(acc_full, 1);
-    mbar_init(act_ready, 4);
+    mbar_init(&acc_full[0], 1);
+    mbar_init(&acc_full[1], 1);
+    for (int c = 0; c < CH_ACT_CHUNKS; ++c) mbar_init(&act_ready[c], 4);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 256);
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -109,12 +113,12 @@ __global__ void __launch_bounds__(256, 1) tc_chain_kernel(const __grid_constant_
     int g = 0;
     for (int l = 0; l < L; ++l) {
       const ChainLayer& Ly = E.layer[l];
-      if (l == 0) mbar_wait(a0_full, 0);
-      else mbar_wait(act_ready, (l - 1) & 1);
-      tc_fence_after();
+      const uint32_t acc = tmem + (uint32_t)((l & 1) * 256);
       const uint32_t idesc = idesc_bf16_f32(128, Ly.N, false, MODE == 0);
       const int nkb = (Ly.K + 63) / 64;
+      if (l == 0) mbar_wait(a0_full, 0);
       for (int kb = 0; kb < nkb; ++kb, ++g) {
+        if (l > 0) mbar_wait(&act_ready[kb], (l - 1) & 1);   // chunk kb of this layer's input
         const int s = g % CH_STAGES;
         mbar_wait(&w_full[s], (g / CH_STAGES) & 1);
         tc_fence_after();
@@ -124,42 +128,49 @@ __global__ void __launch_bounds__(256, 1) tc_chain_kernel(const __grid_constant_
           const uint64_t ad = smem_desc_sw128(act_base + kb * CH_CHUNK + ks * 32, 16, 1024);
           const uint64_t bd = MODE == 0 ? smem_desc_sw128(wb + ks * 2048, 8192, 1024)
                                         : smem_desc_sw128(wb + ks * 32, 16, 1024);
-          mma_bf16(tmem, ad, bd, idesc, (kb | ks) != 0);
+          mma_bf16(acc, ad, bd, idesc, (kb | ks) != 0);
         }
         mma_commit(&w_empty[s]);
       }
-      mma_commit(acc_full);
+      mma_commit(&acc_full[l & 1]);
     }
   } else if (warp >= 4) {
-    // -------------------------------------------------------------------- epilogue
-    const int q = warp - 4;
+    // -------------------------------------------------------------------- epilogue (2 warpgroups)
+    const int wg = (warp - 4) >> 2;
+    const int q = warp & 3;
     const int r = q * 32 + lane;
     const int row = m0 + r;
     const bool rv = row < p.M;
     if (MODE == 0) {                                   // all biases of this encoder -> SMEM
       for (int l = 0; l < L; ++l)
-        for (int c = threadIdx.x - 128; c < E.layer[l].N; c += 128) sBias[l * 256 + c] = E.layer[l].bias[c];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int c = threadIdx.x - 128; c < E.layer[l].N; c += 256) sBias[l * 256 + c] = E.layer[l].bias[c];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
     }
     float stat = 0.f;
     for (int l = 0; l < L; ++l) {
       const ChainLayer& Ly = E.layer[l];
       const bool last = l == L - 1;
       const int N = Ly.N;
-      uint4 zp[32];                                    // BWD: Z_{l-1} row, fetched during the MMA
+      const int nch = N / 64;
+      const uint32_t acc = tmem + (uint32_t)((l & 1) * 256);
+      // this warpgroup's column range
+      const int cbeg = (nch == 1) ? (wg == 0 ? 0 : N) : (wg == 0 ? 0 : (nch + 1) / 2 * 64);
+      const int cend = (nch == 1) ? (wg == 0 ? N : N) : (wg == 0 ? (nch + 1) / 2 * 64 : N);
+      uint4 zp[16];                                    // BWD: this half of the Z_{l-1} row
       if (MODE == 1 && rv) {
-        const uint4* zr = reinterpret_cast<const uint4*>(Ly.zprev + (size_t)row * N);
+        const uint4* zr = reinterpret_cast<const uint4*>(Ly.zprev + (size_t)row * N + cbeg);
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (8 * j < N) zp[j] = zr[j];
+        for (int j = 0; j < 16; ++j)
+          if (cbeg + 8 * j < cend) zp[j] = zr[j];
       }
-      mbar_wait(acc_full, l & 1);
+      mbar_wait(&acc_full[l & 1], (l >> 1) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < 256; c0 += 32) {         // fully unrolled: zp[] stays in registers
-        if (c0 >= N) break;
+      for (int cc = 0; cc < 128; cc += 32) {           // at most 128 columns per warpgroup
+        const int c0 = cbeg + cc;
+        if (c0 >= cend) break;
         uint32_t raw[32];
-        tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + c0, raw);
+        tmem_ld32_nowait(acc + ((uint32_t)(q * 32) << 16) + c0, raw);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(256, 1) tc_chain_kernel(const __grid_constant_
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const uint32_t zw = reinterpret_cast<const uint32_t*>(zp)[(c0 >> 1) + i];
+            const uint32_t zw = reinterpret_cast<const uint32_t*>(zp)[(cc >> 1) + i];
             const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zw));
             float g0, g1;
             if (p.act == CRL_ACT_SILU) {
@@ -225,8 +236,8 @@ __global__ void __launch_bounds__(256, 1) tc_chain_kernel(const __grid_constant_
             for (int u = 0; u < 4; ++u) o[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
           }
         }
-        // next step's A operand: bf16 into the SW128 K-major SMEM buffer (rows >= M write 0s)
         if (!(MODE == 0 && last)) {
+          // next step's A operand: bf16 into the SW128 K-major SMEM chunk (rows >= M write 0s)
           uint8_t* ch = sAct + (c0 >> 6) * CH_CHUNK;
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -234,27 +245,38 @@ __global__ void __launch_bounds__(256, 1) tc_chain_kernel(const __grid_constant_
                                  : make_uint4(0u, 0u, 0u, 0u);
             *reinterpret_cast<uint4*>(ch + ch_sw128(r, (c0 & 63) + 8 * u)) = val;
           }
+          if (((c0 + 32) & 63) == 0 && l + 1 < L) {    // a full 64-feature chunk is written
+            tc_fence_before();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&act_ready[c0 >> 6]);
+          }
         }
       }
-      tc_fence_before();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(act_ready);
     }
-    if (MODE == 0 && rv && E.out_stat != nullptr)
-      E.out_stat[row] = p.energy == CRL_ENERGY_L2 ? stat
-                        : (p.energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(stat), kEpsCos) : 0.f);
+    if (MODE == 0) {
+      // row statistic of Y: warpgroup 1 hands its columns' partial sum to warpgroup 0
+      float* sStat = sBias;                            // biases are no longer needed
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (wg == 1) sStat[r] = stat;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (wg == 0 && rv && E.out_stat != nullptr) {
+        const float st = stat + sStat[r];
+        E.out_stat[row] = p.energy == CRL_ENERGY_L2 ? st
+                          : (p.energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(st), kEpsCos) : 0.f);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 512);
   }
 }
 
 size_t tc_chain_smem() {
-  return 1024 + CH_ACT_CHUNKS * CH_CHUNK + CH_STAGES * CH_WSTAGE + CH_BIAS * 4 + 128;
+  return 1024 + CH_ACT_CHUNKS * CH_CHUNK + CH_STAGES * CH_WSTAGE + CH_BIAS * 4 + 256;
 }
 
 bool tc_chain_supported(int in0, int width, int D, int depth) {
@@ -274,7 +296,7 @@ static cudaError_t launch_chain(const ChainMaps& m0, const ChainMaps& m1, const 
     attr = true;
   }
   dim3 grid((p.M + 127) / 128, nenc);
-  return launch_pdl(tc_chain_kernel<MODE>, grid, dim3(256), smem, st, m0, m1, p);
+  return launch_pdl(tc_chain_kernel<MODE>, grid, dim3(384), smem, st, m0, m1, p);
 }
 
 cudaError_t tc_chain_forward(const ChainMaps& m0, const ChainMaps& m1, const ChainParams& p, cudaStream_t st) {
