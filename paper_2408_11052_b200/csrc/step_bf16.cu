@@ -115,6 +115,7 @@ crl_status bf16_prepare(crl_ctx* ctx) {
     F.energy = Bw.energy = k.energy;
     F.fac_ok = ctx->fac_ok;
     F.fac_init = std::getenv("CRL_FORCE_EXACT_Q") ? 0 : 1;
+    F.dbg = Bw.dbg = std::getenv("CRL_CHAIN_DBG") ? std::atoi(std::getenv("CRL_CHAIN_DBG")) : 0;
     Bw.fac_ok = nullptr;
     for (int e = 0; e < 2; ++e) {
       const EncoderPlan& P = *plans[e];
@@ -134,6 +135,13 @@ crl_status bf16_prepare(crl_ctx* ctx) {
         cl.out_z = (l < L - 1) ? Zb[e][l] : nullptr;
         cl.out_f = (l == L - 1) ? Yf[e] : nullptr;
         ctx->chain_fwd[e].w[l] = T[l].fwdB;
+        // TMA-store targets: whole 128 x 64 chunks straight from the kernel's SW128 SMEM buffers
+        bool ok = tc::make_map_bf16(&ctx->chain_fwd[e].st_out[l], cl.out_act, Lp.out, k.batch_local, Lp.out, 64,
+                                    128);
+        if (l < L - 1)
+          ok = ok && tc::make_map_bf16(&ctx->chain_fwd[e].st_z[l], cl.out_z, Lp.out, k.batch_local, Lp.out, 64,
+                                       128);
+        if (!ok) return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the chain outputs");
       }
       be.L = L - 1;
       be.out_stat = nullptr;
@@ -146,7 +154,8 @@ crl_status bf16_prepare(crl_ctx* ctx) {
         cl.out_act = dzb[e][l - 1];
         cl.zprev = Zb[e][l - 1];
         if (!tc::make_map_bf16(&ctx->chain_bwd[e].w[s2], ctx->wshadow + Lp.w_off, Lp.out, Lp.in, Lp.out, 64,
-                               Lp.in))
+                               Lp.in) ||
+            !tc::make_map_bf16(&ctx->chain_bwd[e].st_out[s2], cl.out_act, Lp.in, k.batch_local, Lp.in, 64, 128))
           return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the chain weights");
       }
     }

@@ -6,18 +6,22 @@
 // One CTA owns 128 rows of the batch and runs EVERY layer of one encoder (blockIdx.y picks
 // phi or psi, so both encoders run in one launch).  Activations never leave the SM between
 // layers: layer l's epilogue writes its bf16 output straight into the SMEM operand buffer
-// (SW128 K-major, one 16 KB chunk per 64 features) that layer l+1's tcgen05.mma reads.
-// Pipelining: the TMEM accumulator is double-buffered and every 64-feature chunk is handed
-// to the MMA warp as soon as it is written (act_ready[c]), so layer l+1's MMAs overlap layer
-// l's epilogue; two epilogue warpgroups split the columns of each layer; the weights stream
-// through a 3-stage TMA ring that runs ahead across layer boundaries.
-//   FWD : Z_l = X_l W_l + b_l, X_{l+1} = SiLU(Z_l) (Z_l, X_{l+1} also stored for backward);
+// (SW128 K-major, one 16 KB chunk per 64 features) that layer l+1's tcgen05.mma reads, and
+// the same SMEM chunk is written to HBM by one TMA bulk-tensor store (the activations are
+// needed again by the backward pass) — coalesced and asynchronous, instead of row-per-thread
+// global stores.  Pipelining: the TMEM accumulator is double-buffered and every 64-feature
+// chunk is handed to the MMA warp as soon as it is written (act_ready[c]), so layer l+1's
+// MMAs overlap layer l's epilogue; two epilogue warpgroups split the columns; the weights
+// stream through a TMA ring that runs ahead across layer boundaries.
+//   FWD : Z_l = X_l W_l + b_l, X_{l+1} = SiLU(Z_l) (Z_l, X_{l+1} stored for backward);
 //         output Y (fp32 + bf16) and the per-row statistic of the bf16 Y used by the logits
 //         stage (L2: |y|^2, cos: 1/max(|y|, eps)).
 //   BWD : dZ_{l-1} = (dZ_l W_l^T) * SiLU'(Z_{l-1}) for l = L-1 .. 1, starting from dY;
 //         every dZ is stored for the dW / db reductions.
 // SiLU uses sigmoid(z) = (1 + tanh(z/2)) / 2 with the tanh.approx MUFU op (one MUFU op per
 // element instead of exp + reciprocal); the path's tolerance is 2e-2 (north_star).
+#include <cstdio>
+
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_chain.h"
@@ -25,8 +29,9 @@
 namespace crl {
 namespace tc {
 
-constexpr int CH_STAGES = 3;
+constexpr int CH_STAGES = 2;
 constexpr int CH_ACT_CHUNKS = 5;                  // K <= 320
+constexpr int CH_STG_CHUNKS = 4;                  // Z_l / Y staging for the TMA stores
 constexpr uint32_t CH_CHUNK = 128 * 128;          // 128 rows x 64 bf16 (one SW128 K chunk)
 constexpr uint32_t CH_WSTAGE = 64 * 256 * 2;      // 64 K rows x up to 256 N
 constexpr int CH_BIAS = kChainMaxL * 256;
@@ -36,10 +41,83 @@ __device__ __forceinline__ float tanh_approx(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float sig_fast(float z) { return fmaf(0.5f, tanh_approx(0.5f * z), 0.5f); }
 
-__device__ __forceinline__ uint32_t ch_sw128(int r, int k) {
-  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2);
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void wg_sync(int wg) { asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory"); }
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+// silu(z) = z sigmoid(z) = h + h tanh(h), h = z/2
+__device__ __forceinline__ float silu_fast(float z) {
+  const float h = 0.5f * z;
+  return fmaf(h, tanh_approx(h), h);
+}
+// silu'(z) = s (1 + z (1 - s)) = 1/2 + (t + h (1 - t^2)) / 2, t = tanh(h), h = z/2
+__device__ __forceinline__ float silu_grad_fast(float z) {
+  const float h = 0.5f * z;
+  const float t = tanh_approx(h);
+  return fmaf(0.5f, fmaf(h, fmaf(-t, t, 1.f), t), 0.5f);
+}
+// FWD hidden layer: Z = acc + b (bf16 pairs zk), X' = act(Z) (bf16 pairs pk)
+template <bool SILU>
+__device__ __forceinline__ void epi_fwd_hidden(uint32_t* raw, uint32_t bias_a, uint32_t* pk, uint32_t* zk) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float4 b = lds128f(bias_a + 16u * j);
+    const float z0 = __uint_as_float(raw[4 * j]) + b.x, z1 = __uint_as_float(raw[4 * j + 1]) + b.y;
+    const float z2 = __uint_as_float(raw[4 * j + 2]) + b.z, z3 = __uint_as_float(raw[4 * j + 3]) + b.w;
+    zk[2 * j] = pack_bf16x2(z0, z1);
+    zk[2 * j + 1] = pack_bf16x2(z2, z3);
+    if (SILU) {
+      pk[2 * j] = pack_bf16x2(silu_fast(z0), silu_fast(z1));
+      pk[2 * j + 1] = pack_bf16x2(silu_fast(z2), silu_fast(z3));
+    } else {
+      pk[2 * j] = pack_bf16x2(fmaxf(z0, 0.f), fmaxf(z1, 0.f));
+      pk[2 * j + 1] = pack_bf16x2(fmaxf(z2, 0.f), fmaxf(z3, 0.f));
+    }
+  }
+}
+// FWD output layer: Y = acc + b (fp32 back into raw, bf16 pairs pk); returns sum of bf16(Y)^2
+__device__ __forceinline__ float epi_fwd_last(uint32_t* raw, uint32_t bias_a, uint32_t* pk) {
+  float st = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float4 b = lds128f(bias_a + 16u * j);
+    const float y0 = __uint_as_float(raw[4 * j]) + b.x, y1 = __uint_as_float(raw[4 * j + 1]) + b.y;
+    const float y2 = __uint_as_float(raw[4 * j + 2]) + b.z, y3 = __uint_as_float(raw[4 * j + 3]) + b.w;
+    raw[4 * j] = __float_as_uint(y0); raw[4 * j + 1] = __float_as_uint(y1);
+    raw[4 * j + 2] = __float_as_uint(y2); raw[4 * j + 3] = __float_as_uint(y3);
+    pk[2 * j] = pack_bf16x2(y0, y1);
+    pk[2 * j + 1] = pack_bf16x2(y2, y3);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[2 * j]));
+    const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[2 * j + 1]));
+    st = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(c.x, c.x, fmaf(c.y, c.y, st))));
+  }
+  return st;
+}
+// BWD: dZ_{l-1} = acc * act'(Z_{l-1})
+template <bool SILU>
+__device__ __forceinline__ void epi_bwd(const uint32_t* raw, const uint32_t* zw, uint32_t* pk) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zw[i]));
+    const float g0 = SILU ? silu_grad_fast(z.x) : (z.x > 0.f ? 1.f : 0.f);
+    const float g1 = SILU ? silu_grad_fast(z.y) : (z.y > 0.f ? 1.f : 0.f);
+    pk[i] = pack_bf16x2(__uint_as_float(raw[2 * i]) * g0, __uint_as_float(raw[2 * i + 1]) * g1);
+  }
 }
 
 template <int MODE>   // 0 = forward, 1 = backward dX chain
@@ -49,7 +127,8 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAct = smem;
-  uint8_t* sW = sAct + CH_ACT_CHUNKS * CH_CHUNK;
+  uint8_t* sStg = sAct + CH_ACT_CHUNKS * CH_CHUNK;
+  uint8_t* sW = sStg + CH_STG_CHUNKS * CH_CHUNK;
   float* sBias = reinterpret_cast<float*>(sW + CH_STAGES * CH_WSTAGE);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + CH_BIAS);
   uint64_t* a0_full = bars;
@@ -65,6 +144,10 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * 128;
   const int L = E.L;
+  // dbg & 4: clock64 trace of CTA (0,0) printed at exit (measurement only)
+  __shared__ long long s_tr[64];
+  const bool trace = (p.dbg & 4) && blockIdx.x == 0 && blockIdx.y == 0;
+#define CH_TR(i) do { if (trace) s_tr[(i)] = clock64(); } while (0)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mp.a0);
@@ -82,6 +165,7 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_launch();
+  if (threadIdx.x == 0) CH_TR(0);
   if (MODE == 0 && p.fac_ok != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
     *p.fac_ok = p.fac_init;
 
@@ -98,6 +182,7 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % CH_STAGES;
         mbar_wait(&w_empty[s], ((g / CH_STAGES) & 1) ^ 1);
+        if (g < 20) CH_TR(1 + g);
         mbar_expect_tx(&w_full[s], bytes);
         uint8_t* dst = sW + s * CH_WSTAGE;
         if (MODE == 0) {
@@ -121,6 +206,7 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
         if (l > 0) mbar_wait(&act_ready[kb], (l - 1) & 1);   // chunk kb of this layer's input
         const int s = g % CH_STAGES;
         mbar_wait(&w_full[s], (g / CH_STAGES) & 1);
+        if (g < 20) CH_TR(21 + g);
         tc_fence_after();
         const uint32_t wb = smem_u32(sW + s * CH_WSTAGE);
 #pragma unroll
@@ -141,6 +227,8 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
     const int r = q * 32 + lane;
     const int row = m0 + r;
     const bool rv = row < p.M;
+    const bool storer = (q == 0 && lane == 0);          // issues this warpgroup's TMA stores
+    const bool st_ok = !(p.dbg & 1);
     if (MODE == 0) {                                   // all biases of this encoder -> SMEM
       for (int l = 0; l < L; ++l)
         for (int c = threadIdx.x - 128; c < E.layer[l].N; c += 256) sBias[l * 256 + c] = E.layer[l].bias[c];
@@ -153,107 +241,91 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
       const int N = Ly.N;
       const int nch = N / 64;
       const uint32_t acc = tmem + (uint32_t)((l & 1) * 256);
-      // this warpgroup's column range
-      const int cbeg = (nch == 1) ? (wg == 0 ? 0 : N) : (wg == 0 ? 0 : (nch + 1) / 2 * 64);
-      const int cend = (nch == 1) ? (wg == 0 ? N : N) : (wg == 0 ? (nch + 1) / 2 * 64 : N);
-      uint4 zp[16];                                    // BWD: this half of the Z_{l-1} row
+      // this warpgroup's 64-feature chunks
+      const int cb = (nch == 1) ? (wg == 0 ? 0 : 1) : (wg == 0 ? 0 : (nch + 1) / 2);
+      const int ce = (nch == 1) ? 1 : (wg == 0 ? (nch + 1) / 2 : nch);
+      uint4 zp[16];                                    // BWD: this warpgroup's part of the Z_{l-1} row
       if (MODE == 1 && rv) {
-        const uint4* zr = reinterpret_cast<const uint4*>(Ly.zprev + (size_t)row * N + cbeg);
+        const uint4* zr = reinterpret_cast<const uint4*>(Ly.zprev + (size_t)row * N + cb * 64);
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (cbeg + 8 * j < cend) zp[j] = zr[j];
+          if (cb * 64 + 8 * j < ce * 64) zp[j] = zr[j];
       }
       mbar_wait(&acc_full[l & 1], (l >> 1) & 1);
+      if (storer && l < 5) CH_TR(42 + 5 * wg + l);
       tc_fence_after();
+      // SMEM chunks are about to be rewritten: the previous layer's TMA stores (of either
+      // warpgroup: the chunk split changes with N) must have read them
+      if (storer) bulk_wait_read();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
 #pragma unroll
-      for (int cc = 0; cc < 128; cc += 32) {           // at most 128 columns per warpgroup
-        const int c0 = cbeg + cc;
-        if (c0 >= cend) break;
-        uint32_t raw[32];
-        tmem_ld32_nowait(acc + ((uint32_t)(q * 32) << 16) + c0, raw);
+      for (int cc = 0; cc < 2; ++cc) {                 // at most 2 chunks (128 features) per warpgroup
+        const int c = cb + cc;
+        if (c >= ce) break;
+        uint32_t raw[64];
+        tmem_ld32_nowait(acc + ((uint32_t)(q * 32) << 16) + 64 * c, *reinterpret_cast<uint32_t(*)[32]>(raw));
+        tmem_ld32_nowait(acc + ((uint32_t)(q * 32) << 16) + 64 * c + 32,
+                         *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
         tmem_ld_wait();
-        float v[32];
+        if (storer && wg == 0 && l == 1) CH_TR(58 + 3 * cc);
+        uint32_t pk[32];                               // bf16 pairs of the value feeding the next step
+        // (branch-free specialised loops: a per-element branch on `last` / the activation
+        // serialises the MUFU latency of every element)
+        const uint32_t bias_a = smem_u32(sBias) + (uint32_t)(l * 256 + 64 * c) * 4u;
+        const uint32_t row_a = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+        const uint32_t act_a = smem_u32(((MODE == 0 && last) ? sStg : sAct) + c * CH_CHUNK) + row_a;
+        if (MODE == 0 && !last) {
+          uint32_t zk[32];                             // bf16 pairs of Z
+          if (p.act == CRL_ACT_SILU) epi_fwd_hidden<true>(raw, bias_a, pk, zk);
+          else epi_fwd_hidden<false>(raw, bias_a, pk, zk);
+          const uint32_t z_a = smem_u32(sStg + c * CH_CHUNK) + row_a;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
-        uint32_t pk[16];                               // bf16 pairs of the value written on
-        if (MODE == 0) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += sBias[l * 256 + c0 + i];
-          if (!last) {
-            uint32_t zk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              zk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-              float a0 = v[2 * i], a1 = v[2 * i + 1];
-              a0 = p.act == CRL_ACT_SILU ? a0 * sig_fast(a0) : fmaxf(a0, 0.f);
-              a1 = p.act == CRL_ACT_SILU ? a1 * sig_fast(a1) : fmaxf(a1, 0.f);
-              pk[i] = pack_bf16x2(a0, a1);
-            }
-            if (rv) {
-              uint4* zo = reinterpret_cast<uint4*>(Ly.out_z + (size_t)row * N + c0);
-              uint4* xo = reinterpret_cast<uint4*>(Ly.out_act + (size_t)row * N + c0);
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                zo[u] = make_uint4(zk[4 * u], zk[4 * u + 1], zk[4 * u + 2], zk[4 * u + 3]);
-                xo[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-              const float2 yb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[i]));
-              stat = fmaf(yb.x, yb.x, fmaf(yb.y, yb.y, stat));
-            }
-            if (rv) {
-              float4* yo = reinterpret_cast<float4*>(Ly.out_f + (size_t)row * N + c0);
-#pragma unroll
-              for (int u = 0; u < 8; ++u) yo[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-              uint4* xo = reinterpret_cast<uint4*>(Ly.out_act + (size_t)row * N + c0);
-#pragma unroll
-              for (int u = 0; u < 4; ++u) xo[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-            }
-          }
+          for (int u = 0; u < 8; ++u)
+            sts128(z_a + (uint32_t)((u ^ (r & 7)) << 4), make_uint4(zk[4 * u], zk[4 * u + 1], zk[4 * u + 2], zk[4 * u + 3]));
+        } else if (MODE == 0) {
+          stat += epi_fwd_last(raw, bias_a, pk);
         } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint32_t zw = reinterpret_cast<const uint32_t*>(zp)[(cc >> 1) + i];
-            const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zw));
-            float g0, g1;
-            if (p.act == CRL_ACT_SILU) {
-              const float s0 = sig_fast(z.x), s1 = sig_fast(z.y);
-              g0 = s0 * fmaf(z.x, 1.f - s0, 1.f);
-              g1 = s1 * fmaf(z.y, 1.f - s1, 1.f);
-            } else {
-              g0 = z.x > 0.f ? 1.f : 0.f;
-              g1 = z.y > 0.f ? 1.f : 0.f;
-            }
-            pk[i] = pack_bf16x2(v[2 * i] * g0, v[2 * i + 1] * g1);
-          }
-          if (rv) {
-            uint4* o = reinterpret_cast<uint4*>(Ly.out_act + (size_t)row * N + c0);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) o[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-          }
+          const uint32_t* zw = reinterpret_cast<const uint32_t*>(zp) + 32 * cc;
+          if (p.act == CRL_ACT_SILU) epi_bwd<true>(raw, zw, pk);
+          else epi_bwd<false>(raw, zw, pk);
         }
-        if (!(MODE == 0 && last)) {
-          // next step's A operand: bf16 into the SW128 K-major SMEM chunk (rows >= M write 0s)
-          uint8_t* ch = sAct + (c0 >> 6) * CH_CHUNK;
+        // SMEM: pk -> the operand chunk (next step's A, also the TMA-store source); FWD hidden:
+        // Z -> the staging chunk (above); FWD last: Y bf16 -> staging, Y fp32 straight to HBM
+        if (storer && wg == 0 && l == 1) CH_TR(59 + 3 * cc);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint4 val = rv ? make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3])
-                                 : make_uint4(0u, 0u, 0u, 0u);
-            *reinterpret_cast<uint4*>(ch + ch_sw128(r, (c0 & 63) + 8 * u)) = val;
+        for (int u = 0; u < 8; ++u)
+          sts128(act_a + (uint32_t)((u ^ (r & 7)) << 4),
+                 rv ? make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]) : make_uint4(0u, 0u, 0u, 0u));
+        if (MODE == 0 && last && rv && st_ok) {
+          float4* yo = reinterpret_cast<float4*>(Ly.out_f + (size_t)row * N + 64 * c);
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            yo[u] = make_float4(__uint_as_float(raw[4 * u]), __uint_as_float(raw[4 * u + 1]),
+                                __uint_as_float(raw[4 * u + 2]), __uint_as_float(raw[4 * u + 3]));
+        }
+        tc_fence_before();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (!(MODE == 0 && last) && lane == 0) mbar_arrive(&act_ready[c]);
+        // whole 128 x 64 chunk written by the 4 warps -> one TMA store per tensor
+        wg_sync(wg);
+        if (storer && wg == 0 && l == 1) CH_TR(60 + 3 * cc);
+        if (storer && st_ok) {
+          if (MODE == 0 && !last) {
+            tma_store_2d(&mp.st_out[l], sAct + c * CH_CHUNK, 64 * c, m0);
+            tma_store_2d(&mp.st_z[l], sStg + c * CH_CHUNK, 64 * c, m0);
+          } else if (MODE == 0) {
+            tma_store_2d(&mp.st_out[l], sStg + c * CH_CHUNK, 64 * c, m0);
+          } else {
+            tma_store_2d(&mp.st_out[l], sAct + c * CH_CHUNK, 64 * c, m0);
           }
-          if (((c0 + 32) & 63) == 0 && l + 1 < L) {    // a full 64-feature chunk is written
-            tc_fence_before();
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&act_ready[c0 >> 6]);
-          }
+          bulk_commit();
         }
       }
+      if (storer && wg == 0 && l < 5) CH_TR(52 + l);
     }
+    if (storer) bulk_wait_all();
+    if (storer && wg == 0) CH_TR(57);
     if (MODE == 0) {
       // row statistic of Y: warpgroup 1 hands its columns' partial sum to warpgroup 0
       float* sStat = sBias;                            // biases are no longer needed
@@ -273,10 +345,15 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  if (trace && threadIdx.x == 0) {
+    printf("CHAIN_TRACE mode=%d L=%d\n", MODE, L);
+    for (int i = 1; i < 64; ++i) printf("CHAIN_TRACE %d %lld\n", i, s_tr[i] - s_tr[0]);
+  }
+#undef CH_TR
 }
 
 size_t tc_chain_smem() {
-  return 1024 + CH_ACT_CHUNKS * CH_CHUNK + CH_STAGES * CH_WSTAGE + CH_BIAS * 4 + 256;
+  return 1024 + (CH_ACT_CHUNKS + CH_STG_CHUNKS) * CH_CHUNK + CH_STAGES * CH_WSTAGE + CH_BIAS * 4 + 256;
 }
 
 bool tc_chain_supported(int in0, int width, int D, int depth) {

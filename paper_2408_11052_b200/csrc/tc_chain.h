@@ -24,11 +24,14 @@ struct ChainEnc {
 struct ChainMaps {
   CUtensorMap a0;                 // FWD: X0 {K0, M} box {64,128};  BWD: dY {D, M} box {64,128}
   CUtensorMap w[kChainMaxL];      // FWD: W_l MN-major {out, in} box {64,64}; BWD: K-major {out, in} box {64, in}
+  CUtensorMap st_out[kChainMaxL]; // TMA-store targets, box {64,128}: FWD X_{l+1} / Y bf16, BWD dZ_{l-1}
+  CUtensorMap st_z[kChainMaxL];   // FWD hidden: Z_l, box {64,128}
 };
 struct ChainParams {
   int M, act, energy;
   int* fac_ok;                    // FWD: re-armed to fac_init by block (0,0) (see tc_logits.cu)
   int fac_init;
+  int dbg;                        // measurement knob (CRL_CHAIN_DBG): 1 = no global stores, 2 = no epilogue math
   ChainEnc enc[2];
 };
 
