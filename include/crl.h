@@ -167,8 +167,11 @@ CRL_API crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float* a,
  *   L = mean_i(alpha_ent log pi_i - f(phi([s_i||a'_i]), psi(g_i)))   (critic frozen).
  *   s [B_l][obs_dim], g [B_l][goal_dim], eps [B_l][act_dim] ~ N(0,1): device.
  *   loss_out: device float[1] or NULL; actor_grads_out: device float[n_actor_params] or NULL;
- *   apply_adam != 0 applies one Adam step (lr_actor) to actor_params.
- * CRL_EUNSUPPORTED if the context was created without an actor. */
+ *   apply_adam != 0 applies one Adam step (lr_actor, adam_b1/b2/eps, weight_decay) to
+ *   actor_params; the step is skipped and CRL_ENONFINITE raised if the loss is non-finite.
+ * Multi-GPU: the loss is the global mean and the gradients are all-reduced (sum of 1/N terms).
+ * fp32 throughout (the critic's fp32 master parameters), launched eagerly on `stream`.
+ * CRL_EUNSUPPORTED if the context was created without an actor (actor_depth = 0). */
 CRL_API crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* g, const float* eps,
                           float alpha_ent, float* loss_out, float* actor_grads_out,
                           int apply_adam, void* stream);

@@ -175,6 +175,41 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   c->stage_s = s.take<float>((size_t)Bl * k.obs_dim);
   c->stage_a = s.take<float>((size_t)Bl * k.act_dim);
   c->stage_g = s.take<float>((size_t)Bl * k.goal_dim);
+  // actor objective (fp32): actor activations, the frozen critic's activations on [s||a'],
+  // head buffers, gradient partials
+  c->has_actor = k.actor_depth > 0 && k.actor_width > 0;
+  if (c->has_actor) {
+    const int A = k.act_dim, Wa = k.actor_width;
+    c->actor_plan = make_encoder_plan(k.obs_dim + k.goal_dim, k.actor_depth, Wa, 2 * A, 0);
+    for (int l = 1; l <= k.actor_depth; ++l) c->aX[l] = s.take<float>((size_t)Bl * Wa);
+    for (int l = 0; l < k.actor_depth; ++l) c->aZ[l] = s.take<float>((size_t)Bl * Wa);
+    c->a_out = s.take<float>((size_t)Bl * 2 * A);
+    c->a_new = s.take<float>((size_t)Bl * A);
+    c->a_logpi = s.take<float>((size_t)Bl);
+    c->a_rowloss = s.take<float>((size_t)Bl);
+    c->a_dout = s.take<float>((size_t)Bl * 2 * A);
+    c->a_da = s.take<float>((size_t)Bl * A);
+    const int wa = Wa > 2 * A ? Wa : 2 * A;
+    c->a_dz[0] = s.take<float>((size_t)Bl * wa);
+    c->a_dz[1] = s.take<float>((size_t)Bl * wa);
+    for (int l = 1; l <= k.depth; ++l) {
+      c->ac_phiX[l] = s.take<float>((size_t)Bl * Wd);
+      c->ac_psiX[l] = s.take<float>((size_t)Bl * Wd);
+    }
+    for (int l = 0; l < k.depth; ++l) {
+      c->ac_phiZ[l] = s.take<float>((size_t)Bl * Wd);
+      c->ac_psiZ[l] = s.take<float>((size_t)Bl * Wd);
+    }
+    c->ac_phi = s.take<float>((size_t)Bl * D);
+    c->ac_psi = s.take<float>((size_t)Bl * D);
+    c->ac_dphi = s.take<float>((size_t)Bl * D);
+    c->ac_dz[0] = s.take<float>((size_t)Bl * wmax);
+    c->ac_dz[1] = s.take<float>((size_t)Bl * wmax);
+    c->a_grads = s.take<float>(c->actor_plan.n_params * c->dw_splits);
+    c->a_loss = s.take<float>(4);
+    c->a_t = s.take<int>(1);
+    c->a_skip = s.take<int>(1);
+  }
   *scr_bytes = (s.off + 255) & ~(size_t)255;
 }
 
@@ -203,6 +238,10 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
   if (k->batch_local < 1 || (long long)k->batch_local * k->world_size < 2)
     return fail(ctx, CRL_EINVAL, "global batch must be >= 2 (InfoNCE needs negatives)");
   if (!(k->lr > 0.f) || !(k->adam_eps > 0.f)) return fail(ctx, CRL_EINVAL, "lr and eps must be > 0");
+  if (k->actor_depth < 0 || k->actor_depth > CRL_MAX_LAYERS - 1 || k->actor_width < 0)
+    return fail(ctx, CRL_EINVAL, "actor_depth must be in [0, 7] and actor_width >= 0");
+  if (k->actor_depth > 0 && k->actor_width > 0 && !(k->lr_actor > 0.f))
+    return fail(ctx, CRL_EINVAL, "lr_actor must be > 0");
   return CRL_OK;
 }
 
@@ -256,6 +295,9 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
     return fail(ctx, CRL_EINVAL, "buffer and scratch must be 256-byte aligned");
   if (cfg->world_size > 1 && !nccl_id)
     return fail(ctx, CRL_EINVAL, "world_size > 1 needs an NCCL unique id");
+  if (cfg->actor_depth > 0 && cfg->actor_width > 0 &&
+      (!mem->actor_params || !mem->actor_adam_m || !mem->actor_adam_v))
+    return fail(ctx, CRL_EINVAL, "actor configured: actor_params / actor_adam_m / actor_adam_v must be non-NULL");
   crl_sizes sz;
   st = crl_workspace_size(cfg, &sz);
   if (st != CRL_OK) return st;
@@ -294,6 +336,7 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaMemset(ctx->open_start, 0, (size_t)cfg->n_envs_local * 4) != cudaSuccess ||
       cudaMemset(ctx->status, 0, 4) != cudaSuccess || cudaMemset(ctx->adam_t, 0, 4) != cudaSuccess ||
       cudaMemset(ctx->skip, 0, 4) != cudaSuccess || cudaMemset(ctx->loss_ticket, 0, 4) != cudaSuccess ||
+      (ctx->has_actor && (cudaMemset(ctx->a_t, 0, 4) != cudaSuccess || cudaMemset(ctx->a_skip, 0, 4) != cudaSuccess)) ||
       cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream3, cudaStreamNonBlocking) != cudaSuccess ||
@@ -621,14 +664,6 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
   ctx->launches = ctx->graph_launches[key];
   if (loss_host) CU(cudaMemcpyAsync(loss_out, loss_dev, 16, cudaMemcpyDeviceToHost, st));
   return CRL_OK;
-}
-
-extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* g, const float* eps,
-                                     float alpha_ent, float* loss_out, float* actor_grads_out,
-                                     int apply_adam, void* stream) {
-  (void)s; (void)g; (void)eps; (void)alpha_ent; (void)loss_out; (void)actor_grads_out;
-  (void)apply_adam; (void)stream;
-  return fail(ctx, CRL_EUNSUPPORTED, "crl_actor_loss: not built yet");
 }
 
 extern "C" crl_status crl_profile_enable(crl_ctx* ctx, int on) {

@@ -151,6 +151,22 @@ struct crl_ctx {
   tc::ChainParams chain_fwd_p{}, chain_bwd_p{};
   float *lg_part_m = nullptr, *lg_part_s = nullptr, *lg_part_da = nullptr, *lg_part_rs = nullptr;
   CUtensorMap lg_row_A, lg_row_B, lg_col_A, lg_col_B;
+  // ---------------- actor objective (crl_actor_loss, actor.cu): fp32 SIMT, critic frozen
+  bool has_actor = false;
+  EncoderPlan actor_plan{};
+  float* aX[CRL_MAX_LAYERS] = {}; float* aZ[CRL_MAX_LAYERS] = {};      // actor activations
+  float *a_out = nullptr;                  // [B_l][2 act]: (mu, log sigma raw)
+  float *a_new = nullptr;                  // [B_l][act]: a' = tanh(mu + sigma eps)
+  float *a_logpi = nullptr, *a_rowloss = nullptr;   // [B_l]
+  float *a_dout = nullptr, *a_da = nullptr;         // [B_l][2 act], [B_l][act]
+  float* a_dz[2] = {nullptr, nullptr};     // actor backward ping-pong [B_l][max(width, 2 act)]
+  float* ac_phiX[CRL_MAX_LAYERS] = {}; float* ac_phiZ[CRL_MAX_LAYERS] = {};   // critic phi on [s||a']
+  float* ac_psiX[CRL_MAX_LAYERS] = {}; float* ac_psiZ[CRL_MAX_LAYERS] = {};   // critic psi on g
+  float *ac_phi = nullptr, *ac_psi = nullptr, *ac_dphi = nullptr;            // [B_l][D]
+  float* ac_dz[2] = {nullptr, nullptr};    // critic dX chain ping-pong [B_l][max(width, D)]
+  float* a_grads = nullptr;                // [dw_splits][n_actor_params]
+  float* a_loss = nullptr;                 // [4]: summed rows (all-reduced), loss
+  int *a_t = nullptr, *a_skip = nullptr;
 };
 
 constexpr int kTcLogitsMinN = 2;         // measured: tensor-core logits win down to N = 256

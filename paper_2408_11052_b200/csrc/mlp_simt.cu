@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(GemmArgs p) {
       } else if (EPI == EPI_BIAS) {
         C[o] = v + p.bias[n];
       } else if (EPI == EPI_DACT) {
-        C[o] = v * act_grad_f(p.Zp[o], p.act);
+        C[o] = p.Zp != nullptr ? v * act_grad_f(p.Zp[o], p.act) : v;   // null: plain dX
       } else {
         C[o] = v;
       }
@@ -227,7 +227,8 @@ cudaError_t mlp_forward_layer_f32(int Bn, int in, int out, const float* X, int l
   return launch_gemm<false, false, EPI_BIAS>(p, 1, st);
 }
 
-// dZ_prev = (dZ W^T) * act'(Z_prev)
+// dZ_prev = (dZ W^T) * act'(Z_prev)   (Zprev == nullptr: dX = dZ W^T; W may point at a row
+// block of a larger [in_total][out] matrix, e.g. the action rows of the first phi layer)
 cudaError_t mlp_backward_dx_f32(int Bn, int in, int out, const float* dZ, const float* W,
                                 const float* Zprev, float* dZprev, int act, cudaStream_t st) {
   GemmArgs p{};
