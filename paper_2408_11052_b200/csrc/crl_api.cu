@@ -135,6 +135,14 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       c->lg_part_s = s.take<float>((size_t)2 * c->lg_splits * Bl);
       c->lg_part_rs = s.take<float>((size_t)2 * c->lg_splits * Bl);
       c->lg_part_da = s.take<float>((size_t)2 * c->lg_splits * Bl * D);
+      c->use_stats = W == 1 && tc_stats_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_STATS");
+      if (c->use_stats) {
+        c->st_splits = tc_stats_splits(Bl, N, 148);
+        c->st_ldc = N + kStatPad;
+        c->st_part_rs = s.take<float>((size_t)c->st_splits * Bl);
+        c->st_colpart = s.take<float>((size_t)((Bl + 127) / 128) * c->st_ldc);
+        c->st_bad = s.take<int>(4);
+      }
     }
   }
   c->phi_out = s.take<float>((size_t)Bl * D);

@@ -45,9 +45,13 @@ cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, floa
 namespace tc {
 bool tc_logits_supports(int D);
 int tc_logits_splits(int Na, int Nb, int D, int num_sms);
+bool tc_stats_supports(int D, int energy);
+int tc_stats_splits(int Na, int Nb, int num_sms);
 }  // namespace tc
 using tc::tc_logits_supports;
 using tc::tc_logits_splits;
+using tc::tc_stats_supports;
+using tc::tc_stats_splits;
 }  // namespace crl
 
 using namespace crl;
@@ -151,6 +155,12 @@ struct crl_ctx {
   tc::ChainParams chain_fwd_p{}, chain_bwd_p{};
   float *lg_part_m = nullptr, *lg_part_s = nullptr, *lg_part_da = nullptr, *lg_part_rs = nullptr;
   CUtensorMap lg_row_A, lg_row_B, lg_col_A, lg_col_B;
+  // fused row + column statistics in one pass (tc_stats.cu; W = 1, L2 / cos, D <= 128)
+  bool use_stats = false;
+  int st_splits = 1, st_ldc = 0;
+  float *st_part_rs = nullptr;                // [st_splits][B_l] row sums
+  float *st_colpart = nullptr;                // [row blocks][st_ldc] column sums
+  int* st_bad = nullptr;                      // set by the merge: the exact online-max path runs
   // ---------------- actor objective (crl_actor_loss, actor.cu): fp32 SIMT, critic frozen
   bool has_actor = false;
   EncoderPlan actor_plan{};
@@ -171,6 +181,7 @@ struct crl_ctx {
 
 constexpr int kTcLogitsMinN = 2;         // measured: tensor-core logits win down to N = 256
 constexpr int kStatPad = 256;            // padding of per-column arrays read by 1-D bulk copies
+constexpr int kChainMinBatch = 8192;     // fused MLP chains from this local batch on (measured)
 
 // Brackets one launch with CUDA events when the context is in profiling mode (events come
 // from a pool so the host enqueue stays cheap; see also spin_kernel below).

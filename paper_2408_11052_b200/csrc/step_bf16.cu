@@ -33,12 +33,15 @@ cudaError_t tc_backward_dx(int, const CUtensorMap&, const CUtensorMap&, int, int
 cudaError_t tc_backward_dw(int, const CUtensorMap&, const CUtensorMap&, int, int, int, float*, int,
                            size_t, cudaStream_t);
 cudaError_t launch_prep_inputs(const float*, const float*, const float*, int, int, int, int,
-                               __nv_bfloat16*, int, __nv_bfloat16*, int, int, cudaStream_t);
+                               __nv_bfloat16*, int, __nv_bfloat16*, int, int, int*, cudaStream_t);
 cudaError_t launch_colsum_bf16(const __nv_bfloat16*, int, int, int, float*, int, size_t, cudaStream_t);
 cudaError_t launch_f32_to_bf16(const float*, __nv_bfloat16*, size_t, int, cudaStream_t);
 bool tc_logits_maps(CUtensorMap*, CUtensorMap*, const __nv_bfloat16*, int, const __nv_bfloat16*, int, int);
 cudaError_t tc_logits_lse(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*,
-                          int, float*, float*, float*, float*, int*, float, float, cudaStream_t);
+                          int, float*, float*, float*, float*, int*, float, float, const int*, cudaStream_t);
+cudaError_t tc_stats_fused(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*, int,
+                           float*, float*, int, float*, float*, float*, float*, int*, int*, float, float, float, float,
+                           cudaStream_t);
 cudaError_t tc_logits_grad(int, int, const CUtensorMap&, const CUtensorMap&, int, int, int, const float*,
                            const float*, const float*, const float*, const float*, float, float, float, float,
                            float, int, float*, float*, const __nv_bfloat16*, const __nv_bfloat16*, float*,
@@ -95,7 +98,12 @@ crl_status bf16_prepare(crl_ctx* ctx) {
       return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the logits operands");
   }
   // fused MLP chains (activations resident in SMEM/TMEM across layers) when the shapes fit
-  ctx->use_chain = ctx->tc_logits && !std::getenv("CRL_NO_CHAIN") && k.depth >= 1 &&
+  // (measured on B200: the chain wins from B_l = 8192 on; below it the per-layer GEMMs, which
+  // spread each layer over more SMs, are as fast or faster.  CRL_CHAIN / CRL_NO_CHAIN force it.)
+  const bool chain_wanted = std::getenv("CRL_CHAIN") ? true
+                            : std::getenv("CRL_NO_CHAIN") ? false
+                            : k.batch_local >= kChainMinBatch;
+  ctx->use_chain = ctx->tc_logits && chain_wanted && k.depth >= 1 &&
                    tc::tc_chain_supported(k.obs_dim + k.act_dim, k.width, k.repr_dim, k.depth) &&
                    tc::tc_chain_supported(k.goal_dim, k.width, k.repr_dim, k.depth);
   if (ctx->use_chain) {
@@ -264,7 +272,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   {
     Stage sg(ctx, st, "prep_inputs");
     CU(tc::launch_prep_inputs(s, a, g, Bl, k.obs_dim, k.act_dim, k.goal_dim, ctx->x0_phi, ctx->ld0_phi,
-                              ctx->x0_psi, ctx->ld0_psi, ctx->num_sms, st));
+                              ctx->x0_psi, ctx->ld0_psi, ctx->num_sms, ctx->use_stats ? ctx->st_bad : nullptr, st));
     ++nl;
   }
   if (ctx->use_chain) {
@@ -300,16 +308,28 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       NC(ncclAllGather(ctx->stat_psi + row_off, ctx->stat_psi, (size_t)Bl, ncclFloat32, ctx->comm, st));
       NC(ncclGroupEnd());
     }
+    const int* gate = nullptr;
+    if (ctx->use_stats) {
+      // one pass: row AND column sums of e^l (no running max: L2 / cos logits are bounded
+      // above); the exact online-max pass below then runs only if a sum under/overflowed
+      Stage sg(ctx, st, "lse_fused");
+      CU(tc::tc_stats_fused(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off, ctx->stat_psi,
+                            ctx->st_splits, ctx->st_part_rs, ctx->st_colpart, ctx->st_ldc, ctx->lse_row, ctx->fac_row,
+                            ctx->lse_col, ctx->fac_col, ctx->fac_ok, ctx->st_bad, invN * c_f, 2.f * invN * k.beta_lse,
+                            invN * c_b, 0.f, st));
+      nl += 2;
+      gate = ctx->st_bad;
+    }
     fork2(ctx, st, st2);
     { Stage sg(ctx, st2, "lse_col");
       CU(tc::tc_logits_lse(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, ctx->stat_psi + row_off,
                            ctx->stat_phi, S, ctx->lg_part_m + (size_t)S * Bl, ctx->lg_part_s + (size_t)S * Bl,
-                           ctx->lse_col, ctx->fac_col, ctx->fac_ok, invN * c_b, 0.f, st2));
+                           ctx->lse_col, ctx->fac_col, ctx->fac_ok, invN * c_b, 0.f, gate, st2));
       nl += 2; }
     { Stage sg(ctx, st, "lse_row");
       CU(tc::tc_logits_lse(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off,
                            ctx->stat_psi, S, ctx->lg_part_m, ctx->lg_part_s, ctx->lse_row, ctx->fac_row,
-                           ctx->fac_ok, invN * c_f, 2.f * invN * k.beta_lse, st));
+                           ctx->fac_ok, invN * c_f, 2.f * invN * k.beta_lse, gate, st));
       nl += 2; }
     join2(ctx, st, st2);
   } else {

@@ -338,11 +338,12 @@ cudaError_t tc_backward_dw(int bn, const CUtensorMap& mapX_mn, const CUtensorMap
 __global__ void prep_inputs_kernel(const float* __restrict__ s, const float* __restrict__ a,
                                    const float* __restrict__ g, int Bn, int obs, int act, int goal,
                                    __nv_bfloat16* __restrict__ x0, int ld0, __nv_bfloat16* __restrict__ g0,
-                                   int ldg) {
+                                   int ldg, int* __restrict__ reset) {
   const int in0 = obs + act;
   const size_t tot0 = (size_t)Bn * in0, totg = (size_t)Bn * goal;
   pdl_wait();
   pdl_launch();
+  if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reset = 0;   // per-step device flag
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot0 + totg;
        i += (size_t)gridDim.x * blockDim.x) {
     if (i < tot0) {
@@ -359,12 +360,12 @@ __global__ void prep_inputs_kernel(const float* __restrict__ s, const float* __r
 
 cudaError_t launch_prep_inputs(const float* s, const float* a, const float* g, int Bn, int obs, int act,
                                int goal, __nv_bfloat16* x0, int ld0, __nv_bfloat16* g0, int ldg,
-                               int num_sms, cudaStream_t st) {
+                               int num_sms, int* reset, cudaStream_t st) {
   size_t tot = (size_t)Bn * (obs + act + goal);
   size_t blocks = (tot + 255) / 256;
   if (blocks > (size_t)num_sms * 4) blocks = (size_t)num_sms * 4;
   return launch_pdl(prep_inputs_kernel, dim3((unsigned)blocks), dim3(256), 0, st, s, a, g, Bn, obs, act, goal,
-                    x0, ld0, g0, ldg);
+                    x0, ld0, g0, ldg, reset);
 }
 
 // db[s][n] = sum over the batch slice s of dZ[b][n] (bf16 in, fp32 out): 64 columns x one

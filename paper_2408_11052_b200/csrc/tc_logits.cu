@@ -60,6 +60,7 @@ struct TcLogitsArgs {
   float* part_s;                   // LSE: [S][Na] running sum
   float* part_da;                  // GRAD: [S][Na][D]
   float* part_rs;                  // GRAD: [S][Na] row sums of w (L2)
+  const int* gate;                 // LSE: if non-null, run only when *gate != 0 (fused-stats fallback)
 };
 
 template <int D>
@@ -113,6 +114,10 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
   const int jbeg = split * p.cols_per_split;
   const int jend = min(p.Nb, jbeg + p.cols_per_split);
   const int ntiles = jend > jbeg ? (jend - jbeg + BNT - 1) / BNT : 0;
+  if (p.gate != nullptr) {          // exact fallback of the fused statistics pass (tc_stats.cu)
+    pdl_wait();
+    if (*p.gate == 0) { pdl_launch(); return; }
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -394,9 +399,10 @@ __global__ void rowstat_bf16_kernel(const __nv_bfloat16* __restrict__ x, int N, 
 // lse[i] = (max_s m + log2(sum_s s * 2^(m_s - max))) * ln 2
 __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int Na, int S,
                                  float* __restrict__ lse, float* __restrict__ fac, int* __restrict__ fac_ok,
-                                 float cc0, float cc1) {
+                                 float cc0, float cc1, const int* __restrict__ gate) {
   pdl_wait();
   pdl_launch();
+  if (gate != nullptr && *gate == 0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= Na) return;
   float mx = -INFINITY;
@@ -535,16 +541,17 @@ static cudaError_t dispatch_lg(int D, int energy, const CUtensorMap& a, const CU
 
 cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                           const float* a_stat, const float* b_stat, int S, float* part_m, float* part_s,
-                          float* lse, float* fac, int* fac_ok, float cc0, float cc1, cudaStream_t st) {
+                          float* lse, float* fac, int* fac_ok, float cc0, float cc1, const int* gate,
+                          cudaStream_t st) {
   TcLogitsArgs p{};
   p.Na = Na; p.Nb = Nb;
   const int bnt = D <= 128 ? 128 : 64;
   p.cols_per_split = ((Nb + S - 1) / S + bnt - 1) / bnt * bnt;
-  p.a_stat = a_stat; p.b_stat = b_stat; p.part_m = part_m; p.part_s = part_s;
+  p.a_stat = a_stat; p.b_stat = b_stat; p.part_m = part_m; p.part_s = part_s; p.gate = gate;
   cudaError_t e = dispatch_lg<false>(D, energy, mA, mB, p, S, st);
   if (e != cudaSuccess) return e;
   return launch_pdl(lse_merge_kernel, dim3((Na + 255) / 256), dim3(256), 0, st, (const float*)part_m,
-                    (const float*)part_s, Na, S, lse, fac, fac_ok, cc0, cc1);
+                    (const float*)part_s, Na, S, lse, fac, fac_ok, cc0, cc1, gate);
 }
 
 cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,

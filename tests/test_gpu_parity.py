@@ -82,7 +82,7 @@ def test_relabel_full_size_ant_sampled_rows():
 
 # ------------------------------------------------------------------------- A2-A6
 
-def _critic_parity(cfg, batch_seed=11, check_adam=True, tol_loss=1e-5, tol_grad=1e-4):
+def _critic_parity(cfg, batch_seed=11, check_adam=True, tol_loss=1e-5, tol_grad=1e-4, per_layer=True):
     ctx, params = make_ctx(cfg)
     B = cfg["batch"]
     s, a, g = crl_synth.random_batch(cfg, B, seed=batch_seed)
@@ -110,7 +110,8 @@ def _critic_parity(cfg, batch_seed=11, check_adam=True, tol_loss=1e-5, tol_grad=
     for enc_in in (cfg["obs_dim"] + cfg["act_dim"], cfg["goal_dim"]):
         for fi, fo in crl_synth.param_shapes(enc_in, cfg["depth"], cfg["width"], cfg["repr_dim"]):
             for n in (fi * fo, fo):
-                assert rel(gr[off:off + n], ref["grads"][off:off + n]) < tol_grad, off
+                if per_layer:
+                    assert rel(gr[off:off + n], ref["grads"][off:off + n]) < tol_grad, off
                 off += n
     if check_adam:
         # The first Adam step maps g -> g/(|g|+eps) ~ sign(g): it magnifies tiny gradient
@@ -242,6 +243,46 @@ def test_critic_step_bf16_tc_logits(energy, loss):
 def test_critic_step_bf16_tc_logits_repr256():
     cfg = crl_synth.preset("ant", batch=1536, width=128, repr_dim=256, precision="bf16", beta_lse=0.3)
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("preset,over", [
+    ("ant", dict(batch=256, energy="l2")),
+    ("ant", dict(batch=300, energy="cos")),                          # ragged last row block
+    ("reacher", dict(batch=130, width=64, depth=3, energy="dot")),   # N = 64 layers, one chunk
+    ("humanoid", dict()),                                           # 285 inputs: 5 K chunks
+    ("sweep4096", dict()),
+])
+def test_critic_step_bf16_fused_chain(preset, over, monkeypatch):
+    """The fused per-row-block MLP chain kernels (all layers of both encoders in one launch,
+    forward and dX backward) are the default only from B_l = 8192; force them here."""
+    monkeypatch.setenv("CRL_CHAIN", "1")
+    cfg = crl_synth.preset(preset, precision="bf16", **over)
+    _critic_parity(cfg, check_adam=cfg["batch"] <= 1024, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("knob,energy", [
+    ("CRL_FORCE_STATS_FALLBACK", "l2"),   # fused pass runs, its merge flags, exact pass redoes it
+    ("CRL_FORCE_STATS_FALLBACK", "cos"),
+    ("CRL_NO_FUSED_STATS", "l2"),         # two-call online-max statistics only
+])
+def test_critic_step_bf16_stats_paths(knob, energy, monkeypatch):
+    """The one-pass row+column statistics (tc_stats.cu) are the default for L2 / cos at W = 1;
+    its exact fallback (taken when a sum under/overflows) and the two-call path are forced."""
+    monkeypatch.setenv(knob, "1")
+    cfg = crl_synth.preset("ant", batch=1100, width=128, energy=energy, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("chain", [False, True])
+def test_critic_step_bf16_relu(chain, monkeypatch):
+    """ReLU on the bf16 path: loss and the global gradient hold the 2e-2 bar; the per-tensor
+    check does not apply (reading A-28: bf16 rounding of Z flips ReLU masks near 0,
+    and an fp64 emulation of the bf16 operand rounding alone already puts the first phi
+    layer's dW ~6% from the fp64 oracle, while SiLU stays at ~0.5%)."""
+    if chain:
+        monkeypatch.setenv("CRL_CHAIN", "1")
+    cfg = crl_synth.preset("ant", batch=300, energy="cos", activation="relu", precision="bf16")
+    _critic_parity(cfg, check_adam=False, tol_loss=BF16_TOL, tol_grad=BF16_TOL, per_layer=False)
 
 
 @pytest.mark.parametrize("energy", ["l2", "cos"])
