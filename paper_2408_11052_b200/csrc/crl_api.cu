@@ -143,6 +143,15 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
         c->st_colpart = s.take<float>((size_t)((Bl + 127) / 128) * c->st_ldc);
         c->st_bad = s.take<int>(4);
       }
+      c->use_gradf = W == 1 && tc_gradf_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_GRAD");
+      if (c->use_gradf) {
+        c->gf_splits = tc_stats_splits(Bl, N, 148);
+        c->gf_part_da = s.take<float>((size_t)c->gf_splits * Bl * D);
+        c->gf_part_rs = s.take<float>((size_t)c->gf_splits * Bl);
+        c->gf_acc_bytes = ((size_t)N * D + N + kStatPad) * 4;
+        c->gf_acc = s.take<float>(c->gf_acc_bytes / 4);
+        c->gf_cs = c->gf_acc + (size_t)N * D;
+      }
     }
   }
   c->phi_out = s.take<float>((size_t)Bl * D);

@@ -4,6 +4,7 @@
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_chain.h"
+#include "tc_dwg.h"
 
 #include <nccl.h>
 
@@ -47,7 +48,9 @@ bool tc_logits_supports(int D);
 int tc_logits_splits(int Na, int Nb, int D, int num_sms);
 bool tc_stats_supports(int D, int energy);
 int tc_stats_splits(int Na, int Nb, int num_sms);
+bool tc_gradf_supports(int D, int energy);
 }  // namespace tc
+using tc::tc_gradf_supports;
 using tc::tc_logits_supports;
 using tc::tc_logits_splits;
 using tc::tc_stats_supports;
@@ -161,6 +164,16 @@ struct crl_ctx {
   float *st_part_rs = nullptr;                // [st_splits][B_l] row sums
   float *st_colpart = nullptr;                // [row blocks][st_ldc] column sums
   int* st_bad = nullptr;                      // set by the merge: the exact online-max path runs
+  // both gradient sides in one pass (tc_gradf.cu; W = 1, L2 / dot, D = 64)
+  bool use_gradf = false;
+  int gf_splits = 1;
+  float *gf_part_da = nullptr, *gf_part_rs = nullptr;   // row side per split
+  float *gf_acc = nullptr, *gf_cs = nullptr;            // column side [N][64], [N] (reductions)
+  size_t gf_acc_bytes = 0;
+  CUtensorMap gf_map;
+  // all weight / bias gradients of both encoders in one grouped launch (tc_dwg.cu)
+  bool use_dwg = false;
+  tc::DwgParams dwg;
   // ---------------- actor objective (crl_actor_loss, actor.cu): fp32 SIMT, critic frozen
   bool has_actor = false;
   EncoderPlan actor_plan{};

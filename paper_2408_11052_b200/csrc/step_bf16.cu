@@ -39,6 +39,11 @@ cudaError_t launch_f32_to_bf16(const float*, __nv_bfloat16*, size_t, int, cudaSt
 bool tc_logits_maps(CUtensorMap*, CUtensorMap*, const __nv_bfloat16*, int, const __nv_bfloat16*, int, int);
 cudaError_t tc_logits_lse(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*,
                           int, float*, float*, float*, float*, int*, float, float, const int*, cudaStream_t);
+cudaError_t tc_grad_fused(int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, int, int, const float*,
+                          const float*, const float*, const float*, const float*, const int*, float, float, float,
+                          float, int, float*, float*, float*, float*, const __nv_bfloat16*, const __nv_bfloat16*,
+                          float*, __nv_bfloat16*, float*, __nv_bfloat16*, cudaStream_t);
+bool tc_gradf_map(CUtensorMap*, float*, int);
 cudaError_t tc_stats_fused(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*, int,
                            float*, float*, int, float*, float*, float*, float*, int*, int*, float, float, float, float,
                            cudaStream_t);
@@ -88,6 +93,23 @@ crl_status bf16_prepare(crl_ctx* ctx) {
   st = build_encoder_plan(ctx, ctx->psi_plan, ctx->x0_psi, ctx->ld0_psi, ctx->psiXb, ctx->psiZb, ctx->dpsib,
                           ctx->dzb_psi, ctx->tc_psi);
   if (st != CRL_OK) return st;
+  // grouped weight / bias gradients: X_l and dZ_l of every layer of both encoders
+  ctx->use_dwg = !std::getenv("CRL_NO_DWG");
+  if (ctx->use_dwg) {
+    tc::dwg_init(ctx->dwg, k.batch_local, ctx->dw_splits, ctx->sizes.n_params);
+    const EncoderPlan* plans[2] = {&ctx->phi_plan, &ctx->psi_plan};
+    std::vector<crl_ctx::TcLayer>* tcs[2] = {&ctx->tc_phi, &ctx->tc_psi};
+    __nv_bfloat16** Xb[2] = {ctx->phiXb, ctx->psiXb};
+    const __nv_bfloat16* x0[2] = {ctx->x0_phi, ctx->x0_psi};
+    const int ld0[2] = {ctx->ld0_phi, ctx->ld0_psi};
+    for (int e = 0; e < 2; ++e)
+      for (int l = 0; l < plans[e]->n_layers; ++l) {
+        const LayerPlan& Lp = plans[e]->layer[l];
+        if (!tc::dwg_add_problem(ctx->dwg, l == 0 ? x0[e] : Xb[e][l], l == 0 ? ld0[e] : k.width, (*tcs[e])[l].dz,
+                                 Lp.in, Lp.out, ctx->grads + Lp.w_off, ctx->grads + Lp.b_off))
+          return fail(ctx, CRL_ECUDA, "grouped weight-gradient setup failed (tensor maps)");
+      }
+  }
   if (ctx->tc_logits) {
     ctx->lg_splits = std::min(ctx->lg_splits, tc::tc_logits_splits(k.batch_local, ctx->N, k.repr_dim,
                                                                    ctx->num_sms));
@@ -96,6 +118,8 @@ crl_status bf16_prepare(crl_ctx* ctx) {
         !tc::tc_logits_maps(&ctx->lg_col_A, &ctx->lg_col_B, ctx->psi_outb, k.batch_local, ctx->phi_outb_g,
                             ctx->N, k.repr_dim))
       return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the logits operands");
+    if (ctx->use_gradf && !tc::tc_gradf_map(&ctx->gf_map, ctx->gf_acc, ctx->N))
+      return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the column-gradient accumulator");
   }
   // fused MLP chains (activations resident in SMEM/TMEM across layers) when the shapes fit
   // (measured on B200: the chain wins from B_l = 8192 on; below it the per-layer GEMMs, which
@@ -201,17 +225,18 @@ static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const Encoder
   for (int l = L - 1; l >= 0; --l) {
     const LayerPlan& Lp = P.layer[l];
     // dW_l and db_l only feed Adam: they run on a side stream, off the dX critical path
-    if (side != st) {
+    // (or all at once in the grouped kernel after both dX chains: ctx->use_dwg)
+    if (side != st && !ctx->use_dwg) {
       cudaEventRecord(ctx->ev_side, st);
       cudaStreamWaitEvent(side, ctx->ev_side, 0);
     }
-    {
+    if (!ctx->use_dwg) {
       Stage sg(ctx, side, std::string(tag) + "_bwd_dw_l" + std::to_string(l));
       CU(tc::tc_backward_dw(T[l].bn_dw, T[l].dwA, T[l].dwB, Bl, Lp.in, Lp.out, ctx->grads + Lp.w_off,
                             ctx->dw_splits, ctx->sizes.n_params, side));
       ++*nl;
     }
-    {
+    if (!ctx->use_dwg) {
       Stage sg(ctx, side, std::string(tag) + "_bwd_db_l" + std::to_string(l));
       CU(tc::launch_colsum_bf16(T[l].dz, Bl, Lp.out, Lp.out, ctx->grads + Lp.b_off, ctx->dw_splits,
                                 ctx->sizes.n_params, side));
@@ -368,8 +393,19 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                             ctx->status, st));
     ++nl;
   }
+  if (ctx->use_gradf) {
+    // both sides of dL/dl from ONE evaluation of every w_ij (tc_gradf.cu); the column side
+    // accumulates by reductions into db_acc / cs_acc, zeroed here
+    CU(cudaMemsetAsync(ctx->gf_acc, 0, ctx->gf_acc_bytes, st));
+    { Stage sg(ctx, st, "grad_fused");
+      CU(tc::tc_grad_fused(k.energy, ctx->lg_row_A, ctx->lg_row_B, ctx->gf_map, Bl, N, ctx->stat_phi, ctx->stat_psi,
+                           ctx->lse_row, ctx->lse_col, ctx->fac_col, ctx->fac_ok, c_f, c_b, k.beta_lse, invN,
+                           ctx->gf_splits, ctx->gf_part_da, ctx->gf_part_rs, ctx->gf_acc, ctx->gf_cs, ctx->phi_outb,
+                           ctx->psi_outb, ctx->dphi, ctx->dphib, ctx->dpsi, ctx->dpsib, st));
+      nl += 3; }
+  }
   fork2(ctx, st, st2);
-  { Stage sg(ctx, st2, "grad_psi");
+  if (!ctx->use_gradf) { Stage sg(ctx, st2, "grad_psi");
     if (ctx->tc_logits) {
       CU(tc::tc_logits_grad(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, row_off, ctx->stat_psi + row_off,
                             ctx->stat_phi, ctx->lse_col, ctx->lse_row_g, ctx->fac_row_g, c_b, c_f, 0.f,
@@ -388,7 +424,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side2, &nl);
     if (rs != CRL_OK) return rs;
   }
-  { Stage sg(ctx, st, "grad_phi");
+  if (!ctx->use_gradf) { Stage sg(ctx, st, "grad_phi");
     if (ctx->tc_logits) {
       CU(tc::tc_logits_grad(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, row_off, ctx->stat_phi + row_off,
                             ctx->stat_psi, ctx->lse_row, ctx->lse_col_g, ctx->fac_col_g, c_f, c_b,
@@ -410,6 +446,13 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     { Stage sg(ctx, st, "mlp_bwd_chain");          // both encoders' dX chains, one launch
       CU(tc::tc_chain_backward(ctx->chain_bwd[0], ctx->chain_bwd[1], ctx->chain_bwd_p, st));
       ++nl; }
+  }
+  if (ctx->use_dwg) {
+    // every dW_l and db_l of both encoders in one grouped launch (tc_dwg.cu)
+    Stage sg(ctx, st, "dw_db_grouped");
+    CU(tc::tc_dwg_launch(ctx->dwg, st));
+    ++nl;
+  } else if (ctx->use_chain) {
     if (side != st) {
       cudaEventRecord(ctx->ev_side, st);
       cudaStreamWaitEvent(side, ctx->ev_side, 0);
@@ -420,7 +463,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     rs = enc_weight_grads_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, side2, &nl);
     if (rs != CRL_OK) return rs;
   }
-  if (side != st) {
+  if (side != st && !ctx->use_dwg) {
     cudaEventRecord(ctx->ev_side, side);
     cudaStreamWaitEvent(st, ctx->ev_side, 0);
     cudaEventRecord(ctx->ev_side, side2);

@@ -1,0 +1,435 @@
+// tc_gradf.cu — the logits gradient pass (A4) for BOTH sides in one pass over the N x N tile
+// grid (BF16 path, W = 1, L2 / dot energy, D = 64).
+//
+// Paper: InfoNCE fwd/bwd/sym P:619-630 and the logsumexp penalty P:361 / Alg. 1 P:1052 give
+// g_ij = dL/dl_ij in closed form (readings A-02..A-05); the energy VJP (App. A.2):
+//   L2:  w_ij = g_ij / r_ij,  dPhi_i = sum_j w_ij psi_j - (sum_j w_ij) phi_i
+//                             dPsi_j = sum_i w_ij phi_i - (sum_i w_ij) psi_j
+//   dot: w_ij = g_ij,         dPhi = W Psi,  dPsi = W^T Phi
+// The two-call design (tc_logits.cu) evaluates every w_ij twice, once per orientation.  Here
+// one CTA (128 rows x a column split) forms each W tile once and feeds three tcgen05 MMAs:
+//   dA   += W . B_t        (M=128 rows, N=64, K=128 cols)   TMEM-resident over the split
+//   dB_t  = W^T . A        (M=128 cols, N=64, K=128 rows)   A and W re-read as MN-major
+//   cs_t  = W^T . 1        (L2 only: the column sums of w)
+// dB_t and cs_t are per (row block, column tile): they are accumulated across row blocks in
+// a global fp32 buffer by TMA bulk-tensor REDUCTIONS (cp.reduce.async.bulk .add.f32, whole
+// 32 KB tiles from a swizzled SMEM staging buffer) and red.global.add (cs).  The row side
+// keeps the per-split partials of tc_logits.cu; grad_merge finishes both sides (the -rs A
+// term, the positive-pair term, fp32 + bf16 outputs).
+// fp32 atomics make the column-side sum order nondeterministic at the 1-ulp level (row side
+// and every other stage stay deterministic); the path's tolerance is 2e-2 (north_star).
+#include <type_traits>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace crl {
+namespace tc {
+namespace gf {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsq(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+}  // namespace gf
+
+struct TcGradFArgs {
+  int Na, Nb;
+  int cols_per_split;              // multiple of 128
+  const float* a_stat;             // [Na]  L2: |a|^2
+  const float* b_stat;             // [Nb padded]
+  const float* lr;                 // [Na]  row LSE (natural log)
+  const float* lc;                 // [Nb padded] column LSE
+  const float* lcf;                // [Nb padded] column coefficient (lse_merge / stats_merge)
+  const int* fac_ok;
+  float c_r, c_c, beta_r, invN;
+  float* part_da;                  // [S][Na][64]
+  float* part_rs;                  // [S][Na]
+  float* cs_acc;                   // [Nb] column sums of w (L2), accumulated
+};
+
+struct GfCfg {
+  static constexpr int D = 64, BNT = 128, STAGES = 3;
+  static constexpr uint32_t A_BYTES = 128 * D * 2;       // 16 KB
+  static constexpr uint32_t B_BYTES = BNT * D * 2;       // 16 KB
+  static constexpr uint32_t W_BYTES = 128 * BNT * 2;     // 32 KB
+  static constexpr uint32_t R_BYTES = BNT * D * 4;       // 32 KB fp32 dB staging (2 x 16 KB halves)
+  static constexpr uint32_t ONES_BYTES = 128 * 128;      // 16 KB: K=128 rows x 64 bf16 ones
+  static constexpr uint32_t STAT_BYTES = BNT * 4;
+  static constexpr size_t smem() {
+    return 1024 + A_BYTES + STAGES * B_BYTES + 2 * W_BYTES + 2 * R_BYTES + ONES_BYTES + STAGES * 3 * STAT_BYTES +
+           3 * 128 * 4 + 256;
+  }
+};
+
+template <int ENERGY>
+__global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                          const __grid_constant__ CUtensorMap tmB,
+                                                          const __grid_constant__ CUtensorMap tmDB,
+                                                          TcGradFArgs p) {
+  using C = GfCfg;
+  constexpr int BNT = C::BNT, STAGES = C::STAGES, D = C::D;
+  constexpr bool L2 = ENERGY == CRL_ENERGY_L2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::A_BYTES;
+  uint8_t* sW = sB + STAGES * C::B_BYTES;
+  uint8_t* sR = sW + 2 * C::W_BYTES;
+  uint8_t* sOnes = sR + 2 * C::R_BYTES;
+  float* sStat = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);      // [STAGES][3][BNT]
+  float* sMerge = sStat + STAGES * 3 * BNT;                            // [3][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + 3 * 128);
+  uint64_t* a_full = bars;
+  uint64_t* b_full = bars + 1;
+  uint64_t* b_empty = b_full + STAGES;
+  uint64_t* s_full = b_empty + STAGES;   // [2]
+  uint64_t* s_empty = s_full + 2;        // [2]
+  uint64_t* w_full = s_empty + 2;        // [2]
+  uint64_t* w_empty = w_full + 2;        // [2]
+  uint64_t* db_full = w_empty + 2;       // [2]
+  uint64_t* db_empty = db_full + 2;      // [2]
+  uint64_t* da_full = db_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a0 = blockIdx.x * 128;
+  const int split = blockIdx.y;
+  const int jbeg = split * p.cols_per_split;
+  const int jend = min(p.Nb, jbeg + p.cols_per_split);
+  const int ntiles = jend > jbeg ? (jend - jbeg + BNT - 1) / BNT : 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmDB);
+    mbar_init(a_full, 1);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
+      mbar_init(&w_full[i], 8); mbar_init(&w_empty[i], 1);
+      mbar_init(&db_full[i], 1); mbar_init(&db_empty[i], 8);
+    }
+    mbar_init(da_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (L2)
+    for (int i = threadIdx.x; i < (int)(C::ONES_BYTES / 16); i += blockDim.x)
+      reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tm_s[2] = {tmem, tmem + 128};
+  const uint32_t tm_da = tmem + 256;
+  const uint32_t tm_db[2] = {tmem + 320, tmem + 384};
+  const uint32_t tm_cs[2] = {tmem + 448, tmem + 464};
+  pdl_wait();
+  pdl_launch();
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    mbar_expect_tx(a_full, C::A_BYTES);
+    tma_load_2d(sA, &tmA, a_full, 0, a0);
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t % STAGES;
+      mbar_wait(&b_empty[s], ((t / STAGES) & 1) ^ 1);
+      const int j0 = jbeg + t * BNT;
+      mbar_expect_tx(&b_full[s], C::B_BYTES + 3 * C::STAT_BYTES);
+      tma_load_2d(sB + s * C::B_BYTES, &tmB, &b_full[s], 0, j0);
+      float* st = sStat + s * 3 * BNT;
+      gf::bulk_g2s(st, p.b_stat + j0, C::STAT_BYTES, &b_full[s]);
+      gf::bulk_g2s(st + BNT, p.lc + j0, C::STAT_BYTES, &b_full[s]);
+      gf::bulk_g2s(st + 2 * BNT, p.lcf + j0, C::STAT_BYTES, &b_full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------------ MMA issuer
+    const uint32_t id_s = idesc_bf16_f32(128, BNT, false, false);
+    const uint32_t id_da = idesc_bf16_f32(128, D, false, true);      // A = W (K-major), B = B tile (MN)
+    const uint32_t id_db = idesc_bf16_f32(128, D, true, true);       // A = W^T (MN), B = A tile (MN)
+    const uint32_t id_cs = idesc_bf16_f32(128, 16, true, true);
+    mbar_wait(a_full, 0);
+    const uint32_t a_base = smem_u32(sA);
+    const uint32_t ones = smem_u32(sOnes);
+    auto issue_s = [&](int t) {
+      const int s = t % STAGES, b = t & 1;
+      mbar_wait(&b_full[s], (t / STAGES) & 1);
+      mbar_wait(&s_empty[b], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        mma_bf16(tm_s[b], smem_desc_sw128(a_base + ks * 32, 16, 1024), smem_desc_sw128(b_base + ks * 32, 16, 1024),
+                 id_s, ks != 0);
+      mma_commit(&s_full[b]);
+    };
+    auto issue_back = [&](int t) {
+      const int s = t % STAGES, b = t & 1;
+      mbar_wait(&w_full[b], (t >> 1) & 1);
+      mbar_wait(&db_empty[b], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
+      const uint32_t w_base = smem_u32(sW + b * C::W_BYTES);
+      // dA += W . B_t   (K = the 128 tile columns j: 64-wide chunks of W 16 KB apart)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int j = 64 * c + 16 * ks;
+          mma_bf16(tm_da, smem_desc_sw128(w_base + c * 16384 + ks * 32, 16, 1024),
+                   smem_desc_sw128(b_base + j * 128, BNT * 128, 1024), id_da, (t | c | ks) != 0);
+        }
+      // dB_t = W^T . A   (K = the 128 tile rows i, 16 per MMA = +2048 B in the SW128 rows)
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        mma_bf16(tm_db[b], smem_desc_sw128(w_base + ks * 2048, 16384, 1024),
+                 smem_desc_sw128(a_base + ks * 2048, 16384, 1024), id_db, ks != 0);
+      if (L2) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          mma_bf16(tm_cs[b], smem_desc_sw128(w_base + ks * 2048, 16384, 1024),
+                   smem_desc_sw128(ones + ks * 2048, 16384, 1024), id_cs, ks != 0);
+      }
+      mma_commit(&db_full[b]);
+      mma_commit(&w_empty[b]);
+      mma_commit(&b_empty[s]);
+    };
+    for (int t = 0; t < ntiles; ++t) {
+      issue_s(t);
+      if (t > 0) issue_back(t - 1);
+    }
+    if (ntiles > 0) issue_back(ntiles - 1);
+    mma_commit(da_full);
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ epilogue
+    const int wg = (warp - 4) >> 2;                       // column half of the tile
+    const int q = warp & 3;                               // TMEM lane quarter
+    const int r = q * 32 + lane;                          // row within the tile
+    const int row = a0 + r;
+    const bool rv = row < p.Na;
+    const bool storer = q == 0 && lane == 0;
+    const float astat = rv ? p.a_stat[row] : 0.f;
+    const float lr2 = rv ? p.lr[row] * gf::kLog2e : INFINITY;      // rows past the batch: p = 0
+    const float lr_nat = rv ? p.lr[row] : 0.f;
+    const bool fac_fast = *p.fac_ok != 0;
+    const float Ei = fac_fast && rv ? gf::ex2(lr2) : 0.f;
+    const float Arow = p.invN * p.c_r + 2.f * p.invN * p.beta_r * lr_nat;
+    const float cc0 = p.invN * p.c_c;
+    const float rmask = rv ? 1.f : 0.f;
+    const uint32_t w_row = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+    float wsum = 0.f;
+
+    // dB_{u} readout: TMEM -> swizzled SMEM staging -> TMA add-reduction into the accumulator
+    auto readout = [&](int u) {
+      const int bu = u & 1;
+      const int j0 = jbeg + u * BNT;
+      mbar_wait(&db_full[bu], (u >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      float cs[16];
+      tmem_ld32_nowait(tm_db[bu] + ((uint32_t)(q * 32) << 16) + 32 * wg, v);
+      if (L2 && wg == 0) tmem_ld16(tm_cs[bu] + ((uint32_t)(q * 32) << 16), cs);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&db_empty[bu]);
+      if (L2 && wg == 0 && j0 + r < jend) atomicAdd(p.cs_acc + j0 + r, cs[0]);
+      // the staging half this warpgroup writes was last read by the reduction of tile u - 2
+      if (storer) gf::bulk_wait_read1();
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
+      const uint32_t dst = smem_u32(sR + bu * C::R_BYTES + wg * 16384) + w_row;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        gf::sts128(dst + (uint32_t)((c ^ (r & 7)) << 4), make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
+      if (storer) {
+        gf::tma_reduce_add_2d(&tmDB, smem_u32(sR + bu * C::R_BYTES + wg * 16384), 32 * wg, j0);
+        gf::bulk_commit();
+      }
+    };
+
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t % STAGES, b = t & 1;
+      const int j0 = jbeg + t * BNT;
+      const int nval = jend - j0;
+      mbar_wait(&s_full[b], (t >> 1) & 1);
+      tc_fence_after();
+      uint32_t raw[2][32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) tmem_ld32_nowait(tm_s[b] + ((uint32_t)(q * 32) << 16) + wg * 64 + 32 * c, raw[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);
+      if (t >= 2) mbar_wait(&w_empty[b], ((t >> 1) - 1) & 1);
+      const float* bst = sStat + s * 3 * BNT;
+      const uint32_t wt = smem_u32(sW + b * C::W_BYTES + wg * 16384) + w_row;
+      auto tile = [&](auto masked) {
+        constexpr bool MASK = decltype(masked)::value;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int c0 = wg * 64 + 32 * c;                // column within the tile
+          float w[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int jl = c0 + i;
+            const float v = __uint_as_float(raw[c][i]);
+            float l, rs = 1.f;
+            if (L2) {
+              const float d2 = fmaxf(fmaf(-2.f, v, astat + bst[jl]), 0.f) + kEpsL2;
+              rs = gf::rsq(d2);
+              l = -d2 * rs;
+            } else {
+              l = v;
+            }
+            float tv = l * gf::kLog2e;
+            if (MASK) tv = jl < nval ? tv : -INFINITY;
+            float g;
+            if (fac_fast) {
+              g = gf::ex2(tv - lr2) * fmaf(Ei, bst[2 * BNT + jl], Arow);
+            } else {
+              const float lc = bst[BNT + jl];
+              g = fmaf(gf::ex2(tv - lr2), Arow, gf::ex2(tv - lc * gf::kLog2e) * cc0) * rmask;
+            }
+            const float wv = L2 ? g * rs : g;
+            if (L2) wsum += wv;
+            w[i] = wv;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = 32 * c + 8 * u;                  // column within this 64-wide half
+            gf::sts128(wt + (uint32_t)((((k >> 3) ^ (r & 7))) << 4),
+                       make_uint4(pack_bf16x2(w[8 * u], w[8 * u + 1]), pack_bf16x2(w[8 * u + 2], w[8 * u + 3]),
+                                  pack_bf16x2(w[8 * u + 4], w[8 * u + 5]), pack_bf16x2(w[8 * u + 6], w[8 * u + 7])));
+          }
+        }
+      };
+      if (nval >= BNT) tile(std::false_type{});
+      else tile(std::true_type{});
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&w_full[b]);
+      if (t > 0) readout(t - 1);
+    }
+    if (ntiles > 0) readout(ntiles - 1);
+    // row side: partial row sums of w (L2) and the split's dA
+    if (wg == 1) sMerge[r] = wsum;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (wg == 0 && rv && L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[r];
+    if (wg == 0) {
+      mbar_wait(da_full, 0);
+      tc_fence_after();
+      float* out = p.part_da + ((size_t)split * p.Na + row) * D;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 16) {
+        float v[16];
+        tmem_ld16(tm_da + ((uint32_t)(q * 32) << 16) + c0, v);
+        if (ntiles == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (rv) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            reinterpret_cast<float4*>(out + c0)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+    }
+    if (storer) gf::bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------------------- host side
+bool make_map_f32(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
+
+bool tc_gradf_supports(int D, int energy) { return D == 64 && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_DOT); }
+
+// the column-side accumulator map: db_acc [Nb][64] fp32, TMA-reduced in boxes {32, 128}
+bool tc_gradf_map(CUtensorMap* m, float* db_acc, int Nb) { return make_map_f32(m, db_acc, 64, Nb, 64, 32, 128); }
+
+template <int E>
+static cudaError_t launch_gf(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& db, const TcGradFArgs& p,
+                             int S, cudaStream_t st) {
+  static bool attr = false;
+  const size_t smem = GfCfg::smem();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gradf_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((p.Na + 127) / 128, S);
+  return launch_pdl(tc_gradf_kernel<E>, grid, dim3(384), smem, st, a, b, db, p);
+}
+
+cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, const __nv_bfloat16* A,
+                              const float* a_stat, const __nv_bfloat16* Bg, const float* b_stat, int row_offset,
+                              float Cdiag, int Na, int D, int S, float* out, __nv_bfloat16* outb, cudaStream_t st);
+
+// Both sides of the gradient.  Row side (A = Phi rows, B = Psi columns): part_da / part_rs
+// per split, merged into dA.  Column side: db_acc [Nb][64] and cs_acc [Nb] must be ZERO on
+// entry (accumulated by reductions), merged into dB.
+cudaError_t tc_grad_fused(int energy, const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mDB, int Na,
+                          int Nb, const float* a_stat, const float* b_stat, const float* lse_row, const float* lse_col,
+                          const float* fac_col, const int* fac_ok, float c_r, float c_c, float beta_r, float invN,
+                          int S, float* part_da, float* part_rs, float* db_acc, float* cs_acc,
+                          const __nv_bfloat16* A, const __nv_bfloat16* B, float* dA, __nv_bfloat16* dAb, float* dB,
+                          __nv_bfloat16* dBb, cudaStream_t st) {
+  TcGradFArgs p{};
+  p.Na = Na; p.Nb = Nb;
+  p.cols_per_split = ((Nb + S - 1) / S + 127) / 128 * 128;
+  p.a_stat = a_stat; p.b_stat = b_stat; p.lr = lse_row; p.lc = lse_col; p.lcf = fac_col; p.fac_ok = fac_ok;
+  p.c_r = c_r; p.c_c = c_c; p.beta_r = beta_r; p.invN = invN;
+  p.part_da = part_da; p.part_rs = part_rs; p.cs_acc = cs_acc;
+  cudaError_t e = energy == CRL_ENERGY_L2 ? launch_gf<CRL_ENERGY_L2>(mA, mB, mDB, p, S, st)
+                                          : launch_gf<CRL_ENERGY_DOT>(mA, mB, mDB, p, S, st);
+  if (e != cudaSuccess) return e;
+  const float Cdiag = invN * (c_r + c_c);
+  e = launch_grad_merge(energy, part_da, part_rs, A, a_stat, B, b_stat, 0, Cdiag, Na, 64, S, dA, dAb, st);
+  if (e != cudaSuccess) return e;
+  // column side: "rows" are the B vectors, the pair partner of B_j is A_j
+  return launch_grad_merge(energy, db_acc, cs_acc, B, b_stat, A, a_stat, 0, Cdiag, Nb, 64, 1, dB, dBb, st);
+}
+
+}  // namespace tc
+}  // namespace crl

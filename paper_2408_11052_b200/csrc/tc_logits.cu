@@ -581,6 +581,20 @@ cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUten
                     (const float*)part_rs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, dA, dAb);
 }
 
+cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, const __nv_bfloat16* A,
+                              const float* a_stat, const __nv_bfloat16* Bg, const float* b_stat, int row_offset,
+                              float Cdiag, int Na, int D, int S, float* out, __nv_bfloat16* outb, cudaStream_t st) {
+  const dim3 g((Na * 32 + 255) / 256);
+  if (energy == CRL_ENERGY_L2)
+    return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2>, g, dim3(256), 0, st, part, prs, A, a_stat, Bg, b_stat,
+                      row_offset, Cdiag, Na, D, S, out, outb);
+  if (energy == CRL_ENERGY_COS)
+    return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, g, dim3(256), 0, st, part, prs, A, a_stat, Bg, b_stat,
+                      row_offset, Cdiag, Na, D, S, out, outb);
+  return launch_pdl(grad_merge_kernel<CRL_ENERGY_DOT>, g, dim3(256), 0, st, part, prs, A, a_stat, Bg, b_stat,
+                    row_offset, Cdiag, Na, D, S, out, outb);
+}
+
 cudaError_t launch_rowstat_bf16(const __nv_bfloat16* x, int N, int D, int energy, float* out, int* fac_ok,
                                 int fac_init, cudaStream_t st) {
   return launch_pdl(rowstat_bf16_kernel, dim3((N * 32 + 255) / 256), dim3(256), 0, st, x, N, D, energy, out,

@@ -26,6 +26,7 @@
 // Row sums stay fp32.  Ragged tiles mask columns j >= N explicitly; rows past the batch are
 // masked through their statistic (L2: |a|^2 = 1e30 -> e = 0; cos: additive -inf mask).
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tc_common.cuh"
@@ -267,7 +268,10 @@ __global__ void __launch_bounds__(384, 1) tc_stats_kernel(const __grid_constant_
       if (t >= 2) mbar_wait(&e_empty[b], ((t >> 1) - 1) & 1);
       const uint32_t st_a = smem_u32(sStat + s * BNT + wg * 64);
       const uint32_t e_a = smem_u32(sE + b * C::E_BYTES + wg * 16384) + e_row;
-      const bool full = nval >= BNT;
+      // two instantiations: full tiles carry no per-element column mask (a uniform `if` inside
+      // one loop gets if-converted into a select per element)
+      auto tile = [&](auto masked) {
+      constexpr bool MASK = decltype(masked)::value;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         float e[32];
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(384, 1) tc_stats_kernel(const __grid_constant_
             e[i] = fs::ex2(l2);
           }
         }
-        if (!full) {                                      // ragged tile: columns j >= N are not logits
+        if (MASK) {                                       // ragged tile: columns j >= N are not logits
 #pragma unroll
           for (int i = 0; i < 32; ++i) e[i] = (wg * 64 + 32 * c + i < nval) ? e[i] : 0.f;
         }
@@ -303,6 +307,9 @@ __global__ void __launch_bounds__(384, 1) tc_stats_kernel(const __grid_constant_
                                 pack_bf16x2(e[8 * u + 4], e[8 * u + 5]), pack_bf16x2(e[8 * u + 6], e[8 * u + 7])));
         }
       }
+      };
+      if (nval >= BNT) tile(std::false_type{});
+      else tile(std::true_type{});
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) { mbar_arrive(&e_full[b]); mbar_arrive(&b_empty[s]); }

@@ -264,6 +264,8 @@ def test_critic_step_bf16_fused_chain(preset, over, monkeypatch):
     ("CRL_FORCE_STATS_FALLBACK", "l2"),   # fused pass runs, its merge flags, exact pass redoes it
     ("CRL_FORCE_STATS_FALLBACK", "cos"),
     ("CRL_NO_FUSED_STATS", "l2"),         # two-call online-max statistics only
+    ("CRL_NO_FUSED_GRAD", "l2"),          # two-call gradient pass (row call + column call)
+    ("CRL_NO_FUSED_GRAD", "dot"),
 ])
 def test_critic_step_bf16_stats_paths(knob, energy, monkeypatch):
     """The one-pass row+column statistics (tc_stats.cu) are the default for L2 / cos at W = 1;
