@@ -133,6 +133,18 @@ def stage_work(stage, cfg, N, Bl):
     fp32 = cfg["precision"] == "fp32"
     dims = lambda i: [i] + [Wd] * depth + [D]
     tc_logits = (not fp32) and D in (64, 128, 256)   # csrc/ctx.h kTcLogitsMinN
+    if stage in ("lse_fused", "grad_fused"):
+        # one-pass statistics (tc_stats.cu) / one-pass gradient (tc_gradf.cu): every logit once,
+        # MUFU ops per logit = 2 for L2 (rsqrt + exp2), 1 for dot / cos (exp2) -- the
+        # algorithmic count of SURVEY §8(d) D3 (4 resp. 2 per step over the two passes)
+        return Bl * N * (2.0 if cfg["energy"] == "l2" else 1.0), "op", "xu"
+    if stage == "dw_db_grouped":
+        # every dW_l = X_l^T dZ_l of both encoders (the bias sums ride on the same tiles)
+        tot = 0.0
+        for ind in (in_phi, in_psi):
+            d = dims(ind)
+            tot += sum(2.0 * Bl * d[l] * d[l + 1] for l in range(len(d) - 1))
+        return tot, "flop", "tensor"
     if stage in ("lse_row", "lse_col", "grad_phi", "grad_psi") and tc_logits:
         # bf16 path: the logits stage is bound by the MUFU/XU pipe: the
         # algorithmic transcendental count of the WHOLE stage is 4 per logit for L2 (one exp +
@@ -177,6 +189,10 @@ def stage_work(stage, cfg, N, Bl):
 
 def roofline(stages, cfg, N, Bl, peaks, peak_kind, clocks, traffic_db):
     known = {k: v for k, v in stages.items() if stage_work(k, cfg, N, Bl)[0] is not None}
+    if "lse_fused" in stages:
+        # lse_row / lse_col are then the exact fallback, gated off by a device flag (early exit)
+        known.pop("lse_row", None)
+        known.pop("lse_col", None)
     name, (ms, cnt) = max(known.items(), key=lambda kv: kv[1][0])
     per_launch_ms = ms / cnt
     work, unit, bound = stage_work(name, cfg, N, Bl)

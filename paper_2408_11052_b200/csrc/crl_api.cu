@@ -145,7 +145,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       }
       c->use_gradf = W == 1 && tc_gradf_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_GRAD");
       if (c->use_gradf) {
-        c->gf_splits = tc_stats_splits(Bl, N, 148);
+        c->gf_splits = tc_gradf_splits(Bl, N, 148);
         c->gf_part_da = s.take<float>((size_t)c->gf_splits * Bl * D);
         c->gf_part_rs = s.take<float>((size_t)c->gf_splits * Bl);
         c->gf_acc_bytes = ((size_t)N * D + N + kStatPad) * 4;

@@ -49,8 +49,10 @@ int tc_logits_splits(int Na, int Nb, int D, int num_sms);
 bool tc_stats_supports(int D, int energy);
 int tc_stats_splits(int Na, int Nb, int num_sms);
 bool tc_gradf_supports(int D, int energy);
+int tc_gradf_splits(int Na, int Nb, int num_sms);
 }  // namespace tc
 using tc::tc_gradf_supports;
+using tc::tc_gradf_splits;
 using tc::tc_logits_supports;
 using tc::tc_logits_splits;
 using tc::tc_stats_supports;

@@ -250,8 +250,12 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
     const float Arow = p.invN * p.c_r + 2.f * p.invN * p.beta_r * lr_nat;
     const float cc0 = p.invN * p.c_c;
     const float rmask = rv ? 1.f : 0.f;
+    constexpr float L2e2 = gf::kLog2e * gf::kLog2e;
+    const float a_l2 = astat * L2e2;
+    const float lsc = L2 ? gf::kLog2e : 1.f;      // L2: w = g rs' L
+    const float EiL = Ei * lsc, ArowL = Arow * lsc, cc0L = cc0 * lsc;
     const uint32_t w_row = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
-    float wsum = 0.f;
+    float wsum4[4] = {0.f, 0.f, 0.f, 0.f};
 
     // dB_{u} readout: TMEM -> swizzled SMEM staging -> TMA add-reduction into the accumulator
     auto readout = [&](int u) {
@@ -299,36 +303,57 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
       if (t >= 2) mbar_wait(&w_empty[b], ((t >> 1) - 1) & 1);
       const float* bst = sStat + s * 3 * BNT;
       const uint32_t wt = smem_u32(sW + b * C::W_BYTES + wg * 16384) + w_row;
-      auto tile = [&](auto masked) {
+      // four instantiations (ragged tile x fast factor path): kernel-uniform choices stay out
+      // of the per-logit code.  Fast L2 path, all in log2 units (L = log2 e):
+      //   d2' = max(L^2 (|a|^2 + |b|^2 - 2 a.b), L^2 eps), rs' = rsqrt(d2') = 1 / (L r)
+      //   t   = l2 - lse2_i = -d2' rs' - lse2_i,  p = 2^t
+      //   w   = g / r = p (E_i cc_j + A_i) L rs'   (L folded into E_i, A_i)
+      auto tile = [&](auto masked, auto fast) {
         constexpr bool MASK = decltype(masked)::value;
+        constexpr bool FAST = decltype(fast)::value;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int c0 = wg * 64 + 32 * c;                // column within the tile
           float w[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int jl = c0 + i;
-            const float v = __uint_as_float(raw[c][i]);
-            float l, rs = 1.f;
-            if (L2) {
-              const float d2 = fmaxf(fmaf(-2.f, v, astat + bst[jl]), 0.f) + kEpsL2;
-              rs = gf::rsq(d2);
-              l = -d2 * rs;
-            } else {
-              l = v;
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 b4 = gf::lds128f(smem_u32(bst + c0 + 4 * i4));
+            const float4 f4 = gf::lds128f(smem_u32(bst + (FAST ? 2 : 1) * BNT + c0 + 4 * i4));
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+            const float ff[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = 4 * i4 + u;
+              const int jl = c0 + i;
+              const float v = __uint_as_float(raw[c][i]);
+              float rs = 1.f, wv;
+              if (FAST) {
+                float tv;
+                if (L2) {
+                  const float d2 = fmaxf(fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2)), kEpsL2 * L2e2);
+                  rs = gf::rsq(d2);
+                  tv = fmaf(-d2, rs, -lr2);
+                } else {
+                  tv = fmaf(v, gf::kLog2e, -lr2);
+                }
+                if (MASK) tv = jl < nval ? tv : -INFINITY;
+                wv = gf::ex2(tv) * fmaf(EiL, ff[u], ArowL);
+              } else {                                    // exact: q = 2^(l2 - lse2'_j)
+                float l2v;
+                if (L2) {
+                  const float d2 = fmaxf(fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2)), kEpsL2 * L2e2);
+                  rs = gf::rsq(d2);
+                  l2v = -d2 * rs;
+                } else {
+                  l2v = v * gf::kLog2e;
+                }
+                if (MASK) l2v = jl < nval ? l2v : -INFINITY;
+                const float qe = gf::ex2(l2v - ff[u] * gf::kLog2e);
+                wv = fmaf(gf::ex2(l2v - lr2), ArowL, qe * cc0L) * rmask;
+              }
+              if (L2) { wv *= rs; wsum4[u] += wv; }
+              w[i] = wv;
             }
-            float tv = l * gf::kLog2e;
-            if (MASK) tv = jl < nval ? tv : -INFINITY;
-            float g;
-            if (fac_fast) {
-              g = gf::ex2(tv - lr2) * fmaf(Ei, bst[2 * BNT + jl], Arow);
-            } else {
-              const float lc = bst[BNT + jl];
-              g = fmaf(gf::ex2(tv - lr2), Arow, gf::ex2(tv - lc * gf::kLog2e) * cc0) * rmask;
-            }
-            const float wv = L2 ? g * rs : g;
-            if (L2) wsum += wv;
-            w[i] = wv;
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -339,8 +364,13 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
           }
         }
       };
-      if (nval >= BNT) tile(std::false_type{});
-      else tile(std::true_type{});
+      if (fac_fast) {
+        if (nval >= BNT) tile(std::false_type{}, std::true_type{});
+        else tile(std::true_type{}, std::true_type{});
+      } else {
+        if (nval >= BNT) tile(std::false_type{}, std::false_type{});
+        else tile(std::true_type{}, std::false_type{});
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&w_full[b]);
@@ -348,6 +378,7 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
     }
     if (ntiles > 0) readout(ntiles - 1);
     // row side: partial row sums of w (L2) and the split's dA
+    const float wsum = (wsum4[0] + wsum4[1]) + (wsum4[2] + wsum4[3]);
     if (wg == 1) sMerge[r] = wsum;
     asm volatile("bar.sync 1, 256;" ::: "memory");
     if (wg == 0 && rv && L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[r];
@@ -384,6 +415,22 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
 bool make_map_f32(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
 
 bool tc_gradf_supports(int D, int energy) { return D == 64 && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_DOT); }
+
+// column splits minimising the makespan (waves x tiles per CTA) of the rb x S grid, <= 16
+int tc_gradf_splits(int Na, int Nb, int num_sms) {
+  const int rb = (Na + 127) / 128;
+  const int tiles = (Nb + 127) / 128;
+  int best = 1;
+  long best_cost = -1;
+  for (int s = 1; s <= 16 && s <= tiles; ++s) {
+    const int cps = (tiles + s - 1) / s;
+    const int sp = (tiles + cps - 1) / cps;
+    const long waves = ((long)rb * sp + num_sms - 1) / num_sms;
+    const long cost = waves * cps;
+    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = sp; }
+  }
+  return best;
+}
 
 // the column-side accumulator map: db_acc [Nb][64] fp32, TMA-reduced in boxes {32, 128}
 bool tc_gradf_map(CUtensorMap* m, float* db_acc, int Nb) { return make_map_f32(m, db_acc, 64, Nb, 64, 32, 128); }

@@ -13,18 +13,22 @@
 // detects it and raises a device flag that runs the exact online-max path instead
 // (reading A-29), so the result never silently loses precision.
 //
-// One CTA = 128 rows of A (Phi) x one column split of B (Psi).  Per 128-column tile:
+// Persistent kernel: one CTA per SM walks work units (row block rb of 128 rows of A = Phi,
+// column chunk ch of B = Psi); the TMEM / barrier pipeline runs across unit boundaries (the A
+// tile is double-buffered).  Per 128-column tile:
 //   S = A . B^T                    tcgen05.mma (M=128, N=128, K=D) into TMEM (double-buffered)
-//   epilogue (thread = row):       e_ij = 2^(l_ij log2 e), row sum in registers, and the bf16
-//                                  tile E written to SMEM (SW128, the layout an MN-major
-//                                  operand expects)
+//   epilogue (thread = row, 4 warpgroups x 32 columns): e_ij = 2^(l_ij log2 e) with packed
+//                                  FFMA2 / FADD2 math, row sums in registers, the bf16 tile E
+//                                  written to SMEM (SW128, the layout an MN-major operand expects)
 //   C = 1 . E                      tcgen05.mma (M=128, N=128, K=128 rows) with an all-ones A:
 //                                  every row of C holds the 128 column sums of the tile
-//   readout (warp 3)               one TMEM row -> colpart[row block][j]
+//   readout (warp 3)               one TMEM row -> colpart[rb][j]
+// Row sums of a unit -> part_rs[ch][row]; stats_merge adds the chunks and the row blocks.
 // E is rounded to bf16 for the column-sum MMA (fp32 accumulation): relative error <= 2^-9
 // per term, unbiased (round-to-nearest), within the path's 2e-2 tolerance (north_star).
-// Row sums stay fp32.  Ragged tiles mask columns j >= N explicitly; rows past the batch are
-// masked through their statistic (L2: |a|^2 = 1e30 -> e = 0; cos: additive -inf mask).
+// Ragged tiles mask columns j >= N explicitly; rows past the batch are masked through their
+// statistic (L2: |a|^2 = 1e30 -> e = 0; cos: additive -1e30 mask).
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -44,10 +48,30 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float rsq(float x) {
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
+// 2^x for a PAIR of x <= 0 on the FMA / ALU pipes (no MUFU): x = n + f with n = rint(x) from
+// the 1.5 * 2^23 shifter, 2^f by the degree-5 Taylor polynomial on [-1/2, 1/2] (relative error
+// < 4e-6) in packed FFMA2, 2^n added to the exponent bits.  x is clamped at -126 through an
+// unsigned min on the bit patterns (x <= 0), so the result is >= 2^-126 > 0 (not an exact
+// zero like ex2.approx.ftz: irrelevant next to the sums it feeds).  A share of the logits
+// takes this path so the XU pipe is not the only unit doing exponentials.
+__device__ __forceinline__ void ex2_pair_fma(float x0, float x1, float& y0, float& y1) {
+  const unsigned lim = 0xC2FC0000u;                 // bits of -126.0f
+  x0 = __uint_as_float(min(__float_as_uint(x0), lim));
+  x1 = __uint_as_float(min(__float_as_uint(x1), lim));
+  const f32x2 x = f2_pack(x0, x1);
+  const f32x2 sh = f2_pack(12582912.f, 12582912.f);
+  const f32x2 j = f2_add(x, sh);
+  const f32x2 f = f2_add(x, f2_fma(j, f2_pack(-1.f, -1.f), sh));   // x - (j - sh) = x - rint(x)
+  f32x2 pp = f2_fma(f2_pack(1.3333558146e-3f, 1.3333558146e-3f), f, f2_pack(9.6181291076e-3f, 9.6181291076e-3f));
+  pp = f2_fma(pp, f, f2_pack(5.5504108665e-2f, 5.5504108665e-2f));
+  pp = f2_fma(pp, f, f2_pack(2.4022650695e-1f, 2.4022650695e-1f));
+  pp = f2_fma(pp, f, f2_pack(6.9314718056e-1f, 6.9314718056e-1f));
+  pp = f2_fma(pp, f, f2_pack(1.f, 1.f));
+  float j0, j1, p0, p1;
+  f2_unpack(j, j0, j1);
+  f2_unpack(pp, p0, p1);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(j0) << 23));   // low bits of j hold n
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(j1) << 23));
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -68,13 +92,24 @@ __device__ __forceinline__ float4 lds128f(uint32_t a) {
 
 struct TcStatsArgs {
   int Na, Nb;
-  int cols_per_split;              // multiple of 128
+  int n_chunks;                    // column chunks per row block (work unit = (rb, chunk))
+  int tiles_per_chunk;             // 128-column tiles per chunk
+  int n_units;                     // row blocks x n_chunks
   const float* a_stat;             // [Na]  L2: |a|^2, cos: 1/max(|a|, eps)
   const float* b_stat;             // [Nb + pad]
-  float* part_rs;                  // [S][Na] row sums of e_ij over this split's columns
-  float* colpart;                  // [R][ldc] column sums of e_ij over this CTA's 128 rows
+  float* part_rs;                  // [n_chunks][Na] row sums of e_ij over one chunk
+  float* colpart;                  // [R][ldc] column sums of e_ij over one row block
   int ldc;
+  int trace;                       // measurement: clock64 trace of CTA 0 (CRL_STATS_TRACE)
 };
+
+constexpr int kStNWG = 4;          // epilogue warpgroups
+#ifndef CRL_ST_EMU
+#define CRL_ST_EMU 0
+#endif
+// of every 4 logit pairs, this many exp2 pairs skip the MUFU (measured on B200 at N = 16384:
+// 1 of 4 is neutral, 186 -> 185 us: the tile loop is latency- not XU-throughput-bound)
+constexpr int kStEmuPairs = CRL_ST_EMU;
 
 template <int D>
 struct StCfg {
@@ -87,27 +122,29 @@ struct StCfg {
   static constexpr uint32_t ONES_BYTES = 128 * 128 * 2;  // all-ones A operand (M=128, K=128)
   static constexpr uint32_t STAT_BYTES = BNT * 4;
   static constexpr size_t smem() {
-    return 1024 + A_BYTES + STAGES * B_BYTES + 2 * E_BYTES + ONES_BYTES + STAGES * STAT_BYTES + 512 + 256;
+    return 1024 + 2 * A_BYTES + STAGES * B_BYTES + 2 * E_BYTES + ONES_BYTES + STAGES * STAT_BYTES + 3 * 512 + 256;
   }
 };
 
 template <int D, int ENERGY>
-__global__ void __launch_bounds__(384, 1) tc_stats_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                          const __grid_constant__ CUtensorMap tmB,
-                                                          TcStatsArgs p) {
+__global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                        const __grid_constant__ CUtensorMap tmB,
+                                                                        TcStatsArgs p) {
   using C = StCfg<D>;
   constexpr int BNT = C::BNT, STAGES = C::STAGES, KC = C::KC;
+  constexpr int NWG = kStNWG, CW = BNT / NWG, NCH = CW / 32;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + C::A_BYTES;
+  uint8_t* sA = smem;                                                 // [2] row-block tiles
+  uint8_t* sB = sA + 2 * C::A_BYTES;
   uint8_t* sE = sB + STAGES * C::B_BYTES;
   uint8_t* sOnes = sE + 2 * C::E_BYTES;
   float* sStat = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);     // [STAGES][BNT]
-  float* sM = sStat + STAGES * BNT;                                   // [128] row-sum hand-off
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sM + 128);
-  uint64_t* a_full = bars;
-  uint64_t* b_full = bars + 1;
+  float* sM = sStat + STAGES * BNT;                                   // [NWG-1][128] row-sum hand-off
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sM + 3 * 128);
+  uint64_t* a_full = bars;                // [2]
+  uint64_t* a_empty = a_full + 2;         // [2]
+  uint64_t* b_full = a_empty + 2;
   uint64_t* b_empty = b_full + STAGES;
   uint64_t* s_full = b_empty + STAGES;    // [2]
   uint64_t* s_empty = s_full + 2;         // [2]
@@ -118,23 +155,26 @@ __global__ void __launch_bounds__(384, 1) tc_stats_kernel(const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rb = blockIdx.x;
-  const int a0 = rb * 128;
-  const int split = blockIdx.y;
-  const int jbeg = split * p.cols_per_split;
-  const int jend = min(p.Nb, jbeg + p.cols_per_split);
-  const int ntiles = jend > jbeg ? (jend - jbeg + BNT - 1) / BNT : 0;
+  const int G = gridDim.x;
+  // the units of this CTA: u = blockIdx.x + k G; unit u = (rb, ch), tiles [ch tpc, (ch+1) tpc)
+  auto unit_rb = [&](int u) { return u / p.n_chunks; };
+  auto unit_j0 = [&](int u) { return (u % p.n_chunks) * p.tiles_per_chunk * BNT; };
+  auto unit_ntiles = [&](int u) {
+    const int j0 = unit_j0(u);
+    const int j1 = min(p.Nb, j0 + p.tiles_per_chunk * BNT);
+    return j1 > j0 ? (j1 - j0 + BNT - 1) / BNT : 0;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    mbar_init(a_full, 1);
-    // a B stage is free once S(t) is computed (MMA commit) and the 8 epilogue warps are done
+    for (int i = 0; i < 2; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
+    // a B stage is free once S(t) is computed (MMA commit) and the epilogue warps are done
     // with its column statistics
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 9); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1 + 4 * NWG); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
-      mbar_init(&e_full[i], 8); mbar_init(&e_empty[i], 1);
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4 * NWG);
+      mbar_init(&e_full[i], 4 * NWG); mbar_init(&e_empty[i], 1);
       mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 1);
     }
     fence_mbar_init();
@@ -152,48 +192,40 @@ __global__ void __launch_bounds__(384, 1) tc_stats_kernel(const __grid_constant_
   const uint32_t tm_c[2] = {tmem + 256, tmem + 384};
   pdl_wait();
   pdl_launch();
+  __shared__ long long s_tr[4][16];
+  const bool trace = p.trace && blockIdx.x == 0;
+  if (trace && threadIdx.x == 0) s_tr[0][0] = clock64();
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------------ TMA producer
-    mbar_expect_tx(a_full, C::A_BYTES);
+    int g = 0, k = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += G, ++k) {
+      const int ua = k & 1;
+      mbar_wait(&a_empty[ua], ((k >> 1) & 1) ^ 1);
+      mbar_expect_tx(&a_full[ua], C::A_BYTES);
 #pragma unroll
-    for (int c = 0; c < KC; ++c) tma_load_2d(sA + c * 128 * 128, &tmA, a_full, 64 * c, a0);
-    for (int t = 0; t < ntiles; ++t) {
-      const int s = t % STAGES;
-      mbar_wait(&b_empty[s], ((t / STAGES) & 1) ^ 1);
-      const int j0 = jbeg + t * BNT;
-      mbar_expect_tx(&b_full[s], C::B_BYTES + C::STAT_BYTES);
-      uint8_t* dst = sB + s * C::B_BYTES;
+      for (int c = 0; c < KC; ++c) tma_load_2d(sA + ua * C::A_BYTES + c * 16384, &tmA, &a_full[ua], 64 * c, unit_rb(u) * 128);
+      const int nt = unit_ntiles(u), j00 = unit_j0(u);
+      for (int t = 0; t < nt; ++t, ++g) {
+        const int s = g % STAGES;
+        mbar_wait(&b_empty[s], ((g / STAGES) & 1) ^ 1);
+        const int j0 = j00 + t * BNT;
+        mbar_expect_tx(&b_full[s], C::B_BYTES + C::STAT_BYTES);
+        uint8_t* dst = sB + s * C::B_BYTES;
 #pragma unroll
-      for (int c = 0; c < KC; ++c) tma_load_2d(dst + c * BNT * 128, &tmB, &b_full[s], 64 * c, j0);
-      fs::bulk_g2s(sStat + s * BNT, p.b_stat + j0, C::STAT_BYTES, &b_full[s]);
+        for (int c = 0; c < KC; ++c) tma_load_2d(dst + c * BNT * 128, &tmB, &b_full[s], 64 * c, j0);
+        fs::bulk_g2s(sStat + s * BNT, p.b_stat + j0, C::STAT_BYTES, &b_full[s]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ------------------------------------------------------------------ MMA issuer
     const uint32_t id_s = idesc_bf16_f32(128, BNT, false, false);
     const uint32_t id_c = idesc_bf16_f32(128, BNT, false, true);     // B = E is MN-major
-    mbar_wait(a_full, 0);
-    const uint32_t a_base = smem_u32(sA);
     const uint32_t ones = smem_u32(sOnes);
-    auto issue_s = [&](int t) {
-      const int s = t % STAGES, b = t & 1;
-      mbar_wait(&b_full[s], (t / STAGES) & 1);
-      mbar_wait(&s_empty[b], ((t >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
-#pragma unroll
-      for (int c = 0; c < KC; ++c)
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          mma_bf16(tm_s[b], smem_desc_sw128(a_base + c * 16384 + ks * 32, 16, 1024),
-                   smem_desc_sw128(b_base + c * BNT * 128 + ks * 32, 16, 1024), id_s, (c | ks) != 0);
-      mma_commit(&s_full[b]);
-      mma_commit(&b_empty[s]);
-    };
-    auto issue_c = [&](int t) {
-      const int b = t & 1;
-      mbar_wait(&e_full[b], (t >> 1) & 1);
-      mbar_wait(&c_empty[b], ((t >> 1) & 1) ^ 1);
+    auto issue_c = [&](int g) {
+      const int b = g & 1;
+      mbar_wait(&e_full[b], (g >> 1) & 1);
+      mbar_wait(&c_empty[b], ((g >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t e_base = smem_u32(sE + b * C::E_BYTES);
       // K = the 128 rows of E, 16 per MMA (+2048 B in the MN-major SW128 layout); the two
@@ -205,119 +237,176 @@ __global__ void __launch_bounds__(384, 1) tc_stats_kernel(const __grid_constant_
       mma_commit(&c_full[b]);
       mma_commit(&e_empty[b]);
     };
-    for (int t = 0; t < ntiles; ++t) {
-      issue_s(t);
-      if (t > 0) issue_c(t - 1);
+    int g = 0, k = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += G, ++k) {
+      const int ua = k & 1;
+      mbar_wait(&a_full[ua], (k >> 1) & 1);
+      const uint32_t a_base = smem_u32(sA + ua * C::A_BYTES);
+      const int nt = unit_ntiles(u);
+      if (nt == 0) mma_commit(&a_empty[ua]);                // empty chunk: hand the A buffer back
+      for (int t = 0; t < nt; ++t, ++g) {
+        const int s = g % STAGES, b = g & 1;
+        mbar_wait(&b_full[s], (g / STAGES) & 1);
+        mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+        if (trace && g < 15) s_tr[1][g + 1] = clock64();
+        tc_fence_after();
+        const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+        for (int c = 0; c < KC; ++c)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            mma_bf16(tm_s[b], smem_desc_sw128(a_base + c * 16384 + ks * 32, 16, 1024),
+                     smem_desc_sw128(b_base + c * BNT * 128 + ks * 32, 16, 1024), id_s, (c | ks) != 0);
+        mma_commit(&s_full[b]);
+        mma_commit(&b_empty[s]);
+        if (t == nt - 1) mma_commit(&a_empty[ua]);        // last S of the unit read this A tile
+        if (g > 0) issue_c(g - 1);
+      }
     }
-    if (ntiles > 0) issue_c(ntiles - 1);
+    if (g > 0) issue_c(g - 1);
   } else if (warp == 3) {
     // ------------------------------------------------------------------ column-sum readout
     // every TMEM row of C holds the same 128 column sums; this warp reads its lane quarter
-    float* out = p.colpart + (size_t)rb * p.ldc;
-    for (int t = 0; t < ntiles; ++t) {
-      const int b = t & 1;
-      const int j0 = jbeg + t * BNT;
-      mbar_wait(&c_full[b], (t >> 1) & 1);
-      tc_fence_after();
-      uint32_t v[4][32];
+    int g = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += G) {
+      float* out = p.colpart + (size_t)unit_rb(u) * p.ldc;
+      const int nt = unit_ntiles(u), j00 = unit_j0(u);
+      const int jend = min(p.Nb, j00 + p.tiles_per_chunk * BNT);
+      for (int t = 0; t < nt; ++t, ++g) {
+        const int b = g & 1;
+        const int j0 = j00 + t * BNT;
+        mbar_wait(&c_full[b], (g >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32];
+          tmem_ld32_nowait(tm_c[b] + (96u << 16) + 32 * c, v);
+          tmem_ld_wait();
+          uint32_t mine = 0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32_nowait(tm_c[b] + (96u << 16) + 32 * c, v[c]);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&c_empty[b]);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t mine = 0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) mine = (i == lane) ? v[c][i] : mine;
-        const int j = j0 + 32 * c + lane;
-        if (j < jend) out[j] = __uint_as_float(mine);
+          for (int i = 0; i < 32; ++i) mine = (i == lane) ? v[i] : mine;
+          const int j = j0 + 32 * c + lane;
+          if (j < jend) out[j] = __uint_as_float(mine);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c_empty[b]);
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
-    const int wg = (warp - 4) >> 2;                       // 64-column half of the tile
+    // NWG warpgroups split the 128 columns of a tile (CW each): 4 warps per SMSP hide the
+    // MUFU / TMEM latencies of the per-logit chain
+    const int wg = (warp - 4) >> 2;                       // column group of the tile
     const int q = warp & 3;                               // TMEM lane quarter
     const int r = q * 32 + lane;                          // row within the tile
-    const int row = a0 + r;
-    const bool rv = row < p.Na;
     constexpr float L2e2 = fs::kLog2e * fs::kLog2e;
-    // L2: d2' = (|a|^2 + |b|^2 - 2 a.b) (log2 e)^2, l2 = -sqrt(d2') (log2 units); rows past
-    // the batch get |a|^2 = 1e30 so e = 0.  cos: l2 = a.b (1/|a|)(1/|b|) log2 e + mask_i.
-    const float astat = rv ? p.a_stat[row] : fs::kMaskBig;
-    const float a_l2 = astat * L2e2;
-    const float a_cos = rv ? astat * fs::kLog2e : 0.f;
-    const float m_cos = rv ? 0.f : -fs::kMaskBig;
     const uint32_t e_row = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
-    float rsum = 0.f;
-    for (int t = 0; t < ntiles; ++t) {
-      const int s = t % STAGES, b = t & 1;
-      const int j0 = jbeg + t * BNT;
-      const int nval = jend - j0;
-      mbar_wait(&s_full[b], (t >> 1) & 1);
-      tc_fence_after();
-      uint32_t raw[2][32];
+    const int cg0 = wg * CW;                              // first column of this group
+    int g = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += G) {
+      const int row = unit_rb(u) * 128 + r;
+      const bool rv = row < p.Na;
+      // L2: d2' = (|a|^2 + |b|^2 - 2 a.b) (log2 e)^2, e = 2^-sqrt(d2') (log2 units); rows
+      // past the batch get |a|^2 = 1e30 so e = 0.  cos: l2 = a.b (1/|a|)(1/|b|) log2 e + mask
+      const float astat = rv ? p.a_stat[row] : fs::kMaskBig;
+      const f32x2 kL2 = f2_pack(L2e2, L2e2);
+      const f32x2 kM2 = ENERGY == CRL_ENERGY_L2 ? f2_pack(-2.f * L2e2, -2.f * L2e2)
+                                                : f2_pack(rv ? 0.f : -fs::kMaskBig, rv ? 0.f : -fs::kMaskBig);
+      const float ka = ENERGY == CRL_ENERGY_L2 ? astat * L2e2 : (rv ? astat * fs::kLog2e : 0.f);
+      const f32x2 kA2 = f2_pack(ka, ka);
+      f32x2 racc[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
+      const int nt = unit_ntiles(u), j00 = unit_j0(u);
+      const int jend = min(p.Nb, j00 + p.tiles_per_chunk * BNT);
+      for (int t = 0; t < nt; ++t, ++g) {
+        const int s = g % STAGES, b = g & 1;
+        const int nval = jend - (j00 + t * BNT);
+        mbar_wait(&s_full[b], (g >> 1) & 1);
+        if (trace && threadIdx.x == 128 && g < 15) s_tr[2][g + 1] = clock64();
+        tc_fence_after();
+        uint32_t raw[NCH][32];
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-        tmem_ld32_nowait(tm_s[b] + ((uint32_t)(q * 32) << 16) + wg * 64 + 32 * c, raw[c]);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[b]);
-      if (t >= 2) mbar_wait(&e_empty[b], ((t >> 1) - 1) & 1);
-      const uint32_t st_a = smem_u32(sStat + s * BNT + wg * 64);
-      const uint32_t e_a = smem_u32(sE + b * C::E_BYTES + wg * 16384) + e_row;
-      // two instantiations: full tiles carry no per-element column mask (a uniform `if` inside
-      // one loop gets if-converted into a select per element)
-      auto tile = [&](auto masked) {
-      constexpr bool MASK = decltype(masked)::value;
+        for (int c = 0; c < NCH; ++c)
+          tmem_ld32_nowait(tm_s[b] + ((uint32_t)(q * 32) << 16) + cg0 + 32 * c, raw[c]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[b]);
+        if (g >= 2) mbar_wait(&e_empty[b], ((g >> 1) - 1) & 1);
+        const uint32_t st_a = smem_u32(sStat + s * BNT + cg0);
+        const uint32_t e_a = smem_u32(sE + b * C::E_BYTES + (cg0 >> 6) * 16384) + e_row;
+        // two instantiations: full tiles carry no per-element column mask (a uniform `if`
+        // inside one loop gets if-converted into a select per element)
+        auto tile = [&](auto masked) {
+          constexpr bool MASK = decltype(masked)::value;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float e[32];
+          for (int c = 0; c < NCH; ++c) {
+            float e[32];
+            // pairs of logits per FFMA2 / FADD2 (sm_100 packed fp32); L2: e = 2^-sqrt(|d2'|)
+            // (|.| and the negation are free MUFU operand modifiers, sqrt(0) = 0 needs no
+            // epsilon: the oracle's sqrt(d2 + 1e-12) differs by <= 1e-6)
 #pragma unroll
-        for (int i4 = 0; i4 < 8; ++i4) {
-          const float4 bs = fs::lds128f(st_a + (uint32_t)(32 * c + 4 * i4) * 4u);
-          const float bb[4] = {bs.x, bs.y, bs.z, bs.w};
+            for (int i4 = 0; i4 < 8; ++i4) {
+              const float4 bs = fs::lds128f(st_a + (uint32_t)(32 * c + 4 * i4) * 4u);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = 4 * i4 + u;
-            const float v = __uint_as_float(raw[c][i]);
-            float l2;
-            if (ENERGY == CRL_ENERGY_L2) {
-              const float d2 = fmaxf(fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2)), kEpsL2 * L2e2);
-              l2 = -d2 * fs::rsq(d2);
-            } else {
-              l2 = fmaf(v * bb[u], a_cos, m_cos);
+              for (int h = 0; h < 2; ++h) {
+                const int i = 4 * i4 + 2 * h;
+                const f32x2 v2 = f2_pack(__uint_as_float(raw[c][i]), __uint_as_float(raw[c][i + 1]));
+                const f32x2 b2 = h ? f2_pack(bs.z, bs.w) : f2_pack(bs.x, bs.y);
+                float x0, x1;
+                if (ENERGY == CRL_ENERGY_L2) {
+                  f2_unpack(f2_fma(kM2, v2, f2_fma(kL2, b2, kA2)), x0, x1);
+                  if (((2 * i4 + h) & 3) < kStEmuPairs) {       // exp2 of this pair on FMA / ALU
+                    fs::ex2_pair_fma(-sqrt_abs(x0), -sqrt_abs(x1), e[i], e[i + 1]);
+                  } else {
+                    e[i] = ex2_neg(sqrt_abs(x0));
+                    e[i + 1] = ex2_neg(sqrt_abs(x1));
+                  }
+                } else {
+                  f2_unpack(f2_fma(f2_mul(v2, b2), kA2, kM2), x0, x1);
+                  e[i] = fs::ex2(x0);
+                  e[i + 1] = fs::ex2(x1);
+                }
+              }
             }
-            e[i] = fs::ex2(l2);
+            if (MASK) {                                   // ragged tile: columns j >= N are not logits
+#pragma unroll
+              for (int i = 0; i < 32; ++i) e[i] = (cg0 + 32 * c + i < nval) ? e[i] : 0.f;
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2) racc[k2 & 1] = f2_add(racc[k2 & 1], f2_pack(e[2 * k2], e[2 * k2 + 1]));
+#pragma unroll
+            for (int v4 = 0; v4 < 4; ++v4) {
+              const int kk = (cg0 & 63) + 32 * c + 8 * v4;   // column within the 64-wide chunk
+              fs::sts128(e_a + (uint32_t)((((kk >> 3) ^ (r & 7))) << 4),
+                         make_uint4(pack_bf16x2(e[8 * v4], e[8 * v4 + 1]), pack_bf16x2(e[8 * v4 + 2], e[8 * v4 + 3]),
+                                    pack_bf16x2(e[8 * v4 + 4], e[8 * v4 + 5]),
+                                    pack_bf16x2(e[8 * v4 + 6], e[8 * v4 + 7])));
+            }
           }
-        }
-        if (MASK) {                                       // ragged tile: columns j >= N are not logits
-#pragma unroll
-          for (int i = 0; i < 32; ++i) e[i] = (wg * 64 + 32 * c + i < nval) ? e[i] : 0.f;
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) rsum += e[i];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = 32 * c + 8 * u;                    // column within this 64-wide half
-          fs::sts128(e_a + (uint32_t)((((k >> 3) ^ (r & 7))) << 4),
-                     make_uint4(pack_bf16x2(e[8 * u], e[8 * u + 1]), pack_bf16x2(e[8 * u + 2], e[8 * u + 3]),
-                                pack_bf16x2(e[8 * u + 4], e[8 * u + 5]), pack_bf16x2(e[8 * u + 6], e[8 * u + 7])));
-        }
+        };
+        if (nval >= BNT) tile(std::false_type{});
+        else tile(std::true_type{});
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&e_full[b]); mbar_arrive(&b_empty[s]); }
+        if (trace && threadIdx.x == 128 && g < 15) s_tr[3][g + 1] = clock64();
       }
-      };
-      if (nval >= BNT) tile(std::false_type{});
-      else tile(std::true_type{});
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) { mbar_arrive(&e_full[b]); mbar_arrive(&b_empty[s]); }
+      // row sums of the unit: warpgroups 1.. hand their partial sums to warpgroup 0
+      float r0, r1, r2, r3;
+      f2_unpack(racc[0], r0, r1);
+      f2_unpack(racc[1], r2, r3);
+      const float rsum = (r0 + r1) + (r2 + r3);
+      if (wg > 0) sM[(wg - 1) * 128 + r] = rsum;
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * NWG) : "memory");
+      if (wg == 0 && rv) {
+        float tot = rsum;
+#pragma unroll
+        for (int gg = 1; gg < NWG; ++gg) tot += sM[(gg - 1) * 128 + r];
+        p.part_rs[(size_t)(u % p.n_chunks) * p.Na + row] = tot;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * NWG) : "memory");   // sM reusable
     }
-    // row sums: warpgroup 1 hands its half to warpgroup 0
-    if (wg == 1) sM[r] = rsum;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (wg == 0 && rv) p.part_rs[(size_t)split * p.Na + row] = rsum + sM[r];
   }
   tc_fence_before();
   __syncthreads();
@@ -325,11 +414,14 @@ __global__ void __launch_bounds__(384, 1) tc_stats_kernel(const __grid_constant_
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  if (trace && threadIdx.x == 0)
+    for (int k = 1; k < 4; ++k)
+      for (int t = 1; t < 16; ++t) printf("STATS_TRACE %d %d %lld\n", k, t - 1, s_tr[k][t] - s_tr[0][0]);
 }
 
 // LSE from plain sums (the fused pass has no running max: shift 0):
-//   threads [0, Na):       LSE_i  = ln sum_s part_rs[s][i]             -> lse_row, fac_row
-//   threads [Na, Na + Nb): LSE'_j = ln sum_r colpart[r][j] (or colsum) -> lse_col, fac_col
+//   threads [0, Na):       LSE_i  = ln sum_s part_rs[s][i]   -> lse_row, fac_row
+//   threads [Na, Na + Nb): LSE'_j = ln sum_r colpart[r][j]   -> lse_col, fac_col
 // fac = 2^-LSE2 (cc0 + cc1 LSE) as in lse_merge (tc_logits.cu).  A sum that is not a normal,
 // finite float well above the underflow range sets *bad (exact online-max path runs).
 __global__ void stats_merge_kernel(const float* __restrict__ part_rs, int S, int Na, const float* __restrict__ colpart,
@@ -365,51 +457,54 @@ bool tc_stats_supports(int D, int energy) {
   return (D == 64 || D == 128) && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_COS);
 }
 
+// Column chunks per row block: enough work units to balance the persistent grid (~8 per SM)
+// without units shorter than 2 tiles; at most 16 (row-sum partials per row).
 int tc_stats_splits(int Na, int Nb, int num_sms) {
   const int rb = (Na + 127) / 128;
   const int tiles = (Nb + 127) / 128;
-  int best = 1;
-  long best_cost = -1;
-  for (int s = 1; s <= 16 && s <= tiles; ++s) {
-    const int cps = (tiles + s - 1) / s;
-    const int sp = (tiles + cps - 1) / cps;
-    const long ctas = (long)rb * sp;
-    const long waves = (ctas + num_sms - 1) / num_sms;
-    const long cost = waves * cps;
-    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = sp; }
-  }
-  return best;
+  int ch = 1;
+  while (ch < 16 && ch * 2 <= tiles && (long)rb * ch < 8L * num_sms) ch *= 2;
+  return ch;
 }
 
+static int g_stats_sms = 148;
+
 template <int D, int ENERGY>
-static cudaError_t launch_st(const CUtensorMap& a, const CUtensorMap& b, const TcStatsArgs& p, int S, cudaStream_t st) {
+static cudaError_t launch_st(const CUtensorMap& a, const CUtensorMap& b, const TcStatsArgs& p, cudaStream_t st) {
   static bool attr = false;
   const size_t smem = StCfg<D>::smem();
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_stats_kernel<D, ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_stats_sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
-  dim3 grid((p.Na + 127) / 128, S);
-  return launch_pdl(tc_stats_kernel<D, ENERGY>, grid, dim3(384), smem, st, a, b, p);
+  dim3 grid(min(p.n_units, g_stats_sms));
+  return launch_pdl(tc_stats_kernel<D, ENERGY>, grid, dim3(128 + 128 * kStNWG), smem, st, a, b, p);
 }
 
 // One fused statistics pass + merge.  mA/mB: the logits operand maps (A box {64,128},
-// B box {64,128}: tc_logits_maps with D <= 128).  part_rs [S][Na], colpart [R][Nb + pad].
+// B box {64,128}: tc_logits_maps with D <= 128).  part_rs [S][Na] (S = tc_stats_splits),
+// colpart [R][ldc].
 cudaError_t tc_stats_fused(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                            const float* a_stat, const float* b_stat, int S, float* part_rs, float* colpart, int ldc,
                            float* lse_row, float* fac_row, float* lse_col, float* fac_col, int* fac_ok, int* bad,
                            float rc0, float rc1, float cc0, float cc1, cudaStream_t st) {
   TcStatsArgs p{};
   p.Na = Na; p.Nb = Nb;
-  p.cols_per_split = ((Nb + S - 1) / S + 127) / 128 * 128;
+  const int tiles = (Nb + 127) / 128;
+  p.n_chunks = S;
+  p.tiles_per_chunk = (tiles + S - 1) / S;
+  p.n_units = ((Na + 127) / 128) * S;
   p.a_stat = a_stat; p.b_stat = b_stat; p.part_rs = part_rs; p.colpart = colpart; p.ldc = ldc;
+  p.trace = std::getenv("CRL_STATS_TRACE") ? 1 : 0;
   cudaError_t e;
-  if (D == 64) e = energy == CRL_ENERGY_L2 ? launch_st<64, CRL_ENERGY_L2>(mA, mB, p, S, st)
-                                           : launch_st<64, CRL_ENERGY_COS>(mA, mB, p, S, st);
-  else if (D == 128) e = energy == CRL_ENERGY_L2 ? launch_st<128, CRL_ENERGY_L2>(mA, mB, p, S, st)
-                                                 : launch_st<128, CRL_ENERGY_COS>(mA, mB, p, S, st);
+  if (D == 64) e = energy == CRL_ENERGY_L2 ? launch_st<64, CRL_ENERGY_L2>(mA, mB, p, st)
+                                           : launch_st<64, CRL_ENERGY_COS>(mA, mB, p, st);
+  else if (D == 128) e = energy == CRL_ENERGY_L2 ? launch_st<128, CRL_ENERGY_L2>(mA, mB, p, st)
+                                                 : launch_st<128, CRL_ENERGY_COS>(mA, mB, p, st);
   else return cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
   const int R = (Na + 127) / 128;
