@@ -193,6 +193,8 @@ def roofline(stages, cfg, N, Bl, peaks, peak_kind, clocks, traffic_db):
         # lse_row / lse_col are then the exact fallback, gated off by a device flag (early exit)
         known.pop("lse_row", None)
         known.pop("lse_col", None)
+    if not known:
+        return None                      # --profile-steps 0: no per-stage measurement
     name, (ms, cnt) = max(known.items(), key=lambda kv: kv[1][0])
     per_launch_ms = ms / cnt
     work, unit, bound = stage_work(name, cfg, N, Bl)

@@ -27,13 +27,13 @@ namespace tc {
 bool make_map_bf16(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
 int tc_pick_bn(int M, int N, int num_sms);
 cudaError_t tc_forward(int, const CUtensorMap&, const CUtensorMap&, int, int, int, const float*,
-                       __nv_bfloat16*, __nv_bfloat16*, int, float*, int, int, cudaStream_t);
+                       __nv_bfloat16*, __nv_bfloat16*, int, float*, int, int, float*, int, cudaStream_t);
 cudaError_t tc_backward_dx(int, const CUtensorMap&, const CUtensorMap&, int, int, int,
                            const __nv_bfloat16*, __nv_bfloat16*, int, int, cudaStream_t);
 cudaError_t tc_backward_dw(int, const CUtensorMap&, const CUtensorMap&, int, int, int, float*, int,
                            size_t, cudaStream_t);
 cudaError_t launch_prep_inputs(const float*, const float*, const float*, int, int, int, int,
-                               __nv_bfloat16*, int, __nv_bfloat16*, int, int, int*, cudaStream_t);
+                               __nv_bfloat16*, int, __nv_bfloat16*, int, int, int*, int*, int, cudaStream_t);
 cudaError_t launch_colsum_bf16(const __nv_bfloat16*, int, int, int, float*, int, size_t, cudaStream_t);
 cudaError_t launch_f32_to_bf16(const float*, __nv_bfloat16*, size_t, int, cudaStream_t);
 bool tc_logits_maps(CUtensorMap*, CUtensorMap*, const __nv_bfloat16*, int, const __nv_bfloat16*, int, int);
@@ -202,7 +202,7 @@ crl_status bf16_prepare(crl_ctx* ctx) {
 
 static crl_status enc_forward_bf16(crl_ctx* ctx, const char* tag, const EncoderPlan& P,
                                    std::vector<crl_ctx::TcLayer>& T, __nv_bfloat16** Xb, __nv_bfloat16** Zb,
-                                   float* yf, __nv_bfloat16* yb, cudaStream_t st, int* nl) {
+                                   float* yf, __nv_bfloat16* yb, float* ystat, cudaStream_t st, int* nl) {
   const crl_config& k = ctx->cfg;
   const int Bl = k.batch_local, L = P.n_layers;
   for (int l = 0; l < L; ++l) {
@@ -211,7 +211,7 @@ static crl_status enc_forward_bf16(crl_ctx* ctx, const char* tag, const EncoderP
     Stage sg(ctx, st, std::string(tag) + "_fwd_l" + std::to_string(l));
     CU(tc::tc_forward(T[l].bn_fwd, T[l].fwdA, T[l].fwdB, Bl, Lp.in, Lp.out, ctx->mem.params + Lp.b_off,
                       last ? nullptr : Zb[l], last ? yb : Xb[l + 1], Lp.out, last ? yf : nullptr, Lp.out,
-                      k.activation, st));
+                      k.activation, last ? ystat : nullptr, k.energy, st));
     ++*nl;
   }
   return CRL_OK;
@@ -294,10 +294,17 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   const float c_b = (k.loss == CRL_LOSS_FWD) ? 0.f : 1.f;
   int nl = 0;
   crl_status rs;
+  const int row_off = k.rank * Bl;
+  // the per-row statistic of Y comes out of the last forward layer's epilogue when that
+  // layer's output row fits one CTA (else a separate row-statistic launch)
+  const bool stat_in_fwd = ctx->tc_logits && !ctx->use_chain && D <= ctx->tc_phi.back().bn_fwd &&
+                           D <= ctx->tc_psi.back().bn_fwd;
   {
     Stage sg(ctx, st, "prep_inputs");
+    // also re-arms the step's device flags (fused-stats fallback gate, fast-factor flag)
     CU(tc::launch_prep_inputs(s, a, g, Bl, k.obs_dim, k.act_dim, k.goal_dim, ctx->x0_phi, ctx->ld0_phi,
-                              ctx->x0_psi, ctx->ld0_psi, ctx->num_sms, ctx->use_stats ? ctx->st_bad : nullptr, st));
+                              ctx->x0_psi, ctx->ld0_psi, ctx->num_sms, ctx->use_stats ? ctx->st_bad : nullptr,
+                              ctx->tc_logits ? ctx->fac_ok : nullptr, std::getenv("CRL_FORCE_EXACT_Q") ? 0 : 1, st));
     ++nl;
   }
   if (ctx->use_chain) {
@@ -308,18 +315,17 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   } else {
     fork2(ctx, st, st2);
     rs = enc_forward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiXb, ctx->psiZb, ctx->psi_out,
-                          ctx->psi_outb, st2, &nl);
+                          ctx->psi_outb, stat_in_fwd ? ctx->stat_psi + row_off : nullptr, st2, &nl);
     if (rs != CRL_OK) return rs;
     rs = enc_forward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiXb, ctx->phiZb, ctx->phi_out,
-                          ctx->phi_outb, st, &nl);
+                          ctx->phi_outb, stat_in_fwd ? ctx->stat_phi + row_off : nullptr, st, &nl);
     if (rs != CRL_OK) return rs;
     join2(ctx, st, st2);
   }
-  const int row_off = k.rank * Bl;
   const int S = ctx->lg_splits;
   if (ctx->tc_logits) {
     // per-row |x|^2 (L2) / 1/|x| (cos) of the bf16-rounded representations
-    if (!ctx->use_chain) { Stage sg(ctx, st, "rowstat");
+    if (!ctx->use_chain && !stat_in_fwd) { Stage sg(ctx, st, "rowstat");
       const int fac_init = std::getenv("CRL_FORCE_EXACT_Q") ? 0 : 1;
       CU(tc::launch_rowstat_bf16(ctx->phi_outb, Bl, D, k.energy, ctx->stat_phi + row_off, ctx->fac_ok, fac_init,
                                  st));
@@ -402,7 +408,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                            ctx->lse_row, ctx->lse_col, ctx->fac_col, ctx->fac_ok, c_f, c_b, k.beta_lse, invN,
                            ctx->gf_splits, ctx->gf_part_da, ctx->gf_part_rs, ctx->gf_acc, ctx->gf_cs, ctx->phi_outb,
                            ctx->psi_outb, ctx->dphi, ctx->dphib, ctx->dpsi, ctx->dpsib, st));
-      nl += 3; }
+      nl += 2; }
   }
   fork2(ctx, st, st2);
   if (!ctx->use_gradf) { Stage sg(ctx, st2, "grad_psi");

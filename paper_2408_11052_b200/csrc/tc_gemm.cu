@@ -34,6 +34,8 @@ struct TcGemmArgs {
   size_t split_stride;             // floats between DW partial slices
   const __nv_bfloat16* zprev;      // DX: pre-activation of the previous layer
   int act;
+  float* out_stat;                 // FWD_OUT (single N tile): row statistic of bf16(Y) for the
+  int stat_energy;                 //   logits stage (L2: |y|^2, cos: 1/max(|y|, eps)), else null
 };
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
@@ -114,7 +116,26 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // prologue above (barriers, TMEM, descriptor prefetch) overlaps the predecessor's tail
+  // prologue above (barriers, TMEM, descriptor prefetch) overlaps the predecessor's tail; the
+  // weight operand (FWD / DX: B = W, written by the previous step's Adam) does not depend on
+  // the predecessor either, so its first STAGES K-blocks are requested before the wait
+  constexpr bool B_IS_W = EPI != TEPI_DW;
+  const int npre = B_IS_W ? min(nkb, STAGES) : 0;
+  auto load_b = [&](int kb, int s) {
+    const int k = kbeg + kb * BK;
+    uint8_t* b_dst = sB + s * S::B_BYTES;
+    if (!B_MN) {
+      tma_load_2d(b_dst, &tmB, &full[s], k, n0);                    // dims {K, N}
+    } else {
+#pragma unroll
+      for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * BK * 128, &tmB, &full[s], n0 + 64 * c, k);
+    }
+  };
+  if (warp == 0 && lane == 0)
+    for (int kb = 0; kb < npre; ++kb) {
+      mbar_expect_tx(&full[kb], S::A_BYTES + S::B_BYTES);
+      load_b(kb, kb);
+    }
   pdl_wait();
   pdl_launch();
 
@@ -123,22 +144,18 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      mbar_expect_tx(&full[s], S::A_BYTES + S::B_BYTES);
+      if (kb >= npre) {
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], S::A_BYTES + S::B_BYTES);
+        load_b(kb, s);
+      }
       const int k = kbeg + kb * BK;
       uint8_t* a_dst = sA + s * S::A_BYTES;
-      uint8_t* b_dst = sB + s * S::B_BYTES;
       if (!A_MN) {
         tma_load_2d(a_dst, &tmA, &full[s], k, m0);                  // dims {K, M}
       } else {
 #pragma unroll
         for (int c = 0; c < BM / 64; ++c) tma_load_2d(a_dst + c * BK * 128, &tmA, &full[s], m0 + 64 * c, k);
-      }
-      if (!B_MN) {
-        tma_load_2d(b_dst, &tmB, &full[s], k, n0);                  // dims {K, N}
-      } else {
-#pragma unroll
-        for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * BK * 128, &tmB, &full[s], n0 + 64 * c, k);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -190,6 +207,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
     }
     mbar_wait(tfull, 0);
     tc_fence_after();
+    float ysq = 0.f;                                      // FWD_OUT: sum of bf16(y)^2 of the row
 #pragma unroll
     for (int c0 = 0; c0 < BN; c0 += 16) {
       float v[16];
@@ -211,6 +229,12 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
           store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
         } else {
           store_f32x16(p.out_f + (size_t)row * p.ld_f + n, v, nvalid);
+          if (p.out_stat != nullptr) {
+            for (int i = 0; i < nvalid; ++i) {
+              const float yb = __bfloat162float(__float2bfloat16_rn(v[i]));
+              ysq = fmaf(yb, yb, ysq);
+            }
+          }
           store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
         }
       } else if (EPI == TEPI_DX) {
@@ -227,6 +251,11 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
         store_f32x16(p.out_f + (size_t)blockIdx.z * p.split_stride + (size_t)row * p.ld_f + n, v, nvalid);
       }
     }
+    // FWD_OUT with the whole output row in this CTA: the logits stage's row statistic
+    // (replaces a separate row-statistic launch; same bf16-rounded vector it will read)
+    if (EPI == TEPI_FWD_OUT && p.out_stat != nullptr && rv)
+      p.out_stat[row] = p.stat_energy == CRL_ENERGY_L2 ? ysq
+                        : (p.stat_energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(ysq), kEpsCos) : 0.f);
   }
   tc_fence_before();
   __syncthreads();
@@ -321,10 +350,12 @@ static cudaError_t dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& 
 
 cudaError_t tc_forward(int bn, const CUtensorMap& mapX, const CUtensorMap& mapW, int Bn, int in, int out,
                        const float* bias, __nv_bfloat16* z, __nv_bfloat16* xn, int ld_bf, float* y_f32,
-                       int ld_f, int act, cudaStream_t st) {
+                       int ld_f, int act, float* y_stat, int energy, cudaStream_t st) {
   TcGemmArgs p{};
   p.M = Bn; p.N = out; p.K = in; p.k_per_split = in;
   p.bias = bias; p.out_z = z; p.out_bf = xn; p.ld_bf = ld_bf; p.out_f = y_f32; p.ld_f = ld_f; p.act = act;
+  p.out_stat = (y_stat != nullptr && out <= bn) ? y_stat : nullptr;     // whole row in one CTA only
+  p.stat_energy = energy;
   if (y_f32 == nullptr) return dispatch_bn<TEPI_FWD_HIDDEN, false, true>(bn, mapX, mapW, p, 1, st);
   return dispatch_bn<TEPI_FWD_OUT, false, true>(bn, mapX, mapW, p, 1, st);
 }
@@ -353,12 +384,15 @@ cudaError_t tc_backward_dw(int bn, const CUtensorMap& mapX_mn, const CUtensorMap
 __global__ void prep_inputs_kernel(const float* __restrict__ s, const float* __restrict__ a,
                                    const float* __restrict__ g, int Bn, int obs, int act, int goal,
                                    __nv_bfloat16* __restrict__ x0, int ld0, __nv_bfloat16* __restrict__ g0,
-                                   int ldg, int* __restrict__ reset) {
+                                   int ldg, int* __restrict__ reset, int* __restrict__ fac_ok, int fac_init) {
   const int in0 = obs + act;
   const size_t tot0 = (size_t)Bn * in0, totg = (size_t)Bn * goal;
   pdl_wait();
   pdl_launch();
-  if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reset = 0;   // per-step device flag
+  if (blockIdx.x == 0 && threadIdx.x == 0) {           // per-step device flags
+    if (reset != nullptr) *reset = 0;
+    if (fac_ok != nullptr) *fac_ok = fac_init;
+  }
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot0 + totg;
        i += (size_t)gridDim.x * blockDim.x) {
     if (i < tot0) {
@@ -375,12 +409,12 @@ __global__ void prep_inputs_kernel(const float* __restrict__ s, const float* __r
 
 cudaError_t launch_prep_inputs(const float* s, const float* a, const float* g, int Bn, int obs, int act,
                                int goal, __nv_bfloat16* x0, int ld0, __nv_bfloat16* g0, int ldg,
-                               int num_sms, int* reset, cudaStream_t st) {
+                               int num_sms, int* reset, int* fac_ok, int fac_init, cudaStream_t st) {
   size_t tot = (size_t)Bn * (obs + act + goal);
   size_t blocks = (tot + 255) / 256;
   if (blocks > (size_t)num_sms * 4) blocks = (size_t)num_sms * 4;
   return launch_pdl(prep_inputs_kernel, dim3((unsigned)blocks), dim3(256), 0, st, s, a, g, Bn, obs, act, goal,
-                    x0, ld0, g0, ldg, reset);
+                    x0, ld0, g0, ldg, reset, fac_ok, fac_init);
 }
 
 // db[s][n] = sum over the batch slice s of dZ[b][n] (bf16 in, fp32 out): 64 columns x one

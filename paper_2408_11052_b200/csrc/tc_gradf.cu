@@ -449,9 +449,12 @@ static cudaError_t launch_gf(const CUtensorMap& a, const CUtensorMap& b, const C
   return launch_pdl(tc_gradf_kernel<E>, grid, dim3(384), smem, st, a, b, db, p);
 }
 
-cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, const __nv_bfloat16* A,
-                              const float* a_stat, const __nv_bfloat16* Bg, const float* b_stat, int row_offset,
-                              float Cdiag, int Na, int D, int S, float* out, __nv_bfloat16* outb, cudaStream_t st);
+struct GradMergeArgs {     // tc_logits.cu
+  const float* part; const float* prs; const __nv_bfloat16* A; const float* a_stat;
+  const __nv_bfloat16* Bg; const float* b_stat; int row_offset; float Cdiag; int Na, D, S;
+  float* out; __nv_bfloat16* outb;
+};
+cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st);
 
 // Both sides of the gradient.  Row side (A = Phi rows, B = Psi columns): part_da / part_rs
 // per split, merged into dA.  Column side: db_acc [Nb][64] and cs_acc [Nb] must be ZERO on
@@ -472,10 +475,10 @@ cudaError_t tc_grad_fused(int energy, const CUtensorMap& mA, const CUtensorMap& 
                                           : launch_gf<CRL_ENERGY_DOT>(mA, mB, mDB, p, S, st);
   if (e != cudaSuccess) return e;
   const float Cdiag = invN * (c_r + c_c);
-  e = launch_grad_merge(energy, part_da, part_rs, A, a_stat, B, b_stat, 0, Cdiag, Na, 64, S, dA, dAb, st);
-  if (e != cudaSuccess) return e;
-  // column side: "rows" are the B vectors, the pair partner of B_j is A_j
-  return launch_grad_merge(energy, db_acc, cs_acc, B, b_stat, A, a_stat, 0, Cdiag, Nb, 64, 1, dB, dBb, st);
+  // row side; column side ("rows" are the B vectors, the pair partner of B_j is A_j): one launch
+  const GradMergeArgs g0{part_da, part_rs, A, a_stat, B, b_stat, 0, Cdiag, Na, 64, S, dA, dAb};
+  const GradMergeArgs g1{db_acc, cs_acc, B, b_stat, A, a_stat, 0, Cdiag, Nb, 64, 1, dB, dBb};
+  return launch_grad_merge2(energy, g0, g1, st);
 }
 
 }  // namespace tc

@@ -425,15 +425,24 @@ __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __re
 // Also adds the positive-pair (delta_ii) term of dL/dl, -C delta_ij with C = invN (c_r + c_c),
 // which the tile epilogue leaves out: its energy chain uses the pair (A_i, B_{row_offset+i})
 // (L2: 1/r_ii from the difference form; cos: 1/|B_i|).
+struct GradMergeArgs {
+  const float* part; const float* prs; const __nv_bfloat16* A; const float* a_stat;
+  const __nv_bfloat16* Bg; const float* b_stat; int row_offset; float Cdiag; int Na, D, S;
+  float* out; __nv_bfloat16* outb;
+};
+
 template <int ENERGY>
-__global__ void grad_merge_kernel(const float* __restrict__ part, const float* __restrict__ prs,
-                                  const __nv_bfloat16* __restrict__ A, const float* __restrict__ a_stat,
-                                  const __nv_bfloat16* __restrict__ Bg, const float* __restrict__ b_stat,
-                                  int row_offset, float Cdiag, int Na, int D, int S, float* __restrict__ out,
-                                  __nv_bfloat16* __restrict__ outb) {
-  pdl_wait();
-  pdl_launch();
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, int lane) {
+  const float* __restrict__ part = g.part;
+  const float* __restrict__ prs = g.prs;
+  const __nv_bfloat16* __restrict__ A = g.A;
+  const float* __restrict__ a_stat = g.a_stat;
+  const __nv_bfloat16* __restrict__ Bg = g.Bg;
+  const float* __restrict__ b_stat = g.b_stat;
+  const int row_offset = g.row_offset, Na = g.Na, D = g.D, S = g.S;
+  const float Cdiag = g.Cdiag;
+  float* __restrict__ out = g.out;
+  __nv_bfloat16* __restrict__ outb = g.outb;
   if (w >= Na) return;
   const size_t ib = (size_t)(row_offset + w) * D;
   float rs = 0.f;
@@ -478,8 +487,25 @@ __global__ void grad_merge_kernel(const float* __restrict__ part, const float* _
   }
 }
 
+template <int ENERGY>
+__global__ void grad_merge_kernel(const GradMergeArgs g) {
+  pdl_wait();
+  pdl_launch();
+  grad_merge_row<ENERGY>(g, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31);
+}
+// both sides of the fused gradient pass in one launch: blockIdx.y picks the row / column side
+template <int ENERGY>
+__global__ void grad_merge2_kernel(const GradMergeArgs g0, const GradMergeArgs g1) {
+  pdl_wait();
+  pdl_launch();
+  grad_merge_row<ENERGY>(blockIdx.y ? g1 : g0, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31);
+}
+
 // ------------------------------------------------------------------------------- host side
 bool make_map_bf16(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
+cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, const __nv_bfloat16* A,
+                              const float* a_stat, const __nv_bfloat16* Bg, const float* b_stat, int row_offset,
+                              float Cdiag, int Na, int D, int S, float* out, __nv_bfloat16* outb, cudaStream_t st);
 
 bool tc_logits_supports(int D) { return D == 64 || D == 128 || D == 256; }
 
@@ -569,30 +595,26 @@ cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUten
   p.part_da = part_da; p.part_rs = part_rs;
   cudaError_t e = dispatch_lg<true>(D, energy, mA, mB, p, S, st);
   if (e != cudaSuccess) return e;
-  const dim3 g((Na * 32 + 255) / 256);
   const float Cdiag = invN * (c_r + c_c);
-  if (energy == CRL_ENERGY_L2)
-    return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2>, g, dim3(256), 0, st, (const float*)part_da,
-                      (const float*)part_rs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, dA, dAb);
-  if (energy == CRL_ENERGY_COS)
-    return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, g, dim3(256), 0, st, (const float*)part_da,
-                      (const float*)part_rs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, dA, dAb);
-  return launch_pdl(grad_merge_kernel<CRL_ENERGY_DOT>, g, dim3(256), 0, st, (const float*)part_da,
-                    (const float*)part_rs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, dA, dAb);
+  return launch_grad_merge(energy, part_da, part_rs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, dA, dAb,
+                           st);
 }
 
 cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, const __nv_bfloat16* A,
                               const float* a_stat, const __nv_bfloat16* Bg, const float* b_stat, int row_offset,
                               float Cdiag, int Na, int D, int S, float* out, __nv_bfloat16* outb, cudaStream_t st) {
-  const dim3 g((Na * 32 + 255) / 256);
-  if (energy == CRL_ENERGY_L2)
-    return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2>, g, dim3(256), 0, st, part, prs, A, a_stat, Bg, b_stat,
-                      row_offset, Cdiag, Na, D, S, out, outb);
-  if (energy == CRL_ENERGY_COS)
-    return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, g, dim3(256), 0, st, part, prs, A, a_stat, Bg, b_stat,
-                      row_offset, Cdiag, Na, D, S, out, outb);
-  return launch_pdl(grad_merge_kernel<CRL_ENERGY_DOT>, g, dim3(256), 0, st, part, prs, A, a_stat, Bg, b_stat,
-                    row_offset, Cdiag, Na, D, S, out, outb);
+  const GradMergeArgs g{part, prs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, out, outb};
+  const dim3 grid((Na * 32 + 255) / 256);
+  if (energy == CRL_ENERGY_L2) return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2>, grid, dim3(256), 0, st, g);
+  if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g);
+  return launch_pdl(grad_merge_kernel<CRL_ENERGY_DOT>, grid, dim3(256), 0, st, g);
+}
+// row side (g0) and column side (g1) of the fused gradient pass, one launch
+cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st) {
+  const dim3 grid((max(g0.Na, g1.Na) * 32 + 255) / 256, 2);
+  if (energy == CRL_ENERGY_L2) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_L2>, grid, dim3(256), 0, st, g0, g1);
+  if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g0, g1);
+  return launch_pdl(grad_merge2_kernel<CRL_ENERGY_DOT>, grid, dim3(256), 0, st, g0, g1);
 }
 
 cudaError_t launch_rowstat_bf16(const __nv_bfloat16* x, int N, int D, int energy, float* out, int* fac_ok,
