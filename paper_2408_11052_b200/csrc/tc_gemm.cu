@@ -15,6 +15,10 @@
 //   warps 4..7      : epilogue, one TMEM lane (= output row) per thread, tcgen05.ld x16,
 //                     fused bias / activation / activation-derivative, vector stores
 // Split-K along blockIdx.z writes deterministic fp32 partial slices (dW).
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 #include "tc_common.cuh"
 
@@ -36,7 +40,19 @@ struct TcGemmArgs {
   int act;
   float* out_stat;                 // FWD_OUT (single N tile): row statistic of bf16(Y) for the
   int stat_energy;                 //   logits stage (L2: |y|^2, cos: 1/max(|y|, eps)), else null
+  int trace;                       // measurement: globaltimer phases of CTA 0 (CRL_GEMM_TRACE)
 };
+
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
 
@@ -103,6 +119,9 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
   const int kbeg = blockIdx.z * p.k_per_split;
   const int kend = min(p.K, kbeg + p.k_per_split);
   const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  const bool trace = p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  __shared__ unsigned long long s_tt[8];
+  if (trace && threadIdx.x == 0) s_tt[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -131,6 +150,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
       for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * BK * 128, &tmB, &full[s], n0 + 64 * c, k);
     }
   };
+  if (trace && threadIdx.x == 0) s_tt[1] = gtimer();
   if (warp == 0 && lane == 0)
     for (int kb = 0; kb < npre; ++kb) {
       mbar_expect_tx(&full[kb], S::A_BYTES + S::B_BYTES);
@@ -138,6 +158,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
     }
   pdl_wait();
   pdl_launch();
+  if (trace && threadIdx.x == 0) s_tt[2] = gtimer();
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -165,6 +186,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
       mbar_wait(&full[s], ph);
+      if (trace && kb == 0) s_tt[3] = gtimer();
       tc_fence_after();
       const uint32_t a_base = smem_u32(sA + s * S::A_BYTES);
       const uint32_t b_base = smem_u32(sB + s * S::B_BYTES);
@@ -206,56 +228,88 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
       }
     }
     mbar_wait(tfull, 0);
+    if (trace && threadIdx.x == 128) s_tt[4] = gtimer();
     tc_fence_after();
-    float ysq = 0.f;                                      // FWD_OUT: sum of bf16(y)^2 of the row
+    float ysq = 0.f;                                     // FWD_OUT: sum of bf16(y)^2 of the row
+    // the whole BN-column row in one burst of TMEM loads (one wait), then branch-free math:
+    // the activation is a kernel-uniform choice hoisted out of the per-element code, and SiLU /
+    // SiLU' use tanh.approx (sigma(z) = (1 + tanh(z/2)) / 2: one MUFU op, no division); the
+    // outputs are rounded to bf16 (2^-9), the tanh.approx error is ~2^-11
+    uint32_t acc[BN];
 #pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
-      if (nkb == 0) {
+    for (int c = 0; c < BN / 32; ++c)
+      tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
+    tmem_ld_wait();
+    if (nkb == 0) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      }
-      const int n = n0 + c0;
-      const int nvalid = min(16, p.N - n);
-      if (!rv || nvalid <= 0) continue;
-      if (EPI == TEPI_FWD_HIDDEN || EPI == TEPI_FWD_OUT) {
+      for (int i = 0; i < BN; ++i) acc[i] = 0u;
+    }
+    auto epilogue = [&](auto silu_c) {
+      constexpr bool SILU = decltype(silu_c)::value;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += sbias[c0 + i];
-        if (EPI == TEPI_FWD_HIDDEN) {
-          store_bf16x16(p.out_z + (size_t)row * p.ld_bf + n, v, nvalid);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = act_f(v[i], p.act);
-          store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
-        } else {
-          store_f32x16(p.out_f + (size_t)row * p.ld_f + n, v, nvalid);
-          if (p.out_stat != nullptr) {
-            for (int i = 0; i < nvalid; ++i) {
-              const float yb = __bfloat162float(__float2bfloat16_rn(v[i]));
-              ysq = fmaf(yb, yb, ysq);
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(acc[c0 + i]);
+        const int n = n0 + c0;
+        const int nvalid = min(16, p.N - n);
+        if (!rv || nvalid <= 0) continue;
+        if (EPI == TEPI_FWD_HIDDEN || EPI == TEPI_FWD_OUT) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += sbias[c0 + i];
+          if (EPI == TEPI_FWD_HIDDEN) {
+            store_bf16x16(p.out_z + (size_t)row * p.ld_bf + n, v, nvalid);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (SILU) {
+                const float h = 0.5f * v[i];
+                v[i] = fmaf(h, tanh_fast(h), h);
+              } else {
+                v[i] = fmaxf(v[i], 0.f);
+              }
+            }
+            store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
+          } else {
+            store_f32x16(p.out_f + (size_t)row * p.ld_f + n, v, nvalid);
+            if (p.out_stat != nullptr) {
+              for (int i = 0; i < nvalid; ++i) {
+                const float yb = __bfloat162float(__float2bfloat16_rn(v[i]));
+                ysq = fmaf(yb, yb, ysq);
+              }
+            }
+            store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
+          }
+        } else if (EPI == TEPI_DX) {
+          const uint32_t w[8] = {zp[c0 / 8].x, zp[c0 / 8].y, zp[c0 / 8].z, zp[c0 / 8].w,
+                                 zp[c0 / 8 + 1].x, zp[c0 / 8 + 1].y, zp[c0 / 8 + 1].z, zp[c0 / 8 + 1].w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+            if (SILU) {
+              // silu'(z) = 1/2 + (t + h (1 - t^2)) / 2, h = z/2, t = tanh(h)
+              const float h0 = 0.5f * z.x, h1 = 0.5f * z.y;
+              const float t0 = tanh_fast(h0), t1 = tanh_fast(h1);
+              v[2 * i] *= fmaf(0.5f, fmaf(h0, fmaf(-t0, t0, 1.f), t0), 0.5f);
+              v[2 * i + 1] *= fmaf(0.5f, fmaf(h1, fmaf(-t1, t1, 1.f), t1), 0.5f);
+            } else {
+              v[2 * i] = z.x > 0.f ? v[2 * i] : 0.f;
+              v[2 * i + 1] = z.y > 0.f ? v[2 * i + 1] : 0.f;
             }
           }
           store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
+        } else {
+          store_f32x16(p.out_f + (size_t)blockIdx.z * p.split_stride + (size_t)row * p.ld_f + n, v, nvalid);
         }
-      } else if (EPI == TEPI_DX) {
-        const uint32_t w[8] = {zp[c0 / 8].x, zp[c0 / 8].y, zp[c0 / 8].z, zp[c0 / 8].w,
-                               zp[c0 / 8 + 1].x, zp[c0 / 8 + 1].y, zp[c0 / 8 + 1].z, zp[c0 / 8 + 1].w};
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
-          v[2 * i] *= act_grad_f(z.x, p.act);
-          v[2 * i + 1] *= act_grad_f(z.y, p.act);
-        }
-        store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);
-      } else {
-        store_f32x16(p.out_f + (size_t)blockIdx.z * p.split_stride + (size_t)row * p.ld_f + n, v, nvalid);
       }
-    }
+    };
+    if (p.act == CRL_ACT_SILU) epilogue(std::true_type{});
+    else epilogue(std::false_type{});
     // FWD_OUT with the whole output row in this CTA: the logits stage's row statistic
     // (replaces a separate row-statistic launch; same bf16-rounded vector it will read)
     if (EPI == TEPI_FWD_OUT && p.out_stat != nullptr && rv)
       p.out_stat[row] = p.stat_energy == CRL_ENERGY_L2 ? ysq
                         : (p.stat_energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(ysq), kEpsCos) : 0.f);
+    if (trace && threadIdx.x == 128) s_tt[5] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
@@ -263,6 +317,10 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
     tc_fence_after();
     tmem_dealloc(tmem, BN);
   }
+  if (trace && threadIdx.x == 0)
+    printf("GEMM_TRACE epi=%d M=%d N=%d K=%d grid=%d,%d,%d entry=%llu prologue=%llu pdl=%llu mma0=%llu acc=%llu end=%llu\n",
+           EPI, p.M, p.N, p.K, gridDim.x, gridDim.y, gridDim.z, s_tt[0] % 100000000ull, s_tt[1] - s_tt[0],
+           s_tt[2] - s_tt[0], s_tt[3] - s_tt[0], s_tt[4] - s_tt[0], s_tt[5] - s_tt[0]);
 }
 
 // -------------------------------------------------------------------------------- host side
@@ -325,7 +383,10 @@ static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const T
     attr = true;
   }
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, splits);
-  return launch_pdl(tc_gemm_kernel<BN, A_MN, B_MN, EPI>, grid, dim3(256), smem, st, a, b, p);
+  static const int trace = std::getenv("CRL_GEMM_TRACE") ? 1 : 0;
+  TcGemmArgs q = p;
+  q.trace = trace;
+  return launch_pdl(tc_gemm_kernel<BN, A_MN, B_MN, EPI>, grid, dim3(256), smem, st, a, b, q);
 }
 
 // Operand maps for one GEMM: boxes follow the kernel's TMA calls.
