@@ -8,6 +8,7 @@
 //   dX   : dZ_{l-1} = (dZ_l W_l^T) * act'(Z_{l-1})  (bf16)
 // All tensor maps are built once at context creation (buffers are context-owned).
 #include "ctx.h"
+#include "tc_gradf.h"
 
 #include <cstdlib>
 
@@ -39,11 +40,6 @@ cudaError_t launch_f32_to_bf16(const float*, __nv_bfloat16*, size_t, int, cudaSt
 bool tc_logits_maps(CUtensorMap*, CUtensorMap*, const __nv_bfloat16*, int, const __nv_bfloat16*, int, int);
 cudaError_t tc_logits_lse(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*,
                           int, float*, float*, float*, float*, int*, float, float, const int*, cudaStream_t);
-cudaError_t tc_grad_fused(int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, int, int, const float*,
-                          const float*, const float*, const float*, const float*, const int*, float, float, float,
-                          float, int, float*, float*, float*, float*, const __nv_bfloat16*, const __nv_bfloat16*,
-                          float*, __nv_bfloat16*, float*, __nv_bfloat16*, cudaStream_t);
-bool tc_gradf_map(CUtensorMap*, float*, int);
 cudaError_t tc_stats_fused(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*, int,
                            float*, float*, int, float*, float*, float*, float*, int*, int*, float, float, float, float,
                            cudaStream_t);
@@ -388,7 +384,13 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     }
     NC(ncclGroupEnd());
   }
-  { Stage sg(ctx, st, "loss");
+  // the loss is reduced inside the fused gradient kernel when that runs (its idle warps)
+  tc::GradfLoss gl;
+  if (ctx->use_gradf) {
+    gl.phi32 = ctx->phi_out; gl.psi32 = ctx->psi_out; gl.part = ctx->loss_part; gl.ticket = ctx->loss_ticket;
+    gl.acc = ctx->loss_acc; gl.out = loss_out; gl.skip = ctx->skip; gl.adam_t = ctx->adam_t; gl.status = ctx->status;
+    gl.c_f = c_f; gl.c_b = c_b; gl.beta = k.beta_lse;
+  } else { Stage sg(ctx, st, "loss");
     CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,
                            ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, W == 1, invN, c_f, c_b,
                            k.beta_lse, loss_out, ctx->skip, ctx->adam_t, ctx->status, st));
@@ -407,7 +409,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(tc::tc_grad_fused(k.energy, ctx->lg_row_A, ctx->lg_row_B, ctx->gf_map, Bl, N, ctx->stat_phi, ctx->stat_psi,
                            ctx->lse_row, ctx->lse_col, ctx->fac_col, ctx->fac_ok, c_f, c_b, k.beta_lse, invN,
                            ctx->gf_splits, ctx->gf_part_da, ctx->gf_part_rs, ctx->gf_acc, ctx->gf_cs, ctx->phi_outb,
-                           ctx->psi_outb, ctx->dphi, ctx->dphib, ctx->dpsi, ctx->dpsib, st));
+                           ctx->psi_outb, ctx->dphi, ctx->dphib, ctx->dpsi, ctx->dpsib, gl, st));
       nl += 2; }
   }
   fork2(ctx, st, st2);

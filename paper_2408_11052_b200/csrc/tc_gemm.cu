@@ -272,9 +272,10 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
           } else {
             store_f32x16(p.out_f + (size_t)row * p.ld_f + n, v, nvalid);
             if (p.out_stat != nullptr) {
-              for (int i = 0; i < nvalid; ++i) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
                 const float yb = __bfloat162float(__float2bfloat16_rn(v[i]));
-                ysq = fmaf(yb, yb, ysq);
+                ysq = i < nvalid ? fmaf(yb, yb, ysq) : ysq;
               }
             }
             store_bf16x16(p.out_bf + (size_t)row * p.ld_bf + n, v, nvalid);

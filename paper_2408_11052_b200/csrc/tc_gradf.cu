@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "tc_common.cuh"
+#include "tc_gradf.h"
 
 namespace crl {
 namespace tc {
@@ -78,7 +79,68 @@ struct TcGradFArgs {
   float* part_da;                  // [S][Na][64]
   float* part_rs;                  // [S][Na]
   float* cs_acc;                   // [Nb] column sums of w (L2), accumulated
+  // the loss (readings A-02..A-05), computed by the otherwise idle warps 2-3 of the column
+  // split 0 CTAs (one launch less on the critical path); null loss_part: not here
+  const float* phi32; const float* psi32;       // fp32 representations (positives l_ii)
+  float* loss_part;                // [row blocks][4] partial sums
+  unsigned* loss_ticket;
+  float* loss_acc;                 // [3] sums of (LSE_i - l_ii), (LSE'_i - l_ii), LSE_i^2
+  float* loss_out;                 // [4] or null
+  int *skip, *adam_t, *status;
+  float loss_cf, loss_cb, loss_beta;
 };
+
+// the loss from the statistics (as optim.cu loss_partial / loss_finalize)
+template <int ENERGY>
+__device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t, int nthr) {
+  __shared__ float red[3][2];
+  float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  for (int r = t; r < 128; r += nthr) {
+    const int i = a0 + r;
+    if (i >= p.Na) break;
+    const float4* a = reinterpret_cast<const float4*>(p.phi32 + (size_t)i * 64);
+    const float4* b = reinterpret_cast<const float4*>(p.psi32 + (size_t)i * 64);
+    float x = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+      const float4 u = a[k], v = b[k];
+      if (ENERGY == CRL_ENERGY_L2) {
+        x = fmaf(u.x - v.x, u.x - v.x, x); x = fmaf(u.y - v.y, u.y - v.y, x);
+        x = fmaf(u.z - v.z, u.z - v.z, x); x = fmaf(u.w - v.w, u.w - v.w, x);
+      } else {
+        x = fmaf(u.x, v.x, x); x = fmaf(u.y, v.y, x); x = fmaf(u.z, v.z, x); x = fmaf(u.w, v.w, x);
+      }
+    }
+    const float l = ENERGY == CRL_ENERGY_L2 ? -sqrtf(x + kEpsL2) : x;
+    const float lr = p.lr[i], lc = p.lc[i];
+    s1 += lr - l; s2 += lc - l; s3 += lr * lr;
+  }
+  s1 = warp_sum(s1); s2 = warp_sum(s2); s3 = warp_sum(s3);
+  const int w = t >> 5;
+  if ((t & 31) == 0) { red[0][w] = s1; red[1][w] = s2; red[2][w] = s3; }
+  asm volatile("bar.sync 4, 64;" ::: "memory");
+  if (t != 0) return;
+  const int rb = a0 / 128, R = (p.Na + 127) / 128;
+  p.loss_part[rb * 4 + 0] = red[0][0] + red[0][1];
+  p.loss_part[rb * 4 + 1] = red[1][0] + red[1][1];
+  p.loss_part[rb * 4 + 2] = red[2][0] + red[2][1];
+  __threadfence();
+  if (atomicAdd(p.loss_ticket, 1u) != (unsigned)(R - 1)) return;
+  __threadfence();
+  float t1 = 0.f, t2 = 0.f, t3 = 0.f;                  // last row block: fixed order, deterministic
+  for (int j = 0; j < R; ++j) {
+    t1 += __ldcg(p.loss_part + j * 4 + 0); t2 += __ldcg(p.loss_part + j * 4 + 1); t3 += __ldcg(p.loss_part + j * 4 + 2);
+  }
+  *p.loss_ticket = 0u;
+  p.loss_acc[0] = t1; p.loss_acc[1] = t2; p.loss_acc[2] = t3;
+  const float Lf = t1 * p.invN, Lb = t2 * p.invN, P = p.loss_beta * t3 * p.invN;
+  const float tot = p.loss_cf * Lf + p.loss_cb * Lb + P;
+  if (p.loss_out) { p.loss_out[0] = Lf; p.loss_out[1] = Lb; p.loss_out[2] = P; p.loss_out[3] = tot; }
+  const bool bad = !isfinite(tot);
+  *p.skip = bad ? 1 : 0;
+  if (bad) set_status(p.status, CRL_ENONFINITE);
+  else *p.adam_t += 1;
+}
 
 struct GfCfg {
   static constexpr int D = 64, BNT = 128, STAGES = 3;
@@ -234,6 +296,8 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
     }
     if (ntiles > 0) issue_back(ntiles - 1);
     mma_commit(da_full);
+  } else if (warp == 2 || warp == 3) {
+    if (p.loss_part != nullptr && split == 0) gradf_loss_rows<ENERGY>(p, a0, threadIdx.x - 64, 64);
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
     const int wg = (warp - 4) >> 2;                       // column half of the tile
@@ -464,13 +528,16 @@ cudaError_t tc_grad_fused(int energy, const CUtensorMap& mA, const CUtensorMap& 
                           const float* fac_col, const int* fac_ok, float c_r, float c_c, float beta_r, float invN,
                           int S, float* part_da, float* part_rs, float* db_acc, float* cs_acc,
                           const __nv_bfloat16* A, const __nv_bfloat16* B, float* dA, __nv_bfloat16* dAb, float* dB,
-                          __nv_bfloat16* dBb, cudaStream_t st) {
+                          __nv_bfloat16* dBb, const GradfLoss& loss, cudaStream_t st) {
   TcGradFArgs p{};
   p.Na = Na; p.Nb = Nb;
   p.cols_per_split = ((Nb + S - 1) / S + 127) / 128 * 128;
   p.a_stat = a_stat; p.b_stat = b_stat; p.lr = lse_row; p.lc = lse_col; p.lcf = fac_col; p.fac_ok = fac_ok;
   p.c_r = c_r; p.c_c = c_c; p.beta_r = beta_r; p.invN = invN;
   p.part_da = part_da; p.part_rs = part_rs; p.cs_acc = cs_acc;
+  p.phi32 = loss.phi32; p.psi32 = loss.psi32; p.loss_part = loss.part; p.loss_ticket = loss.ticket;
+  p.loss_acc = loss.acc; p.loss_out = loss.out; p.skip = loss.skip; p.adam_t = loss.adam_t; p.status = loss.status;
+  p.loss_cf = loss.c_f; p.loss_cb = loss.c_b; p.loss_beta = loss.beta;
   cudaError_t e = energy == CRL_ENERGY_L2 ? launch_gf<CRL_ENERGY_L2>(mA, mB, mDB, p, S, st)
                                           : launch_gf<CRL_ENERGY_DOT>(mA, mB, mDB, p, S, st);
   if (e != cudaSuccess) return e;
