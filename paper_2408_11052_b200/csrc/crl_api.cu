@@ -358,6 +358,7 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream3, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream4, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->cap_body, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
@@ -388,6 +389,7 @@ crl_status crl_destroy(crl_ctx* ctx) {
   if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
   if (ctx->cap_stream3) cudaStreamDestroy(ctx->cap_stream3);
   if (ctx->cap_stream4) cudaStreamDestroy(ctx->cap_stream4);
+  if (ctx->cap_body) cudaStreamDestroy(ctx->cap_body);
   if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);

@@ -110,6 +110,7 @@ struct crl_ctx {
   float *stage_s = nullptr, *stage_a = nullptr, *stage_g = nullptr;
   // runtime
   cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr, cap_stream3 = nullptr, cap_stream4 = nullptr;
+  cudaStream_t cap_body = nullptr;        // captures the bodies of conditional graph nodes
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int> graph_launches;     // kernels per replay of each cached graph

@@ -42,7 +42,7 @@ cudaError_t tc_logits_lse(int, int, const CUtensorMap&, const CUtensorMap&, int,
                           int, float*, float*, float*, float*, int*, float, float, const int*, cudaStream_t);
 cudaError_t tc_stats_fused(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*, int,
                            float*, float*, int, float*, float*, float*, float*, int*, int*, float, float, float, float,
-                           cudaStream_t);
+                           cudaGraphConditionalHandle, cudaStream_t);
 cudaError_t tc_logits_grad(int, int, const CUtensorMap&, const CUtensorMap&, int, int, int, const float*,
                            const float*, const float*, const float*, const float*, float, float, float, float,
                            float, int, float*, float*, const __nv_bfloat16*, const __nv_bfloat16*, float*,
@@ -336,17 +336,53 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       NC(ncclGroupEnd());
     }
     const int* gate = nullptr;
+    cudaGraphConditionalHandle cond = 0;
     if (ctx->use_stats) {
       // one pass: row AND column sums of e^l (no running max: L2 / cos logits are bounded
-      // above); the exact online-max pass below then runs only if a sum under/overflowed
+      // above); the exact online-max pass below then runs only if a sum under/overflowed:
+      // by default as early-exit gated kernels.  CRL_COND_NODE=1 instead captures it as the
+      // body of a conditional (IF) graph node set by the merge kernel -- measured slower on
+      // B200 (ant: 99 -> 107 us/step: the node breaks the programmatic-launch chain).
+      if (st != st2 && std::getenv("CRL_COND_NODE")) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaGraph_t cg = nullptr;
+        CU(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, nullptr, nullptr));
+        if (cs == cudaStreamCaptureStatusActive && cg != nullptr)
+          CU(cudaGraphConditionalHandleCreate(&cond, cg, 0, cudaGraphCondAssignDefault));
+      }
       Stage sg(ctx, st, "lse_fused");
       CU(tc::tc_stats_fused(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off, ctx->stat_psi,
                             ctx->st_splits, ctx->st_part_rs, ctx->st_colpart, ctx->st_ldc, ctx->lse_row, ctx->fac_row,
                             ctx->lse_col, ctx->fac_col, ctx->fac_ok, ctx->st_bad, invN * c_f, 2.f * invN * k.beta_lse,
-                            invN * c_b, 0.f, st));
+                            invN * c_b, 0.f, cond, st));
       nl += 2;
       gate = ctx->st_bad;
     }
+    if (cond != 0) {
+      cudaStreamCaptureStatus cs;
+      cudaGraph_t cg;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      CU(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
+      cudaGraphNodeParams np = {};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = cond;
+      np.conditional.type = cudaGraphCondTypeIf;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      CU(cudaGraphAddNode(&node, cg, deps, nd, &np));
+      CU(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+      CU(cudaStreamBeginCaptureToGraph(ctx->cap_body, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeRelaxed));
+      CU(tc::tc_logits_lse(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, ctx->stat_psi + row_off, ctx->stat_phi,
+                           S, ctx->lg_part_m + (size_t)S * Bl, ctx->lg_part_s + (size_t)S * Bl, ctx->lse_col,
+                           ctx->fac_col, ctx->fac_ok, invN * c_b, 0.f, nullptr, ctx->cap_body));
+      CU(tc::tc_logits_lse(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off, ctx->stat_psi,
+                           S, ctx->lg_part_m, ctx->lg_part_s, ctx->lse_row, ctx->fac_row, ctx->fac_ok, invN * c_f,
+                           2.f * invN * k.beta_lse, nullptr, ctx->cap_body));
+      cudaGraph_t body_out = nullptr;
+      CU(cudaStreamEndCapture(ctx->cap_body, &body_out));
+    } else {
     fork2(ctx, st, st2);
     { Stage sg(ctx, st2, "lse_col");
       CU(tc::tc_logits_lse(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, ctx->stat_psi + row_off,
@@ -359,6 +395,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                            ctx->fac_ok, invN * c_f, 2.f * invN * k.beta_lse, gate, st));
       nl += 2; }
     join2(ctx, st, st2);
+    }
   } else {
     if (W > 1) {
       NC(ncclGroupStart());

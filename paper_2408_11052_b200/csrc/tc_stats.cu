@@ -428,11 +428,14 @@ __global__ void stats_merge_kernel(const float* __restrict__ part_rs, int S, int
                                    int R, int ldc, int Nb, float* __restrict__ lse_row, float* __restrict__ fac_row,
                                    float* __restrict__ lse_col, float* __restrict__ fac_col, int* __restrict__ fac_ok,
                                    int* __restrict__ bad, float rc0, float rc1, float cc0, float cc1,
-                                   int force_bad) {
+                                   int force_bad, cudaGraphConditionalHandle cond) {
   pdl_wait();
   pdl_launch();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (force_bad && i == 0) atomicExch(bad, 1);         // CRL_FORCE_STATS_FALLBACK (tests)
+  if (force_bad && i == 0) {                           // CRL_FORCE_STATS_FALLBACK (tests)
+    atomicExch(bad, 1);
+    if (cond != 0) cudaGraphSetConditional(cond, 1);
+  }
   float t = 0.f, c0, c1;
   float *lse, *fac;
   if (i < Na) {
@@ -444,7 +447,10 @@ __global__ void stats_merge_kernel(const float* __restrict__ part_rs, int S, int
     for (int s = 0; s < R; ++s) t += colpart[(size_t)s * ldc + i];
     lse = lse_col; fac = fac_col; c0 = cc0; c1 = cc1;
   }
-  if (!(t >= 0x1p-100f) || !isfinite(t)) atomicExch(bad, 1);
+  if (!(t >= 0x1p-100f) || !isfinite(t)) {
+    atomicExch(bad, 1);
+    if (cond != 0) cudaGraphSetConditional(cond, 1);   // graph: run the exact statistics node
+  }
   const float l2 = log2f(t);
   lse[i] = l2 * fs::kLn2;
   const bool ok = l2 > -120.f && l2 < 120.f;
@@ -491,7 +497,8 @@ static cudaError_t launch_st(const CUtensorMap& a, const CUtensorMap& b, const T
 cudaError_t tc_stats_fused(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
                            const float* a_stat, const float* b_stat, int S, float* part_rs, float* colpart, int ldc,
                            float* lse_row, float* fac_row, float* lse_col, float* fac_col, int* fac_ok, int* bad,
-                           float rc0, float rc1, float cc0, float cc1, cudaStream_t st) {
+                           float rc0, float rc1, float cc0, float cc1, cudaGraphConditionalHandle cond,
+                           cudaStream_t st) {
   TcStatsArgs p{};
   p.Na = Na; p.Nb = Nb;
   const int tiles = (Nb + 127) / 128;
@@ -510,7 +517,7 @@ cudaError_t tc_stats_fused(int D, int energy, const CUtensorMap& mA, const CUten
   const int R = (Na + 127) / 128;
   return launch_pdl(stats_merge_kernel, dim3((Na + Nb + 255) / 256), dim3(256), 0, st, (const float*)part_rs, S, Na,
                     (const float*)colpart, R, ldc, Nb, lse_row, fac_row, lse_col, fac_col, fac_ok, bad, rc0, rc1,
-                    cc0, cc1, std::getenv("CRL_FORCE_STATS_FALLBACK") ? 1 : 0);
+                    cc0, cc1, std::getenv("CRL_FORCE_STATS_FALLBACK") ? 1 : 0, cond);
 }
 
 }  // namespace tc
