@@ -3,6 +3,7 @@
 #pragma once
 #include "common.cuh"
 #include "tc_common.cuh"
+#include "tc_cchain.h"
 #include "tc_chain.h"
 #include "tc_dwg.h"
 
@@ -177,6 +178,10 @@ struct crl_ctx {
   // all weight / bias gradients of both encoders in one grouped launch (tc_dwg.cu)
   bool use_dwg = false;
   tc::DwgParams dwg;
+  // cluster-split MLP chains for small batches (tc_cchain.cu): one launch per direction
+  bool use_cchain = false;
+  tc::CChainMaps cchain_fwd[2], cchain_bwd[2];
+  tc::CChainParams cchain_fwd_p{}, cchain_bwd_p{};
   // ---------------- actor objective (crl_actor_loss, actor.cu): fp32 SIMT, critic frozen
   bool has_actor = false;
   EncoderPlan actor_plan{};

@@ -188,6 +188,65 @@ crl_status bf16_prepare(crl_ctx* ctx) {
       }
     }
   }
+  // cluster-split chains for the small batches the per-row-block chain does not cover
+  ctx->use_cchain = !ctx->use_chain && ctx->tc_logits && !std::getenv("CRL_NO_CCHAIN") &&
+                    (std::getenv("CRL_CCHAIN") || k.batch_local < kChainMinBatch) &&
+                    tc::tc_cchain_supported(k.obs_dim + k.act_dim, k.width, k.repr_dim, k.depth) &&
+                    tc::tc_cchain_supported(k.goal_dim, k.width, k.repr_dim, k.depth);
+  if (ctx->use_cchain) {
+    const int Bl = k.batch_local, row_off = k.rank * Bl;
+    const EncoderPlan* plans[2] = {&ctx->phi_plan, &ctx->psi_plan};
+    std::vector<crl_ctx::TcLayer>* tcs[2] = {&ctx->tc_phi, &ctx->tc_psi};
+    __nv_bfloat16** Xb[2] = {ctx->phiXb, ctx->psiXb};
+    __nv_bfloat16** Zb[2] = {ctx->phiZb, ctx->psiZb};
+    __nv_bfloat16** dzb[2] = {ctx->dzb_phi, ctx->dzb_psi};
+    __nv_bfloat16* Yb[2] = {ctx->phi_outb, ctx->psi_outb};
+    float* Yf[2] = {ctx->phi_out, ctx->psi_out};
+    float* stat[2] = {ctx->stat_phi + row_off, ctx->stat_psi + row_off};
+    tc::CChainParams& F = ctx->cchain_fwd_p;
+    tc::CChainParams& Bw = ctx->cchain_bwd_p;
+    F = tc::CChainParams{};
+    Bw = tc::CChainParams{};
+    F.M = Bw.M = Bl;
+    F.act = Bw.act = k.activation;
+    F.energy = Bw.energy = k.energy;
+    F.store_ok = Bw.store_ok = std::getenv("CRL_CCHAIN_NOSTORE") ? 0 : 1;
+    for (int e = 0; e < 2; ++e) {
+      const EncoderPlan& P = *plans[e];
+      const int L = P.n_layers;
+      auto& T = *tcs[e];
+      tc::CChainEnc& fe = F.enc[e];
+      tc::CChainEnc& be = Bw.enc[e];
+      fe.L = L;
+      fe.out_stat = stat[e];
+      ctx->cchain_fwd[e].a0 = T[0].fwdA;
+      bool ok = true;
+      for (int l = 0; l < L; ++l) {
+        const LayerPlan& Lp = P.layer[l];
+        tc::CChainLayer& cl = fe.layer[l];
+        cl.K = Lp.in; cl.N = Lp.out;
+        cl.bias = ctx->mem.params + Lp.b_off;
+        cl.out_z = (l < L - 1) ? Zb[e][l] : nullptr;
+        cl.out_act = (l == L - 1) ? Yb[e] : nullptr;
+        cl.out_f = (l == L - 1) ? Yf[e] : nullptr;
+        ctx->cchain_fwd[e].w[l] = T[l].fwdB;                      // W_l {out, in}, box {64, 64}
+        if (l < L - 1) ok = ok && tc::make_map_bf16(&ctx->cchain_fwd[e].st[l], Xb[e][l + 1], Lp.out, Bl, Lp.out, 64, 128);
+      }
+      be.L = L - 1;
+      be.out_stat = nullptr;
+      ctx->cchain_bwd[e].a0 = T[L - 1].dxA;                       // dY, box {64, 128}
+      for (int s2 = 0; s2 < L - 1; ++s2) {
+        const int l = L - 1 - s2;
+        const LayerPlan& Lp = P.layer[l];
+        tc::CChainLayer& cl = be.layer[s2];
+        cl.K = Lp.out; cl.N = Lp.in;
+        cl.zprev = Zb[e][l - 1];
+        ctx->cchain_bwd[e].w[s2] = T[l].fwdB;                     // the same bytes, read K-major
+        ok = ok && tc::make_map_bf16(&ctx->cchain_bwd[e].st[s2], dzb[e][l - 1], Lp.in, Bl, Lp.in, 64, 128);
+      }
+      if (!ok) return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the cluster chains");
+    }
+  }
   // initial bf16 shadow of the caller's parameters; zero the padded input rows
   CU(tc::launch_f32_to_bf16(ctx->mem.params, ctx->wshadow, ctx->sizes.n_params, ctx->num_sms, 0));
   CU(cudaMemset(ctx->x0_phi, 0, (size_t)k.batch_local * ctx->ld0_phi * 2));
@@ -308,6 +367,11 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     Stage sg(ctx, st, "mlp_fwd_chain");
     CU(tc::tc_chain_forward(ctx->chain_fwd[0], ctx->chain_fwd[1], ctx->chain_fwd_p, st));
     ++nl;
+  } else if (ctx->use_cchain) {
+    // both encoders, every layer, one launch of 4-CTA clusters; also the row statistics of Y
+    Stage sg(ctx, st, "mlp_fwd_cchain");
+    CU(tc::tc_cchain_forward(ctx->cchain_fwd[0], ctx->cchain_fwd[1], ctx->cchain_fwd_p, st));
+    ++nl;
   } else {
     fork2(ctx, st, st2);
     rs = enc_forward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiXb, ctx->psiZb, ctx->psi_out,
@@ -321,7 +385,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   const int S = ctx->lg_splits;
   if (ctx->tc_logits) {
     // per-row |x|^2 (L2) / 1/|x| (cos) of the bf16-rounded representations
-    if (!ctx->use_chain && !stat_in_fwd) { Stage sg(ctx, st, "rowstat");
+    if (!ctx->use_chain && !ctx->use_cchain && !stat_in_fwd) { Stage sg(ctx, st, "rowstat");
       const int fac_init = std::getenv("CRL_FORCE_EXACT_Q") ? 0 : 1;
       CU(tc::launch_rowstat_bf16(ctx->phi_outb, Bl, D, k.energy, ctx->stat_phi + row_off, ctx->fac_ok, fac_init,
                                  st));
@@ -465,7 +529,8 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     nl += 2; }
   cudaStream_t side = (st == st2) ? st : ctx->cap_stream3;      // phi weight gradients
   cudaStream_t side2 = (st == st2) ? st : ctx->cap_stream4;     // psi weight gradients
-  if (!ctx->use_chain) {
+  const bool fused_bwd = ctx->use_chain || ctx->use_cchain;      // one dX-chain launch for both
+  if (!fused_bwd) {
     rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side2, &nl);
     if (rs != CRL_OK) return rs;
   }
@@ -482,14 +547,19 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(tc::launch_f32_to_bf16(ctx->dphi, ctx->dphib, (size_t)Bl * D, ctx->num_sms, st));
     }
     nl += 2; }
-  if (!ctx->use_chain) {
+  if (!fused_bwd) {
     rs = enc_backward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiZb, st, side, &nl);
     if (rs != CRL_OK) return rs;
     join2(ctx, st, st2);
-  } else {
+  } else if (ctx->use_chain) {
     join2(ctx, st, st2);
     { Stage sg(ctx, st, "mlp_bwd_chain");          // both encoders' dX chains, one launch
       CU(tc::tc_chain_backward(ctx->chain_bwd[0], ctx->chain_bwd[1], ctx->chain_bwd_p, st));
+      ++nl; }
+  } else {
+    join2(ctx, st, st2);
+    { Stage sg(ctx, st, "mlp_bwd_cchain");         // both encoders' dX chains, 4-CTA clusters
+      CU(tc::tc_cchain_backward(ctx->cchain_bwd[0], ctx->cchain_bwd[1], ctx->cchain_bwd_p, st));
       ++nl; }
   }
   if (ctx->use_dwg) {
@@ -497,7 +567,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     Stage sg(ctx, st, "dw_db_grouped");
     CU(tc::tc_dwg_launch(ctx->dwg, st));
     ++nl;
-  } else if (ctx->use_chain) {
+  } else if (fused_bwd) {
     if (side != st) {
       cudaEventRecord(ctx->ev_side, st);
       cudaStreamWaitEvent(side, ctx->ev_side, 0);

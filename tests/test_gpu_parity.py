@@ -266,11 +266,13 @@ def test_critic_step_bf16_fused_chain(preset, over, monkeypatch):
     ("CRL_NO_FUSED_STATS", "l2"),         # two-call online-max statistics only
     ("CRL_NO_FUSED_GRAD", "l2"),          # two-call gradient pass (row call + column call)
     ("CRL_NO_FUSED_GRAD", "dot"),
+    ("CRL_FORCE_STATS_FALLBACK,CRL_COND_NODE", "l2"),   # fallback as a conditional graph node
 ])
 def test_critic_step_bf16_stats_paths(knob, energy, monkeypatch):
     """The one-pass row+column statistics (tc_stats.cu) are the default for L2 / cos at W = 1;
     its exact fallback (taken when a sum under/overflows) and the two-call path are forced."""
-    monkeypatch.setenv(knob, "1")
+    for kn in knob.split(","):
+        monkeypatch.setenv(kn, "1")
     cfg = crl_synth.preset("ant", batch=1100, width=128, energy=energy, precision="bf16")
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
 
