@@ -211,6 +211,7 @@ crl_status bf16_prepare(crl_ctx* ctx) {
     F.act = Bw.act = k.activation;
     F.energy = Bw.energy = k.energy;
     F.store_ok = Bw.store_ok = std::getenv("CRL_CCHAIN_NOSTORE") ? 0 : 1;
+    F.trace = Bw.trace = std::getenv("CRL_CCHAIN_TRACE") ? 1 : 0;
     for (int e = 0; e < 2; ++e) {
       const EncoderPlan& P = *plans[e];
       const int L = P.n_layers;

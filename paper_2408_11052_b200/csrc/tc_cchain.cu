@@ -17,6 +17,7 @@
 //         per-row statistic of bf16(Y) for the logits stage.
 //   BWD : dZ_{l-1} = (dZ_l W_l^T) * SiLU'(Z_{l-1}), l = L-1 .. 1, from dY; dZ stored by TMA.
 // blockIdx.y picks phi or psi: both encoders in one launch.
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -63,6 +64,18 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
+// mbarrier wait with cluster-scope acquire (the arrivals are remote releases)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEC_%=;\n\t"
+      "bra WAITC_%=;\n"
+      "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ float tanh_fast(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -83,8 +96,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
   float* sStat = sBias + kCChainMaxL * 64;                     // [128] row-stat hand-off
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 128);
   uint64_t* a0_full = bars;                 // first-layer input (from HBM) in act buffer 0
-  uint64_t* in_full = bars + 1;             // [2] full next-layer input arrived (local + 3 peers)
-  uint64_t* w_full = in_full + 2;           // [2]
+  uint64_t* in_full = bars + 1;             // [2][4] next-layer input chunk j arrived (per source CTA)
+  uint64_t* w_full = in_full + 2 * NC;      // [2]
   uint64_t* w_empty = w_full + 2;           // [2]
   uint64_t* acc_full = w_empty + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 2);
@@ -101,7 +114,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
     tma_prefetch_desc(&mp.a0);
     mbar_init(a0_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&in_full[i], 1);
+      for (int j = 0; j < NC; ++j) mbar_init(&in_full[i * NC + j], 1);   // leader arrival (+ peer bytes)
       mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1);
       mbar_init(&acc_full[i], 1);
     }
@@ -139,8 +152,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
       sBias[i] = (s < L && col < E.layer[s].N) ? E.layer[s].bias[col] : 0.f;
     }
   }
+  __shared__ unsigned long long s_tt[24];
+  const bool trace = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
+  auto gt = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+  if (trace && threadIdx.x == 0) s_tt[0] = gt();
   pdl_wait();
   pdl_launch();
+  if (trace && threadIdx.x == 0) s_tt[1] = gt();
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -159,22 +177,31 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
       const CChainLayer& Ly = E.layer[s];
       const int nkc = (Ly.K + 63) / 64;
       const uint32_t acc = tmem + (uint32_t)((s & 1) * 64);
-      // input of step s: HBM tile (s = 0) or the exchanged chunks (buffer s & 1)
+      // input of step s: HBM tile (s = 0) or the exchanged chunks (buffer s & 1), consumed in
+      // arrival order: this CTA's own chunk first, then the peers' as their copies land
       if (s == 0) mbar_wait(a0_full, 0);
-      else mbar_wait(&in_full[s & 1], ((s - 1) >> 1) & 1);
       mbar_wait(&w_full[s & 1], (s >> 1) & 1);
-      tc_fence_after();
       const uint32_t a_base = smem_u32(sAct + (s & 1) * NC * CHUNK);
       const uint32_t w_base = smem_u32(sW + (s & 1) * WSTAGE);
       const uint32_t idesc = idesc_bf16_f32(128, 64, false, MODE == 0);
-      for (int kc = 0; kc < nkc; ++kc)
+      for (int i = 0; i < nkc; ++i) {
+        const int kc = s == 0 ? i : (int)((c + i) % NC);
+        if (s > 0) {
+          mbar_wait_cluster(&in_full[(s & 1) * NC + kc], ((s - 1) >> 1) & 1);
+          // written by (remote) generic-proxy stores, read by the tensor core (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const uint64_t ad = smem_desc_sw128(a_base + kc * CHUNK + ks * 32, 16, 1024);
           const uint64_t bd = MODE == 0 ? smem_desc_sw128(w_base + kc * 8192 + ks * 2048, 8192, 1024)
                                         : smem_desc_sw128(w_base + kc * 8192 + ks * 32, 16, 1024);
-          mma_bf16(acc, ad, bd, idesc, (kc | ks) != 0);
+          mma_bf16(acc, ad, bd, idesc, (i | ks) != 0);
         }
+        if (trace && s < 6 && i == 0) s_tt[12 + 2 * s] = gt();      // first chunk issued
+        if (trace && s < 6 && i == nkc - 1) s_tt[13 + 2 * s] = gt(); // last chunk issued
+      }
       mma_commit(&acc_full[s & 1]);
       mma_commit(&w_empty[s & 1]);
     }
@@ -200,6 +227,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
         for (int j = 0; j < 4; ++j) zp[j] = zr[j];
       }
       mbar_wait(&acc_full[s & 1], (s >> 1) & 1);
+      if (trace && leader && s < 10) s_tt[2 + 2 * s] = gt();
       tc_fence_after();
       uint32_t raw[32];
       tmem_ld32_nowait(tmem + (uint32_t)((s & 1) * 64) + ((uint32_t)(q * 32) << 16) + 32 * wg, raw);
@@ -207,9 +235,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
       float v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
-      if (MODE == 0) {
+      if (MODE == 0) {                               // bias: 8 vector shared loads
+        const uint32_t ba = smem_u32(sBias + s * 64 + 32 * wg);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] += sBias[s * 64 + 32 * wg + i];
+        for (int j = 0; j < 8; ++j) {
+          float4 b;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                       : "r"(ba + 16u * j));
+          v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+        }
       }
       if (last_fwd) {
         // Y fp32 + bf16 and the row statistic of bf16(Y) (CTA 0 holds the whole row)
@@ -278,7 +312,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
           pk[i] = pack_bf16x2(v[2 * i] * g0, v[2 * i + 1] * g1);
         }
       }
-      // the chunk (this CTA's 64 columns of the next-layer input) -> own SMEM buffer
+      // the chunk (this CTA's 64 columns of the next-layer input) -> own SMEM buffer, then one
+      // DSMEM bulk copy to each peer.  (Measured alternative: every thread storing its rows
+      // into the peers with st.shared::cluster is 3x slower per step on B200.)
       const int nb = (s + 1) & 1;
       uint8_t* chunk = sAct + nb * NC * CHUNK + c * CHUNK;
       const uint32_t dst = smem_u32(chunk) + row_off;
@@ -292,28 +328,37 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
       tc_fence_before();
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (leader) {
-        if (p.store_ok) {                            // HBM copy (X_{l+1} or dZ_{l-1})
-          tma_store_2d(&mp.st[s], smem_u32(chunk), 64 * (int)c, m0);
-          bulk_commit();
-        }
+        // the FWD output layer runs on CTA 0 only: the others neither need nor wait for its
+        // input, and must not receive copies they will never wait for
+        const bool to_last = MODE == 0 && s + 1 == L - 1;
         if (!last_bwd) {
-          // push the chunk to the peers that run the next step; they expect it on in_full[nb]
-          // (the FWD output layer runs on CTA 0 only: the others neither need nor wait for
-          // its input, and must not receive copies they will never wait for)
-          const bool to_last = MODE == 0 && s + 1 == L - 1;
           const uint32_t src = smem_u32(chunk);
-          const uint32_t bar_local = smem_u32(&in_full[nb]);
+          const uint32_t bar_local = smem_u32(&in_full[nb * NC + c]);   // "chunk c arrived"
 #pragma unroll
           for (int i = 1; i < NC; ++i) {
             const uint32_t peer = (c + i) % NC;
             if (to_last && peer != 0) continue;
             dsmem_copy(mapa(src, peer), src, CHUNK, mapa(bar_local, peer));
           }
-          if (!to_last || c == 0) mbar_expect_tx(&in_full[nb], (NC - 1) * CHUNK);   // + own arrival
         }
-        // this buffer is rewritten two steps later: its HBM store must have read it by then
-        // (peer copies are covered by causality: the peers consumed it before step s + 2)
-        bulk_wait_read();
+        if (p.store_ok) {                            // HBM copy (X_{l+1} or dZ_{l-1})
+          tma_store_2d(&mp.st[s], smem_u32(chunk), 64 * (int)c, m0);
+          bulk_commit();
+        }
+        // The other buffer is rewritten by the NEXT step's epilogue, which can only start after
+        // the next MMA, which waits for this CTA's arrival below: the HBM store issued one step
+        // ago from that buffer must have read it by then (at most this step's store pending).
+        // (Peer copies are covered by causality: the peers consumed the buffer before that.)
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (!last_bwd && (!to_last || c == 0)) {
+          // the peers' chunks: expect their bytes; this CTA's own chunk: plain arrival
+#pragma unroll
+          for (int j = 0; j < NC; ++j) {
+            if (j == (int)c) mbar_arrive(&in_full[nb * NC + j]);
+            else mbar_expect_tx(&in_full[nb * NC + j], CHUNK);
+          }
+        }
+        if (trace && s < 10) s_tt[3 + 2 * s] = gt();
       }
     }
     if (leader) bulk_wait_all();
@@ -324,6 +369,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 128);
+  }
+  if (trace && threadIdx.x == 0) {
+    printf("CCHAIN_TRACE mode=%d L=%d pdl_wait=%llu", MODE, L, s_tt[1] - s_tt[0]);
+    for (int s = 0; s < L && s < 5; ++s)
+      printf(" | s%d mma0=%llu mmaN=%llu acc=%llu done=%llu", s, s_tt[12 + 2 * s] - s_tt[0], s_tt[13 + 2 * s] - s_tt[0],
+             s_tt[2 + 2 * s] - s_tt[0], s_tt[3 + 2 * s] - s_tt[0]);
+    printf(" | end=%llu\n", gt() - s_tt[0]);
   }
 }
 

@@ -30,6 +30,7 @@ struct CChainMaps {
 struct CChainParams {
   int M, act, energy;
   int store_ok;                   // 1 (measurement knob: 0 skips the HBM stores)
+  int trace;                      // measurement: globaltimer trace of cluster 0 (CRL_CCHAIN_TRACE)
   CChainEnc enc[2];
 };
 
