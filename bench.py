@@ -157,12 +157,13 @@ def stage_work(stage, cfg, N, Bl):
     if stage in ("grad_phi", "grad_psi"):
         # the two backward contractions (W Psi and W^T Phi): 2 N^2 D each, one per launch
         return 2.0 * Bl * N * D, "flop", "alu"
-    if stage in ("mlp_fwd_chain", "mlp_bwd_chain"):
-        # fused chains: every layer of both encoders (forward), every dX step (backward)
+    if stage in ("mlp_fwd_chain", "mlp_bwd_chain", "mlp_fwd_cchain", "mlp_bwd_cchain"):
+        # fused chains (per-row-block or cluster-split): every layer of both encoders
+        # (forward), every dX step (backward)
         tot = 0.0
         for ind in (in_phi, in_psi):
             d = dims(ind)
-            rng = range(len(d) - 1) if stage == "mlp_fwd_chain" else range(1, len(d) - 1)
+            rng = range(len(d) - 1) if stage.startswith("mlp_fwd") else range(1, len(d) - 1)
             tot += sum(2.0 * Bl * d[l] * d[l + 1] for l in rng)
         return tot, "flop", "tensor"
     if stage == "rowstat":
