@@ -96,20 +96,20 @@ __global__ void __launch_bounds__(256) relabel_sample_kernel(
     float* __restrict__ s_out, float* __restrict__ a_out, float* __restrict__ g_out,
     int64_t* __restrict__ idx_out, int* __restrict__ status) {
   extern __shared__ uint64_t q_sm[];
-  // stage Q[0..T] in shared memory
+  // stage Q[0..T] in shared memory; the loads are in flight while the attempts below run
+  // (they only need ep_end), the barrier comes just before the first Q lookup
   for (int k = threadIdx.x; k <= T; k += blockDim.x) q_sm[k] = qtab[k];
-  __syncthreads();
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int r = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (r >= B_l) return;
+  const bool active = r < B_l;                 // no early return: every thread reaches the barrier
   const uint32_t rho = (uint32_t)rank * (uint32_t)B_l + (uint32_t)r;
   const uint32_t n = tau_new - tau_old + 1;
 
   int found = -1;
   uint32_t e = 0, tau = 0, L = 0, x2 = 0, x3 = 0;
-  for (int base = 0; base < 64 && found < 0; base += 32) {
+  for (int base = 0; active && base < 64 && found < 0; base += 32) {
     const uint32_t att = (uint32_t)(base + lane);
     U4 x = philox4x32_10(U4{rho, att, step_lo, step_hi}, seed_lo, seed_hi);
     uint32_t ee = (uint32_t)(((uint64_t)x.x * (uint64_t)E) >> 32);
@@ -130,10 +130,12 @@ __global__ void __launch_bounds__(256) relabel_sample_kernel(
     }
   }
   if (found < 0) {
-    if (lane == 0) set_status(status, CRL_ESAMPLER);
+    if (active && lane == 0) set_status(status, CRL_ESAMPLER);
     // deterministic fill so downstream stays finite
     e = 0; tau = tau_old; L = 1; x2 = 0; x3 = 0;
   }
+  __syncthreads();                             // Q staged
+  if (!active) return;
   // k = min{k in [1, L] : Q[k] > t},  t = (R * Q[L]) >> 64
   const uint64_t R = ((uint64_t)x2 << 32) | (uint64_t)x3;
   const uint64_t tt = mulhi64(R, q_sm[L]);

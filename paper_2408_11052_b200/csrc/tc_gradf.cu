@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_gradf.h"
+#include "tc_merge.cuh"
 
 namespace crl {
 namespace tc {
@@ -513,11 +514,6 @@ static cudaError_t launch_gf(const CUtensorMap& a, const CUtensorMap& b, const C
   return launch_pdl(tc_gradf_kernel<E>, grid, dim3(384), smem, st, a, b, db, p);
 }
 
-struct GradMergeArgs {     // tc_logits.cu
-  const float* part; const float* prs; const __nv_bfloat16* A; const float* a_stat;
-  const __nv_bfloat16* Bg; const float* b_stat; int row_offset; float Cdiag; int Na, D, S;
-  float* out; __nv_bfloat16* outb;
-};
 cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st);
 
 // Both sides of the gradient.  Row side (A = Phi rows, B = Psi columns): part_da / part_rs
