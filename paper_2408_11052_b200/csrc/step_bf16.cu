@@ -120,9 +120,16 @@ crl_status bf16_prepare(crl_ctx* ctx) {
   // fused MLP chains (activations resident in SMEM/TMEM across layers) when the shapes fit
   // (measured on B200: the chain wins from B_l = 8192 on; below it the per-layer GEMMs, which
   // spread each layer over more SMs, are as fast or faster.  CRL_CHAIN / CRL_NO_CHAIN force it.)
+  // The cluster chains below (4 CTAs per 128 rows and encoder) win while they fit in one wave;
+  // once 8 ceil(B_l / 128) CTAs exceed the SM count the per-row-block chain is faster (measured:
+  // B_l = 2048 cchain 114 us/step vs chain 135; B_l = 4096 cchain 175 vs chain 165).
+  const bool cchain_shapes = tc::tc_cchain_supported(k.obs_dim + k.act_dim, k.width, k.repr_dim, k.depth) &&
+                             tc::tc_cchain_supported(k.goal_dim, k.width, k.repr_dim, k.depth);
+  const bool cchain_one_wave = 8 * ((k.batch_local + 127) / 128) <= ctx->num_sms;
   const bool chain_wanted = std::getenv("CRL_CHAIN") ? true
                             : std::getenv("CRL_NO_CHAIN") ? false
-                            : k.batch_local >= kChainMinBatch;
+                            : (k.batch_local >= kChainMinBatch || (cchain_shapes && !cchain_one_wave &&
+                                                                   !std::getenv("CRL_CCHAIN")));
   ctx->use_chain = ctx->tc_logits && chain_wanted && k.depth >= 1 &&
                    tc::tc_chain_supported(k.obs_dim + k.act_dim, k.width, k.repr_dim, k.depth) &&
                    tc::tc_chain_supported(k.goal_dim, k.width, k.repr_dim, k.depth);
@@ -190,9 +197,7 @@ crl_status bf16_prepare(crl_ctx* ctx) {
   }
   // cluster-split chains for the small batches the per-row-block chain does not cover
   ctx->use_cchain = !ctx->use_chain && ctx->tc_logits && !std::getenv("CRL_NO_CCHAIN") &&
-                    (std::getenv("CRL_CCHAIN") || k.batch_local < kChainMinBatch) &&
-                    tc::tc_cchain_supported(k.obs_dim + k.act_dim, k.width, k.repr_dim, k.depth) &&
-                    tc::tc_cchain_supported(k.goal_dim, k.width, k.repr_dim, k.depth);
+                    (std::getenv("CRL_CCHAIN") || k.batch_local < kChainMinBatch) && cchain_shapes;
   if (ctx->use_cchain) {
     const int Bl = k.batch_local, row_off = k.rank * Bl;
     const EncoderPlan* plans[2] = {&ctx->phi_plan, &ctx->psi_plan};

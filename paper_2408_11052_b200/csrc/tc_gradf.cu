@@ -18,6 +18,9 @@
 // term, the positive-pair term, fp32 + bf16 outputs).
 // fp32 atomics make the column-side sum order nondeterministic at the 1-ulp level (row side
 // and every other stage stay deterministic); the path's tolerance is 2e-2 (north_star).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -40,6 +43,26 @@ __device__ __forceinline__ float rsq(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+__device__ __forceinline__ float rsq_abs(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(fabsf(x)));
+  return y;
+}
+__device__ __forceinline__ float ex2_neg(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-x));
+  return y;
+}
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld1_nowait(uint32_t taddr, uint32_t& r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -89,6 +112,7 @@ struct TcGradFArgs {
   float* loss_out;                 // [4] or null
   int *skip, *adam_t, *status;
   float loss_cf, loss_cb, loss_beta;
+  int dbg;                         // timing ablations (CRL_GF_DBG): 1 no back-MMAs, 2 no W math, 4 no dB reduce
 };
 
 // the loss from the statistics (as optim.cu loss_partial / loss_finalize)
@@ -144,7 +168,9 @@ __device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t, int nthr) {
 }
 
 struct GfCfg {
-  static constexpr int D = 64, BNT = 128, STAGES = 3;
+  static constexpr int D = 64, BNT = 128, STAGES = 3, NWG = 4;   // 4 epilogue warpgroups
+  static constexpr int NT = 128 + 128 * NWG;                     // 4 role warps + epilogue
+  static constexpr int NDB = D + 16;                             // dB MMA width: 64 d + 16 ones
   static constexpr uint32_t A_BYTES = 128 * D * 2;       // 16 KB
   static constexpr uint32_t B_BYTES = BNT * D * 2;       // 16 KB
   static constexpr uint32_t W_BYTES = 128 * BNT * 2;     // 32 KB
@@ -152,27 +178,31 @@ struct GfCfg {
   static constexpr uint32_t ONES_BYTES = 128 * 128;      // 16 KB: K=128 rows x 64 bf16 ones
   static constexpr uint32_t STAT_BYTES = BNT * 4;
   static constexpr size_t smem() {
-    return 1024 + A_BYTES + STAGES * B_BYTES + 2 * W_BYTES + 2 * R_BYTES + ONES_BYTES + STAGES * 3 * STAT_BYTES +
-           3 * 128 * 4 + 256;
+    return 1024 + A_BYTES + ONES_BYTES + STAGES * B_BYTES + 2 * W_BYTES + 2 * R_BYTES + STAGES * 3 * STAT_BYTES +
+           3 * 128 * 4 + 320;
   }
 };
 
 template <int ENERGY>
-__global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                          const __grid_constant__ CUtensorMap tmB,
-                                                          const __grid_constant__ CUtensorMap tmDB,
-                                                          TcGradFArgs p) {
+__global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                const __grid_constant__ CUtensorMap tmB,
+                                                                const __grid_constant__ CUtensorMap tmDB,
+                                                                TcGradFArgs p) {
   using C = GfCfg;
-  constexpr int BNT = C::BNT, STAGES = C::STAGES, D = C::D;
+  constexpr int BNT = C::BNT, STAGES = C::STAGES, D = C::D, NWG = C::NWG;
+  constexpr int NEPI = 4 * NWG;                           // epilogue warps
   constexpr bool L2 = ENERGY == CRL_ENERGY_L2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // sOnes sits right after sA: the dB MMA reads B = [A | 1] as one MN-major operand whose
+  // second 64-wide N chunk (LBO = 16 KB away) is all ones, so its columns 64..79 are the
+  // column sums of w (L2) at no extra instruction
   uint8_t* sA = smem;
-  uint8_t* sB = sA + C::A_BYTES;
+  uint8_t* sOnes = sA + C::A_BYTES;
+  uint8_t* sB = sOnes + C::ONES_BYTES;
   uint8_t* sW = sB + STAGES * C::B_BYTES;
   uint8_t* sR = sW + 2 * C::W_BYTES;
-  uint8_t* sOnes = sR + 2 * C::R_BYTES;
-  float* sStat = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);      // [STAGES][3][BNT]
+  float* sStat = reinterpret_cast<float*>(sR + 2 * C::R_BYTES);        // [STAGES][3][BNT]
   float* sMerge = sStat + STAGES * 3 * BNT;                            // [3][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + 3 * 128);
   uint64_t* a_full = bars;
@@ -185,7 +215,9 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
   uint64_t* db_full = w_empty + 2;       // [2]
   uint64_t* db_empty = db_full + 2;      // [2]
   uint64_t* da_full = db_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_full + 1);
+  uint64_t* r_full = da_full + 1;        // [half][buf]: the 8 warps of a half staged dB
+  uint64_t* r_free = r_full + 4;         // [half][buf]: the reduction that last read it is done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r_free + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a0 = blockIdx.x * 128;
@@ -193,6 +225,15 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
   const int jbeg = split * p.cols_per_split;
   const int jend = min(p.Nb, jbeg + p.cols_per_split);
   const int ntiles = jend > jbeg ? (jend - jbeg + BNT - 1) / BNT : 0;
+  // the row blocks walk their column tiles from staggered starting points: in lockstep they
+  // would all TMA-reduce into the same dB tile (and red.add the same column sums) at once
+  const int rot = ntiles > 0 ? blockIdx.x % ntiles : 0;
+  auto tile_j0 = [&](int t) { const int tt = t + rot; return jbeg + (tt >= ntiles ? tt - ntiles : tt) * BNT; };
+  __shared__ long long s_tr[7][17];
+  __shared__ long long s_trw[16][16];             // W done per epilogue warp (dbg & 32)
+  const bool trace = (p.dbg & 8) && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && blockIdx.y == 0;
+  const int tr_sh = (p.dbg & 16) ? 3 : 0;          // trace every tile, or every 8th (dbg & 16)
+  if (trace && threadIdx.x == 0) s_tr[0][0] = clock64();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -201,11 +242,12 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
     mbar_init(a_full, 1);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
-      mbar_init(&w_full[i], 8); mbar_init(&w_empty[i], 1);
-      mbar_init(&db_full[i], 1); mbar_init(&db_empty[i], 8);
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], NEPI);
+      mbar_init(&w_full[i], NEPI); mbar_init(&w_empty[i], 1);
+      mbar_init(&db_full[i], 1); mbar_init(&db_empty[i], NEPI);
     }
     mbar_init(da_full, 1);
+    for (int i = 0; i < 4; ++i) { mbar_init(&r_full[i], 8); mbar_init(&r_free[i], 1); }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -216,11 +258,9 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // TMEM columns: S[2] 0..255, dA 256..319, dB[2] (80 wide: d | column sums) 320..479
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tm_s[2] = {tmem, tmem + 128};
   const uint32_t tm_da = tmem + 256;
-  const uint32_t tm_db[2] = {tmem + 320, tmem + 384};
-  const uint32_t tm_cs[2] = {tmem + 448, tmem + 464};
   pdl_wait();
   pdl_launch();
 
@@ -231,7 +271,7 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % STAGES;
       mbar_wait(&b_empty[s], ((t / STAGES) & 1) ^ 1);
-      const int j0 = jbeg + t * BNT;
+      const int j0 = tile_j0(t);
       mbar_expect_tx(&b_full[s], C::B_BYTES + 3 * C::STAT_BYTES);
       tma_load_2d(sB + s * C::B_BYTES, &tmB, &b_full[s], 0, j0);
       float* st = sStat + s * 3 * BNT;
@@ -243,11 +283,9 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
     // ------------------------------------------------------------------ MMA issuer
     const uint32_t id_s = idesc_bf16_f32(128, BNT, false, false);
     const uint32_t id_da = idesc_bf16_f32(128, D, false, true);      // A = W (K-major), B = B tile (MN)
-    const uint32_t id_db = idesc_bf16_f32(128, D, true, true);       // A = W^T (MN), B = A tile (MN)
-    const uint32_t id_cs = idesc_bf16_f32(128, 16, true, true);
+    const uint32_t id_db = idesc_bf16_f32(128, L2 ? C::NDB : D, true, true);   // A = W^T, B = [A | 1] (MN)
     mbar_wait(a_full, 0);
     const uint32_t a_base = smem_u32(sA);
-    const uint32_t ones = smem_u32(sOnes);
     auto issue_s = [&](int t) {
       const int s = t % STAGES, b = t & 1;
       mbar_wait(&b_full[s], (t / STAGES) & 1);
@@ -256,9 +294,10 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
       const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks)
-        mma_bf16(tm_s[b], smem_desc_sw128(a_base + ks * 32, 16, 1024), smem_desc_sw128(b_base + ks * 32, 16, 1024),
-                 id_s, ks != 0);
+        mma_bf16(tmem + 128 * b, smem_desc_sw128(a_base + ks * 32, 16, 1024),
+                 smem_desc_sw128(b_base + ks * 32, 16, 1024), id_s, ks != 0);
       mma_commit(&s_full[b]);
+      if (trace && (t & ((1 << tr_sh) - 1)) == 0 && (t >> tr_sh) < 16) s_tr[1][(t >> tr_sh) + 1] = clock64();
     };
     auto issue_back = [&](int t) {
       const int s = t % STAGES, b = t & 1;
@@ -267,6 +306,10 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
       tc_fence_after();
       const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
       const uint32_t w_base = smem_u32(sW + b * C::W_BYTES);
+      if (p.dbg & 1) {
+        mma_commit(&db_full[b]); mma_commit(&w_empty[b]); mma_commit(&b_empty[s]);
+        return;
+      }
       // dA += W . B_t   (K = the 128 tile columns j: 64-wide chunks of W 16 KB apart)
 #pragma unroll
       for (int c = 0; c < 2; ++c)
@@ -276,37 +319,39 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
           mma_bf16(tm_da, smem_desc_sw128(w_base + c * 16384 + ks * 32, 16, 1024),
                    smem_desc_sw128(b_base + j * 128, BNT * 128, 1024), id_da, (t | c | ks) != 0);
         }
-      // dB_t = W^T . A   (K = the 128 tile rows i, 16 per MMA = +2048 B in the SW128 rows)
+      // [dB_t | cs_t] = W^T . [A | 1]   (K = the 128 tile rows i, 16 per MMA = +2048 B)
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks)
-        mma_bf16(tm_db[b], smem_desc_sw128(w_base + ks * 2048, 16384, 1024),
+        mma_bf16(tmem + 320 + C::NDB * b, smem_desc_sw128(w_base + ks * 2048, 16384, 1024),
                  smem_desc_sw128(a_base + ks * 2048, 16384, 1024), id_db, ks != 0);
-      if (L2) {
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          mma_bf16(tm_cs[b], smem_desc_sw128(w_base + ks * 2048, 16384, 1024),
-                   smem_desc_sw128(ones + ks * 2048, 16384, 1024), id_cs, ks != 0);
-      }
       mma_commit(&db_full[b]);
       mma_commit(&w_empty[b]);
       mma_commit(&b_empty[s]);
+      if (trace && (t & ((1 << tr_sh) - 1)) == 0 && (t >> tr_sh) < 16) s_tr[2][(t >> tr_sh) + 1] = clock64();
     };
+    // S runs two tiles ahead (S_0, S_1 up front; S_{t+2} right after the back-MMAs of tile
+    // t).  The back-MMAs go first: S_{t+2} waits for B_{t+2}, whose stage the back-MMAs of
+    // t-1 free, and issuing it first closed a loop (back MMAs -> TMA -> S -> back MMAs) that
+    // set the per-tile period (measured, clock64 trace: ~3250 clk/tile).
+    for (int t = 0; t < ntiles && t < 2; ++t) issue_s(t);
     for (int t = 0; t < ntiles; ++t) {
-      issue_s(t);
-      if (t > 0) issue_back(t - 1);
+      issue_back(t);
+      if (t + 2 < ntiles) issue_s(t + 2);
     }
-    if (ntiles > 0) issue_back(ntiles - 1);
     mma_commit(da_full);
   } else if (warp == 2 || warp == 3) {
     if (p.loss_part != nullptr && split == 0) gradf_loss_rows<ENERGY>(p, a0, threadIdx.x - 64, 64);
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
-    const int wg = (warp - 4) >> 2;                       // column half of the tile
+    const int wg = (warp - 4) >> 2;                       // column quarter of the tile
     const int q = warp & 3;                               // TMEM lane quarter
     const int r = q * 32 + lane;                          // row within the tile
     const int row = a0 + r;
     const bool rv = row < p.Na;
-    const bool storer = q == 0 && lane == 0;
+    const int half = wg >> 1;                             // 64-column half (W) / 32-column half (dB)
+    const int swg = (p.dbg & 64) ? 1 : 0, cwg = (p.dbg & 64) ? 3 : 0;
+    const bool storer = (wg & 1) == swg && q == 0 && lane == 0;   // issues the reductions of its half
+    const uint32_t lq = (uint32_t)(q * 32) << 16;
     const float astat = rv ? p.a_stat[row] : 0.f;
     const float lr2 = rv ? p.lr[row] * gf::kLog2e : INFINITY;      // rows past the batch: p = 0
     const float lr_nat = rv ? p.lr[row] : 0.f;
@@ -316,120 +361,162 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
     const float cc0 = p.invN * p.c_c;
     const float rmask = rv ? 1.f : 0.f;
     constexpr float L2e2 = gf::kLog2e * gf::kLog2e;
-    const float a_l2 = astat * L2e2;
+    const float a_l2 = (astat + kEpsL2) * L2e2;
     const float lsc = L2 ? gf::kLog2e : 1.f;      // L2: w = g rs' L
     const float EiL = Ei * lsc, ArowL = Arow * lsc, cc0L = cc0 * lsc;
     const uint32_t w_row = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
-    float wsum4[4] = {0.f, 0.f, 0.f, 0.f};
+    f32x2 wsum2 = f2_pack(0.f, 0.f);
 
-    // dB_{u} readout: TMEM -> swizzled SMEM staging -> TMA add-reduction into the accumulator
+    // dB_{u} readout: TMEM -> swizzled SMEM staging -> TMA add-reduction into the accumulator.
+    // No warpgroup barrier: each warp stages its rows and arrives on r_full; the storer of the
+    // half issues the reduction of tile u - 1 at readout u (its r_full has long completed), so
+    // only mbarrier phases couple the warps and the XU work of one warp overlaps the readout of
+    // another.  Staging buffer reuse (every 2 tiles) waits on r_free, which the storer arrives
+    // on once cp.async.bulk.wait_group.read says the previous reduction read it.
+    const uint32_t r_base = smem_u32(sR + half * 16384);
+    auto issue_reduce = [&](int u) {
+      const int bu = u & 1;
+      mbar_wait(&r_full[half * 2 + bu], (u >> 1) & 1);
+      if (!(p.dbg & 4)) {
+        gf::tma_reduce_add_2d(&tmDB, r_base + bu * C::R_BYTES, 32 * half, tile_j0(u));
+        gf::bulk_commit();
+      }
+    };
     auto readout = [&](int u) {
       const int bu = u & 1;
-      const int j0 = jbeg + u * BNT;
+      const int j0 = tile_j0(u);
+      const uint32_t tdb = tmem + 320 + C::NDB * bu + lq;
+      if (storer) {
+        if (u >= 1) issue_reduce(u - 1);
+        gf::bulk_wait_read1();                      // the reduction of tile u - 2 has read buffer bu
+        mbar_arrive(&r_free[half * 2 + bu]);
+      }
       mbar_wait(&db_full[bu], (u >> 1) & 1);
+      if (trace && threadIdx.x == 128 && (u & ((1 << tr_sh) - 1)) == 0 && (u >> tr_sh) < 16) s_tr[6][(u >> tr_sh) + 1] = clock64();
       tc_fence_after();
-      uint32_t v[32];
-      float cs[16];
-      tmem_ld32_nowait(tm_db[bu] + ((uint32_t)(q * 32) << 16) + 32 * wg, v);
-      if (L2 && wg == 0) tmem_ld16(tm_cs[bu] + ((uint32_t)(q * 32) << 16), cs);
+      uint32_t v[16], cs = 0u;
+      gf::tmem_ld16_nowait(tdb + 16 * wg, v);      // d columns [16 wg, 16 wg + 16)
+      if (L2 && wg == cwg) gf::tmem_ld1_nowait(tdb + D, cs);   // column 64: sum_i w_ij
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&db_empty[bu]);
-      if (L2 && wg == 0 && j0 + r < jend) atomicAdd(p.cs_acc + j0 + r, cs[0]);
-      // the staging half this warpgroup writes was last read by the reduction of tile u - 2
-      if (storer) gf::bulk_wait_read1();
-      asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
-      const uint32_t dst = smem_u32(sR + bu * C::R_BYTES + wg * 16384) + w_row;
+      if (L2 && wg == cwg && !(p.dbg & 128) && j0 + r < jend) atomicAdd(p.cs_acc + j0 + r, __uint_as_float(cs));
+      mbar_wait(&r_free[half * 2 + bu], (u >> 1) & 1);
+      const uint32_t dst = r_base + bu * C::R_BYTES + w_row;
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        gf::sts128(dst + (uint32_t)((c ^ (r & 7)) << 4), make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
-      if (storer) {
-        gf::tma_reduce_add_2d(&tmDB, smem_u32(sR + bu * C::R_BYTES + wg * 16384), 32 * wg, j0);
-        gf::bulk_commit();
+      for (int c = 0; c < 4; ++c) {
+        const int g = 4 * (wg & 1) + c;
+        gf::sts128(dst + (uint32_t)((g ^ (r & 7)) << 4), make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r_full[half * 2 + bu]);
+      if (trace && threadIdx.x == 128 && (u & ((1 << tr_sh) - 1)) == 0 && (u >> tr_sh) < 16) s_tr[5][(u >> tr_sh) + 1] = clock64();
     };
 
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % STAGES, b = t & 1;
-      const int j0 = jbeg + t * BNT;
+      const int j0 = tile_j0(t);
       const int nval = jend - j0;
+      const int c0 = 32 * wg;                             // this warpgroup's 32 tile columns
       mbar_wait(&s_full[b], (t >> 1) & 1);
+      if (trace && threadIdx.x == 128 && (t & ((1 << tr_sh) - 1)) == 0 && (t >> tr_sh) < 16) s_tr[3][(t >> tr_sh) + 1] = clock64();
       tc_fence_after();
-      uint32_t raw[2][32];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) tmem_ld32_nowait(tm_s[b] + ((uint32_t)(q * 32) << 16) + wg * 64 + 32 * c, raw[c]);
+      uint32_t raw[32];
+      tmem_ld32_nowait(tmem + 128 * b + lq + c0, raw);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[b]);
       if (t >= 2) mbar_wait(&w_empty[b], ((t >> 1) - 1) & 1);
       const float* bst = sStat + s * 3 * BNT;
-      const uint32_t wt = smem_u32(sW + b * C::W_BYTES + wg * 16384) + w_row;
+      const uint32_t wt = smem_u32(sW + b * C::W_BYTES + half * 16384) + w_row;
       // four instantiations (ragged tile x fast factor path): kernel-uniform choices stay out
-      // of the per-logit code.  Fast L2 path, all in log2 units (L = log2 e):
-      //   d2' = max(L^2 (|a|^2 + |b|^2 - 2 a.b), L^2 eps), rs' = rsqrt(d2') = 1 / (L r)
-      //   t   = l2 - lse2_i = -d2' rs' - lse2_i,  p = 2^t
-      //   w   = g / r = p (E_i cc_j + A_i) L rs'   (L folded into E_i, A_i)
+      // of the per-logit code.  Fast L2 path, all in log2 units (L = log2 e), pairs of logits
+      // per FFMA2 / FMUL2 / FADD2:
+      //   d2' = L^2 (|a|^2 + eps + |b|^2 - 2 a.b), rs' = rsqrt(|d2'|) = 1 / (L r)
+      //   t   = d2' rs' + lse2_i,  p = 2^-t            (= 2^(l2 - lse2_i))
+      //   w   = g / r = p (E_i cc_j + A_i) L rs'       (L folded into E_i, A_i)
+      // (|.| and the negation are free MUFU operand modifiers)
       auto tile = [&](auto masked, auto fast) {
         constexpr bool MASK = decltype(masked)::value;
         constexpr bool FAST = decltype(fast)::value;
+        float w[32];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int c0 = wg * 64 + 32 * c;                // column within the tile
-          float w[32];
+        for (int i4 = 0; i4 < 8; ++i4) {
+          const float4 b4 = gf::lds128f(smem_u32(bst + c0 + 4 * i4));
+          const float4 f4 = gf::lds128f(smem_u32(bst + (FAST ? 2 : 1) * BNT + c0 + 4 * i4));
+          if (FAST) {
 #pragma unroll
-          for (int i4 = 0; i4 < 8; ++i4) {
-            const float4 b4 = gf::lds128f(smem_u32(bst + c0 + 4 * i4));
-            const float4 f4 = gf::lds128f(smem_u32(bst + (FAST ? 2 : 1) * BNT + c0 + 4 * i4));
+            for (int h = 0; h < 2; ++h) {
+              const int i = 4 * i4 + 2 * h;
+              const f32x2 v2 = f2_pack(__uint_as_float(raw[i]), __uint_as_float(raw[i + 1]));
+              const f32x2 b2 = h ? f2_pack(b4.z, b4.w) : f2_pack(b4.x, b4.y);
+              const f32x2 f2 = h ? f2_pack(f4.z, f4.w) : f2_pack(f4.x, f4.y);
+              const f32x2 fac = f2_fma(f2_pack(EiL, EiL), f2, f2_pack(ArowL, ArowL));
+              float t0, t1, rs0 = 1.f, rs1 = 1.f;
+              if (L2) {
+                const f32x2 d2 = f2_fma(f2_pack(-2.f * L2e2, -2.f * L2e2), v2,
+                                        f2_fma(f2_pack(L2e2, L2e2), b2, f2_pack(a_l2, a_l2)));
+                float d0, d1;
+                f2_unpack(d2, d0, d1);
+                rs0 = gf::rsq_abs(d0);
+                rs1 = gf::rsq_abs(d1);
+                f2_unpack(f2_fma(d2, f2_pack(rs0, rs1), f2_pack(lr2, lr2)), t0, t1);
+              } else {
+                f2_unpack(f2_fma(v2, f2_pack(-gf::kLog2e, -gf::kLog2e), f2_pack(lr2, lr2)), t0, t1);
+              }
+              if (MASK) {
+                t0 = c0 + i < nval ? t0 : INFINITY;
+                t1 = c0 + i + 1 < nval ? t1 : INFINITY;
+              }
+              f32x2 wv = f2_mul(f2_pack(gf::ex2_neg(t0), gf::ex2_neg(t1)), fac);
+              if (L2) {
+                wv = f2_mul(wv, f2_pack(rs0, rs1));
+                wsum2 = f2_add(wsum2, wv);
+              }
+              f2_unpack(wv, w[i], w[i + 1]);
+            }
+          } else {                                        // exact: q = 2^(l2 - lse2'_j)
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
             const float ff[4] = {f4.x, f4.y, f4.z, f4.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int i = 4 * i4 + u;
-              const int jl = c0 + i;
-              const float v = __uint_as_float(raw[c][i]);
-              float rs = 1.f, wv;
-              if (FAST) {
-                float tv;
-                if (L2) {
-                  const float d2 = fmaxf(fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2)), kEpsL2 * L2e2);
-                  rs = gf::rsq(d2);
-                  tv = fmaf(-d2, rs, -lr2);
-                } else {
-                  tv = fmaf(v, gf::kLog2e, -lr2);
-                }
-                if (MASK) tv = jl < nval ? tv : -INFINITY;
-                wv = gf::ex2(tv) * fmaf(EiL, ff[u], ArowL);
-              } else {                                    // exact: q = 2^(l2 - lse2'_j)
-                float l2v;
-                if (L2) {
-                  const float d2 = fmaxf(fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2)), kEpsL2 * L2e2);
-                  rs = gf::rsq(d2);
-                  l2v = -d2 * rs;
-                } else {
-                  l2v = v * gf::kLog2e;
-                }
-                if (MASK) l2v = jl < nval ? l2v : -INFINITY;
-                const float qe = gf::ex2(l2v - ff[u] * gf::kLog2e);
-                wv = fmaf(gf::ex2(l2v - lr2), ArowL, qe * cc0L) * rmask;
+              const float v = __uint_as_float(raw[i]);
+              float rs = 1.f, l2v;
+              if (L2) {
+                const float d2 = fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2));
+                rs = gf::rsq_abs(d2);
+                l2v = -fabsf(d2) * rs;
+              } else {
+                l2v = v * gf::kLog2e;
               }
-              if (L2) { wv *= rs; wsum4[u] += wv; }
+              if (MASK) l2v = c0 + i < nval ? l2v : -INFINITY;
+              const float qe = gf::ex2(l2v - ff[u] * gf::kLog2e);
+              float wv = fmaf(gf::ex2(l2v - lr2), ArowL, qe * cc0L) * rmask;
+              if (L2) { wv *= rs; wsum2 = f2_add(wsum2, f2_pack(wv, 0.f)); }
               w[i] = wv;
             }
           }
+        }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int k = 32 * c + 8 * u;                  // column within this 64-wide half
-            gf::sts128(wt + (uint32_t)((((k >> 3) ^ (r & 7))) << 4),
-                       make_uint4(pack_bf16x2(w[8 * u], w[8 * u + 1]), pack_bf16x2(w[8 * u + 2], w[8 * u + 3]),
-                                  pack_bf16x2(w[8 * u + 4], w[8 * u + 5]), pack_bf16x2(w[8 * u + 6], w[8 * u + 7])));
-          }
+        for (int u = 0; u < 4; ++u) {
+          const int k = 32 * (wg & 1) + 8 * u;             // column within this 64-wide half
+          gf::sts128(wt + (uint32_t)((((k >> 3) ^ (r & 7))) << 4),
+                     make_uint4(pack_bf16x2(w[8 * u], w[8 * u + 1]), pack_bf16x2(w[8 * u + 2], w[8 * u + 3]),
+                                pack_bf16x2(w[8 * u + 4], w[8 * u + 5]), pack_bf16x2(w[8 * u + 6], w[8 * u + 7])));
         }
       };
-      if (fac_fast) {
+      if (p.dbg & 2) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = 32 * (wg & 1) + 8 * u;
+          gf::sts128(wt + (uint32_t)((((k >> 3) ^ (r & 7))) << 4),
+                     make_uint4(raw[8 * u], raw[8 * u + 2], raw[8 * u + 4], raw[8 * u + 6]));
+        }
+      } else if (fac_fast) {
         if (nval >= BNT) tile(std::false_type{}, std::true_type{});
         else tile(std::true_type{}, std::true_type{});
       } else {
@@ -439,31 +526,33 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&w_full[b]);
+      if (trace && (p.dbg & 32) && lane == 0 && t < 16) s_trw[warp - 4][t] = clock64();
+      if (trace && threadIdx.x == 128 && (t & ((1 << tr_sh) - 1)) == 0 && (t >> tr_sh) < 16) s_tr[4][(t >> tr_sh) + 1] = clock64();
       if (t > 0) readout(t - 1);
     }
     if (ntiles > 0) readout(ntiles - 1);
+    if (storer && ntiles > 0) issue_reduce(ntiles - 1);
     // row side: partial row sums of w (L2) and the split's dA
-    const float wsum = (wsum4[0] + wsum4[1]) + (wsum4[2] + wsum4[3]);
-    if (wg == 1) sMerge[r] = wsum;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (wg == 0 && rv && L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[r];
-    if (wg == 0) {
-      mbar_wait(da_full, 0);
-      tc_fence_after();
-      float* out = p.part_da + ((size_t)split * p.Na + row) * D;
-#pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 16) {
-        float v[16];
-        tmem_ld16(tm_da + ((uint32_t)(q * 32) << 16) + c0, v);
-        if (ntiles == 0) {
+    float ws0, ws1;
+    f2_unpack(wsum2, ws0, ws1);
+    const float wsum = ws0 + ws1;
+    if (wg > 0) sMerge[(wg - 1) * 128 + r] = wsum;
+    asm volatile("bar.sync 1, %0;" ::"n"(128 * NWG) : "memory");
+    if (wg == 0 && rv && L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[r] + sMerge[128 + r] + sMerge[256 + r];
+    mbar_wait(da_full, 0);
+    tc_fence_after();
+    {
+      float v[16];
+      tmem_ld16(tm_da + lq + 16 * wg, v);
+      if (ntiles == 0) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        }
-        if (rv) {
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+      if (rv) {
+        float* out = p.part_da + ((size_t)split * p.Na + row) * D + 16 * wg;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            reinterpret_cast<float4*>(out + c0)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<float4*>(out)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       }
     }
     if (storer) gf::bulk_wait_all();
@@ -474,6 +563,12 @@ __global__ void __launch_bounds__(384, 1) tc_gradf_kernel(const __grid_constant_
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  if (trace && (p.dbg & 32) && threadIdx.x == 0)
+    for (int t = 0; t < 16 && t < ntiles; ++t)
+      for (int w = 0; w < 16; ++w) printf("GF_TRW %d %d %d %lld\n", blockIdx.x, t, w, s_trw[w][t] - s_tr[0][0]);
+  if (trace && threadIdx.x == 0)
+    for (int k = 1; k < 7; ++k)
+      for (int t = 1; t < 17; ++t) printf("GF_TRACE %d %d %d %lld\n", blockIdx.x, k, t - 1, s_tr[k][t] - s_tr[0][0]);
 }
 
 // ------------------------------------------------------------------------------- host side
@@ -483,6 +578,7 @@ bool tc_gradf_supports(int D, int energy) { return D == 64 && (energy == CRL_ENE
 
 // column splits minimising the makespan (waves x tiles per CTA) of the rb x S grid, <= 16
 int tc_gradf_splits(int Na, int Nb, int num_sms) {
+  if (const char* e = std::getenv("CRL_GF_SPLITS")) return std::max(1, std::min(16, std::atoi(e)));
   const int rb = (Na + 127) / 128;
   const int tiles = (Nb + 127) / 128;
   int best = 1;
@@ -511,7 +607,7 @@ static cudaError_t launch_gf(const CUtensorMap& a, const CUtensorMap& b, const C
     attr = true;
   }
   dim3 grid((p.Na + 127) / 128, S);
-  return launch_pdl(tc_gradf_kernel<E>, grid, dim3(384), smem, st, a, b, db, p);
+  return launch_pdl(tc_gradf_kernel<E>, grid, dim3(GfCfg::NT), smem, st, a, b, db, p);
 }
 
 cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st);
@@ -534,6 +630,7 @@ cudaError_t tc_grad_fused(int energy, const CUtensorMap& mA, const CUtensorMap& 
   p.phi32 = loss.phi32; p.psi32 = loss.psi32; p.loss_part = loss.part; p.loss_ticket = loss.ticket;
   p.loss_acc = loss.acc; p.loss_out = loss.out; p.skip = loss.skip; p.adam_t = loss.adam_t; p.status = loss.status;
   p.loss_cf = loss.c_f; p.loss_cb = loss.c_b; p.loss_beta = loss.beta;
+  p.dbg = std::getenv("CRL_GF_DBG") ? std::atoi(std::getenv("CRL_GF_DBG")) : 0;
   cudaError_t e = energy == CRL_ENERGY_L2 ? launch_gf<CRL_ENERGY_L2>(mA, mB, mDB, p, S, st)
                                           : launch_gf<CRL_ENERGY_DOT>(mA, mB, mDB, p, S, st);
   if (e != cudaSuccess) return e;
