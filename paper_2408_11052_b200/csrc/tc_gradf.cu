@@ -84,8 +84,30 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
                "r"(src), "r"(x), "r"(y)
                : "memory");
 }
+// mbarrier wait; built with -DCRL_GF_WATCHDOG it reports a stuck barrier and traps instead of
+// hanging (debugging aid)
+__device__ __noinline__ void wait_report(int id, uint32_t parity) {
+  printf("GF_WATCHDOG block (%d,%d) thread %d barrier %d parity %u\n", blockIdx.x, blockIdx.y, threadIdx.x, id,
+         parity);
+  __trap();
+}
+__device__ __forceinline__ void wait_wd(uint64_t* bar, uint32_t parity, int id) {
+#ifndef CRL_GF_WATCHDOG
+  (void)id;
+  mbar_wait(bar, parity);
+  return;
+#endif
+  uint32_t ok = 0;
+  for (uint32_t n = 0;; ++n) {
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    if (n == (1u << 24)) wait_report(id, parity);
+  }
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 }  // namespace gf
@@ -117,8 +139,8 @@ struct TcGradFArgs {
 
 // the loss from the statistics (as optim.cu loss_partial / loss_finalize)
 template <int ENERGY>
-__device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t, int nthr) {
-  __shared__ float red[3][2];
+__device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t) {
+  constexpr int nthr = 32;
   float s1 = 0.f, s2 = 0.f, s3 = 0.f;
   for (int r = t; r < 128; r += nthr) {
     const int i = a0 + r;
@@ -141,14 +163,11 @@ __device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t, int nthr) {
     s1 += lr - l; s2 += lc - l; s3 += lr * lr;
   }
   s1 = warp_sum(s1); s2 = warp_sum(s2); s3 = warp_sum(s3);
-  const int w = t >> 5;
-  if ((t & 31) == 0) { red[0][w] = s1; red[1][w] = s2; red[2][w] = s3; }
-  asm volatile("bar.sync 4, 64;" ::: "memory");
   if (t != 0) return;
   const int rb = a0 / 128, R = (p.Na + 127) / 128;
-  p.loss_part[rb * 4 + 0] = red[0][0] + red[0][1];
-  p.loss_part[rb * 4 + 1] = red[1][0] + red[1][1];
-  p.loss_part[rb * 4 + 2] = red[2][0] + red[2][1];
+  p.loss_part[rb * 4 + 0] = s1;
+  p.loss_part[rb * 4 + 1] = s2;
+  p.loss_part[rb * 4 + 2] = s3;
   __threadfence();
   if (atomicAdd(p.loss_ticket, 1u) != (unsigned)(R - 1)) return;
   __threadfence();
@@ -168,9 +187,9 @@ __device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t, int nthr) {
 }
 
 struct GfCfg {
-  static constexpr int D = 64, BNT = 128, STAGES = 3, NWG = 4;   // 4 epilogue warpgroups
-  static constexpr int NT = 128 + 128 * NWG;                     // 4 role warps + epilogue
-  static constexpr int NDB = D + 16;                             // dB MMA width: 64 d + 16 ones
+  static constexpr int D = 64, BNT = 128, STAGES = 3;
+  static constexpr int NT = 128 + 512;                 // 4 role warps + 2 groups x 2 warpgroups
+  static constexpr int NDB = D + 16;                   // dB MMA width: 64 d + 16 ones
   static constexpr uint32_t A_BYTES = 128 * D * 2;       // 16 KB
   static constexpr uint32_t B_BYTES = BNT * D * 2;       // 16 KB
   static constexpr uint32_t W_BYTES = 128 * BNT * 2;     // 32 KB
@@ -179,18 +198,21 @@ struct GfCfg {
   static constexpr uint32_t STAT_BYTES = BNT * 4;
   static constexpr size_t smem() {
     return 1024 + A_BYTES + ONES_BYTES + STAGES * B_BYTES + 2 * W_BYTES + 2 * R_BYTES + STAGES * 3 * STAT_BYTES +
-           3 * 128 * 4 + 320;
+           3 * 128 * 4 + 256;
   }
 };
 
+// Warp roles: 0 TMA producer, 1 S-MMA issuer, 2 back-MMA issuer (+ TMEM owner), 3 the loss
+// (split-0 CTAs); 4..19 two epilogue GROUPS of 8 warps that ping-pong over the tiles: group
+// g = t & 1 owns S / W / dB buffer g, computes W_t (warpgroup k of the group: tile columns
+// [64k, 64k + 64)) and reads dB_{t-2} back out while the other group keeps the XU busy.
 template <int ENERGY>
 __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                 const __grid_constant__ CUtensorMap tmB,
                                                                 const __grid_constant__ CUtensorMap tmDB,
                                                                 TcGradFArgs p) {
   using C = GfCfg;
-  constexpr int BNT = C::BNT, STAGES = C::STAGES, D = C::D, NWG = C::NWG;
-  constexpr int NEPI = 4 * NWG;                           // epilogue warps
+  constexpr int BNT = C::BNT, STAGES = C::STAGES, D = C::D;
   constexpr bool L2 = ENERGY == CRL_ENERGY_L2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -215,9 +237,7 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
   uint64_t* db_full = w_empty + 2;       // [2]
   uint64_t* db_empty = db_full + 2;      // [2]
   uint64_t* da_full = db_empty + 2;
-  uint64_t* r_full = da_full + 1;        // [half][buf]: the 8 warps of a half staged dB
-  uint64_t* r_free = r_full + 4;         // [half][buf]: the reduction that last read it is done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r_free + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a0 = blockIdx.x * 128;
@@ -229,11 +249,6 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
   // would all TMA-reduce into the same dB tile (and red.add the same column sums) at once
   const int rot = ntiles > 0 ? blockIdx.x % ntiles : 0;
   auto tile_j0 = [&](int t) { const int tt = t + rot; return jbeg + (tt >= ntiles ? tt - ntiles : tt) * BNT; };
-  __shared__ long long s_tr[7][17];
-  __shared__ long long s_trw[16][16];             // W done per epilogue warp (dbg & 32)
-  const bool trace = (p.dbg & 8) && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && blockIdx.y == 0;
-  const int tr_sh = (p.dbg & 16) ? 3 : 0;          // trace every tile, or every 8th (dbg & 16)
-  if (trace && threadIdx.x == 0) s_tr[0][0] = clock64();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -242,12 +257,11 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
     mbar_init(a_full, 1);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], NEPI);
-      mbar_init(&w_full[i], NEPI); mbar_init(&w_empty[i], 1);
-      mbar_init(&db_full[i], 1); mbar_init(&db_empty[i], NEPI);
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
+      mbar_init(&w_full[i], 8); mbar_init(&w_empty[i], 1);
+      mbar_init(&db_full[i], 1); mbar_init(&db_empty[i], 8);
     }
     mbar_init(da_full, 1);
-    for (int i = 0; i < 4; ++i) { mbar_init(&r_full[i], 8); mbar_init(&r_free[i], 1); }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -280,13 +294,13 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
       gf::bulk_g2s(st + 2 * BNT, p.lcf + j0, C::STAT_BYTES, &b_full[s]);
     }
   } else if (warp == 1 && lane == 0) {
-    // ------------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------------ S-MMA issuer
+    // S_{t+2} is issued as soon as group t & 1 has pulled S_t into registers; the back-MMAs
+    // have their own issuing thread, so neither waits behind the other's dependencies
     const uint32_t id_s = idesc_bf16_f32(128, BNT, false, false);
-    const uint32_t id_da = idesc_bf16_f32(128, D, false, true);      // A = W (K-major), B = B tile (MN)
-    const uint32_t id_db = idesc_bf16_f32(128, L2 ? C::NDB : D, true, true);   // A = W^T, B = [A | 1] (MN)
     mbar_wait(a_full, 0);
     const uint32_t a_base = smem_u32(sA);
-    auto issue_s = [&](int t) {
+    for (int t = 0; t < ntiles; ++t) {
       const int s = t % STAGES, b = t & 1;
       mbar_wait(&b_full[s], (t / STAGES) & 1);
       mbar_wait(&s_empty[b], ((t >> 1) & 1) ^ 1);
@@ -297,60 +311,53 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
         mma_bf16(tmem + 128 * b, smem_desc_sw128(a_base + ks * 32, 16, 1024),
                  smem_desc_sw128(b_base + ks * 32, 16, 1024), id_s, ks != 0);
       mma_commit(&s_full[b]);
-      if (trace && (t & ((1 << tr_sh) - 1)) == 0 && (t >> tr_sh) < 16) s_tr[1][(t >> tr_sh) + 1] = clock64();
-    };
-    auto issue_back = [&](int t) {
+    }
+  } else if (warp == 2 && lane == 0) {
+    // ------------------------------------------------------------------ back-MMA issuer
+    const uint32_t id_da = idesc_bf16_f32(128, D, false, true);      // A = W (K-major), B = B tile (MN)
+    const uint32_t id_db = idesc_bf16_f32(128, L2 ? C::NDB : D, true, true);   // A = W^T, B = [A | 1] (MN)
+    mbar_wait(a_full, 0);
+    const uint32_t a_base = smem_u32(sA);
+    for (int t = 0; t < ntiles; ++t) {
       const int s = t % STAGES, b = t & 1;
       mbar_wait(&w_full[b], (t >> 1) & 1);
       mbar_wait(&db_empty[b], ((t >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
-      const uint32_t w_base = smem_u32(sW + b * C::W_BYTES);
-      if (p.dbg & 1) {
-        mma_commit(&db_full[b]); mma_commit(&w_empty[b]); mma_commit(&b_empty[s]);
-        return;
+      if (!(p.dbg & 1)) {
+        const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
+        const uint32_t w_base = smem_u32(sW + b * C::W_BYTES);
+        // dA += W . B_t   (K = the 128 tile columns j: 64-wide chunks of W 16 KB apart)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const int j = 64 * c + 16 * ks;
+            mma_bf16(tm_da, smem_desc_sw128(w_base + c * 16384 + ks * 32, 16, 1024),
+                     smem_desc_sw128(b_base + j * 128, BNT * 128, 1024), id_da, (t | c | ks) != 0);
+          }
+        // [dB_t | cs_t] = W^T . [A | 1]   (K = the 128 tile rows i, 16 per MMA = +2048 B)
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          mma_bf16(tmem + 320 + C::NDB * b, smem_desc_sw128(w_base + ks * 2048, 16384, 1024),
+                   smem_desc_sw128(a_base + ks * 2048, 16384, 1024), id_db, ks != 0);
       }
-      // dA += W . B_t   (K = the 128 tile columns j: 64-wide chunks of W 16 KB apart)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const int j = 64 * c + 16 * ks;
-          mma_bf16(tm_da, smem_desc_sw128(w_base + c * 16384 + ks * 32, 16, 1024),
-                   smem_desc_sw128(b_base + j * 128, BNT * 128, 1024), id_da, (t | c | ks) != 0);
-        }
-      // [dB_t | cs_t] = W^T . [A | 1]   (K = the 128 tile rows i, 16 per MMA = +2048 B)
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-        mma_bf16(tmem + 320 + C::NDB * b, smem_desc_sw128(w_base + ks * 2048, 16384, 1024),
-                 smem_desc_sw128(a_base + ks * 2048, 16384, 1024), id_db, ks != 0);
       mma_commit(&db_full[b]);
       mma_commit(&w_empty[b]);
-      mma_commit(&b_empty[s]);
-      if (trace && (t & ((1 << tr_sh) - 1)) == 0 && (t >> tr_sh) < 16) s_tr[2][(t >> tr_sh) + 1] = clock64();
-    };
-    // S runs two tiles ahead (S_0, S_1 up front; S_{t+2} right after the back-MMAs of tile
-    // t).  The back-MMAs go first: S_{t+2} waits for B_{t+2}, whose stage the back-MMAs of
-    // t-1 free, and issuing it first closed a loop (back MMAs -> TMA -> S -> back MMAs) that
-    // set the per-tile period (measured, clock64 trace: ~3250 clk/tile).
-    for (int t = 0; t < ntiles && t < 2; ++t) issue_s(t);
-    for (int t = 0; t < ntiles; ++t) {
-      issue_back(t);
-      if (t + 2 < ntiles) issue_s(t + 2);
+      mma_commit(&b_empty[s]);              // S_t finished before W_t could start
     }
     mma_commit(da_full);
-  } else if (warp == 2 || warp == 3) {
-    if (p.loss_part != nullptr && split == 0) gradf_loss_rows<ENERGY>(p, a0, threadIdx.x - 64, 64);
+  } else if (warp == 3) {
+    if (p.loss_part != nullptr && split == 0) gradf_loss_rows<ENERGY>(p, a0, lane);
   } else if (warp >= 4) {
-    // ------------------------------------------------------------------ epilogue
-    const int wg = (warp - 4) >> 2;                       // column quarter of the tile
+    // ------------------------------------------------------------------ epilogue groups
+    const int wgid = (warp - 4) >> 2;                     // 0..3
+    const int grp = wgid >> 1;                            // tiles t with t & 1 == grp
+    const int k = wgid & 1;                               // 64-column half of the tile
     const int q = warp & 3;                               // TMEM lane quarter
     const int r = q * 32 + lane;                          // row within the tile
     const int row = a0 + r;
     const bool rv = row < p.Na;
-    const int half = wg >> 1;                             // 64-column half (W) / 32-column half (dB)
-    const int swg = (p.dbg & 64) ? 1 : 0, cwg = (p.dbg & 64) ? 3 : 0;
-    const bool storer = (wg & 1) == swg && q == 0 && lane == 0;   // issues the reductions of its half
+    const bool storer = q == 0 && lane == 0;              // issues the reductions of its half
     const uint32_t lq = (uint32_t)(q * 32) << 16;
     const float astat = rv ? p.a_stat[row] : 0.f;
     const float lr2 = rv ? p.lr[row] * gf::kLog2e : INFINITY;      // rows past the batch: p = 0
@@ -365,158 +372,144 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
     const float lsc = L2 ? gf::kLog2e : 1.f;      // L2: w = g rs' L
     const float EiL = Ei * lsc, ArowL = Arow * lsc, cc0L = cc0 * lsc;
     const uint32_t w_row = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+    const uint32_t bar_id = 2 + wgid;
     f32x2 wsum2 = f2_pack(0.f, 0.f);
 
-    // dB_{u} readout: TMEM -> swizzled SMEM staging -> TMA add-reduction into the accumulator.
-    // No warpgroup barrier: each warp stages its rows and arrives on r_full; the storer of the
-    // half issues the reduction of tile u - 1 at readout u (its r_full has long completed), so
-    // only mbarrier phases couple the warps and the XU work of one warp overlaps the readout of
-    // another.  Staging buffer reuse (every 2 tiles) waits on r_free, which the storer arrives
-    // on once cp.async.bulk.wait_group.read says the previous reduction read it.
-    const uint32_t r_base = smem_u32(sR + half * 16384);
-    auto issue_reduce = [&](int u) {
-      const int bu = u & 1;
-      mbar_wait(&r_full[half * 2 + bu], (u >> 1) & 1);
-      if (!(p.dbg & 4)) {
-        gf::tma_reduce_add_2d(&tmDB, r_base + bu * C::R_BYTES, 32 * half, tile_j0(u));
-        gf::bulk_commit();
-      }
-    };
+    // dB_u readout (u & 1 == grp): TMEM -> swizzled SMEM staging (this warpgroup's 32 d
+    // columns = one 16 KB half) -> TMA add-reduction into the accumulator
     auto readout = [&](int u) {
       const int bu = u & 1;
       const int j0 = tile_j0(u);
       const uint32_t tdb = tmem + 320 + C::NDB * bu + lq;
-      if (storer) {
-        if (u >= 1) issue_reduce(u - 1);
-        gf::bulk_wait_read1();                      // the reduction of tile u - 2 has read buffer bu
-        mbar_arrive(&r_free[half * 2 + bu]);
-      }
       mbar_wait(&db_full[bu], (u >> 1) & 1);
-      if (trace && threadIdx.x == 128 && (u & ((1 << tr_sh) - 1)) == 0 && (u >> tr_sh) < 16) s_tr[6][(u >> tr_sh) + 1] = clock64();
       tc_fence_after();
-      uint32_t v[16], cs = 0u;
-      gf::tmem_ld16_nowait(tdb + 16 * wg, v);      // d columns [16 wg, 16 wg + 16)
-      if (L2 && wg == cwg) gf::tmem_ld1_nowait(tdb + D, cs);   // column 64: sum_i w_ij
+      uint32_t v[32], cs = 0u;
+      tmem_ld32_nowait(tdb + 32 * k, v);           // d columns [32 k, 32 k + 32)
+      if (L2 && k == 0) gf::tmem_ld1_nowait(tdb + D, cs);   // column 64: sum_i w_ij
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&db_empty[bu]);
-      if (L2 && wg == cwg && !(p.dbg & 128) && j0 + r < jend) atomicAdd(p.cs_acc + j0 + r, __uint_as_float(cs));
-      mbar_wait(&r_free[half * 2 + bu], (u >> 1) & 1);
-      const uint32_t dst = r_base + bu * C::R_BYTES + w_row;
+      if (L2 && k == 0 && j0 + r < jend) atomicAdd(p.cs_acc + j0 + r, __uint_as_float(cs));
+      if (storer) gf::bulk_wait_read0();            // the reduction of u - 2 has read the buffer
+      asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+      const uint32_t dst = smem_u32(sR + bu * C::R_BYTES + k * 16384) + w_row;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int g = 4 * (wg & 1) + c;
-        gf::sts128(dst + (uint32_t)((g ^ (r & 7)) << 4), make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
-      }
+      for (int c = 0; c < 8; ++c)
+        gf::sts128(dst + (uint32_t)((c ^ (r & 7)) << 4), make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&r_full[half * 2 + bu]);
-      if (trace && threadIdx.x == 128 && (u & ((1 << tr_sh) - 1)) == 0 && (u >> tr_sh) < 16) s_tr[5][(u >> tr_sh) + 1] = clock64();
+      asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+      if (storer && !(p.dbg & 4)) {
+        gf::tma_reduce_add_2d(&tmDB, smem_u32(sR + bu * C::R_BYTES + k * 16384), 32 * k, j0);
+        gf::bulk_commit();
+      }
     };
 
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = grp; t < ntiles; t += 2) {
       const int s = t % STAGES, b = t & 1;
       const int j0 = tile_j0(t);
       const int nval = jend - j0;
-      const int c0 = 32 * wg;                             // this warpgroup's 32 tile columns
       mbar_wait(&s_full[b], (t >> 1) & 1);
-      if (trace && threadIdx.x == 128 && (t & ((1 << tr_sh) - 1)) == 0 && (t >> tr_sh) < 16) s_tr[3][(t >> tr_sh) + 1] = clock64();
       tc_fence_after();
-      uint32_t raw[32];
-      tmem_ld32_nowait(tmem + 128 * b + lq + c0, raw);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[b]);
       if (t >= 2) mbar_wait(&w_empty[b], ((t >> 1) - 1) & 1);
       const float* bst = sStat + s * 3 * BNT;
-      const uint32_t wt = smem_u32(sW + b * C::W_BYTES + half * 16384) + w_row;
+      const uint32_t wt = smem_u32(sW + b * C::W_BYTES + k * 16384) + w_row;
       // four instantiations (ragged tile x fast factor path): kernel-uniform choices stay out
       // of the per-logit code.  Fast L2 path, all in log2 units (L = log2 e), pairs of logits
       // per FFMA2 / FMUL2 / FADD2:
       //   d2' = L^2 (|a|^2 + eps + |b|^2 - 2 a.b), rs' = rsqrt(|d2'|) = 1 / (L r)
       //   t   = d2' rs' + lse2_i,  p = 2^-t            (= 2^(l2 - lse2_i))
       //   w   = g / r = p (E_i cc_j + A_i) L rs'       (L folded into E_i, A_i)
-      // (|.| and the negation are free MUFU operand modifiers)
+      // (|.| and the negation are free MUFU operand modifiers).  Two 32-column sub-chunks;
+      // the S buffer is handed back after the second TMEM load.
       auto tile = [&](auto masked, auto fast) {
         constexpr bool MASK = decltype(masked)::value;
         constexpr bool FAST = decltype(fast)::value;
-        float w[32];
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          const int c0 = 64 * k + 32 * c;                 // tile column of this sub-chunk
+          uint32_t raw[32];
+          tmem_ld32_nowait(tmem + 128 * b + lq + c0, raw);
+          tmem_ld_wait();
+          if (c == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[b]);
+          }
+          float w[32];
+          if (p.dbg & 2) {
 #pragma unroll
-        for (int i4 = 0; i4 < 8; ++i4) {
-          const float4 b4 = gf::lds128f(smem_u32(bst + c0 + 4 * i4));
-          const float4 f4 = gf::lds128f(smem_u32(bst + (FAST ? 2 : 1) * BNT + c0 + 4 * i4));
-          if (FAST) {
+            for (int i = 0; i < 32; ++i) w[i] = __uint_as_float(raw[i]);
+          } else {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int i = 4 * i4 + 2 * h;
-              const f32x2 v2 = f2_pack(__uint_as_float(raw[i]), __uint_as_float(raw[i + 1]));
-              const f32x2 b2 = h ? f2_pack(b4.z, b4.w) : f2_pack(b4.x, b4.y);
-              const f32x2 f2 = h ? f2_pack(f4.z, f4.w) : f2_pack(f4.x, f4.y);
-              const f32x2 fac = f2_fma(f2_pack(EiL, EiL), f2, f2_pack(ArowL, ArowL));
-              float t0, t1, rs0 = 1.f, rs1 = 1.f;
-              if (L2) {
-                const f32x2 d2 = f2_fma(f2_pack(-2.f * L2e2, -2.f * L2e2), v2,
-                                        f2_fma(f2_pack(L2e2, L2e2), b2, f2_pack(a_l2, a_l2)));
-                float d0, d1;
-                f2_unpack(d2, d0, d1);
-                rs0 = gf::rsq_abs(d0);
-                rs1 = gf::rsq_abs(d1);
-                f2_unpack(f2_fma(d2, f2_pack(rs0, rs1), f2_pack(lr2, lr2)), t0, t1);
-              } else {
-                f2_unpack(f2_fma(v2, f2_pack(-gf::kLog2e, -gf::kLog2e), f2_pack(lr2, lr2)), t0, t1);
-              }
-              if (MASK) {
-                t0 = c0 + i < nval ? t0 : INFINITY;
-                t1 = c0 + i + 1 < nval ? t1 : INFINITY;
-              }
-              f32x2 wv = f2_mul(f2_pack(gf::ex2_neg(t0), gf::ex2_neg(t1)), fac);
-              if (L2) {
-                wv = f2_mul(wv, f2_pack(rs0, rs1));
-                wsum2 = f2_add(wsum2, wv);
-              }
-              f2_unpack(wv, w[i], w[i + 1]);
-            }
-          } else {                                        // exact: q = 2^(l2 - lse2'_j)
-            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
-            const float ff[4] = {f4.x, f4.y, f4.z, f4.w};
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 b4 = gf::lds128f(smem_u32(bst + c0 + 4 * i4));
+            const float4 f4 = gf::lds128f(smem_u32(bst + (FAST ? 2 : 1) * BNT + c0 + 4 * i4));
+            if (FAST) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int i = 4 * i4 + u;
-              const float v = __uint_as_float(raw[i]);
-              float rs = 1.f, l2v;
-              if (L2) {
-                const float d2 = fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2));
-                rs = gf::rsq_abs(d2);
-                l2v = -fabsf(d2) * rs;
-              } else {
-                l2v = v * gf::kLog2e;
+              for (int h = 0; h < 2; ++h) {
+                const int i = 4 * i4 + 2 * h;
+                const f32x2 v2 = f2_pack(__uint_as_float(raw[i]), __uint_as_float(raw[i + 1]));
+                const f32x2 b2 = h ? f2_pack(b4.z, b4.w) : f2_pack(b4.x, b4.y);
+                const f32x2 f2 = h ? f2_pack(f4.z, f4.w) : f2_pack(f4.x, f4.y);
+                const f32x2 fac = f2_fma(f2_pack(EiL, EiL), f2, f2_pack(ArowL, ArowL));
+                float t0, t1, rs0 = 1.f, rs1 = 1.f;
+                if (L2) {
+                  const f32x2 d2 = f2_fma(f2_pack(-2.f * L2e2, -2.f * L2e2), v2,
+                                          f2_fma(f2_pack(L2e2, L2e2), b2, f2_pack(a_l2, a_l2)));
+                  float d0, d1;
+                  f2_unpack(d2, d0, d1);
+                  rs0 = gf::rsq_abs(d0);
+                  rs1 = gf::rsq_abs(d1);
+                  f2_unpack(f2_fma(d2, f2_pack(rs0, rs1), f2_pack(lr2, lr2)), t0, t1);
+                } else {
+                  f2_unpack(f2_fma(v2, f2_pack(-gf::kLog2e, -gf::kLog2e), f2_pack(lr2, lr2)), t0, t1);
+                }
+                if (MASK) {
+                  t0 = c0 + i < nval ? t0 : INFINITY;
+                  t1 = c0 + i + 1 < nval ? t1 : INFINITY;
+                }
+                f32x2 wv = f2_mul(f2_pack(gf::ex2_neg(t0), gf::ex2_neg(t1)), fac);
+                if (L2) {
+                  wv = f2_mul(wv, f2_pack(rs0, rs1));
+                  wsum2 = f2_add(wsum2, wv);
+                }
+                f2_unpack(wv, w[i], w[i + 1]);
               }
-              if (MASK) l2v = c0 + i < nval ? l2v : -INFINITY;
-              const float qe = gf::ex2(l2v - ff[u] * gf::kLog2e);
-              float wv = fmaf(gf::ex2(l2v - lr2), ArowL, qe * cc0L) * rmask;
-              if (L2) { wv *= rs; wsum2 = f2_add(wsum2, f2_pack(wv, 0.f)); }
-              w[i] = wv;
+            } else {                                      // exact: q = 2^(l2 - lse2'_j)
+              const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+              const float ff[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int i = 4 * i4 + u;
+                const float v = __uint_as_float(raw[i]);
+                float rs = 1.f, l2v;
+                if (L2) {
+                  const float d2 = fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2));
+                  rs = gf::rsq_abs(d2);
+                  l2v = -fabsf(d2) * rs;
+                } else {
+                  l2v = v * gf::kLog2e;
+                }
+                if (MASK) l2v = c0 + i < nval ? l2v : -INFINITY;
+                const float qe = gf::ex2(l2v - ff[u] * gf::kLog2e);
+                float wv = fmaf(gf::ex2(l2v - lr2), ArowL, qe * cc0L) * rmask;
+                if (L2) { wv *= rs; wsum2 = f2_add(wsum2, f2_pack(wv, 0.f)); }
+                w[i] = wv;
+              }
             }
           }
-        }
+          }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = 32 * (wg & 1) + 8 * u;             // column within this 64-wide half
-          gf::sts128(wt + (uint32_t)((((k >> 3) ^ (r & 7))) << 4),
-                     make_uint4(pack_bf16x2(w[8 * u], w[8 * u + 1]), pack_bf16x2(w[8 * u + 2], w[8 * u + 3]),
-                                pack_bf16x2(w[8 * u + 4], w[8 * u + 5]), pack_bf16x2(w[8 * u + 6], w[8 * u + 7])));
+          for (int u = 0; u < 4; ++u) {
+            const int kk = 32 * c + 8 * u;                 // column within this 64-wide half
+            gf::sts128(wt + (uint32_t)((((kk >> 3) ^ (r & 7))) << 4),
+                       make_uint4(pack_bf16x2(w[8 * u], w[8 * u + 1]), pack_bf16x2(w[8 * u + 2], w[8 * u + 3]),
+                                  pack_bf16x2(w[8 * u + 4], w[8 * u + 5]), pack_bf16x2(w[8 * u + 6], w[8 * u + 7])));
+          }
         }
       };
-      if (p.dbg & 2) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = 32 * (wg & 1) + 8 * u;
-          gf::sts128(wt + (uint32_t)((((k >> 3) ^ (r & 7))) << 4),
-                     make_uint4(raw[8 * u], raw[8 * u + 2], raw[8 * u + 4], raw[8 * u + 6]));
-        }
-      } else if (fac_fast) {
+      if (fac_fast) {
         if (nval >= BNT) tile(std::false_type{}, std::true_type{});
         else tile(std::true_type{}, std::true_type{});
       } else {
@@ -526,30 +519,29 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&w_full[b]);
-      if (trace && (p.dbg & 32) && lane == 0 && t < 16) s_trw[warp - 4][t] = clock64();
-      if (trace && threadIdx.x == 128 && (t & ((1 << tr_sh) - 1)) == 0 && (t >> tr_sh) < 16) s_tr[4][(t >> tr_sh) + 1] = clock64();
-      if (t > 0) readout(t - 1);
+      if (t >= 2) readout(t - 2);
     }
-    if (ntiles > 0) readout(ntiles - 1);
-    if (storer && ntiles > 0) issue_reduce(ntiles - 1);
+    // the last tile of this group
+    const int tl = ntiles - 1 - ((ntiles - 1 - grp) & 1);
+    if (tl >= 0) readout(tl);
     // row side: partial row sums of w (L2) and the split's dA
     float ws0, ws1;
     f2_unpack(wsum2, ws0, ws1);
     const float wsum = ws0 + ws1;
-    if (wg > 0) sMerge[(wg - 1) * 128 + r] = wsum;
-    asm volatile("bar.sync 1, %0;" ::"n"(128 * NWG) : "memory");
-    if (wg == 0 && rv && L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[r] + sMerge[128 + r] + sMerge[256 + r];
+    if (wgid > 0) sMerge[(wgid - 1) * 128 + r] = wsum;
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    if (wgid == 0 && rv && L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[r] + sMerge[128 + r] + sMerge[256 + r];
     mbar_wait(da_full, 0);
     tc_fence_after();
     {
       float v[16];
-      tmem_ld16(tm_da + lq + 16 * wg, v);
+      tmem_ld16(tm_da + lq + 16 * wgid, v);
       if (ntiles == 0) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = 0.f;
       }
       if (rv) {
-        float* out = p.part_da + ((size_t)split * p.Na + row) * D + 16 * wg;
+        float* out = p.part_da + ((size_t)split * p.Na + row) * D + 16 * wgid;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           reinterpret_cast<float4*>(out)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -563,12 +555,6 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-  if (trace && (p.dbg & 32) && threadIdx.x == 0)
-    for (int t = 0; t < 16 && t < ntiles; ++t)
-      for (int w = 0; w < 16; ++w) printf("GF_TRW %d %d %d %lld\n", blockIdx.x, t, w, s_trw[w][t] - s_tr[0][0]);
-  if (trace && threadIdx.x == 0)
-    for (int k = 1; k < 7; ++k)
-      for (int t = 1; t < 17; ++t) printf("GF_TRACE %d %d %d %lld\n", blockIdx.x, k, t - 1, s_tr[k][t] - s_tr[0][0]);
 }
 
 // ------------------------------------------------------------------------------- host side
