@@ -451,7 +451,7 @@ crl_status crl_relabel_sample(crl_ctx* ctx, uint64_t seed, uint64_t step, float*
   Stage sg(ctx, (cudaStream_t)stream, "relabel");
   CU(launch_relabel_sample(k.batch_local, k.rank, k.n_envs_local, k.capacity, k.obs_dim, k.act_dim,
                            k.goal_dim, k.goal_offset, ctx->obs_stride, ctx->act_stride,
-                           (uint32_t)tau_old, (uint32_t)tau_new, seed, step, ctx->obs_ring,
+                           (uint32_t)tau_old, (uint32_t)tau_new, seed, step, k.gamma, ctx->obs_ring,
                            ctx->act_ring, ctx->ep_end, ctx->qtab, s, a, g, idx, ctx->status,
                            (cudaStream_t)stream));
   ctx->launches = 1;

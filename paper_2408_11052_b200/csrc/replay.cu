@@ -12,6 +12,8 @@
 //   open_start [E_l] u32   absolute index where the currently open episode began
 //   qtab     [T+1] u64     Q[k] = floor((1 - gamma^k) 2^64), built on the host
 // Device index arithmetic is integer-only, so sampled indices are bit-exact.
+#include <cmath>
+
 #include "common.cuh"
 
 namespace crl {
@@ -81,35 +83,36 @@ __global__ void __launch_bounds__(256) buffer_insert_kernel(
 // ---------------------------------------------------------------------------------------
 // A1: one warp per row.  Lane a evaluates attempt a (and a+32) of the rejection loop in
 // parallel; the first accepted attempt (lowest a) wins via ballot, which reproduces the
-// sequential "first valid attempt" of the contract.  The offset k is an inverse-CDF lookup
-// in the u64 table Q (binary search in shared memory).  Rows are then gathered by the
-// whole warp (vectorised when the row stride allows).
+// sequential "first valid attempt" of the contract.  The offset k is the inverse-CDF lookup
+// k = min{k in [1, L] : Q[k] > t} in the u64 table Q (L2-resident): an fp64 estimate
+// k~ = ceil(log(1 - t 2^-64) / log gamma) places a 32-entry window Q[k~-16 .. k~+15], one
+// coalesced load, and a ballot over "Q[k] > t" takes the first index.  The decision is the
+// exact integer comparison; the window is accepted only if it brackets the answer
+// (Q[first - 1] <= t), else a binary search over Q in global memory decides (a fallback for
+// estimates off by more than 16, which the fp64 estimate does not produce for T <= 2^20).
+// Rows are then gathered by the whole warp.
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
 
 __global__ void __launch_bounds__(256) relabel_sample_kernel(
     int B_l, int rank, int E, int T, int obs_dim, int act_dim, int goal_dim, int goal_offset,
     int obs_stride, int act_stride, uint32_t tau_old, uint32_t tau_new,
-    uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo, uint32_t step_hi,
+    uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo, uint32_t step_hi, double log_gamma,
     const float* __restrict__ obs_ring, const float* __restrict__ act_ring,
     const uint32_t* __restrict__ ep_end, const uint64_t* __restrict__ qtab,
     float* __restrict__ s_out, float* __restrict__ a_out, float* __restrict__ g_out,
     int64_t* __restrict__ idx_out, int* __restrict__ status) {
-  extern __shared__ uint64_t q_sm[];
-  // stage Q[0..T] in shared memory; the loads are in flight while the attempts below run
-  // (they only need ep_end), the barrier comes just before the first Q lookup
-  for (int k = threadIdx.x; k <= T; k += blockDim.x) q_sm[k] = qtab[k];
-
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int r = blockIdx.x * (blockDim.x >> 5) + warp;
-  const bool active = r < B_l;                 // no early return: every thread reaches the barrier
+  const bool active = r < B_l;
+  if (!active) return;                         // warp-uniform
   const uint32_t rho = (uint32_t)rank * (uint32_t)B_l + (uint32_t)r;
   const uint32_t n = tau_new - tau_old + 1;
 
   int found = -1;
   uint32_t e = 0, tau = 0, L = 0, x2 = 0, x3 = 0;
-  for (int base = 0; active && base < 64 && found < 0; base += 32) {
+  for (int base = 0; base < 64 && found < 0; base += 32) {
     const uint32_t att = (uint32_t)(base + lane);
     U4 x = philox4x32_10(U4{rho, att, step_lo, step_hi}, seed_lo, seed_hi);
     uint32_t ee = (uint32_t)(((uint64_t)x.x * (uint64_t)E) >> 32);
@@ -130,21 +133,31 @@ __global__ void __launch_bounds__(256) relabel_sample_kernel(
     }
   }
   if (found < 0) {
-    if (active && lane == 0) set_status(status, CRL_ESAMPLER);
+    if (lane == 0) set_status(status, CRL_ESAMPLER);
     // deterministic fill so downstream stays finite
     e = 0; tau = tau_old; L = 1; x2 = 0; x3 = 0;
   }
-  __syncthreads();                             // Q staged
-  if (!active) return;
-  // k = min{k in [1, L] : Q[k] > t},  t = (R * Q[L]) >> 64
+  // k = min{k in [1, L] : Q[k] > t},  t = (R * Q[L]) >> 64   (Q[0] = 0 <= t < Q[L])
   const uint64_t R = ((uint64_t)x2 << 32) | (uint64_t)x3;
-  const uint64_t tt = mulhi64(R, q_sm[L]);
-  uint32_t lo = 1, hi = L;                     // invariant: answer in [lo, hi], Q[hi] > tt
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (q_sm[mid] > tt) hi = mid; else lo = mid + 1;
+  const uint64_t tt = mulhi64(R, __ldg(qtab + L));
+  const double u = (double)tt * 5.421010862427522e-20;          // t 2^-64
+  const double kf = ceil(log1p(-u) / log_gamma);
+  const uint32_t kest = kf >= 1.0 ? (kf <= (double)L ? (uint32_t)kf : L) : 1u;
+  const uint32_t base = kest > 16u ? kest - 16u : 1u;           // window Q[base-1 .. base+30]
+  const uint32_t kw = base - 1u + (uint32_t)lane;
+  const bool above = kw > L || __ldg(qtab + kw) > tt;
+  const unsigned bal = __ballot_sync(0xffffffffu, above);
+  uint32_t k;
+  if (bal != 0u && (bal & 1u) == 0u) {
+    k = base - 1u + (uint32_t)(__ffs(bal) - 1);
+  } else {
+    uint32_t lo = 1, hi = L;                   // invariant: answer in [lo, hi], Q[hi] > tt
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(qtab + mid) > tt) hi = mid; else lo = mid + 1;
+    }
+    k = lo;
   }
-  const uint32_t k = lo;
   const uint32_t slot = tau % (uint32_t)T;
   const uint32_t gslot = (tau + k) % (uint32_t)T;
   const float* srow = obs_ring + ((size_t)e * T + slot) * obs_stride;
@@ -176,21 +189,15 @@ cudaError_t launch_buffer_insert(const float* obs, const float* act, const uint8
 
 cudaError_t launch_relabel_sample(int B_l, int rank, int E, int T, int obs_dim, int act_dim,
                                   int goal_dim, int goal_offset, int obs_stride, int act_stride,
-                                  uint32_t tau_old, uint32_t tau_new, uint64_t seed, uint64_t step,
+                                  uint32_t tau_old, uint32_t tau_new, uint64_t seed, uint64_t step, double gamma,
                                   const float* obs_ring, const float* act_ring,
                                   const uint32_t* ep_end, const uint64_t* qtab, float* s, float* a,
                                   float* g, int64_t* idx, int* status, cudaStream_t st) {
   const int warps = 8;
   dim3 grid((B_l + warps - 1) / warps);
-  size_t smem = sizeof(uint64_t) * (size_t)(T + 1);
-  if (smem > 48 * 1024) {
-    cudaError_t err = cudaFuncSetAttribute(relabel_sample_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-  }
-  relabel_sample_kernel<<<grid, warps * 32, smem, st>>>(
+  relabel_sample_kernel<<<grid, warps * 32, 0, st>>>(
       B_l, rank, E, T, obs_dim, act_dim, goal_dim, goal_offset, obs_stride, act_stride, tau_old,
-      tau_new, (uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)step, (uint32_t)(step >> 32),
+      tau_new, (uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)step, (uint32_t)(step >> 32), std::log(gamma),
       obs_ring, act_ring, ep_end, qtab, s, a, g, idx, status);
   return cudaGetLastError();
 }

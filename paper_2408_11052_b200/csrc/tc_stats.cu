@@ -73,6 +73,23 @@ __device__ __forceinline__ void ex2_pair_fma(float x0, float x1, float& y0, floa
   y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(j0) << 23));   // low bits of j hold n
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(j1) << 23));
 }
+// sqrt(|x|) for a PAIR on the FMA pipe: y ~ 1/sqrt from the exponent-halving integer guess
+// (one IMAD.HI each: magic + floor(-bits / 2)), two Newton steps y <- y (3/2 - (x/2 y) y) in
+// packed FFMA2 / FMUL2 (relative error ~5e-6; x = 0 gives 0), then sqrt = x y
+__device__ __forceinline__ void sqrt_pair_fma(float x0, float x1, float& r0, float& r1) {
+  x0 = fabsf(x0);
+  x1 = fabsf(x1);
+  int i0, i1;
+  asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(i0) : "r"(__float_as_int(x0)), "r"((int)0x80000000), "r"(0x5f375a86));
+  asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(i1) : "r"(__float_as_int(x1)), "r"((int)0x80000000), "r"(0x5f375a86));
+  const f32x2 x = f2_pack(x0, x1);
+  const f32x2 nhx = f2_mul(x, f2_pack(-0.5f, -0.5f));
+  f32x2 y = f2_pack(__int_as_float(i0), __int_as_float(i1));
+  const f32x2 c15 = f2_pack(1.5f, 1.5f);
+#pragma unroll
+  for (int it = 0; it < 2; ++it) y = f2_mul(y, f2_fma(f2_mul(nhx, y), y, c15));
+  f2_unpack(f2_mul(x, y), r0, r1);
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -110,6 +127,13 @@ constexpr int kStNWG = 4;          // epilogue warpgroups
 // of every 4 logit pairs, this many exp2 pairs skip the MUFU (measured on B200 at N = 16384:
 // 1 of 4 is neutral, 186 -> 185 us: the tile loop is latency- not XU-throughput-bound)
 constexpr int kStEmuPairs = CRL_ST_EMU;
+#ifndef CRL_ST_SQRT_EMU
+#define CRL_ST_SQRT_EMU 0
+#endif
+// of every 4 logit pairs, this many take sqrt on the FMA pipe (Newton) instead of the MUFU
+// (measured on B200 at N = 16384: 0 -> 194 us, 1 -> 199, 2 -> 200, 4 -> 251: the kernel is
+// issue / latency- rather than XU-bound, so moving work to the FMA pipe does not pay)
+constexpr int kStSqrtPairs = CRL_ST_SQRT_EMU;
 
 template <int D>
 struct StCfg {
@@ -356,7 +380,12 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
                 float x0, x1;
                 if (ENERGY == CRL_ENERGY_L2) {
                   f2_unpack(f2_fma(kM2, v2, f2_fma(kL2, b2, kA2)), x0, x1);
-                  if (((2 * i4 + h) & 3) < kStEmuPairs) {       // exp2 of this pair on FMA / ALU
+                  if (((2 * i4 + h) & 3) < kStSqrtPairs) {      // sqrt of this pair on the FMA pipe
+                    float r0, r1;
+                    fs::sqrt_pair_fma(x0, x1, r0, r1);
+                    e[i] = ex2_neg(r0);
+                    e[i + 1] = ex2_neg(r1);
+                  } else if (((2 * i4 + h) & 3) < kStEmuPairs) {       // exp2 of this pair on FMA / ALU
                     fs::ex2_pair_fma(-sqrt_abs(x0), -sqrt_abs(x1), e[i], e[i + 1]);
                   } else {
                     e[i] = ex2_neg(sqrt_abs(x0));
