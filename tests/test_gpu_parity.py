@@ -61,6 +61,25 @@ def test_relabel_bit_exact(name, n_chunks, U, B):
     assert ctx.status() == 0
 
 
+@pytest.mark.parametrize("gamma", [0.0, 0.5, 0.9, 0.999, 0.99999])
+def test_relabel_bit_exact_gamma(gamma):
+    """The offset lookup (fp64 window estimate + exact integer decision, binary-search
+    fallback) across discounts: gamma = 0 (k = 1 always), short and long geometric tails."""
+    cfg = crl_synth.preset("reacher", precision="fp32", batch=256)
+    cfg["gamma"] = gamma
+    ctx, _ = make_ctx(cfg)
+    chunks = fill_buffer(ctx, cfg, 20, U=62)
+    bufs = oracle_buffers(cfg, chunks)
+    for step in (0, 7):
+        s, a, g, idx = _sample_gpu(ctx, cfg, step)
+        os_, oa, og, oidx = oreplay.relabel_sample(bufs[0], SEED, step, 256, gamma=gamma,
+                                                   goal_offset=cfg["goal_offset"],
+                                                   goal_dim=cfg["goal_dim"])
+        assert np.array_equal(idx, oidx)
+        assert np.array_equal(g.view(np.uint32), og.view(np.uint32))
+    assert ctx.status() == 0
+
+
 def test_relabel_full_size_ant_sampled_rows():
     """configs[1] at full size (1024 envs x 1000, wrapped ring): the oracle recomputes a
     sample of rows one by one."""
