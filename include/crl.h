@@ -176,6 +176,21 @@ CRL_API crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* g, 
                           float alpha_ent, float* loss_out, float* actor_grads_out,
                           int apply_adam, void* stream);
 
+/* Entropy coefficient update ("a tuneable entropy coefficient"; the paper gives no
+ * rule, reading A-32 takes SAC's automatic tuning):
+ *   L_alpha = alpha * (-mean_i log pi_i - target_entropy),  alpha = exp(*log_alpha),
+ * one Adam step on log_alpha (context adam_b1/b2/eps, no weight decay, own step counter)
+ * with gradient dL_alpha/dlog_alpha = L_alpha; mean log pi is the global mean from the last
+ * crl_actor_loss on this context (CRL_ESTATE if there was none).
+ *   log_alpha: device float[1], read and updated in place.  alpha_out: device float[1] or
+ *   NULL (exp of the new log_alpha).  loss_out: device float[1] or NULL (L_alpha).
+ * A non-finite L_alpha leaves log_alpha unchanged and sets CRL_ENONFINITE in the status word.
+ * Launched on `stream` after the actor loss (stream order carries the dependency).
+ * CRL_EUNSUPPORTED without an actor; CRL_EINVAL for NULL log_alpha, lr <= 0 or a
+ * non-finite target. */
+CRL_API crl_status crl_entropy_update(crl_ctx* ctx, float target_entropy, float lr, float* log_alpha,
+                                      float* alpha_out, float* loss_out, void* stream);
+
 /* Device status word: CRL_OK or the first device-detected fault since the last reset.
  * sync != 0 synchronises the device first; reset clears it. */
 CRL_API crl_status crl_get_status(crl_ctx* ctx, int sync, int reset);

@@ -15,6 +15,11 @@ Actor (Eq. 3, §5.1 P:313 "tuneable entropy coefficient", App. C alpha
   L_actor = (1/N) sum_i (alpha_ent log pi_i - f(phi([s_i || a'_i]), psi(g_i)))
   differentiated w.r.t. the actor parameters only (critic frozen).
 
+Entropy coefficient ("a tuneable entropy coefficient"; the paper gives no rule,
+reading A-32 takes SAC's automatic tuning):
+  L_alpha = alpha (-mean_i log pi_i - H_target),  alpha = exp(log_alpha),
+  one Adam step (oracle/adam.py, no weight decay) on log_alpha with gradient L_alpha.
+
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 """
 import numpy as np
@@ -126,3 +131,15 @@ def actor_loss(actor_params, critic_params, s, g, eps_noise, *, alpha_ent, obs_d
     g_pi, _ = mlp.backward(pi_layers, cache_pi, np.concatenate([dmu, dlog_sig_raw], axis=1),
                            activation)
     return dict(loss=loss, grads=mlp.pack(g_pi), a_new=a_new, log_pi=log_pi, f_diag=f)
+
+
+def entropy_update(log_pi, log_alpha, m, v, t, *, target_entropy, lr, b1=0.9, b2=0.999, eps=1e-8):
+    """One step of the entropy-coefficient tuning (reading A-32).  log_pi: the GLOBAL batch's
+    log pi (mean taken here).  Returns dict(log_alpha, alpha, loss, m, v, t)."""
+    alpha = np.exp(np.float64(log_alpha))
+    loss = alpha * (-np.mean(np.asarray(log_pi, np.float64)) - target_entropy)
+    # d/dlog_alpha [exp(log_alpha) c] = exp(log_alpha) c = loss
+    p, m, v, t = adam.adam_step(np.array([log_alpha], np.float64), np.array([loss]), np.array([m]),
+                                np.array([v]), t, lr=lr, b1=b1, b2=b2, eps=eps, wd=0.0)
+    return dict(log_alpha=float(p[0]), alpha=float(np.exp(p[0])), loss=float(loss), m=float(m[0]),
+                v=float(v[0]), t=t)

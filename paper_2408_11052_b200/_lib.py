@@ -24,7 +24,7 @@ PRECISION = {"fp32": 0, "bf16": 1}
 
 EXPORTED = ["crl_abi_version", "crl_workspace_size", "crl_create", "crl_destroy",
             "crl_nccl_unique_id", "crl_buffer_insert", "crl_relabel_sample", "crl_critic_step",
-            "crl_actor_loss", "crl_get_status", "crl_last_error", "crl_debug_tensor",
+            "crl_actor_loss", "crl_entropy_update", "crl_get_status", "crl_last_error", "crl_debug_tensor",
             "crl_last_launch_count", "crl_profile_enable", "crl_profile_read"]
 
 
@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH):
         "crl_relabel_sample": (i, [vp, u64, u64, vp, vp, vp, vp, vp]),
         "crl_critic_step": (i, [vp, vp, vp, vp, vp, vp, vp]),
         "crl_actor_loss": (i, [vp, vp, vp, vp, f, vp, vp, i, vp]),
+        "crl_entropy_update": (i, [vp, f, f, vp, vp, vp, vp]),
         "crl_get_status": (i, [vp, i, i]),
         "crl_last_error": (ctypes.c_char_p, [vp]),
         "crl_debug_tensor": (i, [vp, ctypes.c_char_p, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]),
@@ -247,6 +248,15 @@ class CrlContext:
         _check(self.lib.crl_actor_loss(self._h, _ptr(s), _ptr(g), _ptr(eps), float(alpha_ent),
                                        _ptr(loss_out), _ptr(actor_grads_out), int(apply_adam),
                                        _stream(stream)), self._h)
+
+    def entropy_update(self, log_alpha, target_entropy=None, lr=3e-4, alpha_out=None, loss_out=None,
+                       stream=None):
+        """One Adam step on the entropy coefficient (crl_entropy_update); log_alpha is a device
+        float[1] updated in place.  Default target entropy -act_dim / 2 (reading A-32)."""
+        if target_entropy is None:
+            target_entropy = -0.5 * self.cfg.act_dim
+        _check(self.lib.crl_entropy_update(self._h, float(target_entropy), float(lr), _ptr(log_alpha),
+                                           _ptr(alpha_out), _ptr(loss_out), _stream(stream)), self._h)
 
     # ------------------------------------------------------------------ utilities
     def status(self, sync=True, reset=False) -> int:

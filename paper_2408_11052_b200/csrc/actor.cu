@@ -96,21 +96,25 @@ __global__ void actor_diag_kernel(int Bl, int D, int energy, float invN, float a
   if (lane == 0) rowloss[row] = alpha * logpi[row] - f;
 }
 
-// one CTA: deterministic sum of the per-row losses into a_loss[0]
+// one CTA: deterministic sums of the per-row losses and log pi into a_loss[0..1]
 __global__ void __launch_bounds__(1024) actor_loss_sum_kernel(int Bl, const float* __restrict__ rowloss,
+                                                              const float* __restrict__ logpi,
                                                               float* __restrict__ acc) {
   pdl_wait();
   pdl_launch();
-  __shared__ float red[32];
-  float s = 0.f;
-  for (int i = threadIdx.x; i < Bl; i += blockDim.x) s += rowloss[i];
+  __shared__ float red[2][32];
+  float s = 0.f, lp = 0.f;
+  for (int i = threadIdx.x; i < Bl; i += blockDim.x) { s += rowloss[i]; lp += logpi[i]; }
   s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  lp = warp_sum(lp);
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = s; red[1][threadIdx.x >> 5] = lp; }
   __syncthreads();
   if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[0][threadIdx.x] : 0.f;
+    float w = threadIdx.x < (blockDim.x >> 5) ? red[1][threadIdx.x] : 0.f;
     v = warp_sum(v);
-    if (threadIdx.x == 0) acc[0] = v;
+    w = warp_sum(w);
+    if (threadIdx.x == 0) { acc[0] = v; acc[1] = w; }
   }
 }
 
@@ -121,7 +125,8 @@ __global__ void actor_loss_finalize_kernel(float* __restrict__ acc, float invN, 
   pdl_wait();
   pdl_launch();
   const float L = acc[0] * invN;
-  acc[1] = L;
+  acc[2] = L;
+  acc[3] = acc[1] * invN;                          // mean log pi (global): the entropy update's input
   if (loss_out) loss_out[0] = L;
   const bool bad = !isfinite(L);
   if (bad) set_status(status, CRL_ENONFINITE);
@@ -203,9 +208,10 @@ extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* 
                 alpha_ent, (const float*)ctx->ac_phi, (const float*)ctx->ac_psi, (const float*)ctx->a_logpi,
                 ctx->ac_dphi, ctx->a_rowloss));
   ++nl;
-  CU(launch_pdl(actor_loss_sum_kernel, dim3(1), dim3(1024), 0, st, Bl, (const float*)ctx->a_rowloss, ctx->a_loss));
+  CU(launch_pdl(actor_loss_sum_kernel, dim3(1), dim3(1024), 0, st, Bl, (const float*)ctx->a_rowloss,
+                (const float*)ctx->a_logpi, ctx->a_loss));
   ++nl;
-  if (W > 1) NC(ncclAllReduce(ctx->a_loss, ctx->a_loss, 1, ncclFloat32, ncclSum, ctx->comm, st));
+  if (W > 1) NC(ncclAllReduce(ctx->a_loss, ctx->a_loss, 2, ncclFloat32, ncclSum, ctx->comm, st));
   CU(launch_pdl(actor_loss_finalize_kernel, dim3(1), dim3(1), 0, st, ctx->a_loss, invN, loss_out, ctx->a_skip,
                 ctx->a_t, apply_adam, ctx->status));
   ++nl;
@@ -263,5 +269,57 @@ extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* 
     ++nl;
   }
   ctx->launches = nl;
+  ctx->actor_loss_done = true;
+  return CRL_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Entropy coefficient ("a tuneable entropy coefficient"; reading A-32): SAC-style
+// automatic tuning of alpha = exp(log_alpha) towards a target entropy H,
+//   L_alpha = alpha (-E[log pi] - H),   dL_alpha / d log_alpha = alpha (-E[log pi] - H)
+// (E[log pi] held constant: it is the mean of the last crl_actor_loss), one Adam step on
+// log_alpha with the context's b1 / b2 / eps and no weight decay.
+// ---------------------------------------------------------------------------------------
+__global__ void entropy_update_kernel(const float* __restrict__ acc, float target, float lr, float b1, float b2,
+                                      float eps, float* __restrict__ log_alpha, float* __restrict__ mv,
+                                      int* __restrict__ t, float* __restrict__ alpha_out,
+                                      float* __restrict__ loss_out, int* __restrict__ status) {
+  const float mean_logpi = acc[3];
+  const float la = *log_alpha;
+  const float alpha = expf(la);
+  const float gl = alpha * (-mean_logpi - target);
+  if (loss_out) loss_out[0] = gl;
+  if (!isfinite(gl)) {
+    set_status(status, CRL_ENONFINITE);
+    if (alpha_out) alpha_out[0] = alpha;
+    return;
+  }
+  const int tn = *t + 1;
+  const float m = b1 * mv[0] + (1.f - b1) * gl;
+  const float v = b2 * mv[1] + (1.f - b2) * gl * gl;
+  const float mhat = m / (1.f - powf(b1, (float)tn));
+  const float vhat = v / (1.f - powf(b2, (float)tn));
+  const float la_new = la - lr * (mhat / (sqrtf(vhat) + eps));
+  mv[0] = m;
+  mv[1] = v;
+  *t = tn;
+  *log_alpha = la_new;
+  if (alpha_out) alpha_out[0] = expf(la_new);
+}
+
+extern "C" crl_status crl_entropy_update(crl_ctx* ctx, float target_entropy, float lr, float* log_alpha,
+                                         float* alpha_out, float* loss_out, void* stream) {
+  if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
+  if (!ctx->has_actor) return fail(ctx, CRL_EUNSUPPORTED, "context created without an actor (actor_depth = 0)");
+  if (!log_alpha) return fail(ctx, CRL_EINVAL, "entropy_update: NULL log_alpha");
+  if (!(lr > 0.f) || !std::isfinite(lr) || !std::isfinite(target_entropy))
+    return fail(ctx, CRL_EINVAL, "entropy_update: lr must be > 0 and the target finite");
+  if (!ctx->actor_loss_done) return fail(ctx, CRL_ESTATE, "entropy_update needs a prior crl_actor_loss");
+  const crl_config& k = ctx->cfg;
+  cudaStream_t st = (cudaStream_t)stream;
+  entropy_update_kernel<<<1, 1, 0, st>>>(ctx->a_loss, target_entropy, lr, k.adam_b1, k.adam_b2, k.adam_eps,
+                                         log_alpha, ctx->ent_mv, ctx->ent_t, alpha_out, loss_out, ctx->status);
+  CU(cudaGetLastError());
+  ctx->launches = 1;
   return CRL_OK;
 }

@@ -226,6 +226,8 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     c->a_loss = s.take<float>(4);
     c->a_t = s.take<int>(1);
     c->a_skip = s.take<int>(1);
+    c->ent_mv = s.take<float>(2);
+    c->ent_t = s.take<int>(1);
   }
   *scr_bytes = (s.off + 255) & ~(size_t)255;
 }
@@ -353,7 +355,8 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaMemset(ctx->open_start, 0, (size_t)cfg->n_envs_local * 4) != cudaSuccess ||
       cudaMemset(ctx->status, 0, 4) != cudaSuccess || cudaMemset(ctx->adam_t, 0, 4) != cudaSuccess ||
       cudaMemset(ctx->skip, 0, 4) != cudaSuccess || cudaMemset(ctx->loss_ticket, 0, 4) != cudaSuccess ||
-      (ctx->has_actor && (cudaMemset(ctx->a_t, 0, 4) != cudaSuccess || cudaMemset(ctx->a_skip, 0, 4) != cudaSuccess)) ||
+      (ctx->has_actor && (cudaMemset(ctx->a_t, 0, 4) != cudaSuccess || cudaMemset(ctx->a_skip, 0, 4) != cudaSuccess ||
+                          cudaMemset(ctx->ent_mv, 0, 8) != cudaSuccess || cudaMemset(ctx->ent_t, 0, 4) != cudaSuccess)) ||
       cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->cap_stream3, cudaStreamNonBlocking) != cudaSuccess ||

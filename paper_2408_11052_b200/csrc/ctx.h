@@ -196,8 +196,11 @@ struct crl_ctx {
   float *ac_phi = nullptr, *ac_psi = nullptr, *ac_dphi = nullptr;            // [B_l][D]
   float* ac_dz[2] = {nullptr, nullptr};    // critic dX chain ping-pong [B_l][max(width, D)]
   float* a_grads = nullptr;                // [dw_splits][n_actor_params]
-  float* a_loss = nullptr;                 // [4]: summed rows (all-reduced), loss
+  float* a_loss = nullptr;                 // [4]: summed rows, summed log pi (all-reduced), loss, mean log pi
   int *a_t = nullptr, *a_skip = nullptr;
+  float* ent_mv = nullptr;                 // [2] Adam moments of log alpha (entropy coefficient)
+  int* ent_t = nullptr;                    // its step counter
+  bool actor_loss_done = false;            // a crl_actor_loss has produced a mean log pi
 };
 
 constexpr int kTcLogitsMinN = 2;         // measured: tensor-core logits win down to N = 256

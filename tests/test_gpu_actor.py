@@ -95,3 +95,42 @@ def test_actor_loss_without_actor_is_unsupported():
     with pytest.raises(CrlError) as e:
         ctx.actor_loss(z, z, z, 0.1)
     assert e.value.code == 7             # CRL_EUNSUPPORTED
+
+
+def test_entropy_update_parity():
+    """crl_entropy_update (reading A-32) against oracle/critic.py entropy_update over three
+    Adam steps, fed the oracle's log pi of the same actor call (the GPU's mean log pi is fp32:
+    1e-5 relative on the loss, 1e-6 absolute on log alpha)."""
+    import torch
+    from oracle import critic as oc
+    cfg = crl_synth.preset("ant", batch=300)
+    A = cfg["act_dim"]
+    actor = crl_synth.init_actor_params(cfg, 43)
+    ctx, critic = _ctx(cfg, actor)
+    N = cfg["batch"]
+    s, _, g = crl_synth.random_batch(cfg, N, seed=9)
+    eps = np.random.default_rng(109).standard_normal((N, A)).astype(np.float32)
+    ds, dg, de = (torch.from_numpy(x).cuda() for x in (s, g, eps))
+    log_alpha = torch.full((1,), np.log(0.1), dtype=torch.float32, device="cuda")
+    alpha = torch.zeros(1, device="cuda")
+    lossa = torch.zeros(1, device="cuda")
+    from paper_2408_11052_b200 import CrlError
+    with pytest.raises(CrlError):                  # no actor loss yet: CRL_ESTATE
+        ctx.entropy_update(log_alpha, lr=1e-2)
+    ctx.actor_loss(ds, dg, de, 0.1)
+    ref = oc.actor_loss(actor.astype(np.float64), critic, s, g, eps, alpha_ent=0.1, obs_dim=cfg["obs_dim"],
+                        act_dim=A, goal_dim=cfg["goal_dim"], depth=cfg["depth"], width=cfg["width"],
+                        repr_dim=cfg["repr_dim"], actor_depth=2, actor_width=256,
+                        energy_kind=cfg["energy"], activation=cfg["activation"])
+    H = -0.5 * A
+    la, m, v, t = float(np.float32(np.log(0.1))), 0.0, 0.0, 0
+    for it in range(3):
+        ctx.entropy_update(log_alpha, target_entropy=H, lr=1e-2, alpha_out=alpha, loss_out=lossa)
+        torch.cuda.synchronize()
+        assert ctx.status() == 0
+        o = oc.entropy_update(ref["log_pi"], la, m, v, t, target_entropy=H, lr=1e-2, b1=ctx.cfg.adam_b1,
+                              b2=ctx.cfg.adam_b2, eps=ctx.cfg.adam_eps)
+        assert abs(float(lossa.cpu()[0]) - o["loss"]) <= 1e-5 * abs(o["loss"]), (it, float(lossa.cpu()[0]), o)
+        assert abs(float(log_alpha.cpu()[0]) - o["log_alpha"]) <= 1e-6, (it, float(log_alpha.cpu()[0]), o)
+        assert abs(float(alpha.cpu()[0]) - o["alpha"]) <= 1e-6 * o["alpha"] + 1e-7
+        la, m, v, t = o["log_alpha"], o["m"], o["v"], o["t"]

@@ -274,3 +274,36 @@ def test_bf16_round_is_round_to_nearest_even():
     x = np.array([1.0, 1.0 + 2**-8, 1.0 + 3 * 2**-8, -3.14159], np.float32)
     r = critic.bf16_round(x)
     assert r[0] == 1.0 and r[1] == 1.0 and r[2] == 1.0 + 2**-6 and abs(r[3] + 3.140625) < 1e-12
+
+
+# ------------------------------------------------------------------ entropy coefficient (A-32)
+
+def test_entropy_update_first_step_closed_form():
+    """First Adam step from zero moments: m^ = g, v^ = g^2, so log_alpha moves by exactly
+    -lr g / (|g| + eps); g = alpha (-mean log pi - H)."""
+    log_pi = np.array([-1.5, -0.5, -2.0, -1.0])            # mean -1.25
+    la, H, lr = math.log(0.2), -2.0, 1e-3
+    out = critic.entropy_update(log_pi, la, 0.0, 0.0, 0, target_entropy=H, lr=lr)
+    g = 0.2 * (1.25 - (-2.0))                               # alpha (-mean - H) = 0.2 * 3.25
+    assert out["loss"] == pytest.approx(g, rel=1e-15)
+    assert out["log_alpha"] == pytest.approx(la - lr * g / (abs(g) + 1e-8), rel=1e-15)
+    assert out["alpha"] == pytest.approx(math.exp(out["log_alpha"]), rel=1e-15)
+    assert out["t"] == 1
+
+
+def test_entropy_update_direction():
+    """Policy entropy above the target (-mean log pi > H) lowers alpha; below raises it."""
+    H = -3.0
+    hi = critic.entropy_update(np.full(8, 1.0), 0.0, 0.0, 0.0, 0, target_entropy=H, lr=1e-2)
+    lo = critic.entropy_update(np.full(8, 5.0), 0.0, 0.0, 0.0, 0, target_entropy=H, lr=1e-2)
+    assert hi["alpha"] < 1.0 < lo["alpha"]
+
+
+def test_entropy_update_gradient_finite_difference():
+    """The Adam input is dL/dlog_alpha: check it against a central difference of
+    L(log_alpha) = exp(log_alpha) (-mean log pi - H) (zero-lr call exposes the loss)."""
+    log_pi = np.array([0.3, -0.7, 1.1])
+    H, la, h = 0.5, -0.4, 1e-6
+    f = lambda x: critic.entropy_update(log_pi, x, 0, 0, 0, target_entropy=H, lr=1e-30)["loss"]
+    fd = (f(la + h) - f(la - h)) / (2 * h)
+    assert f(la) == pytest.approx(fd, rel=1e-8)
