@@ -42,6 +42,8 @@ def parse():
     p.add_argument("--precision", default="bf16")
     p.add_argument("--energy", default=None)
     p.add_argument("--profile-steps", type=int, default=20)
+    p.add_argument("--bulk-updates", type=int, default=256,
+                   help="A1 bulk-mode measurement: updates per crl_relabel_sample_bulk call (0: skip)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -407,6 +409,37 @@ def run_ours(args):
     stages = ctx.profile_read()
     ctx.profile_enable(False)
 
+    # ---- A1 in bulk mode (F4): many updates' rows in one launch, HBM fraction of the gather
+    bulk = None
+    if rank == 0 and args.bulk_updates > 0:
+        nb = args.bulk_updates
+        bs = torch.empty(nb * Bl, cfg["obs_dim"], device="cuda")
+        ba = torch.empty(nb * Bl, cfg["act_dim"], device="cuda")
+        bg = torch.empty(nb * Bl, cfg["goal_dim"], device="cuda")
+        bi = torch.empty(nb * Bl, 3, dtype=torch.int64, device="cuda")
+        with torch.cuda.stream(stream):
+            for i in range(3):
+                ctx.relabel_sample_bulk(crl_synth.PHILOX_SEED, 40_000_000 + i * nb, nb, bs, ba, bg, bi, stream=stream)
+            b0 = [torch.cuda.Event(enable_timing=True) for _ in range(10)]
+            b1 = [torch.cuda.Event(enable_timing=True) for _ in range(10)]
+            for i in range(10):
+                flush.zero_()
+                b0[i].record(stream)
+                ctx.relabel_sample_bulk(crl_synth.PHILOX_SEED, 41_000_000 + i * nb, nb, bs, ba, bg, bi, stream=stream)
+                b1[i].record(stream)
+        torch.cuda.synchronize()
+        us = sum(x.elapsed_time(y) for x, y in zip(b0, b1)) / 10 * 1e3
+        # algorithmic bytes per row: read s, a, g + the ep_end word, write s, a, g
+        # and the three int64 indices
+        row_bytes = 2 * 4 * (cfg["obs_dim"] + cfg["act_dim"] + cfg["goal_dim"]) + 4 + 24
+        gbs = nb * Bl * row_bytes / (us * 1e-6) / 1e9
+        peaks_b, _ = load_peaks()
+        hbm = peaks_b.get("hbm_gbs") if isinstance(peaks_b, dict) else None
+        bulk = {"rows": nb * Bl, "n_updates": nb, "us": round(us, 2), "bytes_per_row": row_bytes,
+                "achieved_GBs": round(gbs, 1), "hbm_peak_GBs": hbm,
+                "frac": round(gbs / hbm, 4) if hbm else None,
+                "note": "crl_relabel_sample_bulk: one launch for n_updates batches (L2 flushed before each)"}
+
     if rank == 0:
         peaks, kind = load_peaks()
         try:
@@ -433,7 +466,8 @@ def run_ours(args):
                            "beta_lse": cfg["beta_lse"], "buffer": f"{cfg['n_envs']}x{cfg['capacity']}",
                            "parallelism": f"dp{world}", "l2_flush": "256 MiB memset between timed steps"},
                 "clocks": clocks, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-                "gpu_launches_per_step": launches_per_step, "roofline": rl, "cpu_baseline": cpu,
+                "gpu_launches_per_step": launches_per_step, "roofline": rl, "relabel_bulk": bulk,
+                "cpu_baseline": cpu,
                 "device_status": status}
         print(json.dumps(line), flush=True)
     ctx.close()

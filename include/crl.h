@@ -146,6 +146,14 @@ CRL_API crl_status crl_buffer_insert(crl_ctx* ctx, const float* obs, const float
 CRL_API crl_status crl_relabel_sample(crl_ctx* ctx, uint64_t seed, uint64_t step, float* s, float* a,
                               float* g, int64_t* idx, void* stream);
 
+/* F4 — bulk sampling for several updates in one launch (Alg. 1 P:1044-1046 runs num_updates
+ * gradient steps per collection round).  Output row u*batch_local + r is
+ * exactly row r of crl_relabel_sample(seed, step0 + u): s[n_updates*B_l][obs_dim],
+ * a[n_updates*B_l][act_dim], g[n_updates*B_l][goal_dim], idx[n_updates*B_l][3] (idx may be
+ * NULL), all device.  CRL_EINVAL if n_updates < 1 or n_updates * batch_local > 2^30. */
+CRL_API crl_status crl_relabel_sample_bulk(crl_ctx* ctx, uint64_t seed, uint64_t step0, int n_updates,
+                                           float* s, float* a, float* g, int64_t* idx, void* stream);
+
 /* A2-A6 — one critic update (Alg. 1) on the batch (s, a, g):
  *   phi = phi_enc([s||a]), psi = psi_enc(g); l_ij = f(phi_i, psi_j) over the GLOBAL batch
  *   (global negatives, reading A-21); L = c_f L_fwd + c_b L_bwd + beta mean_i LSE_i^2

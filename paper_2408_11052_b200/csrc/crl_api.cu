@@ -441,24 +441,36 @@ crl_status crl_buffer_insert(crl_ctx* ctx, const float* obs, const float* act, c
   return CRL_OK;
 }
 
-crl_status crl_relabel_sample(crl_ctx* ctx, uint64_t seed, uint64_t step, float* s, float* a,
-                              float* g, int64_t* idx, void* stream) {
+static crl_status relabel(crl_ctx* ctx, uint64_t seed, uint64_t step, int n_upd, float* s, float* a, float* g,
+                          int64_t* idx, void* stream) {
   if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
   if (!s || !a || !g) return fail(ctx, CRL_EINVAL, "sample: NULL output");
+  if (n_upd < 1 || (long)n_upd * ctx->cfg.batch_local > (1l << 30))
+    return fail(ctx, CRL_EINVAL, "sample: n_updates must be >= 1 and n_updates * batch_local <= 2^30");
   const crl_config& k = ctx->cfg;
   const uint64_t n_ins = ctx->n_ins;
   const uint64_t tau_new = n_ins - 1;
   const uint64_t tau_old = n_ins > (uint64_t)k.capacity ? n_ins - k.capacity : 0;
   if (n_ins < 2) return fail(ctx, CRL_ESTATE, "buffer holds fewer than 2 slots per env");
   if (ctx->prof_on) spin_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(100000ull);
-  Stage sg(ctx, (cudaStream_t)stream, "relabel");
-  CU(launch_relabel_sample(k.batch_local, k.rank, k.n_envs_local, k.capacity, k.obs_dim, k.act_dim,
+  Stage sg(ctx, (cudaStream_t)stream, n_upd > 1 ? "relabel_bulk" : "relabel");
+  CU(launch_relabel_sample(k.batch_local, n_upd, k.rank, k.n_envs_local, k.capacity, k.obs_dim, k.act_dim,
                            k.goal_dim, k.goal_offset, ctx->obs_stride, ctx->act_stride,
                            (uint32_t)tau_old, (uint32_t)tau_new, seed, step, k.gamma, ctx->obs_ring,
                            ctx->act_ring, ctx->ep_end, ctx->qtab, s, a, g, idx, ctx->status,
                            (cudaStream_t)stream));
   ctx->launches = 1;
   return CRL_OK;
+}
+
+crl_status crl_relabel_sample(crl_ctx* ctx, uint64_t seed, uint64_t step, float* s, float* a,
+                              float* g, int64_t* idx, void* stream) {
+  return relabel(ctx, seed, step, 1, s, a, g, idx, stream);
+}
+
+crl_status crl_relabel_sample_bulk(crl_ctx* ctx, uint64_t seed, uint64_t step0, int n_updates, float* s,
+                                   float* a, float* g, int64_t* idx, void* stream) {
+  return relabel(ctx, seed, step0, n_updates, s, a, g, idx, stream);
 }
 
 }  // extern "C"

@@ -315,3 +315,35 @@ def test_critic_step_bf16_tc_logits_exact_q_path(energy, monkeypatch):
     monkeypatch.setenv("CRL_FORCE_EXACT_Q", "1")
     cfg = crl_synth.preset("ant", batch=1100, width=128, energy=energy, precision="bf16")
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+def test_relabel_bulk_matches_single_calls_and_oracle():
+    """F4 bulk sampling: row u*B + r equals row r of the single call at step0 + u (bitwise)
+    and the oracle's sample at that step."""
+    cfg = crl_synth.preset("reacher", precision="fp32", batch=96)
+    ctx, _ = make_ctx(cfg)
+    chunks = fill_buffer(ctx, cfg, 20, U=62)
+    bufs = oracle_buffers(cfg, chunks)
+    n, B, step0 = 5, 96, 2 ** 32 - 2                  # the step crosses the 32-bit boundary
+    s = torch.empty(n * B, cfg["obs_dim"], device="cuda")
+    a = torch.empty(n * B, cfg["act_dim"], device="cuda")
+    g = torch.empty(n * B, cfg["goal_dim"], device="cuda")
+    idx = torch.empty(n * B, 3, dtype=torch.int64, device="cuda")
+    ctx.relabel_sample_bulk(SEED, step0, n, s, a, g, idx)
+    torch.cuda.synchronize()
+    for u in range(n):
+        s1, a1, g1, i1 = _sample_gpu(ctx, cfg, step0 + u)
+        sl = slice(u * B, (u + 1) * B)
+        assert np.array_equal(idx[sl].cpu().numpy(), i1)
+        assert np.array_equal(s[sl].cpu().numpy().view(np.uint32), s1.view(np.uint32))
+        assert np.array_equal(a[sl].cpu().numpy().view(np.uint32), a1.view(np.uint32))
+        assert np.array_equal(g[sl].cpu().numpy().view(np.uint32), g1.view(np.uint32))
+        if u in (0, n - 1):
+            _, _, og, oidx = oreplay.relabel_sample(bufs[0], SEED, step0 + u, B, gamma=cfg["gamma"],
+                                                    goal_offset=cfg["goal_offset"], goal_dim=cfg["goal_dim"])
+            assert np.array_equal(i1, oidx)
+            assert np.array_equal(g1.view(np.uint32), og.view(np.uint32))
+    from paper_2408_11052_b200 import CrlError
+    with pytest.raises(CrlError):
+        ctx.relabel_sample_bulk(SEED, 0, 0, s, a, g)
+    assert ctx.status() == 0
