@@ -29,9 +29,17 @@
 namespace crl {
 namespace tc {
 
-constexpr int CH_STAGES = 2;
+// Weight K-block stages and store staging per mode (same SMEM total): the forward stages Z_l /
+// Y for TMA stores (4 chunks) and keeps 2 weight stages; the backward has no staging and keeps
+// 4 weight stages = a whole 256-wide layer, so the next layer's weights are requested before
+// this layer's dZ stores enter the SM's TMA queue (measured: 2 stages put the last two
+// blocks ~4000 clk behind the stores; backward 66 -> 63 us at N = 16384.  Direct-from-register
+// Z stores in the forward, to free room for 4 stages there, were slower: 66 -> 72 us)
+template <int MODE> struct ChCfg {
+  static constexpr int STAGES = MODE == 0 ? 2 : 4;
+  static constexpr int STG_CHUNKS = MODE == 0 ? 4 : 0;
+};
 constexpr int CH_ACT_CHUNKS = 5;                  // K <= 320
-constexpr int CH_STG_CHUNKS = 4;                  // Z_l / Y staging for the TMA stores
 constexpr uint32_t CH_CHUNK = 128 * 128;          // 128 rows x 64 bf16 (one SW128 K chunk)
 constexpr uint32_t CH_WSTAGE = 64 * 256 * 2;      // 64 K rows x up to 256 N
 constexpr int CH_BIAS = kChainMaxL * 256;
@@ -72,10 +80,10 @@ __device__ __forceinline__ float silu_grad_fast(float z) {
   return fmaf(0.5f, fmaf(h, fmaf(-t, t, 1.f), t), 0.5f);
 }
 // FWD hidden layer: Z = acc + b (bf16 pairs zk), X' = act(Z) (bf16 pairs pk)
-template <bool SILU>
+template <bool SILU, int NE>
 __device__ __forceinline__ void epi_fwd_hidden(uint32_t* raw, uint32_t bias_a, uint32_t* pk, uint32_t* zk) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < NE / 4; ++j) {
     const float4 b = lds128f(bias_a + 16u * j);
     const float z0 = __uint_as_float(raw[4 * j]) + b.x, z1 = __uint_as_float(raw[4 * j + 1]) + b.y;
     const float z2 = __uint_as_float(raw[4 * j + 2]) + b.z, z3 = __uint_as_float(raw[4 * j + 3]) + b.w;
@@ -91,10 +99,11 @@ __device__ __forceinline__ void epi_fwd_hidden(uint32_t* raw, uint32_t bias_a, u
   }
 }
 // FWD output layer: Y = acc + b (fp32 back into raw, bf16 pairs pk); returns sum of bf16(Y)^2
+template <int NE>
 __device__ __forceinline__ float epi_fwd_last(uint32_t* raw, uint32_t bias_a, uint32_t* pk) {
   float st = 0.f;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < NE / 4; ++j) {
     const float4 b = lds128f(bias_a + 16u * j);
     const float y0 = __uint_as_float(raw[4 * j]) + b.x, y1 = __uint_as_float(raw[4 * j + 1]) + b.y;
     const float y2 = __uint_as_float(raw[4 * j + 2]) + b.z, y3 = __uint_as_float(raw[4 * j + 3]) + b.w;
@@ -109,10 +118,10 @@ __device__ __forceinline__ float epi_fwd_last(uint32_t* raw, uint32_t bias_a, ui
   return st;
 }
 // BWD: dZ_{l-1} = acc * act'(Z_{l-1})
-template <bool SILU>
+template <bool SILU, int NE>
 __device__ __forceinline__ void epi_bwd(const uint32_t* raw, const uint32_t* zw, uint32_t* pk) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < NE / 2; ++i) {
     const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zw[i]));
     const float g0 = SILU ? silu_grad_fast(z.x) : (z.x > 0.f ? 1.f : 0.f);
     const float g1 = SILU ? silu_grad_fast(z.y) : (z.y > 0.f ? 1.f : 0.f);
@@ -120,15 +129,19 @@ __device__ __forceinline__ void epi_bwd(const uint32_t* raw, const uint32_t* zw,
   }
 }
 
+constexpr int CH_NWG = 4;                        // epilogue warpgroups: one 64-feature chunk each
+constexpr int CH_NT = 128 + 128 * CH_NWG;
+
 template <int MODE>   // 0 = forward, 1 = backward dX chain
-__global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant__ ChainMaps maps0,
+__global__ void __launch_bounds__(CH_NT, 1) tc_chain_kernel(const __grid_constant__ ChainMaps maps0,
                                                           const __grid_constant__ ChainMaps maps1,
                                                           const ChainParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAct = smem;
   uint8_t* sStg = sAct + CH_ACT_CHUNKS * CH_CHUNK;
-  uint8_t* sW = sStg + CH_STG_CHUNKS * CH_CHUNK;
+  constexpr int CH_STAGES = ChCfg<MODE>::STAGES;
+  uint8_t* sW = sStg + ChCfg<MODE>::STG_CHUNKS * CH_CHUNK;
   float* sBias = reinterpret_cast<float*>(sW + CH_STAGES * CH_WSTAGE);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + CH_BIAS);
   uint64_t* a0_full = bars;
@@ -148,6 +161,11 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
   __shared__ long long s_tr[64];
   const bool trace = (p.dbg & 4) && blockIdx.x == 0 && blockIdx.y == 0;
 #define CH_TR(i) do { if (trace) s_tr[(i)] = clock64(); } while (0)
+  // row blocks walk the K blocks of each layer from staggered starts (dbg & 8 disables): in
+  // lockstep every CTA fetches the same weight block from the same L2 lines at once
+  // (measured at N = 16384: forward 66 -> 63 us, backward unchanged)
+  const int rot = (p.dbg & 8) ? 0 : (int)blockIdx.x;
+  auto kb_rot = [&](int i, int n) { return (i + rot) % n; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mp.a0);
@@ -179,7 +197,8 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
       const ChainLayer& Ly = E.layer[l];
       const int nkb = (Ly.K + 63) / 64;
       const uint32_t bytes = 64u * Ly.N * 2u;
-      for (int kb = 0; kb < nkb; ++kb, ++g) {
+      for (int kbi = 0; kbi < nkb; ++kbi, ++g) {
+        const int kb = kb_rot(kbi, nkb);
         const int s = g % CH_STAGES;
         mbar_wait(&w_empty[s], ((g / CH_STAGES) & 1) ^ 1);
         if (g < 20) CH_TR(1 + g);
@@ -202,7 +221,8 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
       const uint32_t idesc = idesc_bf16_f32(128, Ly.N, false, MODE == 0);
       const int nkb = (Ly.K + 63) / 64;
       if (l == 0) mbar_wait(a0_full, 0);
-      for (int kb = 0; kb < nkb; ++kb, ++g) {
+      for (int kbi = 0; kbi < nkb; ++kbi, ++g) {
+        const int kb = kb_rot(kbi, nkb);
         if (l > 0) mbar_wait(&act_ready[kb], (l - 1) & 1);   // chunk kb of this layer's input
         const int s = g % CH_STAGES;
         mbar_wait(&w_full[s], (g / CH_STAGES) & 1);
@@ -214,14 +234,16 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
           const uint64_t ad = smem_desc_sw128(act_base + kb * CH_CHUNK + ks * 32, 16, 1024);
           const uint64_t bd = MODE == 0 ? smem_desc_sw128(wb + ks * 2048, 8192, 1024)
                                         : smem_desc_sw128(wb + ks * 32, 16, 1024);
-          mma_bf16(acc, ad, bd, idesc, (kb | ks) != 0);
+          mma_bf16(acc, ad, bd, idesc, (kbi | ks) != 0);
         }
         mma_commit(&w_empty[s]);
       }
       mma_commit(&acc_full[l & 1]);
     }
   } else if (warp >= 4) {
-    // -------------------------------------------------------------------- epilogue (2 warpgroups)
+    // -------------------------------------------------------------------- epilogue (4 warpgroups)
+    // warpgroup wg owns the 64-feature chunks c = wg, wg + 4, ... of every layer output and
+    // handles each as two 32-column halves (register budget of 640 threads)
     const int wg = (warp - 4) >> 2;
     const int q = warp & 3;
     const int r = q * 32 + lane;
@@ -229,10 +251,11 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
     const bool rv = row < p.M;
     const bool storer = (q == 0 && lane == 0);          // issues this warpgroup's TMA stores
     const bool st_ok = !(p.dbg & 1);
+    const uint32_t row_a = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
     if (MODE == 0) {                                   // all biases of this encoder -> SMEM
       for (int l = 0; l < L; ++l)
-        for (int c = threadIdx.x - 128; c < E.layer[l].N; c += 256) sBias[l * 256 + c] = E.layer[l].bias[c];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+        for (int c = threadIdx.x - 128; c < E.layer[l].N; c += 128 * CH_NWG) sBias[l * 256 + c] = E.layer[l].bias[c];
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * CH_NWG) : "memory");
     }
     float stat = 0.f;
     for (int l = 0; l < L; ++l) {
@@ -241,67 +264,58 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
       const int N = Ly.N;
       const int nch = N / 64;
       const uint32_t acc = tmem + (uint32_t)((l & 1) * 256);
-      // this warpgroup's 64-feature chunks
-      const int cb = (nch == 1) ? (wg == 0 ? 0 : 1) : (wg == 0 ? 0 : (nch + 1) / 2);
-      const int ce = (nch == 1) ? 1 : (wg == 0 ? (nch + 1) / 2 : nch);
-      uint4 zp[16];                                    // BWD: this warpgroup's part of the Z_{l-1} row
-      if (MODE == 1 && rv) {
-        const uint4* zr = reinterpret_cast<const uint4*>(Ly.zprev + (size_t)row * N + cb * 64);
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (cb * 64 + 8 * j < ce * 64) zp[j] = zr[j];
-      }
       mbar_wait(&acc_full[l & 1], (l >> 1) & 1);
-      if (storer && l < 5) CH_TR(42 + 5 * wg + l);
+      if (storer && l < 5 && wg < 2) CH_TR(42 + 5 * wg + l);
       tc_fence_after();
-      // SMEM chunks are about to be rewritten: the previous layer's TMA stores (of either
-      // warpgroup: the chunk split changes with N) must have read them
+      // SMEM chunks are about to be rewritten: the previous layer's TMA stores (of any
+      // warpgroup: the chunk owners change with N) must have read them
       if (storer) bulk_wait_read();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {                 // at most 2 chunks (128 features) per warpgroup
-        const int c = cb + cc;
-        if (c >= ce) break;
-        uint32_t raw[64];
-        tmem_ld32_nowait(acc + ((uint32_t)(q * 32) << 16) + 64 * c, *reinterpret_cast<uint32_t(*)[32]>(raw));
-        tmem_ld32_nowait(acc + ((uint32_t)(q * 32) << 16) + 64 * c + 32,
-                         *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
-        tmem_ld_wait();
-        if (storer && wg == 0 && l == 1) CH_TR(58 + 3 * cc);
-        uint32_t pk[32];                               // bf16 pairs of the value feeding the next step
-        // (branch-free specialised loops: a per-element branch on `last` / the activation
-        // serialises the MUFU latency of every element)
-        const uint32_t bias_a = smem_u32(sBias) + (uint32_t)(l * 256 + 64 * c) * 4u;
-        const uint32_t row_a = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * CH_NWG) : "memory");
+      for (int c = wg; c < nch; c += CH_NWG) {
+        const uint32_t bias_c = smem_u32(sBias) + (uint32_t)(l * 256 + 64 * c) * 4u;
         const uint32_t act_a = smem_u32(((MODE == 0 && last) ? sStg : sAct) + c * CH_CHUNK) + row_a;
-        if (MODE == 0 && !last) {
-          uint32_t zk[32];                             // bf16 pairs of Z
-          if (p.act == CRL_ACT_SILU) epi_fwd_hidden<true>(raw, bias_a, pk, zk);
-          else epi_fwd_hidden<false>(raw, bias_a, pk, zk);
-          const uint32_t z_a = smem_u32(sStg + c * CH_CHUNK) + row_a;
+        const uint32_t z_a = smem_u32(sStg + c * CH_CHUNK) + row_a;
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            sts128(z_a + (uint32_t)((u ^ (r & 7)) << 4), make_uint4(zk[4 * u], zk[4 * u + 1], zk[4 * u + 2], zk[4 * u + 3]));
-        } else if (MODE == 0) {
-          stat += epi_fwd_last(raw, bias_a, pk);
-        } else {
-          const uint32_t* zw = reinterpret_cast<const uint32_t*>(zp) + 32 * cc;
-          if (p.act == CRL_ACT_SILU) epi_bwd<true>(raw, zw, pk);
-          else epi_bwd<false>(raw, zw, pk);
-        }
-        // SMEM: pk -> the operand chunk (next step's A, also the TMA-store source); FWD hidden:
-        // Z -> the staging chunk (above); FWD last: Y bf16 -> staging, Y fp32 straight to HBM
-        if (storer && wg == 0 && l == 1) CH_TR(59 + 3 * cc);
+        for (int hf = 0; hf < 2; ++hf) {                 // 32-column halves of the chunk
+          uint4 zp[4];                                   // BWD: Z_{l-1} row, these 32 features
+          if (MODE == 1 && rv) {
+            const uint4* zr = reinterpret_cast<const uint4*>(Ly.zprev + (size_t)row * N + 64 * c + 32 * hf);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          sts128(act_a + (uint32_t)((u ^ (r & 7)) << 4),
-                 rv ? make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]) : make_uint4(0u, 0u, 0u, 0u));
-        if (MODE == 0 && last && rv && st_ok) {
-          float4* yo = reinterpret_cast<float4*>(Ly.out_f + (size_t)row * N + 64 * c);
+            for (int j = 0; j < 4; ++j) zp[j] = zr[j];
+          }
+          uint32_t raw[32];
+          tmem_ld32_nowait(acc + ((uint32_t)(q * 32) << 16) + 64 * c + 32 * hf, raw);
+          tmem_ld_wait();
+          uint32_t pk[16];                               // bf16 pairs of the value feeding the next step
+          const uint32_t bias_a = bias_c + 128u * hf;
+          if (MODE == 0 && !last) {
+            uint32_t zk[16];                             // bf16 pairs of Z
+            if (p.act == CRL_ACT_SILU) epi_fwd_hidden<true, 32>(raw, bias_a, pk, zk);
+            else epi_fwd_hidden<false, 32>(raw, bias_a, pk, zk);
 #pragma unroll
-          for (int u = 0; u < 16; ++u)
-            yo[u] = make_float4(__uint_as_float(raw[4 * u]), __uint_as_float(raw[4 * u + 1]),
-                                __uint_as_float(raw[4 * u + 2]), __uint_as_float(raw[4 * u + 3]));
+            for (int u = 0; u < 4; ++u)
+              sts128(z_a + (uint32_t)(((u + 4 * hf) ^ (r & 7)) << 4),
+                     make_uint4(zk[4 * u], zk[4 * u + 1], zk[4 * u + 2], zk[4 * u + 3]));
+          } else if (MODE == 0) {
+            stat += epi_fwd_last<32>(raw, bias_a, pk);
+          } else {
+            const uint32_t* zw = reinterpret_cast<const uint32_t*>(zp);
+            if (p.act == CRL_ACT_SILU) epi_bwd<true, 32>(raw, zw, pk);
+            else epi_bwd<false, 32>(raw, zw, pk);
+          }
+          // SMEM: pk -> the operand chunk (next step's A, also the TMA-store source); FWD
+          // hidden: Z -> the staging chunk (above); FWD last: Y bf16 -> staging, Y fp32 -> HBM
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            sts128(act_a + (uint32_t)(((u + 4 * hf) ^ (r & 7)) << 4),
+                   rv ? make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]) : make_uint4(0u, 0u, 0u, 0u));
+          if (MODE == 0 && last && rv && st_ok) {
+            float4* yo = reinterpret_cast<float4*>(Ly.out_f + (size_t)row * N + 64 * c + 32 * hf);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              yo[u] = make_float4(__uint_as_float(raw[4 * u]), __uint_as_float(raw[4 * u + 1]),
+                                  __uint_as_float(raw[4 * u + 2]), __uint_as_float(raw[4 * u + 3]));
+          }
         }
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -309,7 +323,6 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
         if (!(MODE == 0 && last) && lane == 0) mbar_arrive(&act_ready[c]);
         // whole 128 x 64 chunk written by the 4 warps -> one TMA store per tensor
         wg_sync(wg);
-        if (storer && wg == 0 && l == 1) CH_TR(60 + 3 * cc);
         if (storer && st_ok) {
           if (MODE == 0 && !last) {
             tma_store_2d(&mp.st_out[l], sAct + c * CH_CHUNK, 64 * c, m0);
@@ -327,13 +340,14 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
     if (storer) bulk_wait_all();
     if (storer && wg == 0) CH_TR(57);
     if (MODE == 0) {
-      // row statistic of Y: warpgroup 1 hands its columns' partial sum to warpgroup 0
+      // row statistic of Y: warpgroups 1.. hand their columns' partial sums to warpgroup 0
       float* sStat = sBias;                            // biases are no longer needed
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (wg == 1) sStat[r] = stat;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * CH_NWG) : "memory");
+      if (wg > 0) sStat[(wg - 1) * 128 + r] = stat;
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * CH_NWG) : "memory");
       if (wg == 0 && rv && E.out_stat != nullptr) {
-        const float st = stat + sStat[r];
+        float st = stat;
+        for (int w = 1; w < CH_NWG; ++w) st += sStat[(w - 1) * 128 + r];
         E.out_stat[row] = p.energy == CRL_ENERGY_L2 ? st
                           : (p.energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(st), kEpsCos) : 0.f);
       }
@@ -353,7 +367,9 @@ __global__ void __launch_bounds__(384, 1) tc_chain_kernel(const __grid_constant_
 }
 
 size_t tc_chain_smem() {
-  return 1024 + (CH_ACT_CHUNKS + CH_STG_CHUNKS) * CH_CHUNK + CH_STAGES * CH_WSTAGE + CH_BIAS * 4 + 256;
+  static_assert(ChCfg<0>::STG_CHUNKS * CH_CHUNK + ChCfg<0>::STAGES * CH_WSTAGE ==
+                ChCfg<1>::STG_CHUNKS * CH_CHUNK + ChCfg<1>::STAGES * CH_WSTAGE, "one SMEM size for both modes");
+  return 1024 + (CH_ACT_CHUNKS + ChCfg<0>::STG_CHUNKS) * CH_CHUNK + ChCfg<0>::STAGES * CH_WSTAGE + CH_BIAS * 4 + 256;
 }
 
 bool tc_chain_supported(int in0, int width, int D, int depth) {
@@ -373,7 +389,7 @@ static cudaError_t launch_chain(const ChainMaps& m0, const ChainMaps& m1, const 
     attr = true;
   }
   dim3 grid((p.M + 127) / 128, nenc);
-  return launch_pdl(tc_chain_kernel<MODE>, grid, dim3(384), smem, st, m0, m1, p);
+  return launch_pdl(tc_chain_kernel<MODE>, grid, dim3(CH_NT), smem, st, m0, m1, p);
 }
 
 cudaError_t tc_chain_forward(const ChainMaps& m0, const ChainMaps& m1, const ChainParams& p, cudaStream_t st) {
