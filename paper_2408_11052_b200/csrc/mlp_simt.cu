@@ -1,3 +1,5 @@
+#include <algorithm>
+#include <cstdlib>
 // mlp_simt.cu — fp32 SIMT GEMMs for the phi/psi encoders (A2 forward, A5 backward).
 //
 // Paper: §3.1 P:193-195 (phi(s,a), psi(g)), Table 2, §5.4 (width/depth).
@@ -253,6 +255,7 @@ cudaError_t mlp_backward_dw_f32(int Bn, int in, int out, const float* X, int ldx
 
 // The number of batch slices the dW GEMMs use for batch Bn (same on every call).
 int dw_splits_for(int Bn) {
+  if (const char* e = std::getenv("CRL_DW_SPLITS")) return std::max(1, std::min(16, std::atoi(e)));
   int s = Bn / 512;
   return s < 1 ? 1 : (s > 8 ? 8 : s);
 }

@@ -14,6 +14,8 @@
 // Replaces 2 launches per layer (tc_gemm dW + colsum) with one for the whole backward.
 #include "common.cuh"
 #include "tc_common.cuh"
+#include <cstdlib>
+
 #include "tc_dwg.h"
 
 namespace crl {
@@ -114,6 +116,40 @@ __global__ void __launch_bounds__(256, 1) tc_dwg_kernel(const __grid_constant__ 
     mbar_wait(tfull, 0);
     tc_fence_after();
     float* dw = pr.dW + (size_t)split * P.split_stride;
+    if (pr.tma_w) {
+      // TMEM -> SW128 fp32 staging in the (now idle) B stages: bn / 32 boxes of 128 rows x 32
+      // columns, 16 KB each -> TMA stores (whole 128 B row segments instead of per-thread
+      // 16 B pieces of 1 KB-strided rows)
+      const int r = q * 32 + lane;
+      const uint32_t stg = smem_u32(sB) + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+#pragma unroll 1
+      for (int c0 = 0; c0 < bn; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+        if (nkb == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        const uint32_t cb = stg + (uint32_t)(c0 >> 5) * 16384u;
+        const int g0 = (c0 & 31) >> 2;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cb + (uint32_t)(((g0 + i) ^ (r & 7)) << 4)),
+                       "f"(v[4 * i]), "f"(v[4 * i + 1]), "f"(v[4 * i + 2]), "f"(v[4 * i + 3])
+                       : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (q == 0 && lane == 0) {
+        for (int j = 0; j < bn / 32; ++j)
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                           reinterpret_cast<uint64_t>(&pr.mapW)),
+                       "r"(smem_u32(sB) + (uint32_t)j * 16384u), "r"(n0 + 32 * j), "r"(m0), "r"(split)
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    } else {
 #pragma unroll 1
     for (int c0 = 0; c0 < bn; c0 += 16) {
       float v[16];
@@ -134,6 +170,7 @@ __global__ void __launch_bounds__(256, 1) tc_dwg_kernel(const __grid_constant__ 
           for (int i = 0; i < nvalid; ++i) dst[i] = v[i];
         }
       }
+    }
     }
     if (do_db && q == 0) {
       // every TMEM row of the second accumulator holds the 64 column sums of this tile
@@ -160,6 +197,7 @@ __global__ void __launch_bounds__(256, 1) tc_dwg_kernel(const __grid_constant__ 
 }
 
 bool make_map_bf16(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
+bool make_map_f32_3d(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
 
 bool dwg_add_problem(DwgParams& P, const __nv_bfloat16* X, int ldx, const __nv_bfloat16* dZ, int M, int N,
                      float* dW, float* db) {
@@ -170,6 +208,10 @@ bool dwg_add_problem(DwgParams& P, const __nv_bfloat16* X, int ldx, const __nv_b
   if (!make_map_bf16(&pr.mapX, X, M, P.K, ldx, 64, 64) || !make_map_bf16(&pr.mapDZ, dZ, N, P.K, N, 64, 64))
     return false;
   pr.M = M; pr.N = N; pr.dW = dW; pr.db = db;
+  // TMA-store epilogue when the partial slices are 16 B aligned (rows: N, slices: split_stride)
+  pr.tma_w = !std::getenv("CRL_DWG_NO_TMA_STORE") && (reinterpret_cast<uintptr_t>(dW) % 16 == 0) &&
+             (N % 4 == 0) && (P.split_stride % 4 == 0) &&
+             make_map_f32_3d(&pr.mapW, dW, N, M, P.splits, N, P.split_stride, 32, 128);
   // wide tiles only pay once K (= batch) is long; short K is latency bound: more, narrower
   // tiles spread the epilogue over more SMs (measured: B = 256 prefers 64, B >= 4096 256)
   pr.bn = P.K < 2048 ? 64 : (N >= GNMAX ? GNMAX : (N + 63) / 64 * 64);

@@ -12,9 +12,11 @@ constexpr int kDwgMaxProblems = 16;
 struct DwgProblem {
   CUtensorMap mapX;        // X_l  [K][ldx] bf16, box {64, 64}
   CUtensorMap mapDZ;       // dZ_l [K][N]   bf16, box {64, 64}
+  CUtensorMap mapW;        // dW_l partials [splits][M][N] fp32, box {32, 128, 1} (TMA-store epilogue)
   int M, N;                // dW_l is [M = in][N = out]
   int bn;                  // columns per tile (multiple of 64, <= 256)
   int mblk, nblk, tiles;   // tiles = mblk * nblk * splits
+  int tma_w;               // dW tile leaves through SMEM staging + TMA stores (16 B aligned rows)
   float* dW;               // slice 0 of the split-K partials (slice s at + s * split_stride)
   float* db;               // same, [N]
 };

@@ -372,6 +372,21 @@ bool make_map_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
   return r == CUDA_SUCCESS;
 }
 
+// fp32 [depth][outer][inner] with explicit pitches (elements), SW128 boxes {box_inner, box_outer, 1}
+bool make_map_f32_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t depth,
+                     uint64_t pitch_elems, uint64_t depth_pitch_elems, uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {inner, outer, depth};
+  cuuint64_t strides[2] = {pitch_elems * 4, depth_pitch_elems * 4};
+  cuuint32_t box[3] = {box_inner, box_outer, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcGemmArgs& p, int splits,
                              cudaStream_t st) {
