@@ -57,9 +57,14 @@ typedef enum {
   CRL_EUNSUPPORTED = 7   /* configuration not supported by this build                      */
 } crl_status;
 
-typedef enum { CRL_ENERGY_L2 = 0, CRL_ENERGY_DOT = 1, CRL_ENERGY_COS = 2 } crl_energy;
+typedef enum {
+  CRL_ENERGY_L2 = 0, CRL_ENERGY_DOT = 1, CRL_ENERGY_COS = 2, CRL_ENERGY_L1 = 3, CRL_ENERGY_L2SQ = 4
+} crl_energy;
 /* L2: f = -||phi - psi||_2 (App. A.2, sign per reading A-01)
- * DOT: f = <phi, psi>;  COS: f = <phi,psi>/(||phi|| ||psi||) */
+ * DOT: f = <phi, psi>;  COS: f = <phi,psi>/(||phi|| ||psi||)
+ * L1: f = -||phi - psi||_1 (derivative 0 at ties, reading A-33);
+ * L2SQ: f = -||phi - psi||_2^2 ("L2 w/o sqrt").  L1 and L2SQ run on
+ * the fp32 path (critic and actor); a bf16 context with them is CRL_EUNSUPPORTED. */
 typedef enum { CRL_LOSS_FWD = 0, CRL_LOSS_BWD = 1, CRL_LOSS_SYM = 2 } crl_loss;
 /* InfoNCE forward / backward / symmetric = fwd + bwd (App. A.2) */
 typedef enum { CRL_ACT_SILU = 0, CRL_ACT_RELU = 1 } crl_activation;

@@ -91,6 +91,10 @@ def _energy_diag_grad_phi(kind, phi, psi):
         npsi = np.maximum(np.linalg.norm(psi, axis=1), energy.EPS_COS)
         v = psi / npsi[:, None]
         return energy._cos_back(phi, v)
+    if kind == "l2sq":
+        return -2.0 * (phi - psi)
+    if kind == "l1":
+        return -np.sign(phi - psi)
     raise ValueError(kind)
 
 

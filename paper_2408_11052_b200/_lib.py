@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libcrl.so")
 CRL_OK, CRL_EINVAL, CRL_ESTATE, CRL_ECUDA, CRL_ENCCL, CRL_ENONFINITE, CRL_ESAMPLER, CRL_EUNSUPPORTED = range(8)
 STATUS_NAMES = ["CRL_OK", "CRL_EINVAL", "CRL_ESTATE", "CRL_ECUDA", "CRL_ENCCL", "CRL_ENONFINITE",
                 "CRL_ESAMPLER", "CRL_EUNSUPPORTED"]
-ENERGY = {"l2": 0, "dot": 1, "cos": 2}
+ENERGY = {"l2": 0, "dot": 1, "cos": 2, "l1": 3, "l2sq": 4}
 LOSS = {"fwd": 0, "bwd": 1, "sym": 2}
 ACT = {"silu": 0, "relu": 1}
 PRECISION = {"fp32": 0, "bf16": 1}

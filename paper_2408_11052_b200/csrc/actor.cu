@@ -71,6 +71,19 @@ __global__ void actor_diag_kernel(int Bl, int D, int energy, float invN, float a
     f = -r;
     const float c = invN / r;                    // -(1/N) * (-(x - y) / r)
     for (int k = lane; k < D; k += 32) dx[k] = c * (x[k] - y[k]);
+  } else if (energy == CRL_ENERGY_L2SQ) {        // f = -|x - y|^2, df/dx = -2 (x - y)
+    float ss = 0.f;
+    for (int k = lane; k < D; k += 32) { const float d = x[k] - y[k]; ss = fmaf(d, d, ss); }
+    f = -warp_sum(ss);
+    for (int k = lane; k < D; k += 32) dx[k] = 2.f * invN * (x[k] - y[k]);
+  } else if (energy == CRL_ENERGY_L1) {          // f = -|x - y|_1, df/dx = -sign(x - y)
+    float sa = 0.f;
+    for (int k = lane; k < D; k += 32) sa += fabsf(x[k] - y[k]);
+    f = -warp_sum(sa);
+    for (int k = lane; k < D; k += 32) {
+      const float d = x[k] - y[k];
+      dx[k] = invN * (float)((d > 0.f) - (d < 0.f));
+    }
   } else if (energy == CRL_ENERGY_DOT) {         // f = x . y
     float s = 0.f;
     for (int k = lane; k < D; k += 32) s = fmaf(x[k], y[k], s);

@@ -247,7 +247,9 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
     return fail(ctx, CRL_EUNSUPPORTED, "repr_dim must be one of 16, 32, 64, 128, 256");
   if (k->activation != CRL_ACT_SILU && k->activation != CRL_ACT_RELU)
     return fail(ctx, CRL_EINVAL, "activation");
-  if (k->energy < 0 || k->energy > 2) return fail(ctx, CRL_EINVAL, "energy");
+  if (k->energy < 0 || k->energy > 4) return fail(ctx, CRL_EINVAL, "energy");
+  if (k->precision == CRL_BF16 && k->energy > CRL_ENERGY_COS)
+    return fail(ctx, CRL_EUNSUPPORTED, "L1 / L2SQ energies run on the fp32 path only");
   if (k->loss < 0 || k->loss > 2) return fail(ctx, CRL_EINVAL, "loss");
   if (k->precision != CRL_FP32 && k->precision != CRL_BF16) return fail(ctx, CRL_EINVAL, "precision");
   if (k->precision == CRL_BF16 && (k->width % 16 != 0))

@@ -16,7 +16,9 @@
 //   (A,B) = (Phi,Psi): lr = LSE, lc = LSE', (c_r,c_c) = (c_f,c_b), beta_r = beta.
 //   With (A,B) = (Psi,Phi): lr = LSE', lc = LSE, (c_r,c_c) = (c_b,c_f), beta_c = beta.
 //   Energy chain: dot w = g;  L2 w = g / r (r = -l) and dA_i = sum_j w_ij B_j - (sum_j w_ij) A_i;
-//   cos w = g / |B_j|, du_i = sum_j w_ij B_j, dA_i = (du_i - (du_i.u_i) u_i) / |A_i|.
+//   cos w = g / |B_j|, du_i = sum_j w_ij B_j, dA_i = (du_i - (du_i.u_i) u_i) / |A_i|;
+//   L2sq (F3) w = 2 g with the L2 form; L1 (F3) dA_ik = sum_j g_ij sign(B_jk - A_ik) (no
+//   contraction form: an ALU pass over the same W tile, reading A-33 for ties).
 // L2 uses the difference form sum_k (a_k - b_k)^2 (no cancellation) on this fp32 path.
 //
 // Tiling: TR (16/32/64) A-rows per CTA, 64 B-rows per column tile; A and the column tiles
@@ -149,9 +151,11 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
       for (int i = 0; i < RI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          if (ENERGY == CRL_ENERGY_L2) {
+          if (ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) {
             const float d = a[i] - b[j];
             acc[i][j] = fmaf(d, d, acc[i][j]);
+          } else if (ENERGY == CRL_ENERGY_L1) {
+            acc[i][j] += fabsf(a[i] - b[j]);
           } else {
             acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
           }
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
       for (int j = 0; j < 4; ++j) {
         float v = acc[i][j];
         if (ENERGY == CRL_ENERGY_L2) v = -sqrtf(v + kEpsL2);
+        if (ENERGY == CRL_ENERGY_L2SQ || ENERGY == CRL_ENERGY_L1) v = -v;
         if (ENERGY == CRL_ENERGY_COS) v = v * nA[ty + 16 * i] * nB[buf * TC + tx + 16 * j];
         acc[i][j] = v;                    // acc now holds l_ij
       }
@@ -200,11 +205,12 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
             const float g = p.invN * (p.c_r * (pe - dlt) + p.c_c * (qe - dlt)) +
                             2.f * p.invN * (p.beta_r * lr_i[i] * pe + p.beta_c * lcj * qe);
             if (ENERGY == CRL_ENERGY_L2) w = g / (-lv);
+            else if (ENERGY == CRL_ENERGY_L2SQ) w = 2.f * g;
             else if (ENERGY == CRL_ENERGY_COS) w = g * nB[buf * TC + tx + 16 * j];
             else w = g;
           }
           Ws[(ty + 16 * i) * BPITCH + tx + 16 * j] = w;
-          if (ENERGY == CRL_ENERGY_L2) wsum[i] += w;
+          if (ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) wsum[i] += w;
         }
       }
       __syncthreads();
@@ -218,7 +224,15 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
         for (int c = 0; c < DC; ++c) {
           const float bv = B_[(tx + 16 * c) * BPITCH + jj];
 #pragma unroll
-          for (int i = 0; i < RI; ++i) acc2[i][c % (GRAD ? DC : 1)] = fmaf(w[i], bv, acc2[i][c % (GRAD ? DC : 1)]);
+          for (int i = 0; i < RI; ++i) {
+            if (ENERGY == CRL_ENERGY_L1) {
+              const float d = bv - At[(tx + 16 * c) * AP + ty + 16 * i];
+              const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+              acc2[i][c % (GRAD ? DC : 1)] = fmaf(w[i], sg, acc2[i][c % (GRAD ? DC : 1)]);
+            } else {
+              acc2[i][c % (GRAD ? DC : 1)] = fmaf(w[i], bv, acc2[i][c % (GRAD ? DC : 1)]);
+            }
+          }
         }
       }
     }
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
       const int rl = ty + 16 * i;
       const int r = a0 + rl;
       float* acc_i = acc2[i];
-      if (ENERGY == CRL_ENERGY_L2) {
+      if (ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) {
         float ws = wsum[i];
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
@@ -308,6 +322,8 @@ static cudaError_t launch_logits_e(int energy, const LogitsArgs& p, cudaStream_t
     case CRL_ENERGY_L2: return launch_logits_tr<D, CRL_ENERGY_L2, GRAD>(p, st);
     case CRL_ENERGY_DOT: return launch_logits_tr<D, CRL_ENERGY_DOT, GRAD>(p, st);
     case CRL_ENERGY_COS: return launch_logits_tr<D, CRL_ENERGY_COS, GRAD>(p, st);
+    case CRL_ENERGY_L1: return launch_logits_tr<D, CRL_ENERGY_L1, GRAD>(p, st);
+    case CRL_ENERGY_L2SQ: return launch_logits_tr<D, CRL_ENERGY_L2SQ, GRAD>(p, st);
   }
   return cudaErrorInvalidValue;
 }

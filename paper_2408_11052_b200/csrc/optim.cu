@@ -54,12 +54,14 @@ __global__ void __launch_bounds__(256) loss_partial_kernel(
     float x = 0.f, na = 0.f, nb = 0.f;
     for (int k = lane; k < D; k += 32) {
       const float av = a[k], bv = b[k];
-      if (energy == CRL_ENERGY_L2) { const float d = av - bv; x = fmaf(d, d, x); }
+      if (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_L2SQ) { const float d = av - bv; x = fmaf(d, d, x); }
+      else if (energy == CRL_ENERGY_L1) x += fabsf(av - bv);
       else { x = fmaf(av, bv, x); na = fmaf(av, av, na); nb = fmaf(bv, bv, nb); }
     }
     x = warp_sum(x);
     float l;
     if (energy == CRL_ENERGY_L2) l = -sqrtf(x + kEpsL2);
+    else if (energy == CRL_ENERGY_L2SQ || energy == CRL_ENERGY_L1) l = -x;
     else if (energy == CRL_ENERGY_DOT) l = x;
     else {
       na = warp_sum(na); nb = warp_sum(nb);

@@ -69,6 +69,8 @@ def _run(cfg, alpha, seed=5, clip_bias=False, steps=1):
     ("ant", "dot", "silu", 0.0),         # alpha = 0: random-goal setting (App. C)
     ("ant", "cos", "relu", 0.05),
     ("humanoid", "l2", "silu", 0.1),     # obs 268, act 17 (wide first layers, ragged tiles)
+    ("reacher", "l1", "silu", 0.1),      # F3 energies
+    ("ant", "l2sq", "relu", 0.05),
 ])
 def test_actor_loss_parity(preset, energy, act, alpha):
     cfg = crl_synth.preset(preset, energy=energy, activation=act)

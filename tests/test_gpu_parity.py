@@ -153,6 +153,28 @@ def test_critic_step_fp32_small(energy, loss):
     _critic_parity(cfg)
 
 
+@pytest.mark.parametrize("energy", ["l1", "l2sq"])
+@pytest.mark.parametrize("loss", ["fwd", "bwd", "sym"])
+def test_critic_step_fp32_f3_energies(energy, loss):
+    """L1 and L2-without-sqrt energies (App. A.2) on the fp32
+    path, same bar as the other energies (ragged batch, several column tiles)."""
+    cfg = crl_synth.preset("reacher", batch=200, width=64, energy=energy, loss=loss)
+    _critic_parity(cfg)
+
+
+def test_critic_step_f3_energies_repr256_ant():
+    cfg = crl_synth.preset("ant", precision="fp32", batch=130, repr_dim=256, energy="l1")
+    _critic_parity(cfg)
+
+
+@pytest.mark.parametrize("energy", ["l1", "l2sq"])
+def test_f3_energies_bf16_unsupported(energy):
+    from paper_2408_11052_b200 import CrlError
+    cfg = crl_synth.preset("reacher", precision="bf16", batch=64, energy=energy)
+    with pytest.raises(CrlError):
+        make_ctx(cfg)
+
+
 @pytest.mark.parametrize("B", [2, 3, 65, 130])
 def test_critic_step_fp32_ragged(B):
     cfg = crl_synth.preset("reacher", batch=B, width=96, depth=3, beta_lse=0.0)

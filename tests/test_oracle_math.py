@@ -11,7 +11,7 @@ import pytest
 
 from oracle import adam, critic, energy, losses, mlp
 
-ENERGIES = ["l2", "dot", "cos"]
+ENERGIES = ["l2", "dot", "cos", "l1", "l2sq"]
 KINDS = ["fwd", "bwd", "sym"]
 
 
@@ -307,3 +307,45 @@ def test_entropy_update_gradient_finite_difference():
     f = lambda x: critic.entropy_update(log_pi, x, 0, 0, 0, target_entropy=H, lr=1e-30)["loss"]
     fd = (f(la + h) - f(la - h)) / (2 * h)
     assert f(la) == pytest.approx(fd, rel=1e-8)
+
+
+# ------------------------------------------------------------------ F3 energies (L1, L2 w/o sqrt)
+
+def test_l2sq_and_l1_logits_closed_forms():
+    """App. A.2 P:612/P:616 on integer vectors: -||x - y||_2^2 and -||x - y||_1 by hand."""
+    phi = np.array([[1.0, 2.0, -1.0], [0.0, 0.0, 0.0]])
+    psi = np.array([[0.0, 4.0, 1.0], [1.0, 1.0, 1.0], [-2.0, 2.0, 0.5]])
+    l2sq = energy.logits("l2sq", phi, psi)
+    l1 = energy.logits("l1", phi, psi)
+    assert l2sq[0, 0] == -(1 + 4 + 4) and l2sq[1, 1] == -3 and l2sq[0, 2] == -(9 + 0 + 2.25)
+    assert l1[0, 0] == -(1 + 2 + 2) and l1[1, 1] == -3 and l1[0, 2] == -(3 + 0 + 1.5)
+    # L2sq is the square of the L2 distance (up to the L2 epsilon)
+    l2 = energy.logits("l2", phi, psi)
+    assert np.allclose(-l2sq, l2 ** 2 - energy.EPS_L2, rtol=1e-12, atol=1e-12)
+    assert np.allclose(energy.diag_logits("l1", phi, psi[:2]), np.diag(l1[:, :2]))
+    assert np.allclose(energy.diag_logits("l2sq", phi, psi[:2]), np.diag(l2sq[:, :2]))
+
+
+@pytest.mark.parametrize("kind", ["l1", "l2sq"])
+def test_l1_l2sq_vjp_finite_differences(kind):
+    """The VJPs of the F3 energies against central differences of sum(G * logits) (random
+    points: no L1 ties within the step)."""
+    rng = np.random.default_rng(3)
+    phi = rng.standard_normal((5, 4)); psi = rng.standard_normal((6, 4)); G = rng.standard_normal((5, 6))
+    dphi, dpsi = energy.vjp(kind, phi, psi, G)
+    f = lambda P, Q: float((G * energy.logits(kind, P, Q)).sum())
+    h = 1e-6
+    for (i, k) in [(0, 0), (2, 3), (4, 1)]:
+        e = np.zeros_like(phi); e[i, k] = h
+        assert (f(phi + e, psi) - f(phi - e, psi)) / (2 * h) == pytest.approx(dphi[i, k], rel=1e-6, abs=1e-8)
+    for (j, k) in [(0, 1), (5, 2), (3, 0)]:
+        e = np.zeros_like(psi); e[j, k] = h
+        assert (f(phi, psi + e) - f(phi, psi - e)) / (2 * h) == pytest.approx(dpsi[j, k], rel=1e-6, abs=1e-8)
+
+
+def test_l1_subgradient_at_ties_is_zero():
+    """Reading A-33: at phi_k == psi_k the L1 derivative is taken as 0."""
+    phi = np.array([[1.0, 2.0]]); psi = np.array([[1.0, 0.0]])
+    dphi, dpsi = energy.vjp("l1", phi, psi, np.ones((1, 1)))
+    assert dphi[0, 0] == 0.0 and dpsi[0, 0] == 0.0
+    assert dphi[0, 1] == -1.0 and dpsi[0, 1] == 1.0
