@@ -21,7 +21,9 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 """
 import numpy as np
 
-LOSS_COEF = {"fwd": (1.0, 0.0), "bwd": (0.0, 1.0), "sym": (1.0, 1.0)}
+LOSS_COEF = {"fwd": (1.0, 0.0), "bwd": (0.0, 1.0), "sym": (1.0, 1.0),
+             "flatnce_fwd": (1.0, 0.0), "flatnce_bwd": (0.0, 1.0)}
+FLAT = ("flatnce_fwd", "flatnce_bwd")
 
 
 def lse_rows(l):
@@ -50,5 +52,26 @@ def loss_and_grad(l, kind="sym", beta=0.1):
     q = np.exp(l - lsec[None, :])
     I = np.eye(N)
     G = (cf * (p - I) + cb * (q - I)) / N + (2.0 * beta / N) * lse[:, None] * p
+    if kind in FLAT:
+        # FlatNCE (reading A-24): L = (1/N) sum_i log(S_i / sg[S_i]) with
+        # S_i = sum_j exp(l_ij - l_ii): value 0; its gradient, written out,
+        #   dL/dl_ij = (1/N) exp(l_ij - l_ii) / S_i = p_ij / N (j != i),
+        #   dL/dl_ii = -(1/N) (S_i - 1) / S_i = (p_ii - 1) / N,
+        # is the InfoNCE gradient above (bwd: the same with columns)
+        L_fwd = 0.0
+        L_bwd = 0.0
+        total = P
     comps = dict(L_fwd=L_fwd, L_bwd=L_bwd, penalty=P, total=total, lse_row=lse, lse_col=lsec)
     return comps, G
+
+
+def flatnce_literal(l, l_detached, kind="flatnce_fwd"):
+    """The printed FlatNCE objective with an explicit stop-gradient argument (A-24 sign):
+    (1/N) sum_i log(S_i(l) / S_i(l_detached)), S_i = sum_j exp(l_ij - l_ii); columns for bwd.
+    Used by the tests to pin the gradient above by finite differences."""
+    l = np.asarray(l, np.float64); l0 = np.asarray(l_detached, np.float64)
+    if kind == "flatnce_bwd":
+        l, l0 = l.T, l0.T
+    d = np.diag(l)[:, None]; d0 = np.diag(l0)[:, None]
+    S = np.exp(l - d).sum(1); S0 = np.exp(l0 - d0).sum(1)
+    return float(np.mean(np.log(S / S0)))

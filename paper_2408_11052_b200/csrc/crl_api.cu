@@ -250,7 +250,7 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
   if (k->energy < 0 || k->energy > 4) return fail(ctx, CRL_EINVAL, "energy");
   if (k->precision == CRL_BF16 && k->energy > CRL_ENERGY_COS)
     return fail(ctx, CRL_EUNSUPPORTED, "L1 / L2SQ energies run on the fp32 path only");
-  if (k->loss < 0 || k->loss > 2) return fail(ctx, CRL_EINVAL, "loss");
+  if (k->loss < 0 || k->loss > 4) return fail(ctx, CRL_EINVAL, "loss");
   if (k->precision != CRL_FP32 && k->precision != CRL_BF16) return fail(ctx, CRL_EINVAL, "precision");
   if (k->precision == CRL_BF16 && (k->width % 16 != 0))
     return fail(ctx, CRL_EUNSUPPORTED, "bf16 path needs width % 16 == 0");
@@ -550,8 +550,13 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
   const crl_config& k = ctx->cfg;
   const int Bl = k.batch_local, W = k.world_size, N = ctx->N, D = k.repr_dim;
   const float invN = 1.0f / (float)N;
-  const float c_f = (k.loss == CRL_LOSS_BWD) ? 0.f : 1.f;
-  const float c_b = (k.loss == CRL_LOSS_FWD) ? 0.f : 1.f;
+  // (c_f, c_b): fwd / FlatNCE-fwd (1, 0), bwd / FlatNCE-bwd (0, 1), sym (1, 1); the loss
+  // kernels get them negated for FlatNCE (reported value 0, reading A-24)
+  const bool bwd_only = k.loss == CRL_LOSS_BWD || k.loss == CRL_LOSS_FLATNCE_BWD;
+  const bool fwd_only = k.loss == CRL_LOSS_FWD || k.loss == CRL_LOSS_FLATNCE_FWD;
+  const float c_f = bwd_only ? 0.f : 1.f;
+  const float c_b = fwd_only ? 0.f : 1.f;
+  const float lsgn = (k.loss == CRL_LOSS_FLATNCE_FWD || k.loss == CRL_LOSS_FLATNCE_BWD) ? -1.f : 1.f;
   int nl = 0;
   crl_status rs;
   // A2: encoders forward (phi on st, psi on st2)
@@ -584,12 +589,12 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
   }
   { Stage sg(ctx, st, "loss");
     CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,
-                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, W == 1, invN, c_f, c_b, k.beta_lse, loss_out, ctx->skip,
+                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, W == 1, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip,
                            ctx->adam_t, ctx->status, st));
     ++nl; }
   if (W > 1) {
     NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
-    CU(launch_loss_finalize(ctx->loss_acc, invN, c_f, c_b, k.beta_lse, loss_out, ctx->skip,
+    CU(launch_loss_finalize(ctx->loss_acc, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip,
                             ctx->adam_t, ctx->status, st));
     ++nl;
   }

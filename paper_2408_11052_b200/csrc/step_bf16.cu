@@ -351,8 +351,13 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   const crl_config& k = ctx->cfg;
   const int Bl = k.batch_local, W = k.world_size, N = ctx->N, D = k.repr_dim;
   const float invN = 1.0f / (float)N;
-  const float c_f = (k.loss == CRL_LOSS_BWD) ? 0.f : 1.f;
-  const float c_b = (k.loss == CRL_LOSS_FWD) ? 0.f : 1.f;
+  // (c_f, c_b): fwd / FlatNCE-fwd (1, 0), bwd / FlatNCE-bwd (0, 1), sym (1, 1); the loss
+  // kernels get them negated for FlatNCE (reported value 0, reading A-24)
+  const bool bwd_only = k.loss == CRL_LOSS_BWD || k.loss == CRL_LOSS_FLATNCE_BWD;
+  const bool fwd_only = k.loss == CRL_LOSS_FWD || k.loss == CRL_LOSS_FLATNCE_FWD;
+  const float c_f = bwd_only ? 0.f : 1.f;
+  const float c_b = fwd_only ? 0.f : 1.f;
+  const float lsgn = (k.loss == CRL_LOSS_FLATNCE_FWD || k.loss == CRL_LOSS_FLATNCE_BWD) ? -1.f : 1.f;
   int nl = 0;
   crl_status rs;
   const int row_off = k.rank * Bl;
@@ -496,15 +501,15 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   if (ctx->use_gradf) {
     gl.phi32 = ctx->phi_out; gl.psi32 = ctx->psi_out; gl.part = ctx->loss_part; gl.ticket = ctx->loss_ticket;
     gl.acc = ctx->loss_acc; gl.out = loss_out; gl.skip = ctx->skip; gl.adam_t = ctx->adam_t; gl.status = ctx->status;
-    gl.c_f = c_f; gl.c_b = c_b; gl.beta = k.beta_lse;
+    gl.c_f = lsgn * c_f; gl.c_b = lsgn * c_b; gl.beta = k.beta_lse;
   } else { Stage sg(ctx, st, "loss");
     CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,
-                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, W == 1, invN, c_f, c_b,
+                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, W == 1, invN, lsgn * c_f, lsgn * c_b,
                            k.beta_lse, loss_out, ctx->skip, ctx->adam_t, ctx->status, st));
     ++nl; }
   if (W > 1) {
     NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
-    CU(launch_loss_finalize(ctx->loss_acc, invN, c_f, c_b, k.beta_lse, loss_out, ctx->skip, ctx->adam_t,
+    CU(launch_loss_finalize(ctx->loss_acc, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip, ctx->adam_t,
                             ctx->status, st));
     ++nl;
   }

@@ -178,8 +178,12 @@ __device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t) {
   *p.loss_ticket = 0u;
   p.loss_acc[0] = t1; p.loss_acc[1] = t2; p.loss_acc[2] = t3;
   const float Lf = t1 * p.invN, Lb = t2 * p.invN, P = p.loss_beta * t3 * p.invN;
-  const float tot = p.loss_cf * Lf + p.loss_cb * Lb + P;
-  if (p.loss_out) { p.loss_out[0] = Lf; p.loss_out[1] = Lb; p.loss_out[2] = P; p.loss_out[3] = tot; }
+  const bool flat = p.loss_cf < 0.f || p.loss_cb < 0.f;        // FlatNCE: see optim.cu
+  const float tot = fabsf(p.loss_cf) * Lf + fabsf(p.loss_cb) * Lb + P;
+  if (p.loss_out) {
+    p.loss_out[0] = flat ? 0.f : Lf; p.loss_out[1] = flat ? 0.f : Lb; p.loss_out[2] = P;
+    p.loss_out[3] = flat ? P : tot;
+  }
   const bool bad = !isfinite(tot);
   *p.skip = bad ? 1 : 0;
   if (bad) set_status(p.status, CRL_ENONFINITE);

@@ -281,6 +281,19 @@ def test_critic_step_bf16_tc_logits(energy, loss):
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
 
 
+@pytest.mark.parametrize("loss", ["flatnce_fwd", "flatnce_bwd"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_critic_step_flatnce(loss, precision):
+    """F3 FlatNCE (reading A-24): InfoNCE gradient, reported L_fwd = L_bwd = 0 and total =
+    the logsumexp penalty, on both precisions."""
+    if precision == "fp32":
+        cfg = crl_synth.preset("reacher", batch=200, width=64, loss=loss)
+        _critic_parity(cfg)
+    else:
+        cfg = crl_synth.preset("ant", batch=1100, width=128, loss=loss, precision="bf16")
+        _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
 def test_critic_step_bf16_tc_logits_repr256():
     cfg = crl_synth.preset("ant", batch=1536, width=128, repr_dim=256, precision="bf16", beta_lse=0.3)
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)

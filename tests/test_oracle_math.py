@@ -349,3 +349,28 @@ def test_l1_subgradient_at_ties_is_zero():
     dphi, dpsi = energy.vjp("l1", phi, psi, np.ones((1, 1)))
     assert dphi[0, 0] == 0.0 and dpsi[0, 0] == 0.0
     assert dphi[0, 1] == -1.0 and dpsi[0, 1] == 1.0
+
+
+# ------------------------------------------------------------------ F3 FlatNCE (reading A-24)
+
+@pytest.mark.parametrize("kind", ["flatnce_fwd", "flatnce_bwd"])
+def test_flatnce_value_zero_and_gradient_of_literal_formula(kind):
+    """The printed FlatNCE objective with the stop-gradient held at the evaluation point: its
+    value there is 0 and its finite-difference gradient equals the oracle's G (independent of
+    the InfoNCE closed form it coincides with)."""
+    rng = np.random.default_rng(21)
+    l = rng.standard_normal((5, 5))
+    comps, G = losses.loss_and_grad(l, kind, beta=0.0)
+    assert comps["L_fwd"] == 0.0 and comps["L_bwd"] == 0.0 and comps["total"] == 0.0
+    assert losses.flatnce_literal(l, l, kind) == 0.0
+    fd = fd_grad(lambda x: losses.flatnce_literal(x, l, kind), l)
+    assert rel_err(G, fd) < 1e-7
+    # and it is the InfoNCE gradient of the same direction
+    _, Gi = losses.loss_and_grad(l, "fwd" if kind == "flatnce_fwd" else "bwd", beta=0.0)
+    assert np.allclose(G, Gi, rtol=0, atol=1e-15)
+
+
+def test_flatnce_penalty_only_total():
+    l = np.random.default_rng(2).standard_normal((4, 4))
+    c, _ = losses.loss_and_grad(l, "flatnce_fwd", beta=0.1)
+    assert c["total"] == c["penalty"] > 0.0
