@@ -66,13 +66,18 @@ typedef enum {
  * L2SQ: f = -||phi - psi||_2^2 ("L2 w/o sqrt").  L1 and L2SQ run on
  * the fp32 path (critic and actor); a bf16 context with them is CRL_EUNSUPPORTED. */
 typedef enum {
-  CRL_LOSS_FWD = 0, CRL_LOSS_BWD = 1, CRL_LOSS_SYM = 2, CRL_LOSS_FLATNCE_FWD = 3, CRL_LOSS_FLATNCE_BWD = 4
+  CRL_LOSS_FWD = 0, CRL_LOSS_BWD = 1, CRL_LOSS_SYM = 2, CRL_LOSS_FLATNCE_FWD = 3, CRL_LOSS_FLATNCE_BWD = 4,
+  CRL_LOSS_FB = 5, CRL_LOSS_DPO = 6, CRL_LOSS_IPO = 7, CRL_LOSS_SPPO = 8
 } crl_loss;
 /* InfoNCE forward / backward / symmetric = fwd + bwd (App. A.2).
  * FlatNCE fwd / bwd: L = (1/N) sum_i log(S_i / sg[S_i]),
  * S_i = sum_j exp(l_ij - l_ii) (sign per reading A-24): its value is 0 and its gradient is
  * exactly the InfoNCE fwd / bwd gradient, so it runs the InfoNCE kernels and reports
- * L_fwd = L_bwd = 0, total = the logsumexp penalty.  Both precisions. */
+ * L_fwd = L_bwd = 0, total = the logsumexp penalty.  Both precisions.
+ * FB, DPO, IPO, SPPO (readings A-03 mean over the N positives,
+ * A-34 j ranges as printed): no logsumexp in the objective (the row-LSE penalty still
+ * applies); loss_out = (L_pair, 0, penalty, total).  fp32 and world_size 1 only, else
+ * CRL_EUNSUPPORTED at create. */
 typedef enum { CRL_ACT_SILU = 0, CRL_ACT_RELU = 1 } crl_activation;
 typedef enum { CRL_FP32 = 0, CRL_BF16 = 1 } crl_precision;
 /* FP32: SIMT fp32 arithmetic end to end.  BF16: bf16 GEMM operands on the tcgen05 tensor

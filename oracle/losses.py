@@ -40,6 +40,15 @@ def loss_and_grad(l, kind="sym", beta=0.1):
     """Returns (dict of components, G = dL/dl)."""
     l = np.asarray(l, np.float64)
     N = l.shape[0]
+    if kind in PAIRWISE:
+        # pair / FB objectives (F3) + the same row logsumexp penalty (reading A-05)
+        lse = lse_rows(l)
+        P = beta * np.mean(lse ** 2)
+        Lp = pairwise_loss(l, kind)
+        p = np.exp(l - lse[:, None])
+        G = pairwise_grad(l, kind) + (2.0 * beta / N) * lse[:, None] * p
+        comps = dict(L_fwd=Lp, L_bwd=0.0, penalty=P, total=Lp + P, lse_row=lse, lse_col=lse_cols(l))
+        return comps, G
     cf, cb = LOSS_COEF[kind]
     lse = lse_rows(l)
     lsec = lse_cols(l)
@@ -63,6 +72,62 @@ def loss_and_grad(l, kind="sym", beta=0.1):
         total = P
     comps = dict(L_fwd=L_fwd, L_bwd=L_bwd, penalty=P, total=total, lse_row=lse, lse_col=lsec)
     return comps, G
+
+
+PAIRWISE = ("fb", "dpo", "ipo", "sppo")
+
+
+def pairwise_loss(l, kind):
+    """The pair / FB objectives of App. A.2 P:643-658 written out, mean over the N positives
+    (reading A-03: 1/N for the double sums as for InfoNCE; reading A-34: the printed j-range,
+    j = 1..N including j = i, except FB's j != i).  d_i = l_ii.
+      FB  : (1/N) [ -sum_i e^{d_i} + (1/(2(N-1))) sum_i sum_{j!=i} e^{2 l_ij} ]
+      DPO : (1/N) sum_i sum_j -log sigmoid(d_i - l_ij)
+      IPO : (1/N) sum_i sum_j ((d_i - l_ij) - 1)^2
+      SPPO: (1/N) sum_i sum_j [(d_i - 1)^2 + (l_ij + 1)^2]"""
+    l = np.asarray(l, np.float64)
+    N = l.shape[0]
+    d = np.diag(l)
+    off = ~np.eye(N, dtype=bool)
+    if kind == "fb":
+        return (-np.exp(d).sum() + (np.exp(2.0 * l)[off]).sum() / (2.0 * max(N - 1, 1))) / N
+    if kind == "dpo":
+        return np.logaddexp(0.0, l - d[:, None]).sum() / N             # -log sigmoid(x) = log(1 + e^-x)
+    if kind == "ipo":
+        return (((d[:, None] - l) - 1.0) ** 2).sum() / N
+    if kind == "sppo":
+        return (N * ((d - 1.0) ** 2).sum() + ((l + 1.0) ** 2).sum()) / N
+    raise ValueError(kind)
+
+
+def pairwise_grad(l, kind):
+    """dL/dl of pairwise_loss, derived by hand (pinned by finite differences in the tests):
+      off-diagonal g_ij = h(l_ij, d_i) / N, diagonal g_ii = D_i / N with
+      FB  : h = e^{2l} / (N-1),        D_i = -e^{d_i}
+      DPO : h = sigmoid(l - d),        D_i = -sum_{j!=i} h_ij
+      IPO : h = 2 (l - d + 1),         D_i = -sum_{j!=i} h_ij
+      SPPO: h = 2 (l + 1),             D_i = 2 (d_i + 1) + 2 N (d_i - 1)"""
+    l = np.asarray(l, np.float64)
+    N = l.shape[0]
+    d = np.diag(l)
+    off = ~np.eye(N, dtype=bool)
+    if kind == "fb":
+        h = np.exp(2.0 * l) / max(N - 1, 1)
+        D = -np.exp(d)
+    elif kind == "dpo":
+        h = 1.0 / (1.0 + np.exp(-(l - d[:, None])))
+        D = -np.where(off, h, 0.0).sum(1)
+    elif kind == "ipo":
+        h = 2.0 * (l - d[:, None] + 1.0)
+        D = -np.where(off, h, 0.0).sum(1)
+    elif kind == "sppo":
+        h = 2.0 * (l + 1.0)
+        D = 2.0 * (d + 1.0) + 2.0 * N * (d - 1.0)
+    else:
+        raise ValueError(kind)
+    G = np.where(off, h, 0.0)
+    G[np.arange(N), np.arange(N)] = D
+    return G / N
 
 
 def flatnce_literal(l, l_detached, kind="flatnce_fwd"):

@@ -18,7 +18,8 @@ CRL_OK, CRL_EINVAL, CRL_ESTATE, CRL_ECUDA, CRL_ENCCL, CRL_ENONFINITE, CRL_ESAMPL
 STATUS_NAMES = ["CRL_OK", "CRL_EINVAL", "CRL_ESTATE", "CRL_ECUDA", "CRL_ENCCL", "CRL_ENONFINITE",
                 "CRL_ESAMPLER", "CRL_EUNSUPPORTED"]
 ENERGY = {"l2": 0, "dot": 1, "cos": 2, "l1": 3, "l2sq": 4}
-LOSS = {"fwd": 0, "bwd": 1, "sym": 2, "flatnce_fwd": 3, "flatnce_bwd": 4}
+LOSS = {"fwd": 0, "bwd": 1, "sym": 2, "flatnce_fwd": 3, "flatnce_bwd": 4, "fb": 5, "dpo": 6, "ipo": 7,
+        "sppo": 8}
 ACT = {"silu": 0, "relu": 1}
 PRECISION = {"fp32": 0, "bf16": 1}
 

@@ -183,6 +183,11 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     c->dz_psi[1] = s.take<float>((size_t)Bl * wmax);
   }
   c->loss_acc = s.take<float>(16);
+  if (k.loss >= CRL_LOSS_FB) {
+    c->pair_d = s.take<float>((size_t)Bl + kStatPad);
+    c->pair_R = s.take<float>((size_t)Bl + kStatPad);
+    c->pair_L = s.take<float>((size_t)Bl + kStatPad);
+  }
   c->loss_part = s.take<float>((size_t)4 * loss_partial_blocks(Bl));
   c->loss_ticket = s.take<unsigned>(1);
   c->loss_dev = s.take<float>(4);
@@ -250,7 +255,9 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
   if (k->energy < 0 || k->energy > 4) return fail(ctx, CRL_EINVAL, "energy");
   if (k->precision == CRL_BF16 && k->energy > CRL_ENERGY_COS)
     return fail(ctx, CRL_EUNSUPPORTED, "L1 / L2SQ energies run on the fp32 path only");
-  if (k->loss < 0 || k->loss > 4) return fail(ctx, CRL_EINVAL, "loss");
+  if (k->loss < 0 || k->loss > 8) return fail(ctx, CRL_EINVAL, "loss");
+  if (k->loss >= CRL_LOSS_FB && (k->precision != CRL_FP32 || k->world_size != 1))
+    return fail(ctx, CRL_EUNSUPPORTED, "FB / DPO / IPO / SPPO run on the fp32 path with world_size 1");
   if (k->precision != CRL_FP32 && k->precision != CRL_BF16) return fail(ctx, CRL_EINVAL, "precision");
   if (k->precision == CRL_BF16 && (k->width % 16 != 0))
     return fail(ctx, CRL_EUNSUPPORTED, "bf16 path needs width % 16 == 0");
@@ -559,6 +566,7 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
   const float lsgn = (k.loss == CRL_LOSS_FLATNCE_FWD || k.loss == CRL_LOSS_FLATNCE_BWD) ? -1.f : 1.f;
   int nl = 0;
   crl_status rs;
+  const bool pair = k.loss >= CRL_LOSS_FB;        // F3 pair / FB losses (W = 1, fp32)
   // A2: encoders forward (phi on st, psi on st2)
   fork(ctx, st, st2);
   rs = enc_forward(ctx, "psi", ctx->psi_plan, g, k.goal_dim, nullptr, 0, 0, ctx->psiX, ctx->psiZ,
@@ -586,6 +594,39 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
     NC(ncclAllGather(ctx->lse_row, ctx->lse_row_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
     NC(ncclAllGather(ctx->lse_col, ctx->lse_col_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
     NC(ncclGroupEnd());
+  }
+  if (pair) {
+    // d_i = l_ii, per-row pair sums, the loss; then both sides of the gradient
+    { Stage sg(ctx, st, "pair_stats");
+      CU(launch_pair_diag(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->pair_d, st)); ++nl;
+      CU(logits_pair_stats_f32(D, k.energy, k.loss, ctx->phi_out, Bl, 0, ctx->psi_out, N, ctx->pair_d,
+                               ctx->pair_R, ctx->pair_L, st)); ++nl; }
+    { Stage sg(ctx, st, "loss");
+      CU(launch_pair_loss(ctx->pair_L, ctx->pair_d, ctx->lse_row, Bl, k.loss, invN, k.beta_lse, loss_out,
+                          ctx->loss_acc, ctx->skip, ctx->adam_t, ctx->status, st)); ++nl; }
+    fork(ctx, st, st2);
+    { Stage sg(ctx, st2, "grad_psi");
+      CU(logits_pair_grad_f32(D, k.energy, k.loss, 1, ctx->psi_out, Bl, 0, ctx->phi_out, N, ctx->pair_d,
+                              ctx->pair_R, ctx->lse_row, k.beta_lse, invN, ctx->dpsi, st2)); ++nl; }
+    rs = enc_backward(ctx, "psi", ctx->psi_plan, g, k.goal_dim, nullptr, 0, 0, ctx->psiX, ctx->psiZ,
+                      ctx->dpsi, ctx->dz_psi, st2, &nl);
+    if (rs != CRL_OK) return rs;
+    { Stage sg(ctx, st, "grad_phi");
+      CU(logits_pair_grad_f32(D, k.energy, k.loss, 0, ctx->phi_out, Bl, 0, ctx->psi_out, N, ctx->pair_d,
+                              ctx->pair_R, ctx->lse_row, k.beta_lse, invN, ctx->dphi, st)); ++nl; }
+    rs = enc_backward(ctx, "phi", ctx->phi_plan, s, k.obs_dim, a, k.act_dim, k.obs_dim, ctx->phiX,
+                      ctx->phiZ, ctx->dphi, ctx->dz, st, &nl);
+    if (rs != CRL_OK) return rs;
+    join(ctx, st, st2);
+    { Stage sg(ctx, st, "adam");
+      CU(launch_adam(ctx->mem.params, ctx->grads, ctx->dw_splits, ctx->mem.adam_m, ctx->mem.adam_v,
+                     ctx->sizes.n_params, k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay,
+                     ctx->adam_t, ctx->skip, ctx->status, nullptr, ctx->num_sms, st));
+      ++nl; }
+    if (grads_out)
+      CU(cudaMemcpyAsync(grads_out, ctx->grads, ctx->sizes.n_params * 4, cudaMemcpyDeviceToDevice, st));
+    ctx->launches = nl;
+    return CRL_OK;
   }
   { Stage sg(ctx, st, "loss");
     CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,

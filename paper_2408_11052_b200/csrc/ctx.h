@@ -40,6 +40,13 @@ cudaError_t launch_loss_partial(const float*, const float*, int, int, int, const
                                 const float*, float*, float*, unsigned*, int, float, float, float,
                                 float, float*, int*, int*, int*, cudaStream_t);
 int loss_partial_blocks(int Bl);
+cudaError_t launch_pair_diag(const float*, const float*, int, int, int, float*, cudaStream_t);
+cudaError_t launch_pair_loss(const float*, const float*, const float*, int, int, float, float, float*, float*, int*,
+                             int*, int*, cudaStream_t);
+cudaError_t logits_pair_stats_f32(int, int, int, const float*, int, int, const float*, int, const float*, float*,
+                                  float*, cudaStream_t);
+cudaError_t logits_pair_grad_f32(int, int, int, int, const float*, int, int, const float*, int, const float*,
+                                 const float*, const float*, float, float, float*, cudaStream_t);
 cudaError_t launch_loss_finalize(const float*, float, float, float, float, float*, int*, int*,
                                  int*, cudaStream_t);
 cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, float, float, float,
@@ -106,6 +113,7 @@ struct crl_ctx {
   float *lse_row = nullptr, *lse_col = nullptr, *lse_row_g = nullptr, *lse_col_g = nullptr;
   float *dphi = nullptr, *dpsi = nullptr, *dz[2] = {nullptr, nullptr}, *dz_psi[2] = {nullptr, nullptr};
   float *loss_acc = nullptr, *loss_dev = nullptr, *loss_part = nullptr;
+  float *pair_d = nullptr, *pair_R = nullptr, *pair_L = nullptr;   // F3 pair losses [B_l]
   unsigned* loss_ticket = nullptr;
   int *status = nullptr, *adam_t = nullptr, *skip = nullptr;
   float *stage_s = nullptr, *stage_a = nullptr, *stage_g = nullptr;

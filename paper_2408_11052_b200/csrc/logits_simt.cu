@@ -36,8 +36,43 @@ struct LogitsArgs {
   const float* lr;                          // grad: row statistic [Na]
   const float* lc;                          // grad: column statistic [Nb]
   float c_r, c_c, beta_r, beta_c, invN;
-  float* out;                               // lse: [Na]; grad: dA [Na][D]
+  float* out;                               // lse: [Na]; grad: dA [Na][D]; pair stats: R [Na]
+  // pairwise / FB losses (F3): per-PHI-index statistics (rows for orient 0, columns for 1)
+  const float* pd = nullptr;                // diagonal l_kk
+  const float* pR = nullptr;                // sum_{j != k} h(l_kj, d_k)      (DPO, IPO)
+  const float* plse = nullptr;              // row logsumexp (penalty term)
+  int orient = 0, loss = 0, Ntot = 0;
+  float inv_nm1 = 0.f;                      // 1 / (N - 1)
+  float* out2 = nullptr;                    // pair stats: per-row loss sums [Na]
 };
+
+// pairwise / FB losses (oracle/losses.py pairwise_grad): off-diagonal g = h / N, diagonal D / N
+__device__ __forceinline__ float pair_h(int loss, float l, float d, float inv_nm1) {
+  switch (loss) {
+    case CRL_LOSS_FB: return __expf(2.f * l) * inv_nm1;
+    case CRL_LOSS_DPO: return 1.f / (1.f + __expf(d - l));
+    case CRL_LOSS_IPO: return 2.f * (l - d + 1.f);
+    default: return 2.f * (l + 1.f);                              // SPPO
+  }
+}
+__device__ __forceinline__ float pair_diag(int loss, float d, float R, int N) {
+  switch (loss) {
+    case CRL_LOSS_FB: return -__expf(d);
+    case CRL_LOSS_DPO:
+    case CRL_LOSS_IPO: return -R;
+    default: return 2.f * (d + 1.f) + 2.f * (float)N * (d - 1.f);  // SPPO
+  }
+}
+// the loss contribution of pair (i, j) (per-row extras -e^{d_i} (FB), N (d_i - 1)^2 (SPPO) are
+// added by the loss kernel)
+__device__ __forceinline__ float pair_term(int loss, float l, float d, bool diag, float inv_nm1) {
+  switch (loss) {
+    case CRL_LOSS_FB: return diag ? 0.f : 0.5f * inv_nm1 * __expf(2.f * l);
+    case CRL_LOSS_DPO: { const float x = l - d; return fmaxf(x, 0.f) + log1pf(__expf(-fabsf(x))); }
+    case CRL_LOSS_IPO: { const float x = d - l - 1.f; return x * x; }
+    default: { const float x = l + 1.f; return x * x; }            // SPPO
+  }
+}
 
 constexpr int TC = 64;                      // columns per tile
 constexpr int BPITCH = TC + 1;
@@ -58,7 +93,7 @@ struct LSmem {
   }
 };
 
-template <int D, int TR, int ENERGY, bool GRAD>
+template <int D, int TR, int ENERGY, bool GRAD, bool PAIR>
 __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
   constexpr int AP = TR + 1;
   constexpr int RI = TR / 16;              // rows per thread
@@ -94,16 +129,21 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
   cpa_commit();
 
   float lr_i[RI];
+  float pd_i[RI], pl_i[RI], pR_i[RI];                     // PAIR: this row's phi-index stats (orient 0)
 #pragma unroll
   for (int i = 0; i < RI; ++i) {
     const int r = a0 + ty + 16 * i;
-    lr_i[i] = (GRAD && r < p.Na) ? p.lr[r] : 0.0f;
+    lr_i[i] = (GRAD && !PAIR && r < p.Na) ? p.lr[r] : 0.0f;
+    const bool own = PAIR && r < p.Na && p.orient == 0;
+    pd_i[i] = own ? p.pd[p.row_offset + r] : 0.f;
+    pl_i[i] = (own && GRAD) ? p.plse[p.row_offset + r] : 0.f;
+    pR_i[i] = (own && GRAD && p.pR) ? p.pR[p.row_offset + r] : 0.f;
   }
   float m_run[RI], s_run[RI], wsum[RI];
   float acc2[RI][GRAD ? DC : 1];
 #pragma unroll
   for (int i = 0; i < RI; ++i) {
-    m_run[i] = -CUDART_INF_F; s_run[i] = 0.f; wsum[i] = 0.f;
+    m_run[i] = PAIR ? 0.f : -CUDART_INF_F; s_run[i] = 0.f; wsum[i] = 0.f;
 #pragma unroll
     for (int c = 0; c < (GRAD ? DC : 1); ++c) acc2[i][c] = 0.f;
   }
@@ -175,7 +215,21 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
         acc[i][j] = v;                    // acc now holds l_ij
       }
 
-    if (!GRAD) {
+    if (PAIR && !GRAD) {
+      // pair statistics of this row: m_run <- sum_{j != i} h, s_run <- sum_j loss term
+#pragma unroll
+      for (int i = 0; i < RI; ++i) {
+        const int ig = p.row_offset + a0 + ty + 16 * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!valid[j]) continue;
+          const int jg = b0 + tx + 16 * j;
+          const bool dg = ig == jg;
+          if (!dg) m_run[i] += pair_h(p.loss, acc[i][j], pd_i[i], p.inv_nm1);
+          s_run[i] += pair_term(p.loss, acc[i][j], pd_i[i], dg, p.inv_nm1);
+        }
+      }
+    } else if (!GRAD) {
 #pragma unroll
       for (int i = 0; i < RI; ++i) {
         float mx = m_run[i];
@@ -199,11 +253,22 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
           float w = 0.f;
           if (valid[j]) {
             const float lv = acc[i][j];
-            const float pe = expf(lv - lr_i[i]);
-            const float qe = expf(lv - lcj);
-            const float dlt = (ig == jg) ? 1.f : 0.f;
-            const float g = p.invN * (p.c_r * (pe - dlt) + p.c_c * (qe - dlt)) +
-                            2.f * p.invN * (p.beta_r * lr_i[i] * pe + p.beta_c * lcj * qe);
+            float g;
+            if (PAIR) {
+              // phi index of the pair: the row (orient 0) or the column (orient 1)
+              const bool o1 = p.orient != 0;
+              const float d = o1 ? p.pd[jg] : pd_i[i];
+              const float ls = o1 ? p.plse[jg] : pl_i[i];
+              const float gp = (ig != jg) ? pair_h(p.loss, lv, d, p.inv_nm1)
+                                          : pair_diag(p.loss, d, o1 ? (p.pR ? p.pR[jg] : 0.f) : pR_i[i], p.Ntot);
+              g = p.invN * gp + 2.f * p.invN * p.beta_r * ls * expf(lv - ls);
+            } else {
+              const float pe = expf(lv - lr_i[i]);
+              const float qe = expf(lv - lcj);
+              const float dlt = (ig == jg) ? 1.f : 0.f;
+              g = p.invN * (p.c_r * (pe - dlt) + p.c_c * (qe - dlt)) +
+                  2.f * p.invN * (p.beta_r * lr_i[i] * pe + p.beta_c * lcj * qe);
+            }
             if (ENERGY == CRL_ENERGY_L2) w = g / (-lv);
             else if (ENERGY == CRL_ENERGY_L2SQ) w = 2.f * g;
             else if (ENERGY == CRL_ENERGY_COS) w = g * nB[buf * TC + tx + 16 * j];
@@ -239,7 +304,19 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
     __syncthreads();                       // buffer `buf` is refilled two tiles later
   }
 
-  if (!GRAD) {
+  if (PAIR && !GRAD) {
+#pragma unroll
+    for (int i = 0; i < RI; ++i) {
+      float R = m_run[i], Lr = s_run[i];
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        R += __shfl_xor_sync(0xffffffffu, R, o);
+        Lr += __shfl_xor_sync(0xffffffffu, Lr, o);
+      }
+      const int r = a0 + ty + 16 * i;
+      if (tx == 0 && r < p.Na) { p.out[r] = R; p.out2[r] = Lr; }
+    }
+  } else if (!GRAD) {
 #pragma unroll
     for (int i = 0; i < RI; ++i) {
       float m = m_run[i], s = s_run[i];
@@ -294,23 +371,23 @@ __global__ void __launch_bounds__(256) logits_rows_kernel(LogitsArgs p) {
 static int g_sms_logits = 148;
 void logits_set_num_sms(int n) { g_sms_logits = n > 0 ? n : 148; }
 
-template <int D, int TR, int ENERGY, bool GRAD>
+template <int D, int TR, int ENERGY, bool GRAD, bool PAIR = false>
 static cudaError_t launch_logits_t(const LogitsArgs& p, cudaStream_t st) {
   const size_t smem = sizeof(float) * LSmem<D, TR>::floats(GRAD);
   static bool attr_set = false;   // per template instance
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(logits_rows_kernel<D, TR, ENERGY, GRAD>,
+    cudaError_t e = cudaFuncSetAttribute(logits_rows_kernel<D, TR, ENERGY, GRAD, PAIR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid((p.Na + TR - 1) / TR);
-  return launch_pdl(logits_rows_kernel<D, TR, ENERGY, GRAD>, grid, dim3(256), smem, st, p);
-  return cudaGetLastError();
+  return launch_pdl(logits_rows_kernel<D, TR, ENERGY, GRAD, PAIR>, grid, dim3(256), smem, st, p);
 }
 
 template <int D, int ENERGY, bool GRAD>
 static cudaError_t launch_logits_tr(const LogitsArgs& p, cudaStream_t st) {
+  if (p.loss >= CRL_LOSS_FB) return launch_logits_t<D, 16, ENERGY, GRAD, true>(p, st);   // F3 pair losses
   if (p.Na >= 64 * g_sms_logits) return launch_logits_t<D, 64, ENERGY, GRAD>(p, st);
   if (p.Na >= 16 * g_sms_logits) return launch_logits_t<D, 32, ENERGY, GRAD>(p, st);
   return launch_logits_t<D, 16, ENERGY, GRAD>(p, st);
@@ -357,6 +434,31 @@ cudaError_t logits_grad_f32(int D, int energy, const float* A, int Na, int row_o
   p.A = A; p.Na = Na; p.row_offset = row_offset; p.B = B; p.Nb = Nb;
   p.lr = lr; p.lc = lc; p.c_r = c_r; p.c_c = c_c; p.beta_r = beta_r; p.beta_c = beta_c;
   p.invN = invN; p.out = dA;
+  return launch_logits_d<true>(D, energy, p, st);
+}
+
+
+
+// F3 pair / FB losses.  Row statistics (orient 0, A = Phi rows, B = Psi): R_i = sum_{j != i}
+// h(l_ij, d_i), Lrow_i = sum_j (loss term); d = the diagonal l_kk (global, [N]).
+cudaError_t logits_pair_stats_f32(int D, int energy, int loss, const float* A, int Na, int row_offset,
+                                  const float* B, int Nb, const float* diag, float* R_out, float* L_out,
+                                  cudaStream_t st) {
+  LogitsArgs p{};
+  p.A = A; p.Na = Na; p.row_offset = row_offset; p.B = B; p.Nb = Nb; p.out = R_out; p.out2 = L_out;
+  p.pd = diag; p.loss = loss; p.Ntot = Nb; p.inv_nm1 = Nb > 1 ? 1.f / (float)(Nb - 1) : 1.f;
+  return launch_logits_d<false>(D, energy, p, st);
+}
+// dA for a pair / FB loss: orient 0: (A, B) = (Phi, Psi); orient 1: (A, B) = (Psi, Phi).
+// diag / R / lse are indexed by the Phi index (global, [N]); beta = the row-LSE penalty weight.
+cudaError_t logits_pair_grad_f32(int D, int energy, int loss, int orient, const float* A, int Na, int row_offset,
+                                 const float* B, int Nb, const float* diag, const float* R, const float* lse,
+                                 float beta, float invN, float* dA, cudaStream_t st) {
+  LogitsArgs p{};
+  p.A = A; p.Na = Na; p.row_offset = row_offset; p.B = B; p.Nb = Nb; p.out = dA;
+  p.pd = diag; p.pR = R; p.plse = lse; p.orient = orient; p.loss = loss; p.Ntot = Nb;
+  p.inv_nm1 = Nb > 1 ? 1.f / (float)(Nb - 1) : 1.f;
+  p.beta_r = beta; p.invN = invN;
   return launch_logits_d<true>(D, energy, p, st);
 }
 

@@ -185,6 +185,86 @@ __global__ void __launch_bounds__(256) adam_kernel(
   if (bad) set_status(status, CRL_ENONFINITE);
 }
 
+// ---------------------------------------------------------------------------------------
+// F3 pair / FB losses (oracle/losses.py pairwise_loss).  d_i = l_ii (warp per row), then one
+// CTA adds the per-row sums in a fixed order:
+//   L_pair = (1/N) sum_i (Lrow_i + extra_i),  extra = -e^{d_i} (FB), N (d_i - 1)^2 (SPPO)
+//   P = beta (1/N) sum_i LSE_i^2,  loss_out = (L_pair, 0, P, L_pair + P)
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) pair_diag_kernel(const float* __restrict__ phi, const float* __restrict__ psi,
+                                                        int Bl, int D, int energy, float* __restrict__ d) {
+  pdl_wait();
+  pdl_launch();
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= Bl) return;
+  const float* a = phi + (size_t)i * D;
+  const float* b = psi + (size_t)i * D;
+  float x = 0.f, na = 0.f, nb = 0.f;
+  for (int k = lane; k < D; k += 32) {
+    const float av = a[k], bv = b[k];
+    if (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_L2SQ) { const float t = av - bv; x = fmaf(t, t, x); }
+    else if (energy == CRL_ENERGY_L1) x += fabsf(av - bv);
+    else { x = fmaf(av, bv, x); na = fmaf(av, av, na); nb = fmaf(bv, bv, nb); }
+  }
+  x = warp_sum(x);
+  float l;
+  if (energy == CRL_ENERGY_L2) l = -sqrtf(x + kEpsL2);
+  else if (energy == CRL_ENERGY_L2SQ || energy == CRL_ENERGY_L1) l = -x;
+  else if (energy == CRL_ENERGY_DOT) l = x;
+  else {
+    na = warp_sum(na); nb = warp_sum(nb);
+    l = x / (fmaxf(sqrtf(na), kEpsCos) * fmaxf(sqrtf(nb), kEpsCos));
+  }
+  if (lane == 0) d[i] = l;
+}
+
+__global__ void __launch_bounds__(1024) pair_loss_kernel(const float* __restrict__ Lrow, const float* __restrict__ d,
+                                                         const float* __restrict__ lse, int Bl, int loss, float invN,
+                                                         float beta, float* __restrict__ loss_out, float* __restrict__ acc,
+                                                         int* __restrict__ skip, int* __restrict__ adam_t,
+                                                         int* __restrict__ status) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ float red[2][32];
+  float s = 0.f, q = 0.f;
+  const float Nf = 1.f / invN;
+  for (int i = threadIdx.x; i < Bl; i += blockDim.x) {
+    float e = Lrow[i];
+    if (loss == CRL_LOSS_FB) e -= expf(d[i]);
+    if (loss == CRL_LOSS_SPPO) e += Nf * (d[i] - 1.f) * (d[i] - 1.f);
+    s += e;
+    q += lse[i] * lse[i];
+  }
+  s = warp_sum(s);
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = s; red[1][threadIdx.x >> 5] = q; }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  float a = threadIdx.x < (blockDim.x >> 5) ? red[0][threadIdx.x] : 0.f;
+  float b = threadIdx.x < (blockDim.x >> 5) ? red[1][threadIdx.x] : 0.f;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (threadIdx.x != 0) return;
+  const float L = a * invN, P = beta * b * invN, tot = L + P;
+  acc[0] = L; acc[1] = 0.f; acc[2] = P;
+  if (loss_out) { loss_out[0] = L; loss_out[1] = 0.f; loss_out[2] = P; loss_out[3] = tot; }
+  const bool bad = !isfinite(tot);
+  *skip = bad ? 1 : 0;
+  if (bad) set_status(status, CRL_ENONFINITE);
+  else *adam_t += 1;
+}
+
+cudaError_t launch_pair_diag(const float* phi, const float* psi, int Bl, int D, int energy, float* d,
+                             cudaStream_t st) {
+  return launch_pdl(pair_diag_kernel, dim3((Bl * 32 + 255) / 256), dim3(256), 0, st, phi, psi, Bl, D, energy, d);
+}
+cudaError_t launch_pair_loss(const float* Lrow, const float* d, const float* lse, int Bl, int loss, float invN,
+                             float beta, float* loss_out, float* acc, int* skip, int* adam_t, int* status,
+                             cudaStream_t st) {
+  return launch_pdl(pair_loss_kernel, dim3(1), dim3(1024), 0, st, Lrow, d, lse, Bl, loss, invN, beta, loss_out, acc,
+                    skip, adam_t, status);
+}
+
 int loss_partial_blocks(int Bl) { return (Bl + kLossRowsPerCta - 1) / kLossRowsPerCta; }
 
 cudaError_t launch_loss_partial(const float* phi, const float* psi, int Bl, int D, int energy,

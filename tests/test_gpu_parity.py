@@ -294,6 +294,25 @@ def test_critic_step_flatnce(loss, precision):
         _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
 
 
+@pytest.mark.parametrize("loss", ["fb", "dpo", "ipo", "sppo"])
+@pytest.mark.parametrize("energy", ["l2", "dot", "cos", "l1", "l2sq"])
+def test_critic_step_fp32_pair_losses(loss, energy):
+    """F3 FB / DPO / IPO / SPPO on the fp32 path: ragged batch over several column
+    tiles, logsumexp penalty on."""
+    cfg = crl_synth.preset("reacher", batch=150, width=64, energy=energy, loss=loss)
+    if loss == "fb" and energy == "dot":
+        cfg["beta_lse"] = 0.0
+    _critic_parity(cfg)
+
+
+@pytest.mark.parametrize("loss", ["fb", "sppo"])
+def test_pair_losses_bf16_or_dp_unsupported(loss):
+    from paper_2408_11052_b200 import CrlError
+    cfg = crl_synth.preset("reacher", precision="bf16", batch=64, loss=loss)
+    with pytest.raises(CrlError):
+        make_ctx(cfg)
+
+
 def test_critic_step_bf16_tc_logits_repr256():
     cfg = crl_synth.preset("ant", batch=1536, width=128, repr_dim=256, precision="bf16", beta_lse=0.3)
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)

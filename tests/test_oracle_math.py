@@ -374,3 +374,37 @@ def test_flatnce_penalty_only_total():
     l = np.random.default_rng(2).standard_normal((4, 4))
     c, _ = losses.loss_and_grad(l, "flatnce_fwd", beta=0.1)
     assert c["total"] == c["penalty"] > 0.0
+
+
+# ------------------------------------------------------------------ F3 pairwise / FB losses
+
+@pytest.mark.parametrize("N", [2, 5])
+def test_pairwise_losses_closed_forms_at_zero_logits(N):
+    """l = 0: DPO = N log 2 (N^2 terms log 2, mean over N), IPO = N, SPPO = 2 N, FB = -1/2."""
+    z = np.zeros((N, N))
+    assert losses.pairwise_loss(z, "dpo") == pytest.approx(N * math.log(2.0), rel=1e-15)
+    assert losses.pairwise_loss(z, "ipo") == pytest.approx(N, rel=1e-15)
+    assert losses.pairwise_loss(z, "sppo") == pytest.approx(2 * N, rel=1e-15)
+    assert losses.pairwise_loss(z, "fb") == pytest.approx(-0.5, rel=1e-15)
+
+
+@pytest.mark.parametrize("kind", ["fb", "dpo", "ipo", "sppo"])
+@pytest.mark.parametrize("beta", [0.0, 0.1])
+def test_pairwise_gradient_finite_differences(kind, beta):
+    rng = np.random.default_rng(7)
+    l = rng.standard_normal((6, 6)) * 0.7
+    comps, G = losses.loss_and_grad(l, kind, beta)
+    fd = fd_grad(lambda x: losses.loss_and_grad(x, kind, beta)[0]["total"], l)
+    assert rel_err(G, fd) < 1e-7
+    assert comps["total"] == pytest.approx(comps["L_fwd"] + comps["penalty"], rel=1e-15)
+
+
+def test_ipo_sppo_minimisers():
+    """IPO is zero exactly when every positive beats every negative by 1 (and the j = i term
+    contributes (0 - 1)^2 = 1 per row); SPPO's off-diagonal part vanishes at l_ij = -1."""
+    N = 4
+    l = -np.ones((N, N)); np.fill_diagonal(l, 0.0)
+    assert losses.pairwise_loss(l, "ipo") == pytest.approx(1.0, rel=1e-15)   # (1/N) * N rows * 1
+    l2 = -np.ones((N, N)); np.fill_diagonal(l2, 1.0)
+    # SPPO: diag (d-1)^2 = 0; (l+1)^2 = 0 off-diagonal, (1+1)^2 = 4 on the diagonal: (1/N) N 4
+    assert losses.pairwise_loss(l2, "sppo") == pytest.approx(4.0, rel=1e-15)
