@@ -138,32 +138,9 @@ struct TcGradFArgs {
 };
 
 // the loss from the statistics (as optim.cu loss_partial / loss_finalize)
-template <int ENERGY>
-__device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t) {
-  constexpr int nthr = 32;
-  float s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  for (int r = t; r < 128; r += nthr) {
-    const int i = a0 + r;
-    if (i >= p.Na) break;
-    const float4* a = reinterpret_cast<const float4*>(p.phi32 + (size_t)i * 64);
-    const float4* b = reinterpret_cast<const float4*>(p.psi32 + (size_t)i * 64);
-    float x = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < 16; ++k) {
-      const float4 u = a[k], v = b[k];
-      if (ENERGY == CRL_ENERGY_L2) {
-        x = fmaf(u.x - v.x, u.x - v.x, x); x = fmaf(u.y - v.y, u.y - v.y, x);
-        x = fmaf(u.z - v.z, u.z - v.z, x); x = fmaf(u.w - v.w, u.w - v.w, x);
-      } else {
-        x = fmaf(u.x, v.x, x); x = fmaf(u.y, v.y, x); x = fmaf(u.z, v.z, x); x = fmaf(u.w, v.w, x);
-      }
-    }
-    const float l = ENERGY == CRL_ENERGY_L2 ? -sqrtf(x + kEpsL2) : x;
-    const float lr = p.lr[i], lc = p.lc[i];
-    s1 += lr - l; s2 += lc - l; s3 += lr * lr;
-  }
-  s1 = warp_sum(s1); s2 = warp_sum(s2); s3 = warp_sum(s3);
-  if (t != 0) return;
+// row block a0 / 128's partial sums -> loss_part; the last row block (ticket) adds them in a
+// fixed order and finalises the loss (as optim.cu loss_finalize)
+__device__ void gradf_loss_finish(const TcGradFArgs& p, int a0, float s1, float s2, float s3) {
   const int rb = a0 / 128, R = (p.Na + 127) / 128;
   p.loss_part[rb * 4 + 0] = s1;
   p.loss_part[rb * 4 + 1] = s2;
@@ -189,6 +166,74 @@ __device__ void gradf_loss_rows(const TcGradFArgs& p, int a0, int t) {
   if (bad) set_status(p.status, CRL_ENONFINITE);
   else *p.adam_t += 1;
 }
+
+// one warp (warp 3, while the epilogue works through a long column range)
+template <int ENERGY>
+__device__ void gradf_loss_rows_warp(const TcGradFArgs& p, int a0, int t) {
+  float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  for (int r = t; r < 128; r += 32) {
+    const int i = a0 + r;
+    if (i >= p.Na) break;
+    const float4* a = reinterpret_cast<const float4*>(p.phi32 + (size_t)i * 64);
+    const float4* b = reinterpret_cast<const float4*>(p.psi32 + (size_t)i * 64);
+    float x = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+      const float4 u = a[k], v = b[k];
+      if (ENERGY == CRL_ENERGY_L2) {
+        x = fmaf(u.x - v.x, u.x - v.x, x); x = fmaf(u.y - v.y, u.y - v.y, x);
+        x = fmaf(u.z - v.z, u.z - v.z, x); x = fmaf(u.w - v.w, u.w - v.w, x);
+      } else {
+        x = fmaf(u.x, v.x, x); x = fmaf(u.y, v.y, x); x = fmaf(u.z, v.z, x); x = fmaf(u.w, v.w, x);
+      }
+    }
+    const float l = ENERGY == CRL_ENERGY_L2 ? -sqrtf(x + kEpsL2) : x;
+    const float lr = p.lr[i], lc = p.lc[i];
+    s1 += lr - l; s2 += lc - l; s3 += lr * lr;
+  }
+  s1 = warp_sum(s1); s2 = warp_sum(s2); s3 = warp_sum(s3);
+  if (t == 0) gradf_loss_finish(p, a0, s1, s2, s3);
+}
+
+template <int ENERGY>
+__device__ void gradf_loss_rows_epi(const TcGradFArgs& p, int a0, int t) {
+  // the 512 epilogue threads, once their tiles are done: 4 threads per row (16 floats each,
+  // coalesced 64 B pieces), fixed-order reductions (shuffles, then 16 warp partials)
+  __shared__ float red[3][16];
+  const int rl = t >> 2, q4 = t & 3;
+  const int i = a0 + rl;
+  const bool ok = i < p.Na;
+  const float4* a = reinterpret_cast<const float4*>(p.phi32 + (size_t)(ok ? i : 0) * 64) + 4 * q4;
+  const float4* b = reinterpret_cast<const float4*>(p.psi32 + (size_t)(ok ? i : 0) * 64) + 4 * q4;
+  float x = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float4 u = a[k], v = b[k];
+    if (ENERGY == CRL_ENERGY_L2) {
+      x = fmaf(u.x - v.x, u.x - v.x, x); x = fmaf(u.y - v.y, u.y - v.y, x);
+      x = fmaf(u.z - v.z, u.z - v.z, x); x = fmaf(u.w - v.w, u.w - v.w, x);
+    } else {
+      x = fmaf(u.x, v.x, x); x = fmaf(u.y, v.y, x); x = fmaf(u.z, v.z, x); x = fmaf(u.w, v.w, x);
+    }
+  }
+  x += __shfl_xor_sync(0xffffffffu, x, 1);
+  x += __shfl_xor_sync(0xffffffffu, x, 2);
+  float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (ok && q4 == 0) {
+    const float l = ENERGY == CRL_ENERGY_L2 ? -sqrtf(x + kEpsL2) : x;
+    const float lr = p.lr[i], lc = p.lc[i];
+    s1 = lr - l; s2 = lc - l; s3 = lr * lr;
+  }
+  s1 = warp_sum(s1); s2 = warp_sum(s2); s3 = warp_sum(s3);
+  if ((t & 31) == 0) { red[0][t >> 5] = s1; red[1][t >> 5] = s2; red[2][t >> 5] = s3; }
+  asm volatile("bar.sync 6, 512;" ::: "memory");
+  if (t != 0) return;
+  s1 = 0.f; s2 = 0.f; s3 = 0.f;
+  for (int w = 0; w < 16; ++w) { s1 += red[0][w]; s2 += red[1][w]; s3 += red[2][w]; }
+  if (t != 0) return;
+  gradf_loss_finish(p, a0, s1, s2, s3);
+}
+
 
 struct GfCfg {
   static constexpr int D = 64, BNT = 128, STAGES = 3;
@@ -351,7 +396,8 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
     }
     mma_commit(da_full);
   } else if (warp == 3) {
-    if (p.loss_part != nullptr && split == 0) gradf_loss_rows<ENERGY>(p, a0, lane);
+    // short column ranges: the epilogue threads take the loss after their tiles (below)
+    if (p.loss_part != nullptr && split == 0 && ntiles > 2) gradf_loss_rows_warp<ENERGY>(p, a0, lane);
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue groups
     const int wgid = (warp - 4) >> 2;                     // 0..3
@@ -551,6 +597,7 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
           reinterpret_cast<float4*>(out)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       }
     }
+    if (p.loss_part != nullptr && split == 0 && ntiles <= 2) gradf_loss_rows_epi<ENERGY>(p, a0, threadIdx.x - 128);
     if (storer) gf::bulk_wait_all();
   }
   tc_fence_before();
