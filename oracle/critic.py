@@ -27,10 +27,11 @@ import numpy as np
 from . import adam, energy, losses, mlp
 
 
-def split_critic_params(flat, obs_dim, act_dim, goal_dim, depth, width, repr_dim):
+def split_critic_params(flat, obs_dim, act_dim, goal_dim, depth, width, repr_dim, layernorm=False):
     flat = np.asarray(flat, np.float64)
-    phi_layers, n_phi = mlp.unpack(flat, obs_dim + act_dim, depth, width, repr_dim)
-    psi_layers, n_psi = mlp.unpack(flat[n_phi:], goal_dim, depth, width, repr_dim)
+    up = mlp.unpack_ln if layernorm else mlp.unpack
+    phi_layers, n_phi = up(flat, obs_dim + act_dim, depth, width, repr_dim)
+    psi_layers, n_psi = up(flat[n_phi:], goal_dim, depth, width, repr_dim)
     assert n_phi + n_psi == flat.size, (n_phi, n_psi, flat.size)
     return phi_layers, psi_layers
 
@@ -46,20 +47,23 @@ def bf16_round(x):
 
 def critic_forward_backward(params, s, a, g, *, obs_dim, act_dim, goal_dim, depth, width,
                             repr_dim, energy_kind="l2", loss_kind="sym", beta=0.1,
-                            activation="silu"):
-    """Everything up to (not including) the optimiser.  Returns a dict."""
+                            activation="silu", layernorm=False):
+    """Everything up to (not including) the optimiser.  Returns a dict.  layernorm: the F2
+    encoders (LayerNorm before every hidden activation, oracle/mlp.py)."""
     phi_layers, psi_layers = split_critic_params(params, obs_dim, act_dim, goal_dim, depth,
-                                                 width, repr_dim)
+                                                 width, repr_dim, layernorm)
+    fwd, bwd, pk = (mlp.forward_ln, mlp.backward_ln, mlp.pack_ln) if layernorm else \
+        (mlp.forward, mlp.backward, mlp.pack)
     x_phi = np.concatenate([np.asarray(s, np.float64), np.asarray(a, np.float64)], axis=1)
     x_psi = np.asarray(g, np.float64)
-    Phi, cache_phi = mlp.forward(phi_layers, x_phi, activation)
-    Psi, cache_psi = mlp.forward(psi_layers, x_psi, activation)
+    Phi, cache_phi = fwd(phi_layers, x_phi, activation)
+    Psi, cache_psi = fwd(psi_layers, x_psi, activation)
     l = energy.logits(energy_kind, Phi, Psi)
     comps, G = losses.loss_and_grad(l, loss_kind, beta)
     dPhi, dPsi = energy.vjp(energy_kind, Phi, Psi, G)
-    g_phi, _ = mlp.backward(phi_layers, cache_phi, dPhi, activation)
-    g_psi, _ = mlp.backward(psi_layers, cache_psi, dPsi, activation)
-    grads = np.concatenate([mlp.pack(g_phi), mlp.pack(g_psi)])
+    g_phi, _ = bwd(phi_layers, cache_phi, dPhi, activation)
+    g_psi, _ = bwd(psi_layers, cache_psi, dPsi, activation)
+    grads = np.concatenate([pk(g_phi), pk(g_psi)])
     return dict(comps, phi=Phi, psi=Psi, logits=l, dlogits=G, dphi=dPhi, dpsi=dPsi, grads=grads)
 
 

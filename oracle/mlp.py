@@ -14,6 +14,15 @@ Backward (reverse mode, written out):
 Flat parameter layout (shared *convention* with include/crl.h, not code): for each layer
 W[in][out] row-major then b[out].
 
+LayerNorm variant (§5.4 P:462-465 "adding layer normalization before every activation",
+App. A.4; reading A-35: per-row over the features, learnable gain
+gamma and shift beta, eps = 1e-6 inside the square root (flax default)):
+  hidden:  Z_l = X_l W_l + b_l,  Zh = (Z_l - mu) / sqrt(var + eps),  Y_l = gamma Zh + beta,
+           X_{l+1} = act(Y_l)
+  layout per hidden layer: W, b, gamma[out], beta[out]; output layer W, b.
+  backward: dY = dX_{l+1} * act'(Y);  dgamma = sum_rows dY Zh,  dbeta = sum_rows dY;
+           dZ = rstd (g - mean(g) - Zh mean(g Zh)),  g = dY gamma  (row means over features)
+
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 """
 import numpy as np
@@ -87,4 +96,73 @@ def backward(layers, cache, dY, act="silu"):
         dX = dZ @ W.T
         if l > 0:
             dZ = dX * act_grad(Zs[l - 1], act)
+    return grads, dX
+
+
+LN_EPS = 1e-6
+
+
+def unpack_ln(flat, in_dim, depth, width, out_dim):
+    """Flat vector -> list of layers; hidden layers are (W, b, gamma, beta), the output
+    layer (W, b).  Returns (layers, n_used)."""
+    flat = np.asarray(flat, np.float64)
+    layers, off = [], 0
+    dims = layer_dims(in_dim, depth, width, out_dim)
+    for li, (fi, fo) in enumerate(dims):
+        W = flat[off:off + fi * fo].reshape(fi, fo); off += fi * fo
+        b = flat[off:off + fo]; off += fo
+        if li < len(dims) - 1:
+            gm = flat[off:off + fo]; off += fo
+            bt = flat[off:off + fo]; off += fo
+            layers.append((W, b, gm, bt))
+        else:
+            layers.append((W, b))
+    return layers, off
+
+
+def pack_ln(layers):
+    return np.concatenate([np.concatenate([t.ravel() for t in L]) for L in layers])
+
+
+def forward_ln(layers, x, act="silu"):
+    """Returns (Y, cache); cache = (Xs, Zs, Zhs, Ys, rstds)."""
+    X = np.asarray(x, np.float64)
+    Xs, Zs, Zhs, Ys, rs = [], [], [], [], []
+    for l, L in enumerate(layers):
+        Xs.append(X)
+        Z = X @ L[0] + L[1]
+        if l < len(layers) - 1:
+            mu = Z.mean(axis=1, keepdims=True)
+            var = ((Z - mu) ** 2).mean(axis=1, keepdims=True)
+            rstd = 1.0 / np.sqrt(var + LN_EPS)
+            Zh = (Z - mu) * rstd
+            Y = L[2] * Zh + L[3]
+            Zs.append(Z); Zhs.append(Zh); Ys.append(Y); rs.append(rstd)
+            X = act_fn(Y, act)
+        else:
+            X = Z
+    return X, (Xs, Zs, Zhs, Ys, rs)
+
+
+def backward_ln(layers, cache, dY_out, act="silu"):
+    """Returns (grads as list of tuples matching the layers, dX0)."""
+    Xs, Zs, Zhs, Ys, rs = cache
+    dZ = np.asarray(dY_out, np.float64)
+    grads = [None] * len(layers)
+    for l in range(len(layers) - 1, -1, -1):
+        W = layers[l][0]
+        gW, gb = Xs[l].T @ dZ, dZ.sum(axis=0)
+        if l < len(layers) - 1:
+            grads[l] = (gW, gb) + grads[l][2:]
+        else:
+            grads[l] = (gW, gb)
+        dX = dZ @ W.T
+        if l > 0:
+            k = l - 1
+            dYk = dX * act_grad(Ys[k], act)
+            gm = layers[k][2]
+            Zh = Zhs[k]
+            g = dYk * gm
+            dZ = rs[k] * (g - g.mean(axis=1, keepdims=True) - Zh * (g * Zh).mean(axis=1, keepdims=True))
+            grads[k] = (None, None, (dYk * Zh).sum(axis=0), dYk.sum(axis=0))
     return grads, dX

@@ -408,3 +408,60 @@ def test_ipo_sppo_minimisers():
     l2 = -np.ones((N, N)); np.fill_diagonal(l2, 1.0)
     # SPPO: diag (d-1)^2 = 0; (l+1)^2 = 0 off-diagonal, (1+1)^2 = 4 on the diagonal: (1/N) N 4
     assert losses.pairwise_loss(l2, "sppo") == pytest.approx(4.0, rel=1e-15)
+
+
+# ------------------------------------------------------------------ F2 LayerNorm encoders (A-35)
+
+def _ln_params(rng, in_dim, depth, width, out_dim):
+    parts = []
+    for li, (fi, fo) in enumerate(mlp.layer_dims(in_dim, depth, width, out_dim)):
+        parts += [rng.standard_normal(fi * fo) / np.sqrt(fi), rng.standard_normal(fo) * 0.1]
+        if li < depth:
+            parts += [1.0 + 0.2 * rng.standard_normal(fo), 0.1 * rng.standard_normal(fo)]
+    return np.concatenate(parts)
+
+
+def test_layernorm_forward_properties():
+    """With gamma = 1, beta = 0 every hidden pre-activation row has mean 0 and variance
+    var / (var + eps) (~1); LN is invariant to a per-row shift and positive scale of Z."""
+    rng = np.random.default_rng(4)
+    p = _ln_params(rng, 5, 2, 16, 3)
+    layers, n = mlp.unpack_ln(p, 5, 2, 16, 3)
+    assert n == p.size
+    layers = [(L[0], L[1], np.ones_like(L[2]), np.zeros_like(L[3])) if len(L) == 4 else L for L in layers]
+    x = rng.standard_normal((7, 5))
+    _, (Xs, Zs, Zhs, Ys, rs) = mlp.forward_ln(layers, x)
+    for Y, Z in zip(Ys, Zs):
+        assert np.allclose(Y.mean(1), 0.0, atol=1e-12)
+        var = Z.var(1)
+        assert np.allclose((Y ** 2).mean(1), var / (var + mlp.LN_EPS), rtol=1e-12)
+    W0, b0, g0, bt0 = layers[0]
+    lay2 = [(3.0 * W0, 3.0 * b0 + 0.0, g0, bt0)] + layers[1:]          # Z -> 3 Z: LN output unchanged (eps aside)
+    y1, _ = mlp.forward_ln(layers, x); y2, _ = mlp.forward_ln(lay2, x)
+    assert np.allclose(y1, y2, rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("act", ["silu", "relu"])
+def test_layernorm_mlp_gradient_finite_differences(act):
+    rng = np.random.default_rng(5)
+    p = _ln_params(rng, 4, 2, 8, 3)
+    x = rng.standard_normal((6, 4))
+    G = rng.standard_normal((6, 3))
+    def f(q):
+        L, _ = mlp.unpack_ln(q, 4, 2, 8, 3)
+        return float((mlp.forward_ln(L, x, act)[0] * G).sum())
+    L, _ = mlp.unpack_ln(p, 4, 2, 8, 3)
+    _, cache = mlp.forward_ln(L, x, act)
+    grads, _ = mlp.backward_ln(L, cache, G, act)
+    assert rel_err(mlp.pack_ln(grads), fd_grad(f, p)) < 1e-7
+
+
+def test_critic_layernorm_end_to_end_finite_differences():
+    rng = np.random.default_rng(6)
+    kw = dict(obs_dim=3, act_dim=2, goal_dim=2, depth=2, width=8, repr_dim=4, energy_kind="l2",
+              loss_kind="sym", beta=0.1, activation="silu", layernorm=True)
+    p = np.concatenate([_ln_params(rng, 5, 2, 8, 4), _ln_params(rng, 2, 2, 8, 4)])
+    s, a, g = rng.standard_normal((6, 3)), rng.standard_normal((6, 2)), rng.standard_normal((6, 2))
+    out = critic.critic_forward_backward(p, s, a, g, **kw)
+    fd = fd_grad(lambda q: critic.critic_forward_backward(q, s, a, g, **kw)["total"], p)
+    assert rel_err(out["grads"], fd) < 1e-6
