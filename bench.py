@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--workload", default="ant")
     p.add_argument("--precision", default="bf16")
     p.add_argument("--energy", default=None)
+    p.add_argument("--loss", default=None, help="fwd / bwd / sym / flatnce_* / fb / dpo / ipo / sppo")
+    p.add_argument("--layernorm", action="store_true", help="F2 LayerNorm encoders (fp32 path)")
     p.add_argument("--profile-steps", type=int, default=20)
     p.add_argument("--bulk-updates", type=int, default=256,
                    help="A1 bulk-mode measurement: updates per crl_relabel_sample_bulk call (0: skip)")
@@ -56,6 +58,10 @@ def workload_cfg(args):
         over["precision"] = args.precision
     if args.energy:
         over["energy"] = args.energy
+    if args.loss:
+        over["loss"] = args.loss
+    if args.layernorm:
+        over["layernorm"] = 1
     return crl_synth.preset(args.workload, **over)
 
 
@@ -250,7 +256,7 @@ def oracle_steps(cfg, chunks, seconds, max_steps, seed_step0=0, warm=1):
     kw = dict(obs_dim=cfg["obs_dim"], act_dim=cfg["act_dim"], goal_dim=cfg["goal_dim"],
               depth=cfg["depth"], width=cfg["width"], repr_dim=cfg["repr_dim"],
               energy_kind=cfg["energy"], loss_kind=cfg["loss"], beta=cfg["beta_lse"],
-              activation=cfg["activation"])
+              activation=cfg["activation"], layernorm=bool(cfg.get("layernorm", 0)))
     B = cfg["batch"]
     times = []
     step = seed_step0
@@ -463,7 +469,8 @@ def run_ours(args):
                            "obs_dim": cfg["obs_dim"], "act_dim": cfg["act_dim"],
                            "goal_dim": cfg["goal_dim"], "encoders": f"{cfg['depth']}x{cfg['width']}",
                            "repr_dim": cfg["repr_dim"], "energy": cfg["energy"], "loss": cfg["loss"],
-                           "beta_lse": cfg["beta_lse"], "buffer": f"{cfg['n_envs']}x{cfg['capacity']}",
+                           "beta_lse": cfg["beta_lse"], "layernorm": int(cfg.get("layernorm", 0)),
+                           "buffer": f"{cfg['n_envs']}x{cfg['capacity']}",
                            "parallelism": f"dp{world}", "l2_flush": "256 MiB memset between timed steps"},
                 "clocks": clocks, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
                 "gpu_launches_per_step": launches_per_step, "roofline": rl, "relabel_bulk": bulk,

@@ -78,36 +78,44 @@ def param_shapes(in_dim: int, depth: int, width: int, out_dim: int):
     return [(dims[i], dims[i + 1]) for i in range(len(dims) - 1)]
 
 
-def encoder_param_count(in_dim, depth, width, out_dim) -> int:
-    return sum(i * o + o for i, o in param_shapes(in_dim, depth, width, out_dim))
+def encoder_param_count(in_dim, depth, width, out_dim, layernorm=False) -> int:
+    return (sum(i * o + o for i, o in param_shapes(in_dim, depth, width, out_dim))
+            + (2 * width * depth if layernorm else 0))
 
 
 def critic_param_count(cfg) -> int:
-    return (encoder_param_count(cfg["obs_dim"] + cfg["act_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"])
-            + encoder_param_count(cfg["goal_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"]))
+    ln = bool(cfg.get("layernorm", 0))
+    return (encoder_param_count(cfg["obs_dim"] + cfg["act_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"], ln)
+            + encoder_param_count(cfg["goal_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"], ln))
 
 
 # ----------------------------------------------------------------------------
 # Parameters
 # ----------------------------------------------------------------------------
 
-def init_encoder(rng: np.random.Generator, in_dim, depth, width, out_dim) -> np.ndarray:
-    """Flat fp32: per layer W[in][out] (row-major) then b[out].  W ~ U(+-1/sqrt(fan_in)),
+def init_encoder(rng: np.random.Generator, in_dim, depth, width, out_dim, layernorm=False) -> np.ndarray:
+    """Flat fp32: per layer W[in][out] (row-major) then b[out] (+ LayerNorm gamma[out],
+    beta[out] on hidden layers when `layernorm`, F2).  W ~ U(+-1/sqrt(fan_in)),
     b ~ U(+-0.1/sqrt(fan_in)) (non-zero so bias gradients are exercised; A-14 says the
-    paper is silent on initialisation)."""
+    paper is silent on initialisation); gamma ~ 1 + U(+-0.1), beta ~ U(+-0.1) (not exactly
+    1 / 0, so their gradients and the gain are exercised)."""
     parts = []
-    for fi, fo in param_shapes(in_dim, depth, width, out_dim):
+    for li, (fi, fo) in enumerate(param_shapes(in_dim, depth, width, out_dim)):
         bound = 1.0 / np.sqrt(fi)
         parts.append(rng.uniform(-bound, bound, size=(fi, fo)).astype(np.float32).ravel())
         parts.append(rng.uniform(-0.1 * bound, 0.1 * bound, size=(fo,)).astype(np.float32))
+        if layernorm and li < depth:
+            parts.append((1.0 + rng.uniform(-0.1, 0.1, size=(fo,))).astype(np.float32))
+            parts.append(rng.uniform(-0.1, 0.1, size=(fo,)).astype(np.float32))
     return np.concatenate(parts)
 
 
 def init_critic_params(cfg, seed: int = 42) -> np.ndarray:
     """phi encoder params followed by psi encoder params (include/crl.h layout)."""
     rng = np.random.default_rng(seed)
-    phi = init_encoder(rng, cfg["obs_dim"] + cfg["act_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"])
-    psi = init_encoder(rng, cfg["goal_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"])
+    ln = bool(cfg.get("layernorm", 0))
+    phi = init_encoder(rng, cfg["obs_dim"] + cfg["act_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"], ln)
+    psi = init_encoder(rng, cfg["goal_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"], ln)
     return np.concatenate([phi, psi])
 
 

@@ -99,6 +99,11 @@ typedef struct {
   int batch_local, world_size, rank; /* global batch N = batch_local * world_size          */
   int actor_depth, actor_width;    /* actor MLP [s||g] -> (mu, log sigma)          */
   float lr_actor;                  /* policy_lr                                    */
+  int layernorm;                   /* 1: LayerNorm before every hidden activation (F2;
+                                      §5.4, reading A-35: per-row over features,
+                                      gain + shift, eps 1e-6).  Parameters per hidden layer:
+                                      W, b, gamma[out], beta[out].  fp32 path only (bf16 ->
+                                      CRL_EUNSUPPORTED); the actor has no LayerNorm. */
 } crl_config;
 
 typedef struct {

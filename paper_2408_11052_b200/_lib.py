@@ -46,7 +46,7 @@ class _Config(ctypes.Structure):
                 ("precision", ctypes.c_int), ("batch_local", ctypes.c_int),
                 ("world_size", ctypes.c_int), ("rank", ctypes.c_int),
                 ("actor_depth", ctypes.c_int), ("actor_width", ctypes.c_int),
-                ("lr_actor", ctypes.c_float)]
+                ("lr_actor", ctypes.c_float), ("layernorm", ctypes.c_int)]
 
 
 class _Sizes(ctypes.Structure):
@@ -138,6 +138,7 @@ class CrlConfig:
     actor_depth: int = 0
     actor_width: int = 0
     lr_actor: float = 6e-4
+    layernorm: int = 0
 
     @classmethod
     def from_preset(cls, p: dict, **over):
@@ -151,7 +152,8 @@ class CrlConfig:
                   activation=p["activation"], energy=p["energy"], loss=p["loss"],
                   beta_lse=p["beta_lse"], lr=p["lr"], adam_b1=p["adam_b1"], adam_b2=p["adam_b2"],
                   adam_eps=p["adam_eps"], weight_decay=p["weight_decay"],
-                  precision=p["precision"], world_size=world, rank=rank)
+                  precision=p["precision"], world_size=world, rank=rank,
+                  layernorm=int(p.get("layernorm", 0)))
         kw.update(over)
         return cls(**kw)
 

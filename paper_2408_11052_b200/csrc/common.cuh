@@ -15,7 +15,7 @@ namespace crl {
 // Host-side plan of one encoder: layer l has W[in][out] at w_off and b[out] at b_off in the
 // flat parameter buffer (include/crl.h layout).
 // ---------------------------------------------------------------------------------------
-struct LayerPlan { int in, out; size_t w_off, b_off; };
+struct LayerPlan { int in, out; size_t w_off, b_off, g_off, be_off; };   // g/be: LayerNorm (F2)
 struct EncoderPlan {
   int n_layers;          // depth hidden + 1 output
   int in_dim;
@@ -23,7 +23,8 @@ struct EncoderPlan {
   LayerPlan layer[CRL_MAX_LAYERS];
 };
 
-inline EncoderPlan make_encoder_plan(int in_dim, int depth, int width, int out_dim, size_t off) {
+// hidden layers: W, b (+ LayerNorm gamma, beta when `ln`); output layer: W, b
+inline EncoderPlan make_encoder_plan(int in_dim, int depth, int width, int out_dim, size_t off, bool ln = false) {
   EncoderPlan p{};
   p.n_layers = depth + 1;
   p.in_dim = in_dim;
@@ -37,6 +38,12 @@ inline EncoderPlan make_encoder_plan(int in_dim, int depth, int width, int out_d
     off += (size_t)prev * o;
     p.layer[l].b_off = off;
     off += o;
+    if (ln && l < depth) {
+      p.layer[l].g_off = off;
+      off += o;
+      p.layer[l].be_off = off;
+      off += o;
+    }
     prev = o;
   }
   p.n_params = off - p.param_off;

@@ -81,6 +81,11 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     }
     for (int l = 0; l < k.depth; ++l) {
       c->phiZ[l] = s.take<float>((size_t)Bl * Wd);
+      if (k.layernorm) {
+        c->phiY[l] = s.take<float>((size_t)Bl * Wd); c->psiY[l] = s.take<float>((size_t)Bl * Wd);
+        c->phiMu[l] = s.take<float>((size_t)Bl); c->psiMu[l] = s.take<float>((size_t)Bl);
+        c->phiRs[l] = s.take<float>((size_t)Bl); c->psiRs[l] = s.take<float>((size_t)Bl);
+      }
       c->psiZ[l] = s.take<float>((size_t)Bl * Wd);
     }
   } else {
@@ -259,6 +264,11 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
   if (k->loss >= CRL_LOSS_FB && (k->precision != CRL_FP32 || k->world_size != 1))
     return fail(ctx, CRL_EUNSUPPORTED, "FB / DPO / IPO / SPPO run on the fp32 path with world_size 1");
   if (k->precision != CRL_FP32 && k->precision != CRL_BF16) return fail(ctx, CRL_EINVAL, "precision");
+  if (k->layernorm != 0 && k->layernorm != 1) return fail(ctx, CRL_EINVAL, "layernorm must be 0 or 1");
+  if (k->layernorm && (k->precision != CRL_FP32 || k->width > 2048))
+    return fail(ctx, CRL_EUNSUPPORTED, "LayerNorm encoders run on the fp32 path with width <= 2048");
+  if (k->layernorm && k->actor_depth > 0)
+    return fail(ctx, CRL_EUNSUPPORTED, "the actor's frozen-critic pass has no LayerNorm encoders");
   if (k->precision == CRL_BF16 && (k->width % 16 != 0))
     return fail(ctx, CRL_EUNSUPPORTED, "bf16 path needs width % 16 == 0");
   if (k->world_size < 1 || k->rank < 0 || k->rank >= k->world_size)
@@ -289,9 +299,9 @@ crl_status crl_workspace_size(const crl_config* cfg, crl_sizes* out) {
   crl_ctx tmp;
   tmp.cfg = *cfg;
   tmp.phi_plan = make_encoder_plan(cfg->obs_dim + cfg->act_dim, cfg->depth, cfg->width,
-                                   cfg->repr_dim, 0);
+                                   cfg->repr_dim, 0, cfg->layernorm != 0);
   tmp.psi_plan = make_encoder_plan(cfg->goal_dim, cfg->depth, cfg->width, cfg->repr_dim,
-                                   tmp.phi_plan.n_params);
+                                   tmp.phi_plan.n_params, cfg->layernorm != 0);
   tmp.sizes.n_params = tmp.phi_plan.n_params + tmp.psi_plan.n_params;
   if (cfg->actor_depth > 0 && cfg->actor_width > 0) {
     EncoderPlan a = make_encoder_plan(cfg->obs_dim + cfg->goal_dim, cfg->actor_depth,
@@ -336,9 +346,9 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
   ctx->mem = *mem;
   ctx->N = cfg->batch_local * cfg->world_size;
   ctx->phi_plan = make_encoder_plan(cfg->obs_dim + cfg->act_dim, cfg->depth, cfg->width,
-                                    cfg->repr_dim, 0);
+                                    cfg->repr_dim, 0, cfg->layernorm != 0);
   ctx->psi_plan = make_encoder_plan(cfg->goal_dim, cfg->depth, cfg->width, cfg->repr_dim,
-                                    ctx->phi_plan.n_params);
+                                    ctx->phi_plan.n_params, cfg->layernorm != 0);
   size_t bb, sb;
   carve(ctx, (char*)mem->buffer, (char*)mem->scratch, &bb, &sb);
 
@@ -493,6 +503,10 @@ static crl_status enc_forward(crl_ctx* ctx, const char* tag, const EncoderPlan& 
   const crl_config& k = ctx->cfg;
   const float* prm = ctx->mem.params;
   const int Bl = k.batch_local;
+  const bool ln = k.layernorm != 0;               // F2: Z -> LayerNorm -> act (ln.cu)
+  float** Y = X == ctx->phiX ? ctx->phiY : ctx->psiY;
+  float** Mu = X == ctx->phiX ? ctx->phiMu : ctx->psiMu;
+  float** Rs = X == ctx->phiX ? ctx->phiRs : ctx->psiRs;
   for (int l = 0; l < P.n_layers; ++l) {
     const LayerPlan& L = P.layer[l];
     const bool last = (l == P.n_layers - 1);
@@ -501,8 +515,13 @@ static crl_status enc_forward(crl_ctx* ctx, const char* tag, const EncoderPlan& 
     Stage sg(ctx, st, std::string(tag) + "_fwd_l" + std::to_string(l));
     CU(mlp_forward_layer_f32(Bl, L.in, L.out, xin, ldx, l == 0 ? x0b : nullptr, ld0b,
                              l == 0 ? fsplit : 0, prm + L.w_off, prm + L.b_off,
-                             last ? out : Z[l], last ? nullptr : X[l + 1], k.activation, st));
+                             last ? out : Z[l], (last || ln) ? nullptr : X[l + 1], k.activation, st));
     ++*nl;
+    if (ln && !last) {
+      CU(launch_ln_fwd(Bl, L.out, Z[l], prm + L.g_off, prm + L.be_off, k.activation, Y[l], X[l + 1], Mu[l], Rs[l],
+                       st));
+      ++*nl;
+    }
   }
   return CRL_OK;
 }
@@ -513,6 +532,10 @@ static crl_status enc_backward(crl_ctx* ctx, const char* tag, const EncoderPlan&
   const crl_config& k = ctx->cfg;
   const float* prm = ctx->mem.params;
   const int Bl = k.batch_local;
+  const bool ln = k.layernorm != 0;
+  float** Yl = X == ctx->phiX ? ctx->phiY : ctx->psiY;
+  float** Mu = X == ctx->phiX ? ctx->phiMu : ctx->psiMu;
+  float** Rs = X == ctx->phiX ? ctx->phiRs : ctx->psiRs;
   const float* dZ = dY;
   int pp = 0;
   for (int l = P.n_layers - 1; l >= 0; --l) {
@@ -529,8 +552,15 @@ static crl_status enc_backward(crl_ctx* ctx, const char* tag, const EncoderPlan&
     if (l > 0) {
       float* dst = dzbuf[pp];
       Stage sg(ctx, st, std::string(tag) + "_bwd_dx_l" + std::to_string(l));
-      CU(mlp_backward_dx_f32(Bl, L.in, L.out, dZ, prm + L.w_off, Z[l - 1], dst, k.activation, st));
+      // dX * act'(.) at the pre-activation: Z_{l-1}, or with LayerNorm Y_{l-1} (then dY -> dZ)
+      CU(mlp_backward_dx_f32(Bl, L.in, L.out, dZ, prm + L.w_off, ln ? Yl[l - 1] : Z[l - 1], dst, k.activation, st));
       ++*nl;
+      if (ln) {
+        const LayerPlan& Lp = P.layer[l - 1];
+        CU(launch_ln_bwd(Bl, Lp.out, dst, Z[l - 1], Mu[l - 1], Rs[l - 1], prm + Lp.g_off, ctx->grads + Lp.g_off,
+                         ctx->grads + Lp.be_off, ctx->dw_splits, ctx->sizes.n_params, st));
+        ++*nl;
+      }
       dZ = dst;
       pp ^= 1;
     }

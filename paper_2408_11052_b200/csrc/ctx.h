@@ -40,6 +40,10 @@ cudaError_t launch_loss_partial(const float*, const float*, int, int, int, const
                                 const float*, float*, float*, unsigned*, int, float, float, float,
                                 float, float*, int*, int*, int*, cudaStream_t);
 int loss_partial_blocks(int Bl);
+cudaError_t launch_ln_fwd(int, int, const float*, const float*, const float*, int, float*, float*, float*, float*,
+                          cudaStream_t);
+cudaError_t launch_ln_bwd(int, int, float*, const float*, const float*, const float*, const float*, float*, float*,
+                          int, size_t, cudaStream_t);
 cudaError_t launch_pair_diag(const float*, const float*, int, int, int, float*, cudaStream_t);
 cudaError_t launch_pair_loss(const float*, const float*, const float*, int, int, float, float, float*, float*, int*,
                              int*, int*, cudaStream_t);
@@ -108,6 +112,10 @@ struct crl_ctx {
   float* grads = nullptr;             // [dw_splits][n_params] split-K partials, slice 0 = sum
   int dw_splits = 1;
   float* phiX[CRL_MAX_LAYERS] = {}; float* phiZ[CRL_MAX_LAYERS] = {};
+  // F2 LayerNorm: Y = LN(Z) (post-norm, pre-activation), row mean and 1/std per hidden layer
+  float* phiY[CRL_MAX_LAYERS] = {}; float* psiY[CRL_MAX_LAYERS] = {};
+  float* phiMu[CRL_MAX_LAYERS] = {}; float* psiMu[CRL_MAX_LAYERS] = {};
+  float* phiRs[CRL_MAX_LAYERS] = {}; float* psiRs[CRL_MAX_LAYERS] = {};
   float* psiX[CRL_MAX_LAYERS] = {}; float* psiZ[CRL_MAX_LAYERS] = {};
   float *phi_out = nullptr, *psi_out = nullptr, *phi_g = nullptr, *psi_g = nullptr;
   float *lse_row = nullptr, *lse_col = nullptr, *lse_row_g = nullptr, *lse_col_g = nullptr;

@@ -9,7 +9,7 @@ def oracle_kw(cfg):
     return dict(obs_dim=cfg["obs_dim"], act_dim=cfg["act_dim"], goal_dim=cfg["goal_dim"],
                 depth=cfg["depth"], width=cfg["width"], repr_dim=cfg["repr_dim"],
                 energy_kind=cfg["energy"], loss_kind=cfg["loss"], beta=cfg["beta_lse"],
-                activation=cfg["activation"])
+                activation=cfg["activation"], layernorm=bool(cfg.get("layernorm", 0)))
 
 
 def rel(a, b):

@@ -85,3 +85,13 @@ def test_sharded_workspace_is_smaller_per_rank():
     two = workspace_size(CrlConfig.from_preset(cfg, world_size=2, rank=1))
     assert two["buffer_bytes"] < one["buffer_bytes"]
     assert two["n_params"] == one["n_params"]
+
+
+def test_layernorm_param_count_matches_library():
+    """F2: the library's n_params for LayerNorm encoders equals the documented layout (W, b,
+    gamma, beta per hidden layer)."""
+    from paper_2408_11052_b200 import CrlConfig, workspace_size
+    cfg = crl_synth.preset("netscale", precision="fp32", batch=256, layernorm=1)
+    ws = workspace_size(CrlConfig.from_preset(cfg))
+    assert ws["n_params"] == crl_synth.critic_param_count(cfg)
+    assert ws["n_params"] == crl_synth.critic_param_count(dict(cfg, layernorm=0)) + 2 * 2 * 4 * 1024
