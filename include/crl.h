@@ -104,6 +104,10 @@ typedef struct {
                                       gain + shift, eps 1e-6).  Parameters per hidden layer:
                                       W, b, gamma[out], beta[out].  fp32 path only (bf16 ->
                                       CRL_EUNSUPPORTED); the actor has no LayerNorm. */
+  float random_goal_alpha;         /* F4 random-goal mixing in [0, 1] (App. C P:951-964,
+                                      reading A-36): the fraction of sampled rows whose goal
+                                      is the goal slice of a uniformly random stored state
+                                      (idx[2] = -1) instead of the hindsight goal; 0 = off */
 } crl_config;
 
 typedef struct {

@@ -102,12 +102,18 @@ def exact_offset_pmf(L, Q):
 
 
 def relabel_sample(buf: OracleBuffer, seed, step, batch_local, rank=0, world=1, gamma=0.99,
-                   goal_offset=0, goal_dim=2, Q=None, rows=None):
+                   goal_offset=0, goal_dim=2, Q=None, rows=None, alpha=0.0):
     """Hindsight relabel sample of ``batch_local`` rows for rank ``rank`` (C1).
 
     Returns s[B_l][obs], a[B_l][act], g[B_l][goal] (fp32 copies) and idx[B_l][3] int64 =
     (global env, tau, tau+k) with absolute step indices.  ``rows`` (optional) restricts the
     computation to those local rows (others stay zero) — every row is independent.
+
+    ``alpha`` (F4, App. C, reading A-36): random-goal mixing.  With the draw
+    (y0..y3) = Philox(rho, 64, step) (attempt counter 64, past the 0..63 start attempts),
+    a row whose y0 < floor(alpha 2^32) gets the goal slice of a uniformly random stored
+    state: env (y1 E_l) >> 32, slot tau_old + ((y2 n) >> 32); its idx[2] is -1.  alpha is
+    taken at fp32 precision (the ABI field).
     """
     tau_old, tau_new, n = buf.window()
     if n < 2:
@@ -139,6 +145,14 @@ def relabel_sample(buf: OracleBuffer, seed, step, batch_local, rank=0, world=1, 
         a[r] = buf.act[e][tau]
         g[r] = buf.obs[e][tau + k][goal_offset:goal_offset + goal_dim]
         idx[r] = (rank * E_l + e, tau, tau + k)
+        thr = int(float(np.float32(alpha)) * 4294967296.0)
+        if thr > 0:
+            y0, y1, y2, _ = (int(v) for v in philox4x32_10(rho, MAX_ATTEMPTS, step_lo, step_hi, seed_lo, seed_hi))
+            if y0 < thr:
+                e2 = (y1 * E_l) >> 32
+                t2 = tau_old + ((y2 * n) >> 32)
+                g[r] = buf.obs[e2][t2][goal_offset:goal_offset + goal_dim]
+                idx[r, 2] = -1
     return s, a, g, idx
 
 

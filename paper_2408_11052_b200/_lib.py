@@ -46,7 +46,8 @@ class _Config(ctypes.Structure):
                 ("precision", ctypes.c_int), ("batch_local", ctypes.c_int),
                 ("world_size", ctypes.c_int), ("rank", ctypes.c_int),
                 ("actor_depth", ctypes.c_int), ("actor_width", ctypes.c_int),
-                ("lr_actor", ctypes.c_float), ("layernorm", ctypes.c_int)]
+                ("lr_actor", ctypes.c_float), ("layernorm", ctypes.c_int),
+                ("random_goal_alpha", ctypes.c_float)]
 
 
 class _Sizes(ctypes.Structure):
@@ -139,6 +140,7 @@ class CrlConfig:
     actor_width: int = 0
     lr_actor: float = 6e-4
     layernorm: int = 0
+    random_goal_alpha: float = 0.0
 
     @classmethod
     def from_preset(cls, p: dict, **over):

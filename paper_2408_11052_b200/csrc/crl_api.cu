@@ -265,6 +265,8 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
     return fail(ctx, CRL_EUNSUPPORTED, "FB / DPO / IPO / SPPO run on the fp32 path with world_size 1");
   if (k->precision != CRL_FP32 && k->precision != CRL_BF16) return fail(ctx, CRL_EINVAL, "precision");
   if (k->layernorm != 0 && k->layernorm != 1) return fail(ctx, CRL_EINVAL, "layernorm must be 0 or 1");
+  if (!(k->random_goal_alpha >= 0.f && k->random_goal_alpha <= 1.f))
+    return fail(ctx, CRL_EINVAL, "random_goal_alpha must be in [0, 1]");
   if (k->layernorm && (k->precision != CRL_FP32 || k->width > 2048))
     return fail(ctx, CRL_EUNSUPPORTED, "LayerNorm encoders run on the fp32 path with width <= 2048");
   if (k->layernorm && k->actor_depth > 0)
@@ -475,7 +477,8 @@ static crl_status relabel(crl_ctx* ctx, uint64_t seed, uint64_t step, int n_upd,
   Stage sg(ctx, (cudaStream_t)stream, n_upd > 1 ? "relabel_bulk" : "relabel");
   CU(launch_relabel_sample(k.batch_local, n_upd, k.rank, k.n_envs_local, k.capacity, k.obs_dim, k.act_dim,
                            k.goal_dim, k.goal_offset, ctx->obs_stride, ctx->act_stride,
-                           (uint32_t)tau_old, (uint32_t)tau_new, seed, step, k.gamma, ctx->obs_ring,
+                           (uint32_t)tau_old, (uint32_t)tau_new, seed, step, k.gamma,
+                           (uint64_t)((double)k.random_goal_alpha * 4294967296.0), ctx->obs_ring,
                            ctx->act_ring, ctx->ep_end, ctx->qtab, s, a, g, idx, ctx->status,
                            (cudaStream_t)stream));
   ctx->launches = 1;

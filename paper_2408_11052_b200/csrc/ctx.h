@@ -19,7 +19,7 @@ cudaError_t launch_buffer_insert(const float*, const float*, const uint8_t*, int
                                  int, int, uint32_t, float*, float*, uint32_t*, uint32_t*,
                                  cudaStream_t);
 cudaError_t launch_relabel_sample(int, int, int, int, int, int, int, int, int, int, int, uint32_t,
-                                  uint32_t, uint64_t, uint64_t, double, const float*, const float*,
+                                  uint32_t, uint64_t, uint64_t, double, uint64_t, const float*, const float*,
                                   const uint32_t*, const uint64_t*, float*, float*, float*,
                                   int64_t*, int*, cudaStream_t);
 cudaError_t mlp_forward_layer_f32(int, int, int, const float*, int, const float*, int, int,

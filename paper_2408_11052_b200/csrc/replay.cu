@@ -100,7 +100,7 @@ template <int LPR>
 __global__ void __launch_bounds__(256) relabel_sample_kernel(
     int B_l, int n_upd, int rank, int E, int T, int obs_dim, int act_dim, int goal_dim, int goal_offset,
     int obs_stride, int act_stride, uint32_t tau_old, uint32_t tau_new,
-    uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo0, uint32_t step_hi0, double log_gamma,
+    uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo0, uint32_t step_hi0, double log_gamma, uint64_t alpha_t,
     const float* __restrict__ obs_ring, const float* __restrict__ act_ring,
     const uint32_t* __restrict__ ep_end, const uint64_t* __restrict__ qtab,
     float* __restrict__ s_out, float* __restrict__ a_out, float* __restrict__ g_out,
@@ -171,10 +171,20 @@ __global__ void __launch_bounds__(256) relabel_sample_kernel(
     k = lo;
   }
   const uint32_t slot = tau % (uint32_t)T;
-  const uint32_t gslot = (tau + k) % (uint32_t)T;
+  uint32_t ge = e, gslot = (tau + k) % (uint32_t)T;
+  bool rnd_goal = false;
+  if (alpha_t != 0) {
+    // random-goal mixing (F4, App. C): draw 64 (past the start attempts) decides and places it
+    const U4 y = philox4x32_10(U4{rho, 64u, step_lo, step_hi}, seed_lo, seed_hi);
+    if ((uint64_t)y.x < alpha_t) {
+      rnd_goal = true;
+      ge = (uint32_t)(((uint64_t)y.y * (uint64_t)E) >> 32);
+      gslot = (tau_old + (uint32_t)(((uint64_t)y.z * (uint64_t)n) >> 32)) % (uint32_t)T;
+    }
+  }
   const float* srow = obs_ring + ((size_t)e * T + slot) * obs_stride;
   const float* arow = act_ring + ((size_t)e * T + slot) * act_stride;
-  const float* grow = obs_ring + ((size_t)e * T + gslot) * obs_stride + goal_offset;
+  const float* grow = obs_ring + ((size_t)ge * T + gslot) * obs_stride + goal_offset;
   float* so = s_out + (size_t)r * obs_dim;
   float* ao = a_out + (size_t)r * act_dim;
   float* go = g_out + (size_t)r * goal_dim;
@@ -182,7 +192,7 @@ __global__ void __launch_bounds__(256) relabel_sample_kernel(
   for (int c = li; c < act_dim; c += LPR) ao[c] = arow[c];
   for (int c = li; c < goal_dim; c += LPR) go[c] = grow[c];
   if (idx_out != nullptr && li < 3) {
-    int64_t v = li == 0 ? (int64_t)rank * E + e : (li == 1 ? (int64_t)tau : (int64_t)(tau + k));
+    int64_t v = li == 0 ? (int64_t)rank * E + e : (li == 1 ? (int64_t)tau : (rnd_goal ? (int64_t)-1 : (int64_t)(tau + k)));
     idx_out[(size_t)r * 3 + li] = v;
   }
 }
@@ -202,6 +212,7 @@ cudaError_t launch_buffer_insert(const float* obs, const float* act, const uint8
 cudaError_t launch_relabel_sample(int B_l, int n_upd, int rank, int E, int T, int obs_dim, int act_dim,
                                   int goal_dim, int goal_offset, int obs_stride, int act_stride,
                                   uint32_t tau_old, uint32_t tau_new, uint64_t seed, uint64_t step, double gamma,
+                                  uint64_t alpha_t,
                                   const float* obs_ring, const float* act_ring,
                                   const uint32_t* ep_end, const uint64_t* qtab, float* s, float* a,
                                   float* g, int64_t* idx, int* status, cudaStream_t st) {
@@ -216,7 +227,7 @@ cudaError_t launch_relabel_sample(int B_l, int n_upd, int rank, int E, int T, in
   auto kern = narrow ? relabel_sample_kernel<4> : relabel_sample_kernel<32>;
   kern<<<grid, warps * 32, 0, st>>>(
       B_l, n_upd, rank, E, T, obs_dim, act_dim, goal_dim, goal_offset, obs_stride, act_stride, tau_old,
-      tau_new, (uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)step, (uint32_t)(step >> 32), std::log(gamma),
+      tau_new, (uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)step, (uint32_t)(step >> 32), std::log(gamma), alpha_t,
       obs_ring, act_ring, ep_end, qtab, s, a, g, idx, status);
   return cudaGetLastError();
 }

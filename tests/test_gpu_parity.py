@@ -80,6 +80,26 @@ def test_relabel_bit_exact_gamma(gamma):
     assert ctx.status() == 0
 
 
+@pytest.mark.parametrize("alpha", [0.37, 1.0])
+def test_relabel_random_goal_alpha_bit_exact(alpha):
+    """F4 random-goal mixing (App. C, reading A-36): bit-exact vs the oracle, flagged rows
+    carry idx[2] = -1 (single and bulk calls)."""
+    cfg = crl_synth.preset("reacher", precision="fp32", batch=256)
+    ctx, _ = make_ctx(cfg, random_goal_alpha=alpha)
+    chunks = fill_buffer(ctx, cfg, 20, U=62)
+    bufs = oracle_buffers(cfg, chunks)
+    for step in (0, 9):
+        s, a, g, idx = _sample_gpu(ctx, cfg, step)
+        os_, oa, og, oidx = oreplay.relabel_sample(bufs[0], SEED, step, 256, gamma=cfg["gamma"],
+                                                   goal_offset=cfg["goal_offset"], goal_dim=cfg["goal_dim"],
+                                                   alpha=alpha)
+        assert np.array_equal(idx, oidx)
+        assert np.array_equal(s.view(np.uint32), os_.view(np.uint32))
+        assert np.array_equal(g.view(np.uint32), og.view(np.uint32))
+        assert (idx[:, 2] == -1).any()
+    assert ctx.status() == 0
+
+
 def test_relabel_full_size_ant_sampled_rows():
     """configs[1] at full size (1024 envs x 1000, wrapped ring): the oracle recomputes a
     sample of rows one by one."""
