@@ -203,7 +203,9 @@ CRL_API crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float* a,
  *   apply_adam != 0 applies one Adam step (lr_actor, adam_b1/b2/eps, weight_decay) to
  *   actor_params; the step is skipped and CRL_ENONFINITE raised if the loss is non-finite.
  * Multi-GPU: the loss is the global mean and the gradients are all-reduced (sum of 1/N terms).
- * fp32 throughout (the critic's fp32 master parameters), launched eagerly on `stream`.
+ * fp32 throughout (the critic's fp32 master parameters); the schedule is captured once per
+ * (s, g, eps, loss_out, actor_grads_out, apply_adam) into a CUDA graph and replayed on
+ * `stream` (alpha_ent is written to device memory first, so any alpha reuses the graph).
  * CRL_EUNSUPPORTED if the context was created without an actor (actor_depth = 0). */
 CRL_API crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* g, const float* eps,
                           float alpha_ent, float* loss_out, float* actor_grads_out,

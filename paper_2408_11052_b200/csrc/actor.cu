@@ -17,6 +17,8 @@
 // the fp32 SIMT kernels of mlp_simt.cu, the per-row head / energy kernels below.
 #include <cmath>
 
+#include <cstring>
+
 #include "common.cuh"
 #include "ctx.h"
 
@@ -52,7 +54,8 @@ __global__ void actor_head_fwd_kernel(int Bl, int A, const float* __restrict__ o
 }
 
 // one warp per row: f_i = f(phi_i, psi_i), dPhi_i = -(1/N) df/dphi_i, rowloss_i = alpha log pi_i - f_i
-__global__ void actor_diag_kernel(int Bl, int D, int energy, float invN, float alpha, const float* __restrict__ phi,
+__global__ void actor_diag_kernel(int Bl, int D, int energy, float invN, const float* __restrict__ alpha_p,
+                                  const float* __restrict__ phi,
                                   const float* __restrict__ psi, const float* __restrict__ logpi,
                                   float* __restrict__ dphi, float* __restrict__ rowloss) {
   pdl_wait();
@@ -106,7 +109,7 @@ __global__ void actor_diag_kernel(int Bl, int D, int energy, float invN, float a
       dx[k] = -invN * g;
     }
   }
-  if (lane == 0) rowloss[row] = alpha * logpi[row] - f;
+  if (lane == 0) rowloss[row] = *alpha_p * logpi[row] - f;
 }
 
 // one CTA: deterministic sums of the per-row losses and log pi into a_loss[0..1]
@@ -148,9 +151,11 @@ __global__ void actor_loss_finalize_kernel(float* __restrict__ acc, float invN, 
 }
 
 // per row: dL/d(mu, log sigma_raw) from dL/da' (critic path) and the log pi terms
-__global__ void actor_head_bwd_kernel(int Bl, int A, float alpha_invN, const float* __restrict__ out,
+__global__ void actor_head_bwd_kernel(int Bl, int A, const float* __restrict__ alpha_p, float invN,
+                                      const float* __restrict__ out,
                                       const float* __restrict__ eps, const float* __restrict__ a_new,
                                       const float* __restrict__ da, float* __restrict__ dout) {
+  const float alpha_invN = *alpha_p * invN;
   pdl_wait();
   pdl_launch();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
@@ -186,15 +191,13 @@ static crl_status mlp_fwd(crl_ctx* ctx, const EncoderPlan& P, const float* prm, 
   return CRL_OK;
 }
 
-extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* g, const float* eps,
-                                     float alpha_ent, float* loss_out, float* actor_grads_out,
-                                     int apply_adam, void* stream) {
-  if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
-  if (!ctx->has_actor) return fail(ctx, CRL_EUNSUPPORTED, "context created without an actor (actor_depth = 0)");
-  if (!s || !g || !eps) return fail(ctx, CRL_EINVAL, "actor_loss: NULL s, g or eps");
-  if (!(alpha_ent >= 0.f) || !std::isfinite(alpha_ent)) return fail(ctx, CRL_EINVAL, "alpha_ent must be >= 0");
+__global__ void set_scalar_kernel(float* p, float v) { *p = v; }
+
+// the actor step's schedule; alpha is read from ctx->a_alpha (device) so one captured graph
+// serves every alpha (the entropy tuning changes it each step)
+static crl_status enqueue_actor(crl_ctx* ctx, const float* s, const float* g, const float* eps, float* loss_out,
+                                float* actor_grads_out, int apply_adam, cudaStream_t st) {
   const crl_config& k = ctx->cfg;
-  cudaStream_t st = (cudaStream_t)stream;
   const int Bl = k.batch_local, A = k.act_dim, D = k.repr_dim, W = k.world_size;
   const float invN = 1.0f / (float)ctx->N;
   const float* cp = ctx->mem.params;              // frozen critic (fp32 master copy)
@@ -218,7 +221,7 @@ extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* 
                k.activation, st, &nl);
   if (rs != CRL_OK) return rs;
   CU(launch_pdl(actor_diag_kernel, dim3((Bl * 32 + 255) / 256), dim3(256), 0, st, Bl, D, k.energy, invN,
-                alpha_ent, (const float*)ctx->ac_phi, (const float*)ctx->ac_psi, (const float*)ctx->a_logpi,
+                (const float*)ctx->a_alpha, (const float*)ctx->ac_phi, (const float*)ctx->ac_psi, (const float*)ctx->a_logpi,
                 ctx->ac_dphi, ctx->a_rowloss));
   ++nl;
   CU(launch_pdl(actor_loss_sum_kernel, dim3(1), dim3(1024), 0, st, Bl, (const float*)ctx->a_rowloss,
@@ -246,7 +249,7 @@ extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* 
                            k.activation, st));
     ++nl;
   }
-  CU(launch_pdl(actor_head_bwd_kernel, dim3(rb), dim3(128), 0, st, Bl, A, alpha_ent * invN,
+  CU(launch_pdl(actor_head_bwd_kernel, dim3(rb), dim3(128), 0, st, Bl, A, (const float*)ctx->a_alpha, invN,
                 (const float*)ctx->a_out, eps, (const float*)ctx->a_new, (const float*)ctx->a_da, ctx->a_dout));
   ++nl;
   // actor backward: dW, db (split-K partials), dX with act'
@@ -282,6 +285,42 @@ extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* 
     ++nl;
   }
   ctx->launches = nl;
+  return CRL_OK;
+}
+
+extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* g, const float* eps,
+                                     float alpha_ent, float* loss_out, float* actor_grads_out,
+                                     int apply_adam, void* stream) {
+  if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
+  if (!ctx->has_actor) return fail(ctx, CRL_EUNSUPPORTED, "context created without an actor (actor_depth = 0)");
+  if (!s || !g || !eps) return fail(ctx, CRL_EINVAL, "actor_loss: NULL s, g or eps");
+  if (!(alpha_ent >= 0.f) || !std::isfinite(alpha_ent)) return fail(ctx, CRL_EINVAL, "alpha_ent must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  set_scalar_kernel<<<1, 1, 0, st>>>(ctx->a_alpha, alpha_ent);      // stream-ordered, outside the graph
+  CU(cudaGetLastError());
+  if (ctx->prof_on || std::getenv("CRL_ACTOR_EAGER")) {
+    crl_status rs = enqueue_actor(ctx, s, g, eps, loss_out, actor_grads_out, apply_adam, st);
+    if (rs == CRL_OK) ctx->actor_loss_done = true;
+    return rs;
+  }
+  // captured once per (pointers, apply_adam) and replayed: ~20 dependent launches become one
+  ActorKey key{s, g, eps, loss_out, actor_grads_out, apply_adam};
+  auto it = ctx->actor_graphs.find(key);
+  if (it == ctx->actor_graphs.end()) {
+    CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    crl_status rs = enqueue_actor(ctx, s, g, eps, loss_out, actor_grads_out, apply_adam, ctx->cap_stream);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    if (rs != CRL_OK) { if (graph) cudaGraphDestroy(graph); return rs; }
+    CU(ce);
+    cudaGraphExec_t exec = nullptr;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CU(ce);
+    it = ctx->actor_graphs.emplace(key, std::make_pair(exec, ctx->launches)).first;
+  }
+  CU(cudaGraphLaunch(it->second.first, st));
+  ctx->launches = it->second.second;
   ctx->actor_loss_done = true;
   return CRL_OK;
 }

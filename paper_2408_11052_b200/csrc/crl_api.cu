@@ -236,6 +236,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     c->a_loss = s.take<float>(4);
     c->a_t = s.take<int>(1);
     c->a_skip = s.take<int>(1);
+    c->a_alpha = s.take<float>(1);
     c->ent_mv = s.take<float>(2);
     c->ent_t = s.take<int>(1);
   }
@@ -407,6 +408,7 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
 crl_status crl_destroy(crl_ctx* ctx) {
   if (!ctx) return CRL_OK;
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : ctx->actor_graphs) cudaGraphExecDestroy(kv.second.first);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);

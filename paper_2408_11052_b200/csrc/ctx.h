@@ -97,6 +97,14 @@ struct GraphKey {
   }
 };
 
+struct ActorKey {
+  const void *s, *g, *eps, *loss, *grads;
+  int adam;
+  bool operator<(const ActorKey& o) const {
+    return std::tie(s, g, eps, loss, grads, adam) < std::tie(o.s, o.g, o.eps, o.loss, o.grads, o.adam);
+  }
+};
+
 struct crl_ctx {
   crl_config cfg{};
   crl_sizes sizes{};
@@ -214,6 +222,8 @@ struct crl_ctx {
   float* a_grads = nullptr;                // [dw_splits][n_actor_params]
   float* a_loss = nullptr;                 // [4]: summed rows, summed log pi (all-reduced), loss, mean log pi
   int *a_t = nullptr, *a_skip = nullptr;
+  float* a_alpha = nullptr;                // [1] the entropy coefficient of the current actor call
+  std::map<ActorKey, std::pair<cudaGraphExec_t, int>> actor_graphs;   // captured actor steps
   float* ent_mv = nullptr;                 // [2] Adam moments of log alpha (entropy coefficient)
   int* ent_t = nullptr;                    // its step counter
   bool actor_loss_done = false;            // a crl_actor_loss has produced a mean log pi
