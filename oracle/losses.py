@@ -53,14 +53,11 @@ def loss_and_grad(l, kind="sym", beta=0.1):
     lse = lse_rows(l)
     lsec = lse_cols(l)
     diag = np.diag(l)
+    G = grad_rows(l, np.arange(N), lse, lsec, kind, beta)
     L_fwd = np.mean(lse - diag)
     L_bwd = np.mean(lsec - diag)
     P = beta * np.mean(lse ** 2)
     total = cf * L_fwd + cb * L_bwd + P
-    p = np.exp(l - lse[:, None])
-    q = np.exp(l - lsec[None, :])
-    I = np.eye(N)
-    G = (cf * (p - I) + cb * (q - I)) / N + (2.0 * beta / N) * lse[:, None] * p
     if kind in FLAT:
         # FlatNCE (reading A-24): L = (1/N) sum_i log(S_i / sg[S_i]) with
         # S_i = sum_j exp(l_ij - l_ii): value 0; its gradient, written out,
@@ -72,6 +69,23 @@ def loss_and_grad(l, kind="sym", beta=0.1):
         total = P
     comps = dict(L_fwd=L_fwd, L_bwd=L_bwd, penalty=P, total=total, lse_row=lse, lse_col=lsec)
     return comps, G
+
+
+def grad_rows(l_rows, row_ids, lse, lsec, kind="sym", beta=0.1):
+    """Rows `row_ids` of dL/dl (InfoNCE family) from those logits rows and the statistics:
+    G_ij = (1/N)[c_f (p_ij - delta_ij) + c_b (q_ij - delta_ij)] + (2 beta / N) LSE_i p_ij,
+    p = exp(l_ij - LSE_i), q = exp(l_ij - LSE'_j).  loss_and_grad uses it for the whole
+    matrix; the full-size GPU tests use it for sampled rows (statistics from blockwise passes)."""
+    l_rows = np.asarray(l_rows, np.float64)
+    row_ids = np.asarray(row_ids)
+    N = l_rows.shape[1]
+    cf, cb = LOSS_COEF[kind]
+    li = lse[row_ids][:, None]
+    p = np.exp(l_rows - li)
+    q = np.exp(l_rows - np.asarray(lsec)[None, :])
+    D = np.zeros_like(l_rows)
+    D[np.arange(len(row_ids)), row_ids] = 1.0
+    return (cf * (p - D) + cb * (q - D)) / N + (2.0 * beta / N) * li * p
 
 
 PAIRWISE = ("fb", "dpo", "ipo", "sppo")

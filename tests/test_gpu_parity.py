@@ -356,6 +356,81 @@ def test_pair_losses_bf16_or_dp_unsupported(loss):
         make_ctx(cfg)
 
 
+@pytest.mark.parametrize("preset", ["sweep16384", "netscale"])
+def test_critic_step_bf16_full_size_sampled(preset):
+    """configs[3] at its largest batch and configs[4] (4 x 1024, D 256) at full size, in the
+    launch configuration bench.py times: the oracle recomputes sampled outputs one by one --
+    phi / psi rows, row and column logsumexps (each needs the oracle's encoders over the whole
+    batch, then O(N D) per sampled row) -- against the bf16 bar (2e-2)."""
+    from oracle import mlp as omlp
+    cfg = crl_synth.preset(preset, precision="bf16")
+    N = cfg["batch"]
+    ctx, params = make_ctx(cfg)
+    s, a, g = crl_synth.random_batch(cfg, N, seed=13)
+    loss = torch.zeros(4, device="cuda")
+    ctx.critic_step(torch.from_numpy(s).cuda(), torch.from_numpy(a).cuda(), torch.from_numpy(g).cuda(), loss)
+    torch.cuda.synchronize()
+    assert ctx.status() == 0
+    phi_l, psi_l = ocritic.split_critic_params(params.astype(np.float64), cfg["obs_dim"], cfg["act_dim"],
+                                               cfg["goal_dim"], cfg["depth"], cfg["width"], cfg["repr_dim"])
+    Phi, _ = omlp.forward(phi_l, np.concatenate([s, a], axis=1).astype(np.float64), cfg["activation"])
+    Psi, _ = omlp.forward(psi_l, g.astype(np.float64), cfg["activation"])
+    rows = np.random.default_rng(5).choice(N, 48, replace=False)
+    gphi = ctx.debug_tensor("phi").cpu().numpy().reshape(N, -1)
+    gpsi = ctx.debug_tensor("psi").cpu().numpy().reshape(N, -1)
+    glr = ctx.debug_tensor("lse_row").cpu().numpy()
+    glc = ctx.debug_tensor("lse_col").cpu().numpy()
+    for i in rows:
+        assert rel(gphi[i], Phi[i]) < BF16_TOL, i
+        assert rel(gpsi[i], Psi[i]) < BF16_TOL, i
+        lr = logsumexp(energy_row(cfg["energy"], Phi[i], Psi))
+        lc = logsumexp(energy_row(cfg["energy"], Psi[i], Phi))
+        assert abs(glr[i] - lr) <= BF16_TOL * max(1.0, abs(lr)), (i, glr[i], lr)
+        assert abs(glc[i] - lc) <= BF16_TOL * max(1.0, abs(lc)), (i, glc[i], lc)
+    assert np.isfinite(loss.cpu().numpy()).all()
+    if preset != "sweep16384":
+        return
+    # sampled gradient rows: every row and column logsumexp from a blockwise oracle pass over
+    # the N x N logits, then dPhi_i / dPsi_j for the sampled rows through the oracle's VJP
+    from oracle import energy as oenergy
+    from oracle import losses as olosses
+    lse = np.empty(N)
+    cm = np.full(N, -np.inf); cs = np.zeros(N)
+    for r0 in range(0, N, 1024):
+        L = oenergy.logits(cfg["energy"], Phi[r0:r0 + 1024], Psi)
+        lse[r0:r0 + 1024] = olosses.lse_rows(L)
+        m = np.maximum(cm, L.max(0))
+        cs = cs * np.exp(cm - m) + np.exp(L - m[None, :]).sum(0)
+        cm = m
+    lsec = cm + np.log(cs)
+    gdphi = ctx.debug_tensor("dphi").cpu().numpy().reshape(N, -1)
+    gdpsi = ctx.debug_tensor("dpsi").cpu().numpy().reshape(N, -1)
+    for i in rows[:16]:
+        Lr = oenergy.logits(cfg["energy"], Phi[i:i + 1], Psi)
+        Gr = olosses.grad_rows(Lr, [i], lse, lsec, cfg["loss"], cfg["beta_lse"])
+        dphi_i, _ = oenergy.vjp(cfg["energy"], Phi[i:i + 1], Psi, Gr)
+        assert rel(gdphi[i], dphi_i[0]) < BF16_TOL, (i, rel(gdphi[i], dphi_i[0]))
+        # column j = i: the same formula on the transposed problem (rows <-> columns)
+        Lc = oenergy.logits(cfg["energy"], Psi[i:i + 1], Phi)
+        kind_t = {"fwd": "bwd", "bwd": "fwd"}.get(cfg["loss"], cfg["loss"])
+        Gc = olosses.grad_rows(Lc, [i], lsec, lse, kind_t, 0.0)
+        # the penalty acts on row LSEs only: its column-side term is (2 beta / N) LSE_k p_k,j
+        Gc = Gc + (2.0 * cfg["beta_lse"] / N) * (lse * np.exp(Lc[0] - lse))[None, :]
+        dpsi_i, _ = oenergy.vjp(cfg["energy"], Psi[i:i + 1], Phi, Gc)
+        assert rel(gdpsi[i], dpsi_i[0]) < BF16_TOL, (i, rel(gdpsi[i], dpsi_i[0]))
+
+
+def energy_row(kind, x, Y):
+    """f(x, y_j) for every row y_j of Y (oracle/energy.py, one row at a time)."""
+    from oracle import energy as oenergy
+    return oenergy.logits(kind, x[None, :], Y)[0]
+
+
+def logsumexp(v):
+    m = v.max()
+    return m + np.log(np.exp(v - m).sum())
+
+
 def test_critic_step_bf16_tc_logits_repr256():
     cfg = crl_synth.preset("ant", batch=1536, width=128, repr_dim=256, precision="bf16", beta_lse=0.3)
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
