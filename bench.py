@@ -454,6 +454,15 @@ def run_ours(args):
         except Exception:
             traffic_db = {}
         rl = roofline(stages, cfg, N, Bl, peaks, kind, clocks, traffic_db)
+        if rl is not None:
+            # the small-batch regime is bound by the chain of dependent launches, not by a unit:
+            # the measured graph floor (scratch/graph_floor.cu: ~1.1 us per dependent PDL kernel
+            # on B200) times this step's launches, against the measured step time
+            floor = 1.1 * launches_per_step
+            rl["latency"] = {"launches_per_step": launches_per_step, "graph_floor_us_per_launch": 1.1,
+                             "floor_us": round(floor, 2),
+                             "frac": round(floor / (total_ms / args.steps * 1e3), 4),
+                             "source": "scratch/graph_floor.cu (dependent tiny kernels, CUDA graph + PDL)"}
         cpu = None
         if not args.no_cpu_baseline:
             val, cores, n = oracle_steps(cfg, chunks, args.cpu_seconds, 10_000)
