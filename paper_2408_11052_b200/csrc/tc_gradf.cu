@@ -7,15 +7,18 @@
 //                             dPsi_j = sum_i w_ij phi_i - (sum_i w_ij) psi_j
 //   dot: w_ij = g_ij,         dPhi = W Psi,  dPsi = W^T Phi
 // The two-call design (tc_logits.cu) evaluates every w_ij twice, once per orientation.  Here
-// one CTA (128 rows x a column split) forms each W tile once and feeds three tcgen05 MMAs:
-//   dA   += W . B_t        (M=128 rows, N=64, K=128 cols)   TMEM-resident over the split
-//   dB_t  = W^T . A        (M=128 cols, N=64, K=128 rows)   A and W re-read as MN-major
-//   cs_t  = W^T . 1        (L2 only: the column sums of w)
-// dB_t and cs_t are per (row block, column tile): they are accumulated across row blocks in
-// a global fp32 buffer by TMA bulk-tensor REDUCTIONS (cp.reduce.async.bulk .add.f32, whole
-// 32 KB tiles from a swizzled SMEM staging buffer) and red.global.add (cs).  The row side
-// keeps the per-split partials of tc_logits.cu; grad_merge finishes both sides (the -rs A
-// term, the positive-pair term, fp32 + bf16 outputs).
+// one CTA (128 rows x a column split) forms each W tile once and feeds the tcgen05 MMAs:
+//   S_t          = A . B_t^T      (M=128 rows, N=128 cols, K=64)
+//   dA          += W . B_t        (M=128 rows, N=64, K=128 cols)   TMEM-resident over the split
+//   [dB_t | cs_t] = W^T . [A | 1] (M=128 cols, N=80, K=128 rows)   one MMA per K step: the
+//                                  all-ones chunk sits 16 KB after A (L2: column sums of w)
+// Two epilogue groups of 8 warps ping-pong over the tiles (group t & 1 owns S / W / dB buffer
+// t & 1): one group's readout and synchronisation overlap the other's XU work.  S and the
+// back-MMAs have separate issuing threads.  dB_t is accumulated across row blocks in a global
+// fp32 buffer by TMA bulk-tensor REDUCTIONS (cp.reduce.async.bulk .add.f32 of 16 KB halves
+// from swizzled SMEM staging) and cs_t by red.global.add; the row side keeps per-split
+// partials; grad_merge2 finishes both sides (the -rs A term, the positive-pair term, fp32 +
+// bf16 outputs).  The loss (readings A-02..A-05) is reduced in the same kernel.
 // fp32 atomics make the column-side sum order nondeterministic at the 1-ulp level (row side
 // and every other stage stay deterministic); the path's tolerance is 2e-2 (north_star).
 #include <algorithm>
@@ -54,13 +57,6 @@ __device__ __forceinline__ float ex2_neg(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-x));
   return y;
 }
-__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_ld1_nowait(uint32_t taddr, uint32_t& r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
 }
@@ -84,29 +80,7 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
                "r"(src), "r"(x), "r"(y)
                : "memory");
 }
-// mbarrier wait; built with -DCRL_GF_WATCHDOG it reports a stuck barrier and traps instead of
-// hanging (debugging aid)
-__device__ __noinline__ void wait_report(int id, uint32_t parity) {
-  printf("GF_WATCHDOG block (%d,%d) thread %d barrier %d parity %u\n", blockIdx.x, blockIdx.y, threadIdx.x, id,
-         parity);
-  __trap();
-}
-__device__ __forceinline__ void wait_wd(uint64_t* bar, uint32_t parity, int id) {
-#ifndef CRL_GF_WATCHDOG
-  (void)id;
-  mbar_wait(bar, parity);
-  return;
-#endif
-  uint32_t ok = 0;
-  for (uint32_t n = 0;; ++n) {
-    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
-                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    if (ok) return;
-    if (n == (1u << 24)) wait_report(id, parity);
-  }
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
