@@ -44,6 +44,10 @@ def parse():
     p.add_argument("--loss", default=None, help="fwd / bwd / sym / flatnce_* / fb / dpo / ipo / sppo")
     p.add_argument("--layernorm", action="store_true", help="F2 LayerNorm encoders (fp32 path)")
     p.add_argument("--profile-steps", type=int, default=20)
+    p.add_argument("--sample-every", type=int, default=16,
+                   help="batches sampled per crl_relabel_sample_bulk launch inside the timed steps "
+                        "(Alg. 1: a collection round's updates are sampled together); 1 = one "
+                        "crl_relabel_sample per step")
     p.add_argument("--bulk-updates", type=int, default=256,
                    help="A1 bulk-mode measurement: updates per crl_relabel_sample_bulk call (0: skip)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -330,19 +334,29 @@ def run_ours(args):
         for obs, act, done in crl_synth.rank_chunks(chunks, rank, world):
             ctx.buffer_insert(torch.from_numpy(obs).cuda(), torch.from_numpy(act).cuda(),
                               torch.from_numpy(done).cuda(), stream=stream)
-    s = torch.empty(Bl, cfg["obs_dim"], device="cuda")
-    a = torch.empty(Bl, cfg["act_dim"], device="cuda")
-    g = torch.empty(Bl, cfg["goal_dim"], device="cuda")
+    nb = max(1, args.sample_every)
+    s_all = torch.empty(nb * Bl, cfg["obs_dim"], device="cuda")
+    a_all = torch.empty(nb * Bl, cfg["act_dim"], device="cuda")
+    g_all = torch.empty(nb * Bl, cfg["goal_dim"], device="cuda")
+    s, a, g = s_all[:Bl], a_all[:Bl], g_all[:Bl]
     loss = torch.zeros(4, device="cuda")
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
     def step(i):
-        ctx.relabel_sample(crl_synth.PHILOX_SEED, i, s, a, g, stream=stream)
-        ctx.critic_step(s, a, g, loss, stream=stream)
+        # every step trains on its own freshly sampled batch (step counter i): with nb > 1 the
+        # batches of nb consecutive steps come from one bulk launch (row u*B + r of the bulk
+        # call = row r of the single call at step0 + u, bit-exact), issued at the first of them
+        k = i % nb
+        if nb == 1:
+            ctx.relabel_sample(crl_synth.PHILOX_SEED, i, s, a, g, stream=stream)
+        elif k == 0:
+            ctx.relabel_sample_bulk(crl_synth.PHILOX_SEED, i, nb, s_all, a_all, g_all, stream=stream)
+        sl = slice(k * Bl, (k + 1) * Bl)
+        ctx.critic_step(s_all[sl], a_all[sl], g_all[sl], loss, stream=stream)
 
-    for i in range(args.warmup):
+    for i in range(max(args.warmup, nb)):          # every slice's graph captured before timing
         step(i)
-    launches_per_step = 1 + ctx.launch_count()
+    launches_per_step = 1.0 / nb + ctx.launch_count()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -351,11 +365,13 @@ def run_ours(args):
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clk = ClockSampler(local)
     clk.start()
+    t0 = -(-max(args.warmup, nb) // nb) * nb       # timed steps start on a bulk boundary
+    n_bulk = sum(1 for i in range(args.steps) if nb > 1 and (t0 + i) % nb == 0)
     with torch.cuda.stream(stream):
         for i in range(args.steps):
             flush.zero_()                         # L2 flush between timed iterations
             ev0[i].record(stream)
-            step(args.warmup + i)
+            step(t0 + i)
             ev1[i].record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -418,30 +434,30 @@ def run_ours(args):
     # ---- A1 in bulk mode (F4): many updates' rows in one launch, HBM fraction of the gather
     bulk = None
     if rank == 0 and args.bulk_updates > 0:
-        nb = args.bulk_updates
-        bs = torch.empty(nb * Bl, cfg["obs_dim"], device="cuda")
-        ba = torch.empty(nb * Bl, cfg["act_dim"], device="cuda")
-        bg = torch.empty(nb * Bl, cfg["goal_dim"], device="cuda")
-        bi = torch.empty(nb * Bl, 3, dtype=torch.int64, device="cuda")
+        nbu = args.bulk_updates
+        bs = torch.empty(nbu * Bl, cfg["obs_dim"], device="cuda")
+        ba = torch.empty(nbu * Bl, cfg["act_dim"], device="cuda")
+        bg = torch.empty(nbu * Bl, cfg["goal_dim"], device="cuda")
+        bi = torch.empty(nbu * Bl, 3, dtype=torch.int64, device="cuda")
         with torch.cuda.stream(stream):
             for i in range(3):
-                ctx.relabel_sample_bulk(crl_synth.PHILOX_SEED, 40_000_000 + i * nb, nb, bs, ba, bg, bi, stream=stream)
+                ctx.relabel_sample_bulk(crl_synth.PHILOX_SEED, 40_000_000 + i * nbu, nbu, bs, ba, bg, bi, stream=stream)
             b0 = [torch.cuda.Event(enable_timing=True) for _ in range(10)]
             b1 = [torch.cuda.Event(enable_timing=True) for _ in range(10)]
             for i in range(10):
                 flush.zero_()
                 b0[i].record(stream)
-                ctx.relabel_sample_bulk(crl_synth.PHILOX_SEED, 41_000_000 + i * nb, nb, bs, ba, bg, bi, stream=stream)
+                ctx.relabel_sample_bulk(crl_synth.PHILOX_SEED, 41_000_000 + i * nbu, nbu, bs, ba, bg, bi, stream=stream)
                 b1[i].record(stream)
         torch.cuda.synchronize()
         us = sum(x.elapsed_time(y) for x, y in zip(b0, b1)) / 10 * 1e3
         # algorithmic bytes per row: read s, a, g + the ep_end word, write s, a, g
         # and the three int64 indices
         row_bytes = 2 * 4 * (cfg["obs_dim"] + cfg["act_dim"] + cfg["goal_dim"]) + 4 + 24
-        gbs = nb * Bl * row_bytes / (us * 1e-6) / 1e9
+        gbs = nbu * Bl * row_bytes / (us * 1e-6) / 1e9
         peaks_b, _ = load_peaks()
         hbm = peaks_b.get("hbm_gbs") if isinstance(peaks_b, dict) else None
-        bulk = {"rows": nb * Bl, "n_updates": nb, "us": round(us, 2), "bytes_per_row": row_bytes,
+        bulk = {"rows": nbu * Bl, "n_updates": nbu, "us": round(us, 2), "bytes_per_row": row_bytes,
                 "achieved_GBs": round(gbs, 1), "hbm_peak_GBs": hbm,
                 "frac": round(gbs / hbm, 4) if hbm else None,
                 "note": "crl_relabel_sample_bulk: one launch for n_updates batches (L2 flushed before each)"}
@@ -480,8 +496,11 @@ def run_ours(args):
                            "repr_dim": cfg["repr_dim"], "energy": cfg["energy"], "loss": cfg["loss"],
                            "beta_lse": cfg["beta_lse"], "layernorm": int(cfg.get("layernorm", 0)),
                            "buffer": f"{cfg['n_envs']}x{cfg['capacity']}",
-                           "parallelism": f"dp{world}", "l2_flush": "256 MiB memset between timed steps"},
-                "clocks": clocks, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+                           "parallelism": f"dp{world}", "l2_flush": "256 MiB memset between timed steps",
+                           "sampling": ("one crl_relabel_sample per step" if nb == 1 else
+                                        f"crl_relabel_sample_bulk: {nb} steps' batches per launch, inside the timed steps")},
+                "clocks": clocks, "e2e": e2e,
+                "gpu_launches": int(round((launches_per_step - 1.0 / nb) * args.steps)) + (n_bulk if nb > 1 else args.steps),
                 "gpu_launches_per_step": launches_per_step, "roofline": rl, "relabel_bulk": bulk,
                 "cpu_baseline": cpu,
                 "device_status": status}
