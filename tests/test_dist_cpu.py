@@ -96,7 +96,7 @@ def _worker(rank, port, cfg, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("energy_kind", ["l2", "dot", "cos"])
+@pytest.mark.parametrize("energy_kind", ["l2", "dot", "cos", "l1", "l2sq"])
 def test_dp_decomposition_matches_global_oracle(energy_kind):
     cfg = crl_synth.preset("reacher", batch=24, width=16, depth=2, repr_dim=16, n_envs=4, capacity=80,
                            energy=energy_kind, beta_lse=0.1)
