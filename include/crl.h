@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define CRL_ABI_VERSION 1
+#define CRL_ABI_VERSION 2   /* 2: crl_config gained layernorm, random_goal_alpha */
 
 #if defined(__GNUC__)
 #define CRL_API __attribute__((visibility("default")))

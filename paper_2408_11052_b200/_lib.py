@@ -98,7 +98,7 @@ def load_library(path: str = LIB_PATH):
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
         fn.restype, fn.argtypes = res, args
-    if lib.crl_abi_version() != 1:
+    if lib.crl_abi_version() != 2:
         raise RuntimeError("libcrl.so ABI version mismatch")
     _lib = lib
     return lib
