@@ -52,6 +52,21 @@ __device__ __forceinline__ float rsq_abs(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(fabsf(x)));
   return y;
 }
+// 1/sqrt(|x|) for a PAIR on the FMA pipe: exponent-halving integer guess (one IMAD.HI each),
+// two Newton steps y <- y (3/2 - (x/2) y^2) in packed FFMA2 / FMUL2 (relative error ~5e-6)
+__device__ __forceinline__ void rsq_pair_fma(float x0, float x1, float& r0, float& r1) {
+  x0 = fabsf(x0);
+  x1 = fabsf(x1);
+  int i0, i1;
+  asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(i0) : "r"(__float_as_int(x0)), "r"((int)0x80000000), "r"(0x5f375a86));
+  asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(i1) : "r"(__float_as_int(x1)), "r"((int)0x80000000), "r"(0x5f375a86));
+  const f32x2 nhx = f2_mul(f2_pack(x0, x1), f2_pack(-0.5f, -0.5f));
+  f32x2 y = f2_pack(__int_as_float(i0), __int_as_float(i1));
+  const f32x2 c15 = f2_pack(1.5f, 1.5f);
+#pragma unroll
+  for (int it = 0; it < 2; ++it) y = f2_mul(y, f2_fma(f2_mul(nhx, y), y, c15));
+  f2_unpack(y, r0, r1);
+}
 __device__ __forceinline__ float ex2_neg(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-x));
@@ -85,6 +100,13 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 }  // namespace gf
+
+#ifndef CRL_GF_RSQ_EMU
+#define CRL_GF_RSQ_EMU 0
+#endif
+// of every 4 logit pairs, this many take rsqrt on the FMA pipe instead of the MUFU (measured on
+// B200, N = 16384: 0 -> 271 us, 1 -> 270, 2 -> 286, 4 -> 331: not XU-bound, off)
+constexpr int kGfRsqEmuPairs = CRL_GF_RSQ_EMU;
 
 struct TcGradFArgs {
   int Na, Nb;
@@ -483,8 +505,12 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                                           f2_fma(f2_pack(L2e2, L2e2), b2, f2_pack(a_l2, a_l2)));
                   float d0, d1;
                   f2_unpack(d2, d0, d1);
-                  rs0 = gf::rsq_abs(d0);
-                  rs1 = gf::rsq_abs(d1);
+                  if (((2 * i4 + h) & 3) < kGfRsqEmuPairs) {        // rsqrt of this pair on the FMA pipe
+                    gf::rsq_pair_fma(d0, d1, rs0, rs1);
+                  } else {
+                    rs0 = gf::rsq_abs(d0);
+                    rs1 = gf::rsq_abs(d1);
+                  }
                   f2_unpack(f2_fma(d2, f2_pack(rs0, rs1), f2_pack(lr2, lr2)), t0, t1);
                 } else {
                   f2_unpack(f2_fma(v2, f2_pack(-gf::kLog2e, -gf::kLog2e), f2_pack(lr2, lr2)), t0, t1);
