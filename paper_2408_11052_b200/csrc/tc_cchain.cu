@@ -30,6 +30,7 @@ namespace tc {
 namespace cc {
 constexpr uint32_t CHUNK = 128 * 128;            // 128 rows x 64 bf16 (SW128 K chunk)
 constexpr uint32_t WSTAGE = 4 * 64 * 64 * 2;     // 4 K-chunks x (64 K rows x 64 N) = 32 KB
+constexpr uint32_t WSTAGE0 = 5 * 64 * 64 * 2;    // stage 0 also holds a 5-chunk first layer (in0 <= 320)
 constexpr int NC = 4;                            // cluster size = hidden width / 64
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -91,8 +92,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAct = smem;                                        // [2][4] chunks (layer-parity buffers)
-  uint8_t* sW = sAct + 2 * NC * CHUNK;                         // [2] weight stages
-  float* sBias = reinterpret_cast<float*>(sW + 2 * WSTAGE);    // [kCChainMaxL][64]
+  uint8_t* sX4 = sAct + 2 * NC * CHUNK;                        // 5th K chunk of a wide first-layer input
+  uint8_t* sW = sX4 + CHUNK;                                   // weight stages: 0 (40 KB), 1 (32 KB)
+  float* sBias = reinterpret_cast<float*>(sW + WSTAGE0 + WSTAGE);   // [kCChainMaxL][64]
   float* sStat = sBias + kCChainMaxL * 64;                     // [128] row-stat hand-off
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 128);
   uint64_t* a0_full = bars;                 // first-layer input (from HBM) in act buffer 0
@@ -137,7 +139,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
     for (int kc = 0; kc < nkc; ++kc)
       // FWD: W_l [in][out] MN-major slice, box {64 (out), 64 (in)} at (n0, 64 kc)
       // BWD: W_l rows n0.. as the K-major B of dZ W^T, box {64 (out = k), 64 (in = n)}
-      tma_load_2d(sW + st * WSTAGE + kc * 8192, &mp.w[s], &w_full[st], MODE == 0 ? n0 : 64 * kc,
+      tma_load_2d(sW + (st ? WSTAGE0 : 0u) + kc * 8192, &mp.w[s], &w_full[st], MODE == 0 ? n0 : 64 * kc,
                   MODE == 0 ? 64 * kc : n0);
   };
   // the weights do not depend on the predecessor kernel: request the first two layers now
@@ -164,7 +166,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
     // ------------------------------------------------------------------ TMA producer
     const int nch0 = (E.layer[0].K + 63) / 64;
     mbar_expect_tx(a0_full, (uint32_t)nch0 * CHUNK);
-    for (int k = 0; k < nch0; ++k) tma_load_2d(sAct + k * CHUNK, &mp.a0, a0_full, 64 * k, m0);
+    for (int k = 0; k < nch0; ++k) tma_load_2d(k < NC ? sAct + k * CHUNK : sX4, &mp.a0, a0_full, 64 * k, m0);
     for (int s = 2; s < L; ++s) {
       if (!active(s)) continue;
       mbar_wait(&w_empty[s & 1], ((s >> 1) - 1) & 1);
@@ -182,7 +184,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
       if (s == 0) mbar_wait(a0_full, 0);
       mbar_wait(&w_full[s & 1], (s >> 1) & 1);
       const uint32_t a_base = smem_u32(sAct + (s & 1) * NC * CHUNK);
-      const uint32_t w_base = smem_u32(sW + (s & 1) * WSTAGE);
+      const uint32_t w_base = smem_u32(sW + ((s & 1) ? WSTAGE0 : 0u));
       const uint32_t idesc = idesc_bf16_f32(128, 64, false, MODE == 0);
       for (int i = 0; i < nkc; ++i) {
         const int kc = s == 0 ? i : (int)((c + i) % NC);
@@ -194,7 +196,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t ad = smem_desc_sw128(a_base + kc * CHUNK + ks * 32, 16, 1024);
+          const uint32_t a_chunk = (s == 0 && kc == NC) ? smem_u32(sX4) : a_base + kc * CHUNK;
+          const uint64_t ad = smem_desc_sw128(a_chunk + ks * 32, 16, 1024);
           const uint64_t bd = MODE == 0 ? smem_desc_sw128(w_base + kc * 8192 + ks * 2048, 8192, 1024)
                                         : smem_desc_sw128(w_base + kc * 8192 + ks * 32, 16, 1024);
           mma_bf16(acc, ad, bd, idesc, (i | ks) != 0);
@@ -379,10 +382,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
-size_t tc_cchain_smem() { return 1024 + 2 * cc::NC * cc::CHUNK + 2 * cc::WSTAGE + kCChainMaxL * 64 * 4 + 512 + 256; }
+size_t tc_cchain_smem() {
+  return 1024 + (2 * cc::NC + 1) * cc::CHUNK + cc::WSTAGE0 + cc::WSTAGE + kCChainMaxL * 64 * 4 + 512 + 256;
+}
 
 bool tc_cchain_supported(int in0, int width, int D, int depth) {
-  return width == 256 && D == 64 && in0 <= 256 && depth >= 1 && depth + 1 <= kCChainMaxL;
+  return width == 256 && D == 64 && in0 <= 320 && depth >= 1 && depth + 1 <= kCChainMaxL;
 }
 
 template <int MODE>
