@@ -186,7 +186,9 @@ CRL_API crl_status crl_relabel_sample_bulk(crl_ctx* ctx, uint64_t seed, uint64_t
  *   are never stored; dL/dl consumed in-pass; reverse mode through both encoders; gradients
  *   all-reduced across ranks; one fused bias-corrected Adam step on `params` (A-15).
  *   s [B_l][obs_dim], a [B_l][act_dim], g [B_l][goal_dim]: host or device.
- *   loss_out: float[4] = (L_fwd, L_bwd, penalty, total), host or device, may be NULL.
+ *   loss_out: float[4] = (L_fwd, L_bwd, penalty, total), host or device, may be NULL
+ *   (page-locked host memory is written in place by the loss kernel; other host memory by a
+ *   device-to-host copy on `stream`).
  *   grads_out: device float[n_params] pre-Adam global gradients, or NULL.
  * The device sequence is captured once per distinct pointer tuple into a CUDA graph and
  * replayed.  If the gradient or loss is non-finite the Adam step is skipped and the status

@@ -723,6 +723,16 @@ static bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// page-locked host memory the device can address directly (UVA): its device pointer, else null
+static const void* mapped_host_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float* a, const float* g,
                                       float* loss_out, float* grads_out, void* stream) {
   if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
@@ -732,22 +742,29 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
   const crl_config& k = ctx->cfg;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t Bl = k.batch_local;
-  // host batch -> staging (end-to-end path)
-  if (!is_device_ptr(s)) {
-    CU(cudaMemcpyAsync(ctx->stage_s, s, Bl * k.obs_dim * 4, cudaMemcpyHostToDevice, st));
-    s = ctx->stage_s;
-  }
-  if (!is_device_ptr(a)) {
-    CU(cudaMemcpyAsync(ctx->stage_a, a, Bl * k.act_dim * 4, cudaMemcpyHostToDevice, st));
-    a = ctx->stage_a;
-  }
-  if (!is_device_ptr(g)) {
-    CU(cudaMemcpyAsync(ctx->stage_g, g, Bl * k.goal_dim * 4, cudaMemcpyHostToDevice, st));
-    g = ctx->stage_g;
-  }
+  // host batch (end-to-end path): copied to the device staging buffers (reading page-locked
+  // host memory in place from the input kernel was measured slower: Ant e2e 9.2k -> 7.4k
+  // steps/s, the per-element host-link latency); a page-locked host loss is written in place
+  // by the loss kernel (CRL_NO_ZERO_COPY: a device-to-host copy instead)
+  const bool zc = !std::getenv("CRL_NO_ZERO_COPY");
+  auto stage_in = [&](const float*& p, float* stage, size_t n) -> crl_status {
+    if (is_device_ptr(p)) return CRL_OK;
+    CU(cudaMemcpyAsync(stage, p, n * 4, cudaMemcpyHostToDevice, st));
+    p = stage;
+    return CRL_OK;
+  };
+  crl_status rs0;
+  if ((rs0 = stage_in(s, ctx->stage_s, Bl * k.obs_dim)) != CRL_OK) return rs0;
+  if ((rs0 = stage_in(a, ctx->stage_a, Bl * k.act_dim)) != CRL_OK) return rs0;
+  if ((rs0 = stage_in(g, ctx->stage_g, Bl * k.goal_dim)) != CRL_OK) return rs0;
   float* loss_dev = ctx->loss_dev;
-  const bool loss_host = loss_out && !is_device_ptr(loss_out);
+  bool loss_host = loss_out && !is_device_ptr(loss_out);
   if (loss_out && !loss_host) loss_dev = loss_out;
+  if (loss_host && zc)
+    if (const void* d = mapped_host_ptr(loss_out)) {
+      loss_dev = static_cast<float*>(const_cast<void*>(d));
+      loss_host = false;
+    }
 
   if (ctx->prof_on) {                    // eager, event-bracketed launches
     spin_kernel<<<1, 1, 0, st>>>(300000ull);

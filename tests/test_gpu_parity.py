@@ -271,6 +271,30 @@ def test_critic_step_graph_replay_and_host_buffers():
     assert ctx.launch_count() > 0
 
 
+@pytest.mark.parametrize("zero_copy", [True, False])
+def test_critic_step_bf16_host_buffers(zero_copy, monkeypatch):
+    """bf16 path with page-locked host s, a, g (staged by copies) and a host loss written in
+    place by the loss kernel (zero copy) or copied back (CRL_NO_ZERO_COPY) -- both equal the
+    device-buffer run of the same batch bitwise (same kernels, same inputs)."""
+    if not zero_copy:
+        monkeypatch.setenv("CRL_NO_ZERO_COPY", "1")
+    cfg = crl_synth.preset("ant", batch=256, precision="bf16")
+    s, a, g = crl_synth.random_batch(cfg, 256, seed=8)
+    ctx_d, _ = make_ctx(cfg)
+    loss_d = torch.zeros(4, device="cuda")
+    ctx_d.critic_step(*(torch.from_numpy(x).cuda() for x in (s, a, g)), loss_d)
+    ctx_h, _ = make_ctx(cfg)
+    hs, ha, hg = (torch.from_numpy(x).pin_memory() for x in (s, a, g))
+    loss_h = torch.zeros(4).pin_memory()
+    for _ in range(2):                               # second call replays the captured graph
+        ctx_h.critic_step(hs, ha, hg, loss_h)
+        torch.cuda.synchronize()
+        if _ == 0:
+            first = loss_h.numpy().copy()
+    assert np.array_equal(first.view(np.uint32), loss_d.cpu().numpy().view(np.uint32))
+    assert np.isfinite(loss_h.numpy()).all() and ctx_h.status() == 0
+
+
 def test_critic_step_nonfinite_sets_status_and_skips_adam():
     cfg = crl_synth.preset("reacher", batch=64, width=32)
     ctx, params = make_ctx(cfg)
