@@ -17,7 +17,8 @@
  *    pointer with cudaPointerGetAttributes and copies host data itself, on `stream`).
  *  - Ownership: the caller allocates and owns every buffer, including the ones passed in
  *    crl_memory at create time; the library keeps non-owning pointers, which must outlive
- *    the context.  The library performs no device allocation after crl_create.
+ *    the context.  The library performs no device allocation after crl_create (crl_create
+ *    also allocates a small page-locked HOST ring for host batches of crl_critic_step).
  *  - Asynchrony: calls validate their arguments on the host synchronously and return
  *    CRL_EINVAL / CRL_ESTATE at once; device work is enqueued on `stream` (a cudaStream_t,
  *    passed as void*; NULL = legacy default stream) and the call returns without syncing.

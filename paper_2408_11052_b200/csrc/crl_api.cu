@@ -243,6 +243,8 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   *scr_bytes = (s.off + 255) & ~(size_t)255;
 }
 
+static bool make_host_ring(crl_ctx* ctx);
+
 static crl_status validate(const crl_config* k, crl_ctx* ctx) {
   if (!k) return fail(ctx, CRL_EINVAL, "cfg is NULL");
   if (k->obs_dim <= 0 || k->act_dim <= 0 || k->goal_dim <= 0)
@@ -386,6 +388,7 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaStreamCreateWithFlags(&ctx->cap_body, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      !make_host_ring(ctx) ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess)
     return cleanup(fail(nullptr, CRL_ECUDA, "context initialisation failed"));
@@ -418,6 +421,9 @@ crl_status crl_destroy(crl_ctx* ctx) {
   if (ctx->cap_body) cudaStreamDestroy(ctx->cap_body);
   if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  for (int i = 0; i < crl_ctx::kHostSlots; ++i)
+    if (ctx->h_ev[i]) cudaEventDestroy(ctx->h_ev[i]);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
   return CRL_OK;
@@ -714,6 +720,19 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
   return CRL_OK;
 }
 
+// the page-locked host ring of the end-to-end path (host memory; no device allocation)
+static bool make_host_ring(crl_ctx* ctx) {
+  const crl_config& k = ctx->cfg;
+  ctx->h_stage_bytes = (size_t)(reinterpret_cast<char*>(ctx->stage_g) - reinterpret_cast<char*>(ctx->stage_s)) +
+                       (size_t)k.batch_local * k.goal_dim * 4;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage), ctx->h_stage_bytes * crl_ctx::kHostSlots,
+                    cudaHostAllocDefault) != cudaSuccess)
+    return false;
+  for (int i = 0; i < crl_ctx::kHostSlots; ++i)
+    if (cudaEventCreateWithFlags(&ctx->h_ev[i], cudaEventDisableTiming) != cudaSuccess) return false;
+  return true;
+}
+
 static bool is_device_ptr(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -747,6 +766,21 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
   // steps/s, the per-element host-link latency); a page-locked host loss is written in place
   // by the loss kernel (CRL_NO_ZERO_COPY: a device-to-host copy instead)
   const bool zc = !std::getenv("CRL_NO_ZERO_COPY");
+  if (ctx->h_stage && !is_device_ptr(s) && !is_device_ptr(a) && !is_device_ptr(g)) {
+    // host batch: gathered into a page-locked ring slot laid out like the device staging, then
+    // ONE host-to-device copy (three small copies cost three DMA latencies on the timeline)
+    const int slot = ctx->h_slot;
+    ctx->h_slot = (slot + 1) % crl_ctx::kHostSlots;
+    CU(cudaEventSynchronize(ctx->h_ev[slot]));            // the slot's previous copy is done
+    char* hb = ctx->h_stage + (size_t)slot * ctx->h_stage_bytes;
+    char* d0 = reinterpret_cast<char*>(ctx->stage_s);
+    std::memcpy(hb, s, Bl * k.obs_dim * 4);
+    std::memcpy(hb + (reinterpret_cast<char*>(ctx->stage_a) - d0), a, Bl * k.act_dim * 4);
+    std::memcpy(hb + (reinterpret_cast<char*>(ctx->stage_g) - d0), g, Bl * k.goal_dim * 4);
+    CU(cudaMemcpyAsync(ctx->stage_s, hb, ctx->h_stage_bytes, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(ctx->h_ev[slot], st));
+    s = ctx->stage_s; a = ctx->stage_a; g = ctx->stage_g;
+  }
   auto stage_in = [&](const float*& p, float* stage, size_t n) -> crl_status {
     if (is_device_ptr(p)) return CRL_OK;
     CU(cudaMemcpyAsync(stage, p, n * 4, cudaMemcpyHostToDevice, st));

@@ -133,6 +133,13 @@ struct crl_ctx {
   unsigned* loss_ticket = nullptr;
   int *status = nullptr, *adam_t = nullptr, *skip = nullptr;
   float *stage_s = nullptr, *stage_a = nullptr, *stage_g = nullptr;
+  // end-to-end path: page-locked host ring mirroring [stage_s .. stage_g] so a host batch
+  // travels in ONE host-to-device copy (slots reused once their copy has completed)
+  static constexpr int kHostSlots = 4;
+  char* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  int h_slot = 0;
+  cudaEvent_t h_ev[kHostSlots] = {};
   // runtime
   cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr, cap_stream3 = nullptr, cap_stream4 = nullptr;
   cudaStream_t cap_body = nullptr;        // captures the bodies of conditional graph nodes
