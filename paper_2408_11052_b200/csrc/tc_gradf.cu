@@ -163,6 +163,14 @@ __device__ void gradf_loss_finish(const TcGradFArgs& p, int a0, float s1, float 
   else *p.adam_t += 1;
 }
 
+// the positive-pair logit l_ii from the fp32 representations (App. A.2)
+template <int ENERGY>
+__device__ __forceinline__ float gf_diag_logit(float x, float na, float nb) {
+  if (ENERGY == CRL_ENERGY_L2) return -sqrtf(x + kEpsL2);
+  if (ENERGY == CRL_ENERGY_COS) return x / (fmaxf(sqrtf(na), kEpsCos) * fmaxf(sqrtf(nb), kEpsCos));
+  return x;
+}
+
 // one warp (warp 3, while the epilogue works through a long column range)
 template <int ENERGY>
 __device__ void gradf_loss_rows_warp(const TcGradFArgs& p, int a0, int t) {
@@ -172,7 +180,7 @@ __device__ void gradf_loss_rows_warp(const TcGradFArgs& p, int a0, int t) {
     if (i >= p.Na) break;
     const float4* a = reinterpret_cast<const float4*>(p.phi32 + (size_t)i * 64);
     const float4* b = reinterpret_cast<const float4*>(p.psi32 + (size_t)i * 64);
-    float x = 0.f;
+    float x = 0.f, na = 0.f, nb = 0.f;
 #pragma unroll 4
     for (int k = 0; k < 16; ++k) {
       const float4 u = a[k], v = b[k];
@@ -182,8 +190,12 @@ __device__ void gradf_loss_rows_warp(const TcGradFArgs& p, int a0, int t) {
       } else {
         x = fmaf(u.x, v.x, x); x = fmaf(u.y, v.y, x); x = fmaf(u.z, v.z, x); x = fmaf(u.w, v.w, x);
       }
+      if (ENERGY == CRL_ENERGY_COS) {
+        na = fmaf(u.x, u.x, na); na = fmaf(u.y, u.y, na); na = fmaf(u.z, u.z, na); na = fmaf(u.w, u.w, na);
+        nb = fmaf(v.x, v.x, nb); nb = fmaf(v.y, v.y, nb); nb = fmaf(v.z, v.z, nb); nb = fmaf(v.w, v.w, nb);
+      }
     }
-    const float l = ENERGY == CRL_ENERGY_L2 ? -sqrtf(x + kEpsL2) : x;
+    const float l = gf_diag_logit<ENERGY>(x, na, nb);
     const float lr = p.lr[i], lc = p.lc[i];
     s1 += lr - l; s2 += lc - l; s3 += lr * lr;
   }
@@ -201,7 +213,7 @@ __device__ void gradf_loss_rows_epi(const TcGradFArgs& p, int a0, int t) {
   const bool ok = i < p.Na;
   const float4* a = reinterpret_cast<const float4*>(p.phi32 + (size_t)(ok ? i : 0) * 64) + 4 * q4;
   const float4* b = reinterpret_cast<const float4*>(p.psi32 + (size_t)(ok ? i : 0) * 64) + 4 * q4;
-  float x = 0.f;
+  float x = 0.f, na = 0.f, nb = 0.f;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const float4 u = a[k], v = b[k];
@@ -211,12 +223,20 @@ __device__ void gradf_loss_rows_epi(const TcGradFArgs& p, int a0, int t) {
     } else {
       x = fmaf(u.x, v.x, x); x = fmaf(u.y, v.y, x); x = fmaf(u.z, v.z, x); x = fmaf(u.w, v.w, x);
     }
+    if (ENERGY == CRL_ENERGY_COS) {
+      na = fmaf(u.x, u.x, na); na = fmaf(u.y, u.y, na); na = fmaf(u.z, u.z, na); na = fmaf(u.w, u.w, na);
+      nb = fmaf(v.x, v.x, nb); nb = fmaf(v.y, v.y, nb); nb = fmaf(v.z, v.z, nb); nb = fmaf(v.w, v.w, nb);
+    }
   }
   x += __shfl_xor_sync(0xffffffffu, x, 1);
   x += __shfl_xor_sync(0xffffffffu, x, 2);
+  if (ENERGY == CRL_ENERGY_COS) {
+    na += __shfl_xor_sync(0xffffffffu, na, 1); na += __shfl_xor_sync(0xffffffffu, na, 2);
+    nb += __shfl_xor_sync(0xffffffffu, nb, 1); nb += __shfl_xor_sync(0xffffffffu, nb, 2);
+  }
   float s1 = 0.f, s2 = 0.f, s3 = 0.f;
   if (ok && q4 == 0) {
-    const float l = ENERGY == CRL_ENERGY_L2 ? -sqrtf(x + kEpsL2) : x;
+    const float l = gf_diag_logit<ENERGY>(x, na, nb);
     const float lr = p.lr[i], lc = p.lc[i];
     s1 = lr - l; s2 = lc - l; s3 = lr * lr;
   }
@@ -259,6 +279,7 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
   using C = GfCfg;
   constexpr int BNT = C::BNT, STAGES = C::STAGES, D = C::D;
   constexpr bool L2 = ENERGY == CRL_ENERGY_L2;
+  constexpr bool COS = ENERGY == CRL_ENERGY_COS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // sOnes sits right after sA: the dB MMA reads B = [A | 1] as one MN-major operand whose
@@ -415,7 +436,10 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
     const float rmask = rv ? 1.f : 0.f;
     constexpr float L2e2 = gf::kLog2e * gf::kLog2e;
     const float a_l2 = (astat + kEpsL2) * L2e2;
-    const float lsc = L2 ? gf::kLog2e : 1.f;      // L2: w = g rs' L
+    // L2: w = g rs' L.  cos: l = (a.b) r_i s_j and the MMA operand is w' = g r_i s_j (both
+    // sides' dot-form partials come out pre-scaled; grad_merge projects them, A-05)
+    const float lsc = L2 ? gf::kLog2e : (COS ? astat : 1.f);
+    const float nLr = -gf::kLog2e * astat;        // cos: -L r_i
     const float EiL = Ei * lsc, ArowL = Arow * lsc, cc0L = cc0 * lsc;
     const uint32_t w_row = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
     const uint32_t bar_id = 2 + wgid;
@@ -512,6 +536,8 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                     rs1 = gf::rsq_abs(d1);
                   }
                   f2_unpack(f2_fma(d2, f2_pack(rs0, rs1), f2_pack(lr2, lr2)), t0, t1);
+                } else if (COS) {
+                  f2_unpack(f2_fma(f2_mul(v2, b2), f2_pack(nLr, nLr), f2_pack(lr2, lr2)), t0, t1);
                 } else {
                   f2_unpack(f2_fma(v2, f2_pack(-gf::kLog2e, -gf::kLog2e), f2_pack(lr2, lr2)), t0, t1);
                 }
@@ -524,6 +550,7 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                   wv = f2_mul(wv, f2_pack(rs0, rs1));
                   wsum2 = f2_add(wsum2, wv);
                 }
+                if (COS) wv = f2_mul(wv, b2);
                 f2_unpack(wv, w[i], w[i + 1]);
               }
             } else {                                      // exact: q = 2^(l2 - lse2'_j)
@@ -538,6 +565,8 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                   const float d2 = fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2));
                   rs = gf::rsq_abs(d2);
                   l2v = -fabsf(d2) * rs;
+                } else if (COS) {
+                  l2v = v * bb[u] * (-nLr);
                 } else {
                   l2v = v * gf::kLog2e;
                 }
@@ -545,6 +574,7 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                 const float qe = gf::ex2(l2v - ff[u] * gf::kLog2e);
                 float wv = fmaf(gf::ex2(l2v - lr2), ArowL, qe * cc0L) * rmask;
                 if (L2) { wv *= rs; wsum2 = f2_add(wsum2, f2_pack(wv, 0.f)); }
+                if (COS) wv *= bb[u];
                 w[i] = wv;
               }
             }
@@ -611,7 +641,9 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
 // ------------------------------------------------------------------------------- host side
 bool make_map_f32(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
 
-bool tc_gradf_supports(int D, int energy) { return D == 64 && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_DOT); }
+bool tc_gradf_supports(int D, int energy) {
+  return D == 64 && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_DOT || energy == CRL_ENERGY_COS);
+}
 
 // column splits minimising the makespan (waves x tiles per CTA) of the rb x S grid, <= 16
 int tc_gradf_splits(int Na, int Nb, int num_sms) {
@@ -668,13 +700,15 @@ cudaError_t tc_grad_fused(int energy, const CUtensorMap& mA, const CUtensorMap& 
   p.loss_acc = loss.acc; p.loss_out = loss.out; p.skip = loss.skip; p.adam_t = loss.adam_t; p.status = loss.status;
   p.loss_cf = loss.c_f; p.loss_cb = loss.c_b; p.loss_beta = loss.beta;
   p.dbg = std::getenv("CRL_GF_DBG") ? std::atoi(std::getenv("CRL_GF_DBG")) : 0;
-  cudaError_t e = energy == CRL_ENERGY_L2 ? launch_gf<CRL_ENERGY_L2>(mA, mB, mDB, p, S, st)
-                                          : launch_gf<CRL_ENERGY_DOT>(mA, mB, mDB, p, S, st);
+  cudaError_t e = energy == CRL_ENERGY_L2    ? launch_gf<CRL_ENERGY_L2>(mA, mB, mDB, p, S, st)
+                  : energy == CRL_ENERGY_COS ? launch_gf<CRL_ENERGY_COS>(mA, mB, mDB, p, S, st)
+                                             : launch_gf<CRL_ENERGY_DOT>(mA, mB, mDB, p, S, st);
   if (e != cudaSuccess) return e;
   const float Cdiag = invN * (c_r + c_c);
   // row side; column side ("rows" are the B vectors, the pair partner of B_j is A_j): one launch
-  const GradMergeArgs g0{part_da, part_rs, A, a_stat, B, b_stat, 0, Cdiag, Na, 64, S, dA, dAb};
-  const GradMergeArgs g1{db_acc, cs_acc, B, b_stat, A, a_stat, 0, Cdiag, Nb, 64, 1, dB, dBb};
+  const int pre = energy == CRL_ENERGY_COS;        // cos partials carry r_i s_j already
+  const GradMergeArgs g0{part_da, part_rs, A, a_stat, B, b_stat, 0, Cdiag, Na, 64, S, dA, dAb, pre};
+  const GradMergeArgs g1{db_acc, cs_acc, B, b_stat, A, a_stat, 0, Cdiag, Nb, 64, 1, dB, dBb, pre};
   return launch_grad_merge2(energy, g0, g1, st);
 }
 

@@ -542,7 +542,7 @@ cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUten
 cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, const __nv_bfloat16* A,
                               const float* a_stat, const __nv_bfloat16* Bg, const float* b_stat, int row_offset,
                               float Cdiag, int Na, int D, int S, float* out, __nv_bfloat16* outb, cudaStream_t st) {
-  const GradMergeArgs g{part, prs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, out, outb};
+  const GradMergeArgs g{part, prs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, out, outb, 0};
   const dim3 grid((Na * 32 + 255) / 256);
   if (energy == CRL_ENERGY_L2) return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2>, grid, dim3(256), 0, st, g);
   if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g);

@@ -17,6 +17,7 @@ struct GradMergeArgs {
   const float* part; const float* prs; const __nv_bfloat16* A; const float* a_stat;
   const __nv_bfloat16* Bg; const float* b_stat; int row_offset; float Cdiag; int Na, D, S;
   float* out; __nv_bfloat16* outb;
+  int pre;   // cos: part already carries the row's own 1/|A_i| (fused pass, w' = g r_i s_j)
 };
 
 template <int ENERGY>
@@ -49,6 +50,7 @@ __device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, in
   if (ENERGY == CRL_ENERGY_L2) diag = Cdiag / sqrtf(warp_sum(d2) + kEpsL2);   // times (A_i - B_i)
   const float invb = ENERGY == CRL_ENERGY_COS ? b_stat[row_offset + w] : 0.f;
   const float inv = ENERGY == CRL_ENERGY_COS ? a_stat[w] : 0.f;
+  const float osc = g.pre ? 1.f : inv;                   // the final 1/|A_i| factor
   float pr = 0.f;
   for (int c = 0; c < D / 32; ++c) {
     const int k = lane + 32 * c;
@@ -57,7 +59,7 @@ __device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, in
     if (ENERGY == CRL_ENERGY_L2) v += diag * (av[c] - bv[c]) - rs * av[c];
     if (ENERGY == CRL_ENERGY_DOT) v -= Cdiag * bv[c];
     if (ENERGY == CRL_ENERGY_COS) {
-      v -= Cdiag * invb * bv[c];
+      v -= Cdiag * invb * (g.pre ? inv : 1.f) * bv[c];
       pr = fmaf(v, av[c] * inv, pr);
     }
     acc[c] = v;
@@ -68,7 +70,7 @@ __device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, in
     float v = acc[c];
     if (ENERGY == CRL_ENERGY_COS) {
       const float u = av[c] * inv;
-      v = inv < 1.f / kEpsCos ? (v - pr * u) * inv : v * inv;
+      v = inv < 1.f / kEpsCos ? (v - pr * u) * osc : v * osc;
     }
     out[(size_t)w * D + k] = v;
     outb[(size_t)w * D + k] = __float2bfloat16_rn(v);

@@ -380,14 +380,14 @@ def test_pair_losses_bf16_or_dp_unsupported(loss):
         make_ctx(cfg)
 
 
-@pytest.mark.parametrize("preset", ["sweep16384", "netscale"])
-def test_critic_step_bf16_full_size_sampled(preset):
+@pytest.mark.parametrize("preset,energy", [("sweep16384", None), ("sweep16384", "cos"), ("netscale", None)])
+def test_critic_step_bf16_full_size_sampled(preset, energy):
     """configs[3] at its largest batch and configs[4] (4 x 1024, D 256) at full size, in the
     launch configuration bench.py times: the oracle recomputes sampled outputs one by one --
     phi / psi rows, row and column logsumexps (each needs the oracle's encoders over the whole
     batch, then O(N D) per sampled row) -- against the bf16 bar (2e-2)."""
     from oracle import mlp as omlp
-    cfg = crl_synth.preset(preset, precision="bf16")
+    cfg = crl_synth.preset(preset, precision="bf16", **({"energy": energy} if energy else {}))
     N = cfg["batch"]
     ctx, params = make_ctx(cfg)
     s, a, g = crl_synth.random_batch(cfg, N, seed=13)
@@ -481,6 +481,7 @@ def test_critic_step_bf16_fused_chain(preset, over, monkeypatch):
     ("CRL_NO_FUSED_STATS", "l2"),         # two-call online-max statistics only
     ("CRL_NO_FUSED_GRAD", "l2"),          # two-call gradient pass (row call + column call)
     ("CRL_NO_FUSED_GRAD", "dot"),
+    ("CRL_NO_FUSED_GRAD", "cos"),
     ("CRL_FORCE_STATS_FALLBACK,CRL_COND_NODE", "l2"),   # fallback as a conditional graph node
 ])
 def test_critic_step_bf16_stats_paths(knob, energy, monkeypatch):
