@@ -163,6 +163,9 @@ def stage_work(stage, cfg, N, Bl):
         # one sqrt per pass) and 2 for dot/cos; four launches share it -> 1/4 per launch.
         per = (4.0 if cfg["energy"] == "l2" else 2.0) / 4.0
         return Bl * N * per, "op", "xu"
+    if stage == "lse_pair":
+        # both sides' online-max statistics in one launch: half of the stage's count
+        return Bl * N * (4.0 if cfg["energy"] == "l2" else 2.0) / 2.0, "op", "xu"
     if stage in ("lse_row", "lse_col"):
         # fp32 path: the logits GEMM (2 N^2 D, counted once for both orientations) -> N_l N D
         return Bl * N * D * 1.0, "flop", "alu"
@@ -203,9 +206,10 @@ def stage_work(stage, cfg, N, Bl):
 def roofline(stages, cfg, N, Bl, peaks, peak_kind, clocks, traffic_db):
     known = {k: v for k, v in stages.items() if stage_work(k, cfg, N, Bl)[0] is not None}
     if "lse_fused" in stages:
-        # lse_row / lse_col are then the exact fallback, gated off by a device flag (early exit)
+        # lse_pair (lse_row / lse_col) is then the exact fallback, gated off by a device flag (early exit)
         known.pop("lse_row", None)
         known.pop("lse_col", None)
+        known.pop("lse_pair", None)
     if not known:
         return None                      # --profile-steps 0: no per-stage measurement
     name, (ms, cnt) = max(known.items(), key=lambda kv: kv[1][0])

@@ -140,6 +140,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       c->lg_part_s = s.take<float>((size_t)2 * c->lg_splits * Bl);
       c->lg_part_rs = s.take<float>((size_t)2 * c->lg_splits * Bl);
       c->lg_part_da = s.take<float>((size_t)2 * c->lg_splits * Bl * D);
+      c->lg_ticket = s.take<int>((size_t)2 * ((Bl + 127) / 128));
       c->use_stats = W == 1 && tc_stats_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_STATS");
       if (c->use_stats) {
         c->st_splits = tc_stats_splits(Bl, N, 148);
@@ -385,6 +386,7 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaMemset(ctx->open_start, 0, (size_t)cfg->n_envs_local * 4) != cudaSuccess ||
       cudaMemset(ctx->status, 0, 4) != cudaSuccess || cudaMemset(ctx->adam_t, 0, 4) != cudaSuccess ||
       cudaMemset(ctx->skip, 0, 4) != cudaSuccess || cudaMemset(ctx->loss_ticket, 0, 4) != cudaSuccess ||
+      (ctx->lg_ticket && cudaMemset(ctx->lg_ticket, 0, (size_t)2 * ((cfg->batch_local + 127) / 128) * 4) != cudaSuccess) ||
       (ctx->has_actor && (cudaMemset(ctx->a_t, 0, 4) != cudaSuccess || cudaMemset(ctx->a_skip, 0, 4) != cudaSuccess ||
                           cudaMemset(ctx->ent_mv, 0, 8) != cudaSuccess || cudaMemset(ctx->ent_t, 0, 4) != cudaSuccess)) ||
       cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||

@@ -192,6 +192,7 @@ struct crl_ctx {
   tc::ChainMaps chain_fwd[2], chain_bwd[2];
   tc::ChainParams chain_fwd_p{}, chain_bwd_p{};
   float *lg_part_m = nullptr, *lg_part_s = nullptr, *lg_part_da = nullptr, *lg_part_rs = nullptr;
+  int* lg_ticket = nullptr;        // [2][row blocks] in-kernel LSE merge tickets (zeroed at create)
   CUtensorMap lg_row_A, lg_row_B, lg_col_A, lg_col_B;
   // fused row + column statistics in one pass (tc_stats.cu; W = 1, L2 / cos, D <= 128)
   bool use_stats = false;

@@ -412,6 +412,14 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     }
     const int* gate = nullptr;
     cudaGraphConditionalHandle cond = 0;
+    // the two-call online-max statistics, both sides in one launch (merged in-kernel):
+    // row side A = Phi (lse_row / fac_row, penalty coefficient), column side A = Psi
+    const tc::LseSide row_side{&ctx->lg_row_A, &ctx->lg_row_B, ctx->stat_phi + row_off, ctx->stat_psi,
+                               ctx->lg_part_m, ctx->lg_part_s, ctx->lse_row, ctx->fac_row, invN * c_f,
+                               2.f * invN * k.beta_lse};
+    const tc::LseSide col_side{&ctx->lg_col_A, &ctx->lg_col_B, ctx->stat_psi + row_off, ctx->stat_phi,
+                               ctx->lg_part_m + (size_t)S * Bl, ctx->lg_part_s + (size_t)S * Bl, ctx->lse_col,
+                               ctx->fac_col, invN * c_b, 0.f};
     if (ctx->use_stats) {
       // one pass: row AND column sums of e^l (no running max: L2 / cos logits are bounded
       // above); the exact online-max pass below then runs only if a sum under/overflowed:
@@ -449,27 +457,27 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
       CU(cudaStreamBeginCaptureToGraph(ctx->cap_body, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
                                        cudaStreamCaptureModeRelaxed));
-      CU(tc::tc_logits_lse(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, ctx->stat_psi + row_off, ctx->stat_phi,
-                           S, ctx->lg_part_m + (size_t)S * Bl, ctx->lg_part_s + (size_t)S * Bl, ctx->lse_col,
-                           ctx->fac_col, ctx->fac_ok, invN * c_b, 0.f, nullptr, ctx->cap_body));
-      CU(tc::tc_logits_lse(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off, ctx->stat_psi,
-                           S, ctx->lg_part_m, ctx->lg_part_s, ctx->lse_row, ctx->fac_row, ctx->fac_ok, invN * c_f,
-                           2.f * invN * k.beta_lse, nullptr, ctx->cap_body));
+      CU(tc::tc_logits_lse_pair(D, k.energy, row_side, col_side, Bl, N, S, ctx->fac_ok, ctx->lg_ticket, nullptr,
+                                ctx->cap_body));
       cudaGraph_t body_out = nullptr;
       CU(cudaStreamEndCapture(ctx->cap_body, &body_out));
     } else {
-    fork2(ctx, st, st2);
-    { Stage sg(ctx, st2, "lse_col");
-      CU(tc::tc_logits_lse(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, ctx->stat_psi + row_off,
-                           ctx->stat_phi, S, ctx->lg_part_m + (size_t)S * Bl, ctx->lg_part_s + (size_t)S * Bl,
-                           ctx->lse_col, ctx->fac_col, ctx->fac_ok, invN * c_b, 0.f, gate, st2));
-      nl += 2; }
-    { Stage sg(ctx, st, "lse_row");
-      CU(tc::tc_logits_lse(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off,
-                           ctx->stat_psi, S, ctx->lg_part_m, ctx->lg_part_s, ctx->lse_row, ctx->fac_row,
-                           ctx->fac_ok, invN * c_f, 2.f * invN * k.beta_lse, gate, st));
-      nl += 2; }
-    join2(ctx, st, st2);
+    if (std::getenv("CRL_LSE_TWO_CALL")) {   // ablation: the row / column calls on two streams
+      fork2(ctx, st, st2);
+      { Stage sg(ctx, st2, "lse_col");
+        CU(tc::tc_logits_lse(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, ctx->stat_psi + row_off,
+                             ctx->stat_phi, S, col_side.part_m, col_side.part_s, ctx->lse_col, ctx->fac_col,
+                             ctx->fac_ok, invN * c_b, 0.f, gate, st2));
+        nl += 2; }
+      { Stage sg(ctx, st, "lse_row");
+        CU(tc::tc_logits_lse(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off,
+                             ctx->stat_psi, S, row_side.part_m, row_side.part_s, ctx->lse_row, ctx->fac_row,
+                             ctx->fac_ok, invN * c_f, 2.f * invN * k.beta_lse, gate, st));
+        nl += 2; }
+      join2(ctx, st, st2);
+    } else { Stage sg(ctx, st, "lse_pair");
+      CU(tc::tc_logits_lse_pair(D, k.energy, row_side, col_side, Bl, N, S, ctx->fac_ok, ctx->lg_ticket, gate, st));
+      ++nl; }
     }
   } else {
     if (W > 1) {

@@ -22,6 +22,17 @@ struct GradfLoss {
   float c_f = 1.f, c_b = 1.f, beta = 0.f;
 };
 
+// one side of the two-call online-max statistics (tc_logits.cu tc_logits_lse_pair)
+struct LseSide {
+  const CUtensorMap* mA; const CUtensorMap* mB;
+  const float* a_stat; const float* b_stat;
+  float* part_m; float* part_s;     // [S][Na] split partials
+  float* lse; float* fac;           // [Na] outputs
+  float cc0, cc1;                   // column-coefficient constants (lse_merge_kernel)
+};
+cudaError_t tc_logits_lse_pair(int D, int energy, const LseSide& c0, const LseSide& c1, int Na, int Nb, int S,
+                               int* fac_ok, int* ticket, const int* gate, cudaStream_t st);
+
 bool tc_gradf_supports(int D, int energy);
 int tc_gradf_splits(int Na, int Nb, int num_sms);
 bool tc_gradf_map(CUtensorMap* m, float* db_acc, int Nb);

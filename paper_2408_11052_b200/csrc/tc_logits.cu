@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_merge.cuh"
+#include "tc_gradf.h"
 
 namespace crl {
 namespace tc {
@@ -62,6 +63,10 @@ struct TcLogitsArgs {
   float* part_da;                  // GRAD: [S][Na][D]
   float* part_rs;                  // GRAD: [S][Na] row sums of w (L2)
   const int* gate;                 // LSE: if non-null, run only when *gate != 0 (fused-stats fallback)
+  // LSE: if ticket is non-null the last of a row block's S split CTAs merges the block's rows
+  // itself (no lse_merge launch): lse / fac / fac_ok_out as lse_merge_kernel writes them
+  int* ticket;                     // [row blocks], zero between launches (reset by the merger)
+  float* lse; float* fac; int* fac_ok_out; float cc0, cc1;
 };
 
 template <int D>
@@ -85,10 +90,28 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int k) {
   return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2);
 }
 
+// lse[i] = (max_s m + log2(sum_s s * 2^(m_s - max))) * ln 2
+__device__ __forceinline__ void lse_merge_row(const float* __restrict__ pm, const float* __restrict__ ps, int Na,
+                                              int S, int i, float* __restrict__ lse, float* __restrict__ fac,
+                                              int* __restrict__ fac_ok, float cc0, float cc1) {
+  float mx = -INFINITY;
+  for (int s = 0; s < S; ++s) mx = fmaxf(mx, __ldcg(pm + (size_t)s * Na + i));
+  float t = 0.f;
+  for (int s = 0; s < S; ++s) {
+    const float m = __ldcg(pm + (size_t)s * Na + i);
+    if (m != -INFINITY) t += __ldcg(ps + (size_t)s * Na + i) * exp2f(m - mx);
+  }
+  const float l2 = mx + log2f(t);                        // LSE in log2 units
+  lse[i] = l2 * kLn2;
+  // column coefficient for the gradient pass in which these rows are the columns:
+  // cc = 2^(-LSE log2 e) (cc0 + cc1 LSE); needs 2^(-LSE log2 e) to be a normal float
+  const bool ok = l2 > -120.f && l2 < 120.f;
+  fac[i] = ok ? exp2f(-l2) * fmaf(cc1, l2 * kLn2, cc0) : 0.f;
+  if (!ok) *fac_ok = 0;
+}
+
 template <int D, int ENERGY, bool GRAD>
-__global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                           const __grid_constant__ CUtensorMap tmB,
-                                                           TcLogitsArgs p) {
+__device__ __forceinline__ void lg_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcLogitsArgs& p) {
   using C = LgCfg<D>;
   constexpr int BNT = C::BNT, STAGES = C::STAGES, KC = C::KC;
   extern __shared__ uint8_t smem_raw[];
@@ -369,12 +392,45 @@ __global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant
       }
     }
   }
+  if (!GRAD && p.ticket != nullptr) __threadfence();   // partials visible before the ticket
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
   }
+  if (!GRAD && p.ticket != nullptr) {
+    // the last split CTA of this row block merges its 128 rows (threadfence-reduction pattern)
+    __shared__ int s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(p.ticket + blockIdx.x, 1) == (int)gridDim.y - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      if (threadIdx.x < 128 && a0 + (int)threadIdx.x < p.Na)
+        lse_merge_row(p.part_m, p.part_s, p.Na, gridDim.y, a0 + threadIdx.x, p.lse, p.fac, p.fac_ok_out, p.cc0,
+                      p.cc1);
+      if (threadIdx.x == 0) p.ticket[blockIdx.x] = 0;
+    }
+  }
+}
+
+template <int D, int ENERGY, bool GRAD>
+__global__ void __launch_bounds__(384, 1) tc_logits_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                           const __grid_constant__ CUtensorMap tmB,
+                                                           TcLogitsArgs p) {
+  lg_body<D, ENERGY, GRAD>(tmA, tmB, p);
+}
+
+// both sides' statistics (row call on A = Phi, column call on A = Psi) in one launch:
+// blockIdx.z picks the side (same grid shape: W = 1 or both sides B_l x N)
+template <int D, int ENERGY>
+__global__ void __launch_bounds__(384, 1) tc_logits_lse2_kernel(const __grid_constant__ CUtensorMap tmA0,
+                                                                const __grid_constant__ CUtensorMap tmB0,
+                                                                const __grid_constant__ CUtensorMap tmA1,
+                                                                const __grid_constant__ CUtensorMap tmB1,
+                                                                const TcLogitsArgs p0, const TcLogitsArgs p1) {
+  const bool z = blockIdx.z != 0;
+  lg_body<D, ENERGY, false>(z ? tmA1 : tmA0, z ? tmB1 : tmB0, z ? p1 : p0);
 }
 
 // --------------------------------------------------------------------------- merges / prep
@@ -397,7 +453,6 @@ __global__ void rowstat_bf16_kernel(const __nv_bfloat16* __restrict__ x, int N, 
   if (lane == 0) out[w] = energy == CRL_ENERGY_L2 ? s : (energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(s), kEpsCos) : 0.f);
 }
 
-// lse[i] = (max_s m + log2(sum_s s * 2^(m_s - max))) * ln 2
 __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int Na, int S,
                                  float* __restrict__ lse, float* __restrict__ fac, int* __restrict__ fac_ok,
                                  float cc0, float cc1, const int* __restrict__ gate) {
@@ -406,20 +461,7 @@ __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __re
   if (gate != nullptr && *gate == 0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= Na) return;
-  float mx = -INFINITY;
-  for (int s = 0; s < S; ++s) mx = fmaxf(mx, pm[(size_t)s * Na + i]);
-  float t = 0.f;
-  for (int s = 0; s < S; ++s) {
-    const float m = pm[(size_t)s * Na + i];
-    if (m != -INFINITY) t += ps[(size_t)s * Na + i] * exp2f(m - mx);
-  }
-  const float l2 = mx + log2f(t);                        // LSE in log2 units
-  lse[i] = l2 * kLn2;
-  // column coefficient for the gradient pass in which these rows are the columns:
-  // cc = 2^(-LSE log2 e) (cc0 + cc1 LSE); needs 2^(-LSE log2 e) to be a normal float
-  const bool ok = l2 > -120.f && l2 < 120.f;
-  fac[i] = ok ? exp2f(-l2) * fmaf(cc1, l2 * kLn2, cc0) : 0.f;
-  if (!ok) *fac_ok = 0;
+  lse_merge_row(pm, ps, Na, S, i, lse, fac, fac_ok, cc0, cc1);
 }
 
 // dA[i] = sum_s part[s][i]  (+ energy finalisation), fp32 and bf16 outputs.  One warp per row.
@@ -517,6 +559,41 @@ cudaError_t tc_logits_lse(int D, int energy, const CUtensorMap& mA, const CUtens
   if (e != cudaSuccess) return e;
   return launch_pdl(lse_merge_kernel, dim3((Na + 255) / 256), dim3(256), 0, st, (const float*)part_m,
                     (const float*)part_s, Na, S, lse, fac, fac_ok, cc0, cc1, gate);
+}
+
+// both sides of the online-max statistics in ONE launch, each row block merged in-kernel by its
+// last split CTA (ticket: [2][row blocks] ints, zero on entry and left zero).  c0 / c1: the
+// row call (A = Phi) and the column call (A = Psi); same Na, Nb.
+cudaError_t tc_logits_lse_pair(int D, int energy, const LseSide& c0, const LseSide& c1, int Na, int Nb, int S,
+                               int* fac_ok, int* ticket, const int* gate, cudaStream_t st) {
+  TcLogitsArgs p[2]{};
+  const int bnt = D <= 128 ? 128 : 64;
+  const int rb = (Na + 127) / 128;
+  for (int z = 0; z < 2; ++z) {
+    const LseSide& c = z ? c1 : c0;
+    p[z].Na = Na; p[z].Nb = Nb;
+    p[z].cols_per_split = ((Nb + S - 1) / S + bnt - 1) / bnt * bnt;
+    p[z].a_stat = c.a_stat; p[z].b_stat = c.b_stat; p[z].part_m = c.part_m; p[z].part_s = c.part_s;
+    p[z].gate = gate; p[z].ticket = ticket + z * rb;
+    p[z].lse = c.lse; p[z].fac = c.fac; p[z].fac_ok_out = fac_ok; p[z].cc0 = c.cc0; p[z].cc1 = c.cc1;
+  }
+  auto go = [&](auto kern, size_t smem) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(kern, dim3(rb, S, 2), dim3(384), smem, st, *c0.mA, *c0.mB, *c1.mA, *c1.mB, p[0], p[1]);
+  };
+#define CRL_LG2(DD)                                                                                   \
+  if (D == DD) {                                                                                      \
+    const size_t sm = LgCfg<DD>::smem(false);                                                          \
+    if (energy == CRL_ENERGY_L2) return go(tc_logits_lse2_kernel<DD, CRL_ENERGY_L2>, sm);              \
+    if (energy == CRL_ENERGY_DOT) return go(tc_logits_lse2_kernel<DD, CRL_ENERGY_DOT>, sm);            \
+    return go(tc_logits_lse2_kernel<DD, CRL_ENERGY_COS>, sm);                                          \
+  }
+  CRL_LG2(64)
+  CRL_LG2(128)
+  CRL_LG2(256)
+#undef CRL_LG2
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t tc_logits_grad(int D, int energy, const CUtensorMap& mA, const CUtensorMap& mB, int Na, int Nb,
