@@ -544,3 +544,27 @@ def test_relabel_bulk_matches_single_calls_and_oracle():
     with pytest.raises(CrlError):
         ctx.relabel_sample_bulk(SEED, 0, 0, s, a, g)
     assert ctx.status() == 0
+
+
+@pytest.mark.parametrize("energy,knob", [("dot", None), ("l2", "CRL_FORCE_STATS_FALLBACK")])
+def test_lse_pair_ticket_rearms_across_steps(energy, knob, monkeypatch):
+    """The two-sided statistics launch merges each row block in-kernel by its last split CTA
+    (ticket counters left at zero).  With a negligible lr the parameters stay fixed, so every replay
+    of the captured step must reproduce the oracle's row and column logsumexps (lr = 1e-12:
+    the Adam steps stay below one fp32 ulp of the weights)."""
+    if knob:
+        monkeypatch.setenv(knob, "1")
+    cfg = crl_synth.preset("ant", batch=1100, width=128, energy=energy, precision="bf16", lr=1e-12)
+    ctx, params = make_ctx(cfg)
+    s, a, g = crl_synth.random_batch(cfg, cfg["batch"], seed=21)
+    z = np.zeros_like(params, dtype=np.float64)
+    ref = ocritic.critic_step(params.astype(np.float64), z, z, 0, s, a, g, lr=1e-12, **oracle_kw(cfg))
+    st, at, gt = (torch.from_numpy(x).cuda() for x in (s, a, g))
+    loss = torch.zeros(4, device="cuda")
+    for _ in range(4):
+        ctx.critic_step(st, at, gt, loss)
+        torch.cuda.synchronize()
+        assert ctx.status() == 0
+        assert rel(ctx.debug_tensor("lse_row").cpu().numpy(), ref["lse_row"]) < BF16_TOL
+        assert rel(ctx.debug_tensor("lse_col").cpu().numpy(), ref["lse_col"]) < BF16_TOL
+        assert abs(loss[3].item() - ref["total"]) <= BF16_TOL * abs(ref["total"])
