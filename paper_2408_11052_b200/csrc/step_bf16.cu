@@ -34,7 +34,8 @@ cudaError_t tc_backward_dx(int, const CUtensorMap&, const CUtensorMap&, int, int
 cudaError_t tc_backward_dw(int, const CUtensorMap&, const CUtensorMap&, int, int, int, float*, int,
                            size_t, cudaStream_t);
 cudaError_t launch_prep_inputs(const float*, const float*, const float*, int, int, int, int,
-                               __nv_bfloat16*, int, __nv_bfloat16*, int, int, int*, int*, int, cudaStream_t);
+                               __nv_bfloat16*, int, __nv_bfloat16*, int, int, int*, int*, int, float*, size_t,
+                               cudaStream_t);
 cudaError_t launch_colsum_bf16(const __nv_bfloat16*, int, int, int, float*, int, size_t, cudaStream_t);
 cudaError_t launch_f32_to_bf16(const float*, __nv_bfloat16*, size_t, int, cudaStream_t);
 bool tc_logits_maps(CUtensorMap*, CUtensorMap*, const __nv_bfloat16*, int, const __nv_bfloat16*, int, int);
@@ -370,7 +371,9 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     // also re-arms the step's device flags (fused-stats fallback gate, fast-factor flag)
     CU(tc::launch_prep_inputs(s, a, g, Bl, k.obs_dim, k.act_dim, k.goal_dim, ctx->x0_phi, ctx->ld0_phi,
                               ctx->x0_psi, ctx->ld0_psi, ctx->num_sms, ctx->use_stats ? ctx->st_bad : nullptr,
-                              ctx->tc_logits ? ctx->fac_ok : nullptr, std::getenv("CRL_FORCE_EXACT_Q") ? 0 : 1, st));
+                              ctx->tc_logits ? ctx->fac_ok : nullptr, std::getenv("CRL_FORCE_EXACT_Q") ? 0 : 1,
+                              ctx->use_gradf ? ctx->gf_acc : nullptr, ctx->use_gradf ? ctx->gf_acc_bytes / 4 : 0,
+                              st));
     ++nl;
   }
   if (ctx->use_chain) {
@@ -523,8 +526,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   }
   if (ctx->use_gradf) {
     // both sides of dL/dl from ONE evaluation of every w_ij (tc_gradf.cu); the column side
-    // accumulates by reductions into db_acc / cs_acc, zeroed here
-    CU(cudaMemsetAsync(ctx->gf_acc, 0, ctx->gf_acc_bytes, st));
+    // accumulates by reductions into db_acc / cs_acc, zeroed by prep_inputs at the step start
     { Stage sg(ctx, st, "grad_fused");
       CU(tc::tc_grad_fused(k.energy, ctx->lg_row_A, ctx->lg_row_B, ctx->gf_map, Bl, N, ctx->stat_phi, ctx->stat_psi,
                            ctx->lse_row, ctx->lse_col, ctx->fac_col, ctx->fac_ok, c_f, c_b, k.beta_lse, invN,

@@ -461,7 +461,8 @@ cudaError_t tc_backward_dw(int bn, const CUtensorMap& mapX_mn, const CUtensorMap
 __global__ void prep_inputs_kernel(const float* __restrict__ s, const float* __restrict__ a,
                                    const float* __restrict__ g, int Bn, int obs, int act, int goal,
                                    __nv_bfloat16* __restrict__ x0, int ld0, __nv_bfloat16* __restrict__ g0,
-                                   int ldg, int* __restrict__ reset, int* __restrict__ fac_ok, int fac_init) {
+                                   int ldg, int* __restrict__ reset, int* __restrict__ fac_ok, int fac_init,
+                                   float* __restrict__ zero, size_t zero_n) {
   const int in0 = obs + act;
   const size_t tot0 = (size_t)Bn * in0, totg = (size_t)Bn * goal;
   pdl_wait();
@@ -482,16 +483,21 @@ __global__ void prep_inputs_kernel(const float* __restrict__ s, const float* __r
       g0[(size_t)r * ldg + c] = __float2bfloat16_rn(g[j]);
     }
   }
+  // the fused gradient pass's reduction accumulator (a memset node here would cut the
+  // programmatic-launch chain of the step graph)
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < zero_n; i += (size_t)gridDim.x * blockDim.x)
+    zero[i] = 0.f;
 }
 
 cudaError_t launch_prep_inputs(const float* s, const float* a, const float* g, int Bn, int obs, int act,
                                int goal, __nv_bfloat16* x0, int ld0, __nv_bfloat16* g0, int ldg,
-                               int num_sms, int* reset, int* fac_ok, int fac_init, cudaStream_t st) {
+                               int num_sms, int* reset, int* fac_ok, int fac_init, float* zero, size_t zero_n,
+                               cudaStream_t st) {
   size_t tot = (size_t)Bn * (obs + act + goal);
   size_t blocks = (tot + 255) / 256;
   if (blocks > (size_t)num_sms * 4) blocks = (size_t)num_sms * 4;
   return launch_pdl(prep_inputs_kernel, dim3((unsigned)blocks), dim3(256), 0, st, s, a, g, Bn, obs, act, goal,
-                    x0, ld0, g0, ldg, reset, fac_ok, fac_init);
+                    x0, ld0, g0, ldg, reset, fac_ok, fac_init, zero, zero_n);
 }
 
 // db[s][n] = sum over the batch slice s of dZ[b][n] (bf16 in, fp32 out): 64 columns x one
