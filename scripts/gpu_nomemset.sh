@@ -1,4 +1,4 @@
-# gradient accumulator zeroed inside prep_inputs instead of a memset graph node
+# step-graph edge experiments (memset node removed; no fork / join without second-stream work)
 set -x
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -x -q -k "bf16 or ticket" 2>&1 | tail -3
