@@ -115,7 +115,9 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     const char* mn = std::getenv("CRL_TC_LOGITS_MIN_N");
     c->tc_logits = N >= (mn ? std::atoi(mn) : kTcLogitsMinN) && tc_logits_supports(D);
     if (c->tc_logits) {
-      c->lg_splits = tc_logits_splits(Bl, N, D, 148);
+      // both sides share the SMs (one two-sided statistics launch; the two gradient calls run
+      // concurrently): the split count minimises the makespan on half of them each
+      c->lg_splits = tc_logits_splits(Bl, N, D, 148 / 2);
       if (W > 1) {
         c->phi_outb_g = s.take<__nv_bfloat16>((size_t)N * D);
         c->psi_outb_g = s.take<__nv_bfloat16>((size_t)N * D);
