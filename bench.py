@@ -295,9 +295,9 @@ def run_reference(args):
     # each step is a full oracle critic step on the workload; bounded by --cpu-seconds overall
     steps = max(1, args.steps)
     budget = max(args.cpu_seconds, 1.0)
-    val, cores, n = oracle_steps(cfg, chunks, budget, steps, warm=min(args.warmup, 2))
+    val, cores, n = oracle_steps(cfg, chunks, budget, steps, warm=args.warmup)
     line = {"metric": METRIC, "value": round(val, 4), "unit": UNIT, "impl": "reference",
-            "n_gpus": args.gpus, "steps": n, "warmup": min(args.warmup, 2),
+            "n_gpus": args.gpus, "steps": n, "warmup": args.warmup,
             "ms_per_step": round(1e3 / val, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "global_batch": cfg["batch"],
