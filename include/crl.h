@@ -39,7 +39,8 @@
 extern "C" {
 #endif
 
-#define CRL_ABI_VERSION 2   /* 2: crl_config gained layernorm, random_goal_alpha */
+#define CRL_ABI_VERSION 3   /* 2: crl_config gained layernorm, random_goal_alpha;
+                               3: random goals go to the actor's goals only (crl_relabel_sample_mixed) */
 
 #if defined(__GNUC__)
 #define CRL_API __attribute__((visibility("default")))
@@ -106,9 +107,10 @@ typedef struct {
                                       W, b, gamma[out], beta[out].  fp32 path only (bf16 ->
                                       CRL_EUNSUPPORTED); the actor has no LayerNorm. */
   float random_goal_alpha;         /* F4 random-goal mixing in [0, 1] (App. C P:951-964,
-                                      reading A-36): the fraction of sampled rows whose goal
-                                      is the goal slice of a uniformly random stored state
-                                      (idx[2] = -1) instead of the hindsight goal; 0 = off */
+                                      reading A-36): the fraction of the ACTOR's goals
+                                      (crl_relabel_sample_mixed g_actor) that is the goal
+                                      slice of a uniformly random stored state instead of the
+                                      hindsight goal; the critic's g is never mixed; 0 = off */
 } crl_config;
 
 typedef struct {
@@ -179,6 +181,18 @@ CRL_API crl_status crl_relabel_sample(crl_ctx* ctx, uint64_t seed, uint64_t step
  * NULL), all device.  CRL_EINVAL if n_updates < 1 or n_updates * batch_local > 2^30. */
 CRL_API crl_status crl_relabel_sample_bulk(crl_ctx* ctx, uint64_t seed, uint64_t step0, int n_updates,
                                            float* s, float* a, float* g, int64_t* idx, void* stream);
+
+/* F4 — bulk sampling plus the actor's goals under random-goal mixing (App. C P:951-964 mixes
+ * uniformly random goals into the POLICY objective; reading A-36).  s, a, g, idx exactly as
+ * crl_relabel_sample_bulk (g = hindsight goals: the critic's batch).  g_actor
+ * [n_updates*B_l][goal_dim] (device, required): row r is g's row unless Philox draw
+ * (rho, 64, step) has y0 < floor(random_goal_alpha 2^32), in which case it is the goal slice
+ * of the stored state (env (y1 E_l) >> 32, slot tau_old + ((y2 n) >> 32)).  Bit-exact
+ * w.r.t. oracle/replay.py random_goal_mix.  Errors as crl_relabel_sample_bulk; CRL_EINVAL
+ * for a NULL g_actor. */
+CRL_API crl_status crl_relabel_sample_mixed(crl_ctx* ctx, uint64_t seed, uint64_t step0, int n_updates,
+                                            float* s, float* a, float* g, float* g_actor, int64_t* idx,
+                                            void* stream);
 
 /* A2-A6 — one critic update (Alg. 1) on the batch (s, a, g):
  *   phi = phi_enc([s||a]), psi = psi_enc(g); l_ij = f(phi_i, psi_j) over the GLOBAL batch

@@ -102,6 +102,25 @@ def _energy_diag_grad_phi(kind, phi, psi):
     raise ValueError(kind)
 
 
+def tanh_gaussian_sample_log_prob(mu, log_sig, eps_noise):
+    """The policy of Eq. 3 as a tanh-squashed diagonal Gaussian (reading A-27 for
+    the clip, done by the caller): u = mu + sigma eps, a' = tanh(u) and, by the change of
+    variables a' = tanh(u) (du/da' = 1 / (1 - tanh(u)^2)),
+        log pi(a') = sum_k [log N(u_k; mu_k, sigma_k^2)] - sum_k log(1 - a'_k^2 + 1e-6)
+                   = sum_k (-eps_k^2/2 - log sigma_k - log(2 pi)/2) - sum_k log(1 - a'_k^2 + 1e-6)
+    (log N(u; mu, sigma^2) = -(u - mu)^2 / (2 sigma^2) - log sigma - log(2 pi)/2 with
+    (u - mu) / sigma = eps; the 1e-6 keeps the log finite as |a'| -> 1).
+    Returns (a' [N][act], log pi [N])."""
+    mu = np.asarray(mu, np.float64); log_sig = np.asarray(log_sig, np.float64)
+    eps_noise = np.asarray(eps_noise, np.float64)
+    sig = np.exp(log_sig)
+    u = mu + sig * eps_noise
+    a_new = np.tanh(u)
+    log_pi = (-0.5 * eps_noise ** 2 - log_sig - 0.5 * np.log(2 * np.pi)).sum(1) \
+        - np.log(1.0 - a_new ** 2 + 1e-6).sum(1)
+    return a_new, log_pi
+
+
 def actor_loss(actor_params, critic_params, s, g, eps_noise, *, alpha_ent, obs_dim, act_dim,
                goal_dim, depth, width, repr_dim, actor_depth=2, actor_width=256,
                energy_kind="l2", activation="silu"):
@@ -118,10 +137,7 @@ def actor_loss(actor_params, critic_params, s, g, eps_noise, *, alpha_ent, obs_d
     mu, log_sig_raw = out[:, :act_dim], out[:, act_dim:]
     log_sig = np.clip(log_sig_raw, LOG_SIG_MIN, LOG_SIG_MAX)
     sig = np.exp(log_sig)
-    u = mu + sig * eps_noise
-    a_new = np.tanh(u)
-    log_pi = (-0.5 * eps_noise ** 2 - log_sig - 0.5 * np.log(2 * np.pi)).sum(1) \
-        - np.log(1.0 - a_new ** 2 + 1e-6).sum(1)
+    a_new, log_pi = tanh_gaussian_sample_log_prob(mu, log_sig, eps_noise)
     Phi, cache_phi = mlp.forward(phi_layers, np.concatenate([s, a_new], axis=1), activation)
     Psi, _ = mlp.forward(psi_layers, g, activation)
     f = energy.diag_logits(energy_kind, Phi, Psi)

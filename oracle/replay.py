@@ -102,18 +102,15 @@ def exact_offset_pmf(L, Q):
 
 
 def relabel_sample(buf: OracleBuffer, seed, step, batch_local, rank=0, world=1, gamma=0.99,
-                   goal_offset=0, goal_dim=2, Q=None, rows=None, alpha=0.0):
+                   goal_offset=0, goal_dim=2, Q=None, rows=None):
     """Hindsight relabel sample of ``batch_local`` rows for rank ``rank`` (C1).
 
     Returns s[B_l][obs], a[B_l][act], g[B_l][goal] (fp32 copies) and idx[B_l][3] int64 =
     (global env, tau, tau+k) with absolute step indices.  ``rows`` (optional) restricts the
     computation to those local rows (others stay zero) — every row is independent.
 
-    ``alpha`` (F4, App. C, reading A-36): random-goal mixing.  With the draw
-    (y0..y3) = Philox(rho, 64, step) (attempt counter 64, past the 0..63 start attempts),
-    a row whose y0 < floor(alpha 2^32) gets the goal slice of a uniformly random stored
-    state: env (y1 E_l) >> 32, slot tau_old + ((y2 n) >> 32); its idx[2] is -1.  alpha is
-    taken at fp32 precision (the ABI field).
+    These are the critic's goals (always hindsight goals); the random-goal mixture of App. C
+    applies to the actor's goals only: see ``random_goal_mix``.
     """
     tau_old, tau_new, n = buf.window()
     if n < 2:
@@ -145,15 +142,36 @@ def relabel_sample(buf: OracleBuffer, seed, step, batch_local, rank=0, world=1, 
         a[r] = buf.act[e][tau]
         g[r] = buf.obs[e][tau + k][goal_offset:goal_offset + goal_dim]
         idx[r] = (rank * E_l + e, tau, tau + k)
-        thr = int(float(np.float32(alpha)) * 4294967296.0)
-        if thr > 0:
-            y0, y1, y2, _ = (int(v) for v in philox4x32_10(rho, MAX_ATTEMPTS, step_lo, step_hi, seed_lo, seed_hi))
-            if y0 < thr:
-                e2 = (y1 * E_l) >> 32
-                t2 = tau_old + ((y2 * n) >> 32)
-                g[r] = buf.obs[e2][t2][goal_offset:goal_offset + goal_dim]
-                idx[r, 2] = -1
     return s, a, g, idx
+
+
+def random_goal_mix(buf: OracleBuffer, seed, step, batch_local, g, alpha, rank=0, goal_offset=0,
+                    goal_dim=2, rows=None):
+    """The actor's goals under random-goal mixing (F4; App. C P:951-964 mixes random goals into
+    the POLICY objective only, reading A-36).  Starting from the hindsight goals ``g`` of the
+    same (seed, step) sample: with the draw (y0..y3) = Philox(rho, 64, step) (attempt counter
+    64, past the 0..63 start attempts of ``relabel_sample``), a row whose
+    y0 < floor(alpha 2^32) takes the goal slice of a uniformly random stored state: env
+    (y1 E_l) >> 32, slot tau_old + ((y2 n) >> 32).  alpha is taken at fp32 precision (the ABI
+    field).  Returns (g_actor fp32 [B_l][goal_dim], flagged bool [B_l])."""
+    tau_old, tau_new, n = buf.window()
+    E_l = buf.E
+    g_actor = np.array(g, np.float32, copy=True)
+    flagged = np.zeros(batch_local, bool)
+    seed_lo, seed_hi = seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF
+    step_lo, step_hi = step & 0xFFFFFFFF, (step >> 32) & 0xFFFFFFFF
+    thr = int(float(np.float32(alpha)) * 4294967296.0)
+    if thr == 0:
+        return g_actor, flagged
+    for r in (range(batch_local) if rows is None else rows):
+        rho = rank * batch_local + r
+        y0, y1, y2, _ = (int(v) for v in philox4x32_10(rho, MAX_ATTEMPTS, step_lo, step_hi, seed_lo, seed_hi))
+        if y0 < thr:
+            e2 = (y1 * E_l) >> 32
+            t2 = tau_old + ((y2 * n) >> 32)
+            g_actor[r] = buf.obs[e2][t2][goal_offset:goal_offset + goal_dim]
+            flagged[r] = True
+    return g_actor, flagged
 
 
 def relabel_sample_sharded(bufs, seed, step, batch_local, **kw):

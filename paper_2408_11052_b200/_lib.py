@@ -25,7 +25,7 @@ PRECISION = {"fp32": 0, "bf16": 1}
 
 EXPORTED = ["crl_abi_version", "crl_workspace_size", "crl_create", "crl_destroy",
             "crl_nccl_unique_id", "crl_buffer_insert", "crl_relabel_sample", "crl_critic_step",
-            "crl_actor_loss", "crl_entropy_update", "crl_relabel_sample_bulk", "crl_get_status", "crl_last_error", "crl_debug_tensor",
+            "crl_actor_loss", "crl_entropy_update", "crl_relabel_sample_bulk", "crl_relabel_sample_mixed", "crl_get_status", "crl_last_error", "crl_debug_tensor",
             "crl_last_launch_count", "crl_profile_enable", "crl_profile_read"]
 
 
@@ -84,6 +84,7 @@ def load_library(path: str = LIB_PATH):
         "crl_buffer_insert": (i, [vp, vp, vp, vp, i, vp]),
         "crl_relabel_sample": (i, [vp, u64, u64, vp, vp, vp, vp, vp]),
         "crl_relabel_sample_bulk": (i, [vp, u64, u64, i, vp, vp, vp, vp, vp]),
+        "crl_relabel_sample_mixed": (i, [vp, u64, u64, i, vp, vp, vp, vp, vp, vp]),
         "crl_critic_step": (i, [vp, vp, vp, vp, vp, vp, vp]),
         "crl_actor_loss": (i, [vp, vp, vp, vp, f, vp, vp, i, vp]),
         "crl_entropy_update": (i, [vp, f, f, vp, vp, vp, vp]),
@@ -98,7 +99,7 @@ def load_library(path: str = LIB_PATH):
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
         fn.restype, fn.argtypes = res, args
-    if lib.crl_abi_version() != 2:
+    if lib.crl_abi_version() != 3:
         raise RuntimeError("libcrl.so ABI version mismatch")
     _lib = lib
     return lib
@@ -249,6 +250,11 @@ class CrlContext:
         """n_updates batches in one launch: row u*B_l + r = row r of relabel_sample(seed, step0 + u)."""
         _check(self.lib.crl_relabel_sample_bulk(self._h, seed, step0, int(n_updates), _ptr(s), _ptr(a),
                                                 _ptr(g), _ptr(idx), _stream(stream)), self._h)
+
+    def relabel_sample_mixed(self, seed, step0, n_updates, s, a, g, g_actor, idx=None, stream=None):
+        """As relabel_sample_bulk, plus the actor's goals with random-goal mixing in g_actor."""
+        _check(self.lib.crl_relabel_sample_mixed(self._h, seed, step0, int(n_updates), _ptr(s), _ptr(a),
+                                                 _ptr(g), _ptr(g_actor), _ptr(idx), _stream(stream)), self._h)
 
     def critic_step(self, s, a, g, loss_out=None, grads_out=None, stream=None):
         _check(self.lib.crl_critic_step(self._h, _ptr(s), _ptr(a), _ptr(g), _ptr(loss_out),

@@ -306,6 +306,15 @@ extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* 
   // captured once per (pointers, apply_adam) and replayed: ~20 dependent launches become one
   ActorKey key{s, g, eps, loss_out, actor_grads_out, apply_adam};
   auto it = ctx->actor_graphs.find(key);
+  if (it == ctx->actor_graphs.end() && ctx->actor_graphs.size() >= crl_ctx::kMaxGraphs) {
+    // bounded cache (as crl_critic_step): evict the least recently replayed actor graph
+    auto lru = ctx->actor_graphs.begin();
+    for (auto u = ctx->actor_graphs.begin(); u != ctx->actor_graphs.end(); ++u)
+      if (ctx->actor_use[u->first] < ctx->actor_use[lru->first]) lru = u;
+    cudaGraphExecDestroy(lru->second.first);
+    ctx->actor_use.erase(lru->first);
+    ctx->actor_graphs.erase(lru);
+  }
   if (it == ctx->actor_graphs.end()) {
     CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
     crl_status rs = enqueue_actor(ctx, s, g, eps, loss_out, actor_grads_out, apply_adam, ctx->cap_stream);
@@ -320,6 +329,7 @@ extern "C" crl_status crl_actor_loss(crl_ctx* ctx, const float* s, const float* 
     it = ctx->actor_graphs.emplace(key, std::make_pair(exec, ctx->launches)).first;
   }
   CU(cudaGraphLaunch(it->second.first, st));
+  ctx->actor_use[key] = ++ctx->use_clock;
   ctx->launches = it->second.second;
   ctx->actor_loss_done = true;
   return CRL_OK;

@@ -54,6 +54,18 @@ __global__ void spin_kernel(unsigned long long ns) {
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// SM count of the current device (split counts of the logits kernels, hence scratch sizes);
+// 148 (B200) when no device is visible (crl_workspace_size is a pure host call)
+static int device_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      n <= 0) {
+    cudaGetLastError();
+    return 148;
+  }
+  return n;
+}
+
 static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
                   size_t* scr_bytes) {
   const crl_config& k = c->cfg;
@@ -117,7 +129,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     if (c->tc_logits) {
       // both sides share the SMs (one two-sided statistics launch; the two gradient calls run
       // concurrently): the split count minimises the makespan on half of them each
-      c->lg_splits = tc_logits_splits(Bl, N, D, 148 / 2);
+      c->lg_splits = tc_logits_splits(Bl, N, D, device_sms() / 2);
       if (W > 1) {
         c->phi_outb_g = s.take<__nv_bfloat16>((size_t)N * D);
         c->psi_outb_g = s.take<__nv_bfloat16>((size_t)N * D);
@@ -145,7 +157,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       c->lg_ticket = s.take<int>((size_t)2 * ((Bl + 127) / 128));
       c->use_stats = W == 1 && tc_stats_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_STATS");
       if (c->use_stats) {
-        c->st_splits = tc_stats_splits(Bl, N, 148);
+        c->st_splits = tc_stats_splits(Bl, N, device_sms());
         c->st_ldc = N + kStatPad;
         c->st_part_rs = s.take<float>((size_t)c->st_splits * Bl);
         c->st_colpart = s.take<float>((size_t)((Bl + 127) / 128) * c->st_ldc);
@@ -153,7 +165,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       }
       c->use_gradf = W == 1 && tc_gradf_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_GRAD");
       if (c->use_gradf) {
-        c->gf_splits = tc_gradf_splits(Bl, N, 148);
+        c->gf_splits = tc_gradf_splits(Bl, N, device_sms());
         c->gf_part_da = s.take<float>((size_t)c->gf_splits * Bl * D);
         c->gf_part_rs = s.take<float>((size_t)c->gf_splits * Bl);
         c->gf_acc_bytes = ((size_t)N * D + N + kStatPad) * 4;
@@ -204,7 +216,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   c->skip = s.take<int>(1);
   c->stage_s = s.take<float>((size_t)Bl * k.obs_dim);
   c->stage_a = s.take<float>((size_t)Bl * k.act_dim);
-  c->stage_g = s.take<float>((size_t)Bl * k.goal_dim);
+  c->stage_g = s.take<float>((size_t)Bl * k.goal_dim + 64);   // + 256 B: the host ring's slot pitch
   // actor objective (fp32): actor activations, the frozen critic's activations on [s||a'],
   // head buffers, gradient partials
   c->has_actor = k.actor_depth > 0 && k.actor_width > 0;
@@ -481,7 +493,7 @@ crl_status crl_buffer_insert(crl_ctx* ctx, const float* obs, const float* act, c
 }
 
 static crl_status relabel(crl_ctx* ctx, uint64_t seed, uint64_t step, int n_upd, float* s, float* a, float* g,
-                          int64_t* idx, void* stream) {
+                          float* g_actor, int64_t* idx, void* stream) {
   if (!ctx) return fail(ctx, CRL_EINVAL, "ctx is NULL");
   if (!s || !a || !g) return fail(ctx, CRL_EINVAL, "sample: NULL output");
   if (n_upd < 1 || (long)n_upd * ctx->cfg.batch_local > (1l << 30))
@@ -497,7 +509,7 @@ static crl_status relabel(crl_ctx* ctx, uint64_t seed, uint64_t step, int n_upd,
                            k.goal_dim, k.goal_offset, ctx->obs_stride, ctx->act_stride,
                            (uint32_t)tau_old, (uint32_t)tau_new, seed, step, k.gamma,
                            (uint64_t)((double)k.random_goal_alpha * 4294967296.0), ctx->obs_ring,
-                           ctx->act_ring, ctx->ep_end, ctx->qtab, s, a, g, idx, ctx->status,
+                           ctx->act_ring, ctx->ep_end, ctx->qtab, s, a, g, g_actor, idx, ctx->status,
                            (cudaStream_t)stream));
   ctx->launches = 1;
   return CRL_OK;
@@ -505,12 +517,18 @@ static crl_status relabel(crl_ctx* ctx, uint64_t seed, uint64_t step, int n_upd,
 
 crl_status crl_relabel_sample(crl_ctx* ctx, uint64_t seed, uint64_t step, float* s, float* a,
                               float* g, int64_t* idx, void* stream) {
-  return relabel(ctx, seed, step, 1, s, a, g, idx, stream);
+  return relabel(ctx, seed, step, 1, s, a, g, nullptr, idx, stream);
 }
 
 crl_status crl_relabel_sample_bulk(crl_ctx* ctx, uint64_t seed, uint64_t step0, int n_updates, float* s,
                                    float* a, float* g, int64_t* idx, void* stream) {
-  return relabel(ctx, seed, step0, n_updates, s, a, g, idx, stream);
+  return relabel(ctx, seed, step0, n_updates, s, a, g, nullptr, idx, stream);
+}
+
+crl_status crl_relabel_sample_mixed(crl_ctx* ctx, uint64_t seed, uint64_t step0, int n_updates, float* s,
+                                    float* a, float* g, float* g_actor, int64_t* idx, void* stream) {
+  if (ctx && !g_actor) return fail(ctx, CRL_EINVAL, "sample_mixed: NULL g_actor");
+  return relabel(ctx, seed, step0, n_updates, s, a, g, g_actor, idx, stream);
 }
 
 }  // extern "C"
@@ -733,8 +751,10 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
 // the page-locked host ring of the end-to-end path (host memory; no device allocation)
 static bool make_host_ring(crl_ctx* ctx) {
   const crl_config& k = ctx->cfg;
-  ctx->h_stage_bytes = (size_t)(reinterpret_cast<char*>(ctx->stage_g) - reinterpret_cast<char*>(ctx->stage_s)) +
-                       (size_t)k.batch_local * k.goal_dim * 4;
+  // slot pitch rounded up to 256 B: every slot base stays 16-byte aligned for the device's
+  // 16 B loads whatever B_l * dims is (odd batches with goal_dim 2, e.g.)
+  ctx->h_stage_bytes = ((size_t)(reinterpret_cast<char*>(ctx->stage_g) - reinterpret_cast<char*>(ctx->stage_s)) +
+                        (size_t)k.batch_local * k.goal_dim * 4 + 255) & ~(size_t)255;
   if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage), ctx->h_stage_bytes * crl_ctx::kHostSlots,
                     cudaHostAllocDefault) != cudaSuccess)
     return false;
@@ -791,7 +811,7 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
     // ahead of a DMA copy for this size, Ant e2e 11.25k -> 11.7k steps/s; CRL_DMA_COPY = copy)
     if (!std::getenv("CRL_DMA_COPY")) {
       const size_t n16 = (ctx->h_stage_bytes + 15) / 16;
-      pull_host_kernel<<<(unsigned)std::min<size_t>((n16 + 255) / 256, 148), 256, 0, st>>>(
+      pull_host_kernel<<<(unsigned)std::min<size_t>((n16 + 255) / 256, (size_t)ctx->num_sms), 256, 0, st>>>(
           reinterpret_cast<uint4*>(ctx->stage_s), reinterpret_cast<const uint4*>(hb), n16);
       CU(cudaGetLastError());
     } else {
@@ -829,6 +849,18 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
   }
   GraphKey key{s, a, g, loss_dev, grads_out};
   auto it = ctx->graphs.find(key);
+  if (it == ctx->graphs.end() && ctx->graphs.size() >= crl_ctx::kMaxGraphs) {
+    // bounded cache: evict the least recently replayed graph (callers that pass fresh
+    // tensors every step pay a capture per step, but the cache never grows without bound)
+    auto lru = ctx->graph_use.begin();
+    for (auto u = ctx->graph_use.begin(); u != ctx->graph_use.end(); ++u)
+      if (u->second < lru->second) lru = u;
+    const GraphKey old = lru->first;
+    cudaGraphExecDestroy(ctx->graphs[old]);
+    ctx->graphs.erase(old);
+    ctx->graph_launches.erase(old);
+    ctx->graph_use.erase(old);
+  }
   if (it == ctx->graphs.end()) {
     // capture the schedule once on the private capture stream
     CU(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -848,6 +880,7 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
     ctx->graph_launches[key] = ctx->launches;
   }
   CU(cudaGraphLaunch(it->second, st));
+  ctx->graph_use[key] = ++ctx->use_clock;
   ctx->launches = ctx->graph_launches[key];
   if (loss_host) CU(cudaMemcpyAsync(loss_out, loss_dev, 16, cudaMemcpyDeviceToHost, st));
   return CRL_OK;

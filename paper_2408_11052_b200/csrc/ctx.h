@@ -21,7 +21,7 @@ cudaError_t launch_buffer_insert(const float*, const float*, const uint8_t*, int
 cudaError_t launch_relabel_sample(int, int, int, int, int, int, int, int, int, int, int, uint32_t,
                                   uint32_t, uint64_t, uint64_t, double, uint64_t, const float*, const float*,
                                   const uint32_t*, const uint64_t*, float*, float*, float*,
-                                  int64_t*, int*, cudaStream_t);
+                                  float*, int64_t*, int*, cudaStream_t);
 cudaError_t mlp_forward_layer_f32(int, int, int, const float*, int, const float*, int, int,
                                   const float*, const float*, float*, float*, int, cudaStream_t);
 cudaError_t mlp_backward_dx_f32(int, int, int, const float*, const float*, const float*, float*,
@@ -146,6 +146,9 @@ struct crl_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int> graph_launches;     // kernels per replay of each cached graph
+  std::map<GraphKey, uint64_t> graph_use;     // last replay (LRU eviction beyond kMaxGraphs)
+  uint64_t use_clock = 0;
+  static constexpr size_t kMaxGraphs = 16;
   ncclComm_t comm = nullptr;
   int num_sms = 148;
   int launches = 0;
@@ -232,6 +235,7 @@ struct crl_ctx {
   int *a_t = nullptr, *a_skip = nullptr;
   float* a_alpha = nullptr;                // [1] the entropy coefficient of the current actor call
   std::map<ActorKey, std::pair<cudaGraphExec_t, int>> actor_graphs;   // captured actor steps
+  std::map<ActorKey, uint64_t> actor_use;  // last replay (LRU eviction beyond kMaxGraphs)
   float* ent_mv = nullptr;                 // [2] Adam moments of log alpha (entropy coefficient)
   int* ent_t = nullptr;                    // its step counter
   bool actor_loss_done = false;            // a crl_actor_loss has produced a mean log pi

@@ -135,8 +135,12 @@ __global__ void __launch_bounds__(256) adam_kernel(
   const float inv_bc1 = 1.0f / bc1;
   const float inv_sbc2 = 1.0f / sqrtf(bc2);
   bool bad = false;
+  // an element whose gradient is not finite is left untouched (p, m, v keep their values; the
+  // status word reports CRL_ENONFINITE): a non-finite gradient can never poison the master
+  // parameters, the moments or the bf16 shadow (the loss-level check above skips the whole
+  // step; this gate covers a finite loss with a non-finite gradient element)
   auto upd = [&](float pi, float gi, float& mi, float& vi) -> float {
-    bad |= !isfinite(gi);
+    if (!isfinite(gi)) { bad = true; return pi; }
     mi = b1 * mi + (1.f - b1) * gi;
     vi = b2 * vi + (1.f - b2) * gi * gi;
     const float denom = sqrtf(vi) * inv_sbc2 + eps;       // sqrt(v / bc2) + eps

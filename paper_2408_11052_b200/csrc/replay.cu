@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) relabel_sample_kernel(
     const float* __restrict__ obs_ring, const float* __restrict__ act_ring,
     const uint32_t* __restrict__ ep_end, const uint64_t* __restrict__ qtab,
     float* __restrict__ s_out, float* __restrict__ a_out, float* __restrict__ g_out,
-    int64_t* __restrict__ idx_out, int* __restrict__ status) {
+    float* __restrict__ ga_out, int64_t* __restrict__ idx_out, int* __restrict__ status) {
   constexpr int RPW = 32 / LPR;                                 // rows per warp
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR, li = lane % LPR;
@@ -171,28 +171,34 @@ __global__ void __launch_bounds__(256) relabel_sample_kernel(
     k = lo;
   }
   const uint32_t slot = tau % (uint32_t)T;
-  uint32_t ge = e, gslot = (tau + k) % (uint32_t)T;
-  bool rnd_goal = false;
-  if (alpha_t != 0) {
-    // random-goal mixing (F4, App. C): draw 64 (past the start attempts) decides and places it
-    const U4 y = philox4x32_10(U4{rho, 64u, step_lo, step_hi}, seed_lo, seed_hi);
-    if ((uint64_t)y.x < alpha_t) {
-      rnd_goal = true;
-      ge = (uint32_t)(((uint64_t)y.y * (uint64_t)E) >> 32);
-      gslot = (tau_old + (uint32_t)(((uint64_t)y.z * (uint64_t)n) >> 32)) % (uint32_t)T;
-    }
-  }
+  const uint32_t gslot = (tau + k) % (uint32_t)T;
   const float* srow = obs_ring + ((size_t)e * T + slot) * obs_stride;
   const float* arow = act_ring + ((size_t)e * T + slot) * act_stride;
-  const float* grow = obs_ring + ((size_t)ge * T + gslot) * obs_stride + goal_offset;
+  const float* grow = obs_ring + ((size_t)e * T + gslot) * obs_stride + goal_offset;
   float* so = s_out + (size_t)r * obs_dim;
   float* ao = a_out + (size_t)r * act_dim;
   float* go = g_out + (size_t)r * goal_dim;
   for (int c = li; c < obs_dim; c += LPR) so[c] = srow[c];
   for (int c = li; c < act_dim; c += LPR) ao[c] = arow[c];
   for (int c = li; c < goal_dim; c += LPR) go[c] = grow[c];
+  if (ga_out != nullptr) {
+    // the ACTOR's goals with random-goal mixing (F4, App. C P:951-964 mixes random goals into
+    // the policy objective only, reading A-36): draw 64 (past the start attempts) decides
+    // and places it; the critic's g above stays the hindsight goal
+    const float* garow = grow;
+    if (alpha_t != 0) {
+      const U4 y = philox4x32_10(U4{rho, 64u, step_lo, step_hi}, seed_lo, seed_hi);
+      if ((uint64_t)y.x < alpha_t) {
+        const uint32_t ge = (uint32_t)(((uint64_t)y.y * (uint64_t)E) >> 32);
+        const uint32_t gs = (tau_old + (uint32_t)(((uint64_t)y.z * (uint64_t)n) >> 32)) % (uint32_t)T;
+        garow = obs_ring + ((size_t)ge * T + gs) * obs_stride + goal_offset;
+      }
+    }
+    float* gao = ga_out + (size_t)r * goal_dim;
+    for (int c = li; c < goal_dim; c += LPR) gao[c] = garow[c];
+  }
   if (idx_out != nullptr && li < 3) {
-    int64_t v = li == 0 ? (int64_t)rank * E + e : (li == 1 ? (int64_t)tau : (rnd_goal ? (int64_t)-1 : (int64_t)(tau + k)));
+    int64_t v = li == 0 ? (int64_t)rank * E + e : (li == 1 ? (int64_t)tau : (int64_t)(tau + k));
     idx_out[(size_t)r * 3 + li] = v;
   }
 }
@@ -215,7 +221,7 @@ cudaError_t launch_relabel_sample(int B_l, int n_upd, int rank, int E, int T, in
                                   uint64_t alpha_t,
                                   const float* obs_ring, const float* act_ring,
                                   const uint32_t* ep_end, const uint64_t* qtab, float* s, float* a,
-                                  float* g, int64_t* idx, int* status, cudaStream_t st) {
+                                  float* g, float* g_actor, int64_t* idx, int* status, cudaStream_t st) {
   const int warps = 8;
   const long rows = (long)B_l * n_upd;
   // narrow rows (the paper's Reacher / Ant; Humanoid is wide) in large batches: 8 rows per warp
@@ -228,7 +234,7 @@ cudaError_t launch_relabel_sample(int B_l, int n_upd, int rank, int E, int T, in
   kern<<<grid, warps * 32, 0, st>>>(
       B_l, n_upd, rank, E, T, obs_dim, act_dim, goal_dim, goal_offset, obs_stride, act_stride, tau_old,
       tau_new, (uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)step, (uint32_t)(step >> 32), std::log(gamma), alpha_t,
-      obs_ring, act_ring, ep_end, qtab, s, a, g, idx, status);
+      obs_ring, act_ring, ep_end, qtab, s, a, g, g_actor, idx, status);
   return cudaGetLastError();
 }
 

@@ -17,6 +17,27 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
+def relmax(a, b):
+    """Element-wise companion of rel(): max_k |a_k - b_k| / max_k |b_k| (SURVEY 8(c) parity
+    metric: a wrong ragged block or a single bad element cannot hide under a norm)."""
+    a = np.asarray(a, np.float64).ravel(); b = np.asarray(b, np.float64).ravel()
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def param_tensors(cfg):
+    """(name, size) of every parameter tensor in the flat critic layout (include/crl.h): per
+    encoder (phi, then psi) and layer W[in][out], b[out] and, on LayerNorm hidden layers (F2),
+    gamma[out], beta[out]."""
+    ln = bool(cfg.get("layernorm", 0))
+    out = []
+    for enc, enc_in in (("phi", cfg["obs_dim"] + cfg["act_dim"]), ("psi", cfg["goal_dim"])):
+        for li, (fi, fo) in enumerate(crl_synth.param_shapes(enc_in, cfg["depth"], cfg["width"], cfg["repr_dim"])):
+            out += [(f"{enc}.W{li}", fi * fo), (f"{enc}.b{li}", fo)]
+            if ln and li < cfg["depth"]:
+                out += [(f"{enc}.ln_gamma{li}", fo), (f"{enc}.ln_beta{li}", fo)]
+    return out
+
+
 def make_ctx(cfg, world=1, rank=0, nccl_id=None, seed=42, **over):
     import torch
     from paper_2408_11052_b200 import CrlConfig, CrlContext

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     from paper_2408_11052_b200 import EXPORTED
     assert sorted(EXPORTED) == declared_symbols()
-    assert lib.crl_abi_version() == 2
+    assert lib.crl_abi_version() == 3
 
 
 def test_library_is_sm100a():

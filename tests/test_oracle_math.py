@@ -465,3 +465,54 @@ def test_critic_layernorm_end_to_end_finite_differences():
     out = critic.critic_forward_backward(p, s, a, g, **kw)
     fd = fd_grad(lambda q: critic.critic_forward_backward(q, s, a, g, **kw)["total"], p)
     assert rel_err(out["grads"], fd) < 1e-6
+
+
+# ------------------------------------------------------------------ policy log-density pins
+# oracle/critic.py tanh_gaussian_sample_log_prob (Eq. 3: a' ~ pi(.|s, g); the
+# tanh-squashed Gaussian and its change of variables, reading A-27).  Pinned against things
+# other than its own formula: a closed form, scipy's normal log-density (the Gaussian part)
+# and the normalisation of the density over the action box (the Jacobian part).
+
+def test_log_pi_closed_form_at_the_origin():
+    """mu = 0, log sigma = 0, eps = 0: u = 0, a' = 0, so
+    log pi = -(k/2) log(2 pi) - k log(1 + 1e-6)."""
+    for k in (1, 3, 17):
+        a, lp = critic.tanh_gaussian_sample_log_prob(np.zeros((2, k)), np.zeros((2, k)), np.zeros((2, k)))
+        assert np.all(a == 0.0)
+        expect = -0.5 * k * np.log(2 * np.pi) - k * np.log(1.0 + 1e-6)
+        assert np.allclose(lp, expect, rtol=0, atol=1e-13)
+
+
+def test_log_pi_gaussian_part_matches_scipy():
+    """log pi + sum_k log(1 - a'^2 + 1e-6) is the Gaussian log-density of u = mu + sigma eps:
+    scipy.stats.norm.logpdf(u, mu, sigma) summed over the action dims."""
+    from scipy.stats import norm
+    rng = np.random.default_rng(3)
+    mu = rng.normal(0, 0.7, (6, 4)); ls = rng.uniform(-2, 1, (6, 4)); eps = rng.standard_normal((6, 4))
+    a, lp = critic.tanh_gaussian_sample_log_prob(mu, ls, eps)
+    u = mu + np.exp(ls) * eps
+    assert np.allclose(np.tanh(u), a, rtol=0, atol=1e-15)
+    gauss = lp + np.log(1.0 - a ** 2 + 1e-6).sum(1)
+    assert np.allclose(gauss, norm.logpdf(u, mu, np.exp(ls)).sum(1), rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("mu,log_sig", [(0.0, 0.0), (0.3, -0.4), (-1.0, 0.5), (0.8, -2.0)])
+def test_log_pi_density_integrates_to_one_over_the_action_box(mu, log_sig):
+    """exp(log pi(a')) is a probability density on a' in (-1, 1): integrated by quadrature in
+    u = atanh(a') (da' = (1 - tanh(u)^2) du) it gives 1 up to the 1e-6 guard, which removes
+    E[1e-6 / (sech^2 u + 1e-6)] < 1e-3 of mass here (computed independently below).  A wrong sign of the Jacobian term, of
+    log sigma or of the log(2 pi)/2 constant moves the integral by O(1)."""
+    sig = np.exp(log_sig)
+    u = np.linspace(mu - 12 * sig, mu + 12 * sig, 200001)
+    eps = ((u - mu) / sig)[:, None]
+    a, lp = critic.tanh_gaussian_sample_log_prob(np.full_like(eps, mu), np.full_like(eps, log_sig), eps)
+    dens_a = np.exp(lp)                                   # density w.r.t. a'
+    integrand = dens_a * (1.0 - np.tanh(u) ** 2)          # da' = sech^2(u) du
+    total = np.trapezoid(integrand, u)
+    # the mass the guard removes, from scipy's normal density (no oracle code):
+    # int N(u; mu, sigma) sech^2(u) / (sech^2(u) + 1e-6) du
+    from scipy.stats import norm
+    sech2 = 1.0 / np.cosh(u) ** 2
+    expect = np.trapezoid(norm.pdf(u, mu, sig) * sech2 / (sech2 + 1e-6), u)
+    assert 1.0 - 1e-3 < expect <= 1.0
+    assert abs(total - expect) < 1e-9, (total, expect)

@@ -176,10 +176,11 @@ def test_relabel_rejects_tiny_buffer():
 # ------------------------------------------------------------------ F4 random-goal mixing (A-36)
 
 def test_random_goal_alpha_mixing():
-    """App. C: a fraction alpha of rows gets the goal slice of a uniformly random
-    stored state.  alpha = 0 reproduces the hindsight sample exactly; with alpha = 0.3 the
-    flagged fraction matches alpha (binomial 4-sigma band), flagged goals are stored states of
-    the window, unflagged rows are unchanged."""
+    """App. C: a fraction alpha of the ACTOR's goals is the goal slice of a uniformly
+    random stored state (the critic keeps the hindsight goals, reading A-36).  alpha = 0
+    leaves every goal unchanged; with alpha = 0.3 the flagged fraction matches alpha
+    (binomial 4-sigma band), flagged goals are stored states of the window, unflagged rows
+    are the hindsight goals; alpha = 1 flags every row."""
     rng = np.random.default_rng(3)
     E, T, U = 6, 50, 70
     buf = replay.OracleBuffer(E, 4, 2, T)
@@ -189,16 +190,14 @@ def test_random_goal_alpha_mixing():
     buf.insert(obs, act, done)
     B = 2000
     base = replay.relabel_sample(buf, 77, 5, B, gamma=0.9, goal_dim=2)
-    same = replay.relabel_sample(buf, 77, 5, B, gamma=0.9, goal_dim=2, alpha=0.0)
-    for x, y in zip(base, same):
-        assert np.array_equal(x, y)
-    mix = replay.relabel_sample(buf, 77, 5, B, gamma=0.9, goal_dim=2, alpha=0.3)
-    flag = mix[3][:, 2] == -1
+    same, f0 = replay.random_goal_mix(buf, 77, 5, B, base[2], 0.0, goal_dim=2)
+    assert np.array_equal(same, base[2]) and not f0.any()
+    mix, flag = replay.random_goal_mix(buf, 77, 5, B, base[2], 0.3, goal_dim=2)
     assert abs(flag.mean() - 0.3) < 4 * math.sqrt(0.3 * 0.7 / B)
-    assert np.array_equal(mix[2][~flag], base[2][~flag])
-    assert np.array_equal(mix[0], base[0]) and np.array_equal(mix[1], base[1])
+    assert np.array_equal(mix[~flag], base[2][~flag])
     tau_old, tau_new, _ = buf.window()
     stored = {tuple(buf.obs[e][t][:2]) for e in range(E) for t in range(tau_old, tau_new + 1)}
-    assert all(tuple(gg) in stored for gg in mix[2][flag])
-    allr = replay.relabel_sample(buf, 77, 5, 64, gamma=0.9, goal_dim=2, alpha=1.0)
-    assert np.all(allr[3][:, 2] == -1)
+    assert all(tuple(gg) in stored for gg in mix[flag])
+    b64 = replay.relabel_sample(buf, 77, 5, 64, gamma=0.9, goal_dim=2)
+    _, fall = replay.random_goal_mix(buf, 77, 5, 64, b64[2], 1.0, goal_dim=2)
+    assert fall.all()
