@@ -9,8 +9,13 @@ is filled (A0) before the timed region.
   python bench.py [--gpus N --steps K --warmup W] [--workload ant] [--precision fp32]
   python bench.py --impl reference ...     # the CPU oracle timed on the host cores
 
-Default workload = BASELINE.json configs[1] (Ant-shaped, 4x256 encoders, repr 64, batch 256,
-beta 0.1, 1024 envs x 1000).  Prints ONE JSON line on rank 0.
+Default workload = BASELINE.json configs[4] at W = 1 ("netscale": Ant dims, 4x1024 encoders,
+repr 256, global batch 16384, L2, symmetric InfoNCE, beta 0.1, 1024 envs x 1000, bf16): the
+largest single-GPU configuration in BASELINE.json (its metric names no config) and the
+strong-scaling config of the 1/2/4/8-GPU runs.  Prints ONE JSON line on rank 0.
+
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run (N ranks, one
+per GPU, 127.0.0.1 rendezvous).
 """
 import argparse
 import json
@@ -35,10 +40,10 @@ UNIT = "steps/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=1000)
+    p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="ant")
+    p.add_argument("--workload", default="netscale")
     p.add_argument("--precision", default="bf16")
     p.add_argument("--energy", default=None)
     p.add_argument("--loss", default=None, help="fwd / bwd / sym / flatnce_* / fb / dpo / ipo / sppo")
@@ -50,7 +55,10 @@ def parse():
                         "crl_relabel_sample per step")
     p.add_argument("--bulk-updates", type=int, default=256,
                    help="A1 bulk-mode measurement: updates per crl_relabel_sample_bulk call (0: skip)")
-    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--cpu-rows", type=int, default=1024,
+                   help="cpu_baseline / reference arm: oracle sub-batch per timed step when the "
+                        "workload's batch is larger (the step time is extrapolated to the full batch)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -249,11 +257,45 @@ def roofline(stages, cfg, N, Bl, peaks, peak_kind, clocks, traffic_db):
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def oracle_steps(cfg, chunks, seconds, max_steps, seed_step0=0, warm=1):
-    """Time the oracle critic step (relabel + fwd + loss + bwd + Adam) on the host."""
+def host_info():
+    """CPU model and NumPy's BLAS vendor (BASELINE.md §4 asks for both next to the cores)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        b = [x for x in threadpool_info() if x.get("user_api") == "blas"]
+        if b:
+            blas = f"{b[0].get('internal_api')} {b[0].get('version')} ({b[0].get('num_threads')} threads)"
+    except Exception:
+        pass
+    return model, blas
+
+
+def oracle_steps(cfg, chunks, seconds, max_steps, seed_step0=0, warm=1, rows=1024):
+    """Time the oracle critic step (relabel + fwd + loss + bwd + Adam) on the host cores.
+
+    At batch N <= rows every timed step is one whole oracle step.  Above it (the net-scale and
+    large sweep configs: the fp64 oracle's N x N logits would take minutes per step) each timed
+    step runs the oracle's stages on an n = rows sub-batch drawn from the same workload, and
+    the full-batch step time is extrapolated from the stages' measured times with their exact
+    scaling in N:  t(N) = (t_relabel + t_encoders)(N/n) + t_logits (N/n)^2 + t_adam
+    (relabel and both encoders are per-row; energies, loss and VJP are N x N; Adam is per
+    parameter).  Returns (steps/s at N, threads, timed steps, description)."""
     from threadpoolctl import threadpool_info
 
+    from oracle import adam as oadam
     from oracle import critic as ocritic
+    from oracle import energy as oenergy
+    from oracle import losses as olosses
+    from oracle import mlp as omlp
     from oracle import replay as oreplay
     buf = oreplay.OracleBuffer(cfg["n_envs"], cfg["obs_dim"], cfg["act_dim"], cfg["capacity"])
     for obs, act, done in chunks:
@@ -261,21 +303,46 @@ def oracle_steps(cfg, chunks, seconds, max_steps, seed_step0=0, warm=1):
     _, Q = oreplay.geometric_tables(cfg["gamma"], cfg["capacity"])
     params = crl_synth.init_critic_params(cfg, 42).astype(np.float64)
     m = np.zeros_like(params); v = np.zeros_like(params); t = 0
+    ln = bool(cfg.get("layernorm", 0))
     kw = dict(obs_dim=cfg["obs_dim"], act_dim=cfg["act_dim"], goal_dim=cfg["goal_dim"],
               depth=cfg["depth"], width=cfg["width"], repr_dim=cfg["repr_dim"],
               energy_kind=cfg["energy"], loss_kind=cfg["loss"], beta=cfg["beta_lse"],
-              activation=cfg["activation"], layernorm=bool(cfg.get("layernorm", 0)))
+              activation=cfg["activation"], layernorm=ln)
     B = cfg["batch"]
+    n = min(B, rows)
+    scale = B / n
     times = []
     step = seed_step0
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
-        s, a, g, _ = oreplay.relabel_sample(buf, crl_synth.PHILOX_SEED, step, B, gamma=cfg["gamma"],
+        s, a, g, _ = oreplay.relabel_sample(buf, crl_synth.PHILOX_SEED, step, n, gamma=cfg["gamma"],
                                             goal_dim=cfg["goal_dim"], Q=Q)
-        out = ocritic.critic_step(params, m, v, t, s, a, g, lr=cfg["lr"], **kw)
-        params, m, v, t = out["params_new"], out["m_new"], out["v_new"], out["t_new"]
-        times.append(time.perf_counter() - t0)
+        t1 = time.perf_counter()
+        if n == B:
+            out = ocritic.critic_step(params, m, v, t, s, a, g, lr=cfg["lr"], **kw)
+            params, m, v, t = out["params_new"], out["m_new"], out["v_new"], out["t_new"]
+            times.append(time.perf_counter() - t0)
+        else:
+            # the same stages as oracle/critic.py critic_forward_backward + critic_step, timed apart
+            phi_l, psi_l = ocritic.split_critic_params(params, cfg["obs_dim"], cfg["act_dim"], cfg["goal_dim"],
+                                                       cfg["depth"], cfg["width"], cfg["repr_dim"], ln)
+            fwd, bwd, pk = (omlp.forward_ln, omlp.backward_ln, omlp.pack_ln) if ln else \
+                (omlp.forward, omlp.backward, omlp.pack)
+            Phi, c_phi = fwd(phi_l, np.concatenate([s, a], axis=1).astype(np.float64), cfg["activation"])
+            Psi, c_psi = fwd(psi_l, np.asarray(g, np.float64), cfg["activation"])
+            t2 = time.perf_counter()
+            lg = oenergy.logits(cfg["energy"], Phi, Psi)
+            _, G = olosses.loss_and_grad(lg, cfg["loss"], cfg["beta_lse"])
+            dPhi, dPsi = oenergy.vjp(cfg["energy"], Phi, Psi, G)
+            t3 = time.perf_counter()
+            g_phi, _ = bwd(phi_l, c_phi, dPhi, cfg["activation"])
+            g_psi, _ = bwd(psi_l, c_psi, dPsi, cfg["activation"])
+            grads = np.concatenate([pk(g_phi), pk(g_psi)])
+            t4 = time.perf_counter()
+            params, m, v, t = oadam.adam_step(params, grads, m, v, t, cfg["lr"], 0.9, 0.999, 1e-8, 0.0)
+            t5 = time.perf_counter()
+            times.append((t1 - t0 + t2 - t1 + t4 - t3) * scale + (t3 - t2) * scale * scale + (t5 - t4))
         step += 1
         n_timed = len(times) - warm
         if n_timed >= max_steps or (n_timed >= 1 and time.perf_counter() - t_start > seconds):
@@ -283,7 +350,13 @@ def oracle_steps(cfg, chunks, seconds, max_steps, seed_step0=0, warm=1):
     timed = times[warm:] if len(times) > warm else times
     blas = [x for x in threadpool_info() if x.get("user_api") == "blas"]
     cores = blas[0]["num_threads"] if blas else 1
-    return len(timed) / sum(timed), cores, len(timed)
+    if n == B:
+        desc = f"{len(timed)} full oracle critic steps (relabel+fwd+loss+bwd+Adam, fp64 NumPy) at batch {B}"
+    else:
+        desc = (f"{len(timed)} oracle critic steps (relabel+fwd+loss+bwd+Adam, fp64 NumPy) on {n}-row "
+                f"sub-batches of the {cfg['name']} workload, each extrapolated to batch {B} from its "
+                f"stage times: (relabel + encoders) x {scale:g} + (energies + loss + VJP) x {scale * scale:g} + Adam")
+    return len(timed) / sum(timed), cores, len(timed), desc
 
 
 def run_reference(args):
@@ -292,22 +365,49 @@ def run_reference(args):
         return
     cfg = workload_cfg(args)
     chunks = crl_synth.fast_chunks(cfg, n_fill_chunks(cfg))
-    # each step is a full oracle critic step on the workload; bounded by --cpu-seconds overall
+    # each step is one oracle critic step (sub-batched + extrapolated above --cpu-rows); the
+    # whole run is bounded by --cpu-seconds (at least one timed step after the warm-up)
     steps = max(1, args.steps)
     budget = max(args.cpu_seconds, 1.0)
-    val, cores, n = oracle_steps(cfg, chunks, budget, steps, warm=args.warmup)
-    line = {"metric": METRIC, "value": round(val, 4), "unit": UNIT, "impl": "reference",
+    val, cores, n, desc = oracle_steps(cfg, chunks, budget, steps, warm=args.warmup, rows=args.cpu_rows)
+    model, blas = host_info()
+    line = {"metric": METRIC, "value": round(val, 6), "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": n, "warmup": args.warmup,
             "ms_per_step": round(1e3 / val, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "global_batch": cfg["batch"],
                        "energy": cfg["energy"], "loss": cfg["loss"]},
-            "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{n} full oracle critic steps (relabel+fwd+loss+bwd+Adam) "
-                                       f"on the {cfg['name']} workload, batch {cfg['batch']}"},
-            "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+            "cpu_baseline": {"value": round(val, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "cpu_model": model, "blas": blas, "sample": desc},
+            "e2e": {"value": round(val, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def step_bound_us(cfg, N, Bl, peaks):
+    """SURVEY §8(d) D3 algorithmic-work bound of one step on one GPU (µs), with this box's
+    MEASURED_PEAKS: encoders 2 (2 fwd + dX) MACs per row on the sustained bf16 peak (FP32 SIMT
+    for fp32), logits max(6 B_l N D flops on the tensor pipe, 4 (L2) / 2 MUFU ops per logit on
+    148 x 16 op/clk at the max SM clock), sampler and Adam bytes on HBM."""
+    D, Wd, depth = cfg["repr_dim"], cfg["width"], cfg["depth"]
+    fp32 = cfg["precision"] == "fp32"
+    fwd = dx = 0
+    for ind in (cfg["obs_dim"] + cfg["act_dim"], cfg["goal_dim"]):
+        d = [ind] + [Wd] * depth + [D]
+        fwd += sum(d[l] * d[l + 1] for l in range(len(d) - 1))
+        dx += sum(d[l] * d[l + 1] for l in range(1, len(d) - 1))
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    tc = (148 * 128 * 2 * mhz * 1e6) if fp32 else peaks["bf16_tflops_sustained"] * 1e12
+    t_enc = 2.0 * (2 * fwd + dx) * Bl / tc
+    t_ltc = 6.0 * Bl * N * D / tc
+    t_mufu = Bl * N * (4.0 if cfg["energy"] == "l2" else 2.0) / (148 * 16 * mhz * 1e6)
+    row = 2 * 4 * (cfg["obs_dim"] + cfg["act_dim"] + cfg["goal_dim"]) + 4
+    t_samp = row * Bl / (peaks["hbm_gbs"] * 1e9)
+    t_adam = (28.0 if fp32 else 30.0) * crl_synth.critic_param_count(cfg) / (peaks["hbm_gbs"] * 1e9)
+    return {"bound_us": round(1e6 * (t_enc + max(t_ltc, t_mufu) + t_samp + t_adam), 2),
+            "encoders_us": round(1e6 * t_enc, 2), "logits_tensor_us": round(1e6 * t_ltc, 2),
+            "logits_mufu_us": round(1e6 * t_mufu, 2), "sampler_us": round(1e6 * t_samp, 3),
+            "adam_us": round(1e6 * t_adam, 2)}
 
 
 # ----------------------------------------------------------------------------- ours
@@ -391,7 +491,10 @@ def run_ours(args):
     status = ctx.status()
     value = args.steps / (total_ms * 1e-3)
 
-    # ---- end to end: host (pinned) batch in, host loss out, through crl_critic_step
+    # ---- end to end: host (pinned) batch in, host loss out, through crl_critic_step, timed by
+    # the host wall clock over K back-to-back calls (the call a user makes: each one copies its
+    # step's s, a, g from page-locked host memory and writes the loss into page-locked host
+    # memory; the clock stops after the device has finished the last step)
     e2e = None
     if not args.no_e2e:
         K = max(3, min(args.steps, 200))
@@ -406,24 +509,22 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        f0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-        f1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-        with torch.cuda.stream(stream):
-            for i in range(K):
-                flush.zero_()
-                f0[i].record(stream)
-                ctx.critic_step(*hb[i], hloss, stream=stream)
-                f1[i].record(stream)
         torch.cuda.synchronize()
-        e_ms = sum(x.elapsed_time(y) for x, y in zip(f0, f1))
+        w0 = time.perf_counter()
+        for i in range(K):
+            ctx.critic_step(*hb[i], hloss, stream=stream)
+        stream.synchronize()
+        e_ms = (time.perf_counter() - w0) * 1e3
         if world > 1:
             t = torch.tensor([e_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t)
         e2e = {"value": round(K / (e_ms * 1e-3), 3), "unit": UNIT,
                "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in hb[0])),
-               "d2h_bytes_per_step": 16,
-               "note": "crl_critic_step with pinned-host s/a/g and host loss (H2D+D2H inside the timed region)"}
+               "d2h_bytes_per_step": 16, "steps": K,
+               "note": "host wall clock over K back-to-back crl_critic_step calls with page-locked host "
+                       "s/a/g (H2D inside each call) and a page-locked host loss written every step; "
+                       "max over ranks"}
 
     # ---- per-stage profile (eager, event-bracketed) for the roofline
     ctx.profile_enable(True)
@@ -483,12 +584,21 @@ def run_ours(args):
                              "floor_us": round(floor, 2),
                              "frac": round(floor / (total_ms / args.steps * 1e3), 4),
                              "source": "scratch/graph_floor.cu (dependent tiny kernels, CUDA graph + PDL)"}
+        if rl is not None:
+            # the whole step against the SURVEY §8(d) D3 bound (the north_star's roofline target)
+            sb = step_bound_us(cfg, N, Bl, peaks)
+            step_us = total_ms / args.steps * 1e3
+            rl["step"] = dict(sb, measured_us=round(step_us, 2), frac=round(sb["bound_us"] / step_us, 4),
+                              note="bound = encoders + max(logits tensor, logits MUFU) + sampler + Adam "
+                                   "(SURVEY 8(d) D3, MEASURED_PEAKS sustained bf16 / HBM, MUFU at sm_max_mhz); "
+                                   "frac = bound / measured step")
         cpu = None
         if not args.no_cpu_baseline:
-            val, cores, n = oracle_steps(cfg, chunks, args.cpu_seconds, 10_000)
-            cpu = {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
-                   "sample": f"{n} full oracle critic steps (relabel+fwd+loss+bwd+Adam, fp64 NumPy) "
-                             f"on the same {cfg['name']} workload (batch {N}), ~{args.cpu_seconds:.0f} s"}
+            val, cores, n, desc = oracle_steps(cfg, chunks, args.cpu_seconds, 10_000, rows=args.cpu_rows)
+            model, blas = host_info()
+            cpu = {"value": round(val, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "cpu_model": model, "blas": blas,
+                   "sample": f"{desc}; ~{args.cpu_seconds:.0f} s budget"}
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
@@ -514,8 +624,22 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` (N > 1) started without torchrun: become N ranks (one per GPU) via
+    torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        relaunch_under_torchrun(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -6,6 +6,7 @@
 #include "tc_cchain.h"
 #include "tc_chain.h"
 #include "tc_dwg.h"
+#include "tc_pgemm.h"
 
 #include <nccl.h>
 
@@ -179,6 +180,9 @@ struct crl_ctx {
     int bn_fwd = 64, bn_dw = 64, bn_dx = 64;
     const __nv_bfloat16* dz = nullptr;   // dZ_l (bf16) consumed by this layer's backward
     __nv_bfloat16* dzprev = nullptr;     // dZ_{l-1} written by this layer's dX GEMM
+    // wide layers: the persistent CTA-pair GEMM (tc_pgemm.cu) for the forward / dX products
+    bool pg_fwd = false, pg_dx = false;
+    tc::PgemmMaps pgf{}, pgd{};
   };
   std::vector<TcLayer> tc_phi, tc_psi;
   // tensor-core logits stage (bf16 path with N >= kTcLogitsMinN)

@@ -26,6 +26,7 @@ cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, floa
 cudaError_t launch_reduce_partials(float*, size_t, int, cudaStream_t);
 namespace tc {
 bool make_map_bf16(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
+bool make_map_f32(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
 int tc_pick_bn(int M, int N, int num_sms);
 cudaError_t tc_forward(int, const CUtensorMap&, const CUtensorMap&, int, int, int, const float*,
                        __nv_bfloat16*, __nv_bfloat16*, int, float*, int, int, float*, int, cudaStream_t);
@@ -56,7 +57,8 @@ using namespace crl;
 
 static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const __nv_bfloat16* x0, int ld0,
                                      __nv_bfloat16** Xb, __nv_bfloat16** Zb, __nv_bfloat16* dY,
-                                     __nv_bfloat16** dzb, std::vector<crl_ctx::TcLayer>& out) {
+                                     __nv_bfloat16** dzb, float* Yf, __nv_bfloat16* Yb,
+                                     std::vector<crl_ctx::TcLayer>& out) {
   const int Bl = ctx->cfg.batch_local, Wd = ctx->cfg.width, L = P.n_layers;
   out.assign(L, crl_ctx::TcLayer{});
   for (int l = 0; l < L; ++l) {
@@ -78,6 +80,27 @@ static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const _
       ok = ok && tc::make_map_bf16(&T.dxA, T.dz, o, Bl, o, 64, 128) &&     // dZ K-major (K = out)
            tc::make_map_bf16(&T.dxB, W, o, in, o, 64, T.bn_dx);            // W  K-major (N = in)
     if (!ok) return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed (driver entry point missing?)");
+    // wide layers (width >= 256, 64-aligned): the persistent CTA-pair GEMM; its output row
+    // statistic needs the whole representation in one 256-column tile (D <= 256)
+    const bool last = l == L - 1;
+    T.pg_fwd = tc::tc_pgemm_supported(Bl, o, in) && (!last || o <= 256);
+    if (T.pg_fwd) {
+      T.pgf.a = T.fwdA;
+      T.pgf.b = T.fwdB;                                                     // W {out, in} box {64, 64}
+      ok = last ? (tc::make_map_f32(&T.pgf.out0, Yf, o, Bl, o, 32, 32) &&
+                   tc::make_map_bf16(&T.pgf.out1, Yb, o, Bl, o, 64, 32))
+                : (tc::make_map_bf16(&T.pgf.out0, Zb[l], o, Bl, o, 64, 32) &&
+                   tc::make_map_bf16(&T.pgf.out1, Xb[l + 1], o, Bl, o, 64, 32));
+      if (!ok) return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the CTA-pair GEMM");
+    }
+    T.pg_dx = l > 0 && tc::tc_pgemm_supported(Bl, in, o);
+    if (T.pg_dx) {
+      T.pgd.a = T.dxA;                                                      // dZ_l {out, B} box {64, 128}
+      ok = tc::make_map_bf16(&T.pgd.b, W, o, in, o, 64, 128) &&            // W K-major {out, in}
+           tc::make_map_bf16(&T.pgd.out0, T.dzprev, in, Bl, in, 64, 32) &&
+           tc::make_map_bf16(&T.pgd.zin, Zb[l - 1], in, Bl, in, 64, 32);
+      if (!ok) return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the CTA-pair GEMM");
+    }
   }
   return CRL_OK;
 }
@@ -85,10 +108,10 @@ static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const _
 crl_status bf16_prepare(crl_ctx* ctx) {
   const crl_config& k = ctx->cfg;
   crl_status st = build_encoder_plan(ctx, ctx->phi_plan, ctx->x0_phi, ctx->ld0_phi, ctx->phiXb, ctx->phiZb,
-                                     ctx->dphib, ctx->dzb_phi, ctx->tc_phi);
+                                     ctx->dphib, ctx->dzb_phi, ctx->phi_out, ctx->phi_outb, ctx->tc_phi);
   if (st != CRL_OK) return st;
   st = build_encoder_plan(ctx, ctx->psi_plan, ctx->x0_psi, ctx->ld0_psi, ctx->psiXb, ctx->psiZb, ctx->dpsib,
-                          ctx->dzb_psi, ctx->tc_psi);
+                          ctx->dzb_psi, ctx->psi_out, ctx->psi_outb, ctx->tc_psi);
   if (st != CRL_OK) return st;
   // grouped weight / bias gradients: X_l and dZ_l of every layer of both encoders
   ctx->use_dwg = !std::getenv("CRL_NO_DWG");
@@ -271,9 +294,15 @@ static crl_status enc_forward_bf16(crl_ctx* ctx, const char* tag, const EncoderP
     const LayerPlan& Lp = P.layer[l];
     const bool last = l == L - 1;
     Stage sg(ctx, st, std::string(tag) + "_fwd_l" + std::to_string(l));
-    CU(tc::tc_forward(T[l].bn_fwd, T[l].fwdA, T[l].fwdB, Bl, Lp.in, Lp.out, ctx->mem.params + Lp.b_off,
-                      last ? nullptr : Zb[l], last ? yb : Xb[l + 1], Lp.out, last ? yf : nullptr, Lp.out,
-                      k.activation, last ? ystat : nullptr, k.energy, st));
+    if (T[l].pg_fwd) {
+      const tc::PgemmArgs pa{Bl, Lp.out, Lp.in, ctx->mem.params + Lp.b_off, k.activation, last ? ystat : nullptr,
+                             k.energy};
+      CU(tc::tc_pgemm(last ? tc::PG_FWD_OUT : tc::PG_FWD_HIDDEN, T[l].pgf, pa, ctx->num_sms, st));
+    } else {
+      CU(tc::tc_forward(T[l].bn_fwd, T[l].fwdA, T[l].fwdB, Bl, Lp.in, Lp.out, ctx->mem.params + Lp.b_off,
+                        last ? nullptr : Zb[l], last ? yb : Xb[l + 1], Lp.out, last ? yf : nullptr, Lp.out,
+                        k.activation, last ? ystat : nullptr, k.energy, st));
+    }
     ++*nl;
   }
   return CRL_OK;
@@ -306,8 +335,13 @@ static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const Encoder
     }
     if (l > 0) {
       Stage sg(ctx, st, std::string(tag) + "_bwd_dx_l" + std::to_string(l));
-      CU(tc::tc_backward_dx(T[l].bn_dx, T[l].dxA, T[l].dxB, Bl, Lp.in, Lp.out, Zb[l - 1], T[l].dzprev, Lp.in,
-                            k.activation, st));
+      if (T[l].pg_dx) {
+        const tc::PgemmArgs pa{Bl, Lp.in, Lp.out, nullptr, k.activation, nullptr, k.energy};
+        CU(tc::tc_pgemm(tc::PG_DX, T[l].pgd, pa, ctx->num_sms, st));
+      } else {
+        CU(tc::tc_backward_dx(T[l].bn_dx, T[l].dxA, T[l].dxB, Bl, Lp.in, Lp.out, Zb[l - 1], T[l].dzprev, Lp.in,
+                              k.activation, st));
+      }
       ++*nl;
     }
   }
@@ -364,8 +398,9 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   const int row_off = k.rank * Bl;
   // the per-row statistic of Y comes out of the last forward layer's epilogue when that
   // layer's output row fits one CTA (else a separate row-statistic launch)
-  const bool stat_in_fwd = ctx->tc_logits && !ctx->use_chain && D <= ctx->tc_phi.back().bn_fwd &&
-                           D <= ctx->tc_psi.back().bn_fwd;
+  auto stat_fits = [&](const crl_ctx::TcLayer& T) { return T.pg_fwd ? D <= 256 : D <= T.bn_fwd; };
+  const bool stat_in_fwd = ctx->tc_logits && !ctx->use_chain && stat_fits(ctx->tc_phi.back()) &&
+                           stat_fits(ctx->tc_psi.back());
   {
     Stage sg(ctx, st, "prep_inputs");
     // also re-arms the step's device flags (fused-stats fallback gate, fast-factor flag)

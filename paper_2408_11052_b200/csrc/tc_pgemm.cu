@@ -1,0 +1,446 @@
+// tc_pgemm.cu — persistent CTA-pair (tcgen05 cta_group::2) GEMM for the wide encoder layers of
+// the BF16 path (SURVEY §8(a) A2 forward and A5 dX at width 1024: configs[4], §5.4 P:387-465,
+// Table 2).
+//
+//   forward  Z[M][N] = X[M][K] . W[K][N] + b     A = X  K-major, B = W MN-major (as stored)
+//            hidden: Z (bf16) and act(Z) (bf16);  output layer: Y fp32 + Y bf16 + row statistic
+//   dX       dZp[M][N] = (dZ[M][K] . W[N][K]^T) * act'(Zp)   A = dZ K-major, B = W K-major
+//
+// Anatomy.  A cluster of 2 CTAs (a TPC pair) owns one 256 x 256 output tile at a time and walks
+// the tile list persistently (tile t = cluster id + k * #clusters, N fastest so the pairs that
+// run together share their A rows in L2).  The MMA is tcgen05.mma.cta_group::2 (M = 256,
+// N = 256, K = 16): CTA r of the pair stages rows [128 r, 128 r + 128) of A and columns
+// [128 r, 128 r + 128) of B, so each SM reads half the operand bytes of a 1-CTA 128 x 256 tile
+// from its kSmem and the L2 -> kSmem traffic per tile is halved; each CTA's TMEM receives its
+// 128 rows x 256 columns of the accumulator.
+//   warp 0 (lane 0, both CTAs)  TMA producer: 5-stage ring of 64-wide K blocks (32 KB / stage /
+//                               CTA); completion bytes of BOTH CTAs land on the leader's full
+//                               barrier (cta_group::2 TMA)
+//   warp 1 (lane 0, leader)     MMA issuer; stage release and accumulator-ready commits are
+//                               multicast to both CTAs
+//   warps 2..5 (both CTAs)      epilogue: TMEM lane quarter q = warp & 3 (32 rows), 64-column
+//                               chunks: tcgen05.ld -> bias / activation / activation' -> bf16
+//                               (fp32) SW128 staging -> TMA tensor stores (DX: the Z_prev chunk
+//                               arrives by TMA into the same staging buffer first)
+//   TMEM: two 256-column fp32 accumulators (512 columns): tile t's epilogue overlaps tile
+//   t + 1's mainloop; the leader's MMA waits on an "accumulator empty" barrier that all 8
+//   epilogue warps of the pair arrive on.
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+#include "tc_pgemm.h"
+
+namespace crl {
+namespace tc {
+namespace pg {
+
+constexpr int kBK = 64, kStages = 5, kTN = 256;      // K block, ring depth, tile N (= tile M / 1)
+constexpr uint32_t kAHalf = 128 * kBK * 2;          // 16 KB: this CTA's 128 rows of A
+constexpr uint32_t kBHalf = 128 * kBK * 2;          // 16 KB: this CTA's 128 columns of B
+constexpr uint32_t kStage = kAHalf + kBHalf;
+constexpr uint32_t kStgBuf = 32 * 128;             // 4 KB: 32 rows x 128 B (SW128) staging
+constexpr int kNStg = 4;                            // staging buffers per epilogue warp
+constexpr size_t kSmem = 1024 + kStages * kStage + 4 * kNStg * kStgBuf + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's kSmem, completion bytes on a barrier of either CTA of the pair
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t mbar_cluster, int x,
+                                                 int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_local(uint32_t dst, const CUtensorMap* map, uint64_t* mbar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(mbar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void expect_tx_remote(uint32_t mbar_cluster, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(mbar_cluster), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t mbar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cluster) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEC_%=;\n\t"
+      "bra WAITC_%=;\n"
+      "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// arrive (once all previously issued MMAs completed) on the barrier at this offset in both CTAs
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+}  // namespace pg
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    tc_pgemm_kernel(const __grid_constant__ PgemmMaps maps, const PgemmArgs p) {
+  using namespace pg;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sStage = smem;
+  uint8_t* sStg = sStage + kStages * kStage;                         // [4 warps][kNStg][4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * kNStg * kStgBuf);
+  uint64_t* full = bars;                  // [kStages]  leader: both CTAs' TMA bytes
+  uint64_t* empty = full + kStages;        // [kStages]  both: MMA commit (multicast)
+  uint64_t* tfull = empty + kStages;       // [2]       both: accumulator ready (multicast)
+  uint64_t* tempty = tfull + 2;           // [2]       leader: 8 epilogue warps of the pair
+  uint64_t* zbar = tempty + 2;            // [4][kNStg] DX: Z_prev chunk landed (per warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zbar + 4 * kNStg);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
+  const int tiles_n = (p.N + kTN - 1) / kTN;
+  const int n_tiles = ((p.M + 255) / 256) * tiles_n;
+  const int nkb = (p.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&maps.a);
+    tma_prefetch_desc(&maps.b);
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int i = 0; i < 4 * kNStg; ++i) mbar_init(&zbar[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();                          // both CTAs' barriers and TMEM exist
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ TMA producer
+      const uint32_t full_leader = mapa(smem_u32(full), 0);
+      int g = 0;
+      for (int t = cid; t < n_tiles; t += ncl) {
+        const int m0 = (t / tiles_n) * 256 + 128 * (int)rank;
+        const int n0 = (t % tiles_n) * kTN + 128 * (int)rank;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % kStages;
+          mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
+          const uint32_t fb = full_leader + 8u * (uint32_t)s;
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * kStage);
+          const uint32_t a_dst = smem_u32(sStage + s * kStage);
+          const uint32_t b_dst = a_dst + kAHalf;
+          const int k = kb * kBK;
+          tma_load_2d_pair(a_dst, &maps.a, fb, k, m0);                       // A {K, M} box {64, 128}
+          if (EPI == PG_DX) {
+            tma_load_2d_pair(b_dst, &maps.b, fb, k, n0);                     // W {K=out, N=in} box {64, 128}
+          } else {
+            tma_load_2d_pair(b_dst, &maps.b, fb, n0, k);                     // W {N, K} box {64, 64} x 2
+            tma_load_2d_pair(b_dst + kBK * 128, &maps.b, fb, n0 + 64, k);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      // ------------------------------------------------------------------ MMA issuer (leader)
+      const uint32_t idesc = idesc_bf16_f32(256, kTN, false, EPI != PG_DX);
+      int g = 0, it = 0;
+      for (int t = cid; t < n_tiles; t += ncl, ++it) {
+        const int b = it & 1;
+        mbar_wait_acq_cluster(&tempty[b], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + 256u * (uint32_t)b;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % kStages;
+          mbar_wait(&full[s], (g / kStages) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sStage + s * kStage);
+          const uint32_t b_base = a_base + kAHalf;
+#pragma unroll
+          for (int ks = 0; ks < kBK / 16; ++ks) {
+            const uint64_t ad = smem_desc_sw128(a_base + ks * 32, 16, 1024);
+            const uint64_t bd = EPI == PG_DX ? smem_desc_sw128(b_base + ks * 32, 16, 1024)
+                                             : smem_desc_sw128(b_base + ks * 2048, kBK * 128, 1024);
+            mma_pair(d, ad, bd, idesc, (kb | ks) != 0);
+          }
+          commit_pair(&empty[s]);
+        }
+        commit_pair(&tfull[b]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;                               // TMEM lane quarter = 32 rows
+    const int ew = warp - 2;                              // staging owner index
+    const uint32_t stg0 = smem_u32(sStg + (size_t)ew * kNStg * kStgBuf);
+    uint64_t* zb = zbar + ew * kNStg;
+    const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
+    const uint32_t row_sw = (uint32_t)((lane >> 3) * 1024 + (lane & 7) * 128);   // SW128 row base
+    int it = 0;
+    uint32_t zphase = 0;                                   // DX: parity bits of zb[] (one per buffer)
+    for (int t = cid; t < n_tiles; t += ncl, ++it) {
+      const int b = it & 1;
+      const int mrow0 = (t / tiles_n) * 256 + 128 * (int)rank + 32 * q;   // first row of this warp
+      const int ncol0 = (t % tiles_n) * kTN;
+      const int nch = min(kTN, p.N - ncol0) / 64;         // 64-column chunks (N % 64 == 0)
+      if (EPI == PG_DX && lane == 0) {
+        // Z_prev chunks for this tile: issued before the accumulator is ready (latency hidden
+        // behind the mainloop); buffer c holds chunk c (nch <= kNStg)
+        bulk_wait_read<0>();                              // staging reads of the last tile done
+        for (int c = 0; c < nch; ++c) {
+          mbar_expect_tx(&zb[c], kStgBuf);
+          tma_load_2d_local(stg0 + c * kStgBuf, &maps.zin, &zb[c], ncol0 + 64 * c, mrow0);
+        }
+      }
+      if (EPI != PG_DX && lane == 0) bulk_wait_read<0>();  // staging of the previous tile read
+      __syncwarp();
+      mbar_wait(&tfull[b], (it >> 1) & 1);
+      tc_fence_after();
+      float ysq = 0.f;
+      for (int c = 0; c < nch; ++c) {
+        uint32_t v[64];
+        const uint32_t ta = tmem + 256u * (uint32_t)b + ((uint32_t)(q * 32) << 16) + 64u * (uint32_t)c;
+        tmem_ld32_nowait(ta, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32_nowait(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        tmem_ld_wait();
+        if (c == nch - 1) {                               // accumulator b free for tile it + 2
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_remote(tempty_leader + 8u * (uint32_t)b);
+        }
+        const int n = ncol0 + 64 * c;
+        float f[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]);
+        if (EPI == PG_DX) {
+          // dZ_prev = acc * act'(Z_prev); Z_prev from the staging buffer, result written back in place
+          mbar_wait(&zb[c], (zphase >> c) & 1);
+          const uint32_t buf = stg0 + c * kStgBuf + row_sw;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t addr = buf + (uint32_t)(((j ^ (lane & 7))) << 4);
+            const uint4 zz = lds128(addr);
+            const uint32_t w[4] = {zz.x, zz.y, zz.z, zz.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+              float& a0 = f[8 * j + 2 * h];
+              float& a1 = f[8 * j + 2 * h + 1];
+              if (p.act == CRL_ACT_SILU) {
+                const float h0 = 0.5f * z.x, h1 = 0.5f * z.y;
+                const float t0 = pg::tanh_approx(h0), t1 = pg::tanh_approx(h1);
+                a0 *= fmaf(0.5f, fmaf(h0, fmaf(-t0, t0, 1.f), t0), 0.5f);
+                a1 *= fmaf(0.5f, fmaf(h1, fmaf(-t1, t1, 1.f), t1), 0.5f);
+              } else {
+                a0 = z.x > 0.f ? a0 : 0.f;
+                a1 = z.y > 0.f ? a1 : 0.f;
+              }
+            }
+            sts128(addr, make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                                    pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7])));
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&maps.out0, stg0 + c * kStgBuf, n, mrow0);
+            bulk_commit();
+          }
+        } else {
+          // + bias (broadcast loads: every lane reads the same column)
+#pragma unroll
+          for (int i4 = 0; i4 < 16; ++i4) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(p.bias + n) + i4);
+            f[4 * i4] += bb.x; f[4 * i4 + 1] += bb.y; f[4 * i4 + 2] += bb.z; f[4 * i4 + 3] += bb.w;
+          }
+          // buffers: hidden: Z chunk, act(Z) chunk (2 x 4 KB) at (2c) % kNStg and (2c+1) % kNStg;
+          // output layer: Y bf16 (4 KB) + Y fp32 (two 32-column SW128 halves, 2 x 4 KB)
+          if (EPI == PG_FWD_HIDDEN) {
+            if (lane == 0 && c >= 2) bulk_wait_read<1>();  // the buffers of chunk c - 2 are read
+            __syncwarp();
+            const uint32_t bz = stg0 + ((2 * c) % kNStg) * kStgBuf + row_sw;
+            const uint32_t bx = stg0 + ((2 * c + 1) % kNStg) * kStgBuf + row_sw;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t off = (uint32_t)(((j ^ (lane & 7))) << 4);
+              float* z = f + 8 * j;
+              sts128(bz + off, make_uint4(pack_bf16x2(z[0], z[1]), pack_bf16x2(z[2], z[3]), pack_bf16x2(z[4], z[5]),
+                                          pack_bf16x2(z[6], z[7])));
+              float x[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (p.act == CRL_ACT_SILU) {
+                  const float h = 0.5f * z[i];
+                  x[i] = fmaf(h, pg::tanh_approx(h), h);
+                } else {
+                  x[i] = fmaxf(z[i], 0.f);
+                }
+              }
+              sts128(bx + off, make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
+                                          pack_bf16x2(x[6], x[7])));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&maps.out0, bz - row_sw, n, mrow0);
+              tma_store_2d(&maps.out1, bx - row_sw, n, mrow0);
+              bulk_commit();
+            }
+          } else {                                        // PG_FWD_OUT
+            if (lane == 0 && c >= 1) bulk_wait_read<0>();  // chunk c - 1's staging is read
+            __syncwarp();
+            const uint32_t by = stg0 + row_sw;                         // bf16 Y
+            const uint32_t bf0 = stg0 + kStgBuf + row_sw;              // fp32 Y columns 0..31
+            const uint32_t bf1 = stg0 + 2 * kStgBuf + row_sw;          // fp32 Y columns 32..63
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t off = (uint32_t)(((j ^ (lane & 7))) << 4);
+              float* y = f + 8 * j;
+              const uint4 hb = make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]),
+                                          pack_bf16x2(y[6], y[7]));
+              sts128(by + off, hb);
+              // the logits stage's row statistic is taken on the bf16-rounded Y it will read
+              const uint32_t w[4] = {hb.x, hb.y, hb.z, hb.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                const float2 yb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+                ysq = fmaf(yb.x, yb.x, fmaf(yb.y, yb.y, ysq));
+              }
+              // fp32: 8 floats = 2 x 16 B chunks of the 32-column half j / 4
+              const uint32_t bfh = (j < 4) ? bf0 : bf1;
+              const int c16 = 2 * (j & 3);
+              sts128(bfh + (uint32_t)(((c16 ^ (lane & 7))) << 4),
+                     make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]), __float_as_uint(y[3])));
+              sts128(bfh + (uint32_t)((((c16 + 1) ^ (lane & 7))) << 4),
+                     make_uint4(__float_as_uint(y[4]), __float_as_uint(y[5]), __float_as_uint(y[6]), __float_as_uint(y[7])));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&maps.out1, by - row_sw, n, mrow0);
+              tma_store_2d(&maps.out0, bf0 - row_sw, n, mrow0);
+              tma_store_2d(&maps.out0, bf1 - row_sw, n + 32, mrow0);
+              bulk_commit();
+            }
+          }
+        }
+      }
+      if (EPI == PG_DX) zphase ^= (1u << nch) - 1u;
+      if (EPI == PG_FWD_OUT && p.stat != nullptr) {
+        const int row = mrow0 + lane;
+        if (row < p.M)
+          p.stat[row] = p.stat_energy == CRL_ENERGY_L2 ? ysq
+                        : (p.stat_energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(ysq), kEpsCos) : 0.f);
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+  }
+  tc_fence_before();
+  cluster_sync();                          // the peer's MMAs / arrivals are done before TMEM goes
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// -------------------------------------------------------------------------------- host side
+// M: rows (any, >= 256 so a pair has work), N: a multiple of 64 (whole staging chunks), >= 256
+// (the 256-wide tile; narrower layers keep tc_gemm), K: any (TMA zero-fills the last K block)
+bool tc_pgemm_supported(int M, int N, int K) {
+  return M >= 256 && N >= 256 && N % 64 == 0 && K >= 1 && !std::getenv("CRL_NO_PGEMM");
+}
+
+template <int EPI>
+static cudaError_t launch_pg(const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_pgemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)pg::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = ((p.M + 255) / 256) * ((p.N + pg::kTN - 1) / pg::kTN);
+  const int clusters = std::max(1, std::min(tiles, num_sms / 2));
+  return launch_pdl(tc_pgemm_kernel<EPI>, dim3(2 * clusters), dim3(192), pg::kSmem, st, maps, p);
+}
+
+cudaError_t tc_pgemm(int epi, const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
+  switch (epi) {
+    case PG_FWD_HIDDEN: return launch_pg<PG_FWD_HIDDEN>(maps, p, num_sms, st);
+    case PG_FWD_OUT: return launch_pg<PG_FWD_OUT>(maps, p, num_sms, st);
+    case PG_DX: return launch_pg<PG_DX>(maps, p, num_sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tc
+}  // namespace crl

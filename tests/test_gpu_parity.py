@@ -765,3 +765,15 @@ def test_graph_cache_is_bounded_and_exact():
         torch.cuda.synchronize()
         assert np.array_equal(la.cpu().numpy().view(np.uint32), lb.cpu().numpy().view(np.uint32)), it
     assert ctx_a.status() == 0 and ctx_b.status() == 0
+
+
+@pytest.mark.parametrize("batch,width,repr_dim", [
+    (300, 1024, 256),     # ragged last 256-row tile of the CTA-pair GEMM
+    (1100, 320, 64),      # N = 320: a partial 256-column tile (one 64-column chunk)
+    (640, 256, 256),      # width 256, D 256: one N tile per layer, output layer N = 256
+])
+def test_critic_step_bf16_pair_gemm_shapes(batch, width, repr_dim):
+    """The persistent CTA-pair GEMM (tc_pgemm.cu: tcgen05 cta_group::2, 256 x 256 tiles, double
+    TMEM accumulator) serves every forward / dX product with N >= 256; ragged M and N tiles."""
+    cfg = crl_synth.preset("ant", batch=batch, width=width, repr_dim=repr_dim, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
