@@ -172,6 +172,14 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
         c->gf_acc = s.take<float>(c->gf_acc_bytes / 4);
         c->gf_cs = c->gf_acc + (size_t)N * D;
       }
+      // D = 256 (configs[4]): both gradient sides in one persistent launch (tc_grad2.cu)
+      c->use_grad2 = D == 256 && !c->use_gradf && !std::getenv("CRL_NO_GRAD2");
+      if (c->use_grad2) {
+        c->g2_grid = tc::tc_grad2_grid(Bl, device_sms());
+        c->g2_part_da = s.take<float>((size_t)4 * Bl * D);
+        c->g2_part_rs = s.take<float>((size_t)4 * Bl);
+        c->g2_flags = s.take<unsigned char>((size_t)2 * ((Bl + 127) / 128));
+      }
     }
   }
   c->phi_out = s.take<float>((size_t)Bl * D);

@@ -7,6 +7,7 @@
 #include "tc_chain.h"
 #include "tc_dwg.h"
 #include "tc_pgemm.h"
+#include "tc_grad2.h"
 
 #include <nccl.h>
 
@@ -207,6 +208,7 @@ struct crl_ctx {
   float *st_part_rs = nullptr;                // [st_splits][B_l] row sums
   float *st_colpart = nullptr;                // [row blocks][st_ldc] column sums
   int* st_bad = nullptr;                      // set by the merge: the exact online-max path runs
+  CUtensorMap st_A, st_B;                     // its operand maps (A, B boxes {64, 128})
   // both gradient sides in one pass (tc_gradf.cu; W = 1, L2 / dot, D = 64)
   bool use_gradf = false;
   int gf_splits = 1;
@@ -214,6 +216,12 @@ struct crl_ctx {
   float *gf_acc = nullptr, *gf_cs = nullptr;            // column side [N][64], [N] (reductions)
   size_t gf_acc_bytes = 0;
   CUtensorMap gf_map;
+  // both gradient sides in one persistent launch at D = 256 (tc_grad2.cu)
+  bool use_grad2 = false;
+  int g2_grid = 0;
+  float *g2_part_da = nullptr, *g2_part_rs = nullptr;   // [2 sides][2 slots][B_l][D], [2][2][B_l]
+  unsigned char* g2_flags = nullptr;                    // [2 sides][row blocks] slot-1 flags
+  CUtensorMap g2_B0, g2_B1;                             // B operands (box {64, 64}): Psi_g, Phi_g
   // all weight / bias gradients of both encoders in one grouped launch (tc_dwg.cu)
   bool use_dwg = false;
   tc::DwgParams dwg;

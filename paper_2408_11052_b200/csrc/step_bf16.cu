@@ -9,8 +9,10 @@
 // All tensor maps are built once at context creation (buffers are context-owned).
 #include "ctx.h"
 #include "tc_gradf.h"
+#include "tc_merge.cuh"
 
 #include <cstdlib>
+#include <vector>
 
 namespace crl {
 cudaError_t logits_lse_f32(int, int, const float*, int, const float*, int, float*, cudaStream_t);
@@ -50,6 +52,7 @@ cudaError_t tc_logits_grad(int, int, const CUtensorMap&, const CUtensorMap&, int
                            float, int, float*, float*, const __nv_bfloat16*, const __nv_bfloat16*, float*,
                            __nv_bfloat16*, const int*, cudaStream_t);
 cudaError_t launch_rowstat_bf16(const __nv_bfloat16*, int, int, int, float*, int*, int, cudaStream_t);
+cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st);
 }  // namespace tc
 }  // namespace crl
 
@@ -138,6 +141,18 @@ crl_status bf16_prepare(crl_ctx* ctx) {
         !tc::tc_logits_maps(&ctx->lg_col_A, &ctx->lg_col_B, ctx->psi_outb, k.batch_local, ctx->phi_outb_g,
                             ctx->N, k.repr_dim))
       return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the logits operands");
+    if (ctx->use_grad2) {
+      if (!tc::make_map_bf16(&ctx->g2_B0, ctx->psi_outb_g, k.repr_dim, ctx->N, k.repr_dim, 64, 64) ||
+          !tc::make_map_bf16(&ctx->g2_B1, ctx->phi_outb_g, k.repr_dim, ctx->N, k.repr_dim, 64, 64))
+        return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the gradient operands");
+      const int RB = (k.batch_local + 127) / 128;
+      std::vector<unsigned char> fl(2 * RB);
+      tc::tc_grad2_split_flags(k.batch_local, ctx->N, ctx->g2_grid, fl.data());
+      CU(cudaMemcpy(ctx->g2_flags, fl.data(), fl.size(), cudaMemcpyHostToDevice));
+    }
+    if (ctx->use_stats && (!tc::make_map_bf16(&ctx->st_A, ctx->phi_outb, k.repr_dim, k.batch_local, k.repr_dim, 64, 128) ||
+                           !tc::make_map_bf16(&ctx->st_B, ctx->psi_outb_g, k.repr_dim, ctx->N, k.repr_dim, 64, 128)))
+      return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the statistics operands");
     if (ctx->use_gradf && !tc::tc_gradf_map(&ctx->gf_map, ctx->gf_acc, ctx->N))
       return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the column-gradient accumulator");
   }
@@ -472,7 +487,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
           CU(cudaGraphConditionalHandleCreate(&cond, cg, 0, cudaGraphCondAssignDefault));
       }
       Stage sg(ctx, st, "lse_fused");
-      CU(tc::tc_stats_fused(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, ctx->stat_phi + row_off, ctx->stat_psi,
+      CU(tc::tc_stats_fused(D, k.energy, ctx->st_A, ctx->st_B, Bl, N, ctx->stat_phi + row_off, ctx->stat_psi,
                             ctx->st_splits, ctx->st_part_rs, ctx->st_colpart, ctx->st_ldc, ctx->lse_row, ctx->fac_row,
                             ctx->lse_col, ctx->fac_col, ctx->fac_ok, ctx->st_bad, invN * c_f, 2.f * invN * k.beta_lse,
                             invN * c_b, 0.f, cond, st));
@@ -569,8 +584,34 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                            ctx->psi_outb, ctx->dphi, ctx->dphib, ctx->dpsi, ctx->dpsib, gl, st));
       nl += 2; }
   }
+  if (ctx->use_grad2) {
+    // D = 256: both sides of dL/dl -> dPhi, dPsi in one persistent launch, then one merge
+    // launch for both (partial slots, L2 row-sum term, positive pair, cos projection, bf16)
+    Stage sg(ctx, st, "grad_pair");
+    tc::Grad2Args ga{};
+    ga.Na = Bl; ga.Nb = N; ga.invN = invN; ga.fac_ok = ctx->fac_ok;
+    tc::Grad2Side& s0 = ga.side[0];
+    s0.a_stat = ctx->stat_phi + row_off; s0.b_stat = ctx->stat_psi; s0.lr = ctx->lse_row; s0.lc = ctx->lse_col_g;
+    s0.lcf = ctx->fac_col_g; s0.c_r = c_f; s0.c_c = c_b; s0.beta_r = k.beta_lse; s0.beta_c = 0.f;
+    s0.part_da = ctx->g2_part_da; s0.part_rs = ctx->g2_part_rs; s0.A = ctx->phi_outb;
+    tc::Grad2Side& s1 = ga.side[1];
+    s1.a_stat = ctx->stat_psi + row_off; s1.b_stat = ctx->stat_phi; s1.lr = ctx->lse_col; s1.lc = ctx->lse_row_g;
+    s1.lcf = ctx->fac_row_g; s1.c_r = c_b; s1.c_c = c_f; s1.beta_r = 0.f; s1.beta_c = k.beta_lse;
+    s1.part_da = ctx->g2_part_da + (size_t)2 * Bl * D; s1.part_rs = ctx->g2_part_rs + (size_t)2 * Bl;
+    s1.A = ctx->psi_outb;
+    CU(tc::tc_grad2(k.energy, ctx->g2_B0, ctx->g2_B1, ga, ctx->g2_grid, st));
+    const float Cdiag = invN * (c_f + c_b);
+    tc::GradMergeArgs m0{s0.part_da, s0.part_rs, ctx->phi_outb, s0.a_stat, ctx->psi_outb_g, ctx->stat_psi, row_off,
+                         Cdiag, Bl, D, 2, ctx->dphi, ctx->dphib, 0};
+    tc::GradMergeArgs m1{s1.part_da, s1.part_rs, ctx->psi_outb, s1.a_stat, ctx->phi_outb_g, ctx->stat_phi, row_off,
+                         Cdiag, Bl, D, 2, ctx->dpsi, ctx->dpsib, 0};
+    m0.valid1 = ctx->g2_flags;
+    m1.valid1 = ctx->g2_flags + (Bl + 127) / 128;
+    CU(tc::launch_grad_merge2(k.energy, m0, m1, st));
+    nl += 2;
+  }
   fork2(ctx, st, st2);
-  if (!ctx->use_gradf) { Stage sg(ctx, st2, "grad_psi");
+  if (!ctx->use_gradf && !ctx->use_grad2) { Stage sg(ctx, st2, "grad_psi");
     if (ctx->tc_logits) {
       CU(tc::tc_logits_grad(D, k.energy, ctx->lg_col_A, ctx->lg_col_B, Bl, N, row_off, ctx->stat_psi + row_off,
                             ctx->stat_phi, ctx->lse_col, ctx->lse_row_g, ctx->fac_row_g, c_b, c_f, 0.f,
@@ -590,7 +631,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side2, &nl);
     if (rs != CRL_OK) return rs;
   }
-  if (!ctx->use_gradf) { Stage sg(ctx, st, "grad_phi");
+  if (!ctx->use_gradf && !ctx->use_grad2) { Stage sg(ctx, st, "grad_phi");
     if (ctx->tc_logits) {
       CU(tc::tc_logits_grad(D, k.energy, ctx->lg_row_A, ctx->lg_row_B, Bl, N, row_off, ctx->stat_phi + row_off,
                             ctx->stat_psi, ctx->lse_row, ctx->lse_col_g, ctx->fac_col_g, c_f, c_b,

@@ -1,0 +1,432 @@
+// tc_grad2.cu — the logits gradient pass (A4) at D = 256 (configs[4]'s representation size):
+// both sides in ONE persistent launch, dL/dl consumed in registers, dPhi / dPsi on tcgen05.
+//
+// Paper: energies App. A.2 P:607-617 (L2 sign per reading A-01), InfoNCE fwd/bwd/sym P:619-630
+// and the logsumexp penalty P:361 / Alg. 1 P:1052 (readings A-02..A-05).  The gradient of C4,
+//   g_ij = (1/N)[c_r (p_ij - d_ij) + c_c (q_ij - d_ij)] + (2 beta / N) LSE_i p_ij,
+// is mapped through the energy's VJP (C5: L2 w_ij = g_ij / r_ij, cos w_ij = g_ij / |b_j|) and
+// contracted on the tensor core: dA_i = sum_j w_ij B_j (the L2 "- (sum_j w_ij) A_i" term, the
+// positive pair and the cos projection are applied by grad_merge, tc_merge.cuh).
+//   side 0: rows A = Phi (local), columns B = Psi (global)  -> dPhi
+//   side 1: rows A = Psi (local), columns B = Phi (global)  -> dPsi   (coefficients swapped)
+//
+// Schedule (why it differs from tc_logits.cu's two-call GRAD kernel):
+//  * One CTA per SM owns a CONTIGUOUS range of the linearised (side, row block, 64-column
+//    tile) space (stream-K style): every CTA gets the same number of tiles +-1, a row block is
+//    cut into at most two pieces, whose dA partials go to slot 0 (the piece holding the row
+//    block's first tile) and slot 1 (the other piece, flagged for the merge).
+//  * The 128 x 256 A tile of the current row block lives in TMEM (tcgen05.mma with an A
+//    operand in tensor memory): S = A B^T reads only B from SMEM, and the 64 KB of SMEM an
+//    A tile would take hold a 5-deep ring of 32 KB B tiles instead (a B tile is needed until
+//    its dA MMA, one S + one epilogue after its S MMA).
+//  * TMEM (512 columns): S double buffer 2 x 64 | dA accumulator 256 | A 128 (bf16 pairs).
+//  * Per 64-column tile: S = A B^T (M 128, N 64, K 256; 16 MMAs) -> 8 epilogue warps (2 column
+//    halves x 4 lane quarters) form w_ij (one exp2 + one rsqrt / operand modifiers) as a bf16
+//    W tile in SMEM (SW128) -> dA += W B (M 128, N 256, K 64: the same SMEM B tile read as an
+//    MN-major operand).
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+#include "tc_grad2.h"
+
+namespace crl {
+namespace tc {
+namespace g2 {
+
+constexpr int D = 256, BNT = 64, STAGES = 5, NST = 4;   // repr dim, tile columns, B ring, stats ring
+constexpr uint32_t B_BYTES = BNT * D * 2;               // 32 KB: 4 SW128 chunks of [64 rows][64 D]
+constexpr uint32_t W_BYTES = 128 * BNT * 2;             // 16 KB
+constexpr uint32_t STAT_FLOATS = 3 * BNT;               // b_stat, lc, lcf of one tile
+constexpr size_t SMEM = 1024 + STAGES * B_BYTES + 2 * W_BYTES + NST * STAT_FLOATS * 4 + 128 * 4 + 256;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsq(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem]^T
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// 32 lanes x 32 bit, 32 consecutive columns per thread (registers -> TMEM)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t sw128_off(int r, int k) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2);
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// the tile range of CTA c of G over X tiles: [start(c), start(c + 1))
+__host__ __device__ __forceinline__ long range_start(long c, long X, long G) { return (c * X) / G; }
+
+}  // namespace g2
+
+template <int ENERGY>
+__global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant__ CUtensorMap tmB0,
+                                                          const __grid_constant__ CUtensorMap tmB1, const Grad2Args p) {
+  using namespace g2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = smem;                                                     // [STAGES] B tiles
+  uint8_t* sW = sB + STAGES * B_BYTES;                                    // [2] W tiles
+  float* sStat = reinterpret_cast<float*>(sW + 2 * W_BYTES);              // [NST][3][64]
+  float* sMerge = sStat + NST * STAT_FLOATS;                              // [128] row-sum hand-off
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + 128);
+  uint64_t* b_full = bars;                 // [STAGES]
+  uint64_t* b_empty = b_full + STAGES;     // [STAGES]
+  uint64_t* st_full = b_empty + STAGES;    // [NST]
+  uint64_t* st_empty = st_full + NST;      // [NST]
+  uint64_t* s_full = st_empty + NST;       // [2]
+  uint64_t* s_empty = s_full + 2;          // [2]
+  uint64_t* w_full = s_empty + 2;          // [2]
+  uint64_t* w_empty = w_full + 2;          // [2]
+  uint64_t* a_full = w_empty + 2;          // A of the current unit is in TMEM
+  uint64_t* da_full = a_full + 1;          // the unit's dA accumulation is complete
+  uint64_t* da_empty = da_full + 1;        // the unit's dA has been read out
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long X = 2L * p.RB * p.TPB;
+  const long x0 = range_start(blockIdx.x, X, gridDim.x), x1 = range_start(blockIdx.x + 1, X, gridDim.x);
+  // unit = the maximal run of this CTA's tiles inside one (side, row block)
+  auto unit_at = [&](long x, int& side, int& rb, int& tb, int& nt) {
+    const long r = x / p.TPB;
+    tb = (int)(x - r * p.TPB);
+    side = (int)(r / p.RB);
+    rb = (int)(r - (long)side * p.RB);
+    nt = (int)min((long)(p.TPB - tb), x1 - x);
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmB0);
+    tma_prefetch_desc(&tmB1);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
+    for (int s = 0; s < NST; ++s) { mbar_init(&st_full[s], 1); mbar_init(&st_empty[s], 8); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
+      mbar_init(&w_full[i], 8); mbar_init(&w_empty[i], 1);
+    }
+    mbar_init(a_full, 8); mbar_init(da_full, 1); mbar_init(da_empty, 8);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tm_s[2] = {tmem, tmem + 64};
+  const uint32_t tm_da = tmem + 128;
+  const uint32_t tm_a = tmem + 384;
+  pdl_wait();
+  pdl_launch();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      int g = 0;
+      for (long x = x0; x < x1;) {
+        int side, rb, tb, nt;
+        unit_at(x, side, rb, tb, nt);
+        const CUtensorMap* mB = side ? &tmB1 : &tmB0;
+        const Grad2Side& sd = p.side[side];
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int j0 = (tb + t) * BNT;
+          const int sl = g % NST;
+          mbar_wait(&st_empty[sl], ((g / NST) & 1) ^ 1);
+          mbar_expect_tx(&st_full[sl], STAT_FLOATS * 4);
+          float* st = sStat + sl * STAT_FLOATS;
+          bulk_g2s(st, sd.b_stat + j0, BNT * 4, &st_full[sl]);
+          bulk_g2s(st + BNT, sd.lc + j0, BNT * 4, &st_full[sl]);
+          bulk_g2s(st + 2 * BNT, sd.lcf + j0, BNT * 4, &st_full[sl]);
+          const int s = g % STAGES;
+          mbar_wait(&b_empty[s], ((g / STAGES) & 1) ^ 1);
+          mbar_expect_tx(&b_full[s], B_BYTES);
+          uint8_t* dst = sB + s * B_BYTES;
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * (BNT * 128), mB, &b_full[s], 64 * c, j0);
+        }
+        x += nt;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      const uint32_t id_s = idesc_bf16_f32(128, BNT, false, false);
+      const uint32_t id_da = idesc_bf16_f32(128, D, false, true);
+      auto issue_s = [&](int g) {
+        const int s = g % STAGES, b = g & 1;
+        mbar_wait(&b_full[s], (g / STAGES) & 1);
+        mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            mma_ts(tm_s[b], tm_a + (uint32_t)(8 * (4 * c + ks)), smem_desc_sw128(b_base + c * (BNT * 128) + ks * 32, 16, 1024),
+                   id_s, (c | ks) != 0);
+        mma_commit(&s_full[b]);
+      };
+      auto issue_da = [&](int g, bool first, int k) {
+        const int s = g % STAGES, b = g & 1;
+        if (first) {
+          mbar_wait(da_empty, (k & 1) ^ 1);               // unit k - 1's dA has been read out
+          tc_fence_after();
+        }
+        mbar_wait(&w_full[b], (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+        const uint32_t w_base = smem_u32(sW + b * W_BYTES);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)                    // K = the 64 columns of the tile
+          mma_bf16(tm_da, smem_desc_sw128(w_base + ks * 32, 16, 1024),
+                   smem_desc_sw128(b_base + ks * 2048, BNT * 128, 1024), id_da, !(first && ks == 0));
+        mma_commit(&w_empty[b]);
+        mma_commit(&b_empty[s]);
+      };
+      int g = 0, k = 0;
+      for (long x = x0; x < x1; ++k) {
+        int side, rb, tb, nt;
+        unit_at(x, side, rb, tb, nt);
+        mbar_wait(a_full, k & 1);                          // A of this unit in TMEM
+        tc_fence_after();
+        for (int t = 0; t < nt; ++t) {
+          issue_s(g + t);
+          if (t > 0) issue_da(g + t - 1, t == 1, k);
+        }
+        issue_da(g + nt - 1, nt == 1, k);
+        mma_commit(da_full);
+        g += nt;
+        x += nt;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2..9)
+    const int wg = (warp - 2) >> 2;                       // column half of a tile / K half of A
+    const int q = warp & 3;                               // TMEM lane quarter
+    const int r = q * 32 + lane;                          // row within the row block
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const bool fac_fast = *p.fac_ok != 0;
+    int g = 0, k = 0;
+    int prev_side = 0, prev_rb = 0, prev_slot = 0;
+    float wsum = 0.f;
+    auto readout = [&](int side, int rb, int slot, int kk) {
+      // dA of unit kk: this warp's 32 rows x 128 columns (its K half) -> part_da[slot]
+      mbar_wait(da_full, kk & 1);
+      tc_fence_after();
+      const int row = rb * 128 + r;
+      const Grad2Side& sd = p.side[side];
+      const bool rv = row < p.Na;
+      float* out = sd.part_da + ((size_t)slot * p.Na + row) * D + 128 * wg;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32_nowait(tm_da + lane_off + 128 * wg + 32 * c, v);
+        tmem_ld_wait();
+        if (rv) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(out + 32 * c)[i] =
+                make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
+                            __uint_as_float(v[4 * i + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(da_empty);
+      // row sums of w (L2: the "- (sum_j w_ij) A_i" term of the merge): column half 1 hands
+      // its sum to half 0
+      if (ENERGY == CRL_ENERGY_L2) {
+        if (wg == 1) sMerge[r] = wsum;
+        named_sync(1, 256);
+        if (wg == 0 && rv) sd.part_rs[(size_t)slot * p.Na + row] = wsum + sMerge[r];
+        named_sync(1, 256);
+      }
+      wsum = 0.f;
+    };
+    for (long x = x0; x < x1; ++k) {
+      int side, rb, tb, nt;
+      unit_at(x, side, rb, tb, nt);
+      const Grad2Side& sd = p.side[side];
+      const int row = rb * 128 + r;
+      const bool rv = row < p.Na;
+      // ---- A of this row block -> TMEM (the previous unit's S MMAs are complete: its last
+      // tile's S was consumed below).  Row r, K half wg: 128 bf16 = 64 packed 32-bit columns.
+      {
+        uint32_t av[64];
+        if (rv) {
+          const uint4* src = reinterpret_cast<const uint4*>(sd.A + (size_t)row * D + 128 * wg);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint4 u = __ldg(src + i);
+            av[4 * i] = u.x; av[4 * i + 1] = u.y; av[4 * i + 2] = u.z; av[4 * i + 3] = u.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) av[i] = 0u;
+        }
+        tmem_st32(tm_a + lane_off + 64 * wg, *reinterpret_cast<uint32_t(*)[32]>(av));
+        tmem_st32(tm_a + lane_off + 64 * wg + 32, *reinterpret_cast<uint32_t(*)[32]>(av + 32));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full);
+      }
+      if (k > 0) readout(prev_side, prev_rb, prev_slot, k - 1);
+      // per-row constants of this unit (fac_fast: q_ij = p_ij 2^lse2_i 2^-lse2'_j, one MUFU op)
+      const float astat = rv ? sd.a_stat[row] : 0.f;
+      const float lr_nat = rv ? sd.lr[row] : 0.f;
+      const float lr2 = lr_nat * kLog2e;
+      const float Ei = fac_fast ? ex2(lr2) : 0.f;
+      const float Arow = p.invN * sd.c_r + 2.f * p.invN * sd.beta_r * lr_nat;
+      const float cc0 = p.invN * sd.c_c, cc1 = 2.f * p.invN * sd.beta_c;
+      for (int t = 0; t < nt; ++t, ++g) {
+        const int b = g & 1, sl = g % NST;
+        const int j0 = (tb + t) * BNT;
+        const int nval = p.Nb - j0;                       // valid columns of this tile (>= 1)
+        mbar_wait(&s_full[b], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t raw[32];
+        tmem_ld32_nowait(tm_s[b] + lane_off + 32 * wg, raw);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[b]);
+        mbar_wait(&st_full[sl], (g / NST) & 1);
+        const float* bst = sStat + sl * STAT_FLOATS;
+        const int c0 = 32 * wg;
+        float w[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int jl = c0 + i;
+          const float v = __uint_as_float(raw[i]);
+          float l, rs = 0.f;
+          if (ENERGY == CRL_ENERGY_L2) {
+            const float d2 = fmaxf(fmaf(-2.f, v, astat + bst[jl]), 0.f) + kEpsL2;
+            rs = rsq(d2);
+            l = -d2 * rs;
+          } else if (ENERGY == CRL_ENERGY_COS) {
+            l = v * astat * bst[jl];
+          } else {
+            l = v;
+          }
+          const float tv = (jl < nval) ? l * kLog2e : -INFINITY;
+          const float pe = ex2(tv - lr2);
+          float gij;
+          if (fac_fast) {
+            gij = pe * fmaf(Ei, bst[2 * BNT + jl], Arow);
+          } else {
+            const float lc = bst[BNT + jl];
+            const float qe = ex2(tv - lc * kLog2e);
+            gij = fmaf(pe, Arow, qe * fmaf(cc1, lc, cc0));
+          }
+          float wv;
+          if (ENERGY == CRL_ENERGY_L2) wv = gij * rs;
+          else if (ENERGY == CRL_ENERGY_COS) wv = gij * bst[jl];
+          else wv = gij;
+          wv = (jl < nval) ? wv : 0.f;                    // padded columns: no NaN from pad stats
+          if (ENERGY == CRL_ENERGY_L2) wsum += wv;
+          w[i] = wv;
+        }
+        if (g >= 2) mbar_wait(&w_empty[b], ((g >> 1) - 1) & 1);
+        uint8_t* wt = sW + b * W_BYTES;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 pk;
+          pk.x = pack_bf16x2(w[8 * u + 0], w[8 * u + 1]);
+          pk.y = pack_bf16x2(w[8 * u + 2], w[8 * u + 3]);
+          pk.z = pack_bf16x2(w[8 * u + 4], w[8 * u + 5]);
+          pk.w = pack_bf16x2(w[8 * u + 6], w[8 * u + 7]);
+          *reinterpret_cast<uint4*>(wt + sw128_off(r, c0 + 8 * u)) = pk;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&w_full[b]); mbar_arrive(&st_empty[sl]); }
+      }
+      prev_side = side; prev_rb = rb; prev_slot = tb == 0 ? 0 : 1;
+      x += nt;
+    }
+    if (k > 0) readout(prev_side, prev_rb, prev_slot, k - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------------------- host side
+int tc_grad2_grid(int Na, int num_sms) {
+  const int RB = (Na + 127) / 128;
+  // at most 2 pieces per row block: every CTA's range spans >= one row block's tiles
+  return std::max(1, std::min(num_sms, 2 * RB));
+}
+
+// slot-1 flags: row block rb of side s is cut by a CTA boundary (its second piece -> slot 1)
+void tc_grad2_split_flags(int Na, int Nb, int grid, unsigned char* flags /*[2][RB]*/) {
+  const long RB = (Na + 127) / 128, TPB = (Nb + g2::BNT - 1) / g2::BNT, X = 2 * RB * TPB;
+  for (long r = 0; r < 2 * RB; ++r) {
+    const long first = r * TPB, last = first + TPB - 1;
+    bool cut = false;
+    for (long c = 1; c < grid; ++c) {
+      const long st = g2::range_start(c, X, grid);
+      if (st > first && st <= last) { cut = true; break; }
+    }
+    flags[r] = cut ? 1 : 0;
+  }
+}
+
+template <int ENERGY>
+static cudaError_t launch_g2(const CUtensorMap& b0, const CUtensorMap& b1, const Grad2Args& p, int grid,
+                             cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_grad2_kernel<ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)g2::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_pdl(tc_grad2_kernel<ENERGY>, dim3(grid), dim3(320), g2::SMEM, st, b0, b1, p);
+}
+
+cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1, const Grad2Args& p0, int grid,
+                     cudaStream_t st) {
+  Grad2Args p = p0;
+  p.RB = (p.Na + 127) / 128;
+  p.TPB = (p.Nb + g2::BNT - 1) / g2::BNT;
+  if (energy == CRL_ENERGY_L2) return launch_g2<CRL_ENERGY_L2>(mB0, mB1, p, grid, st);
+  if (energy == CRL_ENERGY_COS) return launch_g2<CRL_ENERGY_COS>(mB0, mB1, p, grid, st);
+  return launch_g2<CRL_ENERGY_DOT>(mB0, mB1, p, grid, st);
+}
+
+}  // namespace tc
+}  // namespace crl

@@ -1,0 +1,35 @@
+// tc_grad2.h — both-sides logits gradient pass at D = 256 (tc_grad2.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace crl {
+namespace tc {
+
+struct Grad2Side {
+  const float* a_stat;          // [Na] row statistic of A (L2: |a|^2, cos: 1/|a|, bf16-rounded rows)
+  const float* b_stat;          // [Nb + pad] column statistic of B
+  const float* lr;              // [Na] LSE of this side's rows (natural log)
+  const float* lc;              // [Nb + pad] LSE of the columns
+  const float* lcf;             // [Nb + pad] column factor 2^(-lc log2 e)(invN c_c + 2 invN beta_c lc)
+  float c_r, c_c, beta_r, beta_c;
+  float* part_da;               // [2][Na][256] dA partial slots (slot 1: second piece of a cut row block)
+  float* part_rs;               // [2][Na] row sums of w (L2)
+  const __nv_bfloat16* A;       // [Na][256] bf16 rows (held in TMEM per row block)
+};
+struct Grad2Args {
+  int Na, Nb;                   // rows per side (local batch), columns (global batch)
+  int RB, TPB;                  // filled by tc_grad2: row blocks, 64-column tiles per row block
+  float invN;
+  const int* fac_ok;            // 1: every row / column factor of the step is a normal float
+  Grad2Side side[2];            // 0: rows Phi, columns Psi (dPhi); 1: rows Psi, columns Phi (dPsi)
+};
+
+int tc_grad2_grid(int Na, int num_sms);
+void tc_grad2_split_flags(int Na, int Nb, int grid, unsigned char* flags);
+cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1, const Grad2Args& p, int grid,
+                     cudaStream_t st);
+
+}  // namespace tc
+}  // namespace crl

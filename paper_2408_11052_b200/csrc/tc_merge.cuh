@@ -18,6 +18,7 @@ struct GradMergeArgs {
   const __nv_bfloat16* Bg; const float* b_stat; int row_offset; float Cdiag; int Na, D, S;
   float* out; __nv_bfloat16* outb;
   int pre;   // cos: part already carries the row's own 1/|A_i| (fused pass, w' = g r_i s_j)
+  const unsigned char* valid1 = nullptr;   // tc_grad2: slot 1 holds data only for cut row blocks
 };
 
 template <int ENERGY>
@@ -34,9 +35,11 @@ __device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, in
   __nv_bfloat16* __restrict__ outb = g.outb;
   if (w >= Na) return;
   const size_t ib = (size_t)(row_offset + w) * D;
+  // slots that hold data for this row (tc_grad2: the second slot only for cut row blocks)
+  const int Sr = (g.valid1 != nullptr && S > 1 && !g.valid1[w >> 7]) ? 1 : S;
   float rs = 0.f;
   if (ENERGY == CRL_ENERGY_L2)
-    for (int s = 0; s < S; ++s) rs += prs[(size_t)s * Na + w];
+    for (int s = 0; s < Sr; ++s) rs += prs[(size_t)s * Na + w];
   float av[8], bv[8], acc[8];                            // D <= 256 -> 8 per lane
   float d2 = 0.f;
   for (int c = 0; c < D / 32; ++c) {
@@ -55,7 +58,7 @@ __device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, in
   for (int c = 0; c < D / 32; ++c) {
     const int k = lane + 32 * c;
     float v = 0.f;
-    for (int s = 0; s < S; ++s) v += part[((size_t)s * Na + w) * D + k];
+    for (int s = 0; s < Sr; ++s) v += part[((size_t)s * Na + w) * D + k];
     if (ENERGY == CRL_ENERGY_L2) v += diag * (av[c] - bv[c]) - rs * av[c];
     if (ENERGY == CRL_ENERGY_DOT) v -= Cdiag * bv[c];
     if (ENERGY == CRL_ENERGY_COS) {

@@ -138,15 +138,21 @@ constexpr int kStSqrtPairs = CRL_ST_SQRT_EMU;
 template <int D>
 struct StCfg {
   static constexpr int BNT = 128;
-  static constexpr int STAGES = D <= 64 ? 3 : 2;
-  static constexpr int KC = D / 64;
+  static constexpr int KC = D / 64;                      // 64-wide K chunks of A / B
+  // the B tile is staged in PIECES of up to 2 chunks (D = 256: two 32 KB pieces per tile), so
+  // the ring holds more tiles' worth of look-ahead than whole 64 KB tiles would
+  static constexpr int PC = KC < 2 ? KC : 2;             // chunks per piece
+  static constexpr int NP = KC / PC;                     // pieces per tile
+  static constexpr int STAGES = D <= 64 ? 3 : (D <= 128 ? 2 : 3);   // pieces in flight
+  static constexpr int ABUF = D <= 128 ? 2 : 1;          // row-block A tiles (double-buffered when small)
+  static constexpr int NE = D <= 128 ? 2 : 1;            // bf16 E tiles
   static constexpr uint32_t A_BYTES = 128 * D * 2;
-  static constexpr uint32_t B_BYTES = BNT * D * 2;
+  static constexpr uint32_t P_BYTES = BNT * 64 * 2 * PC; // one B piece
   static constexpr uint32_t E_BYTES = 128 * BNT * 2;     // one bf16 E tile
-  static constexpr uint32_t ONES_BYTES = 128 * 128 * 2;  // all-ones A operand (M=128, K=128)
+  static constexpr uint32_t ONES_BYTES = 128 * 64 * 2;   // all-ones A operand chunk (re-used for K 64..127)
   static constexpr uint32_t STAT_BYTES = BNT * 4;
   static constexpr size_t smem() {
-    return 1024 + 2 * A_BYTES + STAGES * B_BYTES + 2 * E_BYTES + ONES_BYTES + STAGES * STAT_BYTES + 3 * 512 + 256;
+    return 1024 + ABUF * A_BYTES + STAGES * P_BYTES + NE * E_BYTES + ONES_BYTES + 2 * STAT_BYTES + 3 * 512 + 256;
   }
 };
 
@@ -155,28 +161,30 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
                                                                         const __grid_constant__ CUtensorMap tmB,
                                                                         TcStatsArgs p) {
   using C = StCfg<D>;
-  constexpr int BNT = C::BNT, STAGES = C::STAGES, KC = C::KC;
+  constexpr int BNT = C::BNT, STAGES = C::STAGES, KC = C::KC, PC = C::PC, NP = C::NP, ABUF = C::ABUF, NE = C::NE;
   constexpr int NWG = kStNWG, CW = BNT / NWG, NCH = CW / 32;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                                                 // [2] row-block tiles
-  uint8_t* sB = sA + 2 * C::A_BYTES;
-  uint8_t* sE = sB + STAGES * C::B_BYTES;
-  uint8_t* sOnes = sE + 2 * C::E_BYTES;
-  float* sStat = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);     // [STAGES][BNT]
-  float* sM = sStat + STAGES * BNT;                                   // [NWG-1][128] row-sum hand-off
+  uint8_t* sA = smem;                                                 // [ABUF] row-block tiles
+  uint8_t* sB = sA + ABUF * C::A_BYTES;                               // [STAGES] B pieces
+  uint8_t* sE = sB + STAGES * C::P_BYTES;                             // [NE] E tiles
+  uint8_t* sOnes = sE + NE * C::E_BYTES;
+  float* sStat = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);     // [2][BNT] column statistics
+  float* sM = sStat + 2 * BNT;                                        // [NWG-1][128] row-sum hand-off
   uint64_t* bars = reinterpret_cast<uint64_t*>(sM + 3 * 128);
   uint64_t* a_full = bars;                // [2]
   uint64_t* a_empty = a_full + 2;         // [2]
-  uint64_t* b_full = a_empty + 2;
-  uint64_t* b_empty = b_full + STAGES;
+  uint64_t* b_full = a_empty + 2;         // [STAGES]
+  uint64_t* b_empty = b_full + STAGES;    // [STAGES]
   uint64_t* s_full = b_empty + STAGES;    // [2]
   uint64_t* s_empty = s_full + 2;         // [2]
   uint64_t* e_full = s_empty + 2;         // [2]
   uint64_t* e_empty = e_full + 2;         // [2]
   uint64_t* c_full = e_empty + 2;         // [2]
   uint64_t* c_empty = c_full + 2;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_empty + 2);
+  uint64_t* st_full = c_empty + 2;        // [2]
+  uint64_t* st_empty = st_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(st_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
@@ -193,13 +201,14 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int i = 0; i < 2; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
-    // a B stage is free once S(t) is computed (MMA commit) and the epilogue warps are done
-    // with its column statistics
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1 + 4 * NWG); }
+    // a B piece is free once the S MMAs that read it completed; the column statistics of a
+    // tile have their own 2-slot ring, freed by the epilogue warps
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4 * NWG);
       mbar_init(&e_full[i], 4 * NWG); mbar_init(&e_empty[i], 1);
       mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 1);
+      mbar_init(&st_full[i], 1); mbar_init(&st_empty[i], 4 * NWG);
     }
     fence_mbar_init();
   }
@@ -222,23 +231,29 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------------ TMA producer
-    int g = 0, k = 0;
+    int g = 0, k = 0, pc = 0;
     for (int u = blockIdx.x; u < p.n_units; u += G, ++k) {
-      const int ua = k & 1;
-      mbar_wait(&a_empty[ua], ((k >> 1) & 1) ^ 1);
+      const int ua = k % ABUF;
+      mbar_wait(&a_empty[ua], ((k / ABUF) & 1) ^ 1);
       mbar_expect_tx(&a_full[ua], C::A_BYTES);
 #pragma unroll
       for (int c = 0; c < KC; ++c) tma_load_2d(sA + ua * C::A_BYTES + c * 16384, &tmA, &a_full[ua], 64 * c, unit_rb(u) * 128);
       const int nt = unit_ntiles(u), j00 = unit_j0(u);
       for (int t = 0; t < nt; ++t, ++g) {
-        const int s = g % STAGES;
-        mbar_wait(&b_empty[s], ((g / STAGES) & 1) ^ 1);
         const int j0 = j00 + t * BNT;
-        mbar_expect_tx(&b_full[s], C::B_BYTES + C::STAT_BYTES);
-        uint8_t* dst = sB + s * C::B_BYTES;
+        const int sb = g & 1;
+        mbar_wait(&st_empty[sb], ((g >> 1) & 1) ^ 1);
+        mbar_expect_tx(&st_full[sb], C::STAT_BYTES);
+        fs::bulk_g2s(sStat + sb * BNT, p.b_stat + j0, C::STAT_BYTES, &st_full[sb]);
 #pragma unroll
-        for (int c = 0; c < KC; ++c) tma_load_2d(dst + c * BNT * 128, &tmB, &b_full[s], 64 * c, j0);
-        fs::bulk_g2s(sStat + s * BNT, p.b_stat + j0, C::STAT_BYTES, &b_full[s]);
+        for (int pp = 0; pp < NP; ++pp, ++pc) {
+          const int s = pc % STAGES;
+          mbar_wait(&b_empty[s], ((pc / STAGES) & 1) ^ 1);
+          mbar_expect_tx(&b_full[s], C::P_BYTES);
+          uint8_t* dst = sB + s * C::P_BYTES;
+#pragma unroll
+          for (int c = 0; c < PC; ++c) tma_load_2d(dst + c * BNT * 128, &tmB, &b_full[s], 64 * (pp * PC + c), j0);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -247,42 +262,46 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
     const uint32_t id_c = idesc_bf16_f32(128, BNT, false, true);     // B = E is MN-major
     const uint32_t ones = smem_u32(sOnes);
     auto issue_c = [&](int g) {
-      const int b = g & 1;
-      mbar_wait(&e_full[b], (g >> 1) & 1);
+      const int b = g & 1, eb = g % NE;
+      mbar_wait(&e_full[eb], (g / NE) & 1);
       mbar_wait(&c_empty[b], ((g >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t e_base = smem_u32(sE + b * C::E_BYTES);
+      const uint32_t e_base = smem_u32(sE + eb * C::E_BYTES);
       // K = the 128 rows of E, 16 per MMA (+2048 B in the MN-major SW128 layout); the two
-      // 64-column halves of E are 16 KB apart (LBO)
+      // 64-column halves of E are 16 KB apart (LBO); the ones chunk serves both K halves
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks)
-        mma_bf16(tm_c[b], smem_desc_sw128(ones + ks * 32, 16, 1024), smem_desc_sw128(e_base + ks * 2048, 16384, 1024),
+        mma_bf16(tm_c[b], smem_desc_sw128(ones + (ks & 3) * 32, 16, 1024), smem_desc_sw128(e_base + ks * 2048, 16384, 1024),
                  id_c, ks != 0);
       mma_commit(&c_full[b]);
-      mma_commit(&e_empty[b]);
+      mma_commit(&e_empty[eb]);
     };
-    int g = 0, k = 0;
+    int g = 0, k = 0, pc = 0;
     for (int u = blockIdx.x; u < p.n_units; u += G, ++k) {
-      const int ua = k & 1;
-      mbar_wait(&a_full[ua], (k >> 1) & 1);
+      const int ua = k % ABUF;
+      mbar_wait(&a_full[ua], (k / ABUF) & 1);
       const uint32_t a_base = smem_u32(sA + ua * C::A_BYTES);
       const int nt = unit_ntiles(u);
       if (nt == 0) mma_commit(&a_empty[ua]);                // empty chunk: hand the A buffer back
       for (int t = 0; t < nt; ++t, ++g) {
-        const int s = g % STAGES, b = g & 1;
-        mbar_wait(&b_full[s], (g / STAGES) & 1);
+        const int b = g & 1;
         mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
         if (trace && g < 15) s_tr[1][g + 1] = clock64();
-        tc_fence_after();
-        const uint32_t b_base = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
-        for (int c = 0; c < KC; ++c)
+        for (int pp = 0; pp < NP; ++pp, ++pc) {
+          const int s = pc % STAGES;
+          mbar_wait(&b_full[s], (pc / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t b_base = smem_u32(sB + s * C::P_BYTES);
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            mma_bf16(tm_s[b], smem_desc_sw128(a_base + c * 16384 + ks * 32, 16, 1024),
-                     smem_desc_sw128(b_base + c * BNT * 128 + ks * 32, 16, 1024), id_s, (c | ks) != 0);
+          for (int c = 0; c < PC; ++c)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              mma_bf16(tm_s[b], smem_desc_sw128(a_base + (pp * PC + c) * 16384 + ks * 32, 16, 1024),
+                       smem_desc_sw128(b_base + c * BNT * 128 + ks * 32, 16, 1024), id_s, (pp | c | ks) != 0);
+          mma_commit(&b_empty[s]);
+        }
         mma_commit(&s_full[b]);
-        mma_commit(&b_empty[s]);
         if (t == nt - 1) mma_commit(&a_empty[ua]);        // last S of the unit read this A tile
         if (g > 0) issue_c(g - 1);
       }
@@ -343,8 +362,9 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
       const int nt = unit_ntiles(u), j00 = unit_j0(u);
       const int jend = min(p.Nb, j00 + p.tiles_per_chunk * BNT);
       for (int t = 0; t < nt; ++t, ++g) {
-        const int s = g % STAGES, b = g & 1;
+        const int b = g & 1, eb = g % NE;
         const int nval = jend - (j00 + t * BNT);
+        mbar_wait(&st_full[b], (g >> 1) & 1);
         mbar_wait(&s_full[b], (g >> 1) & 1);
         if (trace && threadIdx.x == 128 && g < 15) s_tr[2][g + 1] = clock64();
         tc_fence_after();
@@ -356,9 +376,9 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[b]);
-        if (g >= 2) mbar_wait(&e_empty[b], ((g >> 1) - 1) & 1);
-        const uint32_t st_a = smem_u32(sStat + s * BNT + cg0);
-        const uint32_t e_a = smem_u32(sE + b * C::E_BYTES + (cg0 >> 6) * 16384) + e_row;
+        if (g >= NE) mbar_wait(&e_empty[eb], ((g / NE) - 1) & 1);
+        const uint32_t st_a = smem_u32(sStat + b * BNT + cg0);
+        const uint32_t e_a = smem_u32(sE + eb * C::E_BYTES + (cg0 >> 6) * 16384) + e_row;
         // two instantiations: full tiles carry no per-element column mask (a uniform `if`
         // inside one loop gets if-converted into a select per element)
         auto tile = [&](auto masked) {
@@ -418,7 +438,7 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
         else tile(std::true_type{});
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) { mbar_arrive(&e_full[b]); mbar_arrive(&b_empty[s]); }
+        if (lane == 0) { mbar_arrive(&e_full[eb]); mbar_arrive(&st_empty[b]); }
         if (trace && threadIdx.x == 128 && g < 15) s_tr[3][g + 1] = clock64();
       }
       // row sums of the unit: warpgroups 1.. hand their partial sums to warpgroup 0
@@ -489,7 +509,7 @@ __global__ void stats_merge_kernel(const float* __restrict__ part_rs, int S, int
 
 // ------------------------------------------------------------------------------- host side
 bool tc_stats_supports(int D, int energy) {
-  return (D == 64 || D == 128) && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_COS);
+  return (D == 64 || D == 128 || D == 256) && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_COS);
 }
 
 // Column chunks per row block: enough work units to balance the persistent grid (~8 per SM)
@@ -541,6 +561,8 @@ cudaError_t tc_stats_fused(int D, int energy, const CUtensorMap& mA, const CUten
                                            : launch_st<64, CRL_ENERGY_COS>(mA, mB, p, st);
   else if (D == 128) e = energy == CRL_ENERGY_L2 ? launch_st<128, CRL_ENERGY_L2>(mA, mB, p, st)
                                                  : launch_st<128, CRL_ENERGY_COS>(mA, mB, p, st);
+  else if (D == 256) e = energy == CRL_ENERGY_L2 ? launch_st<256, CRL_ENERGY_L2>(mA, mB, p, st)
+                                                 : launch_st<256, CRL_ENERGY_COS>(mA, mB, p, st);
   else return cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
   const int R = (Na + 127) / 128;

@@ -777,3 +777,29 @@ def test_critic_step_bf16_pair_gemm_shapes(batch, width, repr_dim):
     TMEM accumulator) serves every forward / dX product with N >= 256; ragged M and N tiles."""
     cfg = crl_synth.preset("ant", batch=batch, width=width, repr_dim=repr_dim, precision="bf16")
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("energy", ["l2", "cos"])
+@pytest.mark.parametrize("batch", [1100, 3000])
+def test_critic_step_bf16_stats_d256(energy, batch):
+    """The one-pass row + column statistics (tc_stats.cu) at D = 256 (configs[4]'s repr dim):
+    the B tile staged in two 32 KB K pieces, a single A buffer per unit, ragged N."""
+    cfg = crl_synth.preset("ant", batch=batch, width=256, repr_dim=256, energy=energy, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("energy,knob", [
+    ("l2", None), ("dot", None), ("cos", None),
+    ("l2", "CRL_FORCE_EXACT_Q"),      # exact second exp2 instead of the row / column factors
+    ("cos", "CRL_FORCE_EXACT_Q"),
+    ("l2", "CRL_NO_GRAD2"),           # the two-call gradient kernels (tc_logits.cu)
+    ("dot", "CRL_NO_GRAD2"),
+])
+@pytest.mark.parametrize("batch", [1100, 2900])
+def test_critic_step_bf16_grad2_d256(energy, knob, batch, monkeypatch):
+    """The both-sides gradient pass at D = 256 (tc_grad2.cu: persistent, contiguous tile ranges,
+    A held in TMEM, two partial slots per cut row block) against the oracle; ragged N."""
+    if knob:
+        monkeypatch.setenv(knob, "1")
+    cfg = crl_synth.preset("ant", batch=batch, width=256, repr_dim=256, energy=energy, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
