@@ -308,6 +308,16 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
       const float Ei = fac_fast ? ex2(lr2) : 0.f;
       const float Arow = p.invN * sd.c_r + 2.f * p.invN * sd.beta_r * lr_nat;
       const float cc0 = p.invN * sd.c_c, cc1 = 2.f * p.invN * sd.beta_c;
+      // packed constants of the fast path (log2 units)
+      constexpr float L2e2 = kLog2e * kLog2e;
+      const bool fast_tile = fac_fast;
+      const f32x2 kL2 = f2_pack(L2e2, L2e2), kM2 = f2_pack(-2.f * L2e2, -2.f * L2e2);
+      const float ka = ENERGY == CRL_ENERGY_L2 ? astat * L2e2 : astat * kLog2e;
+      const f32x2 kA2 = f2_pack(ka, ka);
+      const f32x2 kLr2 = f2_pack(lr2, lr2), kLrN2 = f2_pack(-lr2, -lr2), kL1 = f2_pack(kLog2e, kLog2e);
+      const float fe = ENERGY == CRL_ENERGY_L2 ? kLog2e : 1.f;   // L2: w = g rs' log2e
+      const f32x2 kEi2 = f2_pack(Ei * fe, Ei * fe), kAr2 = f2_pack(Arow * fe, Arow * fe);
+      constexpr float kEpsL2e = kEpsL2 * L2e2;
       for (int t = 0; t < nt; ++t, ++g) {
         const int b = g & 1, sl = g % NST;
         const int j0 = (tb + t) * BNT;
@@ -324,6 +334,56 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
         const float* bst = sStat + sl * STAT_FLOATS;
         const int c0 = 32 * wg;
         float w[32];
+        if (fast_tile && nval >= BNT) {
+          // full tile, normal factors: packed fp32 pairs (FFMA2 / FMUL2 / FADD2), constants
+          // folded into log2 units, column statistics by 16-byte loads; per logit 2 MUFU ops
+          //   L2 : x = d2 (log2 e)^2, rs = 1/sqrt(x), s = x rs = r log2 e,
+          //        p = 2^-(s + lse2_i), w = p (Ei lcf_j + A_i) log2e rs = g_ij / r_ij
+          //   cos: p = 2^(v a_i b_j log2 e - lse2_i), w = p (Ei lcf_j + A_i) b_j
+          //   dot: p = 2^(v log2 e - lse2_i),         w = p (Ei lcf_j + A_i)
+          f32x2 ws2 = f2_pack(0.f, 0.f);
+#pragma unroll
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 bs = *reinterpret_cast<const float4*>(bst + c0 + 4 * i4);
+            const float4 lf = *reinterpret_cast<const float4*>(bst + 2 * BNT + c0 + 4 * i4);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int i = 4 * i4 + 2 * h;
+              const f32x2 v2 = f2_pack(__uint_as_float(raw[i]), __uint_as_float(raw[i + 1]));
+              const f32x2 b2 = h ? f2_pack(bs.z, bs.w) : f2_pack(bs.x, bs.y);
+              const f32x2 l2 = h ? f2_pack(lf.z, lf.w) : f2_pack(lf.x, lf.y);
+              const f32x2 fct = f2_fma(kEi2, l2, kAr2);
+              float p0, p1, w0, w1;
+              if (ENERGY == CRL_ENERGY_L2) {
+                float x0, x1;
+                f2_unpack(f2_fma(kM2, v2, f2_fma(kL2, b2, kA2)), x0, x1);
+                x0 = fmaxf(x0, kEpsL2e); x1 = fmaxf(x1, kEpsL2e);
+                const f32x2 rs2 = f2_pack(rsq(x0), rsq(x1));
+                float a0, a1;
+                f2_unpack(f2_fma(f2_pack(x0, x1), rs2, kLr2), a0, a1);
+                p0 = ex2_neg(a0); p1 = ex2_neg(a1);
+                f2_unpack(f2_mul(f2_mul(f2_pack(p0, p1), fct), rs2), w0, w1);
+              } else if (ENERGY == CRL_ENERGY_COS) {
+                float a0, a1;
+                f2_unpack(f2_fma(f2_mul(v2, b2), kA2, kLrN2), a0, a1);
+                p0 = ex2(a0); p1 = ex2(a1);
+                f2_unpack(f2_mul(f2_mul(f2_pack(p0, p1), fct), b2), w0, w1);
+              } else {
+                float a0, a1;
+                f2_unpack(f2_fma(v2, kL1, kLrN2), a0, a1);
+                p0 = ex2(a0); p1 = ex2(a1);
+                f2_unpack(f2_mul(f2_pack(p0, p1), fct), w0, w1);
+              }
+              w[i] = w0; w[i + 1] = w1;
+              if (ENERGY == CRL_ENERGY_L2) ws2 = f2_add(ws2, f2_pack(w0, w1));
+            }
+          }
+          if (ENERGY == CRL_ENERGY_L2) {
+            float s0, s1;
+            f2_unpack(ws2, s0, s1);
+            wsum += s0 + s1;
+          }
+        } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int jl = c0 + i;
@@ -355,6 +415,7 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
           wv = (jl < nval) ? wv : 0.f;                    // padded columns: no NaN from pad stats
           if (ENERGY == CRL_ENERGY_L2) wsum += wv;
           w[i] = wv;
+        }
         }
         if (g >= 2) mbar_wait(&w_empty[b], ((g >> 1) - 1) & 1);
         uint8_t* wt = sW + b * W_BYTES;
