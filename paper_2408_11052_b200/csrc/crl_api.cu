@@ -177,7 +177,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       if (c->use_grad2) {
         c->g2_grid = tc::tc_grad2_grid(Bl, device_sms());
         c->g2_part_da = s.take<float>((size_t)4 * Bl * D);
-        c->g2_part_rs = s.take<float>((size_t)4 * Bl);
+        c->g2_part_rs = s.take<float>((size_t)8 * Bl);
         c->g2_flags = s.take<unsigned char>((size_t)2 * ((Bl + 127) / 128));
       }
     }

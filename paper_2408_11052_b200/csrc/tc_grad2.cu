@@ -11,19 +11,25 @@
 //   side 1: rows A = Psi (local), columns B = Phi (global)  -> dPsi   (coefficients swapped)
 //
 // Schedule (why it differs from tc_logits.cu's two-call GRAD kernel):
-//  * One CTA per SM owns a CONTIGUOUS range of the linearised (side, row block, 64-column
+//  * One CTA per SM owns a CONTIGUOUS range of the linearised (side, row block, 128-column
 //    tile) space (stream-K style): every CTA gets the same number of tiles +-1, a row block is
 //    cut into at most two pieces, whose dA partials go to slot 0 (the piece holding the row
 //    block's first tile) and slot 1 (the other piece, flagged for the merge).
 //  * The 128 x 256 A tile of the current row block lives in TMEM (tcgen05.mma with an A
-//    operand in tensor memory): S = A B^T reads only B from SMEM, and the 64 KB of SMEM an
-//    A tile would take hold a 5-deep ring of 32 KB B tiles instead (a B tile is needed until
-//    its dA MMA, one S + one epilogue after its S MMA).
-//  * TMEM (512 columns): S double buffer 2 x 64 | dA accumulator 256 | A 128 (bf16 pairs).
-//  * Per 64-column tile: S = A B^T (M 128, N 64, K 256; 16 MMAs) -> 8 epilogue warps (2 column
-//    halves x 4 lane quarters) form w_ij (one exp2 + one rsqrt / operand modifiers) as a bf16
-//    W tile in SMEM (SW128) -> dA += W B (M 128, N 256, K 64: the same SMEM B tile read as an
-//    MN-major operand).
+//    operand in tensor memory), so S = A B^T reads only B from SMEM.
+//  * TMEM (512 columns): S 128 | dA accumulator 256 | A 128 (bf16 pairs).
+//  * Per 128-column tile: S = A B^T (M 128, N 128, K 256: 16 MMAs) -> 8 epilogue warps (2
+//    column halves x 4 lane quarters) form w_ij (one exp2 + one rsqrt / operand modifiers) as
+//    a bf16 W tile in SMEM (SW128) -> dA += W B as two N = 128 halves (M 128, K 128: the same
+//    SMEM B tile read as an MN-major operand).
+//  * Why 128-column tiles (measured, scratch/g2_bench.cu + scratch/mma_bench.cu): the MMA
+//    issuer returns only when its MMAs are nearly done, so every barrier wait of the issuing
+//    thread is a tensor-pipe bubble; N = 64 S MMAs are also issue-bound (44 cycles vs the
+//    32-cycle floor).  N = 128 S MMAs run at the 64-cycle floor and halve the waits per
+//    column.  TMEM then holds one S buffer: the issuer puts S(t + 1) ahead of dA(t), so S(t + 1)
+//    runs while the epilogue still works on tile t.
+//  * B arrives as half tiles (D-chunks 2h, 2h + 1: 32 KB) in a 5-deep ring; dA's half h
+//    releases half-slot h of its tile, so the next tile's loads start half a dA earlier.
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -36,11 +42,15 @@ namespace crl {
 namespace tc {
 namespace g2 {
 
-constexpr int D = 256, BNT = 64, STAGES = 5, NST = 4;   // repr dim, tile columns, B ring, stats ring
-constexpr uint32_t B_BYTES = BNT * D * 2;               // 32 KB: 4 SW128 chunks of [64 rows][64 D]
-constexpr uint32_t W_BYTES = 128 * BNT * 2;             // 16 KB
-constexpr uint32_t STAT_FLOATS = 3 * BNT;               // b_stat, lc, lcf of one tile
-constexpr size_t SMEM = 1024 + STAGES * B_BYTES + 2 * W_BYTES + NST * STAT_FLOATS * 4 + 128 * 4 + 256;
+constexpr int D = 256, BNT = 128, NH = 6;              // repr dim, tile columns, B half-tile ring
+constexpr uint32_t CH_BYTES = BNT * 64 * 2;            // 16 KB: one D-chunk [128 j][64 D] (SW128)
+constexpr uint32_t H_BYTES = 2 * CH_BYTES;             // 32 KB: half a B tile (D-chunks 2h, 2h + 1)
+constexpr uint32_t W_BYTES = 128 * BNT * 2;            // 32 KB: W, two K-chunks [128 rows][64 j]
+constexpr uint32_t STAT_FLOATS = 2 * BNT;              // b_stat, lcf of one tile (per warpgroup)
+constexpr uint32_t BAR_BYTES = 256;
+// 231,680 B of the 232,448 available: no alignment slack, the dynamic window must start on a
+// 1 KB boundary (it does: the 1 KB system reservation precedes it; checked at run time)
+constexpr size_t SMEM = NH * H_BYTES + W_BYTES + 2 * STAT_FLOATS * 4 + BAR_BYTES;
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ float ex2(float x) {
@@ -84,33 +94,45 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int k) {
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// measurement: clock64 of pipeline events of CTA 0 (scratch/g2_bench.cu); no-op when null
+__device__ __forceinline__ void g2_trace(unsigned long long* tr, int g, int ev) {
+  if (tr != nullptr && blockIdx.x == 0 && g < 1024) tr[g * 8 + ev] = clock64();
+}
+
 // the tile range of CTA c of G over X tiles: [start(c), start(c + 1))
 __host__ __device__ __forceinline__ long range_start(long c, long X, long G) { return (c * X) / G; }
 
 }  // namespace g2
 
 template <int ENERGY>
-__global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant__ CUtensorMap tmB0,
+__global__ void __launch_bounds__(352, 1) tc_grad2_kernel(const __grid_constant__ CUtensorMap tmB0,
                                                           const __grid_constant__ CUtensorMap tmB1, const Grad2Args p) {
   using namespace g2;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = smem;                                                     // [STAGES] B tiles
-  uint8_t* sW = sB + STAGES * B_BYTES;                                    // [2] W tiles
-  float* sStat = reinterpret_cast<float*>(sW + 2 * W_BYTES);              // [NST][3][64]
-  float* sMerge = sStat + NST * STAT_FLOATS;                              // [128] row-sum hand-off
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + 128);
-  uint64_t* b_full = bars;                 // [STAGES]
-  uint64_t* b_empty = b_full + STAGES;     // [STAGES]
-  uint64_t* st_full = b_empty + STAGES;    // [NST]
-  uint64_t* st_empty = st_full + NST;      // [NST]
-  uint64_t* s_full = st_empty + NST;       // [2]
-  uint64_t* s_empty = s_full + 2;          // [2]
-  uint64_t* w_full = s_empty + 2;          // [2]
-  uint64_t* w_empty = w_full + 2;          // [2]
-  uint64_t* a_full = w_empty + 2;          // A of the current unit is in TMEM
-  uint64_t* da_full = a_full + 1;          // the unit's dA accumulation is complete
-  uint64_t* da_empty = da_full + 1;        // the unit's dA has been read out
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sB = smem_raw;                                                 // [NH] B half tiles
+  uint8_t* sW = sB + NH * H_BYTES;                                        // W tile
+  float* sStat = reinterpret_cast<float*>(sW + W_BYTES);                  // [2 warpgroups][2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 2 * STAT_FLOATS);
+  uint64_t* h_full = bars;                 // [NH]  half tile landed
+  uint64_t* h_empty = h_full + NH;         // [NH]  half tile consumed by its dA
+  uint64_t* st_full = h_empty + NH;        // [2]   column statistics of tile g (slot g & 1) landed
+  uint64_t* st_empty = st_full + 2;        // [2]   ... consumed
+  uint64_t* s_full = st_empty + 2;         //       S of the current tile is in TMEM
+  uint64_t* s_empty = s_full + 1;          //       S has been loaded (the single S buffer is free)
+  uint64_t* w_full = s_empty + 1;          //       W of the current tile is in SMEM
+  uint64_t* w_empty = w_full + 1;          //       dA of the current tile has read W
+  uint64_t* a_full = w_empty + 1;          //       A of the current unit is in TMEM
+  uint64_t* da_full = a_full + 1;          //       the unit's dA accumulation is complete
+  uint64_t* da_empty = da_full + 1;        //       the unit's dA has been read out
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -126,14 +148,13 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
   };
 
   if (warp == 0 && lane == 0) {
+    if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();     // SW128 operands need 1 KB alignment
     tma_prefetch_desc(&tmB0);
     tma_prefetch_desc(&tmB1);
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
-    for (int s = 0; s < NST; ++s) { mbar_init(&st_full[s], 1); mbar_init(&st_empty[s], 8); }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
-      mbar_init(&w_full[i], 8); mbar_init(&w_empty[i], 1);
-    }
+    for (int s = 0; s < NH; ++s) { mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], 1); }
+    for (int e = 0; e < 2; ++e) { mbar_init(&st_full[e], 1); mbar_init(&st_empty[e], 8); }
+    mbar_init(s_full, 1); mbar_init(s_empty, 8);
+    mbar_init(w_full, 8); mbar_init(w_empty, 1);
     mbar_init(a_full, 8); mbar_init(da_full, 1); mbar_init(da_empty, 8);
     fence_mbar_init();
   }
@@ -142,7 +163,7 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tm_s[2] = {tmem, tmem + 64};
+  const uint32_t tm_s = tmem;
   const uint32_t tm_da = tmem + 128;
   const uint32_t tm_a = tmem + 384;
   pdl_wait();
@@ -156,22 +177,41 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
         int side, rb, tb, nt;
         unit_at(x, side, rb, tb, nt);
         const CUtensorMap* mB = side ? &tmB1 : &tmB0;
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int j0 = (tb + t) * BNT;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            const int u = 2 * g + h, hs = u % NH;
+            mbar_wait(&h_empty[hs], ((u / NH) & 1) ^ 1);
+            g2_trace(p.trace, g, h);
+            if (p.dbg & 16) { mbar_arrive(&h_full[hs]); continue; }
+            mbar_expect_tx(&h_full[hs], H_BYTES);
+            uint8_t* dst = sB + hs * H_BYTES;
+            tma_load_2d(dst, mB, &h_full[hs], 64 * (2 * h), j0);            // B {D, rows} box {64, 128}
+            tma_load_2d(dst + CH_BYTES, mB, &h_full[hs], 64 * (2 * h + 1), j0);
+          }
+        }
+        x += nt;
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- column statistics
+      // (their own producer: a slot is free only once the epilogue is done with it, which
+      // must not hold back the B stream)
+      int g = 0;
+      for (long x = x0; x < x1;) {
+        int side, rb, tb, nt;
+        unit_at(x, side, rb, tb, nt);
         const Grad2Side& sd = p.side[side];
         for (int t = 0; t < nt; ++t, ++g) {
           const int j0 = (tb + t) * BNT;
-          const int sl = g % NST;
-          mbar_wait(&st_empty[sl], ((g / NST) & 1) ^ 1);
-          mbar_expect_tx(&st_full[sl], STAT_FLOATS * 4);
-          float* st = sStat + sl * STAT_FLOATS;
-          bulk_g2s(st, sd.b_stat + j0, BNT * 4, &st_full[sl]);
-          bulk_g2s(st + BNT, sd.lc + j0, BNT * 4, &st_full[sl]);
-          bulk_g2s(st + 2 * BNT, sd.lcf + j0, BNT * 4, &st_full[sl]);
-          const int s = g % STAGES;
-          mbar_wait(&b_empty[s], ((g / STAGES) & 1) ^ 1);
-          mbar_expect_tx(&b_full[s], B_BYTES);
-          uint8_t* dst = sB + s * B_BYTES;
-#pragma unroll
-          for (int c = 0; c < D / 64; ++c) tma_load_2d(dst + c * (BNT * 128), mB, &b_full[s], 64 * c, j0);
+          const int e = g & 1;
+          mbar_wait(&st_empty[e], ((g >> 1) & 1) ^ 1);
+          mbar_expect_tx(&st_full[e], STAT_FLOATS * 4);
+          float* st = sStat + e * STAT_FLOATS;
+          bulk_g2s(st, sd.b_stat + j0, BNT * 4, &st_full[e]);
+          bulk_g2s(st + BNT, sd.lcf + j0, BNT * 4, &st_full[e]);
         }
         x += nt;
       }
@@ -182,47 +222,57 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
       const uint32_t id_s = idesc_bf16_f32(128, BNT, false, false);
       const uint32_t id_da = idesc_bf16_f32(128, D, false, true);
       auto issue_s = [&](int g) {
-        const int s = g % STAGES, b = g & 1;
-        mbar_wait(&b_full[s], (g / STAGES) & 1);
-        mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+        mbar_wait(s_empty, (g & 1) ^ 1);                  // S(g - 1) has been loaded
+        mbar_wait(&h_full[(2 * g) % NH], ((2 * g) / NH) & 1);
+        mbar_wait(&h_full[(2 * g + 1) % NH], ((2 * g + 1) / NH) & 1);
         tc_fence_after();
-        const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+        if (!(p.dbg & 4)) {
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
+          for (int c = 0; c < D / 64; ++c) {
+            const uint32_t cb = smem_u32(sB + ((2 * g + (c >> 1)) % NH) * H_BYTES + (c & 1) * CH_BYTES);
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            mma_ts(tm_s[b], tm_a + (uint32_t)(8 * (4 * c + ks)), smem_desc_sw128(b_base + c * (BNT * 128) + ks * 32, 16, 1024),
-                   id_s, (c | ks) != 0);
-        mma_commit(&s_full[b]);
+            for (int ks = 0; ks < 4; ++ks)
+              mma_ts(tm_s, tm_a + (uint32_t)(8 * (4 * c + ks)), smem_desc_sw128(cb + ks * 32, 16, 1024), id_s,
+                     (c | ks) != 0);
+          }
+        }
+        mma_commit(s_full);
+        g2_trace(p.trace, g, 2);
       };
       auto issue_da = [&](int g, bool first, int k) {
-        const int s = g % STAGES, b = g & 1;
         if (first) {
           mbar_wait(da_empty, (k & 1) ^ 1);               // unit k - 1's dA has been read out
           tc_fence_after();
         }
-        mbar_wait(&w_full[b], (g >> 1) & 1);
+        mbar_wait(w_full, g & 1);
         tc_fence_after();
-        const uint32_t b_base = smem_u32(sB + s * B_BYTES);
-        const uint32_t w_base = smem_u32(sW + b * W_BYTES);
+        const int hs0 = (2 * g) % NH;                     // NH even: the halves are adjacent slots
+        if (!(p.dbg & 2)) {
+          const uint32_t w_base = smem_u32(sW), b0 = smem_u32(sB + hs0 * H_BYTES);
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)                    // K = the 64 columns of the tile
-          mma_bf16(tm_da, smem_desc_sw128(w_base + ks * 32, 16, 1024),
-                   smem_desc_sw128(b_base + ks * 2048, BNT * 128, 1024), id_da, !(first && ks == 0));
-        mma_commit(&w_empty[b]);
-        mma_commit(&b_empty[s]);
+          for (int ks = 0; ks < BNT / 16; ++ks)          // K = the 128 columns of the tile, N = D
+            mma_bf16(tm_da, smem_desc_sw128(w_base + (ks >> 2) * CH_BYTES + (ks & 3) * 32, 16, 1024),
+                     smem_desc_sw128(b0 + ks * 2048, CH_BYTES, 1024), id_da, !(first && ks == 0));
+        }
+        mma_commit(&h_empty[hs0]);
+        mma_commit(&h_empty[hs0 + 1]);
+        mma_commit(w_empty);
+        g2_trace(p.trace, g, 3);
       };
+      // S(t + 1) is issued ahead of dA(t): it needs only the epilogue's TMEM load of S(t), while
+      // dA(t) needs the whole W(t), so S(t + 1) runs under tile t's epilogue.  Six half-tile
+      // slots: B(t + 2) streams in while B(t) and B(t + 1) are still referenced.
       int g = 0, k = 0;
       for (long x = x0; x < x1; ++k) {
         int side, rb, tb, nt;
         unit_at(x, side, rb, tb, nt);
         mbar_wait(a_full, k & 1);                          // A of this unit in TMEM
         tc_fence_after();
+        issue_s(g);
         for (int t = 0; t < nt; ++t) {
-          issue_s(g + t);
-          if (t > 0) issue_da(g + t - 1, t == 1, k);
+          if (t + 1 < nt) issue_s(g + t + 1);
+          issue_da(g + t, t == 0, k);
         }
-        issue_da(g + nt - 1, nt == 1, k);
         mma_commit(da_full);
         g += nt;
         x += nt;
@@ -230,16 +280,19 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
     }
   } else {
     // ------------------------------------------------------------------ epilogue (warps 2..9)
-    const int wg = (warp - 2) >> 2;                       // column half of a tile / K half of A
+    // Thread = row r of the row block (TMEM lane); warpgroup wg takes columns 64 wg .. + 63
+    // of every tile (W K-chunk wg), the K half wg of A and the D half wg of dA.
+    const int wg = (warp - 2) >> 2;
     const int q = warp & 3;                               // TMEM lane quarter
     const int r = q * 32 + lane;                          // row within the row block
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const bool tr_lead = p.trace != nullptr && warp == 2 && lane == 0;
     const bool fac_fast = *p.fac_ok != 0;
+    const int c0 = 64 * wg;
     int g = 0, k = 0;
     int prev_side = 0, prev_rb = 0, prev_slot = 0;
-    float wsum = 0.f;
     auto readout = [&](int side, int rb, int slot, int kk) {
-      // dA of unit kk: this warp's 32 rows x 128 columns (its K half) -> part_da[slot]
+      // dA of unit kk: row r, D half wg -> part_da[slot]
       mbar_wait(da_full, kk & 1);
       tc_fence_after();
       const int row = rb * 128 + r;
@@ -262,15 +315,6 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(da_empty);
-      // row sums of w (L2: the "- (sum_j w_ij) A_i" term of the merge): column half 1 hands
-      // its sum to half 0
-      if (ENERGY == CRL_ENERGY_L2) {
-        if (wg == 1) sMerge[r] = wsum;
-        named_sync(1, 256);
-        if (wg == 0 && rv) sd.part_rs[(size_t)slot * p.Na + row] = wsum + sMerge[r];
-        named_sync(1, 256);
-      }
-      wsum = 0.f;
     };
     for (long x = x0; x < x1; ++k) {
       int side, rb, tb, nt;
@@ -310,7 +354,6 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
       const float cc0 = p.invN * sd.c_c, cc1 = 2.f * p.invN * sd.beta_c;
       // packed constants of the fast path (log2 units)
       constexpr float L2e2 = kLog2e * kLog2e;
-      const bool fast_tile = fac_fast;
       const f32x2 kL2 = f2_pack(L2e2, L2e2), kM2 = f2_pack(-2.f * L2e2, -2.f * L2e2);
       const float ka = ENERGY == CRL_ENERGY_L2 ? astat * L2e2 : astat * kLog2e;
       const f32x2 kA2 = f2_pack(ka, ka);
@@ -318,23 +361,35 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
       const float fe = ENERGY == CRL_ENERGY_L2 ? kLog2e : 1.f;   // L2: w = g rs' log2e
       const f32x2 kEi2 = f2_pack(Ei * fe, Ei * fe), kAr2 = f2_pack(Arow * fe, Arow * fe);
       constexpr float kEpsL2e = kEpsL2 * L2e2;
+      float wsum = 0.f;
       for (int t = 0; t < nt; ++t, ++g) {
-        const int b = g & 1, sl = g % NST;
+        const int sl = g & 1;
         const int j0 = (tb + t) * BNT;
         const int nval = p.Nb - j0;                       // valid columns of this tile (>= 1)
-        mbar_wait(&s_full[b], (g >> 1) & 1);
+        mbar_wait(s_full, g & 1);
         tc_fence_after();
-        uint32_t raw[32];
-        tmem_ld32_nowait(tm_s[b] + lane_off + 32 * wg, raw);
-        tmem_ld_wait();
+        if (tr_lead) g2_trace(p.trace, g, 4);
+        uint32_t raw[64];
+        if (p.dbg & 8) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) raw[i] = __float_as_uint(1.f + i + r);
+        } else {
+          tmem_ld32_nowait(tm_s + lane_off + c0, *reinterpret_cast<uint32_t(*)[32]>(raw));
+          tmem_ld32_nowait(tm_s + lane_off + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+          tmem_ld_wait();
+        }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[b]);
-        mbar_wait(&st_full[sl], (g / NST) & 1);
-        const float* bst = sStat + sl * STAT_FLOATS;
-        const int c0 = 32 * wg;
-        float w[32];
-        if (fast_tile && nval >= BNT) {
+        if (lane == 0) mbar_arrive(s_empty);
+        if (tr_lead) g2_trace(p.trace, g, 5);
+        mbar_wait(&st_full[sl], (g >> 1) & 1);
+        const float* bst = sStat + sl * STAT_FLOATS;     // [b_stat 128][lcf 128]
+        const bool fast = fac_fast && nval >= BNT && !(p.dbg & 1);
+        uint32_t pk[32];                                  // bf16 pairs of w, row r, 64 columns
+        if (p.dbg & 1) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pk[i] = raw[2 * i] ^ raw[2 * i + 1];
+        } else if (fast) {
           // full tile, normal factors: packed fp32 pairs (FFMA2 / FMUL2 / FADD2), constants
           // folded into log2 units, column statistics by 16-byte loads; per logit 2 MUFU ops
           //   L2 : x = d2 (log2 e)^2, rs = 1/sqrt(x), s = x rs = r log2 e,
@@ -343,9 +398,9 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
           //   dot: p = 2^(v log2 e - lse2_i),         w = p (Ei lcf_j + A_i)
           f32x2 ws2 = f2_pack(0.f, 0.f);
 #pragma unroll
-          for (int i4 = 0; i4 < 8; ++i4) {
-            const float4 bs = *reinterpret_cast<const float4*>(bst + c0 + 4 * i4);
-            const float4 lf = *reinterpret_cast<const float4*>(bst + 2 * BNT + c0 + 4 * i4);
+          for (int i4 = 0; i4 < 16; ++i4) {
+            const float4 bs = lds_f4(smem_u32(bst + c0 + 4 * i4));
+            const float4 lf = lds_f4(smem_u32(bst + BNT + c0 + 4 * i4));
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int i = 4 * i4 + 2 * h;
@@ -374,7 +429,7 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
                 p0 = ex2(a0); p1 = ex2(a1);
                 f2_unpack(f2_mul(f2_pack(p0, p1), fct), w0, w1);
               }
-              w[i] = w0; w[i + 1] = w1;
+              pk[i >> 1] = pack_bf16x2(w0, w1);
               if (ENERGY == CRL_ENERGY_L2) ws2 = f2_add(ws2, f2_pack(w0, w1));
             }
           }
@@ -385,54 +440,61 @@ __global__ void __launch_bounds__(320, 1) tc_grad2_kernel(const __grid_constant_
           }
         } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int jl = c0 + i;
-          const float v = __uint_as_float(raw[i]);
-          float l, rs = 0.f;
-          if (ENERGY == CRL_ENERGY_L2) {
-            const float d2 = fmaxf(fmaf(-2.f, v, astat + bst[jl]), 0.f) + kEpsL2;
-            rs = rsq(d2);
-            l = -d2 * rs;
-          } else if (ENERGY == CRL_ENERGY_COS) {
-            l = v * astat * bst[jl];
-          } else {
-            l = v;
-          }
-          const float tv = (jl < nval) ? l * kLog2e : -INFINITY;
-          const float pe = ex2(tv - lr2);
-          float gij;
-          if (fac_fast) {
-            gij = pe * fmaf(Ei, bst[2 * BNT + jl], Arow);
-          } else {
-            const float lc = bst[BNT + jl];
-            const float qe = ex2(tv - lc * kLog2e);
-            gij = fmaf(pe, Arow, qe * fmaf(cc1, lc, cc0));
-          }
-          float wv;
-          if (ENERGY == CRL_ENERGY_L2) wv = gij * rs;
-          else if (ENERGY == CRL_ENERGY_COS) wv = gij * bst[jl];
-          else wv = gij;
-          wv = (jl < nval) ? wv : 0.f;                    // padded columns: no NaN from pad stats
-          if (ENERGY == CRL_ENERGY_L2) wsum += wv;
-          w[i] = wv;
-        }
-        }
-        if (g >= 2) mbar_wait(&w_empty[b], ((g >> 1) - 1) & 1);
-        uint8_t* wt = sW + b * W_BYTES;
+          for (int i = 0; i < 64; i += 2) {
+            float wv2[2];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint4 pk;
-          pk.x = pack_bf16x2(w[8 * u + 0], w[8 * u + 1]);
-          pk.y = pack_bf16x2(w[8 * u + 2], w[8 * u + 3]);
-          pk.z = pack_bf16x2(w[8 * u + 4], w[8 * u + 5]);
-          pk.w = pack_bf16x2(w[8 * u + 6], w[8 * u + 7]);
-          *reinterpret_cast<uint4*>(wt + sw128_off(r, c0 + 8 * u)) = pk;
+            for (int e2 = 0; e2 < 2; ++e2) {
+              const int jl = c0 + i + e2;
+              const float v = __uint_as_float(raw[i + e2]);
+              const bool cv = jl < nval;
+              const float bj = bst[jl];
+              float l, rs = 0.f;
+              if (ENERGY == CRL_ENERGY_L2) {
+                const float d2 = fmaxf(fmaf(-2.f, v, astat + bj), 0.f) + kEpsL2;
+                rs = rsq(d2);
+                l = -d2 * rs;
+              } else if (ENERGY == CRL_ENERGY_COS) {
+                l = v * astat * bj;
+              } else {
+                l = v;
+              }
+              const float tv = cv ? l * kLog2e : -INFINITY;
+              const float pe = ex2(tv - lr2);
+              float gij;
+              if (fac_fast) {
+                gij = pe * fmaf(Ei, bst[BNT + jl], Arow);
+              } else {
+                const float lc = cv ? __ldg(sd.lc + j0 + jl) : 0.f;
+                const float qe = ex2(tv - lc * kLog2e);
+                gij = fmaf(pe, Arow, qe * fmaf(cc1, lc, cc0));
+              }
+              float wv;
+              if (ENERGY == CRL_ENERGY_L2) wv = gij * rs;
+              else if (ENERGY == CRL_ENERGY_COS) wv = gij * bj;
+              else wv = gij;
+              wv = cv ? wv : 0.f;                         // padded columns: no NaN from pad stats
+              if (ENERGY == CRL_ENERGY_L2) wsum += wv;
+              wv2[e2] = wv;
+            }
+            pk[i >> 1] = pack_bf16x2(wv2[0], wv2[1]);
+          }
         }
+        if (tr_lead) g2_trace(p.trace, g, 6);
+        if (g >= 1) mbar_wait(w_empty, (g - 1) & 1);      // dA(g - 1) has read W
+        const uint32_t wt = smem_u32(sW + wg * CH_BYTES);  // K-chunk wg = this warp's 64 columns
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          sts_u4(wt + sw128_off(r, 8 * u), make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) { mbar_arrive(&w_full[b]); mbar_arrive(&st_empty[sl]); }
+        if (lane == 0) { mbar_arrive(w_full); mbar_arrive(&st_empty[sl]); }
+        if (tr_lead) g2_trace(p.trace, g, 7);
       }
-      prev_side = side; prev_rb = rb; prev_slot = tb == 0 ? 0 : 1;
+      // this warpgroup's share of the L2 row sums of the unit ("- (sum_j w_ij) A_i" term of
+      // the merge): sub-slot wg of the unit's partial slot
+      const int slot = tb == 0 ? 0 : 1;
+      if (ENERGY == CRL_ENERGY_L2 && rv) sd.part_rs[((size_t)(2 * slot + wg)) * p.Na + row] = wsum;
+      prev_side = side; prev_rb = rb; prev_slot = slot;
       x += nt;
     }
     if (k > 0) readout(prev_side, prev_rb, prev_slot, k - 1);
@@ -476,7 +538,7 @@ static cudaError_t launch_g2(const CUtensorMap& b0, const CUtensorMap& b1, const
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(tc_grad2_kernel<ENERGY>, dim3(grid), dim3(320), g2::SMEM, st, b0, b1, p);
+  return launch_pdl(tc_grad2_kernel<ENERGY>, dim3(grid), dim3(352), g2::SMEM, st, b0, b1, p);
 }
 
 cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1, const Grad2Args& p0, int grid,

@@ -15,7 +15,7 @@ struct Grad2Side {
   const float* lcf;             // [Nb + pad] column factor 2^(-lc log2 e)(invN c_c + 2 invN beta_c lc)
   float c_r, c_c, beta_r, beta_c;
   float* part_da;               // [2][Na][256] dA partial slots (slot 1: second piece of a cut row block)
-  float* part_rs;               // [2][Na] row sums of w (L2)
+  float* part_rs;               // [2 slots][2 warpgroups][Na] row sums of w (L2)
   const __nv_bfloat16* A;       // [Na][256] bf16 rows (held in TMEM per row block)
 };
 struct Grad2Args {
@@ -24,6 +24,8 @@ struct Grad2Args {
   float invN;
   const int* fac_ok;            // 1: every row / column factor of the step is a normal float
   Grad2Side side[2];            // 0: rows Phi, columns Psi (dPhi); 1: rows Psi, columns Phi (dPsi)
+  int dbg;                      // measurement ablations (scratch/g2_bench.cu); 0 in the library
+  unsigned long long* trace;    // measurement: CTA 0 event clocks [1024][8]; null in the library
 };
 
 int tc_grad2_grid(int Na, int num_sms);

@@ -19,6 +19,7 @@ struct GradMergeArgs {
   float* out; __nv_bfloat16* outb;
   int pre;   // cos: part already carries the row's own 1/|A_i| (fused pass, w' = g r_i s_j)
   const unsigned char* valid1 = nullptr;   // tc_grad2: slot 1 holds data only for cut row blocks
+  int prs_sub = 1;                         // row-sum sub-partials per slot (tc_grad2: 2 warpgroups)
 };
 
 template <int ENERGY>
@@ -39,7 +40,7 @@ __device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, in
   const int Sr = (g.valid1 != nullptr && S > 1 && !g.valid1[w >> 7]) ? 1 : S;
   float rs = 0.f;
   if (ENERGY == CRL_ENERGY_L2)
-    for (int s = 0; s < Sr; ++s) rs += prs[(size_t)s * Na + w];
+    for (int s = 0; s < Sr * g.prs_sub; ++s) rs += prs[(size_t)s * Na + w];
   float av[8], bv[8], acc[8];                            // D <= 256 -> 8 per lane
   float d2 = 0.f;
   for (int c = 0; c < D / 32; ++c) {
