@@ -16,6 +16,7 @@
 
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -83,6 +84,10 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   const int Bl = k.batch_local, W = k.world_size, N = Bl * W, D = k.repr_dim, Wd = k.width;
   Carver s{scr_base};
   c->dw_splits = dw_splits_for(Bl);
+  // wide encoders (configs[4]: 4 x 1024) already have ~200 weight-gradient tiles per K slice:
+  // more slices only add partial-buffer traffic (Adam sums them).  Measured on B200 at
+  // netscale: 8 slices 584 steps/s (dW 278 us + Adam 74 us), 2 slices 601 (257 + 48).
+  if (k.width >= 512 && !std::getenv("CRL_DW_SPLITS")) c->dw_splits = std::min(c->dw_splits, 2);
   c->grads = s.take<float>(c->sizes.n_params * c->dw_splits);
   const bool bf = k.precision == CRL_BF16;
   c->bf16 = bf;

@@ -1,7 +1,8 @@
 // tc_merge.cuh — the per-row merge of split gradient partials (shared by the two-call logits
 // kernels, tc_logits.cu, and the fused gradient pass, tc_gradf.cu).
 //
-// dA[i] = sum_s part[s][i]  (+ energy finalisation), fp32 and bf16 outputs.  One warp per row.
+// dA[i] = sum_s part[s][i]  (+ energy finalisation), fp32 and bf16 outputs.  One warp per row;
+// D in {64, 128, 256} (every caller's representation size).
 // Also adds the positive-pair (delta_ii) term of dL/dl, -C delta_ij with C = invN (c_r + c_c),
 // which the tile epilogues leave out: its energy chain uses the pair (A_i, B_{row_offset+i})
 // (L2: 1/r_ii from the difference form; cos: 1/|B_i|).  Readings A-02..A-06.
@@ -22,63 +23,121 @@ struct GradMergeArgs {
   int prs_sub = 1;                         // row-sum sub-partials per slot (tc_grad2: 2 warpgroups)
 };
 
-template <int ENERGY>
-__device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, int lane) {
-  const float* __restrict__ part = g.part;
-  const float* __restrict__ prs = g.prs;
-  const __nv_bfloat16* __restrict__ A = g.A;
-  const float* __restrict__ a_stat = g.a_stat;
-  const __nv_bfloat16* __restrict__ Bg = g.Bg;
-  const float* __restrict__ b_stat = g.b_stat;
-  const int row_offset = g.row_offset, Na = g.Na, D = g.D, S = g.S;
-  const float Cdiag = g.Cdiag;
-  float* __restrict__ out = g.out;
-  __nv_bfloat16* __restrict__ outb = g.outb;
+// V consecutive floats / bf16 of a row from lane-contiguous addresses (16 B vector accesses)
+template <int V>
+__device__ __forceinline__ void ld_f32v(const float* __restrict__ p, float (&v)[V]) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i) {
+      const float4 q = reinterpret_cast<const float4*>(p)[i];
+      v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+    }
+  } else {
+    const float2 q = *reinterpret_cast<const float2*>(p);
+    v[0] = q.x; v[1] = q.y;
+  }
+}
+template <int V>
+__device__ __forceinline__ void ld_bf16v(const __nv_bfloat16* __restrict__ p, float (&v)[V]) {
+  uint32_t w[V / 2];
+  if constexpr (V == 8) {
+    const uint4 q = *reinterpret_cast<const uint4*>(p);
+    w[0] = q.x; w[1] = q.y; w[2] = q.z; w[3] = q.w;
+  } else if constexpr (V == 4) {
+    const uint2 q = *reinterpret_cast<const uint2*>(p);
+    w[0] = q.x; w[1] = q.y;
+  } else {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
+  }
+#pragma unroll
+  for (int i = 0; i < V / 2; ++i) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+    v[2 * i] = f.x; v[2 * i + 1] = f.y;
+  }
+}
+
+// One warp per row, lane l owns elements [V l, V l + V) (V = D / 32): every global access is a
+// 16 B (8 B, 4 B) vector and all loads of the row are in flight before the first reduction.
+template <int ENERGY, int V>
+__device__ __forceinline__ void grad_merge_row_v(const GradMergeArgs& g, int w, int lane) {
+  constexpr int D = 32 * V;
+  const int row_offset = g.row_offset, Na = g.Na, S = g.S;
   if (w >= Na) return;
-  const size_t ib = (size_t)(row_offset + w) * D;
+  const size_t ib = (size_t)(row_offset + w) * D + V * lane;
   // slots that hold data for this row (tc_grad2: the second slot only for cut row blocks)
   const int Sr = (g.valid1 != nullptr && S > 1 && !g.valid1[w >> 7]) ? 1 : S;
+  float av[V], bv[V], acc[V];
+  ld_bf16v<V>(g.A + (size_t)w * D + V * lane, av);
+  ld_bf16v<V>(g.Bg + ib, bv);
+  ld_f32v<V>(g.part + (size_t)w * D + V * lane, acc);
+  for (int s = 1; s < Sr; ++s) {
+    float t[V];
+    ld_f32v<V>(g.part + ((size_t)s * Na + w) * D + V * lane, t);
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] += t[i];
+  }
   float rs = 0.f;
   if (ENERGY == CRL_ENERGY_L2)
-    for (int s = 0; s < Sr * g.prs_sub; ++s) rs += prs[(size_t)s * Na + w];
-  float av[8], bv[8], acc[8];                            // D <= 256 -> 8 per lane
+    for (int s = 0; s < Sr * g.prs_sub; ++s) rs += g.prs[(size_t)s * Na + w];
+  const float Cdiag = g.Cdiag;
   float d2 = 0.f;
-  for (int c = 0; c < D / 32; ++c) {
-    const int k = lane + 32 * c;
-    av[c] = __bfloat162float(A[(size_t)w * D + k]);
-    bv[c] = __bfloat162float(Bg[ib + k]);
-    const float d = av[c] - bv[c];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const float d = av[i] - bv[i];
     d2 = fmaf(d, d, d2);
   }
   float diag = 0.f;                                      // energy-chain weight of the delta term
   if (ENERGY == CRL_ENERGY_L2) diag = Cdiag / sqrtf(warp_sum(d2) + kEpsL2);   // times (A_i - B_i)
-  const float invb = ENERGY == CRL_ENERGY_COS ? b_stat[row_offset + w] : 0.f;
-  const float inv = ENERGY == CRL_ENERGY_COS ? a_stat[w] : 0.f;
+  const float invb = ENERGY == CRL_ENERGY_COS ? g.b_stat[row_offset + w] : 0.f;
+  const float inv = ENERGY == CRL_ENERGY_COS ? g.a_stat[w] : 0.f;
   const float osc = g.pre ? 1.f : inv;                   // the final 1/|A_i| factor
   float pr = 0.f;
-  for (int c = 0; c < D / 32; ++c) {
-    const int k = lane + 32 * c;
-    float v = 0.f;
-    for (int s = 0; s < Sr; ++s) v += part[((size_t)s * Na + w) * D + k];
-    if (ENERGY == CRL_ENERGY_L2) v += diag * (av[c] - bv[c]) - rs * av[c];
-    if (ENERGY == CRL_ENERGY_DOT) v -= Cdiag * bv[c];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    float v = acc[i];
+    if (ENERGY == CRL_ENERGY_L2) v += diag * (av[i] - bv[i]) - rs * av[i];
+    if (ENERGY == CRL_ENERGY_DOT) v -= Cdiag * bv[i];
     if (ENERGY == CRL_ENERGY_COS) {
-      v -= Cdiag * invb * (g.pre ? inv : 1.f) * bv[c];
-      pr = fmaf(v, av[c] * inv, pr);
+      v -= Cdiag * invb * (g.pre ? inv : 1.f) * bv[i];
+      pr = fmaf(v, av[i] * inv, pr);
     }
-    acc[c] = v;
+    acc[i] = v;
   }
   if (ENERGY == CRL_ENERGY_COS) pr = warp_sum(pr);
-  for (int c = 0; c < D / 32; ++c) {
-    const int k = lane + 32 * c;
-    float v = acc[c];
+  uint32_t hb[V / 2];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    float v = acc[i];
     if (ENERGY == CRL_ENERGY_COS) {
-      const float u = av[c] * inv;
+      const float u = av[i] * inv;
       v = inv < 1.f / kEpsCos ? (v - pr * u) * osc : v * osc;
     }
-    out[(size_t)w * D + k] = v;
-    outb[(size_t)w * D + k] = __float2bfloat16_rn(v);
+    acc[i] = v;
   }
+#pragma unroll
+  for (int i = 0; i < V / 2; ++i) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    hb[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  float* out = g.out + (size_t)w * D + V * lane;
+  __nv_bfloat16* outb = g.outb + (size_t)w * D + V * lane;
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < V / 4; ++i)
+      reinterpret_cast<float4*>(out)[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+  } else {
+    *reinterpret_cast<float2*>(out) = make_float2(acc[0], acc[1]);
+  }
+  if constexpr (V == 8) *reinterpret_cast<uint4*>(outb) = make_uint4(hb[0], hb[1], hb[2], hb[3]);
+  else if constexpr (V == 4) *reinterpret_cast<uint2*>(outb) = make_uint2(hb[0], hb[1]);
+  else *reinterpret_cast<uint32_t*>(outb) = hb[0];
+}
+
+template <int ENERGY>
+__device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, int lane) {
+  if (g.D == 256) grad_merge_row_v<ENERGY, 8>(g, w, lane);
+  else if (g.D == 128) grad_merge_row_v<ENERGY, 4>(g, w, lane);
+  else grad_merge_row_v<ENERGY, 2>(g, w, lane);
 }
 
 }  // namespace tc

@@ -473,29 +473,9 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
 //   threads [Na, Na + Nb): LSE'_j = ln sum_r colpart[r][j]   -> lse_col, fac_col
 // fac = 2^-LSE2 (cc0 + cc1 LSE) as in lse_merge (tc_logits.cu).  A sum that is not a normal,
 // finite float well above the underflow range sets *bad (exact online-max path runs).
-__global__ void stats_merge_kernel(const float* __restrict__ part_rs, int S, int Na, const float* __restrict__ colpart,
-                                   int R, int ldc, int Nb, float* __restrict__ lse_row, float* __restrict__ fac_row,
-                                   float* __restrict__ lse_col, float* __restrict__ fac_col, int* __restrict__ fac_ok,
-                                   int* __restrict__ bad, float rc0, float rc1, float cc0, float cc1,
-                                   int force_bad, cudaGraphConditionalHandle cond) {
-  pdl_wait();
-  pdl_launch();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (force_bad && i == 0) {                           // CRL_FORCE_STATS_FALLBACK (tests)
-    atomicExch(bad, 1);
-    if (cond != 0) cudaGraphSetConditional(cond, 1);
-  }
-  float t = 0.f, c0, c1;
-  float *lse, *fac;
-  if (i < Na) {
-    for (int s = 0; s < S; ++s) t += part_rs[(size_t)s * Na + i];
-    lse = lse_row; fac = fac_row; c0 = rc0; c1 = rc1;
-  } else {
-    i -= Na;
-    if (i >= Nb) return;
-    for (int s = 0; s < R; ++s) t += colpart[(size_t)s * ldc + i];
-    lse = lse_col; fac = fac_col; c0 = cc0; c1 = cc1;
-  }
+__device__ __forceinline__ void stats_finalize(float t, int i, float* __restrict__ lse, float* __restrict__ fac,
+                                               int* __restrict__ fac_ok, int* __restrict__ bad, float c0, float c1,
+                                               cudaGraphConditionalHandle cond) {
   if (!(t >= 0x1p-100f) || !isfinite(t)) {
     atomicExch(bad, 1);
     if (cond != 0) cudaGraphSetConditional(cond, 1);   // graph: run the exact statistics node
@@ -505,6 +485,47 @@ __global__ void stats_merge_kernel(const float* __restrict__ part_rs, int S, int
   const bool ok = l2 > -120.f && l2 < 120.f;
   fac[i] = ok ? exp2f(-l2) * fmaf(c1, l2 * fs::kLn2, c0) : 0.f;
   if (!ok) *fac_ok = 0;
+}
+
+// Blocks [0, nrb): 256 rows each, the S column-chunk partials of a row summed by one thread.
+// Blocks [nrb, ..): 32 columns each; the R row-block partials of a column are split over 8
+// thread groups (fixed order: group q sums blocks q, q + 8, ...; the 8 group sums are then
+// added in group order), so each thread has R / 8 loads in flight instead of R in sequence.
+__global__ void __launch_bounds__(256) stats_merge_kernel(
+    const float* __restrict__ part_rs, int S, int Na, const float* __restrict__ colpart, int R, int ldc, int Nb,
+    float* __restrict__ lse_row, float* __restrict__ fac_row, float* __restrict__ lse_col, float* __restrict__ fac_col,
+    int* __restrict__ fac_ok, int* __restrict__ bad, float rc0, float rc1, float cc0, float cc1, int force_bad,
+    cudaGraphConditionalHandle cond, int nrb) {
+  __shared__ float red[8][33];
+  pdl_wait();
+  pdl_launch();
+  if (force_bad && blockIdx.x == 0 && threadIdx.x == 0) {   // CRL_FORCE_STATS_FALLBACK (tests)
+    atomicExch(bad, 1);
+    if (cond != 0) cudaGraphSetConditional(cond, 1);
+  }
+  if ((int)blockIdx.x < nrb) {
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= Na) return;
+    float t = 0.f;
+    for (int s = 0; s < S; ++s) t += part_rs[(size_t)s * Na + i];
+    stats_finalize(t, i, lse_row, fac_row, fac_ok, bad, rc0, rc1, cond);
+    return;
+  }
+  const int c = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int j = ((int)blockIdx.x - nrb) * 32 + c;
+  float t = 0.f;
+  if (j < Nb) {
+#pragma unroll 4
+    for (int s = q; s < R; s += 8) t += colpart[(size_t)s * ldc + j];
+  }
+  red[q][c] = t;
+  __syncthreads();
+  if (q == 0 && j < Nb) {
+    float u = red[0][c];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) u += red[k][c];
+    stats_finalize(u, j, lse_col, fac_col, fac_ok, bad, cc0, cc1, cond);
+  }
 }
 
 // ------------------------------------------------------------------------------- host side
@@ -566,9 +587,10 @@ cudaError_t tc_stats_fused(int D, int energy, const CUtensorMap& mA, const CUten
   else return cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
   const int R = (Na + 127) / 128;
-  return launch_pdl(stats_merge_kernel, dim3((Na + Nb + 255) / 256), dim3(256), 0, st, (const float*)part_rs, S, Na,
+  const int nrb = (Na + 255) / 256, ncb = (Nb + 31) / 32;
+  return launch_pdl(stats_merge_kernel, dim3(nrb + ncb), dim3(256), 0, st, (const float*)part_rs, S, Na,
                     (const float*)colpart, R, ldc, Nb, lse_row, fac_row, lse_col, fac_col, fac_ok, bad, rc0, rc1,
-                    cc0, cc1, std::getenv("CRL_FORCE_STATS_FALLBACK") ? 1 : 0, cond);
+                    cc0, cc1, std::getenv("CRL_FORCE_STATS_FALLBACK") ? 1 : 0, cond, nrb);
 }
 
 }  // namespace tc
