@@ -23,6 +23,7 @@ struct PgemmArgs {
   int act;             // crl_activation
   float* stat;         // output layer (N <= 256): row statistic of bf16(Y) (L2: |y|^2, cos: 1/|y|)
   int stat_energy;
+  int dbg;             // measurement ablations (scratch/pgemm_test.cu); 0 in the library
 };
 
 bool tc_pgemm_supported(int M, int N, int K);

@@ -376,7 +376,6 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[b]);
-        if (g >= NE) mbar_wait(&e_empty[eb], ((g / NE) - 1) & 1);
         const uint32_t st_a = smem_u32(sStat + b * BNT + cg0);
         const uint32_t e_a = smem_u32(sE + eb * C::E_BYTES + (cg0 >> 6) * 16384) + e_row;
         // two instantiations: full tiles carry no per-element column mask (a uniform `if`
@@ -424,6 +423,9 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
             }
 #pragma unroll
             for (int k2 = 0; k2 < 16; ++k2) racc[k2 & 1] = f2_add(racc[k2 & 1], f2_pack(e[2 * k2], e[2 * k2 + 1]));
+            // E(g) overwrites E(g - NE): wait for that tile's column-sum MMA only now, after
+            // this chunk's exponentials (waiting first serialised the math behind the MMA)
+            if (c == 0 && g >= NE) mbar_wait(&e_empty[eb], ((g / NE) - 1) & 1);
 #pragma unroll
             for (int v4 = 0; v4 < 4; ++v4) {
               const int kk = (cg0 & 63) + 32 * c + 8 * v4;   // column within the 64-wide chunk

@@ -101,6 +101,20 @@ int main(int argc, char** argv) {
   cudaEventElapsedTime(&ms, e0, e1);
   double us = ms * 1e3 / IT;
   printf("fwd hidden: %.2f us  %.1f TFLOP/s\n", us, 2.0 * M * N * K / (us * 1e-6) / 1e12);
+  // ablations (PgemmArgs::dbg): 1 no epilogue, 2 no MMA, 4 no TMA operand traffic
+  for (int dbg : {1, 2, 4, 3, 5, 6, 7}) {
+    PgemmArgs px = pa;
+    px.dbg = dbg;
+    for (int i = 0; i < 3; ++i) tc_pgemm(PG_FWD_HIDDEN, mp, px, sms, 0);
+    cudaEventRecord(e0);
+    for (int i = 0; i < IT; ++i) tc_pgemm(PG_FWD_HIDDEN, mp, px, sms, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double u2 = ms * 1e3 / IT;
+    printf("  dbg=%d (%s%s%s): %.2f us  %.1f TFLOP/s-equiv\n", dbg, dbg & 1 ? "no-epi " : "", dbg & 2 ? "no-mma " : "",
+           dbg & 4 ? "no-tma" : "", u2, 2.0 * M * N * K / (u2 * 1e-6) / 1e12);
+  }
   // ---- dX: A = dZ [M][K2], W [N][K2] (in = N, out = K2)
   {
     const int K2 = N, N2 = K;          // dX of this layer: out = N, in = K
