@@ -180,9 +180,11 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       // D = 256 (configs[4]): both gradient sides in one persistent launch (tc_grad2.cu)
       c->use_grad2 = D == 256 && !c->use_gradf && !std::getenv("CRL_NO_GRAD2");
       if (c->use_grad2) {
-        c->g2_grid = tc::tc_grad2_grid(Bl, device_sms());
+        // CTA pairs (tc_grad2p) once a pair has two full row blocks to share the B tile over
+        c->g2_pair = Bl >= 256 && !std::getenv("CRL_NO_GRAD2P");
+        c->g2_grid = c->g2_pair ? tc::tc_grad2p_grid(Bl, device_sms()) : tc::tc_grad2_grid(Bl, device_sms());
         c->g2_part_da = s.take<float>((size_t)4 * Bl * D);
-        c->g2_part_rs = s.take<float>((size_t)8 * Bl);
+        c->g2_part_rs = s.take<float>((size_t)16 * Bl);   // 2 sides x 2 slots x <= 4 warpgroup sub-slots
         c->g2_flags = s.take<unsigned char>((size_t)2 * ((Bl + 127) / 128));
       }
     }

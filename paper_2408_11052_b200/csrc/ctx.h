@@ -222,6 +222,8 @@ struct crl_ctx {
   float *g2_part_da = nullptr, *g2_part_rs = nullptr;   // [2 sides][2 slots][B_l][D], [2][2][B_l]
   unsigned char* g2_flags = nullptr;                    // [2 sides][row blocks] slot-1 flags
   CUtensorMap g2_B0, g2_B1;                             // B operands (box {64, 128}): Psi_g, Phi_g
+  bool g2_pair = false;                                 // CTA-pair variant (tc_grad2p)
+  CUtensorMap g2_S0, g2_S1;                             // pair: S parts (box {64, 64}): Psi_g, Phi_g
   // all weight / bias gradients of both encoders in one grouped launch (tc_dwg.cu)
   bool use_dwg = false;
   tc::DwgParams dwg;

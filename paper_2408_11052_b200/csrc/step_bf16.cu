@@ -147,7 +147,14 @@ crl_status bf16_prepare(crl_ctx* ctx) {
         return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the gradient operands");
       const int RB = (k.batch_local + 127) / 128;
       std::vector<unsigned char> fl(2 * RB);
-      tc::tc_grad2_split_flags(k.batch_local, ctx->N, ctx->g2_grid, fl.data());
+      if (ctx->g2_pair) {
+        if (!tc::make_map_bf16(&ctx->g2_S0, ctx->psi_outb_g, k.repr_dim, ctx->N, k.repr_dim, 64, 64) ||
+            !tc::make_map_bf16(&ctx->g2_S1, ctx->phi_outb_g, k.repr_dim, ctx->N, k.repr_dim, 64, 64))
+          return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the gradient operands");
+        tc::tc_grad2p_split_flags(k.batch_local, ctx->N, ctx->g2_grid, fl.data());
+      } else {
+        tc::tc_grad2_split_flags(k.batch_local, ctx->N, ctx->g2_grid, fl.data());
+      }
       CU(cudaMemcpy(ctx->g2_flags, fl.data(), fl.size(), cudaMemcpyHostToDevice));
     }
     if (ctx->use_stats && (!tc::make_map_bf16(&ctx->st_A, ctx->phi_outb, k.repr_dim, k.batch_local, k.repr_dim, 64, 128) ||
@@ -597,9 +604,12 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     tc::Grad2Side& s1 = ga.side[1];
     s1.a_stat = ctx->stat_psi + row_off; s1.b_stat = ctx->stat_phi; s1.lr = ctx->lse_col; s1.lc = ctx->lse_row_g;
     s1.lcf = ctx->fac_row_g; s1.c_r = c_b; s1.c_c = c_f; s1.beta_r = 0.f; s1.beta_c = k.beta_lse;
-    s1.part_da = ctx->g2_part_da + (size_t)2 * Bl * D; s1.part_rs = ctx->g2_part_rs + (size_t)4 * Bl;
+    // row-sum sub-slots per partial slot: one per epilogue warpgroup of the launched variant
+    const int prs_sub = ctx->g2_pair ? tc::tc_grad2p_warpgroups() : 2;
+    s1.part_da = ctx->g2_part_da + (size_t)2 * Bl * D; s1.part_rs = ctx->g2_part_rs + (size_t)2 * prs_sub * Bl;
     s1.A = ctx->psi_outb;
-    CU(tc::tc_grad2(k.energy, ctx->g2_B0, ctx->g2_B1, ga, ctx->g2_grid, st));
+    if (ctx->g2_pair) CU(tc::tc_grad2p(k.energy, ctx->g2_B0, ctx->g2_B1, ctx->g2_S0, ctx->g2_S1, ga, ctx->g2_grid, st));
+    else CU(tc::tc_grad2(k.energy, ctx->g2_B0, ctx->g2_B1, ga, ctx->g2_grid, st));
     const float Cdiag = invN * (c_f + c_b);
     tc::GradMergeArgs m0{s0.part_da, s0.part_rs, ctx->phi_outb, s0.a_stat, ctx->psi_outb_g, ctx->stat_psi, row_off,
                          Cdiag, Bl, D, 2, ctx->dphi, ctx->dphib, 0};
@@ -607,7 +617,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                          Cdiag, Bl, D, 2, ctx->dpsi, ctx->dpsib, 0};
     m0.valid1 = ctx->g2_flags;
     m1.valid1 = ctx->g2_flags + (Bl + 127) / 128;
-    m0.prs_sub = m1.prs_sub = 2;
+    m0.prs_sub = m1.prs_sub = prs_sub;
     CU(tc::launch_grad_merge2(k.energy, m0, m1, st));
     nl += 2;
   }

@@ -172,5 +172,30 @@ __device__ __forceinline__ float sqrt_abs(float x) {
   return y;
 }
 
+// 2^x for a PAIR of x <= 0 on the FMA / ALU pipes (no MUFU): x = n + f with n = rint(x) from
+// the 1.5 * 2^23 shifter, 2^f by the degree-5 Taylor polynomial on [-1/2, 1/2] (relative error
+// < 4e-6) in packed FFMA2, 2^n added to the exponent bits.  x is clamped at -126 through an
+// unsigned min on the bit patterns (x <= 0), so the result is >= 2^-126 > 0 (not an exact
+// zero like ex2.approx.ftz: irrelevant next to the sums it feeds).  A share of the logits
+// takes this path so the XU pipe is not the only unit doing exponentials.
+__device__ __forceinline__ void ex2_pair_fma(float x0, float x1, float& y0, float& y1) {
+  const unsigned lim = 0xC2FC0000u;                 // bits of -126.0f
+  x0 = __uint_as_float(min(__float_as_uint(x0), lim));
+  x1 = __uint_as_float(min(__float_as_uint(x1), lim));
+  const f32x2 x = f2_pack(x0, x1);
+  const f32x2 sh = f2_pack(12582912.f, 12582912.f);
+  const f32x2 j = f2_add(x, sh);
+  const f32x2 f = f2_add(x, f2_fma(j, f2_pack(-1.f, -1.f), sh));   // x - (j - sh) = x - rint(x)
+  f32x2 pp = f2_fma(f2_pack(1.3333558146e-3f, 1.3333558146e-3f), f, f2_pack(9.6181291076e-3f, 9.6181291076e-3f));
+  pp = f2_fma(pp, f, f2_pack(5.5504108665e-2f, 5.5504108665e-2f));
+  pp = f2_fma(pp, f, f2_pack(2.4022650695e-1f, 2.4022650695e-1f));
+  pp = f2_fma(pp, f, f2_pack(6.9314718056e-1f, 6.9314718056e-1f));
+  pp = f2_fma(pp, f, f2_pack(1.f, 1.f));
+  float j0, j1, p0, p1;
+  f2_unpack(j, j0, j1);
+  f2_unpack(pp, p0, p1);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(j0) << 23));   // low bits of j hold n
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(j1) << 23));
+}
 }  // namespace tc
 }  // namespace crl

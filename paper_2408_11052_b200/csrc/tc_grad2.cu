@@ -37,6 +37,7 @@
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_grad2.h"
+#include "tc_pair.cuh"
 
 namespace crl {
 namespace tc {
@@ -106,6 +107,146 @@ __device__ __forceinline__ void sts_u4(uint32_t a, uint4 v) {
 // measurement: clock64 of pipeline events of CTA 0 (scratch/g2_bench.cu); no-op when null
 __device__ __forceinline__ void g2_trace(unsigned long long* tr, int g, int ev) {
   if (tr != nullptr && blockIdx.x == 0 && g < 1024) tr[g * 8 + ev] = clock64();
+}
+
+// Per-row constants of a unit (row i of this side's A): log2-unit folds of the fast path.
+// fac_fast: q_ij = p_ij 2^lse2_i 2^-lse2'_j, i.e. one MUFU op per logit for both softmaxes.
+template <int ENERGY>
+struct RowConst {
+  float astat, lr2, Ei, Arow, cc0, cc1;
+  f32x2 kL2, kM2, kA2, kLr2, kLrN2, kL1, kEi2, kAr2;
+  __device__ __forceinline__ RowConst(const Grad2Side& sd, int row, bool rv, float invN, bool fac_fast) {
+    constexpr float L2e2 = kLog2e * kLog2e;
+    astat = rv ? sd.a_stat[row] : 0.f;
+    const float lr_nat = rv ? sd.lr[row] : 0.f;
+    lr2 = lr_nat * kLog2e;
+    Ei = fac_fast ? ex2(lr2) : 0.f;
+    Arow = invN * sd.c_r + 2.f * invN * sd.beta_r * lr_nat;
+    cc0 = invN * sd.c_c;
+    cc1 = 2.f * invN * sd.beta_c;
+    kL2 = f2_pack(L2e2, L2e2);
+    kM2 = f2_pack(-2.f * L2e2, -2.f * L2e2);
+    const float ka = ENERGY == CRL_ENERGY_L2 ? astat * L2e2 : astat * kLog2e;
+    kA2 = f2_pack(ka, ka);
+    kLr2 = f2_pack(lr2, lr2);
+    kLrN2 = f2_pack(-lr2, -lr2);
+    kL1 = f2_pack(kLog2e, kLog2e);
+    const float fe = ENERGY == CRL_ENERGY_L2 ? kLog2e : 1.f;   // L2: w = g rs' log2e
+    kEi2 = f2_pack(Ei * fe, Ei * fe);
+    kAr2 = f2_pack(Arow * fe, Arow * fe);
+  }
+};
+
+// w_ij of one row for NC columns c0 .. c0 + NC - 1 of a 128-column tile -> NC / 2 bf16 pairs; the L2
+// row sum of w accumulates into wsum.  raw: S_ij (fp32 bits); bst: [b_stat 128][lcf 128] of the
+// tile in SMEM; lc_tile: the column LSEs of the tile in global memory (exact-q path only).
+// of every 4 logit pairs of the fast path, this many take exp2 on the FMA / ALU pipes
+// (ex2_pair_fma, tc_common.cuh) instead of the MUFU (measured on B200, netscale pair pass:
+// 0 -> 432 us, 1 -> 436, 2 -> 447: the epilogue is latency- rather than XU-bound)
+#ifndef CRL_G2_EMU
+#define CRL_G2_EMU 0
+#endif
+constexpr int kG2EmuPairs = CRL_G2_EMU;
+
+template <int ENERGY, int NC>
+__device__ __forceinline__ void w_tile(const uint32_t (&raw)[NC], const float* bst, int c0, int nval, bool fast,
+                                       bool fac_fast, const RowConst<ENERGY>& k, const float* lc_tile,
+                                       uint32_t (&pk)[NC / 2], float& wsum) {
+  constexpr int BNT = 128;
+  constexpr float kEpsL2e = kEpsL2 * kLog2e * kLog2e;
+  if (fast) {
+    // full tile, normal factors: packed fp32 pairs (FFMA2 / FMUL2 / FADD2), constants
+    // folded into log2 units, column statistics by 16-byte loads; per logit 2 MUFU ops
+    //   L2 : x = d2 (log2 e)^2, rs = 1/sqrt(x), s = x rs = r log2 e,
+    //        p = 2^-(s + lse2_i), w = p (Ei lcf_j + A_i) log2e rs = g_ij / r_ij
+    //   cos: p = 2^(v a_i b_j log2 e - lse2_i), w = p (Ei lcf_j + A_i) b_j
+    //   dot: p = 2^(v log2 e - lse2_i),         w = p (Ei lcf_j + A_i)
+    f32x2 ws2 = f2_pack(0.f, 0.f);
+#pragma unroll
+    for (int i4 = 0; i4 < NC / 4; ++i4) {
+      const float4 bs = lds_f4(smem_u32(bst + c0 + 4 * i4));
+      const float4 lf = lds_f4(smem_u32(bst + BNT + c0 + 4 * i4));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 4 * i4 + 2 * h;
+        const f32x2 v2 = f2_pack(__uint_as_float(raw[i]), __uint_as_float(raw[i + 1]));
+        const f32x2 b2 = h ? f2_pack(bs.z, bs.w) : f2_pack(bs.x, bs.y);
+        const f32x2 l2 = h ? f2_pack(lf.z, lf.w) : f2_pack(lf.x, lf.y);
+        const f32x2 fct = f2_fma(k.kEi2, l2, k.kAr2);
+        float p0, p1, w0, w1;
+        if (ENERGY == CRL_ENERGY_L2) {
+          float x0, x1;
+          f2_unpack(f2_fma(k.kM2, v2, f2_fma(k.kL2, b2, k.kA2)), x0, x1);
+          x0 = fmaxf(x0, kEpsL2e); x1 = fmaxf(x1, kEpsL2e);
+          const f32x2 rs2 = f2_pack(rsq(x0), rsq(x1));
+          float a0, a1;
+          f2_unpack(f2_fma(f2_pack(x0, x1), rs2, k.kLr2), a0, a1);
+          if (((2 * i4 + h) & 3) < kG2EmuPairs) ex2_pair_fma(-a0, -a1, p0, p1);
+          else { p0 = ex2_neg(a0); p1 = ex2_neg(a1); }
+          f2_unpack(f2_mul(f2_mul(f2_pack(p0, p1), fct), rs2), w0, w1);
+        } else if (ENERGY == CRL_ENERGY_COS) {
+          float a0, a1;
+          f2_unpack(f2_fma(f2_mul(v2, b2), k.kA2, k.kLrN2), a0, a1);
+          if (((2 * i4 + h) & 3) < kG2EmuPairs) ex2_pair_fma(a0, a1, p0, p1);
+          else { p0 = ex2(a0); p1 = ex2(a1); }
+          f2_unpack(f2_mul(f2_mul(f2_pack(p0, p1), fct), b2), w0, w1);
+        } else {
+          float a0, a1;
+          f2_unpack(f2_fma(v2, k.kL1, k.kLrN2), a0, a1);
+          if (((2 * i4 + h) & 3) < kG2EmuPairs) ex2_pair_fma(a0, a1, p0, p1);
+          else { p0 = ex2(a0); p1 = ex2(a1); }
+          f2_unpack(f2_mul(f2_pack(p0, p1), fct), w0, w1);
+        }
+        pk[i >> 1] = pack_bf16x2(w0, w1);
+        if (ENERGY == CRL_ENERGY_L2) ws2 = f2_add(ws2, f2_pack(w0, w1));
+      }
+    }
+    if (ENERGY == CRL_ENERGY_L2) {
+      float s0, s1;
+      f2_unpack(ws2, s0, s1);
+      wsum += s0 + s1;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NC; i += 2) {
+      float wv2[2];
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const int jl = c0 + i + e2;
+        const float v = __uint_as_float(raw[i + e2]);
+        const bool cv = jl < nval;
+        const float bj = bst[jl];
+        float l, rs = 0.f;
+        if (ENERGY == CRL_ENERGY_L2) {
+          const float d2 = fmaxf(fmaf(-2.f, v, k.astat + bj), 0.f) + kEpsL2;
+          rs = rsq(d2);
+          l = -d2 * rs;
+        } else if (ENERGY == CRL_ENERGY_COS) {
+          l = v * k.astat * bj;
+        } else {
+          l = v;
+        }
+        const float tv = cv ? l * kLog2e : -INFINITY;
+        const float pe = ex2(tv - k.lr2);
+        float gij;
+        if (fac_fast) {
+          gij = pe * fmaf(k.Ei, bst[BNT + jl], k.Arow);
+        } else {
+          const float lc = cv ? __ldg(lc_tile + jl) : 0.f;
+          const float qe = ex2(tv - lc * kLog2e);
+          gij = fmaf(pe, k.Arow, qe * fmaf(k.cc1, lc, k.cc0));
+        }
+        float wv;
+        if (ENERGY == CRL_ENERGY_L2) wv = gij * rs;
+        else if (ENERGY == CRL_ENERGY_COS) wv = gij * bj;
+        else wv = gij;
+        wv = cv ? wv : 0.f;                               // padded columns: no NaN from pad stats
+        if (ENERGY == CRL_ENERGY_L2) wsum += wv;
+        wv2[e2] = wv;
+      }
+      pk[i >> 1] = pack_bf16x2(wv2[0], wv2[1]);
+    }
+  }
 }
 
 // the tile range of CTA c of G over X tiles: [start(c), start(c + 1))
@@ -345,22 +486,7 @@ __global__ void __launch_bounds__(352, 1) tc_grad2_kernel(const __grid_constant_
         if (lane == 0) mbar_arrive(a_full);
       }
       if (k > 0) readout(prev_side, prev_rb, prev_slot, k - 1);
-      // per-row constants of this unit (fac_fast: q_ij = p_ij 2^lse2_i 2^-lse2'_j, one MUFU op)
-      const float astat = rv ? sd.a_stat[row] : 0.f;
-      const float lr_nat = rv ? sd.lr[row] : 0.f;
-      const float lr2 = lr_nat * kLog2e;
-      const float Ei = fac_fast ? ex2(lr2) : 0.f;
-      const float Arow = p.invN * sd.c_r + 2.f * p.invN * sd.beta_r * lr_nat;
-      const float cc0 = p.invN * sd.c_c, cc1 = 2.f * p.invN * sd.beta_c;
-      // packed constants of the fast path (log2 units)
-      constexpr float L2e2 = kLog2e * kLog2e;
-      const f32x2 kL2 = f2_pack(L2e2, L2e2), kM2 = f2_pack(-2.f * L2e2, -2.f * L2e2);
-      const float ka = ENERGY == CRL_ENERGY_L2 ? astat * L2e2 : astat * kLog2e;
-      const f32x2 kA2 = f2_pack(ka, ka);
-      const f32x2 kLr2 = f2_pack(lr2, lr2), kLrN2 = f2_pack(-lr2, -lr2), kL1 = f2_pack(kLog2e, kLog2e);
-      const float fe = ENERGY == CRL_ENERGY_L2 ? kLog2e : 1.f;   // L2: w = g rs' log2e
-      const f32x2 kEi2 = f2_pack(Ei * fe, Ei * fe), kAr2 = f2_pack(Arow * fe, Arow * fe);
-      constexpr float kEpsL2e = kEpsL2 * L2e2;
+      const RowConst<ENERGY> kc(sd, row, rv, p.invN, fac_fast);
       float wsum = 0.f;
       for (int t = 0; t < nt; ++t, ++g) {
         const int sl = g & 1;
@@ -389,95 +515,8 @@ __global__ void __launch_bounds__(352, 1) tc_grad2_kernel(const __grid_constant_
         if (p.dbg & 1) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) pk[i] = raw[2 * i] ^ raw[2 * i + 1];
-        } else if (fast) {
-          // full tile, normal factors: packed fp32 pairs (FFMA2 / FMUL2 / FADD2), constants
-          // folded into log2 units, column statistics by 16-byte loads; per logit 2 MUFU ops
-          //   L2 : x = d2 (log2 e)^2, rs = 1/sqrt(x), s = x rs = r log2 e,
-          //        p = 2^-(s + lse2_i), w = p (Ei lcf_j + A_i) log2e rs = g_ij / r_ij
-          //   cos: p = 2^(v a_i b_j log2 e - lse2_i), w = p (Ei lcf_j + A_i) b_j
-          //   dot: p = 2^(v log2 e - lse2_i),         w = p (Ei lcf_j + A_i)
-          f32x2 ws2 = f2_pack(0.f, 0.f);
-#pragma unroll
-          for (int i4 = 0; i4 < 16; ++i4) {
-            const float4 bs = lds_f4(smem_u32(bst + c0 + 4 * i4));
-            const float4 lf = lds_f4(smem_u32(bst + BNT + c0 + 4 * i4));
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int i = 4 * i4 + 2 * h;
-              const f32x2 v2 = f2_pack(__uint_as_float(raw[i]), __uint_as_float(raw[i + 1]));
-              const f32x2 b2 = h ? f2_pack(bs.z, bs.w) : f2_pack(bs.x, bs.y);
-              const f32x2 l2 = h ? f2_pack(lf.z, lf.w) : f2_pack(lf.x, lf.y);
-              const f32x2 fct = f2_fma(kEi2, l2, kAr2);
-              float p0, p1, w0, w1;
-              if (ENERGY == CRL_ENERGY_L2) {
-                float x0, x1;
-                f2_unpack(f2_fma(kM2, v2, f2_fma(kL2, b2, kA2)), x0, x1);
-                x0 = fmaxf(x0, kEpsL2e); x1 = fmaxf(x1, kEpsL2e);
-                const f32x2 rs2 = f2_pack(rsq(x0), rsq(x1));
-                float a0, a1;
-                f2_unpack(f2_fma(f2_pack(x0, x1), rs2, kLr2), a0, a1);
-                p0 = ex2_neg(a0); p1 = ex2_neg(a1);
-                f2_unpack(f2_mul(f2_mul(f2_pack(p0, p1), fct), rs2), w0, w1);
-              } else if (ENERGY == CRL_ENERGY_COS) {
-                float a0, a1;
-                f2_unpack(f2_fma(f2_mul(v2, b2), kA2, kLrN2), a0, a1);
-                p0 = ex2(a0); p1 = ex2(a1);
-                f2_unpack(f2_mul(f2_mul(f2_pack(p0, p1), fct), b2), w0, w1);
-              } else {
-                float a0, a1;
-                f2_unpack(f2_fma(v2, kL1, kLrN2), a0, a1);
-                p0 = ex2(a0); p1 = ex2(a1);
-                f2_unpack(f2_mul(f2_pack(p0, p1), fct), w0, w1);
-              }
-              pk[i >> 1] = pack_bf16x2(w0, w1);
-              if (ENERGY == CRL_ENERGY_L2) ws2 = f2_add(ws2, f2_pack(w0, w1));
-            }
-          }
-          if (ENERGY == CRL_ENERGY_L2) {
-            float s0, s1;
-            f2_unpack(ws2, s0, s1);
-            wsum += s0 + s1;
-          }
         } else {
-#pragma unroll
-          for (int i = 0; i < 64; i += 2) {
-            float wv2[2];
-#pragma unroll
-            for (int e2 = 0; e2 < 2; ++e2) {
-              const int jl = c0 + i + e2;
-              const float v = __uint_as_float(raw[i + e2]);
-              const bool cv = jl < nval;
-              const float bj = bst[jl];
-              float l, rs = 0.f;
-              if (ENERGY == CRL_ENERGY_L2) {
-                const float d2 = fmaxf(fmaf(-2.f, v, astat + bj), 0.f) + kEpsL2;
-                rs = rsq(d2);
-                l = -d2 * rs;
-              } else if (ENERGY == CRL_ENERGY_COS) {
-                l = v * astat * bj;
-              } else {
-                l = v;
-              }
-              const float tv = cv ? l * kLog2e : -INFINITY;
-              const float pe = ex2(tv - lr2);
-              float gij;
-              if (fac_fast) {
-                gij = pe * fmaf(Ei, bst[BNT + jl], Arow);
-              } else {
-                const float lc = cv ? __ldg(sd.lc + j0 + jl) : 0.f;
-                const float qe = ex2(tv - lc * kLog2e);
-                gij = fmaf(pe, Arow, qe * fmaf(cc1, lc, cc0));
-              }
-              float wv;
-              if (ENERGY == CRL_ENERGY_L2) wv = gij * rs;
-              else if (ENERGY == CRL_ENERGY_COS) wv = gij * bj;
-              else wv = gij;
-              wv = cv ? wv : 0.f;                         // padded columns: no NaN from pad stats
-              if (ENERGY == CRL_ENERGY_L2) wsum += wv;
-              wv2[e2] = wv;
-            }
-            pk[i >> 1] = pack_bf16x2(wv2[0], wv2[1]);
-          }
+          w_tile<ENERGY, 64>(raw, bst, c0, nval, fast, fac_fast, kc, sd.lc + j0, pk, wsum);
         }
         if (tr_lead) g2_trace(p.trace, g, 6);
         if (g >= 1) mbar_wait(w_empty, (g - 1) & 1);      // dA(g - 1) has read W
@@ -504,6 +543,325 @@ __global__ void __launch_bounds__(352, 1) tc_grad2_kernel(const __grid_constant_
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+}
+
+// =============================================================================== CTA pairs
+// tc_grad2p: the same pass on CTA PAIRS (tcgen05 cta_group::2).  A pair owns 256 rows of a side
+// (CTA r: rows [128 r, 128 r + 128) of the row-block pair, its A tile in its own TMEM) and walks
+// 128-column tiles:
+//   S   = A B^T   M 256, N 128, K 256: rank r stages the B tile's rows [64 r, 64 r + 64)
+//                 (all 256 D: the "S part", 32 KB)
+//   dA += W B     M 256, N 256, K 128: rank r stages the B tile's D half [128 r, 128 r + 128)
+//                 (all 128 rows: the "dA part", 32 KB) and its own W rows
+// so each SM reads half of each B operand from SMEM (the single-CTA pass is bound by its SMEM
+// traffic: TMA 64 + S 64 + dA 96 + W 32 KB per 128 x 128 tile -> here 64 + 32 + 64 + 32).
+// The two parts have their own rings: an S part is free as soon as its S MMA completed.
+// Epilogue, W tile and per-row constants exactly as tc_grad2 (w_tile64).
+namespace g2p {
+constexpr int D = 256, BNT = 128, NS = 2, ND = 3;
+#ifndef CRL_G2P_NWG
+#define CRL_G2P_NWG 4
+#endif
+constexpr int kNWG = CRL_G2P_NWG;                      // epilogue warpgroups (2 or 4)
+constexpr uint32_t SP_CH = 64 * 128;                   // 8 KB: [64 rows][64 D] (SW128)
+constexpr uint32_t SP_BYTES = 4 * SP_CH;               // 32 KB: S part
+constexpr uint32_t DP_CH = BNT * 128;                  // 16 KB: [128 rows][64 D]
+constexpr uint32_t DP_BYTES = 2 * DP_CH;               // 32 KB: dA part
+constexpr uint32_t W_CH = 128 * 128;                   // 16 KB: W K-chunk [128 rows][64 j]
+constexpr uint32_t W_BYTES = 2 * W_CH;                 // one W tile (two are double-buffered)
+constexpr uint32_t STAT_FLOATS = 2 * BNT;
+constexpr size_t SMEM = NS * SP_BYTES + ND * DP_BYTES + 2 * W_BYTES + 2 * STAT_FLOATS * 4 + 256;
+}  // namespace g2p
+
+template <int ENERGY>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG, 1)
+    tc_grad2p_kernel(const __grid_constant__ CUtensorMap tmD0, const __grid_constant__ CUtensorMap tmD1,
+                     const __grid_constant__ CUtensorMap tmS0, const __grid_constant__ CUtensorMap tmS1,
+                     const Grad2Args p) {
+  using namespace g2p;
+  using namespace pair;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sS = smem_raw;                                                 // [NS] S parts
+  uint8_t* sD = sS + NS * SP_BYTES;                                       // [ND] dA parts
+  uint8_t* sW = sD + ND * DP_BYTES;                                       // W tile
+  float* sStat = reinterpret_cast<float*>(sW + 2 * W_BYTES);              // [2][b_stat 128, lcf 128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 2 * STAT_FLOATS);
+  uint64_t* sp_full = bars;                // [NS] leader: both CTAs' S-part bytes
+  uint64_t* sp_free = sp_full + NS;        // [NS] both: S MMA done (multicast)
+  uint64_t* dp_full = sp_free + NS;        // [ND] leader: both CTAs' dA-part bytes
+  uint64_t* dp_free = dp_full + ND;        // [ND] both: dA MMA done
+  uint64_t* st_full = dp_free + ND;        // [2] local column statistics
+  uint64_t* st_empty = st_full + 2;        // [2]
+  uint64_t* s_full = st_empty + 2;         // both: S accumulator ready
+  uint64_t* s_empty = s_full + 1;          // leader: every epilogue warp loaded S
+  uint64_t* w_full = s_empty + 1;          // [2] leader: every epilogue warp wrote W buffer b
+  uint64_t* w_empty = w_full + 2;          // [2] both: the dA of buffer b read it
+  uint64_t* a_full = w_empty + 2;          // leader: A of the unit in both TMEMs
+  uint64_t* da_full = a_full + 1;          // both: the unit's dA complete
+  uint64_t* da_empty = da_full + 1;        // leader: dA read out
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
+  const long X = 2L * p.RB * p.TPB;                                       // p.RB: row-block PAIRS
+  const long x0 = g2::range_start(cid, X, ncl), x1 = g2::range_start(cid + 1, X, ncl);
+  auto unit_at = [&](long x, int& side, int& rb, int& tb, int& nt) {
+    const long r = x / p.TPB;
+    tb = (int)(x - r * p.TPB);
+    side = (int)(r / p.RB);
+    rb = (int)(r - (long)side * p.RB);
+    nt = (int)min((long)(p.TPB - tb), x1 - x);
+  };
+
+  if (warp == 0 && lane == 0) {
+    if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+    tma_prefetch_desc(&tmD0); tma_prefetch_desc(&tmD1);
+    tma_prefetch_desc(&tmS0); tma_prefetch_desc(&tmS1);
+    for (int i = 0; i < NS; ++i) { mbar_init(&sp_full[i], 1); mbar_init(&sp_free[i], 1); }
+    for (int i = 0; i < ND; ++i) { mbar_init(&dp_full[i], 1); mbar_init(&dp_free[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&st_full[i], 1); mbar_init(&st_empty[i], 4 * kNWG); }
+    mbar_init(s_full, 1); mbar_init(s_empty, 8 * kNWG);
+    for (int i = 0; i < 2; ++i) { mbar_init(&w_full[i], 8 * kNWG); mbar_init(&w_empty[i], 1); }
+    mbar_init(a_full, 8 * kNWG); mbar_init(da_full, 1); mbar_init(da_empty, 8 * kNWG);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tm_s = tmem, tm_da = tmem + 128, tm_a = tmem + 384;
+  pdl_wait();
+  pdl_launch();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer (both)
+      int g = 0;
+      for (long x = x0; x < x1;) {
+        int side, rb, tb, nt;
+        unit_at(x, side, rb, tb, nt);
+        const CUtensorMap* mS = side ? &tmS1 : &tmS0;
+        const CUtensorMap* mD = side ? &tmD1 : &tmD0;
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int j0 = (tb + t) * BNT;
+          const int ss = g % NS, ds = g % ND;
+          mbar_wait(&sp_free[ss], ((g / NS) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&sp_full[ss], 2 * SP_BYTES);
+          const uint32_t sfb = mapa(smem_u32(&sp_full[ss]), 0);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            tma_load_2d_pair(smem_u32(sS + ss * SP_BYTES + c * SP_CH), mS, sfb, 64 * c, j0 + 64 * (int)rank);
+          g2::g2_trace(p.trace, g, 0);
+          mbar_wait(&dp_free[ds], ((g / ND) & 1) ^ 1);
+          g2::g2_trace(p.trace, g, 1);
+          if (rank == 0) mbar_expect_tx(&dp_full[ds], 2 * DP_BYTES);
+          const uint32_t dfb = mapa(smem_u32(&dp_full[ds]), 0);
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d_pair(smem_u32(sD + ds * DP_BYTES + c * DP_CH), mD, dfb, 128 * (int)rank + 64 * c, j0);
+        }
+        x += nt;
+      }
+    }
+  } else if (warp == 2 + 4 * kNWG) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- column statistics (local)
+      int g = 0;
+      for (long x = x0; x < x1;) {
+        int side, rb, tb, nt;
+        unit_at(x, side, rb, tb, nt);
+        const Grad2Side& sd = p.side[side];
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int j0 = (tb + t) * BNT;
+          const int e = g & 1;
+          mbar_wait(&st_empty[e], ((g >> 1) & 1) ^ 1);
+          mbar_expect_tx(&st_full[e], STAT_FLOATS * 4);
+          float* st = sStat + e * STAT_FLOATS;
+          g2::bulk_g2s(st, sd.b_stat + j0, BNT * 4, &st_full[e]);
+          g2::bulk_g2s(st + BNT, sd.lcf + j0, BNT * 4, &st_full[e]);
+        }
+        x += nt;
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer (leader)
+      const uint32_t id_s = idesc_bf16_f32(256, BNT, false, false);
+      const uint32_t id_da = idesc_bf16_f32(256, D, false, true);
+      auto issue_s = [&](int g) {
+        mbar_wait(s_empty, (g & 1) ^ 1);      // both CTAs loaded S(g - 1)
+        const int ss = g % NS;
+        mbar_wait(&sp_full[ss], (g / NS) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            mma_pair_ts(tm_s, tm_a + (uint32_t)(8 * (4 * c + ks)),
+                        smem_desc_sw128(smem_u32(sS + ss * SP_BYTES + c * SP_CH) + ks * 32, 16, 1024), id_s,
+                        (c | ks) != 0);
+        commit_pair(&sp_free[ss]);
+        commit_pair(s_full);
+        g2::g2_trace(p.trace, g, 2);
+      };
+      auto issue_da = [&](int g, bool first, int k) {
+        if (first) {
+          mbar_wait(da_empty, (k & 1) ^ 1);   // unit k - 1's dA read out (both)
+          tc_fence_after();
+        }
+        mbar_wait(&w_full[g & 1], (g >> 1) & 1);
+        const int ds = g % ND;
+        mbar_wait(&dp_full[ds], (g / ND) & 1);
+        tc_fence_after();
+        const uint32_t w_base = smem_u32(sW + (g & 1) * W_BYTES), b0 = smem_u32(sD + ds * DP_BYTES);
+#pragma unroll
+        for (int ks = 0; ks < BNT / 16; ++ks)            // K = the 128 rows of the tile
+          mma_pair(tm_da, smem_desc_sw128(w_base + (ks >> 2) * W_CH + (ks & 3) * 32, 16, 1024),
+                   smem_desc_sw128(b0 + ks * 2048, DP_CH, 1024), id_da, !(first && ks == 0));
+        commit_pair(&dp_free[ds]);
+        commit_pair(&w_empty[g & 1]);
+        g2::g2_trace(p.trace, g, 3);
+      };
+      int g = 0, k = 0;
+      for (long x = x0; x < x1; ++k) {
+        int side, rb, tb, nt;
+        unit_at(x, side, rb, tb, nt);
+        mbar_wait(a_full, k & 1);             // A of this unit in both TMEMs
+        tc_fence_after();
+        // S runs two tiles ahead of dA: S(t + 2) needs the TMEM load of S(t + 1) only, so it
+        // enters the pipe ahead of dA(t) and its commit latency (~600 cycles across the pair)
+        // hides under tile t + 1's epilogue (S parts and dA parts have separate rings, so the
+        // early S cannot wait on a slot only a later dA frees)
+        issue_s(g);
+        if (nt > 1) issue_s(g + 1);
+        for (int t = 0; t < nt; ++t) {
+          if (t + 2 < nt) issue_s(g + t + 2);
+          issue_da(g + t, t == 0, k);
+        }
+        commit_pair(da_full);
+        g += nt;
+        x += nt;
+      }
+    }
+  } else if (warp >= 2) {
+    // ------------------------------------------------------------------ epilogue (kNWG warpgroups)
+    // warpgroup wg: columns [CW wg, CW wg + CW) of every tile, the same share of A's K and of
+    // dA's D; 4 warpgroups = 4 warps per SMSP to hide the per-logit MUFU / TMEM latencies
+    constexpr int CW = BNT / kNWG;                        // tile columns per warpgroup
+    constexpr int AK = 128 / kNWG;                        // packed A columns (bf16 pairs) per warpgroup
+    constexpr int DQ = D / kNWG;                          // dA columns per warpgroup
+    const int wg = (warp - 2) >> 2;
+    const int q = warp & 3;
+    const int r = q * 32 + lane;                          // row within this CTA's 128 rows
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const bool fac_fast = *p.fac_ok != 0;
+    const int c0 = CW * wg;
+    const uint32_t s_empty_l = mapa(smem_u32(s_empty), 0), w_full_l = mapa(smem_u32(w_full), 0);   // + 8 b
+    const uint32_t a_full_l = mapa(smem_u32(a_full), 0), da_empty_l = mapa(smem_u32(da_empty), 0);
+    int g = 0, k = 0;
+    int prev_side = 0, prev_rb = 0, prev_slot = 0;
+    auto readout = [&](int side, int rb, int slot, int kk) {
+      mbar_wait(da_full, kk & 1);
+      tc_fence_after();
+      const int row = rb * 256 + 128 * (int)rank + r;
+      const Grad2Side& sd = p.side[side];
+      const bool rv = row < p.Na;
+      float* out = sd.part_da + ((size_t)slot * p.Na + row) * D + DQ * wg;
+#pragma unroll 1
+      for (int c = 0; c < DQ / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32_nowait(tm_da + lane_off + DQ * wg + 32 * c, v);
+        tmem_ld_wait();
+        if (rv) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(out + 32 * c)[i] =
+                make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
+                            __uint_as_float(v[4 * i + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_remote(da_empty_l);
+    };
+    for (long x = x0; x < x1; ++k) {
+      int side, rb, tb, nt;
+      unit_at(x, side, rb, tb, nt);
+      const Grad2Side& sd = p.side[side];
+      const int row = rb * 256 + 128 * (int)rank + r;
+      const bool rv = row < p.Na;
+      {  // A rows -> this CTA's TMEM (the previous unit's S MMAs completed: its last S was loaded)
+        uint32_t av[AK];
+        if (rv) {
+          const uint4* src = reinterpret_cast<const uint4*>(sd.A + (size_t)row * D + 2 * AK * wg);
+#pragma unroll
+          for (int i = 0; i < AK / 4; ++i) {
+            const uint4 u = __ldg(src + i);
+            av[4 * i] = u.x; av[4 * i + 1] = u.y; av[4 * i + 2] = u.z; av[4 * i + 3] = u.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < AK; ++i) av[i] = 0u;
+        }
+#pragma unroll
+        for (int h = 0; h < AK / 32; ++h)
+          g2::tmem_st32(tm_a + lane_off + AK * wg + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(av + 32 * h));
+        g2::tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_remote(a_full_l);
+      }
+      if (k > 0) readout(prev_side, prev_rb, prev_slot, k - 1);
+      const g2::RowConst<ENERGY> kc(sd, row, rv, p.invN, fac_fast);
+      float wsum = 0.f;
+      for (int t = 0; t < nt; ++t, ++g) {
+        const int sl = g & 1;
+        const int j0 = (tb + t) * BNT;
+        const int nval = p.Nb - j0;
+        mbar_wait(s_full, g & 1);
+        tc_fence_after();
+        const bool tl = warp == 2 && lane == 0;
+        if (tl) g2::g2_trace(p.trace, g, 4);
+        uint32_t raw[CW];
+#pragma unroll
+        for (int h = 0; h < CW / 32; ++h)
+          tmem_ld32_nowait(tm_s + lane_off + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(raw + 32 * h));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_remote(s_empty_l);
+        if (tl) g2::g2_trace(p.trace, g, 5);
+        mbar_wait(&st_full[sl], (g >> 1) & 1);
+        const float* bst = sStat + sl * STAT_FLOATS;
+        uint32_t pk[CW / 2];
+        g2::w_tile<ENERGY, CW>(raw, bst, c0, nval, fac_fast && nval >= BNT, fac_fast, kc, sd.lc + j0, pk, wsum);
+        if (tl) g2::g2_trace(p.trace, g, 6);
+        if (g >= 2) mbar_wait(&w_empty[g & 1], ((g >> 1) - 1) & 1);   // dA(g - 2) has read buffer g & 1
+        const uint32_t wt = smem_u32(sW + (g & 1) * W_BYTES + (c0 >> 6) * W_CH);   // K-chunk of these columns
+#pragma unroll
+        for (int u = 0; u < CW / 8; ++u)
+          g2::sts_u4(wt + g2::sw128_off(r, (c0 & 63) + 8 * u),
+                     make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) { arrive_remote(w_full_l + 8u * (uint32_t)(g & 1)); mbar_arrive(&st_empty[sl]); }
+        if (tl) g2::g2_trace(p.trace, g, 7);
+      }
+      const int slot = tb == 0 ? 0 : 1;
+      if (ENERGY == CRL_ENERGY_L2 && rv) sd.part_rs[((size_t)(kNWG * slot + wg)) * p.Na + row] = wsum;
+      prev_side = side; prev_rb = rb; prev_slot = slot;
+      x += nt;
+    }
+    if (k > 0) readout(prev_side, prev_rb, prev_slot, k - 1);
+  }
+  tc_fence_before();
+  cluster_sync();                          // the peer's MMAs / arrivals are done before TMEM goes
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
   }
 }
 
@@ -539,6 +897,52 @@ static cudaError_t launch_g2(const CUtensorMap& b0, const CUtensorMap& b1, const
     attr = true;
   }
   return launch_pdl(tc_grad2_kernel<ENERGY>, dim3(grid), dim3(352), g2::SMEM, st, b0, b1, p);
+}
+
+int tc_grad2p_warpgroups() { return g2p::kNWG; }
+
+// ---- CTA pairs: a pair owns 256-row row-block PAIRS; grid = 2 x pairs
+int tc_grad2p_grid(int Na, int num_sms) {
+  const int RBP = (Na + 255) / 256;
+  return 2 * std::max(1, std::min(num_sms / 2, 2 * RBP));
+}
+// slot-1 flags per 128-row block: a row-block pair cut by a pair boundary flags both its blocks
+void tc_grad2p_split_flags(int Na, int Nb, int grid, unsigned char* flags /*[2][RB]*/) {
+  const long RB = (Na + 127) / 128, RBP = (Na + 255) / 256, TPB = (Nb + g2::BNT - 1) / g2::BNT;
+  const long X = 2 * RBP * TPB, P = grid / 2;
+  for (long side = 0; side < 2; ++side)
+    for (long rb = 0; rb < RB; ++rb) {
+      const long rp = side * RBP + rb / 2, first = rp * TPB, last = first + TPB - 1;
+      bool cut = false;
+      for (long c = 1; c < P; ++c) {
+        const long st = g2::range_start(c, X, P);
+        if (st > first && st <= last) { cut = true; break; }
+      }
+      flags[side * RB + rb] = cut ? 1 : 0;
+    }
+}
+
+template <int ENERGY>
+static cudaError_t launch_g2p(const CUtensorMap& d0, const CUtensorMap& d1, const CUtensorMap& s0,
+                              const CUtensorMap& s1, const Grad2Args& p, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_grad2p_kernel<ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)g2p::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_pdl(tc_grad2p_kernel<ENERGY>, dim3(grid), dim3(96 + 128 * g2p::kNWG), g2p::SMEM, st, d0, d1, s0, s1, p);
+}
+
+cudaError_t tc_grad2p(int energy, const CUtensorMap& mD0, const CUtensorMap& mD1, const CUtensorMap& mS0,
+                      const CUtensorMap& mS1, const Grad2Args& p0, int grid, cudaStream_t st) {
+  Grad2Args p = p0;
+  p.RB = (p.Na + 255) / 256;                              // row-block PAIRS
+  p.TPB = (p.Nb + g2p::BNT - 1) / g2p::BNT;
+  if (energy == CRL_ENERGY_L2) return launch_g2p<CRL_ENERGY_L2>(mD0, mD1, mS0, mS1, p, grid, st);
+  if (energy == CRL_ENERGY_COS) return launch_g2p<CRL_ENERGY_COS>(mD0, mD1, mS0, mS1, p, grid, st);
+  return launch_g2p<CRL_ENERGY_DOT>(mD0, mD1, mS0, mS1, p, grid, st);
 }
 
 cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1, const Grad2Args& p0, int grid,

@@ -32,6 +32,12 @@ int tc_grad2_grid(int Na, int num_sms);
 void tc_grad2_split_flags(int Na, int Nb, int grid, unsigned char* flags);
 cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1, const Grad2Args& p, int grid,
                      cudaStream_t st);
+// CTA-pair variant: D maps box {64, 128} (dA parts), S maps box {64, 64} (S parts); grid = 2 x pairs
+int tc_grad2p_grid(int Na, int num_sms);
+int tc_grad2p_warpgroups();                // epilogue warpgroups = L2 row-sum sub-slots per partial slot
+void tc_grad2p_split_flags(int Na, int Nb, int grid, unsigned char* flags);
+cudaError_t tc_grad2p(int energy, const CUtensorMap& mD0, const CUtensorMap& mD1, const CUtensorMap& mS0,
+                      const CUtensorMap& mS1, const Grad2Args& p, int grid, cudaStream_t st);
 
 }  // namespace tc
 }  // namespace crl

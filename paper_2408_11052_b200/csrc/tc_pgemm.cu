@@ -36,10 +36,12 @@
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_pgemm.h"
+#include "tc_pair.cuh"
 
 namespace crl {
 namespace tc {
 namespace pg {
+using namespace pair;
 
 constexpr int kBK = 64, kStages = 5, kTN = 256;      // K block, ring depth, tile N (= tile M / 1)
 constexpr uint32_t kAHalf = 128 * kBK * 2;          // 16 KB: this CTA's 128 rows of A
@@ -49,38 +51,6 @@ constexpr uint32_t kStgBuf = 32 * 128;             // 4 KB: 32 rows x 128 B (SW1
 constexpr int kNStg = 4;                            // staging buffers per epilogue warp
 constexpr size_t kSmem = 1024 + kStages * kStage + 4 * kNStg * kStgBuf + 256;
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_id_x() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t nclusters_x() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// TMA load into this CTA's kSmem, completion bytes on a barrier of either CTA of the pair
-__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t mbar_cluster, int x,
-                                                 int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(x), "r"(y)
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_2d_local(uint32_t dst, const CUtensorMap* map, uint64_t* mbar, int x, int y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -100,35 +70,6 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void expect_tx_remote(uint32_t mbar_cluster, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(mbar_cluster), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void arrive_remote(uint32_t mbar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cluster) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONEC_%=;\n\t"
-      "bra WAITC_%=;\n"
-      "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-}
-// arrive (once all previously issued MMAs completed) on the barrier at this offset in both CTAs
-__device__ __forceinline__ void commit_pair(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
-          smem_u32(bar))
-      : "memory");
 }
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
@@ -225,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       int g = 0, it = 0;
       for (int t = cid; t < n_tiles; t += ncl, ++it) {
         const int b = it & 1;
-        mbar_wait_acq_cluster(&tempty[b], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + 256u * (uint32_t)b;
         for (int kb = 0; kb < nkb; ++kb, ++g) {

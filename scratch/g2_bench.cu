@@ -55,7 +55,7 @@ int main(int argc, char** argv) {
   int* fac = up(one);
   float *pda, *prs;
   cudaMalloc(&pda, (size_t)4 * N * D * 4);
-  cudaMalloc(&prs, (size_t)8 * N * 4);
+  cudaMalloc(&prs, (size_t)16 * N * 4);
   CUtensorMap m0, m1;
   if (!make_map_bf16(&m0, dA1, D, N, D, 64, 128) || !make_map_bf16(&m1, dA0, D, N, D, 64, 128)) {
     printf("tensor map failed\n");
@@ -76,7 +76,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e1);
   const char* names[] = {"full", "no-epi-math", "no-dA-mma", "", "no-S-mma", "", "S-only(no dA, no math)", "", "",
                          "", "", "", "", "", "", ""};
-  const int variants[] = {0, 1, 2, 4, 3, 6, 5, 7, 15, 23, 31, 8, 16, 24};
+  const int variants[] = {0, 1};
   const double logits = 2.0 * N * (double)N, flops = 4.0 * N * (double)N * D * 2;
   for (int v : variants) {
     ga.dbg = v;
@@ -96,6 +96,73 @@ int main(int argc, char** argv) {
     const double us = 1e3 * ms / iters;
     printf("dbg=%d %-26s %8.1f us  %7.1f TFLOP/s (4 GEMM-eq)  %6.2f Glogit-sides/ms\n", v,
            v < 16 && names[v][0] ? names[v] : "combo", us, flops / us * 1e-6, logits / us * 1e-6);
+  }
+  // ---- CTA-pair variant: time + compare slot sums of dA and row sums with the single-CTA pass
+  {
+    CUtensorMap s0m, s1m;
+    if (!make_map_bf16(&s0m, dA1, D, N, D, 64, 64) || !make_map_bf16(&s1m, dA0, D, N, D, 64, 64)) {
+      printf("tensor map failed\n");
+      return 1;
+    }
+    ga.dbg = 0;
+    const size_t nda = (size_t)4 * N * D, nrs = (size_t)16 * N;
+    auto slot_sum = [&](std::vector<float>& da, std::vector<float>& rs, int nsub) {
+      std::vector<float> h(nda), hr(nrs);
+      cudaMemcpy(h.data(), pda, nda * 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(hr.data(), prs, nrs * 4, cudaMemcpyDeviceToHost);
+      da.assign((size_t)2 * N * D, 0.f);
+      rs.assign((size_t)2 * N, 0.f);
+      for (int sd = 0; sd < 2; ++sd)
+        for (int sl = 0; sl < 2; ++sl)
+          for (size_t i = 0; i < (size_t)N * D; ++i) da[sd * (size_t)N * D + i] += h[((size_t)sd * 2 + sl) * N * D + i];
+      for (int sd = 0; sd < 2; ++sd)
+        for (int u = 0; u < 2 * nsub; ++u)
+          for (int i = 0; i < N; ++i) rs[sd * N + i] += hr[((size_t)sd * 2 * nsub + u) * N + i];
+    };
+    cudaMemset(pda, 0, nda * 4); cudaMemset(prs, 0, nrs * 4);
+    tc_grad2(CRL_ENERGY_L2, m0, m1, ga, grid, 0);
+    cudaDeviceSynchronize();
+    std::vector<float> ref_da, ref_rs, got_da, got_rs;
+    slot_sum(ref_da, ref_rs, 2);
+    ga.side[1].part_rs = prs + (size_t)2 * 4 * N;         // pair: 4 warpgroup sub-slots per slot
+    const int gp = tc_grad2p_grid(N, sms);
+    cudaMemset(pda, 0, nda * 4); cudaMemset(prs, 0, nrs * 4);
+    cudaError_t err = tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, ga, gp, 0);
+    err = err != cudaSuccess ? err : cudaDeviceSynchronize();
+    if (err != cudaSuccess) { printf("pair error %s\n", cudaGetErrorString(err)); return 1; }
+    slot_sum(got_da, got_rs, 4);
+    double md = 0, mr = 0, sd2 = 0, sr2 = 0;
+    for (size_t i = 0; i < ref_da.size(); ++i) { md = std::max(md, (double)std::fabs(got_da[i] - ref_da[i])); sd2 = std::max(sd2, (double)std::fabs(ref_da[i])); }
+    for (size_t i = 0; i < ref_rs.size(); ++i) { mr = std::max(mr, (double)std::fabs(got_rs[i] - ref_rs[i])); sr2 = std::max(sr2, (double)std::fabs(ref_rs[i])); }
+    printf("pair vs single: max|d dA| %.3g (max %.3g)  max|d rs| %.3g (max %.3g)\n", md, sd2, mr, sr2);
+    for (int it = 0; it < 3; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, ga, gp, 0);
+    cudaEventRecord(e0);
+    for (int it = 0; it < 10; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, ga, gp, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double us = 1e3 * ms / 10;
+    printf("pair grid %d: %8.1f us  %7.1f TFLOP/s (4 GEMM-eq)\n", gp, us, flops / us * 1e-6);
+    {
+      unsigned long long* tr;
+      cudaMalloc(&tr, 1024 * 8 * 8);
+      cudaMemset(tr, 0, 1024 * 8 * 8);
+      Grad2Args gt = ga;
+      gt.trace = tr;
+      tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, gt, gp, 0);
+      cudaDeviceSynchronize();
+      std::vector<unsigned long long> ht(1024 * 8);
+      cudaMemcpy(ht.data(), tr, ht.size() * 8, cudaMemcpyDeviceToHost);
+      const unsigned long long t0 = ht[4];
+      printf("pair trace: g: Sfree? Dfree Sissued dAissued Sready Sloaded mathdone Whanded\n");
+      for (int g = 0; g < 24; ++g) {
+        printf("%3d:", g);
+        for (int e = 0; e < 8; ++e) printf(" %7lld", ht[g * 8 + e] ? (long long)(ht[g * 8 + e] - t0) : -1LL);
+        printf("\n");
+      }
+      printf("pair period tiles 50..100: %.0f cyc/tile\n", (double)(ht[100 * 8 + 4] - ht[50 * 8 + 4]) / 50);
+    }
   }
   // event trace of CTA 0 (full variant): per tile the clock of 0 B slot free, 1 S issued, 2 dA
   // issued, 3 S ready (epilogue), 4 S loaded, 5 math done, 6 W buffer free, 7 W handed over

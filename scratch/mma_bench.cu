@@ -6,6 +6,7 @@
 //        scratch/mma_bench.cu -o scratch/mma_bench && scratch/mma_bench
 #include <cstdio>
 #include "tc_common.cuh"
+#include "tc_pair.cuh"
 
 using namespace crl::tc;
 
@@ -181,6 +182,55 @@ void run_tile(int sms, long long* d) {
          MODE == 1 ? "S" : MODE == 2 ? "dA" : "S+dA", (int)INIT, c, e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
+// CTA-pair MMAs (cta_group::2, M = 256): cycles per instruction for N in {128, 256}, A from SMEM
+// (ss) or TMEM (ts); the leader issues, completion multicast to both CTAs
+template <int N, bool TS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma_pair(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t rank = pair::cluster_rank();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  if (warp == 0) pair::tmem_alloc_pair(&slot, 512);
+  tc_fence_before();
+  pair::cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0 && rank == 0) {
+    const uint32_t id = idesc_bf16_f32(256, N, false, false);
+    const uint32_t a_base = smem_u32(smem), b_base = a_base + 65536;
+    long long t0 = clock64();
+    for (int i = 0; i < NMMA; ++i) {
+      const int ks = i & 3;
+      const uint64_t bd = smem_desc_sw128(b_base + ks * 32, 16, 1024);
+      if (TS) pair::mma_pair_ts(tmem, tmem + 256 + 8 * ks, bd, id, 1);
+      else pair::mma_pair(tmem, smem_desc_sw128(a_base + ks * 32, 16, 1024), bd, id, 1);
+    }
+    pair::commit_pair(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+  } else if (threadIdx.x == 0) {
+    mbar_wait(&bar, 0);
+  }
+  tc_fence_before();
+  pair::cluster_sync();
+  if (warp == 0) { tc_fence_after(); pair::tmem_dealloc_pair(tmem, 512); }
+}
+template <int N, bool TS>
+void run_mma_pair(int sms, long long* d) {
+  const int smem = 65536 + 65536;
+  cudaFuncSetAttribute(k_mma_pair<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int rep = 0; rep < 2; ++rep) k_mma_pair<N, TS><<<sms, 128, smem>>>(d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long c;
+  cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+  const double cyc = (double)c / NMMA;
+  printf("pair mma %s N=%3d: %6.1f cyc/MMA  (floor %3d)  %s\n", TS ? "ts" : "ss", N, cyc, 256 * N / 512,
+         e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
 // TMEM -> registers: every warp reads its 32 lanes x 32 columns, ITER times over 128 columns
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1) k_ldtm(long long* out, float* sink) {
@@ -246,6 +296,10 @@ int main() {
   run_mma<128, true>(sms, d);
   run_mma<256, false>(sms, d);
   run_mma<256, true>(sms, d);
+  run_mma_pair<128, false>(sms, d);
+  run_mma_pair<128, true>(sms, d);
+  run_mma_pair<256, false>(sms, d);
+  run_mma_pair<256, true>(sms, d);
   run_tile<1, false>(sms, d);
   run_tile<2, false>(sms, d);
   run_tile<3, false>(sms, d);

@@ -792,13 +792,16 @@ def test_critic_step_bf16_stats_d256(energy, batch):
     ("l2", None), ("dot", None), ("cos", None),
     ("l2", "CRL_FORCE_EXACT_Q"),      # exact second exp2 instead of the row / column factors
     ("cos", "CRL_FORCE_EXACT_Q"),
+    ("l2", "CRL_NO_GRAD2P"),          # the single-CTA pass instead of the CTA-pair one
+    ("cos", "CRL_NO_GRAD2P"),
     ("l2", "CRL_NO_GRAD2"),           # the two-call gradient kernels (tc_logits.cu)
     ("dot", "CRL_NO_GRAD2"),
 ])
 @pytest.mark.parametrize("batch", [1100, 2900])
 def test_critic_step_bf16_grad2_d256(energy, knob, batch, monkeypatch):
     """The both-sides gradient pass at D = 256 (tc_grad2.cu: persistent, contiguous tile ranges,
-    A held in TMEM, two partial slots per cut row block) against the oracle; ragged N."""
+    A held in TMEM, two partial slots per cut row block; by default on CTA pairs, tc_grad2p)
+    against the oracle; ragged N."""
     if knob:
         monkeypatch.setenv(knob, "1")
     cfg = crl_synth.preset("ant", batch=batch, width=256, repr_dim=256, energy=energy, precision="bf16")
