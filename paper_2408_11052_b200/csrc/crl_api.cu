@@ -87,6 +87,9 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   // wide encoders (configs[4]: 4 x 1024) already have ~200 weight-gradient tiles per K slice:
   // more slices only add partial-buffer traffic (Adam sums them).  Measured on B200 at
   // netscale: 8 slices 584 steps/s (dW 278 us + Adam 74 us), 2 slices 601 (257 + 48).
+  // (A CTA-pair variant of the grouped kernel, 256 x 256 tiles, measured slower at netscale:
+  // 668 vs 679 steps/s -- its bias sums double the MMA work of every M-block-0 tile and its
+  // single accumulator serialises the epilogue; not kept.)
   if (k.width >= 512 && !std::getenv("CRL_DW_SPLITS")) c->dw_splits = std::min(c->dw_splits, 2);
   c->grads = s.take<float>(c->sizes.n_params * c->dw_splits);
   const bool bf = k.precision == CRL_BF16;

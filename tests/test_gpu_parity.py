@@ -806,3 +806,12 @@ def test_critic_step_bf16_grad2_d256(energy, knob, batch, monkeypatch):
         monkeypatch.setenv(knob, "1")
     cfg = crl_synth.preset("ant", batch=batch, width=256, repr_dim=256, energy=energy, precision="bf16")
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+def test_critic_step_bf16_wide_dw_long_k():
+    """Weight / bias gradients of wide encoders with a long batch reduction (tc_dwg.cu: 2 K
+    slices for width >= 512, 128 x 256 tiles, the bias sums by an all-ones MMA on M block 0)
+    against the oracle, per tensor; a ragged batch (K not a multiple of the 64-row K block)
+    and the 37-input first layer (one partial M block)."""
+    cfg = crl_synth.preset("ant", batch=4160, width=512, repr_dim=64, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
