@@ -48,16 +48,38 @@ __global__ void __launch_bounds__(256) buffer_insert_kernel(
     uint32_t* __restrict__ ep_end, uint32_t* __restrict__ open_start) {
   const int e = blockIdx.x;
   const uint32_t n_new = n_ins + (uint32_t)U;
-  // copy rows: element-level loop over (u, c) so every row is written by consecutive threads
-  for (int idx = threadIdx.x; idx < U * obs_dim; idx += blockDim.x) {
-    int u = idx / obs_dim, c = idx - u * obs_dim;
-    uint32_t slot = (n_ins + u) % (uint32_t)T;
-    obs_ring[((size_t)e * T + slot) * obs_stride + c] = obs[((size_t)u * E + e) * obs_dim + c];
-  }
-  for (int idx = threadIdx.x; idx < U * act_dim; idx += blockDim.x) {
-    int u = idx / act_dim, c = idx - u * act_dim;
-    uint32_t slot = (n_ins + u) % (uint32_t)T;
-    act_ring[((size_t)e * T + slot) * act_stride + c] = act[((size_t)u * E + e) * act_dim + c];
+  // copy rows: a warp per step u (8 warps over the U steps), lanes along the row, every load
+  // of a warp's rows issued before its stores (the rows are independent; one HBM latency per
+  // group of 8 instead of one per row)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int RPW = 8;                                  // rows in flight per warp
+  for (int u0 = warp; u0 < U; u0 += RPW * nw) {
+    for (int c = lane; c < obs_dim; c += 32) {
+      float v[RPW];
+#pragma unroll
+      for (int k = 0; k < RPW; ++k) {
+        const int u = u0 + k * nw;
+        v[k] = u < U ? obs[((size_t)u * E + e) * obs_dim + c] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < RPW; ++k) {
+        const int u = u0 + k * nw;
+        if (u < U) obs_ring[((size_t)e * T + (n_ins + (uint32_t)u) % (uint32_t)T) * obs_stride + c] = v[k];
+      }
+    }
+    for (int c = lane; c < act_dim; c += 32) {
+      float v[RPW];
+#pragma unroll
+      for (int k = 0; k < RPW; ++k) {
+        const int u = u0 + k * nw;
+        v[k] = u < U ? act[((size_t)u * E + e) * act_dim + c] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < RPW; ++k) {
+        const int u = u0 + k * nw;
+        if (u < U) act_ring[((size_t)e * T + (n_ins + (uint32_t)u) % (uint32_t)T) * act_stride + c] = v[k];
+      }
+    }
   }
   for (int u = threadIdx.x; u < U; u += blockDim.x) {
     uint32_t slot = (n_ins + u) % (uint32_t)T;
@@ -65,13 +87,17 @@ __global__ void __launch_bounds__(256) buffer_insert_kernel(
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
+  // episode ends: the U done flags are read 32 at a time (one ballot) and the closed episodes
+  // are back-filled in step order (each slot at most once)
   uint32_t start = open_start[e];
   const uint32_t lo_keep = n_new > (uint32_t)T ? n_new - (uint32_t)T : 0u;   // oldest kept slot
-  for (int u = 0; u < U; ++u) {
-    if (done[(size_t)u * E + e]) {
-      uint32_t tau_end = n_ins + (uint32_t)u;
-      uint32_t first = start > lo_keep ? start : lo_keep;
+  for (int u0 = 0; u0 < U; u0 += 32) {
+    unsigned bits = __ballot_sync(0xffffffffu, u0 + lane < U && done[(size_t)(u0 + lane) * E + e] != 0);
+    while (bits) {
+      const int u = u0 + __ffs(bits) - 1;
+      bits &= bits - 1u;
+      const uint32_t tau_end = n_ins + (uint32_t)u;
+      const uint32_t first = start > lo_keep ? start : lo_keep;
       for (uint32_t t = first + lane; t <= tau_end; t += 32)
         ep_end[(size_t)e * T + (t % (uint32_t)T)] = tau_end;
       start = tau_end + 1;
