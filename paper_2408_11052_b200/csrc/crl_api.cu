@@ -122,6 +122,16 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     for (int l = 0; l < k.depth; ++l) {
       c->phiZb[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
       c->psiZb[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
+      if (k.layernorm) {                         // F2 on the bf16 path: Y = LN(Z) and its statistics
+        c->phiYb[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd); c->psiYb[l] = s.take<__nv_bfloat16>((size_t)Bl * Wd);
+        c->phiMu[l] = s.take<float>((size_t)Bl); c->psiMu[l] = s.take<float>((size_t)Bl);
+        c->phiRs[l] = s.take<float>((size_t)Bl); c->psiRs[l] = s.take<float>((size_t)Bl);
+      }
+    }
+    if (k.layernorm) {                           // per-CTA dgamma / dbeta partials, one set per encoder
+      c->ln_nblk = 2 * device_sms();
+      c->ln_part_phi = s.take<float>((size_t)c->ln_nblk * 2 * Wd);
+      c->ln_part_psi = s.take<float>((size_t)c->ln_nblk * 2 * Wd);
     }
     c->phi_outb = s.take<__nv_bfloat16>((size_t)Bl * D);
     c->psi_outb = s.take<__nv_bfloat16>((size_t)Bl * D);
@@ -309,8 +319,12 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
   if (k->layernorm != 0 && k->layernorm != 1) return fail(ctx, CRL_EINVAL, "layernorm must be 0 or 1");
   if (!(k->random_goal_alpha >= 0.f && k->random_goal_alpha <= 1.f))
     return fail(ctx, CRL_EINVAL, "random_goal_alpha must be in [0, 1]");
-  if (k->layernorm && (k->precision != CRL_FP32 || k->width > 2048))
-    return fail(ctx, CRL_EUNSUPPORTED, "LayerNorm encoders run on the fp32 path with width <= 2048");
+  if (k->layernorm && k->precision == CRL_FP32 && k->width > 2048)
+    return fail(ctx, CRL_EUNSUPPORTED, "LayerNorm encoders on the fp32 path need width <= 2048");
+  if (k->layernorm && k->precision == CRL_BF16 &&
+      !(ln_bf16_supports(k->width) && (long long)k->batch_local >= 256))
+    return fail(ctx, CRL_EUNSUPPORTED, "LayerNorm encoders on the bf16 path need width in {256, 512, 768, 1024} "
+                                       "and batch_local >= 256 (CTA-pair GEMMs for every hidden layer)");
   if (k->layernorm && k->actor_depth > 0)
     return fail(ctx, CRL_EUNSUPPORTED, "the actor's frozen-critic pass has no LayerNorm encoders");
   if (k->precision == CRL_BF16 && (k->width % 16 != 0))

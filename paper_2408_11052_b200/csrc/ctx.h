@@ -42,6 +42,11 @@ cudaError_t launch_loss_partial(const float*, const float*, int, int, int, const
                                 const float*, float*, float*, unsigned*, int, float, float, float,
                                 float, float*, int*, int*, int*, cudaStream_t);
 int loss_partial_blocks(int Bl);
+bool ln_bf16_supports(int N);
+cudaError_t launch_ln_fwd_bf16(int, int, const __nv_bfloat16*, const float*, const float*, int, __nv_bfloat16*,
+                               __nv_bfloat16*, float*, float*, cudaStream_t);
+cudaError_t launch_ln_bwd_bf16(int, int, __nv_bfloat16*, const __nv_bfloat16*, const float*, const float*, const float*,
+                               float*, int, float*, float*, int, size_t, cudaStream_t);
 cudaError_t launch_ln_fwd(int, int, const float*, const float*, const float*, int, float*, float*, float*, float*,
                           cudaStream_t);
 cudaError_t launch_ln_bwd(int, int, float*, const float*, const float*, const float*, const float*, float*, float*,
@@ -175,6 +180,9 @@ struct crl_ctx {
   // dZ_l of every hidden layer has its own buffer: db_l is reduced on a side stream, so a
   // ping-pong buffer would be overwritten while the side stream still reads it
   __nv_bfloat16* dzb_phi[CRL_MAX_LAYERS] = {};
+  __nv_bfloat16* phiYb[CRL_MAX_LAYERS] = {}; __nv_bfloat16* psiYb[CRL_MAX_LAYERS] = {};   // LN (bf16): Y = LN(Z)
+  int ln_nblk = 0;
+  float* ln_part_phi = nullptr; float* ln_part_psi = nullptr;            // LN (bf16): dgamma / dbeta partials
   __nv_bfloat16* dzb_psi[CRL_MAX_LAYERS] = {};
   struct TcLayer {
     CUtensorMap fwdA, fwdB, dwA, dwB, dxA, dxB;

@@ -60,9 +60,10 @@ using namespace crl;
 
 static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const __nv_bfloat16* x0, int ld0,
                                      __nv_bfloat16** Xb, __nv_bfloat16** Zb, __nv_bfloat16* dY,
-                                     __nv_bfloat16** dzb, float* Yf, __nv_bfloat16* Yb,
+                                     __nv_bfloat16** dzb, float* Yf, __nv_bfloat16* Yb, __nv_bfloat16** LNb,
                                      std::vector<crl_ctx::TcLayer>& out) {
   const int Bl = ctx->cfg.batch_local, Wd = ctx->cfg.width, L = P.n_layers;
+  const bool ln = ctx->cfg.layernorm != 0;        // F2: hidden Z -> LN (ln.cu) -> act; LNb[l] = LN(Z_l)
   out.assign(L, crl_ctx::TcLayer{});
   for (int l = 0; l < L; ++l) {
     auto& T = out[l];
@@ -87,6 +88,8 @@ static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const _
     // statistic needs the whole representation in one 256-column tile (D <= 256)
     const bool last = l == L - 1;
     T.pg_fwd = tc::tc_pgemm_supported(Bl, o, in) && (!last || o <= 256);
+    if (ln && !last && !T.pg_fwd)
+      return fail(ctx, CRL_EUNSUPPORTED, "bf16 LayerNorm needs the CTA-pair GEMM for every hidden layer");
     if (T.pg_fwd) {
       T.pgf.a = T.fwdA;
       T.pgf.b = T.fwdB;                                                     // W {out, in} box {64, 64}
@@ -101,9 +104,11 @@ static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const _
       T.pgd.a = T.dxA;                                                      // dZ_l {out, B} box {64, 128}
       ok = tc::make_map_bf16(&T.pgd.b, W, o, in, o, 64, 128) &&            // W K-major {out, in}
            tc::make_map_bf16(&T.pgd.out0, T.dzprev, in, Bl, in, 64, 32) &&
-           tc::make_map_bf16(&T.pgd.zin, Zb[l - 1], in, Bl, in, 64, 32);
+           tc::make_map_bf16(&T.pgd.zin, ln ? LNb[l - 1] : Zb[l - 1], in, Bl, in, 64, 32);   // act' at Y (LN) / Z
       if (!ok) return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the CTA-pair GEMM");
     }
+    if (ln && l > 0 && !T.pg_dx)
+      return fail(ctx, CRL_EUNSUPPORTED, "bf16 LayerNorm needs the CTA-pair GEMM for every dX product");
   }
   return CRL_OK;
 }
@@ -111,10 +116,10 @@ static crl_status build_encoder_plan(crl_ctx* ctx, const EncoderPlan& P, const _
 crl_status bf16_prepare(crl_ctx* ctx) {
   const crl_config& k = ctx->cfg;
   crl_status st = build_encoder_plan(ctx, ctx->phi_plan, ctx->x0_phi, ctx->ld0_phi, ctx->phiXb, ctx->phiZb,
-                                     ctx->dphib, ctx->dzb_phi, ctx->phi_out, ctx->phi_outb, ctx->tc_phi);
+                                     ctx->dphib, ctx->dzb_phi, ctx->phi_out, ctx->phi_outb, ctx->phiYb, ctx->tc_phi);
   if (st != CRL_OK) return st;
   st = build_encoder_plan(ctx, ctx->psi_plan, ctx->x0_psi, ctx->ld0_psi, ctx->psiXb, ctx->psiZb, ctx->dpsib,
-                          ctx->dzb_psi, ctx->psi_out, ctx->psi_outb, ctx->tc_psi);
+                          ctx->dzb_psi, ctx->psi_out, ctx->psi_outb, ctx->psiYb, ctx->tc_psi);
   if (st != CRL_OK) return st;
   // grouped weight / bias gradients: X_l and dZ_l of every layer of both encoders
   ctx->use_dwg = !std::getenv("CRL_NO_DWG");
@@ -176,7 +181,7 @@ crl_status bf16_prepare(crl_ctx* ctx) {
                             : std::getenv("CRL_NO_CHAIN") ? false
                             : (k.batch_local >= kChainMinBatch || (cchain_shapes && !cchain_one_wave &&
                                                                    !std::getenv("CRL_CCHAIN")));
-  ctx->use_chain = ctx->tc_logits && chain_wanted && k.depth >= 1 &&
+  ctx->use_chain = ctx->tc_logits && chain_wanted && k.depth >= 1 && !k.layernorm &&
                    tc::tc_chain_supported(k.obs_dim + k.act_dim, k.width, k.repr_dim, k.depth) &&
                    tc::tc_chain_supported(k.goal_dim, k.width, k.repr_dim, k.depth);
   if (ctx->use_chain) {
@@ -242,7 +247,7 @@ crl_status bf16_prepare(crl_ctx* ctx) {
     }
   }
   // cluster-split chains for the small batches the per-row-block chain does not cover
-  ctx->use_cchain = !ctx->use_chain && ctx->tc_logits && !std::getenv("CRL_NO_CCHAIN") &&
+  ctx->use_cchain = !ctx->use_chain && ctx->tc_logits && !std::getenv("CRL_NO_CCHAIN") && !k.layernorm &&
                     (std::getenv("CRL_CCHAIN") || k.batch_local < kChainMinBatch) && cchain_shapes;
   if (ctx->use_cchain) {
     const int Bl = k.batch_local, row_off = k.rank * Bl;
@@ -317,9 +322,17 @@ static crl_status enc_forward_bf16(crl_ctx* ctx, const char* tag, const EncoderP
     const bool last = l == L - 1;
     Stage sg(ctx, st, std::string(tag) + "_fwd_l" + std::to_string(l));
     if (T[l].pg_fwd) {
-      const tc::PgemmArgs pa{Bl, Lp.out, Lp.in, ctx->mem.params + Lp.b_off, k.activation, last ? ystat : nullptr,
-                             k.energy};
+      tc::PgemmArgs pa{Bl, Lp.out, Lp.in, ctx->mem.params + Lp.b_off, k.activation, last ? ystat : nullptr,
+                       k.energy};
+      pa.lin = (k.layernorm && !last) ? 1 : 0;          // LN: Z only, then the LayerNorm kernel
       CU(tc::tc_pgemm(last ? tc::PG_FWD_OUT : tc::PG_FWD_HIDDEN, T[l].pgf, pa, ctx->num_sms, st));
+      if (pa.lin) {
+        const bool phi = Xb == ctx->phiXb;
+        CU(launch_ln_fwd_bf16(Bl, Lp.out, Zb[l], ctx->mem.params + Lp.g_off, ctx->mem.params + Lp.be_off,
+                              k.activation, phi ? ctx->phiYb[l] : ctx->psiYb[l], Xb[l + 1],
+                              phi ? ctx->phiMu[l] : ctx->psiMu[l], phi ? ctx->phiRs[l] : ctx->psiRs[l], st));
+        ++*nl;
+      }
     } else {
       CU(tc::tc_forward(T[l].bn_fwd, T[l].fwdA, T[l].fwdB, Bl, Lp.in, Lp.out, ctx->mem.params + Lp.b_off,
                         last ? nullptr : Zb[l], last ? yb : Xb[l + 1], Lp.out, last ? yf : nullptr, Lp.out,
@@ -360,6 +373,15 @@ static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const Encoder
       if (T[l].pg_dx) {
         const tc::PgemmArgs pa{Bl, Lp.in, Lp.out, nullptr, k.activation, nullptr, k.energy};
         CU(tc::tc_pgemm(tc::PG_DX, T[l].pgd, pa, ctx->num_sms, st));
+        if (k.layernorm) {                              // dY_{l-1} (act' at Y) -> dZ_{l-1}, dgamma, dbeta
+          const LayerPlan& Lq = P.layer[l - 1];
+          const bool phi = Zb == ctx->phiZb;
+          CU(launch_ln_bwd_bf16(Bl, Lq.out, T[l].dzprev, Zb[l - 1], phi ? ctx->phiMu[l - 1] : ctx->psiMu[l - 1],
+                                phi ? ctx->phiRs[l - 1] : ctx->psiRs[l - 1], ctx->mem.params + Lq.g_off,
+                                phi ? ctx->ln_part_phi : ctx->ln_part_psi, ctx->ln_nblk, ctx->grads + Lq.g_off,
+                                ctx->grads + Lq.be_off, ctx->dw_splits, ctx->sizes.n_params, st));
+          *nl += 2;
+        }
       } else {
         CU(tc::tc_backward_dx(T[l].bn_dx, T[l].dxA, T[l].dxB, Bl, Lp.in, Lp.out, Zb[l - 1], T[l].dzprev, Lp.in,
                               k.activation, st));

@@ -291,6 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
               float* z = f + 8 * j;
               sts128(bz + off, make_uint4(pack_bf16x2(z[0], z[1]), pack_bf16x2(z[2], z[3]), pack_bf16x2(z[4], z[5]),
                                           pack_bf16x2(z[6], z[7])));
+              if (p.lin) continue;                         // LayerNorm follows: Z only
               float x[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -308,7 +309,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             __syncwarp();
             if (lane == 0) {
               tma_store_2d(&maps.out0, bz - row_sw, n, mrow0);
-              tma_store_2d(&maps.out1, bx - row_sw, n, mrow0);
+              if (!p.lin) tma_store_2d(&maps.out1, bx - row_sw, n, mrow0);
               bulk_commit();
             }
           } else {                                        // PG_FWD_OUT

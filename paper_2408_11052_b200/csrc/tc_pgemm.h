@@ -24,6 +24,7 @@ struct PgemmArgs {
   float* stat;         // output layer (N <= 256): row statistic of bf16(Y) (L2: |y|^2, cos: 1/|y|)
   int stat_energy;
   int dbg;             // measurement ablations (scratch/pgemm_test.cu); 0 in the library
+  int lin;             // hidden: Z only (LayerNorm follows in its own kernel), no act(Z)
 };
 
 bool tc_pgemm_supported(int M, int N, int K);
