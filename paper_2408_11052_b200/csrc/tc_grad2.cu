@@ -696,6 +696,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
         const int ss = g % NS;
         mbar_wait(&sp_full[ss], (g / NS) & 1);
         tc_fence_after();
+        if (!(p.dbg & 4))
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -717,6 +718,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
         mbar_wait(&dp_full[ds], (g / ND) & 1);
         tc_fence_after();
         const uint32_t w_base = smem_u32(sW + (g & 1) * W_BYTES), b0 = smem_u32(sD + ds * DP_BYTES);
+        if (!(p.dbg & 2))
 #pragma unroll
         for (int ks = 0; ks < BNT / 16; ++ks)            // K = the 128 rows of the tile
           mma_pair(tm_da, smem_desc_sw128(w_base + (ks >> 2) * W_CH + (ks & 3) * 32, 16, 1024),
@@ -837,7 +839,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
         mbar_wait(&st_full[sl], (g >> 1) & 1);
         const float* bst = sStat + sl * STAT_FLOATS;
         uint32_t pk[CW / 2];
-        g2::w_tile<ENERGY, CW>(raw, bst, c0, nval, fac_fast && nval >= BNT, fac_fast, kc, sd.lc + j0, pk, wsum);
+        if (p.dbg & 1) {
+#pragma unroll
+          for (int i = 0; i < CW / 2; ++i) pk[i] = raw[2 * i] ^ raw[2 * i + 1];
+        } else {
+          g2::w_tile<ENERGY, CW>(raw, bst, c0, nval, fac_fast && nval >= BNT, fac_fast, kc, sd.lc + j0, pk, wsum);
+        }
         if (tl) g2::g2_trace(p.trace, g, 6);
         if (g >= 2) mbar_wait(&w_empty[g & 1], ((g >> 1) - 1) & 1);   // dA(g - 2) has read buffer g & 1
         const uint32_t wt = smem_u32(sW + (g & 1) * W_BYTES + (c0 >> 6) * W_CH);   // K-chunk of these columns

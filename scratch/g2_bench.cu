@@ -144,6 +144,19 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms, e0, e1);
     const double us = 1e3 * ms / 10;
     printf("pair grid %d: %8.1f us  %7.1f TFLOP/s (4 GEMM-eq)\n", gp, us, flops / us * 1e-6);
+    for (int v : {1, 2, 4, 3, 5, 6, 7}) {
+      Grad2Args gv = ga;
+      gv.dbg = v;
+      for (int it = 0; it < 2; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, gv, gp, 0);
+      cudaEventRecord(e0);
+      for (int it = 0; it < 5; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, gv, gp, 0);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float m2;
+      cudaEventElapsedTime(&m2, e0, e1);
+      printf("  pair dbg=%d (%s%s%s): %8.1f us\n", v, v & 1 ? "no-math " : "", v & 2 ? "no-dA " : "", v & 4 ? "no-S" : "",
+             1e3 * m2 / 5);
+    }
     {
       unsigned long long* tr;
       cudaMalloc(&tr, 1024 * 8 * 8);
