@@ -48,9 +48,18 @@ constexpr uint32_t kAHalf = 128 * kBK * 2;          // 16 KB: this CTA's 128 row
 constexpr uint32_t kBHalf = 128 * kBK * 2;          // 16 KB: this CTA's 128 columns of B
 constexpr uint32_t kStage = kAHalf + kBHalf;
 constexpr uint32_t kStgBuf = 32 * 128;             // 4 KB: 32 rows x 128 B (SW128) staging
-constexpr int kNStg = 4;                            // staging buffers per epilogue warp
-constexpr size_t kSmem = 1024 + kStages * kStage + 4 * kNStg * kStgBuf + 256;
+#ifndef PG_EPIW
+#define PG_EPIW 4
+#endif
+// epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, every other 64-column
+// chunk each).  Measured on B200 (scratch/pgemm_test.cu, 16384 x 1024 x 1024): 34.3 us with 4,
+// 35.0 with 8 -- the epilogue's cost is its output traffic (Z and act(Z): 64 MB), not warps
+constexpr int kEpiW = PG_EPIW;
+constexpr int kNStg = kEpiW == 8 ? 2 : 4;           // staging buffers per epilogue warp
+constexpr size_t kSmem = 1024 + kStages * kStage + kEpiW * kNStg * kStgBuf + 256;
 
+// number of 64-column chunks c = h, h + nh, ... below nch (a warp's chunks in one tile)
+__host__ __device__ __forceinline__ int ci_count(int nch, int h, int nh) { return nch > h ? (nch - 1 - h) / nh + 1 : 0; }
 __device__ __forceinline__ void tma_load_2d_local(uint32_t dst, const CUtensorMap* map, uint64_t* mbar, int x, int y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -88,20 +97,20 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 }  // namespace pg
 
 template <int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW, 1)
     tc_pgemm_kernel(const __grid_constant__ PgemmMaps maps, const PgemmArgs p) {
   using namespace pg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sStage = smem;
-  uint8_t* sStg = sStage + kStages * kStage;                         // [4 warps][kNStg][4 KB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * kNStg * kStgBuf);
+  uint8_t* sStg = sStage + kStages * kStage;                         // [kEpiW warps][kNStg][4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + kEpiW * kNStg * kStgBuf);
   uint64_t* full = bars;                  // [kStages]  leader: both CTAs' TMA bytes
   uint64_t* empty = full + kStages;        // [kStages]  both: MMA commit (multicast)
   uint64_t* tfull = empty + kStages;       // [2]       both: accumulator ready (multicast)
   uint64_t* tempty = tfull + 2;           // [2]       leader: 8 epilogue warps of the pair
-  uint64_t* zbar = tempty + 2;            // [4][kNStg] DX: Z_prev chunk landed (per warp)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zbar + 4 * kNStg);
+  uint64_t* zbar = tempty + 2;            // [kEpiW][kNStg] DX: Z_prev chunk landed (per warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zbar + kEpiW * kNStg);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -114,8 +123,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     tma_prefetch_desc(&maps.a);
     tma_prefetch_desc(&maps.b);
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
-    for (int i = 0; i < 4 * kNStg; ++i) mbar_init(&zbar[i], 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * kEpiW); }
+    for (int i = 0; i < kEpiW * kNStg; ++i) mbar_init(&zbar[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -192,7 +201,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     // ------------------------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;                               // TMEM lane quarter = 32 rows
     const int ew = warp - 2;                              // staging owner index
+    constexpr int nh = kEpiW / 4;                         // warps per lane quarter
+    const int h = ew / 4;                                 // this warp's chunks: c = h, h + nh, ...
     const uint32_t stg0 = smem_u32(sStg + (size_t)ew * kNStg * kStgBuf);
+    // output layer: the h = 0 warps take every chunk with 3 buffers each, borrowing the staging
+    // of their h = 1 partner (idle there) when kNStg = 2
+    const uint32_t stgX = smem_u32(sStg + (size_t)((ew + 4) % kEpiW) * kNStg * kStgBuf);
+    auto obuf = [&](int i) -> uint32_t { return i < kNStg ? stg0 + i * kStgBuf : stgX + (i - kNStg) * kStgBuf; };
+    const int c_first = EPI == PG_FWD_OUT ? 0 : h, c_step = EPI == PG_FWD_OUT ? 1 : nh;
+    const bool active = EPI != PG_FWD_OUT || h == 0;
     uint64_t* zb = zbar + ew * kNStg;
     const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
     const uint32_t row_sw = (uint32_t)((lane >> 3) * 1024 + (lane & 7) * 128);   // SW128 row base
@@ -204,12 +221,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const int ncol0 = (t % tiles_n) * kTN;
       const int nch = min(kTN, p.N - ncol0) / 64;         // 64-column chunks (N % 64 == 0)
       if (EPI == PG_DX && lane == 0) {
-        // Z_prev chunks for this tile: issued before the accumulator is ready (latency hidden
-        // behind the mainloop); buffer c holds chunk c (nch <= kNStg)
+        // Z_prev chunks of this warp for this tile: issued before the accumulator is ready
+        // (latency hidden behind the mainloop); buffer i holds the warp's i-th chunk
         bulk_wait_read<0>();                              // staging reads of the last tile done
-        for (int c = 0; c < nch; ++c) {
-          mbar_expect_tx(&zb[c], kStgBuf);
-          tma_load_2d_local(stg0 + c * kStgBuf, &maps.zin, &zb[c], ncol0 + 64 * c, mrow0);
+        for (int c = h, i = 0; c < nch; c += nh, ++i) {
+          mbar_expect_tx(&zb[i], kStgBuf);
+          tma_load_2d_local(stg0 + i * kStgBuf, &maps.zin, &zb[i], ncol0 + 64 * c, mrow0);
         }
       }
       if (EPI != PG_DX && lane == 0) bulk_wait_read<0>();  // staging of the previous tile read
@@ -217,19 +234,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       mbar_wait(&tfull[b], (it >> 1) & 1);
       tc_fence_after();
       float ysq = 0.f;
-      if (EPI != PG_DX && (p.dbg & 1)) {                  // ablation: accumulator dropped
+      // a warp without chunks in this tile (or the idle half at the output layer) releases the
+      // accumulator right away: every epilogue warp arrives once per tile
+      const int c_last = !active || c_first >= nch ? -1 : c_first + ((nch - 1 - c_first) / c_step) * c_step;
+      if ((EPI != PG_DX && (p.dbg & 1)) || c_last < 0) {  // (dbg & 1: ablation, accumulator dropped)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) arrive_remote(tempty_leader + 8u * (uint32_t)b);
         continue;
       }
-      for (int c = 0; c < nch; ++c) {
+      for (int c = c_first, ci = 0; c < nch; c += c_step, ++ci) {
         uint32_t v[64];
         const uint32_t ta = tmem + 256u * (uint32_t)b + ((uint32_t)(q * 32) << 16) + 64u * (uint32_t)c;
         tmem_ld32_nowait(ta, *reinterpret_cast<uint32_t(*)[32]>(v));
         tmem_ld32_nowait(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tmem_ld_wait();
-        if (c == nch - 1) {                               // accumulator b free for tile it + 2
+        if (c == c_last) {                                // accumulator b free for tile it + 2
           tc_fence_before();
           __syncwarp();
           if (lane == 0) arrive_remote(tempty_leader + 8u * (uint32_t)b);
@@ -240,8 +260,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         for (int i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]);
         if (EPI == PG_DX) {
           // dZ_prev = acc * act'(Z_prev); Z_prev from the staging buffer, result written back in place
-          mbar_wait(&zb[c], (zphase >> c) & 1);
-          const uint32_t buf = stg0 + c * kStgBuf + row_sw;
+          mbar_wait(&zb[ci], (zphase >> ci) & 1);
+          const uint32_t buf = stg0 + ci * kStgBuf + row_sw;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const uint32_t addr = buf + (uint32_t)(((j ^ (lane & 7))) << 4);
@@ -268,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&maps.out0, stg0 + c * kStgBuf, n, mrow0);
+            tma_store_2d(&maps.out0, stg0 + ci * kStgBuf, n, mrow0);
             bulk_commit();
           }
         } else {
@@ -281,10 +301,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           // buffers: hidden: Z chunk, act(Z) chunk (2 x 4 KB) at (2c) % kNStg and (2c+1) % kNStg;
           // output layer: Y bf16 (4 KB) + Y fp32 (two 32-column SW128 halves, 2 x 4 KB)
           if (EPI == PG_FWD_HIDDEN) {
-            if (lane == 0 && c >= 2) bulk_wait_read<1>();  // the buffers of chunk c - 2 are read
+            // the warp's chunk ci uses buffers (2 ci, 2 ci + 1) mod kNStg: those of chunk
+            // ci - kNStg / 2 must have been read by their TMA stores
+            if (lane == 0 && ci >= kNStg / 2) bulk_wait_read<kNStg / 2 - 1>();
             __syncwarp();
-            const uint32_t bz = stg0 + ((2 * c) % kNStg) * kStgBuf + row_sw;
-            const uint32_t bx = stg0 + ((2 * c + 1) % kNStg) * kStgBuf + row_sw;
+            const uint32_t bz = stg0 + ((2 * ci) % kNStg) * kStgBuf + row_sw;
+            const uint32_t bx = stg0 + ((2 * ci + 1) % kNStg) * kStgBuf + row_sw;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const uint32_t off = (uint32_t)(((j ^ (lane & 7))) << 4);
@@ -315,9 +337,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           } else {                                        // PG_FWD_OUT
             if (lane == 0 && c >= 1) bulk_wait_read<0>();  // chunk c - 1's staging is read
             __syncwarp();
-            const uint32_t by = stg0 + row_sw;                         // bf16 Y
-            const uint32_t bf0 = stg0 + kStgBuf + row_sw;              // fp32 Y columns 0..31
-            const uint32_t bf1 = stg0 + 2 * kStgBuf + row_sw;          // fp32 Y columns 32..63
+            const uint32_t by = obuf(0) + row_sw;                      // bf16 Y
+            const uint32_t bf0 = obuf(1) + row_sw;                     // fp32 Y columns 0..31
+            const uint32_t bf1 = obuf(2) + row_sw;                     // fp32 Y columns 32..63
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const uint32_t off = (uint32_t)(((j ^ (lane & 7))) << 4);
@@ -351,7 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           }
         }
       }
-      if (EPI == PG_DX) zphase ^= (1u << nch) - 1u;
+      if (EPI == PG_DX) zphase ^= (1u << (ci_count(nch, h, nh))) - 1u;
       if (EPI == PG_FWD_OUT && p.stat != nullptr) {
         const int row = mrow0 + lane;
         if (row < p.M)
@@ -388,7 +410,7 @@ static cudaError_t launch_pg(const PgemmMaps& maps, const PgemmArgs& p, int num_
   }
   const int tiles = ((p.M + 255) / 256) * ((p.N + pg::kTN - 1) / pg::kTN);
   const int clusters = std::max(1, std::min(tiles, num_sms / 2));
-  return launch_pdl(tc_pgemm_kernel<EPI>, dim3(2 * clusters), dim3(192), pg::kSmem, st, maps, p);
+  return launch_pdl(tc_pgemm_kernel<EPI>, dim3(2 * clusters), dim3(64 + 32 * pg::kEpiW), pg::kSmem, st, maps, p);
 }
 
 cudaError_t tc_pgemm(int epi, const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
