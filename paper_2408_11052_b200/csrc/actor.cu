@@ -227,7 +227,7 @@ static crl_status enqueue_actor(crl_ctx* ctx, const float* s, const float* g, co
   CU(launch_pdl(actor_loss_sum_kernel, dim3(1), dim3(1024), 0, st, Bl, (const float*)ctx->a_rowloss,
                 (const float*)ctx->a_logpi, ctx->a_loss));
   ++nl;
-  if (W > 1) NC(ncclAllReduce(ctx->a_loss, ctx->a_loss, 2, ncclFloat32, ncclSum, ctx->comm, st));
+  if (ctx->dist) NC(ncclAllReduce(ctx->a_loss, ctx->a_loss, 2, ncclFloat32, ncclSum, ctx->comm, st));
   CU(launch_pdl(actor_loss_finalize_kernel, dim3(1), dim3(1), 0, st, ctx->a_loss, invN, loss_out, ctx->a_skip,
                 ctx->a_t, apply_adam, ctx->status));
   ++nl;
@@ -275,7 +275,7 @@ static crl_status enqueue_actor(crl_ctx* ctx, const float* s, const float* g, co
     CU(launch_reduce_partials(ctx->a_grads, na, ctx->dw_splits, st));
     ++nl;
   }
-  if (W > 1) NC(ncclAllReduce(ctx->a_grads, ctx->a_grads, na, ncclFloat32, ncclSum, ctx->comm, st));
+  if (ctx->dist) NC(ncclAllReduce(ctx->a_grads, ctx->a_grads, na, ncclFloat32, ncclSum, ctx->comm, st));
   if (actor_grads_out)
     CU(cudaMemcpyAsync(actor_grads_out, ctx->a_grads, na * 4, cudaMemcpyDeviceToDevice, st));
   if (apply_adam) {

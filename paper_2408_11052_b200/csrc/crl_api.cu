@@ -82,6 +82,8 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   *buf_bytes = (b.off + 255) & ~(size_t)255;
 
   const int Bl = k.batch_local, W = k.world_size, N = Bl * W, D = k.repr_dim, Wd = k.width;
+  const bool dist = W > 1 || force_dist();
+  c->dist = dist;
   Carver s{scr_base};
   c->dw_splits = dw_splits_for(Bl);
   // wide encoders (configs[4]: 4 x 1024) already have ~200 weight-gradient tiles per K slice:
@@ -148,7 +150,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       // both sides share the SMs (one two-sided statistics launch; the two gradient calls run
       // concurrently): the split count minimises the makespan on half of them each
       c->lg_splits = tc_logits_splits(Bl, N, D, device_sms() / 2);
-      if (W > 1) {
+      if (dist) {
         c->phi_outb_g = s.take<__nv_bfloat16>((size_t)N * D);
         c->psi_outb_g = s.take<__nv_bfloat16>((size_t)N * D);
       } else {
@@ -160,7 +162,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       c->fac_ok = s.take<int>(4);
       c->fac_row = s.take<float>((size_t)Bl + kStatPad);
       c->fac_col = s.take<float>((size_t)Bl + kStatPad);
-      if (W > 1) {
+      if (dist) {
         c->fac_row_g = s.take<float>((size_t)N + kStatPad);
         c->fac_col_g = s.take<float>((size_t)N + kStatPad);
       } else {
@@ -173,7 +175,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       c->lg_part_rs = s.take<float>((size_t)2 * c->lg_splits * Bl);
       c->lg_part_da = s.take<float>((size_t)2 * c->lg_splits * Bl * D);
       c->lg_ticket = s.take<int>((size_t)2 * ((Bl + 127) / 128));
-      c->use_stats = W == 1 && tc_stats_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_STATS");
+      c->use_stats = !dist && tc_stats_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_STATS");
       if (c->use_stats) {
         c->st_splits = tc_stats_splits(Bl, N, device_sms());
         c->st_ldc = N + kStatPad;
@@ -181,7 +183,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
         c->st_colpart = s.take<float>((size_t)((Bl + 127) / 128) * c->st_ldc);
         c->st_bad = s.take<int>(4);
       }
-      c->use_gradf = W == 1 && tc_gradf_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_GRAD");
+      c->use_gradf = !dist && tc_gradf_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_GRAD");
       if (c->use_gradf) {
         c->gf_splits = tc_gradf_splits(Bl, N, device_sms());
         c->gf_part_da = s.take<float>((size_t)c->gf_splits * Bl * D);
@@ -204,7 +206,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   }
   c->phi_out = s.take<float>((size_t)Bl * D);
   c->psi_out = s.take<float>((size_t)Bl * D);
-  if (W > 1) {
+  if (dist) {
     c->phi_g = s.take<float>((size_t)N * D);
     c->psi_g = s.take<float>((size_t)N * D);
   } else {
@@ -214,7 +216,7 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   // padded: the tensor-core logits read column statistics with 1-D bulk copies of whole tiles
   c->lse_row = s.take<float>((size_t)Bl + kStatPad);
   c->lse_col = s.take<float>((size_t)Bl + kStatPad);
-  if (W > 1) {
+  if (dist) {
     c->lse_row_g = s.take<float>((size_t)N + kStatPad);
     c->lse_col_g = s.take<float>((size_t)N + kStatPad);
   } else {
@@ -451,9 +453,13 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
     crl_status bs = bf16_prepare(ctx);
     if (bs != CRL_OK) { std::string m = ctx->err; delete ctx; return fail(nullptr, bs, m); }
   }
-  if (cfg->world_size > 1) {
+  if (ctx->dist) {
     ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
+    if (cfg->world_size > 1) {
+      std::memcpy(&id, nccl_id, sizeof(id));
+    } else if (ncclGetUniqueId(&id) != ncclSuccess) {   // CRL_FORCE_DIST: a one-rank communicator
+      return cleanup(fail(nullptr, CRL_ENCCL, "ncclGetUniqueId failed"));
+    }
     ncclResult_t r = ncclCommInitRank(&ctx->comm, cfg->world_size, id, cfg->rank);
     if (r != ncclSuccess)
       return cleanup(fail(nullptr, CRL_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
@@ -677,7 +683,7 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
                    ctx->phiZ, ctx->phi_out, st, &nl);
   if (rs != CRL_OK) return rs;
   join(ctx, st, st2);
-  if (W > 1) {
+  if (ctx->dist) {
     NC(ncclGroupStart());
     NC(ncclAllGather(ctx->phi_out, ctx->phi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
     NC(ncclAllGather(ctx->psi_out, ctx->psi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
@@ -690,7 +696,7 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
   { Stage sg(ctx, st, "lse_row");
     CU(logits_lse_f32(D, k.energy, ctx->phi_out, Bl, ctx->psi_g, N, ctx->lse_row, st)); ++nl; }
   join(ctx, st, st2);
-  if (W > 1) {
+  if (ctx->dist) {
     NC(ncclGroupStart());
     NC(ncclAllGather(ctx->lse_row, ctx->lse_row_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
     NC(ncclAllGather(ctx->lse_col, ctx->lse_col_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
@@ -731,10 +737,10 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
   }
   { Stage sg(ctx, st, "loss");
     CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,
-                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, W == 1, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip,
+                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, !ctx->dist, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip,
                            ctx->adam_t, ctx->status, st));
     ++nl; }
-  if (W > 1) {
+  if (ctx->dist) {
     NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
     CU(launch_loss_finalize(ctx->loss_acc, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip,
                             ctx->adam_t, ctx->status, st));
@@ -759,7 +765,7 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
   if (rs != CRL_OK) return rs;
   join(ctx, st, st2);
   int adam_splits = ctx->dw_splits;
-  if (W > 1) {
+  if (ctx->dist) {
     if (ctx->dw_splits > 1) {
       Stage sg(ctx, st, "reduce_partials");
       CU(launch_reduce_partials(ctx->grads, ctx->sizes.n_params, ctx->dw_splits, st));

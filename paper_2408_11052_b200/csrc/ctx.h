@@ -1,6 +1,7 @@
 // ctx.h — internal definition of crl_ctx and the host-side helpers shared by the C ABI
 // (crl_api.cu) and the BF16 tensor-core schedule (step_bf16.cu).  Not part of the ABI.
 #pragma once
+#include <cstdlib>
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_cchain.h"
@@ -31,6 +32,7 @@ cudaError_t mlp_backward_dx_f32(int, int, int, const float*, const float*, const
 cudaError_t mlp_backward_dw_f32(int, int, int, const float*, int, const float*, int, int,
                                 const float*, float*, float*, int, size_t, cudaStream_t);
 int dw_splits_for(int Bn);
+inline bool force_dist() { return std::getenv("CRL_FORCE_DIST") != nullptr; }
 void gemm_set_num_sms(int n);
 void logits_set_num_sms(int n);
 cudaError_t launch_reduce_partials(float*, size_t, int, cudaStream_t);
@@ -170,6 +172,10 @@ struct crl_ctx {
   size_t ev_pool_next = 0;
   // ---------------- BF16 tensor-core path (precision == CRL_BF16)
   bool bf16 = false;
+  // the data-parallel code path (collectives, global gather buffers, two-call logits): world_size > 1,
+  // or CRL_FORCE_DIST=1 at world_size 1 (a one-rank NCCL communicator: the multi-GPU
+  // schedule exercised on one GPU, tests/test_gpu_parity.py::test_critic_step_forced_dist_path)
+  bool dist = false;
   __nv_bfloat16* wshadow = nullptr;           // bf16 copy of params (written by Adam)
   __nv_bfloat16 *x0_phi = nullptr, *x0_psi = nullptr;   // [B][ld0_phi], [B][ld0_psi]
   int ld0_phi = 0, ld0_psi = 0;

@@ -484,7 +484,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                                  st));
       CU(tc::launch_rowstat_bf16(ctx->psi_outb, Bl, D, k.energy, ctx->stat_psi + row_off, nullptr, 1, st));
       nl += 2; }
-    if (W > 1) {   // global negatives: gather the bf16 representations and their statistics
+    if (ctx->dist) {   // global negatives: gather the bf16 representations and their statistics
       NC(ncclGroupStart());
       NC(ncclAllGather(ctx->phi_outb, ctx->phi_outb_g, (size_t)Bl * D, ncclBfloat16, ctx->comm, st));
       NC(ncclAllGather(ctx->psi_outb, ctx->psi_outb_g, (size_t)Bl * D, ncclBfloat16, ctx->comm, st));
@@ -562,7 +562,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       ++nl; }
     }
   } else {
-    if (W > 1) {
+    if (ctx->dist) {
       NC(ncclGroupStart());
       NC(ncclAllGather(ctx->phi_out, ctx->phi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
       NC(ncclAllGather(ctx->psi_out, ctx->psi_g, (size_t)Bl * D, ncclFloat32, ctx->comm, st));
@@ -575,7 +575,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(logits_lse_f32(D, k.energy, ctx->phi_out, Bl, ctx->psi_g, N, ctx->lse_row, st)); ++nl; }
     join2(ctx, st, st2);
   }
-  if (W > 1) {
+  if (ctx->dist) {
     NC(ncclGroupStart());
     NC(ncclAllGather(ctx->lse_row, ctx->lse_row_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
     NC(ncclAllGather(ctx->lse_col, ctx->lse_col_g, (size_t)Bl, ncclFloat32, ctx->comm, st));
@@ -594,10 +594,10 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     gl.c_f = lsgn * c_f; gl.c_b = lsgn * c_b; gl.beta = k.beta_lse;
   } else { Stage sg(ctx, st, "loss");
     CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,
-                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, W == 1, invN, lsgn * c_f, lsgn * c_b,
+                           ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, !ctx->dist, invN, lsgn * c_f, lsgn * c_b,
                            k.beta_lse, loss_out, ctx->skip, ctx->adam_t, ctx->status, st));
     ++nl; }
-  if (W > 1) {
+  if (ctx->dist) {
     NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
     CU(launch_loss_finalize(ctx->loss_acc, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip, ctx->adam_t,
                             ctx->status, st));
@@ -715,7 +715,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     cudaStreamWaitEvent(st, ctx->ev_side, 0);
   }
   int adam_splits = ctx->dw_splits;
-  if (W > 1) {
+  if (ctx->dist) {
     if (ctx->dw_splits > 1) {
       Stage sg(ctx, st, "reduce_partials");
       CU(launch_reduce_partials(ctx->grads, ctx->sizes.n_params, ctx->dw_splits, st));

@@ -834,3 +834,22 @@ def test_critic_step_bf16_wide_dw_long_k():
     and the 37-input first layer (one partial M block)."""
     cfg = crl_synth.preset("ant", batch=4160, width=512, repr_dim=64, precision="bf16")
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("preset,prec,batch,extra", [
+    ("ant", "fp32", 300, {}),                       # SIMT logits with gathered Phi / Psi
+    ("ant", "bf16", 1100, {}),                      # tensor-core two-call logits (no one-pass at W > 1)
+    ("ant", "bf16", 600, {"width": 256, "repr_dim": 256}),   # D = 256: tc_grad2p with gathered operands
+])
+def test_critic_step_forced_dist_path(preset, prec, batch, extra, monkeypatch):
+    """The data-parallel schedule on one GPU: CRL_FORCE_DIST=1 runs world_size 1 through the
+    multi-GPU code path -- a one-rank NCCL communicator, separate global gather buffers
+    (Phi_g, Psi_g, LSE_g, factors), all-gathers, the loss all-reduce + finalize kernel, the
+    split-partial reduction + gradient all-reduce before Adam -- against the oracle."""
+    monkeypatch.setenv("CRL_FORCE_DIST", "1")
+    cfg = crl_synth.preset(preset, precision=prec, batch=batch, **extra)
+    tol = BF16_TOL if prec == "bf16" else None
+    if tol is None:
+        _critic_parity(cfg)
+    else:
+        _critic_parity(cfg, tol_loss=tol, tol_grad=tol)
