@@ -175,13 +175,15 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
       c->lg_part_rs = s.take<float>((size_t)2 * c->lg_splits * Bl);
       c->lg_part_da = s.take<float>((size_t)2 * c->lg_splits * Bl * D);
       c->lg_ticket = s.take<int>((size_t)2 * ((Bl + 127) / 128));
-      c->use_stats = !dist && tc_stats_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_STATS");
+      // one-pass statistics also at W > 1: each rank's column partials are all-reduced (C2)
+      c->use_stats = tc_stats_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_STATS");
       if (c->use_stats) {
         c->st_splits = tc_stats_splits(Bl, N, device_sms());
         c->st_ldc = N + kStatPad;
         c->st_part_rs = s.take<float>((size_t)c->st_splits * Bl);
         c->st_colpart = s.take<float>((size_t)((Bl + 127) / 128) * c->st_ldc);
         c->st_bad = s.take<int>(4);
+        if (dist) c->st_colsum = s.take<float>((size_t)N + kStatPad);
       }
       c->use_gradf = !dist && tc_gradf_supports(D, k.energy) && !std::getenv("CRL_NO_FUSED_GRAD");
       if (c->use_gradf) {

@@ -176,6 +176,7 @@ struct crl_ctx {
   // or CRL_FORCE_DIST=1 at world_size 1 (a one-rank NCCL communicator: the multi-GPU
   // schedule exercised on one GPU, tests/test_gpu_parity.py::test_critic_step_forced_dist_path)
   bool dist = false;
+  float* st_colsum = nullptr;                           // W > 1: this rank's column sums of e^l [N]
   __nv_bfloat16* wshadow = nullptr;           // bf16 copy of params (written by Adam)
   __nv_bfloat16 *x0_phi = nullptr, *x0_psi = nullptr;   // [B][ld0_phi], [B][ld0_psi]
   int ld0_phi = 0, ld0_psi = 0;

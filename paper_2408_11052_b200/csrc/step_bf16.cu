@@ -46,7 +46,8 @@ cudaError_t tc_logits_lse(int, int, const CUtensorMap&, const CUtensorMap&, int,
                           int, float*, float*, float*, float*, int*, float, float, const int*, cudaStream_t);
 cudaError_t tc_stats_fused(int, int, const CUtensorMap&, const CUtensorMap&, int, int, const float*, const float*, int,
                            float*, float*, int, float*, float*, float*, float*, int*, int*, float, float, float, float,
-                           cudaGraphConditionalHandle, cudaStream_t);
+                           cudaGraphConditionalHandle, cudaStream_t, float*);
+cudaError_t tc_stats_col_finalize(const float*, int, int, float*, float*, int*, int*, float, float, cudaStream_t);
 cudaError_t tc_logits_grad(int, int, const CUtensorMap&, const CUtensorMap&, int, int, int, const float*,
                            const float*, const float*, const float*, const float*, float, float, float, float,
                            float, int, float*, float*, const __nv_bfloat16*, const __nv_bfloat16*, float*,
@@ -519,8 +520,21 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(tc::tc_stats_fused(D, k.energy, ctx->st_A, ctx->st_B, Bl, N, ctx->stat_phi + row_off, ctx->stat_psi,
                             ctx->st_splits, ctx->st_part_rs, ctx->st_colpart, ctx->st_ldc, ctx->lse_row, ctx->fac_row,
                             ctx->lse_col, ctx->fac_col, ctx->fac_ok, ctx->st_bad, invN * c_f, 2.f * invN * k.beta_lse,
-                            invN * c_b, 0.f, cond, st));
+                            invN * c_b, 0.f, cond, st, ctx->dist ? ctx->st_colsum : nullptr));
       nl += 2;
+      if (ctx->dist) {
+        // C2: the column sums of e^l over every rank's rows; this rank finalises its own columns
+        // (the all-gather below distributes them, as after the two-call path); the fallback
+        // gate must agree across ranks (max)
+        NC(ncclGroupStart());
+        NC(ncclAllReduce(ctx->st_colsum, ctx->st_colsum, (size_t)N, ncclFloat32, ncclSum, ctx->comm, st));
+        NC(ncclAllReduce(ctx->st_bad, ctx->st_bad, 1, ncclInt32, ncclMax, ctx->comm, st));
+        NC(ncclGroupEnd());
+        CU(tc::tc_stats_col_finalize(ctx->st_colsum, row_off, Bl, ctx->lse_col, ctx->fac_col, ctx->fac_ok, ctx->st_bad,
+                                     invN * c_b, 0.f, st));
+        ++nl;
+        NC(ncclAllReduce(ctx->st_bad, ctx->st_bad, 1, ncclInt32, ncclMax, ctx->comm, st));
+      }
       gate = ctx->st_bad;
     }
     if (cond != 0) {

@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(256) stats_merge_kernel(
     const float* __restrict__ part_rs, int S, int Na, const float* __restrict__ colpart, int R, int ldc, int Nb,
     float* __restrict__ lse_row, float* __restrict__ fac_row, float* __restrict__ lse_col, float* __restrict__ fac_col,
     int* __restrict__ fac_ok, int* __restrict__ bad, float rc0, float rc1, float cc0, float cc1, int force_bad,
-    cudaGraphConditionalHandle cond, int nrb) {
+    cudaGraphConditionalHandle cond, int nrb, float* __restrict__ colsum) {
   __shared__ float red[8][33];
   pdl_wait();
   pdl_launch();
@@ -501,8 +501,21 @@ __global__ void __launch_bounds__(256) stats_merge_kernel(
     float u = red[0][c];
 #pragma unroll
     for (int k = 1; k < 8; ++k) u += red[k][c];
-    stats_finalize(u, j, lse_col, fac_col, fac_ok, bad, cc0, cc1, cond);
+    // W > 1: this rank's rows only -> the column-sum all-reduce, then stats_col_finalize
+    if (colsum != nullptr) colsum[j] = u;
+    else stats_finalize(u, j, lse_col, fac_col, fac_ok, bad, cc0, cc1, cond);
   }
+}
+
+// W > 1: column sums over ALL ranks' rows (after the all-reduce) -> LSE' and
+// factors of this rank's columns [col0, col0 + n)
+__global__ void stats_col_finalize_kernel(const float* __restrict__ colsum, int col0, int n, float* __restrict__ lse_col,
+                                          float* __restrict__ fac_col, int* __restrict__ fac_ok, int* __restrict__ bad,
+                                          float cc0, float cc1) {
+  pdl_wait();
+  pdl_launch();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) stats_finalize(colsum[col0 + i], i, lse_col, fac_col, fac_ok, bad, cc0, cc1, 0);
 }
 
 // ------------------------------------------------------------------------------- host side
@@ -545,7 +558,7 @@ cudaError_t tc_stats_fused(int D, int energy, const CUtensorMap& mA, const CUten
                            const float* a_stat, const float* b_stat, int S, float* part_rs, float* colpart, int ldc,
                            float* lse_row, float* fac_row, float* lse_col, float* fac_col, int* fac_ok, int* bad,
                            float rc0, float rc1, float cc0, float cc1, cudaGraphConditionalHandle cond,
-                           cudaStream_t st) {
+                           cudaStream_t st, float* colsum) {
   TcStatsArgs p{};
   p.Na = Na; p.Nb = Nb;
   const int tiles = (Nb + 127) / 128;
@@ -567,7 +580,13 @@ cudaError_t tc_stats_fused(int D, int energy, const CUtensorMap& mA, const CUten
   const int nrb = (Na + 255) / 256, ncb = (Nb + 31) / 32;
   return launch_pdl(stats_merge_kernel, dim3(nrb + ncb), dim3(256), 0, st, (const float*)part_rs, S, Na,
                     (const float*)colpart, R, ldc, Nb, lse_row, fac_row, lse_col, fac_col, fac_ok, bad, rc0, rc1,
-                    cc0, cc1, std::getenv("CRL_FORCE_STATS_FALLBACK") ? 1 : 0, cond, nrb);
+                    cc0, cc1, std::getenv("CRL_FORCE_STATS_FALLBACK") ? 1 : 0, cond, nrb, colsum);
+}
+
+cudaError_t tc_stats_col_finalize(const float* colsum, int col0, int n, float* lse_col, float* fac_col, int* fac_ok,
+                                  int* bad, float cc0, float cc1, cudaStream_t st) {
+  return launch_pdl(stats_col_finalize_kernel, dim3((n + 255) / 256), dim3(256), 0, st, colsum, col0, n, lse_col, fac_col,
+                    fac_ok, bad, cc0, cc1);
 }
 
 }  // namespace tc

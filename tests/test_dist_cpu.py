@@ -3,7 +3,8 @@ uses, checked against the single-process oracle on the global ba
 
 Per rank r (rows [r B_l, (r+1) B_l), envs [r E_l, (r+1) E_l)):
   sample its rows from its own buffer shard -> local Phi_l, Psi_l -> all-gather Phi, Psi
-  LSE_l = row LSE of (Phi_l vs Psi_g), LSE'_l = row LSE of (Psi_l vs Phi_g)  (two-call design)
+  LSE_l = row LSE of (Phi_l vs Psi_g), LSE'_l = row LSE of (Psi_l vs Phi_g)  (two-call design);
+  or (one-pass, L2 / cos) column sums of e^l over the local rows, all-reduced, log   (C2)
   all-gather LSE, LSE'; all-reduce the 3 loss partial sums
   dPhi_l from rows of dL/dl (needs LSE'_g), dPsi_l from the transposed problem (needs LSE_g)
   local encoder backward -> all-reduce (sum) of the gradients
@@ -68,6 +69,11 @@ def _worker(rank, port, cfg, out_q):
         lse_l = losses.lse_rows(l_rows)
         lsec_l = losses.lse_rows(l_cols_T)
         lse_g, lsec_g = _gather_rows(lse_l), _gather_rows(lsec_l)
+        # one-pass statistics at W > 1 (the bounded energies): this rank's
+        # column sums of e^l over its rows for ALL N columns, all-reduced, then log
+        colsum = torch.from_numpy(np.exp(l_rows).sum(0))
+        dist.all_reduce(colsum)
+        lsec_onepass = np.log(colsum.numpy())
         diag = energy.diag_logits(E, Phi_l, Psi_l)
         acc = torch.tensor([np.sum(lse_l - diag), np.sum(lsec_l - diag), np.sum(lse_l ** 2)])
         dist.all_reduce(acc)
@@ -91,7 +97,8 @@ def _worker(rank, port, cfg, out_q):
         obj = [bytes(range(128)) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         out_q.put((rank, dict(L_fwd=L_fwd, L_bwd=L_bwd, P=P, grads=grads.numpy(), idx=idx, s=s, a=a, g=g,
-                              id_ok=obj[0] == bytes(range(128)))))
+                              id_ok=obj[0] == bytes(range(128)), lsec_onepass=lsec_onepass,
+                              lsec_local=lsec_l)))
     finally:
         dist.destroy_process_group()
 
@@ -132,6 +139,13 @@ def test_dp_decomposition_matches_global_oracle(energy_kind):
         assert abs(res[r]["P"] - ref["penalty"]) < 1e-12
         assert np.allclose(res[r]["grads"], ref["grads"], rtol=1e-9, atol=1e-12)
         assert res[r]["id_ok"]
+        # C2: the all-reduced one-pass column statistics equal the two-call column LSEs of this
+        # rank's columns and, for every column, the global oracle's (no running max needed for
+        # L2 / cos: e^l <= e)
+        if energy_kind in ("l2", "cos"):
+            Bl = cfg["batch"] // WORLD
+            assert np.allclose(res[r]["lsec_onepass"][r * Bl:(r + 1) * Bl], res[r]["lsec_local"], rtol=1e-12, atol=1e-12)
+            assert np.allclose(res[r]["lsec_onepass"], ref["lse_col"], rtol=1e-12, atol=1e-12)
 
 
 def test_abi_per_rank_workspace_and_validation():
