@@ -158,6 +158,12 @@ def stage_work(stage, cfg, N, Bl):
         # MUFU ops per logit = 2 for L2 (rsqrt + exp2), 1 for dot / cos (exp2) -- the
         # algorithmic count of SURVEY §8(d) D3 (4 resp. 2 per step over the two passes)
         return Bl * N * (2.0 if cfg["energy"] == "l2" else 1.0), "op", "xu"
+    if stage == "grad_pair":
+        # D = 256 gradient pass (tc_grad2p.cu, both sides in one launch): the algorithmic work is
+        # the two contractions dPhi = W Psi, dPsi = W^T Phi (2 x 2 N_l N D flops) -- the S
+        # recompute the kernel also does is NOT counted -- and 2 MUFU ops per logit (L2); at
+        # D = 256 the tensor term binds
+        return 4.0 * Bl * N * D, "flop", "tensor"
     if stage == "dw_db_grouped":
         # every dW_l = X_l^T dZ_l of both encoders (the bias sums ride on the same tiles)
         tot = 0.0
