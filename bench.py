@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--precision", default="bf16")
     p.add_argument("--energy", default=None)
     p.add_argument("--loss", default=None, help="fwd / bwd / sym / flatnce_* / fb / dpo / ipo / sppo")
-    p.add_argument("--layernorm", action="store_true", help="F2 LayerNorm encoders (fp32 path)")
+    p.add_argument("--layernorm", action="store_true", help="F2 LayerNorm encoders (fp32 path; bf16 at widths 256..1024)")
     p.add_argument("--profile-steps", type=int, default=20)
     p.add_argument("--sample-every", type=int, default=16,
                    help="batches sampled per crl_relabel_sample_bulk launch inside the timed steps "

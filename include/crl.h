@@ -66,7 +66,8 @@ typedef enum {
  * DOT: f = <phi, psi>;  COS: f = <phi,psi>/(||phi|| ||psi||)
  * L1: f = -||phi - psi||_1 (derivative 0 at ties, reading A-33);
  * L2SQ: f = -||phi - psi||_2^2 ("L2 w/o sqrt").  L1 and L2SQ run on
- * the fp32 path (critic and actor); a bf16 context with them is CRL_EUNSUPPORTED. */
+ * the fp32 path (critic and actor); L2SQ also on the bf16 tensor-core path (the same
+ * contraction as L2).  A bf16 context with L1 is CRL_EUNSUPPORTED. */
 typedef enum {
   CRL_LOSS_FWD = 0, CRL_LOSS_BWD = 1, CRL_LOSS_SYM = 2, CRL_LOSS_FLATNCE_FWD = 3, CRL_LOSS_FLATNCE_BWD = 4,
   CRL_LOSS_FB = 5, CRL_LOSS_DPO = 6, CRL_LOSS_IPO = 7, CRL_LOSS_SPPO = 8

@@ -314,8 +314,8 @@ static crl_status validate(const crl_config* k, crl_ctx* ctx) {
   if (k->activation != CRL_ACT_SILU && k->activation != CRL_ACT_RELU)
     return fail(ctx, CRL_EINVAL, "activation");
   if (k->energy < 0 || k->energy > 4) return fail(ctx, CRL_EINVAL, "energy");
-  if (k->precision == CRL_BF16 && k->energy > CRL_ENERGY_COS)
-    return fail(ctx, CRL_EUNSUPPORTED, "L1 / L2SQ energies run on the fp32 path only");
+  if (k->precision == CRL_BF16 && k->energy == CRL_ENERGY_L1)
+    return fail(ctx, CRL_EUNSUPPORTED, "the L1 energy (not a contraction) runs on the fp32 path only");
   if (k->loss < 0 || k->loss > 8) return fail(ctx, CRL_EINVAL, "loss");
   if (k->loss >= CRL_LOSS_FB && (k->precision != CRL_FP32 || k->world_size != 1))
     return fail(ctx, CRL_EUNSUPPORTED, "FB / DPO / IPO / SPPO run on the fp32 path with world_size 1");

@@ -270,7 +270,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(384, 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (wg == 0 && rv && E.out_stat != nullptr) {
           const float st = ysq + sStat[r];
-          E.out_stat[row] = p.energy == CRL_ENERGY_L2 ? st
+          E.out_stat[row] = (p.energy == CRL_ENERGY_L2 || p.energy == CRL_ENERGY_L2SQ) ? st
                             : (p.energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(st), kEpsCos) : 0.f);
         }
         break;

@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(CH_NT, 1) tc_chain_kernel(const __grid_constan
       if (wg == 0 && rv && E.out_stat != nullptr) {
         float st = stat;
         for (int w = 1; w < CH_NWG; ++w) st += sStat[(w - 1) * 128 + r];
-        E.out_stat[row] = p.energy == CRL_ENERGY_L2 ? st
+        E.out_stat[row] = (p.energy == CRL_ENERGY_L2 || p.energy == CRL_ENERGY_L2SQ) ? st
                           : (p.energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(st), kEpsCos) : 0.f);
       }
     }

@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
     // FWD_OUT with the whole output row in this CTA: the logits stage's row statistic
     // (replaces a separate row-statistic launch; same bf16-rounded vector it will read)
     if (EPI == TEPI_FWD_OUT && p.out_stat != nullptr && rv)
-      p.out_stat[row] = p.stat_energy == CRL_ENERGY_L2 ? ysq
+      p.out_stat[row] = (p.stat_energy == CRL_ENERGY_L2 || p.stat_energy == CRL_ENERGY_L2SQ) ? ysq
                         : (p.stat_energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(ysq), kEpsCos) : 0.f);
     if (trace && threadIdx.x == 128) s_tt[5] = gtimer();
   }

@@ -124,14 +124,17 @@ struct RowConst {
     Arow = invN * sd.c_r + 2.f * invN * sd.beta_r * lr_nat;
     cc0 = invN * sd.c_c;
     cc1 = 2.f * invN * sd.beta_c;
-    kL2 = f2_pack(L2e2, L2e2);
-    kM2 = f2_pack(-2.f * L2e2, -2.f * L2e2);
+    // L2: x = d2 (log2 e)^2 (sqrt taken per logit); L2^2: x = d2 log2 e is the log2-unit logit
+    constexpr float kx = ENERGY == CRL_ENERGY_L2SQ ? kLog2e : L2e2;
+    kL2 = f2_pack(kx, kx);
+    kM2 = f2_pack(-2.f * kx, -2.f * kx);
     const float ka = ENERGY == CRL_ENERGY_L2 ? astat * L2e2 : astat * kLog2e;
     kA2 = f2_pack(ka, ka);
     kLr2 = f2_pack(lr2, lr2);
     kLrN2 = f2_pack(-lr2, -lr2);
     kL1 = f2_pack(kLog2e, kLog2e);
-    const float fe = ENERGY == CRL_ENERGY_L2 ? kLog2e : 1.f;   // L2: w = g rs' log2e
+    // L2: w = g rs' log2e;  L2^2: w = 2 g (dl/dphi = -2 (phi - psi))
+    const float fe = ENERGY == CRL_ENERGY_L2 ? kLog2e : (ENERGY == CRL_ENERGY_L2SQ ? 2.f : 1.f);
     kEi2 = f2_pack(Ei * fe, Ei * fe);
     kAr2 = f2_pack(Arow * fe, Arow * fe);
   }
@@ -154,11 +157,13 @@ __device__ __forceinline__ void w_tile(const uint32_t (&raw)[NC], const float* b
                                        uint32_t (&pk)[NC / 2], float& wsum) {
   constexpr int BNT = 128;
   constexpr float kEpsL2e = kEpsL2 * kLog2e * kLog2e;
+  constexpr bool DIFF = ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ;   // row sums of w needed
   if (fast) {
     // full tile, normal factors: packed fp32 pairs (FFMA2 / FMUL2 / FADD2), constants
     // folded into log2 units, column statistics by 16-byte loads; per logit 2 MUFU ops
     //   L2 : x = d2 (log2 e)^2, rs = 1/sqrt(x), s = x rs = r log2 e,
     //        p = 2^-(s + lse2_i), w = p (Ei lcf_j + A_i) log2e rs = g_ij / r_ij
+    //   L2^2: x = d2 log2 e, p = 2^-(x + lse2_i), w = p (Ei lcf_j + A_i) 2 = 2 g_ij
     //   cos: p = 2^(v a_i b_j log2 e - lse2_i), w = p (Ei lcf_j + A_i) b_j
     //   dot: p = 2^(v log2 e - lse2_i),         w = p (Ei lcf_j + A_i)
     f32x2 ws2 = f2_pack(0.f, 0.f);
@@ -184,6 +189,13 @@ __device__ __forceinline__ void w_tile(const uint32_t (&raw)[NC], const float* b
           if (((2 * i4 + h) & 3) < kG2EmuPairs) ex2_pair_fma(-a0, -a1, p0, p1);
           else { p0 = ex2_neg(a0); p1 = ex2_neg(a1); }
           f2_unpack(f2_mul(f2_mul(f2_pack(p0, p1), fct), rs2), w0, w1);
+        } else if (ENERGY == CRL_ENERGY_L2SQ) {
+          float x0, x1, a0, a1;
+          f2_unpack(f2_fma(k.kM2, v2, f2_fma(k.kL2, b2, k.kA2)), x0, x1);
+          f2_unpack(f2_add(f2_pack(fmaxf(x0, 0.f), fmaxf(x1, 0.f)), k.kLr2), a0, a1);
+          if (((2 * i4 + h) & 3) < kG2EmuPairs) ex2_pair_fma(-a0, -a1, p0, p1);
+          else { p0 = ex2_neg(a0); p1 = ex2_neg(a1); }
+          f2_unpack(f2_mul(f2_pack(p0, p1), fct), w0, w1);
         } else if (ENERGY == CRL_ENERGY_COS) {
           float a0, a1;
           f2_unpack(f2_fma(f2_mul(v2, b2), k.kA2, k.kLrN2), a0, a1);
@@ -198,10 +210,10 @@ __device__ __forceinline__ void w_tile(const uint32_t (&raw)[NC], const float* b
           f2_unpack(f2_mul(f2_pack(p0, p1), fct), w0, w1);
         }
         pk[i >> 1] = pack_bf16x2(w0, w1);
-        if (ENERGY == CRL_ENERGY_L2) ws2 = f2_add(ws2, f2_pack(w0, w1));
+        if (DIFF) ws2 = f2_add(ws2, f2_pack(w0, w1));
       }
     }
-    if (ENERGY == CRL_ENERGY_L2) {
+    if (DIFF) {
       float s0, s1;
       f2_unpack(ws2, s0, s1);
       wsum += s0 + s1;
@@ -221,6 +233,8 @@ __device__ __forceinline__ void w_tile(const uint32_t (&raw)[NC], const float* b
           const float d2 = fmaxf(fmaf(-2.f, v, k.astat + bj), 0.f) + kEpsL2;
           rs = rsq(d2);
           l = -d2 * rs;
+        } else if (ENERGY == CRL_ENERGY_L2SQ) {
+          l = -fmaxf(fmaf(-2.f, v, k.astat + bj), 0.f);
         } else if (ENERGY == CRL_ENERGY_COS) {
           l = v * k.astat * bj;
         } else {
@@ -238,10 +252,11 @@ __device__ __forceinline__ void w_tile(const uint32_t (&raw)[NC], const float* b
         }
         float wv;
         if (ENERGY == CRL_ENERGY_L2) wv = gij * rs;
+        else if (ENERGY == CRL_ENERGY_L2SQ) wv = 2.f * gij;
         else if (ENERGY == CRL_ENERGY_COS) wv = gij * bj;
         else wv = gij;
         wv = cv ? wv : 0.f;                               // padded columns: no NaN from pad stats
-        if (ENERGY == CRL_ENERGY_L2) wsum += wv;
+        if (DIFF) wsum += wv;
         wv2[e2] = wv;
       }
       pk[i >> 1] = pack_bf16x2(wv2[0], wv2[1]);
@@ -532,7 +547,8 @@ __global__ void __launch_bounds__(352, 1) tc_grad2_kernel(const __grid_constant_
       // this warpgroup's share of the L2 row sums of the unit ("- (sum_j w_ij) A_i" term of
       // the merge): sub-slot wg of the unit's partial slot
       const int slot = tb == 0 ? 0 : 1;
-      if (ENERGY == CRL_ENERGY_L2 && rv) sd.part_rs[((size_t)(2 * slot + wg)) * p.Na + row] = wsum;
+      if ((ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) && rv)
+        sd.part_rs[((size_t)(2 * slot + wg)) * p.Na + row] = wsum;
       prev_side = side; prev_rb = rb; prev_slot = slot;
       x += nt;
     }
@@ -858,7 +874,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
         if (tl) g2::g2_trace(p.trace, g, 7);
       }
       const int slot = tb == 0 ? 0 : 1;
-      if (ENERGY == CRL_ENERGY_L2 && rv) sd.part_rs[((size_t)(kNWG * slot + wg)) * p.Na + row] = wsum;
+      if ((ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) && rv)
+        sd.part_rs[((size_t)(kNWG * slot + wg)) * p.Na + row] = wsum;
       prev_side = side; prev_rb = rb; prev_slot = slot;
       x += nt;
     }
@@ -948,6 +965,7 @@ cudaError_t tc_grad2p(int energy, const CUtensorMap& mD0, const CUtensorMap& mD1
   p.RB = (p.Na + 255) / 256;                              // row-block PAIRS
   p.TPB = (p.Nb + g2p::BNT - 1) / g2p::BNT;
   if (energy == CRL_ENERGY_L2) return launch_g2p<CRL_ENERGY_L2>(mD0, mD1, mS0, mS1, p, grid, st);
+  if (energy == CRL_ENERGY_L2SQ) return launch_g2p<CRL_ENERGY_L2SQ>(mD0, mD1, mS0, mS1, p, grid, st);
   if (energy == CRL_ENERGY_COS) return launch_g2p<CRL_ENERGY_COS>(mD0, mD1, mS0, mS1, p, grid, st);
   return launch_g2p<CRL_ENERGY_DOT>(mD0, mD1, mS0, mS1, p, grid, st);
 }
@@ -958,6 +976,7 @@ cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1,
   p.RB = (p.Na + 127) / 128;
   p.TPB = (p.Nb + g2::BNT - 1) / g2::BNT;
   if (energy == CRL_ENERGY_L2) return launch_g2<CRL_ENERGY_L2>(mB0, mB1, p, grid, st);
+  if (energy == CRL_ENERGY_L2SQ) return launch_g2<CRL_ENERGY_L2SQ>(mB0, mB1, p, grid, st);
   if (energy == CRL_ENERGY_COS) return launch_g2<CRL_ENERGY_COS>(mB0, mB1, p, grid, st);
   return launch_g2<CRL_ENERGY_DOT>(mB0, mB1, p, grid, st);
 }

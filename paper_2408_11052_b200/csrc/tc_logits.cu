@@ -283,6 +283,8 @@ __device__ __forceinline__ void lg_body(const CUtensorMap& tmA, const CUtensorMa
             const float d2 = fmaxf(fmaf(-2.f, v, astat + bst[jl]), 0.f) + kEpsL2;
             rsv[i] = rsq(d2);
             l = -d2 * rsv[i];
+          } else if (ENERGY == CRL_ENERGY_L2SQ) {           // F3, App. A.2: -|a - b|^2
+            l = -fmaxf(fmaf(-2.f, v, astat + bst[jl]), 0.f);
           } else if (ENERGY == CRL_ENERGY_COS) {
             l = v * astat * bst[jl];
           } else {
@@ -312,10 +314,11 @@ __device__ __forceinline__ void lg_body(const CUtensorMap& tmA, const CUtensorMa
           auto grad_w = [&](int i, float g) {
             float wv;
             if (ENERGY == CRL_ENERGY_L2) wv = g * rsv[i];
+            else if (ENERGY == CRL_ENERGY_L2SQ) wv = 2.f * g;  // dl/dphi = -2 (phi - psi)
             else if (ENERGY == CRL_ENERGY_COS) wv = g * bst[c0 + i];
             else wv = g;
             w[i] = wv;
-            if (ENERGY == CRL_ENERGY_L2) wsum += wv;
+            if (ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) wsum += wv;
           };
           if (fac_fast) {
 #pragma unroll
@@ -369,7 +372,8 @@ __device__ __forceinline__ void lg_body(const CUtensorMap& tmA, const CUtensorMa
         p.part_m[(size_t)split * p.Na + row] = mx;
         p.part_s[(size_t)split * p.Na + row] = st;
       } else {
-        if (ENERGY == CRL_ENERGY_L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[256 + r];
+        if (ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ)
+          p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[256 + r];
       }
     }
     if (GRAD && wg == 0) {
@@ -450,7 +454,9 @@ __global__ void rowstat_bf16_kernel(const __nv_bfloat16* __restrict__ x, int N, 
     s = fmaf(v, v, s);
   }
   s = warp_sum(s);
-  if (lane == 0) out[w] = energy == CRL_ENERGY_L2 ? s : (energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(s), kEpsCos) : 0.f);
+  if (lane == 0)
+    out[w] = (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_L2SQ) ? s
+             : (energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(s), kEpsCos) : 0.f);
 }
 
 __global__ void lse_merge_kernel(const float* __restrict__ pm, const float* __restrict__ ps, int Na, int S,
@@ -536,6 +542,7 @@ static cudaError_t dispatch_lg(int D, int energy, const CUtensorMap& a, const CU
 #define CRL_LG(DD)                                                                     \
   if (D == DD) {                                                                       \
     if (energy == CRL_ENERGY_L2) return launch_lg<DD, CRL_ENERGY_L2, GRAD>(a, b, p, S, st); \
+    if (energy == CRL_ENERGY_L2SQ) return launch_lg<DD, CRL_ENERGY_L2SQ, GRAD>(a, b, p, S, st); \
     if (energy == CRL_ENERGY_DOT) return launch_lg<DD, CRL_ENERGY_DOT, GRAD>(a, b, p, S, st); \
     return launch_lg<DD, CRL_ENERGY_COS, GRAD>(a, b, p, S, st);                         \
   }
@@ -586,6 +593,7 @@ cudaError_t tc_logits_lse_pair(int D, int energy, const LseSide& c0, const LseSi
   if (D == DD) {                                                                                      \
     const size_t sm = LgCfg<DD>::smem(false);                                                          \
     if (energy == CRL_ENERGY_L2) return go(tc_logits_lse2_kernel<DD, CRL_ENERGY_L2>, sm);              \
+    if (energy == CRL_ENERGY_L2SQ) return go(tc_logits_lse2_kernel<DD, CRL_ENERGY_L2SQ>, sm);          \
     if (energy == CRL_ENERGY_DOT) return go(tc_logits_lse2_kernel<DD, CRL_ENERGY_DOT>, sm);            \
     return go(tc_logits_lse2_kernel<DD, CRL_ENERGY_COS>, sm);                                          \
   }
@@ -622,6 +630,7 @@ cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, c
   const GradMergeArgs g{part, prs, A, a_stat, Bg, b_stat, row_offset, Cdiag, Na, D, S, out, outb, 0};
   const dim3 grid((Na * 32 + 255) / 256);
   if (energy == CRL_ENERGY_L2) return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2>, grid, dim3(256), 0, st, g);
+  if (energy == CRL_ENERGY_L2SQ) return launch_pdl(grad_merge_kernel<CRL_ENERGY_L2SQ>, grid, dim3(256), 0, st, g);
   if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g);
   return launch_pdl(grad_merge_kernel<CRL_ENERGY_DOT>, grid, dim3(256), 0, st, g);
 }
@@ -629,6 +638,7 @@ cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, c
 cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st) {
   const dim3 grid((max(g0.Na, g1.Na) * 32 + 255) / 256, 2);
   if (energy == CRL_ENERGY_L2) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_L2>, grid, dim3(256), 0, st, g0, g1);
+  if (energy == CRL_ENERGY_L2SQ) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_L2SQ>, grid, dim3(256), 0, st, g0, g1);
   if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g0, g1);
   return launch_pdl(grad_merge2_kernel<CRL_ENERGY_DOT>, grid, dim3(256), 0, st, g0, g1);
 }

@@ -76,8 +76,9 @@ __device__ __forceinline__ void grad_merge_row_v(const GradMergeArgs& g, int w, 
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] += t[i];
   }
+  constexpr bool DIFF = ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ;   // -(sum_j w_ij) A_i form
   float rs = 0.f;
-  if (ENERGY == CRL_ENERGY_L2)
+  if (DIFF)
     for (int s = 0; s < Sr * g.prs_sub; ++s) rs += g.prs[(size_t)s * Na + w];
   const float Cdiag = g.Cdiag;
   float d2 = 0.f;
@@ -88,6 +89,7 @@ __device__ __forceinline__ void grad_merge_row_v(const GradMergeArgs& g, int w, 
   }
   float diag = 0.f;                                      // energy-chain weight of the delta term
   if (ENERGY == CRL_ENERGY_L2) diag = Cdiag / sqrtf(warp_sum(d2) + kEpsL2);   // times (A_i - B_i)
+  if (ENERGY == CRL_ENERGY_L2SQ) diag = 2.f * Cdiag;                            // L2^2: dl/dA = -2 (A - B)
   const float invb = ENERGY == CRL_ENERGY_COS ? g.b_stat[row_offset + w] : 0.f;
   const float inv = ENERGY == CRL_ENERGY_COS ? g.a_stat[w] : 0.f;
   const float osc = g.pre ? 1.f : inv;                   // the final 1/|A_i| factor
@@ -95,7 +97,7 @@ __device__ __forceinline__ void grad_merge_row_v(const GradMergeArgs& g, int w, 
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     float v = acc[i];
-    if (ENERGY == CRL_ENERGY_L2) v += diag * (av[i] - bv[i]) - rs * av[i];
+    if (DIFF) v += diag * (av[i] - bv[i]) - rs * av[i];
     if (ENERGY == CRL_ENERGY_DOT) v -= Cdiag * bv[i];
     if (ENERGY == CRL_ENERGY_COS) {
       v -= Cdiag * invb * (g.pre ? inv : 1.f) * bv[i];

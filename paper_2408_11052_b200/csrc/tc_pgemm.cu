@@ -377,7 +377,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
       if (EPI == PG_FWD_OUT && p.stat != nullptr) {
         const int row = mrow0 + lane;
         if (row < p.M)
-          p.stat[row] = p.stat_energy == CRL_ENERGY_L2 ? ysq
+          p.stat[row] = (p.stat_energy == CRL_ENERGY_L2 || p.stat_energy == CRL_ENERGY_L2SQ) ? ysq
                         : (p.stat_energy == CRL_ENERGY_COS ? 1.f / fmaxf(sqrtf(ysq), kEpsCos) : 0.f);
       }
     }

@@ -328,10 +328,13 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
       // L2: d2' = (|a|^2 + |b|^2 - 2 a.b) (log2 e)^2, e = 2^-sqrt(d2') (log2 units); rows
       // past the batch get |a|^2 = 1e30 so e = 0.  cos: l2 = a.b (1/|a|)(1/|b|) log2 e + mask
       const float astat = rv ? p.a_stat[row] : fs::kMaskBig;
-      const f32x2 kL2 = f2_pack(L2e2, L2e2);
-      const f32x2 kM2 = ENERGY == CRL_ENERGY_L2 ? f2_pack(-2.f * L2e2, -2.f * L2e2)
-                                                : f2_pack(rv ? 0.f : -fs::kMaskBig, rv ? 0.f : -fs::kMaskBig);
-      const float ka = ENERGY == CRL_ENERGY_L2 ? astat * L2e2 : (rv ? astat * fs::kLog2e : 0.f);
+      // L2^2: x = d2 log2 e is the negated log2-unit logit, e = 2^-max(x, 0)
+      constexpr bool DIFF = ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ;
+      constexpr float kx = ENERGY == CRL_ENERGY_L2SQ ? fs::kLog2e : L2e2;
+      const f32x2 kL2 = f2_pack(kx, kx);
+      const f32x2 kM2 = DIFF ? f2_pack(-2.f * kx, -2.f * kx)
+                             : f2_pack(rv ? 0.f : -fs::kMaskBig, rv ? 0.f : -fs::kMaskBig);
+      const float ka = DIFF ? astat * kx : (rv ? astat * fs::kLog2e : 0.f);
       const f32x2 kA2 = f2_pack(ka, ka);
       f32x2 racc[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
       const int nt = unit_ntiles(u), j00 = unit_j0(u);
@@ -385,6 +388,10 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
                     e[i] = ex2_neg(sqrt_abs(x0));
                     e[i + 1] = ex2_neg(sqrt_abs(x1));
                   }
+                } else if (ENERGY == CRL_ENERGY_L2SQ) {
+                  f2_unpack(f2_fma(kM2, v2, f2_fma(kL2, b2, kA2)), x0, x1);
+                  e[i] = ex2_neg(fmaxf(x0, 0.f));
+                  e[i + 1] = ex2_neg(fmaxf(x1, 0.f));
                 } else {
                   f2_unpack(f2_fma(f2_mul(v2, b2), kA2, kM2), x0, x1);
                   e[i] = fs::ex2(x0);
@@ -520,7 +527,8 @@ __global__ void stats_col_finalize_kernel(const float* __restrict__ colsum, int 
 
 // ------------------------------------------------------------------------------- host side
 bool tc_stats_supports(int D, int energy) {
-  return (D == 64 || D == 128 || D == 256) && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_COS);
+  return (D == 64 || D == 128 || D == 256) &&
+         (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_L2SQ || energy == CRL_ENERGY_COS);
 }
 
 // Column chunks per row block: enough work units to balance the persistent grid (~8 per SM)
@@ -568,12 +576,14 @@ cudaError_t tc_stats_fused(int D, int energy, const CUtensorMap& mA, const CUten
   p.a_stat = a_stat; p.b_stat = b_stat; p.part_rs = part_rs; p.colpart = colpart; p.ldc = ldc;
   p.trace = std::getenv("CRL_STATS_TRACE") ? 1 : 0;
   cudaError_t e;
-  if (D == 64) e = energy == CRL_ENERGY_L2 ? launch_st<64, CRL_ENERGY_L2>(mA, mB, p, st)
-                                           : launch_st<64, CRL_ENERGY_COS>(mA, mB, p, st);
-  else if (D == 128) e = energy == CRL_ENERGY_L2 ? launch_st<128, CRL_ENERGY_L2>(mA, mB, p, st)
-                                                 : launch_st<128, CRL_ENERGY_COS>(mA, mB, p, st);
-  else if (D == 256) e = energy == CRL_ENERGY_L2 ? launch_st<256, CRL_ENERGY_L2>(mA, mB, p, st)
-                                                 : launch_st<256, CRL_ENERGY_COS>(mA, mB, p, st);
+#define CRL_ST_DISPATCH(DD)                                                                                  \
+  e = energy == CRL_ENERGY_L2     ? launch_st<DD, CRL_ENERGY_L2>(mA, mB, p, st)                             \
+      : energy == CRL_ENERGY_L2SQ ? launch_st<DD, CRL_ENERGY_L2SQ>(mA, mB, p, st)                           \
+                                  : launch_st<DD, CRL_ENERGY_COS>(mA, mB, p, st);
+  if (D == 64) { CRL_ST_DISPATCH(64) }
+  else if (D == 128) { CRL_ST_DISPATCH(128) }
+  else if (D == 256) { CRL_ST_DISPATCH(256) }
+#undef CRL_ST_DISPATCH
   else return cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
   const int R = (Na + 127) / 128;

@@ -273,12 +273,36 @@ def test_critic_step_f3_energies_repr256_ant():
     _critic_parity(cfg)
 
 
-@pytest.mark.parametrize("energy", ["l1", "l2sq"])
-def test_f3_energies_bf16_unsupported(energy):
+def test_l1_energy_bf16_unsupported():
+    """L1 is not a contraction (no tensor-core form): a bf16 context with it is refused."""
     from paper_2408_11052_b200 import CrlError
-    cfg = crl_synth.preset("reacher", precision="bf16", batch=64, energy=energy)
+    cfg = crl_synth.preset("reacher", precision="bf16", batch=64, energy="l1")
     with pytest.raises(CrlError):
         make_ctx(cfg)
+
+
+@pytest.mark.parametrize("batch,width,repr_dim,knob", [
+    (256, 128, 64, None),                    # SIMT logits (N < 1024)
+    (1100, 128, 64, None),                   # tensor-core logits, one-pass statistics, two-call gradient
+    (1100, 128, 64, "CRL_NO_FUSED_STATS"),   # two-call online-max statistics
+    (1100, 128, 64, "CRL_FORCE_EXACT_Q"),
+    (1100, 256, 256, None),                  # D = 256: CTA-pair both-sides gradient pass
+    (2900, 256, 256, "CRL_NO_GRAD2P"),       # single-CTA both-sides pass
+    (1100, 256, 256, "CRL_NO_GRAD2"),
+])
+def test_critic_step_bf16_l2sq(batch, width, repr_dim, knob, monkeypatch):
+    """SURVEY 8(f) F3 L2-without-sqrt energy (App. A.2) on the bf16 tensor-core path:
+    l_ij = -max(|a|^2 + |b|^2 - 2 a.b, 0) from the same contraction as L2, w_ij = 2 g_ij."""
+    if knob:
+        monkeypatch.setenv(knob, "1")
+    cfg = crl_synth.preset("ant", batch=batch, width=width, repr_dim=repr_dim, energy="l2sq", precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("loss", ["fwd", "bwd", "sym"])
+def test_critic_step_bf16_l2sq_losses(loss):
+    cfg = crl_synth.preset("ant", batch=1100, width=128, energy="l2sq", loss=loss, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
 
 
 @pytest.mark.parametrize("act", ["silu", "relu"])
