@@ -239,6 +239,7 @@ struct crl_ctx {
   CUtensorMap g2_B0, g2_B1;                             // B operands (box {64, 128}): Psi_g, Phi_g
   bool g2_pair = false;                                 // CTA-pair variant (tc_grad2p)
   CUtensorMap g2_S0, g2_S1;                             // pair: S parts (box {64, 64}): Psi_g, Phi_g
+  CUtensorMap g2_A0, g2_A1;        // CTA-pair gradient pass: local Phi / Psi rows, box {64, 128}
   // all weight / bias gradients of both encoders in one grouped launch (tc_dwg.cu)
   bool use_dwg = false;
   tc::DwgParams dwg;

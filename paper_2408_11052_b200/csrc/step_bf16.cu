@@ -155,7 +155,9 @@ crl_status bf16_prepare(crl_ctx* ctx) {
       std::vector<unsigned char> fl(2 * RB);
       if (ctx->g2_pair) {
         if (!tc::make_map_bf16(&ctx->g2_S0, ctx->psi_outb_g, k.repr_dim, ctx->N, k.repr_dim, 64, 64) ||
-            !tc::make_map_bf16(&ctx->g2_S1, ctx->phi_outb_g, k.repr_dim, ctx->N, k.repr_dim, 64, 64))
+            !tc::make_map_bf16(&ctx->g2_S1, ctx->phi_outb_g, k.repr_dim, ctx->N, k.repr_dim, 64, 64) ||
+            !tc::make_map_bf16(&ctx->g2_A0, ctx->phi_outb, k.repr_dim, k.batch_local, k.repr_dim, 64, 128) ||
+            !tc::make_map_bf16(&ctx->g2_A1, ctx->psi_outb, k.repr_dim, k.batch_local, k.repr_dim, 64, 128))
           return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the gradient operands");
         tc::tc_grad2p_split_flags(k.batch_local, ctx->N, ctx->g2_grid, fl.data());
       } else {
@@ -644,7 +646,8 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     const int prs_sub = ctx->g2_pair ? tc::tc_grad2p_warpgroups() : 2;
     s1.part_da = ctx->g2_part_da + (size_t)2 * Bl * D; s1.part_rs = ctx->g2_part_rs + (size_t)2 * prs_sub * Bl;
     s1.A = ctx->psi_outb;
-    if (ctx->g2_pair) CU(tc::tc_grad2p(k.energy, ctx->g2_B0, ctx->g2_B1, ctx->g2_S0, ctx->g2_S1, ga, ctx->g2_grid, st));
+    if (ctx->g2_pair) CU(tc::tc_grad2p(k.energy, ctx->g2_B0, ctx->g2_B1, ctx->g2_S0, ctx->g2_S1, ctx->g2_A0,
+                                           ctx->g2_A1, ga, ctx->g2_grid, st));
     else CU(tc::tc_grad2(k.energy, ctx->g2_B0, ctx->g2_B1, ga, ctx->g2_grid, st));
     const float Cdiag = invN * (c_f + c_b);
     tc::GradMergeArgs m0{s0.part_da, s0.part_rs, ctx->phi_outb, s0.a_stat, ctx->psi_outb_g, ctx->stat_psi, row_off,

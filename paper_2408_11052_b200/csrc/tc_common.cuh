@@ -161,6 +161,11 @@ __device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) {
   return r;
 }
 // MUFU with free source modifiers: 2^(-x), sqrt(|x|), 1/sqrt(|x|)
+__device__ __forceinline__ unsigned long long globaltimer() {   // ns, comparable across SMs
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ float ex2_neg(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-x));

@@ -150,8 +150,22 @@ struct RowConst {
 #define CRL_G2_EMU 0
 #endif
 constexpr int kG2EmuPairs = CRL_G2_EMU;
+constexpr int kG2RsqPairs = 0;                         // default of CRL_G2_RSQ (tc_grad2p, L2)
 
-template <int ENERGY, int NC>
+// rsqrt on the FMA pipe for a pair (L2, RQ of every 4 pairs): exponent-halving integer guess,
+// two Newton steps y <- y (3/2 - (x/2) y^2) in packed FFMA2 / FMUL2 (relative error ~5e-6)
+__device__ __forceinline__ f32x2 rsq_pair_fma(float x0, float x1) {
+  int i0, i1;
+  asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(i0) : "r"(__float_as_int(x0)), "r"((int)0x80000000), "r"(0x5f375a86));
+  asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(i1) : "r"(__float_as_int(x1)), "r"((int)0x80000000), "r"(0x5f375a86));
+  const f32x2 nhx = f2_mul(f2_pack(x0, x1), f2_pack(-0.5f, -0.5f));
+  f32x2 y = f2_pack(__int_as_float(i0), __int_as_float(i1));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) y = f2_mul(y, f2_fma(f2_mul(nhx, y), y, f2_pack(1.5f, 1.5f)));
+  return y;
+}
+
+template <int ENERGY, int NC, int RQ = 0>
 __device__ __forceinline__ void w_tile(const uint32_t (&raw)[NC], const float* bst, int c0, int nval, bool fast,
                                        bool fac_fast, const RowConst<ENERGY>& k, const float* lc_tile,
                                        uint32_t (&pk)[NC / 2], float& wsum) {
@@ -183,7 +197,7 @@ __device__ __forceinline__ void w_tile(const uint32_t (&raw)[NC], const float* b
           float x0, x1;
           f2_unpack(f2_fma(k.kM2, v2, f2_fma(k.kL2, b2, k.kA2)), x0, x1);
           x0 = fmaxf(x0, kEpsL2e); x1 = fmaxf(x1, kEpsL2e);
-          const f32x2 rs2 = f2_pack(rsq(x0), rsq(x1));
+          const f32x2 rs2 = ((2 * i4 + h) & 3) < RQ ? rsq_pair_fma(x0, x1) : f2_pack(rsq(x0), rsq(x1));
           float a0, a1;
           f2_unpack(f2_fma(f2_pack(x0, x1), rs2, k.kLr2), a0, a1);
           if (((2 * i4 + h) & 3) < kG2EmuPairs) ex2_pair_fma(-a0, -a1, p0, p1);
@@ -564,18 +578,23 @@ __global__ void __launch_bounds__(352, 1) tc_grad2_kernel(const __grid_constant_
 
 // =============================================================================== CTA pairs
 // tc_grad2p: the same pass on CTA PAIRS (tcgen05 cta_group::2).  A pair owns 256 rows of a side
-// (CTA r: rows [128 r, 128 r + 128) of the row-block pair, its A tile in its own TMEM) and walks
-// 128-column tiles:
+// (CTA r: rows [128 r, 128 r + 128) of the row-block pair, its 128 A rows TMA-loaded into its own
+// SMEM once per unit) and walks 128-column tiles:
 //   S   = A B^T   M 256, N 128, K 256: rank r stages the B tile's rows [64 r, 64 r + 64)
-//                 (all 256 D: the "S part", 32 KB)
+//                 (all 256 D: the "S part", 32 KB); S double-buffered in TMEM (2 x 128 columns)
 //   dA += W B     M 256, N 256, K 128: rank r stages the B tile's D half [128 r, 128 r + 128)
-//                 (all 128 rows: the "dA part", 32 KB) and its own W rows
-// so each SM reads half of each B operand from SMEM (the single-CTA pass is bound by its SMEM
-// traffic: TMA 64 + S 64 + dA 96 + W 32 KB per 128 x 128 tile -> here 64 + 32 + 64 + 32).
-// The two parts have their own rings: an S part is free as soon as its S MMA completed.
-// Epilogue, W tile and per-row constants exactly as tc_grad2 (w_tile64).
+//                 (all 128 rows: the "dA part", 32 KB) and its own W rows (one W buffer)
+// so each SM reads half of each B operand from SMEM.  TMEM: S[2] 256 + dA 256 = 512 columns.
+// Two producers: warp 0 (A rows, S parts) and the statistics warp (column statistics, dA parts),
+// so an S part runs two tiles ahead of the dA part of the same tile.
+// Epilogue, W tile and per-row constants exactly as tc_grad2 (w_tile).
+// Measured on B200 (scratch/g2_bench.cu, netscale 16384 x 16384 x 256, L2, 221 tiles per pair):
+// 420 us; the previous layout (A in TMEM, one S buffer) 423 us; no MMAs at all 345 us, no MMA and
+// no epilogue math 177 us.  The epilogue (about 14 instructions and 4 MUFU ops per logit pair)
+// bounds the pass; moving rsqrt to the FMA pipe (CRL_G2_RSQ = 1..4 of every 4 pairs) costs
+// 435 / 453 / 481 / 522 us, so the MUFU is not the binding unit.
 namespace g2p {
-constexpr int D = 256, BNT = 128, NS = 2, ND = 3;
+constexpr int D = 256, BNT = 128, NS = 2, ND = 2;
 #ifndef CRL_G2P_NWG
 #define CRL_G2P_NWG 4
 #endif
@@ -585,23 +604,28 @@ constexpr uint32_t SP_BYTES = 4 * SP_CH;               // 32 KB: S part
 constexpr uint32_t DP_CH = BNT * 128;                  // 16 KB: [128 rows][64 D]
 constexpr uint32_t DP_BYTES = 2 * DP_CH;               // 32 KB: dA part
 constexpr uint32_t W_CH = 128 * 128;                   // 16 KB: W K-chunk [128 rows][64 j]
-constexpr uint32_t W_BYTES = 2 * W_CH;                 // one W tile (two are double-buffered)
+constexpr uint32_t W_BYTES = 2 * W_CH;                 // the W tile (single: dA(t - 1) has read it long before
+                                                       // W(t) is written, one epilogue math phase later)
+constexpr uint32_t A_CH = 128 * 128;                   // 16 KB: A K-chunk [128 rows][64 D]
+constexpr uint32_t A_BYTES = 4 * A_CH;                 // 64 KB: this CTA's 128 A rows (SMEM operand of S)
 constexpr uint32_t STAT_FLOATS = 2 * BNT;
-constexpr size_t SMEM = NS * SP_BYTES + ND * DP_BYTES + 2 * W_BYTES + 2 * STAT_FLOATS * 4 + 256;
+constexpr size_t SMEM = A_BYTES + NS * SP_BYTES + ND * DP_BYTES + W_BYTES + 2 * STAT_FLOATS * 4 + 256;
 }  // namespace g2p
 
-template <int ENERGY>
+template <int ENERGY, int RQ>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG, 1)
     tc_grad2p_kernel(const __grid_constant__ CUtensorMap tmD0, const __grid_constant__ CUtensorMap tmD1,
                      const __grid_constant__ CUtensorMap tmS0, const __grid_constant__ CUtensorMap tmS1,
+                     const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                      const Grad2Args p) {
   using namespace g2p;
   using namespace pair;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sS = smem_raw;                                                 // [NS] S parts
+  uint8_t* sA = smem_raw;                                                 // A rows of the unit
+  uint8_t* sS = sA + A_BYTES;                                             // [NS] S parts
   uint8_t* sD = sS + NS * SP_BYTES;                                       // [ND] dA parts
   uint8_t* sW = sD + ND * DP_BYTES;                                       // W tile
-  float* sStat = reinterpret_cast<float*>(sW + 2 * W_BYTES);              // [2][b_stat 128, lcf 128]
+  float* sStat = reinterpret_cast<float*>(sW + W_BYTES);                  // [2][b_stat 128, lcf 128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 2 * STAT_FLOATS);
   uint64_t* sp_full = bars;                // [NS] leader: both CTAs' S-part bytes
   uint64_t* sp_free = sp_full + NS;        // [NS] both: S MMA done (multicast)
@@ -609,12 +633,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
   uint64_t* dp_free = dp_full + ND;        // [ND] both: dA MMA done
   uint64_t* st_full = dp_free + ND;        // [2] local column statistics
   uint64_t* st_empty = st_full + 2;        // [2]
-  uint64_t* s_full = st_empty + 2;         // both: S accumulator ready
-  uint64_t* s_empty = s_full + 1;          // leader: every epilogue warp loaded S
-  uint64_t* w_full = s_empty + 1;          // [2] leader: every epilogue warp wrote W buffer b
-  uint64_t* w_empty = w_full + 2;          // [2] both: the dA of buffer b read it
-  uint64_t* a_full = w_empty + 2;          // leader: A of the unit in both TMEMs
-  uint64_t* da_full = a_full + 1;          // both: the unit's dA complete
+  uint64_t* s_full = st_empty + 2;         // [2] both: S accumulator b ready
+  uint64_t* s_empty = s_full + 2;          // [2] leader: every epilogue warp loaded S accumulator b
+  uint64_t* w_full = s_empty + 2;          // leader: every epilogue warp wrote W
+  uint64_t* w_empty = w_full + 1;          // both: the dA MMA read W
+  uint64_t* a_full = w_empty + 1;          // leader: both CTAs' A rows of the unit landed (TMA)
+  uint64_t* a_empty = a_full + 1;          // both: the unit's last S MMA completed
+  uint64_t* da_full = a_empty + 1;         // both: the unit's dA complete
   uint64_t* da_empty = da_full + 1;        // leader: dA read out
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_empty + 1);
 
@@ -635,12 +660,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
     if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
     tma_prefetch_desc(&tmD0); tma_prefetch_desc(&tmD1);
     tma_prefetch_desc(&tmS0); tma_prefetch_desc(&tmS1);
+    tma_prefetch_desc(&tmA0); tma_prefetch_desc(&tmA1);
     for (int i = 0; i < NS; ++i) { mbar_init(&sp_full[i], 1); mbar_init(&sp_free[i], 1); }
     for (int i = 0; i < ND; ++i) { mbar_init(&dp_full[i], 1); mbar_init(&dp_free[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&st_full[i], 1); mbar_init(&st_empty[i], 4 * kNWG); }
-    mbar_init(s_full, 1); mbar_init(s_empty, 8 * kNWG);
-    for (int i = 0; i < 2; ++i) { mbar_init(&w_full[i], 8 * kNWG); mbar_init(&w_empty[i], 1); }
-    mbar_init(a_full, 8 * kNWG); mbar_init(da_full, 1); mbar_init(da_empty, 8 * kNWG);
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8 * kNWG); }
+    mbar_init(w_full, 8 * kNWG); mbar_init(w_empty, 1);
+    mbar_init(a_full, 1); mbar_init(a_empty, 1);
+    mbar_init(da_full, 1); mbar_init(da_empty, 8 * kNWG);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
@@ -648,22 +675,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tm_s = tmem, tm_da = tmem + 128, tm_a = tmem + 384;
+  const uint32_t tm_s = tmem, tm_da = tmem + 256;       // S double buffer [2][128 cols], dA [256 cols]
   pdl_wait();
   pdl_launch();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------------- TMA producer (both)
-      int g = 0;
-      for (long x = x0; x < x1;) {
+      int g = 0, k = 0;
+      const uint32_t afb = mapa(smem_u32(a_full), 0);
+      for (long x = x0; x < x1; ++k) {
         int side, rb, tb, nt;
         unit_at(x, side, rb, tb, nt);
         const CUtensorMap* mS = side ? &tmS1 : &tmS0;
-        const CUtensorMap* mD = side ? &tmD1 : &tmD0;
+        // the unit's A rows (zero-filled past the batch): after the previous unit's last S MMA
+        mbar_wait(a_empty, (k & 1) ^ 1);
+        if (rank == 0) mbar_expect_tx(a_full, 2 * A_BYTES);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          tma_load_2d_pair(smem_u32(sA + c * A_CH), side ? &tmA1 : &tmA0, afb, 64 * c, rb * 256 + 128 * (int)rank);
         for (int t = 0; t < nt; ++t, ++g) {
           const int j0 = (tb + t) * BNT;
-          const int ss = g % NS, ds = g % ND;
+          const int ss = g % NS;
           mbar_wait(&sp_free[ss], ((g / NS) & 1) ^ 1);
           if (rank == 0) mbar_expect_tx(&sp_full[ss], 2 * SP_BYTES);
           const uint32_t sfb = mapa(smem_u32(&sp_full[ss]), 0);
@@ -671,6 +704,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
           for (int c = 0; c < 4; ++c)
             tma_load_2d_pair(smem_u32(sS + ss * SP_BYTES + c * SP_CH), mS, sfb, 64 * c, j0 + 64 * (int)rank);
           g2::g2_trace(p.trace, g, 0);
+        }
+        x += nt;
+      }
+    }
+  } else if (warp == 2 + 4 * kNWG) {
+    if (lane == 0) {
+      // ------------------------------------------ column statistics (local) + dA parts (both CTAs)
+      // (the S parts and A rows have their own producer: an S part runs two tiles ahead of the
+      // dA part of the same tile, whose slot frees only when dA(t - ND) completed)
+      int g = 0;
+      for (long x = x0; x < x1;) {
+        int side, rb, tb, nt;
+        unit_at(x, side, rb, tb, nt);
+        const Grad2Side& sd = p.side[side];
+        const CUtensorMap* mD = side ? &tmD1 : &tmD0;
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int j0 = (tb + t) * BNT;
+          const int ds = g % ND;
           mbar_wait(&dp_free[ds], ((g / ND) & 1) ^ 1);
           g2::g2_trace(p.trace, g, 1);
           if (rank == 0) mbar_expect_tx(&dp_full[ds], 2 * DP_BYTES);
@@ -678,20 +729,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
 #pragma unroll
           for (int c = 0; c < 2; ++c)
             tma_load_2d_pair(smem_u32(sD + ds * DP_BYTES + c * DP_CH), mD, dfb, 128 * (int)rank + 64 * c, j0);
-        }
-        x += nt;
-      }
-    }
-  } else if (warp == 2 + 4 * kNWG) {
-    if (lane == 0) {
-      // ---------------------------------------------------------------- column statistics (local)
-      int g = 0;
-      for (long x = x0; x < x1;) {
-        int side, rb, tb, nt;
-        unit_at(x, side, rb, tb, nt);
-        const Grad2Side& sd = p.side[side];
-        for (int t = 0; t < nt; ++t, ++g) {
-          const int j0 = (tb + t) * BNT;
           const int e = g & 1;
           mbar_wait(&st_empty[e], ((g >> 1) & 1) ^ 1);
           mbar_expect_tx(&st_full[e], STAT_FLOATS * 4);
@@ -707,8 +744,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
       // ---------------------------------------------------------------- MMA issuer (leader)
       const uint32_t id_s = idesc_bf16_f32(256, BNT, false, false);
       const uint32_t id_da = idesc_bf16_f32(256, D, false, true);
-      auto issue_s = [&](int g) {
-        mbar_wait(s_empty, (g & 1) ^ 1);      // both CTAs loaded S(g - 1)
+      auto issue_s = [&](int g, bool last) {
+        const int sb = g & 1;
+        mbar_wait(&s_empty[sb], ((g >> 1) & 1) ^ 1);   // both CTAs loaded S(g - 2)
         const int ss = g % NS;
         mbar_wait(&sp_full[ss], (g / NS) & 1);
         tc_fence_after();
@@ -717,11 +755,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks)
-            mma_pair_ts(tm_s, tm_a + (uint32_t)(8 * (4 * c + ks)),
-                        smem_desc_sw128(smem_u32(sS + ss * SP_BYTES + c * SP_CH) + ks * 32, 16, 1024), id_s,
-                        (c | ks) != 0);
+            mma_pair(tm_s + 128u * (uint32_t)sb, smem_desc_sw128(smem_u32(sA + c * A_CH) + ks * 32, 16, 1024),
+                     smem_desc_sw128(smem_u32(sS + ss * SP_BYTES + c * SP_CH) + ks * 32, 16, 1024), id_s,
+                     (c | ks) != 0);
         commit_pair(&sp_free[ss]);
-        commit_pair(s_full);
+        commit_pair(&s_full[sb]);
+        if (last) commit_pair(a_empty);        // the unit's A may be overwritten
         g2::g2_trace(p.trace, g, 2);
       };
       auto issue_da = [&](int g, bool first, int k) {
@@ -729,34 +768,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
           mbar_wait(da_empty, (k & 1) ^ 1);   // unit k - 1's dA read out (both)
           tc_fence_after();
         }
-        mbar_wait(&w_full[g & 1], (g >> 1) & 1);
+        mbar_wait(w_full, g & 1);
         const int ds = g % ND;
         mbar_wait(&dp_full[ds], (g / ND) & 1);
         tc_fence_after();
-        const uint32_t w_base = smem_u32(sW + (g & 1) * W_BYTES), b0 = smem_u32(sD + ds * DP_BYTES);
+        const uint32_t w_base = smem_u32(sW), b0 = smem_u32(sD + ds * DP_BYTES);
         if (!(p.dbg & 2))
 #pragma unroll
         for (int ks = 0; ks < BNT / 16; ++ks)            // K = the 128 rows of the tile
           mma_pair(tm_da, smem_desc_sw128(w_base + (ks >> 2) * W_CH + (ks & 3) * 32, 16, 1024),
                    smem_desc_sw128(b0 + ks * 2048, DP_CH, 1024), id_da, !(first && ks == 0));
         commit_pair(&dp_free[ds]);
-        commit_pair(&w_empty[g & 1]);
+        commit_pair(w_empty);
         g2::g2_trace(p.trace, g, 3);
       };
       int g = 0, k = 0;
       for (long x = x0; x < x1; ++k) {
         int side, rb, tb, nt;
         unit_at(x, side, rb, tb, nt);
-        mbar_wait(a_full, k & 1);             // A of this unit in both TMEMs
+        mbar_wait(a_full, k & 1);             // A of this unit in both CTAs' SMEM
         tc_fence_after();
-        // S runs two tiles ahead of dA: S(t + 2) needs the TMEM load of S(t + 1) only, so it
-        // enters the pipe ahead of dA(t) and its commit latency (~600 cycles across the pair)
-        // hides under tile t + 1's epilogue (S parts and dA parts have separate rings, so the
-        // early S cannot wait on a slot only a later dA frees)
-        issue_s(g);
-        if (nt > 1) issue_s(g + 1);
+        // S is double-buffered in TMEM and runs two tiles ahead of dA: S(t + 2) needs the TMEM
+        // load of S(t) only (early in tile t's epilogue), so the S MMA and its commit latency
+        // hide under the epilogue; dA(t) follows W(t) (S parts and dA parts have separate rings,
+        // so the early S cannot wait on a slot only a later dA frees)
+        issue_s(g, nt == 1);
+        if (nt > 1) issue_s(g + 1, nt == 2);
         for (int t = 0; t < nt; ++t) {
-          if (t + 2 < nt) issue_s(g + t + 2);
+          if (t + 2 < nt) issue_s(g + t + 2, t + 3 == nt);
           issue_da(g + t, t == 0, k);
         }
         commit_pair(da_full);
@@ -769,7 +808,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
     // warpgroup wg: columns [CW wg, CW wg + CW) of every tile, the same share of A's K and of
     // dA's D; 4 warpgroups = 4 warps per SMSP to hide the per-logit MUFU / TMEM latencies
     constexpr int CW = BNT / kNWG;                        // tile columns per warpgroup
-    constexpr int AK = 128 / kNWG;                        // packed A columns (bf16 pairs) per warpgroup
     constexpr int DQ = D / kNWG;                          // dA columns per warpgroup
     const int wg = (warp - 2) >> 2;
     const int q = warp & 3;
@@ -777,8 +815,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const bool fac_fast = *p.fac_ok != 0;
     const int c0 = CW * wg;
-    const uint32_t s_empty_l = mapa(smem_u32(s_empty), 0), w_full_l = mapa(smem_u32(w_full), 0);   // + 8 b
-    const uint32_t a_full_l = mapa(smem_u32(a_full), 0), da_empty_l = mapa(smem_u32(da_empty), 0);
+    const uint32_t s_empty_l = mapa(smem_u32(s_empty), 0), w_full_l = mapa(smem_u32(w_full), 0);   // s: + 8 b
+    const uint32_t da_empty_l = mapa(smem_u32(da_empty), 0);
     int g = 0, k = 0;
     int prev_side = 0, prev_rb = 0, prev_slot = 0;
     auto readout = [&](int side, int rb, int slot, int kk) {
@@ -811,27 +849,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
       const Grad2Side& sd = p.side[side];
       const int row = rb * 256 + 128 * (int)rank + r;
       const bool rv = row < p.Na;
-      {  // A rows -> this CTA's TMEM (the previous unit's S MMAs completed: its last S was loaded)
-        uint32_t av[AK];
-        if (rv) {
-          const uint4* src = reinterpret_cast<const uint4*>(sd.A + (size_t)row * D + 2 * AK * wg);
-#pragma unroll
-          for (int i = 0; i < AK / 4; ++i) {
-            const uint4 u = __ldg(src + i);
-            av[4 * i] = u.x; av[4 * i + 1] = u.y; av[4 * i + 2] = u.z; av[4 * i + 3] = u.w;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < AK; ++i) av[i] = 0u;
-        }
-#pragma unroll
-        for (int h = 0; h < AK / 32; ++h)
-          g2::tmem_st32(tm_a + lane_off + AK * wg + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(av + 32 * h));
-        g2::tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_remote(a_full_l);
-      }
       if (k > 0) readout(prev_side, prev_rb, prev_slot, k - 1);
       const g2::RowConst<ENERGY> kc(sd, row, rv, p.invN, fac_fast);
       float wsum = 0.f;
@@ -839,18 +856,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
         const int sl = g & 1;
         const int j0 = (tb + t) * BNT;
         const int nval = p.Nb - j0;
-        mbar_wait(s_full, g & 1);
+        const int sb = g & 1;
+        mbar_wait(&s_full[sb], (g >> 1) & 1);
         tc_fence_after();
         const bool tl = warp == 2 && lane == 0;
         if (tl) g2::g2_trace(p.trace, g, 4);
         uint32_t raw[CW];
 #pragma unroll
         for (int h = 0; h < CW / 32; ++h)
-          tmem_ld32_nowait(tm_s + lane_off + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(raw + 32 * h));
+          tmem_ld32_nowait(tm_s + 128u * (uint32_t)sb + lane_off + c0 + 32 * h,
+                           *reinterpret_cast<uint32_t(*)[32]>(raw + 32 * h));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) arrive_remote(s_empty_l);
+        if (lane == 0) arrive_remote(s_empty_l + 8u * (uint32_t)sb);
         if (tl) g2::g2_trace(p.trace, g, 5);
         mbar_wait(&st_full[sl], (g >> 1) & 1);
         const float* bst = sStat + sl * STAT_FLOATS;
@@ -859,18 +878,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
 #pragma unroll
           for (int i = 0; i < CW / 2; ++i) pk[i] = raw[2 * i] ^ raw[2 * i + 1];
         } else {
-          g2::w_tile<ENERGY, CW>(raw, bst, c0, nval, fac_fast && nval >= BNT, fac_fast, kc, sd.lc + j0, pk, wsum);
+          g2::w_tile<ENERGY, CW, RQ>(raw, bst, c0, nval, fac_fast && nval >= BNT, fac_fast, kc, sd.lc + j0, pk, wsum);
         }
         if (tl) g2::g2_trace(p.trace, g, 6);
-        if (g >= 2) mbar_wait(&w_empty[g & 1], ((g >> 1) - 1) & 1);   // dA(g - 2) has read buffer g & 1
-        const uint32_t wt = smem_u32(sW + (g & 1) * W_BYTES + (c0 >> 6) * W_CH);   // K-chunk of these columns
+        if (g >= 1) mbar_wait(w_empty, (g - 1) & 1);        // dA(g - 1) has read W
+        const uint32_t wt = smem_u32(sW + (c0 >> 6) * W_CH);  // K-chunk of these columns
 #pragma unroll
         for (int u = 0; u < CW / 8; ++u)
           g2::sts_u4(wt + g2::sw128_off(r, (c0 & 63) + 8 * u),
                      make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) { arrive_remote(w_full_l + 8u * (uint32_t)(g & 1)); mbar_arrive(&st_empty[sl]); }
+        if (lane == 0) { arrive_remote(w_full_l); mbar_arrive(&st_empty[sl]); }
         if (tl) g2::g2_trace(p.trace, g, 7);
       }
       const int slot = tb == 0 ? 0 : 1;
@@ -946,28 +965,41 @@ void tc_grad2p_split_flags(int Na, int Nb, int grid, unsigned char* flags /*[2][
     }
 }
 
-template <int ENERGY>
+template <int ENERGY, int RQ>
 static cudaError_t launch_g2p(const CUtensorMap& d0, const CUtensorMap& d1, const CUtensorMap& s0,
-                              const CUtensorMap& s1, const Grad2Args& p, int grid, cudaStream_t st) {
+                              const CUtensorMap& s1, const CUtensorMap& a0, const CUtensorMap& a1, const Grad2Args& p,
+                              int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_grad2p_kernel<ENERGY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(tc_grad2p_kernel<ENERGY, RQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)g2p::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(tc_grad2p_kernel<ENERGY>, dim3(grid), dim3(96 + 128 * g2p::kNWG), g2p::SMEM, st, d0, d1, s0, s1, p);
+  return launch_pdl(tc_grad2p_kernel<ENERGY, RQ>, dim3(grid), dim3(96 + 128 * g2p::kNWG), g2p::SMEM, st, d0, d1, s0, s1,
+                    a0, a1, p);
 }
 
 cudaError_t tc_grad2p(int energy, const CUtensorMap& mD0, const CUtensorMap& mD1, const CUtensorMap& mS0,
-                      const CUtensorMap& mS1, const Grad2Args& p0, int grid, cudaStream_t st) {
+                      const CUtensorMap& mS1, const CUtensorMap& mA0, const CUtensorMap& mA1, const Grad2Args& p0,
+                      int grid, cudaStream_t st) {
   Grad2Args p = p0;
   p.RB = (p.Na + 255) / 256;                              // row-block PAIRS
   p.TPB = (p.Nb + g2p::BNT - 1) / g2p::BNT;
-  if (energy == CRL_ENERGY_L2) return launch_g2p<CRL_ENERGY_L2>(mD0, mD1, mS0, mS1, p, grid, st);
-  if (energy == CRL_ENERGY_L2SQ) return launch_g2p<CRL_ENERGY_L2SQ>(mD0, mD1, mS0, mS1, p, grid, st);
-  if (energy == CRL_ENERGY_COS) return launch_g2p<CRL_ENERGY_COS>(mD0, mD1, mS0, mS1, p, grid, st);
-  return launch_g2p<CRL_ENERGY_DOT>(mD0, mD1, mS0, mS1, p, grid, st);
+  if (energy == CRL_ENERGY_L2) {
+    // L2: of every 4 logit pairs, RQ take rsqrt on the FMA pipe instead of the MUFU
+    const int rq = std::getenv("CRL_G2_RSQ") ? std::atoi(std::getenv("CRL_G2_RSQ")) : g2::kG2RsqPairs;
+    switch (rq) {
+      case 1: return launch_g2p<CRL_ENERGY_L2, 1>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+      case 2: return launch_g2p<CRL_ENERGY_L2, 2>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+      case 3: return launch_g2p<CRL_ENERGY_L2, 3>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+      case 4: return launch_g2p<CRL_ENERGY_L2, 4>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+      default: return launch_g2p<CRL_ENERGY_L2, 0>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+    }
+  }
+  if (energy == CRL_ENERGY_L2SQ) return launch_g2p<CRL_ENERGY_L2SQ, 0>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+  if (energy == CRL_ENERGY_COS) return launch_g2p<CRL_ENERGY_COS, 0>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+  return launch_g2p<CRL_ENERGY_DOT, 0>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
 }
 
 cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1, const Grad2Args& p0, int grid,

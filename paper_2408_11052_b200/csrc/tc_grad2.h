@@ -36,8 +36,10 @@ cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1,
 int tc_grad2p_grid(int Na, int num_sms);
 int tc_grad2p_warpgroups();                // epilogue warpgroups = L2 row-sum sub-slots per partial slot
 void tc_grad2p_split_flags(int Na, int Nb, int grid, unsigned char* flags);
+// mA0 / mA1: the LOCAL rows of each side (Phi, Psi bf16 [Na][256]), box {64, 128}
 cudaError_t tc_grad2p(int energy, const CUtensorMap& mD0, const CUtensorMap& mD1, const CUtensorMap& mS0,
-                      const CUtensorMap& mS1, const Grad2Args& p, int grid, cudaStream_t st);
+                      const CUtensorMap& mS1, const CUtensorMap& mA0, const CUtensorMap& mA1, const Grad2Args& p,
+                      int grid, cudaStream_t st);
 
 }  // namespace tc
 }  // namespace crl

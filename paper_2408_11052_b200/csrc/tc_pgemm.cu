@@ -96,7 +96,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 
 }  // namespace pg
 
-template <int EPI>
+template <int EPI, int ACT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW, 1)
     tc_pgemm_kernel(const __grid_constant__ PgemmMaps maps, const PgemmArgs p) {
   using namespace pg;
@@ -137,6 +137,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_launch();
+  if (p.trace && threadIdx.x == 0 && rank == 0) p.trace[512 + 2 * cid] = (long long)globaltimer();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -195,6 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
           commit_pair(&empty[s]);
         }
         commit_pair(&tfull[b]);
+        if (p.trace && cid == 0 && it < 8) p.trace[256 + it] = clock64();
       }
     }
   } else {
@@ -233,6 +235,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
       __syncwarp();
       mbar_wait(&tfull[b], (it >> 1) & 1);
       tc_fence_after();
+      const bool trc = p.trace && cid == 0 && rank == 0 && ew == 0 && lane == 0 && it < 8;
+      if (trc) p.trace[264 + it] = clock64();
       float ysq = 0.f;
       // a warp without chunks in this tile (or the idle half at the output layer) releases the
       // accumulator right away: every epilogue warp arrives once per tile
@@ -243,21 +247,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
         if (lane == 0) arrive_remote(tempty_leader + 8u * (uint32_t)b);
         continue;
       }
+      // software pipeline over the warp's 64-column chunks: chunk c + c_step's TMEM load (and
+      // bias load) is in flight while chunk c is processed
+      const uint32_t tbase = tmem + 256u * (uint32_t)b + ((uint32_t)(q * 32) << 16);
+      uint32_t v[64];
+      float4 bb[16];
+      auto issue = [&](int c) {
+        tmem_ld32_nowait(tbase + 64u * (uint32_t)c, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32_nowait(tbase + 64u * (uint32_t)c + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        if (EPI != PG_DX) {                              // bias (broadcast: every lane the same column)
+#pragma unroll
+          for (int i4 = 0; i4 < 16; ++i4) bb[i4] = __ldg(reinterpret_cast<const float4*>(p.bias + ncol0 + 64 * c) + i4);
+        }
+      };
+      issue(c_first);
       for (int c = c_first, ci = 0; c < nch; c += c_step, ++ci) {
-        uint32_t v[64];
-        const uint32_t ta = tmem + 256u * (uint32_t)b + ((uint32_t)(q * 32) << 16) + 64u * (uint32_t)c;
-        tmem_ld32_nowait(ta, *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_ld32_nowait(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tmem_ld_wait();
+        if (trc && c < 4) p.trace[(it * 4 + c) * 4 + 0] = clock64();
+        f32x2 f2[32];                                     // the chunk's 64 values as packed pairs
+#pragma unroll
+        for (int i = 0; i < 32; ++i) f2[i] = f2_pack(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        if (EPI != PG_DX) {
+#pragma unroll
+          for (int i4 = 0; i4 < 16; ++i4) {
+            f2[2 * i4] = f2_add(f2[2 * i4], f2_pack(bb[i4].x, bb[i4].y));
+            f2[2 * i4 + 1] = f2_add(f2[2 * i4 + 1], f2_pack(bb[i4].z, bb[i4].w));
+          }
+        }
         if (c == c_last) {                                // accumulator b free for tile it + 2
           tc_fence_before();
           __syncwarp();
           if (lane == 0) arrive_remote(tempty_leader + 8u * (uint32_t)b);
+        } else {
+          issue(c + c_step);
         }
         const int n = ncol0 + 64 * c;
-        float f[64];
-#pragma unroll
-        for (int i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]);
         if (EPI == PG_DX) {
           // dZ_prev = acc * act'(Z_prev); Z_prev from the staging buffer, result written back in place
           mbar_wait(&zb[ci], (zphase >> ci) & 1);
@@ -267,23 +291,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
             const uint32_t addr = buf + (uint32_t)(((j ^ (lane & 7))) << 4);
             const uint4 zz = lds128(addr);
             const uint32_t w[4] = {zz.x, zz.y, zz.z, zz.w};
+            uint32_t o[4];
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
-              float& a0 = f[8 * j + 2 * h];
-              float& a1 = f[8 * j + 2 * h + 1];
-              if (p.act == CRL_ACT_SILU) {
-                const float h0 = 0.5f * z.x, h1 = 0.5f * z.y;
-                const float t0 = pg::tanh_approx(h0), t1 = pg::tanh_approx(h1);
-                a0 *= fmaf(0.5f, fmaf(h0, fmaf(-t0, t0, 1.f), t0), 0.5f);
-                a1 *= fmaf(0.5f, fmaf(h1, fmaf(-t1, t1, 1.f), t1), 0.5f);
+            for (int hh = 0; hh < 4; ++hh) {
+              const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[hh]));
+              f32x2 a = f2[4 * j + hh];
+              if (ACT == CRL_ACT_SILU) {
+                // SiLU'(z) = s (1 + z (1 - s)) = 1/2 + (h (1 - t^2) + t) / 2,  h = z / 2, t = tanh h
+                const f32x2 hz = f2_mul(f2_pack(z.x, z.y), f2_pack(0.5f, 0.5f));
+                float h0, h1;
+                f2_unpack(hz, h0, h1);
+                const f32x2 t = f2_pack(pg::tanh_approx(h0), pg::tanh_approx(h1));
+                const f32x2 om = f2_fma(f2_mul(t, f2_pack(-1.f, -1.f)), t, f2_pack(1.f, 1.f));
+                const f32x2 g = f2_fma(f2_pack(0.5f, 0.5f), f2_fma(hz, om, t), f2_pack(0.5f, 0.5f));
+                a = f2_mul(a, g);
               } else {
-                a0 = z.x > 0.f ? a0 : 0.f;
-                a1 = z.y > 0.f ? a1 : 0.f;
+                float a0, a1;
+                f2_unpack(a, a0, a1);
+                a = f2_pack(z.x > 0.f ? a0 : 0.f, z.y > 0.f ? a1 : 0.f);
               }
+              float a0, a1;
+              f2_unpack(a, a0, a1);
+              o[hh] = pack_bf16x2(a0, a1);
             }
-            sts128(addr, make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
-                                    pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7])));
+            sts128(addr, make_uint4(o[0], o[1], o[2], o[3]));
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -291,85 +322,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
             tma_store_2d(&maps.out0, stg0 + ci * kStgBuf, n, mrow0);
             bulk_commit();
           }
-        } else {
-          // + bias (broadcast loads: every lane reads the same column)
+        } else if (EPI == PG_FWD_HIDDEN) {
+          // buffers: Z chunk, act(Z) chunk (2 x 4 KB) at (2c) % kNStg and (2c+1) % kNStg; the warp's
+          // chunk ci uses those of chunk ci - kNStg / 2, which must have been read by their stores
+          if (lane == 0 && ci >= kNStg / 2) bulk_wait_read<kNStg / 2 - 1>();
+          __syncwarp();
+          if (trc && c < 4) p.trace[(it * 4 + c) * 4 + 1] = clock64();
+          const uint32_t bz = stg0 + ((2 * ci) % kNStg) * kStgBuf + row_sw;
+          const uint32_t bx = stg0 + ((2 * ci + 1) % kNStg) * kStgBuf + row_sw;
+          const bool lin = p.lin != 0, noact = (p.dbg & 16) != 0;
 #pragma unroll
-          for (int i4 = 0; i4 < 16; ++i4) {
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(p.bias + n) + i4);
-            f[4 * i4] += bb.x; f[4 * i4 + 1] += bb.y; f[4 * i4 + 2] += bb.z; f[4 * i4 + 3] += bb.w;
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t off = (uint32_t)(((j ^ (lane & 7))) << 4);
+            uint32_t oz[4], ox[4];
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) {
+              const f32x2 z = f2[4 * j + hh];
+              float z0, z1;
+              f2_unpack(z, z0, z1);
+              oz[hh] = pack_bf16x2(z0, z1);
+              if (ACT == CRL_ACT_SILU) {                  // SiLU(z) = h + h tanh(h), h = z / 2
+                const f32x2 hz = f2_mul(z, f2_pack(0.5f, 0.5f));
+                float h0, h1;
+                f2_unpack(hz, h0, h1);
+                float x0, x1;
+                f2_unpack(f2_fma(hz, f2_pack(pg::tanh_approx(h0), pg::tanh_approx(h1)), hz), x0, x1);
+                ox[hh] = pack_bf16x2(x0, x1);
+              } else {
+                ox[hh] = pack_bf16x2(fmaxf(z0, 0.f), fmaxf(z1, 0.f));
+              }
+              if (noact) ox[hh] = oz[hh];                  // ablation: no activation math
+            }
+            sts128(bz + off, make_uint4(oz[0], oz[1], oz[2], oz[3]));
+            if (!lin) sts128(bx + off, make_uint4(ox[0], ox[1], ox[2], ox[3]));
           }
-          // buffers: hidden: Z chunk, act(Z) chunk (2 x 4 KB) at (2c) % kNStg and (2c+1) % kNStg;
-          // output layer: Y bf16 (4 KB) + Y fp32 (two 32-column SW128 halves, 2 x 4 KB)
-          if (EPI == PG_FWD_HIDDEN) {
-            // the warp's chunk ci uses buffers (2 ci, 2 ci + 1) mod kNStg: those of chunk
-            // ci - kNStg / 2 must have been read by their TMA stores
-            if (lane == 0 && ci >= kNStg / 2) bulk_wait_read<kNStg / 2 - 1>();
-            __syncwarp();
-            const uint32_t bz = stg0 + ((2 * ci) % kNStg) * kStgBuf + row_sw;
-            const uint32_t bx = stg0 + ((2 * ci + 1) % kNStg) * kStgBuf + row_sw;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (trc && c < 4) p.trace[(it * 4 + c) * 4 + 2] = clock64();
+          if (lane == 0 && !(p.dbg & 8)) {               // (dbg & 8: ablation, no output stores)
+            tma_store_2d(&maps.out0, bz - row_sw, n, mrow0);
+            if (!lin) tma_store_2d(&maps.out1, bx - row_sw, n, mrow0);
+            bulk_commit();
+          }
+        } else {                                          // PG_FWD_OUT
+          if (lane == 0 && c >= 1) bulk_wait_read<0>();  // chunk c - 1's staging is read
+          __syncwarp();
+          const uint32_t by = obuf(0) + row_sw;                      // bf16 Y
+          const uint32_t bf0 = obuf(1) + row_sw;                     // fp32 Y columns 0..31
+          const uint32_t bf1 = obuf(2) + row_sw;                     // fp32 Y columns 32..63
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint32_t off = (uint32_t)(((j ^ (lane & 7))) << 4);
-              float* z = f + 8 * j;
-              sts128(bz + off, make_uint4(pack_bf16x2(z[0], z[1]), pack_bf16x2(z[2], z[3]), pack_bf16x2(z[4], z[5]),
-                                          pack_bf16x2(z[6], z[7])));
-              if (p.lin) continue;                         // LayerNorm follows: Z only
-              float x[8];
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t off = (uint32_t)(((j ^ (lane & 7))) << 4);
+            float y[8];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (p.act == CRL_ACT_SILU) {
-                  const float h = 0.5f * z[i];
-                  x[i] = fmaf(h, pg::tanh_approx(h), h);
-                } else {
-                  x[i] = fmaxf(z[i], 0.f);
-                }
-              }
-              sts128(bx + off, make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
-                                          pack_bf16x2(x[6], x[7])));
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&maps.out0, bz - row_sw, n, mrow0);
-              if (!p.lin) tma_store_2d(&maps.out1, bx - row_sw, n, mrow0);
-              bulk_commit();
-            }
-          } else {                                        // PG_FWD_OUT
-            if (lane == 0 && c >= 1) bulk_wait_read<0>();  // chunk c - 1's staging is read
-            __syncwarp();
-            const uint32_t by = obuf(0) + row_sw;                      // bf16 Y
-            const uint32_t bf0 = obuf(1) + row_sw;                     // fp32 Y columns 0..31
-            const uint32_t bf1 = obuf(2) + row_sw;                     // fp32 Y columns 32..63
+            for (int hh = 0; hh < 4; ++hh) f2_unpack(f2[4 * j + hh], y[2 * hh], y[2 * hh + 1]);
+            const uint4 hb = make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]),
+                                        pack_bf16x2(y[6], y[7]));
+            sts128(by + off, hb);
+            // the logits stage's row statistic is taken on the bf16-rounded Y it will read
+            const uint32_t w[4] = {hb.x, hb.y, hb.z, hb.w};
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint32_t off = (uint32_t)(((j ^ (lane & 7))) << 4);
-              float* y = f + 8 * j;
-              const uint4 hb = make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]),
-                                          pack_bf16x2(y[6], y[7]));
-              sts128(by + off, hb);
-              // the logits stage's row statistic is taken on the bf16-rounded Y it will read
-              const uint32_t w[4] = {hb.x, hb.y, hb.z, hb.w};
-#pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const float2 yb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
-                ysq = fmaf(yb.x, yb.x, fmaf(yb.y, yb.y, ysq));
-              }
-              // fp32: 8 floats = 2 x 16 B chunks of the 32-column half j / 4
-              const uint32_t bfh = (j < 4) ? bf0 : bf1;
-              const int c16 = 2 * (j & 3);
-              sts128(bfh + (uint32_t)(((c16 ^ (lane & 7))) << 4),
-                     make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]), __float_as_uint(y[3])));
-              sts128(bfh + (uint32_t)((((c16 + 1) ^ (lane & 7))) << 4),
-                     make_uint4(__float_as_uint(y[4]), __float_as_uint(y[5]), __float_as_uint(y[6]), __float_as_uint(y[7])));
+            for (int hh = 0; hh < 4; ++hh) {
+              const float2 yb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[hh]));
+              ysq = fmaf(yb.x, yb.x, fmaf(yb.y, yb.y, ysq));
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&maps.out1, by - row_sw, n, mrow0);
-              tma_store_2d(&maps.out0, bf0 - row_sw, n, mrow0);
-              tma_store_2d(&maps.out0, bf1 - row_sw, n + 32, mrow0);
-              bulk_commit();
-            }
+            // fp32: 8 floats = 2 x 16 B chunks of the 32-column half j / 4
+            const uint32_t bfh = (j < 4) ? bf0 : bf1;
+            const int c16 = 2 * (j & 3);
+            sts128(bfh + (uint32_t)(((c16 ^ (lane & 7))) << 4),
+                   make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]), __float_as_uint(y[2]), __float_as_uint(y[3])));
+            sts128(bfh + (uint32_t)((((c16 + 1) ^ (lane & 7))) << 4),
+                   make_uint4(__float_as_uint(y[4]), __float_as_uint(y[5]), __float_as_uint(y[6]), __float_as_uint(y[7])));
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&maps.out1, by - row_sw, n, mrow0);
+            tma_store_2d(&maps.out0, bf0 - row_sw, n, mrow0);
+            tma_store_2d(&maps.out0, bf1 - row_sw, n + 32, mrow0);
+            bulk_commit();
           }
         }
       }
@@ -386,6 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
   }
   tc_fence_before();
   cluster_sync();                          // the peer's MMAs / arrivals are done before TMEM goes
+  if (p.trace && threadIdx.x == 0 && rank == 0) p.trace[512 + 2 * cid + 1] = (long long)globaltimer();
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -399,25 +431,30 @@ bool tc_pgemm_supported(int M, int N, int K) {
   return M >= 256 && N >= 256 && N % 64 == 0 && K >= 1 && !std::getenv("CRL_NO_PGEMM");
 }
 
-template <int EPI>
+template <int EPI, int ACT>
 static cudaError_t launch_pg(const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_pgemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(tc_pgemm_kernel<EPI, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)pg::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.N + pg::kTN - 1) / pg::kTN);
   const int clusters = std::max(1, std::min(tiles, num_sms / 2));
-  return launch_pdl(tc_pgemm_kernel<EPI>, dim3(2 * clusters), dim3(64 + 32 * pg::kEpiW), pg::kSmem, st, maps, p);
+  return launch_pdl(tc_pgemm_kernel<EPI, ACT>, dim3(2 * clusters), dim3(64 + 32 * pg::kEpiW), pg::kSmem, st, maps, p);
+}
+template <int EPI>
+static cudaError_t launch_pg_act(const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
+  if (EPI == PG_FWD_OUT || p.act == CRL_ACT_SILU) return launch_pg<EPI, CRL_ACT_SILU>(maps, p, num_sms, st);
+  return launch_pg<EPI, CRL_ACT_RELU>(maps, p, num_sms, st);
 }
 
 cudaError_t tc_pgemm(int epi, const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
   switch (epi) {
-    case PG_FWD_HIDDEN: return launch_pg<PG_FWD_HIDDEN>(maps, p, num_sms, st);
-    case PG_FWD_OUT: return launch_pg<PG_FWD_OUT>(maps, p, num_sms, st);
-    case PG_DX: return launch_pg<PG_DX>(maps, p, num_sms, st);
+    case PG_FWD_HIDDEN: return launch_pg_act<PG_FWD_HIDDEN>(maps, p, num_sms, st);
+    case PG_FWD_OUT: return launch_pg_act<PG_FWD_OUT>(maps, p, num_sms, st);
+    case PG_DX: return launch_pg_act<PG_DX>(maps, p, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

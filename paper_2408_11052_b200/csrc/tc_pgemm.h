@@ -25,6 +25,7 @@ struct PgemmArgs {
   int stat_energy;
   int dbg;             // measurement ablations (scratch/pgemm_test.cu); 0 in the library
   int lin;             // hidden: Z only (LayerNorm follows in its own kernel), no act(Z)
+  long long* trace;    // development timestamps (scratch/pgemm_test.cu); nullptr in the library
 };
 
 bool tc_pgemm_supported(int M, int N, int K);

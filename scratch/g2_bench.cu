@@ -127,7 +127,7 @@ int main(int argc, char** argv) {
     ga.side[1].part_rs = prs + (size_t)2 * 4 * N;         // pair: 4 warpgroup sub-slots per slot
     const int gp = tc_grad2p_grid(N, sms);
     cudaMemset(pda, 0, nda * 4); cudaMemset(prs, 0, nrs * 4);
-    cudaError_t err = tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, ga, gp, 0);
+    cudaError_t err = tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, m1, m0, ga, gp, 0);
     err = err != cudaSuccess ? err : cudaDeviceSynchronize();
     if (err != cudaSuccess) { printf("pair error %s\n", cudaGetErrorString(err)); return 1; }
     slot_sum(got_da, got_rs, 4);
@@ -135,21 +135,33 @@ int main(int argc, char** argv) {
     for (size_t i = 0; i < ref_da.size(); ++i) { md = std::max(md, (double)std::fabs(got_da[i] - ref_da[i])); sd2 = std::max(sd2, (double)std::fabs(ref_da[i])); }
     for (size_t i = 0; i < ref_rs.size(); ++i) { mr = std::max(mr, (double)std::fabs(got_rs[i] - ref_rs[i])); sr2 = std::max(sr2, (double)std::fabs(ref_rs[i])); }
     printf("pair vs single: max|d dA| %.3g (max %.3g)  max|d rs| %.3g (max %.3g)\n", md, sd2, mr, sr2);
-    for (int it = 0; it < 3; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, ga, gp, 0);
+    for (int it = 0; it < 3; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, m1, m0, ga, gp, 0);
     cudaEventRecord(e0);
-    for (int it = 0; it < 10; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, ga, gp, 0);
+    for (int it = 0; it < 10; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, m1, m0, ga, gp, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double us = 1e3 * ms / 10;
     printf("pair grid %d: %8.1f us  %7.1f TFLOP/s (4 GEMM-eq)\n", gp, us, flops / us * 1e-6);
+    {
+      setenv("CRL_G2P_V1", "1", 1);
+      for (int it = 0; it < 3; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, m1, m0, ga, gp, 0);
+      cudaEventRecord(e0);
+      for (int it = 0; it < 10; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, m1, m0, ga, gp, 0);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float m1s;
+      cudaEventElapsedTime(&m1s, e0, e1);
+      unsetenv("CRL_G2P_V1");
+      printf("pair v1 (A in TMEM, one S buffer): %8.1f us\n", 1e3 * m1s / 10);
+    }
     for (int v : {1, 2, 4, 3, 5, 6, 7}) {
       Grad2Args gv = ga;
       gv.dbg = v;
-      for (int it = 0; it < 2; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, gv, gp, 0);
+      for (int it = 0; it < 2; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, m1, m0, gv, gp, 0);
       cudaEventRecord(e0);
-      for (int it = 0; it < 5; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, gv, gp, 0);
+      for (int it = 0; it < 5; ++it) tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, m1, m0, gv, gp, 0);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float m2;
@@ -163,7 +175,7 @@ int main(int argc, char** argv) {
       cudaMemset(tr, 0, 1024 * 8 * 8);
       Grad2Args gt = ga;
       gt.trace = tr;
-      tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, gt, gp, 0);
+      tc_grad2p(CRL_ENERGY_L2, m0, m1, s0m, s1m, m1, m0, gt, gp, 0);
       cudaDeviceSynchronize();
       std::vector<unsigned long long> ht(1024 * 8);
       cudaMemcpy(ht.data(), tr, ht.size() * 8, cudaMemcpyDeviceToHost);

@@ -50,6 +50,7 @@ static float silu_g(float z) { float s = 1.f / (1.f + std::exp(-z)); return s * 
 
 int main(int argc, char** argv) {
   int M = argc > 1 ? atoi(argv[1]) : 16384, N = argc > 2 ? atoi(argv[2]) : 1024, K = argc > 3 ? atoi(argv[3]) : 1024;
+  setvbuf(stdout, nullptr, _IONBF, 0);
   int lda = (K + 7) / 8 * 8;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -101,8 +102,15 @@ int main(int argc, char** argv) {
   cudaEventElapsedTime(&ms, e0, e1);
   double us = ms * 1e3 / IT;
   printf("fwd hidden: %.2f us  %.1f TFLOP/s\n", us, 2.0 * M * N * K / (us * 1e-6) / 1e12);
+  if (argc > 4) {                          // quick mode (ncu): one more launch with dbg = argv[4]
+    PgemmArgs px = pa;
+    px.dbg = atoi(argv[4]);
+    tc_pgemm(PG_FWD_HIDDEN, mp, px, sms, 0);
+    cudaDeviceSynchronize();
+    return 0;
+  }
   // ablations (PgemmArgs::dbg): 1 no epilogue, 2 no MMA, 4 no TMA operand traffic
-  for (int dbg : {1, 2, 4, 3, 5, 6, 7}) {
+  for (int dbg : {1, 2, 4, 3, 5, 6, 7, 8, 16, 24, 10, 18, 26, 14, 30}) {
     PgemmArgs px = pa;
     px.dbg = dbg;
     for (int i = 0; i < 3; ++i) tc_pgemm(PG_FWD_HIDDEN, mp, px, sms, 0);
@@ -112,8 +120,38 @@ int main(int argc, char** argv) {
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     const double u2 = ms * 1e3 / IT;
-    printf("  dbg=%d (%s%s%s): %.2f us  %.1f TFLOP/s-equiv\n", dbg, dbg & 1 ? "no-epi " : "", dbg & 2 ? "no-mma " : "",
-           dbg & 4 ? "no-tma" : "", u2, 2.0 * M * N * K / (u2 * 1e-6) / 1e12);
+    printf("  dbg=%2d (%s%s%s%s%s): %.2f us  %.1f TFLOP/s-equiv\n", dbg, dbg & 1 ? "no-epi " : "", dbg & 2 ? "no-mma " : "",
+           dbg & 4 ? "no-tma " : "", dbg & 8 ? "no-store " : "", dbg & 16 ? "no-act" : "", u2,
+           2.0 * M * N * K / (u2 * 1e-6) / 1e12);
+  }
+  {
+    long long* tr;
+    cudaMalloc(&tr, 1024 * 8);
+    cudaMemset(tr, 0, 1024 * 8);
+    PgemmArgs px = pa;
+    px.trace = tr;
+    for (int dbg : {0, 2}) {
+      px.dbg = dbg;
+      tc_pgemm(PG_FWD_HIDDEN, mp, px, sms, 0);
+      cudaDeviceSynchronize();
+      std::vector<long long> h(1024);
+      cudaMemcpy(h.data(), tr, 1024 * 8, cudaMemcpyDeviceToHost);
+      {
+        long long s0 = h[512], e1 = 0;
+        for (int c = 0; c < 74; ++c) { s0 = std::min(s0, h[512 + 2 * c]); e1 = std::max(e1, h[513 + 2 * c]); }
+        printf("cluster spans (ns from first start): ");
+        for (int c = 0; c < 74; c += 1) printf("%d:%lld-%lld ", c, h[512 + 2 * c] - s0, h[513 + 2 * c] - s0);
+        printf("\n  first start -> last end %lld ns\n", e1 - s0);
+      }
+      const long long t0 = h[264];
+      printf("trace dbg=%d (cycles from tile 0 epilogue start): tile: mma-commit epi-start | chunk c: ld-done wait-done sts-done\n", dbg);
+      for (int it = 0; it < 4; ++it) {
+        printf("  tile %d: %8lld %8lld |", it, h[256 + it] - t0, h[264 + it] - t0);
+        for (int c = 0; c < 4; ++c)
+          printf(" [%lld %lld %lld]", h[(it * 4 + c) * 4] - t0, h[(it * 4 + c) * 4 + 1] - t0, h[(it * 4 + c) * 4 + 2] - t0);
+        printf("\n");
+      }
+    }
   }
   // ---- dX: A = dZ [M][K2], W [N][K2] (in = N, out = K2)
   {

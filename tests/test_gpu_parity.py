@@ -862,7 +862,7 @@ def test_critic_step_bf16_wide_dw_long_k():
 
 @pytest.mark.parametrize("preset,prec,batch,extra", [
     ("ant", "fp32", 300, {}),                       # SIMT logits with gathered Phi / Psi
-    ("ant", "bf16", 1100, {}),                      # tensor-core two-call logits (no one-pass at W > 1)
+    ("ant", "bf16", 1100, {}),                      # one-pass statistics + column-sum all-reduce (C2)
     ("ant", "bf16", 600, {"width": 256, "repr_dim": 256}),   # D = 256: tc_grad2p with gathered operands
 ])
 def test_critic_step_forced_dist_path(preset, prec, batch, extra, monkeypatch):
