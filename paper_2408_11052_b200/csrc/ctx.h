@@ -7,6 +7,7 @@
 #include "tc_cchain.h"
 #include "tc_chain.h"
 #include "tc_dwg.h"
+#include "tc_pdw.h"
 #include "tc_pgemm.h"
 #include "tc_grad2.h"
 
@@ -243,6 +244,8 @@ struct crl_ctx {
   // all weight / bias gradients of both encoders in one grouped launch (tc_dwg.cu)
   bool use_dwg = false;
   tc::DwgParams dwg;
+  bool use_pdw = false;            // wide encoders: dW / db on CTA pairs (tc_pdw.cu) instead of tc_dwg
+  tc::PdwParams pdw;
   // cluster-split MLP chains for small batches (tc_cchain.cu): one launch per direction
   bool use_cchain = false;
   tc::CChainMaps cchain_fwd[2], cchain_bwd[2];

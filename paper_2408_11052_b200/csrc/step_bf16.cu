@@ -123,7 +123,26 @@ crl_status bf16_prepare(crl_ctx* ctx) {
                           ctx->dzb_psi, ctx->psi_out, ctx->psi_outb, ctx->psiYb, ctx->tc_psi);
   if (st != CRL_OK) return st;
   // grouped weight / bias gradients: X_l and dZ_l of every layer of both encoders
-  ctx->use_dwg = !std::getenv("CRL_NO_DWG");
+  // wide encoders (configs[4]: width 1024): every dW / db on CTA pairs, 256 x 256 tiles
+  ctx->use_pdw = k.width >= 512 && tc::pdw_supported(k.batch_local, ctx->dw_splits);
+  if (ctx->use_pdw) {
+    tc::pdw_init(ctx->pdw, k.batch_local, ctx->dw_splits, ctx->sizes.n_params);
+    const EncoderPlan* plans[2] = {&ctx->phi_plan, &ctx->psi_plan};
+    std::vector<crl_ctx::TcLayer>* tcs[2] = {&ctx->tc_phi, &ctx->tc_psi};
+    __nv_bfloat16** Xb[2] = {ctx->phiXb, ctx->psiXb};
+    const __nv_bfloat16* x0[2] = {ctx->x0_phi, ctx->x0_psi};
+    const int ld0[2] = {ctx->ld0_phi, ctx->ld0_psi};
+    for (int e = 0; e < 2 && ctx->use_pdw; ++e)
+      for (int l = 0; l < plans[e]->n_layers; ++l) {
+        const LayerPlan& Lp = plans[e]->layer[l];
+        if (!tc::pdw_add_problem(ctx->pdw, l == 0 ? x0[e] : Xb[e][l], l == 0 ? ld0[e] : k.width, (*tcs[e])[l].dz,
+                                 Lp.in, Lp.out, ctx->grads + Lp.w_off, ctx->grads + Lp.b_off)) {
+          ctx->use_pdw = false;                 // (alignment / table size): the grouped kernel
+          break;
+        }
+      }
+  }
+  ctx->use_dwg = !ctx->use_pdw && !std::getenv("CRL_NO_DWG");
   if (ctx->use_dwg) {
     tc::dwg_init(ctx->dwg, k.batch_local, ctx->dw_splits, ctx->sizes.n_params);
     const EncoderPlan* plans[2] = {&ctx->phi_plan, &ctx->psi_plan};
@@ -355,17 +374,17 @@ static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const Encoder
     const LayerPlan& Lp = P.layer[l];
     // dW_l and db_l only feed Adam: they run on a side stream, off the dX critical path
     // (or all at once in the grouped kernel after both dX chains: ctx->use_dwg)
-    if (side != st && !ctx->use_dwg) {
+    if (side != st && !ctx->use_dwg && !ctx->use_pdw) {
       cudaEventRecord(ctx->ev_side, st);
       cudaStreamWaitEvent(side, ctx->ev_side, 0);
     }
-    if (!ctx->use_dwg) {
+    if (!ctx->use_dwg && !ctx->use_pdw) {
       Stage sg(ctx, side, std::string(tag) + "_bwd_dw_l" + std::to_string(l));
       CU(tc::tc_backward_dw(T[l].bn_dw, T[l].dwA, T[l].dwB, Bl, Lp.in, Lp.out, ctx->grads + Lp.w_off,
                             ctx->dw_splits, ctx->sizes.n_params, side));
       ++*nl;
     }
-    if (!ctx->use_dwg) {
+    if (!ctx->use_dwg && !ctx->use_pdw) {
       Stage sg(ctx, side, std::string(tag) + "_bwd_db_l" + std::to_string(l));
       CU(tc::launch_colsum_bf16(T[l].dz, Bl, Lp.out, Lp.out, ctx->grads + Lp.b_off, ctx->dw_splits,
                                 ctx->sizes.n_params, side));
@@ -709,7 +728,12 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(tc::tc_cchain_backward(ctx->cchain_bwd[0], ctx->cchain_bwd[1], ctx->cchain_bwd_p, st));
       ++nl; }
   }
-  if (ctx->use_dwg) {
+  if (ctx->use_pdw) {
+    // every dW_l and db_l of both encoders on CTA pairs (tc_pdw.cu)
+    Stage sg(ctx, st, "dw_db_pairs");
+    CU(tc::tc_pdw_launch(ctx->pdw, ctx->num_sms, st));
+    ++nl;
+  } else if (ctx->use_dwg) {
     // every dW_l and db_l of both encoders in one grouped launch (tc_dwg.cu)
     Stage sg(ctx, st, "dw_db_grouped");
     CU(tc::tc_dwg_launch(ctx->dwg, st));
@@ -725,7 +749,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     rs = enc_weight_grads_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, side2, &nl);
     if (rs != CRL_OK) return rs;
   }
-  if (side != st && !ctx->use_dwg) {
+  if (side != st && !ctx->use_dwg && !ctx->use_pdw) {
     cudaEventRecord(ctx->ev_side, side);
     cudaStreamWaitEvent(st, ctx->ev_side, 0);
     cudaEventRecord(ctx->ev_side, side2);

@@ -1,0 +1,38 @@
+// tc_pdw.h — weight / bias gradients of the wide encoders on CTA pairs (tc_pdw.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace crl {
+namespace tc {
+
+constexpr int kPdwMaxProblems = 16;
+
+struct alignas(64) PdwProblem {
+  CUtensorMap a;           // X_l  [K][ldx] bf16, box {64, 64}: the MN-major A operand (M = in)
+  CUtensorMap b;           // dZ_l [K][N]   bf16, box {64, 64}: the MN-major B operand
+  CUtensorMap out;         // dW_l partial slices fp32 [S][M][N], box {32, 32, 1} (TMA stores)
+  float* db;               // db_l slice 0 ([N]; slice s at + s * split_stride)
+  int M, N;                // dW_l is [M = in][N = out]
+  int tiles_n, tiles;      // 256 x 256 tiles per slice along N; work items = tiles_m * tiles_n * S
+};
+
+struct PdwParams {
+  PdwProblem prob[kPdwMaxProblems];
+  int n, total;            // problems, work items
+  int K, splits, kb_per_split;
+  long long split_stride;  // floats between partial slices (the parameter count)
+  int dbg;                 // measurement ablations (env CRL_PDW_DBG): 1 no bias reads, 2 no MMA, 4 no TMA
+};
+
+void pdw_init(PdwParams& P, int K, int splits, size_t split_stride);
+// X: [K][ldx] bf16 (ldx >= M), dZ: [K][N] bf16, dW / db: slice-0 destinations in the gradient
+// buffer.  Returns false when a tensor map cannot be encoded or the table is full.
+bool pdw_add_problem(PdwParams& P, const __nv_bfloat16* X, int ldx, const __nv_bfloat16* dZ, int M, int N,
+                     float* dW, float* db);
+bool pdw_supported(int K, int splits);
+cudaError_t tc_pdw_launch(const PdwParams& P, int num_sms, cudaStream_t st);
+
+}  // namespace tc
+}  // namespace crl
