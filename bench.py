@@ -164,7 +164,7 @@ def stage_work(stage, cfg, N, Bl):
         # recompute the kernel also does is NOT counted -- and 2 MUFU ops per logit (L2); at
         # D = 256 the tensor term binds
         return 4.0 * Bl * N * D, "flop", "tensor"
-    if stage == "dw_db_grouped":
+    if stage in ("dw_db_grouped", "dw_db_pairs"):
         # every dW_l = X_l^T dZ_l of both encoders (the bias sums ride on the same tiles)
         tot = 0.0
         for ind in (in_phi, in_psi):
@@ -209,6 +209,10 @@ def stage_work(stage, cfg, N, Bl):
         return float(row * Bl), "byte", "hbm"
     if stage == "loss":
         return float(Bl * D * 4 * 2), "byte", "hbm"
+    if stage.startswith("enc_fwd_l") or stage.startswith("enc_bwd_dx_l"):
+        # one CTA-pair launch for layer l of BOTH encoders (tc_pgemm2)
+        l = int(stage.rsplit("_l", 1)[1])
+        return sum(2.0 * Bl * dims(ind)[l] * dims(ind)[l + 1] for ind in (in_phi, in_psi)), "flop", "tensor"
     for tag, ind in (("phi", in_phi), ("psi", in_psi)):
         if stage.startswith(tag + "_"):
             l = int(stage.rsplit("_l", 1)[1])

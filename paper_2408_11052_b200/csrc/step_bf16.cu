@@ -365,6 +365,83 @@ static crl_status enc_forward_bf16(crl_ctx* ctx, const char* tag, const EncoderP
   return CRL_OK;
 }
 
+// The phi and psi encoders have the same depth and width: with CTA-pair GEMMs on every layer,
+// layer l of both runs as ONE persistent launch (tc_pgemm2: one wave quantisation for 2 x 256
+// tiles instead of two, half the launches) instead of two kernels on two streams.
+static bool pg_pair_layers(const crl_ctx* ctx, bool dx) {
+  if (std::getenv("CRL_NO_PG_MERGE")) return false;
+  const EncoderPlan &A = ctx->phi_plan, &B = ctx->psi_plan;
+  if (A.n_layers != B.n_layers) return false;
+  for (int l = dx ? 1 : 0; l < A.n_layers; ++l) {
+    const bool a = dx ? ctx->tc_phi[l].pg_dx : ctx->tc_phi[l].pg_fwd;
+    const bool b = dx ? ctx->tc_psi[l].pg_dx : ctx->tc_psi[l].pg_fwd;
+    if (!a || !b || A.layer[l].out != B.layer[l].out) return false;
+  }
+  return true;
+}
+
+static crl_status enc_forward_pair_bf16(crl_ctx* ctx, float* stat_phi, float* stat_psi, cudaStream_t st, int* nl) {
+  const crl_config& k = ctx->cfg;
+  const int Bl = k.batch_local, L = ctx->phi_plan.n_layers;
+  for (int l = 0; l < L; ++l) {
+    const bool last = l == L - 1;
+    Stage sg(ctx, st, "enc_fwd_l" + std::to_string(l));
+    tc::PgemmArgs pa[2];
+    const EncoderPlan* P[2] = {&ctx->phi_plan, &ctx->psi_plan};
+    float* stat[2] = {stat_phi, stat_psi};
+    for (int e = 0; e < 2; ++e) {
+      const LayerPlan& Lp = P[e]->layer[l];
+      pa[e] = tc::PgemmArgs{Bl, Lp.out, Lp.in, ctx->mem.params + Lp.b_off, k.activation, last ? stat[e] : nullptr,
+                            k.energy};
+      pa[e].lin = (k.layernorm && !last) ? 1 : 0;
+    }
+    CU(tc::tc_pgemm2(last ? tc::PG_FWD_OUT : tc::PG_FWD_HIDDEN, ctx->tc_phi[l].pgf, pa[0], ctx->tc_psi[l].pgf,
+                     pa[1], ctx->num_sms, st));
+    ++*nl;
+    if (pa[0].lin) {
+      for (int e = 0; e < 2; ++e) {
+        const LayerPlan& Lp = P[e]->layer[l];
+        const bool phi = e == 0;
+        CU(launch_ln_fwd_bf16(Bl, Lp.out, phi ? ctx->phiZb[l] : ctx->psiZb[l], ctx->mem.params + Lp.g_off,
+                              ctx->mem.params + Lp.be_off, k.activation, phi ? ctx->phiYb[l] : ctx->psiYb[l],
+                              phi ? ctx->phiXb[l + 1] : ctx->psiXb[l + 1], phi ? ctx->phiMu[l] : ctx->psiMu[l],
+                              phi ? ctx->phiRs[l] : ctx->psiRs[l], st));
+        ++*nl;
+      }
+    }
+  }
+  return CRL_OK;
+}
+
+static crl_status enc_backward_pair_bf16(crl_ctx* ctx, cudaStream_t st, int* nl) {
+  const crl_config& k = ctx->cfg;
+  const int Bl = k.batch_local, L = ctx->phi_plan.n_layers;
+  for (int l = L - 1; l >= 1; --l) {
+    Stage sg(ctx, st, "enc_bwd_dx_l" + std::to_string(l));
+    tc::PgemmArgs pa[2];
+    const EncoderPlan* P[2] = {&ctx->phi_plan, &ctx->psi_plan};
+    for (int e = 0; e < 2; ++e) {
+      const LayerPlan& Lp = P[e]->layer[l];
+      pa[e] = tc::PgemmArgs{Bl, Lp.in, Lp.out, nullptr, k.activation, nullptr, k.energy};
+    }
+    CU(tc::tc_pgemm2(tc::PG_DX, ctx->tc_phi[l].pgd, pa[0], ctx->tc_psi[l].pgd, pa[1], ctx->num_sms, st));
+    ++*nl;
+    if (k.layernorm) {                                  // dY_{l-1} (act' at Y) -> dZ_{l-1}, dgamma, dbeta
+      for (int e = 0; e < 2; ++e) {
+        const bool phi = e == 0;
+        const LayerPlan& Lq = P[e]->layer[l - 1];
+        std::vector<crl_ctx::TcLayer>& T = phi ? ctx->tc_phi : ctx->tc_psi;
+        CU(launch_ln_bwd_bf16(Bl, Lq.out, T[l].dzprev, phi ? ctx->phiZb[l - 1] : ctx->psiZb[l - 1],
+                              phi ? ctx->phiMu[l - 1] : ctx->psiMu[l - 1], phi ? ctx->phiRs[l - 1] : ctx->psiRs[l - 1],
+                              ctx->mem.params + Lq.g_off, phi ? ctx->ln_part_phi : ctx->ln_part_psi, ctx->ln_nblk,
+                              ctx->grads + Lq.g_off, ctx->grads + Lq.be_off, ctx->dw_splits, ctx->sizes.n_params, st));
+        *nl += 2;
+      }
+    }
+  }
+  return CRL_OK;
+}
+
 static crl_status enc_backward_bf16(crl_ctx* ctx, const char* tag, const EncoderPlan& P,
                                     std::vector<crl_ctx::TcLayer>& T, __nv_bfloat16** Zb, cudaStream_t st,
                                     cudaStream_t side, int* nl) {
@@ -487,6 +564,10 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     Stage sg(ctx, st, "mlp_fwd_cchain");
     CU(tc::tc_cchain_forward(ctx->cchain_fwd[0], ctx->cchain_fwd[1], ctx->cchain_fwd_p, st));
     ++nl;
+  } else if (pg_pair_layers(ctx, false)) {
+    rs = enc_forward_pair_bf16(ctx, stat_in_fwd ? ctx->stat_phi + row_off : nullptr,
+                               stat_in_fwd ? ctx->stat_psi + row_off : nullptr, st, &nl);
+    if (rs != CRL_OK) return rs;
   } else {
     fork2(ctx, st, st2);
     rs = enc_forward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiXb, ctx->psiZb, ctx->psi_out,
@@ -696,7 +777,10 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
   cudaStream_t side = (st == st2) ? st : ctx->cap_stream3;      // phi weight gradients
   cudaStream_t side2 = (st == st2) ? st : ctx->cap_stream4;     // psi weight gradients
   const bool fused_bwd = ctx->use_chain || ctx->use_cchain;      // one dX-chain launch for both
-  if (!fused_bwd) {
+  // both encoders' dX layers as joint CTA-pair launches (the gradient pass gives dPhi and dPsi at once)
+  const bool pair_bwd = !fused_bwd && (ctx->use_pdw || ctx->use_dwg) && (ctx->use_grad2 || ctx->use_gradf) &&
+                        pg_pair_layers(ctx, true);
+  if (!fused_bwd && !pair_bwd) {
     rs = enc_backward_bf16(ctx, "psi", ctx->psi_plan, ctx->tc_psi, ctx->psiZb, st2, side2, &nl);
     if (rs != CRL_OK) return rs;
   }
@@ -713,7 +797,11 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(tc::launch_f32_to_bf16(ctx->dphi, ctx->dphib, (size_t)Bl * D, ctx->num_sms, st));
     }
     nl += 2; }
-  if (!fused_bwd) {
+  if (pair_bwd) {
+    join2(ctx, st, st2);
+    rs = enc_backward_pair_bf16(ctx, st, &nl);
+    if (rs != CRL_OK) return rs;
+  } else if (!fused_bwd) {
     rs = enc_backward_bf16(ctx, "phi", ctx->phi_plan, ctx->tc_phi, ctx->phiZb, st, side, &nl);
     if (rs != CRL_OK) return rs;
     join2(ctx, st, st2);

@@ -98,7 +98,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 
 template <int EPI, int ACT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW, 1)
-    tc_pgemm_kernel(const __grid_constant__ PgemmMaps maps, const PgemmArgs p) {
+    tc_pgemm_kernel(const __grid_constant__ PgemmJob J) {
   using namespace pg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -115,13 +115,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-  const int tiles_n = (p.N + kTN - 1) / kTN;
-  const int n_tiles = ((p.M + 255) / 256) * tiles_n;
-  const int nkb = (p.K + kBK - 1) / kBK;
+  const int n_tiles = J.total;
+  // tile t of the job: problem pi, local tile tt; that problem's maps / arguments / shape
+#define PG_TILE(t)                                                    \
+  const int pi = (J.np > 1 && (t) >= J.nt0) ? 1 : 0;                  \
+  const int tt = (t) - (pi ? J.nt0 : 0);                              \
+  const PgemmMaps& maps = J.maps[pi];                                 \
+  const PgemmArgs& p = J.args[pi];                                    \
+  const int tiles_n = (p.N + kTN - 1) / kTN;                          \
+  const int nkb = (p.K + kBK - 1) / kBK;                              \
+  (void)maps; (void)nkb; (void)tiles_n;
+  const PgemmArgs& p0 = J.args[0];
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&maps.a);
-    tma_prefetch_desc(&maps.b);
+    for (int i = 0; i < J.np; ++i) { tma_prefetch_desc(&J.maps[i].a); tma_prefetch_desc(&J.maps[i].b); }
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 2 * kEpiW); }
     for (int i = 0; i < kEpiW * kNStg; ++i) mbar_init(&zbar[i], 1);
@@ -137,7 +144,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_launch();
-  if (p.trace && threadIdx.x == 0 && rank == 0) p.trace[512 + 2 * cid] = (long long)globaltimer();
+  if (p0.trace && threadIdx.x == 0 && rank == 0) p0.trace[512 + 2 * cid] = (long long)globaltimer();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -145,8 +152,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
       const uint32_t full_leader = mapa(smem_u32(full), 0);
       int g = 0;
       for (int t = cid; t < n_tiles; t += ncl) {
-        const int m0 = (t / tiles_n) * 256 + 128 * (int)rank;
-        const int n0 = (t % tiles_n) * kTN + 128 * (int)rank;
+        PG_TILE(t)
+        const int m0 = (tt / tiles_n) * 256 + 128 * (int)rank;
+        const int n0 = (tt % tiles_n) * kTN + 128 * (int)rank;
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = g % kStages;
           mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
@@ -175,6 +183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
       const uint32_t idesc = idesc_bf16_f32(256, kTN, false, EPI != PG_DX);
       int g = 0, it = 0;
       for (int t = cid; t < n_tiles; t += ncl, ++it) {
+        PG_TILE(t)
         const int b = it & 1;
         mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -196,7 +205,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
           commit_pair(&empty[s]);
         }
         commit_pair(&tfull[b]);
-        if (p.trace && cid == 0 && it < 8) p.trace[256 + it] = clock64();
+        if (p0.trace && cid == 0 && it < 8) p0.trace[256 + it] = clock64();
       }
     }
   } else {
@@ -218,9 +227,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
     int it = 0;
     uint32_t zphase = 0;                                   // DX: parity bits of zb[] (one per buffer)
     for (int t = cid; t < n_tiles; t += ncl, ++it) {
+      PG_TILE(t)
       const int b = it & 1;
-      const int mrow0 = (t / tiles_n) * 256 + 128 * (int)rank + 32 * q;   // first row of this warp
-      const int ncol0 = (t % tiles_n) * kTN;
+      const int mrow0 = (tt / tiles_n) * 256 + 128 * (int)rank + 32 * q;   // first row of this warp
+      const int ncol0 = (tt % tiles_n) * kTN;
       const int nch = min(kTN, p.N - ncol0) / 64;         // 64-column chunks (N % 64 == 0)
       if (EPI == PG_DX && lane == 0) {
         // Z_prev chunks of this warp for this tile: issued before the accumulator is ready
@@ -417,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
   }
   tc_fence_before();
   cluster_sync();                          // the peer's MMAs / arrivals are done before TMEM goes
-  if (p.trace && threadIdx.x == 0 && rank == 0) p.trace[512 + 2 * cid + 1] = (long long)globaltimer();
+  if (p0.trace && threadIdx.x == 0 && rank == 0) p0.trace[512 + 2 * cid + 1] = (long long)globaltimer();
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -432,7 +442,7 @@ bool tc_pgemm_supported(int M, int N, int K) {
 }
 
 template <int EPI, int ACT>
-static cudaError_t launch_pg(const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
+static cudaError_t launch_pg(const PgemmJob& J, int num_sms, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_pgemm_kernel<EPI, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -440,23 +450,46 @@ static cudaError_t launch_pg(const PgemmMaps& maps, const PgemmArgs& p, int num_
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles = ((p.M + 255) / 256) * ((p.N + pg::kTN - 1) / pg::kTN);
-  const int clusters = std::max(1, std::min(tiles, num_sms / 2));
-  return launch_pdl(tc_pgemm_kernel<EPI, ACT>, dim3(2 * clusters), dim3(64 + 32 * pg::kEpiW), pg::kSmem, st, maps, p);
+  const int clusters = std::max(1, std::min(J.total, num_sms / 2));
+  return launch_pdl(tc_pgemm_kernel<EPI, ACT>, dim3(2 * clusters), dim3(64 + 32 * pg::kEpiW), pg::kSmem, st, J);
 }
 template <int EPI>
-static cudaError_t launch_pg_act(const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
-  if (EPI == PG_FWD_OUT || p.act == CRL_ACT_SILU) return launch_pg<EPI, CRL_ACT_SILU>(maps, p, num_sms, st);
-  return launch_pg<EPI, CRL_ACT_RELU>(maps, p, num_sms, st);
+static cudaError_t launch_pg_act(const PgemmJob& J, int num_sms, cudaStream_t st) {
+  if (EPI == PG_FWD_OUT || J.args[0].act == CRL_ACT_SILU) return launch_pg<EPI, CRL_ACT_SILU>(J, num_sms, st);
+  return launch_pg<EPI, CRL_ACT_RELU>(J, num_sms, st);
+}
+static int pg_tiles(const PgemmArgs& p) { return ((p.M + 255) / 256) * ((p.N + pg::kTN - 1) / pg::kTN); }
+
+static cudaError_t pg_run(int epi, const PgemmJob& J, int num_sms, cudaStream_t st) {
+  switch (epi) {
+    case PG_FWD_HIDDEN: return launch_pg_act<PG_FWD_HIDDEN>(J, num_sms, st);
+    case PG_FWD_OUT: return launch_pg_act<PG_FWD_OUT>(J, num_sms, st);
+    case PG_DX: return launch_pg_act<PG_DX>(J, num_sms, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t tc_pgemm(int epi, const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st) {
-  switch (epi) {
-    case PG_FWD_HIDDEN: return launch_pg_act<PG_FWD_HIDDEN>(maps, p, num_sms, st);
-    case PG_FWD_OUT: return launch_pg_act<PG_FWD_OUT>(maps, p, num_sms, st);
-    case PG_DX: return launch_pg_act<PG_DX>(maps, p, num_sms, st);
-  }
-  return cudaErrorInvalidValue;
+  PgemmJob J{};
+  J.maps[0] = maps;
+  J.args[0] = p;
+  J.np = 1;
+  J.nt0 = J.total = pg_tiles(p);
+  return pg_run(epi, J, num_sms, st);
+}
+
+cudaError_t tc_pgemm2(int epi, const PgemmMaps& maps0, const PgemmArgs& p0, const PgemmMaps& maps1,
+                      const PgemmArgs& p1, int num_sms, cudaStream_t st) {
+  if (p0.act != p1.act) return cudaErrorInvalidValue;
+  PgemmJob J{};
+  J.maps[0] = maps0;
+  J.maps[1] = maps1;
+  J.args[0] = p0;
+  J.args[1] = p1;
+  J.np = 2;
+  J.nt0 = pg_tiles(p0);
+  J.total = J.nt0 + pg_tiles(p1);
+  return pg_run(epi, J, num_sms, st);
 }
 
 }  // namespace tc

@@ -28,7 +28,18 @@ struct PgemmArgs {
   long long* trace;    // development timestamps (scratch/pgemm_test.cu); nullptr in the library
 };
 
+// Up to two independent problems (the phi and psi encoders' same layer) in ONE persistent
+// launch: the pairs walk problem 0's tiles, then problem 1's (one wave quantisation, not two)
+struct PgemmJob {
+  PgemmMaps maps[2];
+  PgemmArgs args[2];
+  int np, nt0, total;   // problems, tiles of problem 0, all tiles
+};
+
 bool tc_pgemm_supported(int M, int N, int K);
+// both problems share the epilogue kind and activation
+cudaError_t tc_pgemm2(int epi, const PgemmMaps& maps0, const PgemmArgs& p0, const PgemmMaps& maps1,
+                      const PgemmArgs& p1, int num_sms, cudaStream_t st);
 cudaError_t tc_pgemm(int epi, const PgemmMaps& maps, const PgemmArgs& p, int num_sms, cudaStream_t st);
 
 }  // namespace tc
