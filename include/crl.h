@@ -251,7 +251,9 @@ CRL_API const char* crl_last_error(const crl_ctx* ctx);   /* ctx may be NULL (gl
 
 /* Debug taps (parity tests): device pointer and element count of an internal fp32 tensor
  * written by the last crl_critic_step: "phi" [B_l][D], "psi" [B_l][D], "lse_row" [B_l],
- * "lse_col" [B_l] (this rank's columns), "dphi", "dpsi" [B_l][D], "grads" [n_params].
+ * "lse_col" [B_l] (this rank's columns), "dphi", "dpsi" [B_l][D], "grads" [n_params] (the
+ * reduced pre-Adam gradient on the bf16 path only when the step was given grads_out: without
+ * it the split-K partials are summed inside the Adam kernel and not written back).
  * Valid until the next call on the context. */
 CRL_API crl_status crl_debug_tensor(crl_ctx* ctx, const char* name, const float** ptr, size_t* count);
 

@@ -65,6 +65,8 @@ cudaError_t launch_loss_finalize(const float*, float, float, float, float, float
                                  int*, cudaStream_t);
 cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, float, float, float,
                         float, const int*, const int*, int*, void*, int, cudaStream_t);
+cudaError_t launch_adam_ex(float*, float*, int, float*, float*, size_t, float, float, float, float,
+                           float, const int*, const int*, int*, void*, int, int, cudaStream_t);
 namespace tc {
 bool tc_logits_supports(int D);
 int tc_logits_splits(int Na, int Nb, int D, int num_sms);

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) adam_kernel(
     float* __restrict__ p, float* __restrict__ g, int S, float* __restrict__ m,
     float* __restrict__ v, size_t n, float lr, float b1, float b2, float eps, float wd,
     const int* __restrict__ adam_t, const int* __restrict__ skip, int* __restrict__ status,
-    __nv_bfloat16_raw* __restrict__ shadow) {
+    __nv_bfloat16_raw* __restrict__ shadow, int keep_sum) {
   pdl_wait();
   pdl_launch();
   if (*skip) return;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) adam_kernel(
       const float4 h = reinterpret_cast<const float4*>(g + (size_t)sl * n)[i];
       gv.x += h.x; gv.y += h.y; gv.z += h.z; gv.w += h.w;
     }
-    if (S > 1) reinterpret_cast<float4*>(g)[i] = gv;
+    if (S > 1 && keep_sum) reinterpret_cast<float4*>(g)[i] = gv;   // the reduced gradient, for grads_out
     float4 pv = reinterpret_cast<const float4*>(p)[i];
     float4 mv = reinterpret_cast<const float4*>(m)[i];
     float4 vv = reinterpret_cast<const float4*>(v)[i];
@@ -288,16 +288,29 @@ cudaError_t launch_loss_finalize(const float* acc, float invN, float c_f, float 
                     skip, adam_t, status);
 }
 
+cudaError_t launch_adam_ex(float* p, float* g, int S, float* m, float* v, size_t n, float lr,
+                           float b1, float b2, float eps, float wd, const int* adam_t,
+                           const int* skip, int* status, void* shadow_bf16, int num_sms, int keep_sum,
+                           cudaStream_t st);
 cudaError_t launch_adam(float* p, float* g, int S, float* m, float* v, size_t n, float lr,
                         float b1, float b2, float eps, float wd, const int* adam_t,
                         const int* skip, int* status, void* shadow_bf16, int num_sms,
                         cudaStream_t st) {
+  return launch_adam_ex(p, g, S, m, v, n, lr, b1, b2, eps, wd, adam_t, skip, status, shadow_bf16, num_sms, 1, st);
+}
+
+// keep_sum = 0: the split-K partials are summed in registers only (nobody reads the reduced
+// gradient after the update: no grads_out), saving one write of the gradient buffer
+cudaError_t launch_adam_ex(float* p, float* g, int S, float* m, float* v, size_t n, float lr,
+                           float b1, float b2, float eps, float wd, const int* adam_t,
+                           const int* skip, int* status, void* shadow_bf16, int num_sms, int keep_sum,
+                           cudaStream_t st) {
   size_t blocks = (n / 4 + 255) / 256 + 1;
   size_t cap = (size_t)num_sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   return launch_pdl(adam_kernel, dim3((unsigned)blocks), dim3(256), 0, st, p, g, S, m, v, n, lr, b1, b2, eps,
-                    wd, adam_t, skip, status, reinterpret_cast<__nv_bfloat16_raw*>(shadow_bf16));
+                    wd, adam_t, skip, status, reinterpret_cast<__nv_bfloat16_raw*>(shadow_bf16), keep_sum);
 }
 
 }  // namespace crl

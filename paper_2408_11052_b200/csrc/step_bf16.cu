@@ -25,6 +25,8 @@ cudaError_t launch_loss_finalize(const float*, float, float, float, float, float
                                  int*, cudaStream_t);
 cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, float, float, float,
                         float, const int*, const int*, int*, void*, int, cudaStream_t);
+cudaError_t launch_adam_ex(float*, float*, int, float*, float*, size_t, float, float, float, float,
+                           float, const int*, const int*, int*, void*, int, int, cudaStream_t);
 cudaError_t launch_reduce_partials(float*, size_t, int, cudaStream_t);
 namespace tc {
 bool make_map_bf16(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
@@ -854,9 +856,9 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     NC(ncclAllReduce(ctx->grads, ctx->grads, ctx->sizes.n_params, ncclFloat32, ncclSum, ctx->comm, st));
   }
   { Stage sg(ctx, st, "adam");
-    CU(launch_adam(ctx->mem.params, ctx->grads, adam_splits, ctx->mem.adam_m, ctx->mem.adam_v,
-                   ctx->sizes.n_params, k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay, ctx->adam_t,
-                   ctx->skip, ctx->status, ctx->wshadow, ctx->num_sms, st));
+    CU(launch_adam_ex(ctx->mem.params, ctx->grads, adam_splits, ctx->mem.adam_m, ctx->mem.adam_v,
+                      ctx->sizes.n_params, k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay, ctx->adam_t,
+                      ctx->skip, ctx->status, ctx->wshadow, ctx->num_sms, grads_out != nullptr, st));
     ++nl; }
   if (grads_out)
     CU(cudaMemcpyAsync(grads_out, ctx->grads, ctx->sizes.n_params * 4, cudaMemcpyDeviceToDevice, st));
