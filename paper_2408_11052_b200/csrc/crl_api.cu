@@ -450,6 +450,14 @@ crl_status crl_create(const crl_config* cfg, const crl_memory* mem, const void* 
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess)
     return cleanup(fail(nullptr, CRL_ECUDA, "context initialisation failed"));
+  if (ctx->dist) {
+    const char* nb = std::getenv("CRL_AR_BUCKETS");
+    ctx->ar_buckets = std::max(1, std::min(crl_ctx::kMaxArBuckets, nb ? std::atoi(nb) : 4));
+    ctx->ev_bkt.resize(2 * crl_ctx::kMaxArBuckets, nullptr);
+    for (auto& e : ctx->ev_bkt)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+        return cleanup(fail(nullptr, CRL_ECUDA, "context initialisation failed (bucket events)"));
+  }
 
   if (ctx->bf16) {
     crl_status bs = bf16_prepare(ctx);
@@ -482,6 +490,8 @@ crl_status crl_destroy(crl_ctx* ctx) {
   if (ctx->cap_stream4) cudaStreamDestroy(ctx->cap_stream4);
   if (ctx->cap_body) cudaStreamDestroy(ctx->cap_body);
   if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
+  for (auto e : ctx->ev_bkt)
+    if (e) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   for (int i = 0; i < crl_ctx::kHostSlots; ++i)
     if (ctx->h_ev[i]) cudaEventDestroy(ctx->h_ev[i]);
@@ -660,6 +670,53 @@ static void join(crl_ctx* ctx, cudaStream_t s0, cudaStream_t s1) {
   cudaStreamWaitEvent(s0, ctx->ev_join, 0);
 }
 
+crl_status crl::enqueue_allreduce_adam(crl_ctx* ctx, cudaStream_t st, cudaStream_t st2, void* shadow, int keep_sum,
+                                  int* nl) {
+  const crl_config& k = ctx->cfg;
+  const size_t n = ctx->sizes.n_params;
+  if (!ctx->dist) {
+    Stage sg(ctx, st, "adam");
+    CU(launch_adam_ex(ctx->mem.params, ctx->grads, ctx->dw_splits, ctx->mem.adam_m, ctx->mem.adam_v, n, k.lr,
+                      k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay, ctx->adam_t, ctx->skip, ctx->status, shadow,
+                      ctx->num_sms, keep_sum, st));
+    ++*nl;
+    return CRL_OK;
+  }
+  // buckets of the flat gradient (256-float aligned): bucket b's partials are reduced on st, its
+  // all-reduce runs on the communication stream, and Adam on bucket b waits for that bucket
+  // only -- Adam of bucket b overlaps the all-reduce of bucket b + 1 (element-wise update)
+  cudaStream_t cs = (st == st2) ? st : ctx->cap_stream3;
+  const int NB = ctx->ar_buckets;
+  const size_t per = ((n + NB - 1) / NB + 255) / 256 * 256;
+  int nb = 0;
+  for (size_t off = 0; off < n; off += per, ++nb) {
+    const size_t len = std::min(per, n - off);
+    if (ctx->dw_splits > 1) {
+      Stage sg(ctx, st, "reduce_partials");
+      CU(launch_reduce_partials_range(ctx->grads + off, len, n, ctx->dw_splits, st));
+      ++*nl;
+    }
+    if (cs != st) {
+      cudaEventRecord(ctx->ev_bkt[nb], st);
+      cudaStreamWaitEvent(cs, ctx->ev_bkt[nb], 0);
+    }
+    NC(ncclAllReduce(ctx->grads + off, ctx->grads + off, len, ncclFloat32, ncclSum, ctx->comm, cs));
+    if (cs != st) cudaEventRecord(ctx->ev_bkt[crl_ctx::kMaxArBuckets + nb], cs);
+  }
+  nb = 0;
+  for (size_t off = 0; off < n; off += per, ++nb) {
+    const size_t len = std::min(per, n - off);
+    if (cs != st) cudaStreamWaitEvent(st, ctx->ev_bkt[crl_ctx::kMaxArBuckets + nb], 0);
+    Stage sg(ctx, st, "adam");
+    CU(launch_adam_ex(ctx->mem.params + off, ctx->grads + off, 1, ctx->mem.adam_m + off, ctx->mem.adam_v + off, len,
+                      k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay, ctx->adam_t, ctx->skip, ctx->status,
+                      shadow ? static_cast<void*>(static_cast<__nv_bfloat16*>(shadow) + off) : nullptr,
+                      ctx->num_sms, keep_sum, st));
+    ++*nl;
+  }
+  return CRL_OK;
+}
+
 static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, const float* g,
                                  float* loss_out, float* grads_out, cudaStream_t st,
                                  cudaStream_t st2) {
@@ -766,22 +823,9 @@ static crl_status enqueue_critic(crl_ctx* ctx, const float* s, const float* a, c
                     ctx->phiZ, ctx->dphi, ctx->dz, st, &nl);
   if (rs != CRL_OK) return rs;
   join(ctx, st, st2);
-  int adam_splits = ctx->dw_splits;
-  if (ctx->dist) {
-    if (ctx->dw_splits > 1) {
-      Stage sg(ctx, st, "reduce_partials");
-      CU(launch_reduce_partials(ctx->grads, ctx->sizes.n_params, ctx->dw_splits, st));
-      ++nl;
-    }
-    adam_splits = 1;
-    NC(ncclAllReduce(ctx->grads, ctx->grads, ctx->sizes.n_params, ncclFloat32, ncclSum, ctx->comm, st));
-  }
-  // A6: Adam (sums the split-K partials in the same pass)
-  { Stage sg(ctx, st, "adam");
-    CU(launch_adam(ctx->mem.params, ctx->grads, adam_splits, ctx->mem.adam_m, ctx->mem.adam_v,
-                   ctx->sizes.n_params, k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay,
-                   ctx->adam_t, ctx->skip, ctx->status, nullptr, ctx->num_sms, st));
-    ++nl; }
+  // A6: Adam (sums the split-K partials in the same pass); W > 1: bucketed all-reduce first
+  rs = enqueue_allreduce_adam(ctx, st, st2, nullptr, 1, &nl);
+  if (rs != CRL_OK) return rs;
   if (grads_out)   // slice 0 holds the reduced pre-Adam gradient after the Adam kernel
     CU(cudaMemcpyAsync(grads_out, ctx->grads, ctx->sizes.n_params * 4, cudaMemcpyDeviceToDevice, st));
   ctx->launches = nl;

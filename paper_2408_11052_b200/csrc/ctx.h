@@ -37,6 +37,11 @@ inline bool force_dist() { return std::getenv("CRL_FORCE_DIST") != nullptr; }
 void gemm_set_num_sms(int n);
 void logits_set_num_sms(int n);
 cudaError_t launch_reduce_partials(float*, size_t, int, cudaStream_t);
+cudaError_t launch_reduce_partials_range(float*, size_t, size_t, int, cudaStream_t);
+// W > 1: split-K partials reduced, gradient all-reduced in buckets on a communication stream,
+// Adam per bucket on st as soon as its bucket is reduced; W = 1: plain Adam
+crl_status enqueue_allreduce_adam(crl_ctx* ctx, cudaStream_t st, cudaStream_t st2, void* shadow, int keep_sum,
+                                  int* nl);
 bool logits_simt_supports(int D);
 cudaError_t logits_lse_f32(int, int, const float*, int, const float*, int, float*, cudaStream_t);
 cudaError_t logits_grad_f32(int, int, const float*, int, int, const float*, int, const float*,
@@ -156,6 +161,10 @@ struct crl_ctx {
   cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr, cap_stream3 = nullptr, cap_stream4 = nullptr;
   cudaStream_t cap_body = nullptr;        // captures the bodies of conditional graph nodes
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side = nullptr;
+  // C4 bucketed gradient all-reduce (W > 1): [2][kMaxArBuckets] events (partials reduced, all-reduced)
+  static constexpr int kMaxArBuckets = 8;
+  int ar_buckets = 1;
+  std::vector<cudaEvent_t> ev_bkt;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int> graph_launches;     // kernels per replay of each cached graph
   std::map<GraphKey, uint64_t> graph_use;     // last replay (LRU eviction beyond kMaxGraphs)

@@ -260,22 +260,27 @@ int dw_splits_for(int Bn) {
   return s < 1 ? 1 : (s > 8 ? 8 : s);
 }
 
-// g[i] = sum_s part[s][i]  (in place into slice 0)
-__global__ void reduce_partials_kernel(float* part, size_t n, int S) {
+// g[i] = sum_s part[s * stride + i] for i < n  (in place into slice 0)
+__global__ void reduce_partials_kernel(float* part, size_t n, size_t stride, int S) {
   pdl_wait();
   pdl_launch();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     float v = part[i];
-    for (int s = 1; s < S; ++s) v += part[(size_t)s * n + i];
+    for (int s = 1; s < S; ++s) v += part[(size_t)s * stride + i];
     part[i] = v;
   }
 }
 
-cudaError_t launch_reduce_partials(float* part, size_t n, int S, cudaStream_t st) {
+cudaError_t launch_reduce_partials_range(float* part, size_t n, size_t stride, int S, cudaStream_t st) {
   size_t blocks = (n + 255) / 256;
   if (blocks > (size_t)g_num_sms * 8) blocks = (size_t)g_num_sms * 8;
-  return launch_pdl(reduce_partials_kernel, dim3((unsigned)blocks), dim3(256), 0, st, part, n, S);
+  if (blocks == 0) blocks = 1;
+  return launch_pdl(reduce_partials_kernel, dim3((unsigned)blocks), dim3(256), 0, st, part, n, stride, S);
+}
+
+cudaError_t launch_reduce_partials(float* part, size_t n, int S, cudaStream_t st) {
+  return launch_reduce_partials_range(part, n, n, S, st);
 }
 
 }  // namespace crl

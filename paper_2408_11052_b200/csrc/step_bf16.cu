@@ -845,21 +845,9 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     cudaEventRecord(ctx->ev_side, side2);
     cudaStreamWaitEvent(st, ctx->ev_side, 0);
   }
-  int adam_splits = ctx->dw_splits;
-  if (ctx->dist) {
-    if (ctx->dw_splits > 1) {
-      Stage sg(ctx, st, "reduce_partials");
-      CU(launch_reduce_partials(ctx->grads, ctx->sizes.n_params, ctx->dw_splits, st));
-      ++nl;
-    }
-    adam_splits = 1;
-    NC(ncclAllReduce(ctx->grads, ctx->grads, ctx->sizes.n_params, ncclFloat32, ncclSum, ctx->comm, st));
-  }
-  { Stage sg(ctx, st, "adam");
-    CU(launch_adam_ex(ctx->mem.params, ctx->grads, adam_splits, ctx->mem.adam_m, ctx->mem.adam_v,
-                      ctx->sizes.n_params, k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay, ctx->adam_t,
-                      ctx->skip, ctx->status, ctx->wshadow, ctx->num_sms, grads_out != nullptr, st));
-    ++nl; }
+  // A6: Adam; W > 1: split-K partials reduced and the gradient all-reduced in buckets first (C4)
+  rs = enqueue_allreduce_adam(ctx, st, st2, ctx->wshadow, grads_out != nullptr, &nl);
+  if (rs != CRL_OK) return rs;
   if (grads_out)
     CU(cudaMemcpyAsync(grads_out, ctx->grads, ctx->sizes.n_params * 4, cudaMemcpyDeviceToDevice, st));
   ctx->launches = nl;
