@@ -134,8 +134,15 @@ crl_status bf16_prepare(crl_ctx* ctx) {
     __nv_bfloat16** Xb[2] = {ctx->phiXb, ctx->psiXb};
     const __nv_bfloat16* x0[2] = {ctx->x0_phi, ctx->x0_psi};
     const int ld0[2] = {ctx->ld0_phi, ctx->ld0_psi};
+    // problem order = work-item order: the pairs take items round-robin, so the first layers
+    // (K = in <= 37: their X tiles are mostly TMA zero-fill, about half the operand traffic of
+    // a full item) go LAST and fill the final partial round (makespan 3.5 instead of 4 items
+    // at netscale: 208 full + 16 half items on 74 pairs)
+    const int L = plans[0]->n_layers;
+    const bool natural = std::getenv("CRL_PDW_NATURAL_ORDER") != nullptr;   // measurement knob
+    for (int pass = 0; pass < (natural ? 1 : 2) && ctx->use_pdw; ++pass)
     for (int e = 0; e < 2 && ctx->use_pdw; ++e)
-      for (int l = 0; l < plans[e]->n_layers; ++l) {
+      for (int l = natural ? 0 : (pass == 0 ? 1 : 0); l < (natural || pass == 0 ? L : 1); ++l) {
         const LayerPlan& Lp = plans[e]->layer[l];
         if (!tc::pdw_add_problem(ctx->pdw, l == 0 ? x0[e] : Xb[e][l], l == 0 ? ld0[e] : k.width, (*tcs[e])[l].dz,
                                  Lp.in, Lp.out, ctx->grads + Lp.w_off, ctx->grads + Lp.b_off)) {

@@ -17,9 +17,9 @@
 //   warp 0 (lane 0, both CTAs)  TMA producer, 5-stage ring (32 KB / stage / CTA)
 //   warp 1 (lane 0, leader)     MMA issuer; stage-consumed commits multicast to both CTAs
 //   warps 2..5 (both CTAs)      epilogue (TMEM lane quarter = 32 rows of dW)
-//   warps 6..9 (both CTAs)      bias gradient: on items of M tile 0, the column sums of the dZ
-//                               stage this CTA staged (its 128 out-columns), read from SMEM after
-//                               the MMA consumed it (16 of the K block's 64 rows each);
+//   warps 6.. (both CTAs)       bias gradient: on items of M tile 0, the column sums of the dZ
+//                               stage this CTA staged (its 128 NH out-columns), read from SMEM
+//                               after the MMA consumed it (64 / kBiasW of the K block's rows each);
 //                               the stage is refilled only after they arrived
 // db_l is thus a by-product of dW_l's operand stream: no ones-MMA, no second pass over dZ_l.
 #include <cstdio>
@@ -39,16 +39,22 @@ bool make_map_f32_3d(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, ui
 namespace pdw {
 using namespace pair;
 
-#ifndef CRL_PDW_STAGES
-#define CRL_PDW_STAGES 6
-#endif
-constexpr int kBK = 64, kStages = CRL_PDW_STAGES, kTN = 256;
+constexpr int kBK = 64;
 constexpr uint32_t kHalf = 128 * kBK * 2;            // 16 KB: 128 MN-columns x 64 K rows
-constexpr uint32_t kStage = 2 * kHalf;               // A half + B half
 constexpr uint32_t kStgBuf = 32 * 128;               // 4 KB: 32 rows x 32 fp32 (SW128)
-constexpr int kNStg = kStages >= 6 ? 2 : 4;          // staging buffers per epilogue warp (SMEM budget)
-constexpr int kBiasW = 4;                            // bias-gradient warps (16 K rows of a stage each)
-constexpr size_t kSmem = kStages * kStage + 4 * kNStg * kStgBuf + kBiasW * 128 * 4 + 256;
+// NH 256-column halves per work item (NH = 2: 256 x 512 dW tiles, both TMEM accumulators, 25 %
+// less operand traffic per flop; NH = 1: 256 x 256 tiles, double-buffered accumulators)
+template <int NH>
+struct Cfg {
+  static constexpr int kStages = NH == 2 ? 4 : 6;
+  static constexpr uint32_t kStage = kHalf * (1 + NH);           // A half + NH B halves
+  static constexpr int kNStg = 2;                                // staging buffers per epilogue warp
+  static constexpr int kTN = 256 * NH;                           // item width
+  static constexpr int kNbuf = 2 / NH;                           // accumulator buffers
+  static constexpr int kBiasW = NH == 2 ? 2 : 4;                 // bias-gradient warps (64 / kBiasW K rows each)
+  static constexpr int kThreads = 192 + 32 * kBiasW;
+  static constexpr size_t kSmem = kStages * kStage + 4 * kNStg * kStgBuf + kBiasW * 128 * NH * 4 + 256;
+};
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int x, int y, int z) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
@@ -88,19 +94,23 @@ __device__ __forceinline__ Item decode(const PdwParams& P, int it) {
 
 }  // namespace pdw
 
+template <int NH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     tc_pdw_kernel(const __grid_constant__ PdwParams P) {
   using namespace pdw;
+  using C = Cfg<NH>;
+  constexpr int kStages = C::kStages, kNStg = C::kNStg, kTN = C::kTN, kNbuf = C::kNbuf, kBiasW = C::kBiasW;
+  constexpr uint32_t kStage = C::kStage;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sStage = smem_raw;
   uint8_t* sStg = sStage + kStages * kStage;                        // [4 warps][kNStg][4 KB]
-  float* sDb = reinterpret_cast<float*>(sStg + 4 * kNStg * kStgBuf);  // [kBiasW][128] bias partials
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDb + kBiasW * 128);
+  float* sDb = reinterpret_cast<float*>(sStg + 4 * kNStg * kStgBuf);  // [kBiasW][128 NH] bias partials
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDb + kBiasW * 128 * NH);
   uint64_t* full = bars;                  // [kStages]  leader: both CTAs' TMA bytes
-  uint64_t* empty = full + kStages;        // [kStages]  both: MMA commit + the 2 bias warps
+  uint64_t* empty = full + kStages;        // [kStages]  both: MMA commit + the bias warps
   uint64_t* used = empty + kStages;        // [kStages]  both: MMA commit (the bias warps may read)
-  uint64_t* tfull = used + kStages;        // [2]       both: accumulator ready
-  uint64_t* tempty = tfull + 2;           // [2]       leader: the 8 epilogue warps of the pair
+  uint64_t* tfull = used + kStages;        // [kNbuf]   both: accumulator(s) ready
+  uint64_t* tempty = tfull + 2;           // [kNbuf]   leader: the 8 epilogue warps of the pair
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -116,7 +126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();   // SW128 operand tiles need 1 KB alignment
     for (int p = 0; p < P.n; ++p) { tma_prefetch_desc(&P.prob[p].a); tma_prefetch_desc(&P.prob[p].b); }
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1 + kBiasW); mbar_init(&used[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int i = 0; i < kNbuf; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc_pair(tmem_slot, 512);
@@ -135,47 +145,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       for (int it = cid; it < P.total; it += ncl) {
         const Item w = decode(P, it);
         const PdwProblem& pr = P.prob[w.p];
-        const int m0 = w.tm * 256 + 128 * (int)rank, n0 = w.tn * kTN + 128 * (int)rank;
+        const int m0 = w.tm * 256 + 128 * (int)rank;
+        // halves with columns (an N = 256 layer in a 512-wide item: its second half is skipped)
+        const int nhi = (NH == 2 && w.tn * kTN + 256 >= pr.N) ? 1 : NH;
         int kb0, kb1;
         kb_range(w.slice, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % kStages;
           mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
           if (P.dbg & 4) { if (rank == 0) mbar_arrive(&full[s]); continue; }
-          if (rank == 0) mbar_expect_tx(&full[s], 2 * kStage);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * kHalf * (1 + nhi));
           const uint32_t fb = full_leader + 8u * (uint32_t)s;
-          const uint32_t a_dst = smem_u32(sStage + s * kStage), b_dst = a_dst + kHalf;
+          const uint32_t a_dst = smem_u32(sStage + s * kStage);
           const int k = kb * kBK;
           tma_load_2d_pair(a_dst, &pr.a, fb, m0, k);                 // X {in, K} box {64, 64} x 2
           tma_load_2d_pair(a_dst + kBK * 128, &pr.a, fb, m0 + 64, k);
-          tma_load_2d_pair(b_dst, &pr.b, fb, n0, k);                 // dZ {out, K} box {64, 64} x 2
-          tma_load_2d_pair(b_dst + kBK * 128, &pr.b, fb, n0 + 64, k);
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {                             // dZ {out, K} box {64, 64} x 2 per half
+            if (h >= nhi) break;
+            const int n0 = w.tn * kTN + 256 * h + 128 * (int)rank;
+            const uint32_t b_dst = a_dst + kHalf * (1 + h);
+            tma_load_2d_pair(b_dst, &pr.b, fb, n0, k);
+            tma_load_2d_pair(b_dst + kBK * 128, &pr.b, fb, n0 + 64, k);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
       // ---------------------------------------------------------------- MMA issuer (leader)
-      const uint32_t idesc = idesc_bf16_f32(256, kTN, true, true);
+      const uint32_t idesc = idesc_bf16_f32(256, 256, true, true);
       int g = 0, n = 0;
       for (int it = cid; it < P.total; it += ncl, ++n) {
         const Item w = decode(P, it);
+        const int nhi = (NH == 2 && w.tn * kTN + 256 >= P.prob[w.p].N) ? 1 : NH;
         int kb0, kb1;
         kb_range(w.slice, kb0, kb1);
-        const int b = n & 1;
-        mbar_wait(&tempty[b], ((n >> 1) & 1) ^ 1);
+        const int b = n % kNbuf;
+        mbar_wait(&tempty[b], ((n / kNbuf) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + 256u * (uint32_t)b;
+        const uint32_t d = tmem + 256u * NH * (uint32_t)b;
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % kStages;
           mbar_wait(&full[s], (g / kStages) & 1);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sStage + s * kStage), b_base = a_base + kHalf;
+          const uint32_t a_base = smem_u32(sStage + s * kStage);
           if (!(P.dbg & 2))
 #pragma unroll
           for (int ks = 0; ks < kBK / 16; ++ks)
-            mma_pair(d, smem_desc_sw128(a_base + ks * 2048, kBK * 128, 1024),
-                     smem_desc_sw128(b_base + ks * 2048, kBK * 128, 1024), idesc, (kb != kb0 || ks != 0));
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+              if (h < nhi)
+              mma_pair(d + 256u * h, smem_desc_sw128(a_base + ks * 2048, kBK * 128, 1024),
+                       smem_desc_sw128(a_base + kHalf * (1 + h) + ks * 2048, kBK * 128, 1024), idesc,
+                       (kb != kb0 || ks != 0));
           commit_pair(&used[s]);
           commit_pair(&empty[s]);
         }
@@ -184,11 +207,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     }
   } else if (warp >= 6) {
     // ------------------------------------------------------------------ bias gradient (warps 6..9)
-    // warp h sums K rows [16 h, 16 h + 16) of each stage; lane l reads 16 bytes (8 out-columns
-    // 8 (l % 16) .. + 7 of this CTA's 128: box (l % 16) / 8, chunk l % 8 of the SW128 row) of
-    // row 2 i + l / 16
+    // this CTA's dZ columns of a stage: 2 NH boxes of 64 (box bx = half bx / 2, CTA columns
+    // [64 (bx & 1), +64) of it).  Lane l reads 16 bytes (8 columns: box (l % 16NH) / 8, chunk
+    // l % 8 of the SW128 row) of K row RPI i + l / 16NH; warp h sums rows [RW h, RW h + RW)
+    constexpr int LPR = 16 * NH, RPI = 32 / LPR;          // lanes per row, rows per instruction
+    constexpr int RW = 64 / kBiasW;                       // K rows per bias warp
     const int hw = warp - 6;
-    const int box = (lane & 15) >> 3, chunk = lane & 7, rsub = lane >> 4;
+    const int box = (lane % LPR) >> 3, chunk = lane & 7, rsub = lane / LPR;
     int g = 0;
     for (int it = cid; it < P.total; it += ncl) {
       const Item w = decode(P, it);
@@ -202,8 +227,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         if (do_db) {
           const uint32_t base = smem_u32(sStage + s * kStage) + kHalf + (uint32_t)box * (kBK * 128);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = 16 * hw + 2 * i + rsub;
+          for (int i = 0; i < RW / RPI; ++i) {
+            const int r = RW * hw + RPI * i + rsub;
             const uint4 v = lds128(base + (uint32_t)r * 128u + (uint32_t)((chunk ^ (r & 7)) << 4));
             const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -218,30 +243,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         float c[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) f2_unpack(acc[j], c[2 * j], c[2 * j + 1]);
+        if (RPI == 2) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) c[j] += __shfl_xor_sync(0xffffffffu, c[j], 16);   // rows 2 i, 2 i + 1
-        if (lane < 16) {
-          float4* dst4 = reinterpret_cast<float4*>(sDb + 128 * hw + 8 * lane);
+          for (int j = 0; j < 8; ++j) c[j] += __shfl_xor_sync(0xffffffffu, c[j], 16);   // rows 2 i, 2 i + 1
+        }
+        if (lane < LPR) {                                   // this CTA's column 8 lane .. + 7
+          float4* dst4 = reinterpret_cast<float4*>(sDb + 128 * NH * hw + 8 * lane);
           dst4[0] = make_float4(c[0], c[1], c[2], c[3]);
           dst4[1] = make_float4(c[4], c[5], c[6], c[7]);
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (hw == 0) {                                    // 128 columns, 4 per lane
-          float4 o = reinterpret_cast<const float4*>(sDb)[lane];
-#pragma unroll
-          for (int h = 1; h < 4; ++h) {
-            const float4 t = reinterpret_cast<const float4*>(sDb + 128 * h)[lane];
-            o.x += t.x; o.y += t.y; o.z += t.z; o.w += t.w;
-          }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kBiasW) : "memory");
+        if (hw == 0) {                                    // 128 NH columns, 4 NH per lane
           const PdwProblem& pr = P.prob[w.p];
-          const int col = w.tn * kTN + 128 * (int)rank + 4 * lane;
-          float* dst = pr.db + (size_t)w.slice * (size_t)P.split_stride + col;
-          const float v[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (col + i < pr.N) dst[i] = v[i];
+          for (int h = 0; h < NH; ++h) {
+            const int cl = 128 * h + 4 * lane;            // CTA column: half h, 128 per half
+            float4 o = *reinterpret_cast<const float4*>(sDb + cl);
+#pragma unroll
+            for (int x = 1; x < kBiasW; ++x) {
+              const float4 t = *reinterpret_cast<const float4*>(sDb + 128 * NH * x + cl);
+              o.x += t.x; o.y += t.y; o.z += t.z; o.w += t.w;
+            }
+            const int col = w.tn * kTN + 256 * h + 128 * (int)rank + 4 * lane;
+            float* dst = pr.db + (size_t)w.slice * (size_t)P.split_stride + col;
+            const float v[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (col + i < pr.N) dst[i] = v[i];
+          }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");    // sDb reusable
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kBiasW) : "memory");    // sDb reusable
       }
     }
   } else {
@@ -255,15 +286,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     for (int it = cid; it < P.total; it += ncl, ++n) {
       const Item w = decode(P, it);
       const PdwProblem& pr = P.prob[w.p];
-      const int b = n & 1;
+      const int b = n % kNbuf;
       const int mrow0 = w.tm * 256 + 128 * (int)rank + 32 * q;
       const int ncol0 = w.tn * kTN;
       const int nch = min(kTN, pr.N - ncol0 + 63) / 64;   // 64-column chunks with data
       if (lane == 0) bulk_wait_read<0>();                 // staging of the previous item read
       __syncwarp();
-      mbar_wait(&tfull[b], (n >> 1) & 1);
+      mbar_wait(&tfull[b], (n / kNbuf) & 1);
       tc_fence_after();
-      const uint32_t tbase = tmem + 256u * (uint32_t)b + ((uint32_t)(q * 32) << 16);
+      const uint32_t tbase = tmem + 256u * NH * (uint32_t)b + ((uint32_t)(q * 32) << 16);
       uint32_t v[64];
       tmem_ld32_nowait(tbase, *reinterpret_cast<uint32_t(*)[32]>(v));
       tmem_ld32_nowait(tbase + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
@@ -272,7 +303,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         uint32_t f[64];
 #pragma unroll
         for (int i = 0; i < 64; ++i) f[i] = v[i];
-        if (c == nch - 1) {                               // accumulator b free for item n + 2
+        if (c == nch - 1) {                               // accumulator(s) b free for item n + kNbuf
           tc_fence_before();
           __syncwarp();
           if (lane == 0) arrive_remote(tempty_leader + 8u * (uint32_t)b);
@@ -281,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           tmem_ld32_nowait(tbase + 64u * (uint32_t)(c + 1) + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         }
         // chunk c: fp32 columns [64 c, 64 c + 32) and [64 c + 32, 64 c + 64) in buffers
-        // (2 c) % 4 and (2 c + 1) % 4, free once chunk c - 2's stores read them
+        // (2 c) % kNStg and (2 c + 1) % kNStg, free once chunk c - kNStg / 2's stores read them
         if (lane == 0 && c >= kNStg / 2) bulk_wait_read<kNStg / 2 - 1>();
         __syncwarp();
         const uint32_t b0 = stg0 + ((2 * c) % kNStg) * kStgBuf, b1 = stg0 + ((2 * c + 1) % kNStg) * kStgBuf;
@@ -313,6 +344,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 // -------------------------------------------------------------------------------- host side
 void pdw_init(PdwParams& P, int K, int splits, size_t split_stride) {
   P = PdwParams{};
+  const char* nh = std::getenv("CRL_PDW_NH");
+  P.nh = nh && std::atoi(nh) == 1 ? 1 : 2;
   P.K = K;
   P.splits = splits;
   const int nkb = (K + pdw::kBK - 1) / pdw::kBK;
@@ -345,29 +378,34 @@ bool pdw_add_problem(PdwParams& P, const __nv_bfloat16* X, int ldx, const __nv_b
   pr.db = db;
   pr.M = M;
   pr.N = N;
-  pr.tiles_n = (N + pdw::kTN - 1) / pdw::kTN;
+  pr.tiles_n = (N + 256 * P.nh - 1) / (256 * P.nh);
   pr.tiles = ((M + 255) / 256) * pr.tiles_n * P.splits;
   P.total += pr.tiles;
   ++P.n;
   return true;
 }
 
-cudaError_t tc_pdw_launch(const PdwParams& P, int num_sms, cudaStream_t st) {
+template <int NH>
+static cudaError_t launch_pdw(const PdwParams& P, int num_sms, cudaStream_t st) {
   static bool attr = false;
+  constexpr size_t smem = pdw::Cfg<NH>::kSmem;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_pdw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pdw::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(tc_pdw_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (P.total == 0) return cudaSuccess;
-  if (const char* d = std::getenv("CRL_PDW_DBG")) {
+  const int clusters = std::max(1, std::min(P.total, num_sms / 2));
+  if (const char* d = std::getenv("CRL_PDW_DBG")) {        // measurement ablations
     PdwParams Q = P;
     Q.dbg = std::atoi(d);
-    const int clusters = std::max(1, std::min(P.total, num_sms / 2));
-    return launch_pdl(tc_pdw_kernel, dim3(2 * clusters), dim3(320), pdw::kSmem, st, Q);
+    return launch_pdl(tc_pdw_kernel<NH>, dim3(2 * clusters), dim3(pdw::Cfg<NH>::kThreads), smem, st, Q);
   }
-  const int clusters = std::max(1, std::min(P.total, num_sms / 2));
-  return launch_pdl(tc_pdw_kernel, dim3(2 * clusters), dim3(320), pdw::kSmem, st, P);
+  return launch_pdl(tc_pdw_kernel<NH>, dim3(2 * clusters), dim3(pdw::Cfg<NH>::kThreads), smem, st, P);
+}
+
+cudaError_t tc_pdw_launch(const PdwParams& P, int num_sms, cudaStream_t st) {
+  if (P.total == 0) return cudaSuccess;
+  return P.nh == 1 ? launch_pdw<1>(P, num_sms, st) : launch_pdw<2>(P, num_sms, st);
 }
 
 }  // namespace tc

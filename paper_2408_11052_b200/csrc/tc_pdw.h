@@ -15,7 +15,7 @@ struct alignas(64) PdwProblem {
   CUtensorMap out;         // dW_l partial slices fp32 [S][M][N], box {32, 32, 1} (TMA stores)
   float* db;               // db_l slice 0 ([N]; slice s at + s * split_stride)
   int M, N;                // dW_l is [M = in][N = out]
-  int tiles_n, tiles;      // 256 x 256 tiles per slice along N; work items = tiles_m * tiles_n * S
+  int tiles_n, tiles;      // 256 x 256 nh tiles per slice along N; work items = tiles_m * tiles_n * S
 };
 
 struct PdwParams {
@@ -24,6 +24,7 @@ struct PdwParams {
   int K, splits, kb_per_split;
   long long split_stride;  // floats between partial slices (the parameter count)
   int dbg;                 // measurement ablations (env CRL_PDW_DBG): 1 no bias reads, 2 no MMA, 4 no TMA
+  int nh;                  // 256-column halves per item: 2 (256 x 512 tiles, default) or 1 (CRL_PDW_NH=1)
 };
 
 void pdw_init(PdwParams& P, int K, int splits, size_t split_stride);
