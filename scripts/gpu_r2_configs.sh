@@ -24,4 +24,6 @@ run sweep16384_cos --workload sweep16384 --energy cos
 run sweep16384_dot --workload sweep16384 --energy dot
 run sweep4096_cos --workload sweep4096 --energy cos
 run netscale_ln --workload netscale --layernorm
+run sweep16384_l2sq --workload sweep16384 --energy l2sq
+run netscale_l2sq --workload netscale --energy l2sq
 cat $OUT/lines.jsonl

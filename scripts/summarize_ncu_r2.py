@@ -13,7 +13,7 @@ import subprocess
 import sys
 
 STAGE = {"tc_grad2p_kernel": "grad_pair", "tc_stats_kernel": "lse_fused", "tc_dwg_kernel": "dw_db_grouped",
-         "adam_kernel": "adam", "grad_merge2_kernel": "grad_merge"}
+         "tc_pdw_kernel": "dw_db_pairs", "adam_kernel": "adam", "grad_merge2_kernel": "grad_merge"}
 METRICS = [("gpu__time_duration.sum", "us", 1e-3),
            ("dram__bytes_read.sum", "MB rd", 1e-6), ("dram__bytes_write.sum", "MB wr", 1e-6),
            ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "% tensor", 1),
