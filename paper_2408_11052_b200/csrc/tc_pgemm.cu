@@ -48,15 +48,17 @@ constexpr uint32_t kAHalf = 128 * kBK * 2;          // 16 KB: this CTA's 128 row
 constexpr uint32_t kBHalf = 128 * kBK * 2;          // 16 KB: this CTA's 128 columns of B
 constexpr uint32_t kStage = kAHalf + kBHalf;
 constexpr uint32_t kStgBuf = 32 * 128;             // 4 KB: 32 rows x 128 B (SW128) staging
-#ifndef PG_EPIW
-#define PG_EPIW 4
-#endif
-// epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, every other 64-column
-// chunk each).  Measured on B200 (scratch/pgemm_test.cu, 16384 x 1024 x 1024): 34.3 us with 4,
-// 35.0 with 8 -- the epilogue's cost is its output traffic (Z and act(Z): 64 MB), not warps
-constexpr int kEpiW = PG_EPIW;
-constexpr int kNStg = kEpiW == 8 ? 2 : 4;           // staging buffers per epilogue warp
-constexpr size_t kSmem = 1024 + kStages * kStage + kEpiW * kNStg * kStgBuf + 256;
+// epilogue warps EW: 4 (one per TMEM lane quarter, 4 staging buffers each) or 8 (two per
+// quarter, every other 64-column chunk each, 2 buffers): the same 64 KB of staging.  Measured on
+// B200 (scratch/pgemm_test.cu, 16384 x 1024 x 1024): 34.3 us with 4, 35.0 with 8 -- an SMEM-bound
+// mainloop leaves the epilogue no bandwidth to gain; the short-K layers (K <= 256: the first
+// layer, the output layer's dX) are epilogue-bound and take 8
+template <int EW>
+struct Epi {
+  static constexpr int kEpiW = EW;
+  static constexpr int kNStg = EW == 8 ? 2 : 4;     // staging buffers per epilogue warp
+};
+constexpr size_t kSmem = 1024 + kStages * kStage + 16 * kStgBuf + 256;
 
 // number of 64-column chunks c = h, h + nh, ... below nch (a warp's chunks in one tile)
 __host__ __device__ __forceinline__ int ci_count(int nch, int h, int nh) { return nch > h ? (nch - 1 - h) / nh + 1 : 0; }
@@ -96,10 +98,11 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 
 }  // namespace pg
 
-template <int EPI, int ACT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW, 1)
+template <int EPI, int ACT, int EW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
     tc_pgemm_kernel(const __grid_constant__ PgemmJob J) {
   using namespace pg;
+  constexpr int kEpiW = Epi<EW>::kEpiW, kNStg = Epi<EW>::kNStg;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sStage = smem;
@@ -270,8 +273,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
           for (int i4 = 0; i4 < 16; ++i4) bb[i4] = __ldg(reinterpret_cast<const float4*>(p.bias + ncol0 + 64 * c) + i4);
         }
       };
-      issue(c_first);
+      // 4 epilogue warps: chunk c + c_step's loads in flight while chunk c is processed; 8 warps
+      // (two per lane quarter hide each other's latency) load chunk by chunk (register budget)
+      constexpr bool kPipe = EW == 4;
+      if (kPipe) issue(c_first);
       for (int c = c_first, ci = 0; c < nch; c += c_step, ++ci) {
+        if (!kPipe) issue(c);
         tmem_ld_wait();
         if (trc && c < 4) p.trace[(it * 4 + c) * 4 + 0] = clock64();
         f32x2 f2[32];                                     // the chunk's 64 values as packed pairs
@@ -289,7 +296,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * pg::kEpiW,
           __syncwarp();
           if (lane == 0) arrive_remote(tempty_leader + 8u * (uint32_t)b);
         } else {
-          issue(c + c_step);
+          if (kPipe) issue(c + c_step);
         }
         const int n = ncol0 + 64 * c;
         if (EPI == PG_DX) {
@@ -441,22 +448,32 @@ bool tc_pgemm_supported(int M, int N, int K) {
   return M >= 256 && N >= 256 && N % 64 == 0 && K >= 1 && !std::getenv("CRL_NO_PGEMM");
 }
 
-template <int EPI, int ACT>
+template <int EPI, int ACT, int EW>
 static cudaError_t launch_pg(const PgemmJob& J, int num_sms, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_pgemm_kernel<EPI, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(tc_pgemm_kernel<EPI, ACT, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)pg::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int clusters = std::max(1, std::min(J.total, num_sms / 2));
-  return launch_pdl(tc_pgemm_kernel<EPI, ACT>, dim3(2 * clusters), dim3(64 + 32 * pg::kEpiW), pg::kSmem, st, J);
+  return launch_pdl(tc_pgemm_kernel<EPI, ACT, EW>, dim3(2 * clusters), dim3(64 + 32 * EW), pg::kSmem, st, J);
+}
+template <int EPI, int ACT>
+static cudaError_t launch_pg_ew(const PgemmJob& J, int num_sms, cudaStream_t st) {
+  // short K (<= 256): the epilogue is the bound, twice the epilogue warps
+  int kmax = J.args[0].K;
+  if (J.np > 1) kmax = std::max(kmax, J.args[1].K);
+  const char* e = std::getenv("CRL_PG_EPIW");
+  const int ew = e ? std::atoi(e) : (kmax <= 256 ? 8 : 4);
+  if (ew == 8) return launch_pg<EPI, ACT, 8>(J, num_sms, st);
+  return launch_pg<EPI, ACT, 4>(J, num_sms, st);
 }
 template <int EPI>
 static cudaError_t launch_pg_act(const PgemmJob& J, int num_sms, cudaStream_t st) {
-  if (EPI == PG_FWD_OUT || J.args[0].act == CRL_ACT_SILU) return launch_pg<EPI, CRL_ACT_SILU>(J, num_sms, st);
-  return launch_pg<EPI, CRL_ACT_RELU>(J, num_sms, st);
+  if (EPI == PG_FWD_OUT || J.args[0].act == CRL_ACT_SILU) return launch_pg_ew<EPI, CRL_ACT_SILU>(J, num_sms, st);
+  return launch_pg_ew<EPI, CRL_ACT_RELU>(J, num_sms, st);
 }
 static int pg_tiles(const PgemmArgs& p) { return ((p.M + 255) / 256) * ((p.N + pg::kTN - 1) / pg::kTN); }
 
