@@ -167,6 +167,7 @@ __device__ void gradf_loss_finish(const TcGradFArgs& p, int a0, float s1, float 
 template <int ENERGY>
 __device__ __forceinline__ float gf_diag_logit(float x, float na, float nb) {
   if (ENERGY == CRL_ENERGY_L2) return -sqrtf(x + kEpsL2);
+  if (ENERGY == CRL_ENERGY_L2SQ) return -x;
   if (ENERGY == CRL_ENERGY_COS) return x / (fmaxf(sqrtf(na), kEpsCos) * fmaxf(sqrtf(nb), kEpsCos));
   return x;
 }
@@ -184,7 +185,7 @@ __device__ void gradf_loss_rows_warp(const TcGradFArgs& p, int a0, int t) {
 #pragma unroll 4
     for (int k = 0; k < 16; ++k) {
       const float4 u = a[k], v = b[k];
-      if (ENERGY == CRL_ENERGY_L2) {
+      if (ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) {
         x = fmaf(u.x - v.x, u.x - v.x, x); x = fmaf(u.y - v.y, u.y - v.y, x);
         x = fmaf(u.z - v.z, u.z - v.z, x); x = fmaf(u.w - v.w, u.w - v.w, x);
       } else {
@@ -217,7 +218,7 @@ __device__ void gradf_loss_rows_epi(const TcGradFArgs& p, int a0, int t) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const float4 u = a[k], v = b[k];
-    if (ENERGY == CRL_ENERGY_L2) {
+    if (ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) {
       x = fmaf(u.x - v.x, u.x - v.x, x); x = fmaf(u.y - v.y, u.y - v.y, x);
       x = fmaf(u.z - v.z, u.z - v.z, x); x = fmaf(u.w - v.w, u.w - v.w, x);
     } else {
@@ -279,6 +280,8 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
   using C = GfCfg;
   constexpr int BNT = C::BNT, STAGES = C::STAGES, D = C::D;
   constexpr bool L2 = ENERGY == CRL_ENERGY_L2;
+  constexpr bool SQ = ENERGY == CRL_ENERGY_L2SQ;                 // L2^2: l = -d2, w = 2 g
+  constexpr bool DIFF = L2 || SQ;                                // -(sum w) a terms: column sums, row sums
   constexpr bool COS = ENERGY == CRL_ENERGY_COS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
-  if (L2)
+  if (DIFF)
     for (int i = threadIdx.x; i < (int)(C::ONES_BYTES / 16); i += blockDim.x)
       reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
   } else if (warp == 2 && lane == 0) {
     // ------------------------------------------------------------------ back-MMA issuer
     const uint32_t id_da = idesc_bf16_f32(128, D, false, true);      // A = W (K-major), B = B tile (MN)
-    const uint32_t id_db = idesc_bf16_f32(128, L2 ? C::NDB : D, true, true);   // A = W^T, B = [A | 1] (MN)
+    const uint32_t id_db = idesc_bf16_f32(128, DIFF ? C::NDB : D, true, true);   // A = W^T, B = [A | 1] (MN)
     mbar_wait(a_full, 0);
     const uint32_t a_base = smem_u32(sA);
     for (int t = 0; t < ntiles; ++t) {
@@ -435,10 +438,10 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
     const float cc0 = p.invN * p.c_c;
     const float rmask = rv ? 1.f : 0.f;
     constexpr float L2e2 = gf::kLog2e * gf::kLog2e;
-    const float a_l2 = (astat + kEpsL2) * L2e2;
+    const float a_l2 = SQ ? astat * gf::kLog2e : (astat + kEpsL2) * L2e2;
     // L2: w = g rs' L.  cos: l = (a.b) r_i s_j and the MMA operand is w' = g r_i s_j (both
     // sides' dot-form partials come out pre-scaled; grad_merge projects them, A-05)
-    const float lsc = L2 ? gf::kLog2e : (COS ? astat : 1.f);
+    const float lsc = L2 ? gf::kLog2e : (SQ ? 2.f : (COS ? astat : 1.f));
     const float nLr = -gf::kLog2e * astat;        // cos: -L r_i
     const float EiL = Ei * lsc, ArowL = Arow * lsc, cc0L = cc0 * lsc;
     const uint32_t w_row = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
@@ -455,12 +458,12 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
       tc_fence_after();
       uint32_t v[32], cs = 0u;
       tmem_ld32_nowait(tdb + 32 * k, v);           // d columns [32 k, 32 k + 32)
-      if (L2 && k == 0) gf::tmem_ld1_nowait(tdb + D, cs);   // column 64: sum_i w_ij
+      if (DIFF && k == 0) gf::tmem_ld1_nowait(tdb + D, cs);   // column 64: sum_i w_ij
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&db_empty[bu]);
-      if (L2 && k == 0 && j0 + r < jend) atomicAdd(p.cs_acc + j0 + r, __uint_as_float(cs));
+      if (DIFF && k == 0 && j0 + r < jend) atomicAdd(p.cs_acc + j0 + r, __uint_as_float(cs));
       if (storer) gf::bulk_wait_read0();            // the reduction of u - 2 has read the buffer
       asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
       const uint32_t dst = smem_u32(sR + bu * C::R_BYTES + k * 16384) + w_row;
@@ -536,6 +539,11 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                     rs1 = gf::rsq_abs(d1);
                   }
                   f2_unpack(f2_fma(d2, f2_pack(rs0, rs1), f2_pack(lr2, lr2)), t0, t1);
+                } else if (SQ) {                          // t = max(d2 L, 0) + lse2_i
+                  float d0, d1;
+                  f2_unpack(f2_fma(f2_pack(-2.f * gf::kLog2e, -2.f * gf::kLog2e), v2,
+                                   f2_fma(f2_pack(gf::kLog2e, gf::kLog2e), b2, f2_pack(a_l2, a_l2))), d0, d1);
+                  f2_unpack(f2_add(f2_pack(fmaxf(d0, 0.f), fmaxf(d1, 0.f)), f2_pack(lr2, lr2)), t0, t1);
                 } else if (COS) {
                   f2_unpack(f2_fma(f2_mul(v2, b2), f2_pack(nLr, nLr), f2_pack(lr2, lr2)), t0, t1);
                 } else {
@@ -546,10 +554,8 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                   t1 = c0 + i + 1 < nval ? t1 : INFINITY;
                 }
                 f32x2 wv = f2_mul(f2_pack(gf::ex2_neg(t0), gf::ex2_neg(t1)), fac);
-                if (L2) {
-                  wv = f2_mul(wv, f2_pack(rs0, rs1));
-                  wsum2 = f2_add(wsum2, wv);
-                }
+                if (L2) wv = f2_mul(wv, f2_pack(rs0, rs1));
+                if (DIFF) wsum2 = f2_add(wsum2, wv);
                 if (COS) wv = f2_mul(wv, b2);
                 f2_unpack(wv, w[i], w[i + 1]);
               }
@@ -565,6 +571,8 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                   const float d2 = fmaf(-2.f * L2e2, v, fmaf(L2e2, bb[u], a_l2));
                   rs = gf::rsq_abs(d2);
                   l2v = -fabsf(d2) * rs;
+                } else if (SQ) {
+                  l2v = -fmaxf(fmaf(-2.f * gf::kLog2e, v, fmaf(gf::kLog2e, bb[u], a_l2)), 0.f);
                 } else if (COS) {
                   l2v = v * bb[u] * (-nLr);
                 } else {
@@ -573,7 +581,8 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
                 if (MASK) l2v = c0 + i < nval ? l2v : -INFINITY;
                 const float qe = gf::ex2(l2v - ff[u] * gf::kLog2e);
                 float wv = fmaf(gf::ex2(l2v - lr2), ArowL, qe * cc0L) * rmask;
-                if (L2) { wv *= rs; wsum2 = f2_add(wsum2, f2_pack(wv, 0.f)); }
+                if (L2) wv *= rs;
+                if (DIFF) wsum2 = f2_add(wsum2, f2_pack(wv, 0.f));
                 if (COS) wv *= bb[u];
                 w[i] = wv;
               }
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
     const float wsum = ws0 + ws1;
     if (wgid > 0) sMerge[(wgid - 1) * 128 + r] = wsum;
     asm volatile("bar.sync 1, 512;" ::: "memory");
-    if (wgid == 0 && rv && L2) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[r] + sMerge[128 + r] + sMerge[256 + r];
+    if (wgid == 0 && rv && DIFF) p.part_rs[(size_t)split * p.Na + row] = wsum + sMerge[r] + sMerge[128 + r] + sMerge[256 + r];
     mbar_wait(da_full, 0);
     tc_fence_after();
     {
@@ -642,7 +651,8 @@ __global__ void __launch_bounds__(GfCfg::NT, 1) tc_gradf_kernel(const __grid_con
 bool make_map_f32(CUtensorMap*, const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t);
 
 bool tc_gradf_supports(int D, int energy) {
-  return D == 64 && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_DOT || energy == CRL_ENERGY_COS);
+  return D == 64 && (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_L2SQ || energy == CRL_ENERGY_DOT ||
+                     energy == CRL_ENERGY_COS);
 }
 
 // column splits minimising the makespan (waves x tiles per CTA) of the rb x S grid, <= 16
@@ -700,8 +710,9 @@ cudaError_t tc_grad_fused(int energy, const CUtensorMap& mA, const CUtensorMap& 
   p.loss_acc = loss.acc; p.loss_out = loss.out; p.skip = loss.skip; p.adam_t = loss.adam_t; p.status = loss.status;
   p.loss_cf = loss.c_f; p.loss_cb = loss.c_b; p.loss_beta = loss.beta;
   p.dbg = std::getenv("CRL_GF_DBG") ? std::atoi(std::getenv("CRL_GF_DBG")) : 0;
-  cudaError_t e = energy == CRL_ENERGY_L2    ? launch_gf<CRL_ENERGY_L2>(mA, mB, mDB, p, S, st)
-                  : energy == CRL_ENERGY_COS ? launch_gf<CRL_ENERGY_COS>(mA, mB, mDB, p, S, st)
+  cudaError_t e = energy == CRL_ENERGY_L2     ? launch_gf<CRL_ENERGY_L2>(mA, mB, mDB, p, S, st)
+                  : energy == CRL_ENERGY_L2SQ ? launch_gf<CRL_ENERGY_L2SQ>(mA, mB, mDB, p, S, st)
+                  : energy == CRL_ENERGY_COS  ? launch_gf<CRL_ENERGY_COS>(mA, mB, mDB, p, S, st)
                                              : launch_gf<CRL_ENERGY_DOT>(mA, mB, mDB, p, S, st);
   if (e != cudaSuccess) return e;
   const float Cdiag = invN * (c_r + c_c);
