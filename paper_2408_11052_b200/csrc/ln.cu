@@ -178,7 +178,14 @@ __global__ void __launch_bounds__(256) ln_fwd_bf16_kernel(int Bn, const __nv_bfl
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       y[i] = fmaf(gg[i], (z[j][i] - m) * r, bb[i]);
-      x[i] = act == CRL_ACT_SILU ? y[i] / (1.f + __expf(-y[i])) : fmaxf(y[i], 0.f);
+      if (act == CRL_ACT_SILU) {                         // SiLU(y) = h + h tanh(h), h = y / 2 (as the GEMM epilogues)
+        const float h = 0.5f * y[i];
+        float t;
+        asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+        x[i] = fmaf(h, t, h);
+      } else {
+        x[i] = fmaxf(y[i], 0.f);
+      }
     }
     uint4 oy, ox;
     __nv_bfloat162 t;
@@ -277,19 +284,41 @@ __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(int Bn, int rows_per_b
   for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) part[(size_t)blockIdx.x * 2 * N + k] = red[k];
 }
 
-// dgamma / dbeta = the sum of the CTA partials in CTA order, into K slice 0 of the gradient
-// buffer; the other slices (summed by Adam) get zeros
-__global__ void ln_param_reduce_kernel(int N, int nblk, const float* __restrict__ part, float* __restrict__ dgamma,
-                                       float* __restrict__ dbeta, int S, size_t split_stride) {
+// dgamma / dbeta = the sum of the CTA partials, into K slice 0 of the gradient buffer; the other
+// slices (summed by Adam) get zeros.  One CTA per 32 columns: warp w sums partials w, w + 8, ...
+// of its lane's column (coalesced 128 B rows, many loads in flight), then the 8 warp sums are
+// added in warp order (deterministic).  (One thread per column walking all nblk partials left
+// 8 CTAs on the whole GPU: ~30 us per call, latency-bound.)
+__global__ void __launch_bounds__(256) ln_param_reduce_kernel(int N, int nblk, const float* __restrict__ part,
+                                                              float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                              int S, size_t split_stride) {
+  __shared__ float red[8][32];
   pdl_wait();
   pdl_launch();
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= 2 * N) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 32 + lane;
   float t = 0.f;
-  for (int b = 0; b < nblk; ++b) t += part[(size_t)b * 2 * N + k];
+  if (k < 2 * N) {
+    float t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    int b = warp;
+    for (; b + 24 < nblk; b += 32) {
+      t += part[(size_t)b * 2 * N + k];
+      t1 += part[(size_t)(b + 8) * 2 * N + k];
+      t2 += part[(size_t)(b + 16) * 2 * N + k];
+      t3 += part[(size_t)(b + 24) * 2 * N + k];
+    }
+    for (; b < nblk; b += 8) t += part[(size_t)b * 2 * N + k];
+    t = (t + t1) + (t2 + t3);
+  }
+  red[warp][lane] = t;
+  __syncthreads();
+  if (warp != 0 || k >= 2 * N) return;
+  float o = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) o += red[w][lane];
   float* dst = k < N ? dgamma + k : dbeta + (k - N);
-  dst[0] = t;
-  for (int s = 1; s < S; ++s) dst[(size_t)s * split_stride] = 0.f;
+  dst[0] = o;
+  for (int s2 = 1; s2 < S; ++s2) dst[(size_t)s2 * split_stride] = 0.f;
 }
 
 bool ln_bf16_supports(int N) { return N % 256 == 0 && N >= 256 && N <= 1024; }
@@ -320,7 +349,7 @@ cudaError_t launch_ln_bwd_bf16(int Bn, int N, __nv_bfloat16* dYZ, const __nv_bfl
     case 4: e = launch_pdl(ln_bwd_bf16_kernel<4>, grid, blk, 0, st, Bn, rpb, dYZ, Z, mu, rstd, gamma, part); break;
   }
   if (e != cudaSuccess) return e;
-  return launch_pdl(ln_param_reduce_kernel, dim3((2 * N + 255) / 256), dim3(256), 0, st, N, nblk,
+  return launch_pdl(ln_param_reduce_kernel, dim3((2 * N + 31) / 32), dim3(256), 0, st, N, nblk,
                     (const float*)part, dgamma, dbeta, S, split_stride);
 }
 
