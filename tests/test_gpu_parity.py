@@ -877,3 +877,32 @@ def test_critic_step_forced_dist_path(preset, prec, batch, extra, monkeypatch):
         _critic_parity(cfg)
     else:
         _critic_parity(cfg, tol_loss=tol, tol_grad=tol)
+
+
+@pytest.mark.parametrize("knobs", [
+    {},                                        # defaults: pdw 256 x 512 items, merged pair GEMMs
+    {"CRL_PDW_NH": "1"},                       # 256 x 256 dW items, double-buffered accumulators
+    {"CRL_NO_PG_MERGE": "1"},                  # one pair-GEMM launch per encoder and layer
+    {"CRL_PG_EPIW": "4"},                      # 4 epilogue warps on the short-K layers too
+    {"CRL_PG_EPIW": "8"},                      # 8 epilogue warps on every layer
+    {"CRL_NO_PDW": "1"},                       # the grouped single-CTA dW kernel
+])
+def test_critic_step_bf16_wide_kernel_variants(knobs, monkeypatch):
+    """The wide-encoder kernels' selectable variants (round 2: tc_pdw items of 256 x 512 / 256 x
+    256, tc_pgemm2 merged launches, 4 / 8 epilogue warps) against the oracle, per tensor: a
+    ragged batch over 2 K slices and widths where the first / output layers are short-K."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    cfg = crl_synth.preset("ant", batch=1100, width=512, repr_dim=256, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("buckets", ["1", "3", "8"])
+def test_critic_step_forced_dist_buckets(buckets, monkeypatch):
+    """C4: the gradient all-reduce in 1 / 3 / 8 buckets (bucket sizes rounded to 256 floats, a
+    short last bucket, Adam per bucket on the communication-stream events) on the one-rank
+    communicator, against the oracle."""
+    monkeypatch.setenv("CRL_FORCE_DIST", "1")
+    monkeypatch.setenv("CRL_AR_BUCKETS", buckets)
+    cfg = crl_synth.preset("ant", batch=600, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
