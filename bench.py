@@ -106,9 +106,12 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
-    def stop(self):
+    def stop(self, t_lo=None, t_hi=None):
+        """Samples taken in [t_lo, t_hi] (host monotonic clock around the timed region; the
+        sampler runs from before the warm-up so nvidia-smi is up when timing starts).  A timed
+        region shorter than one 100 ms sample period keeps the samples nearest to it."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.15)
@@ -119,7 +122,13 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if t_lo is not None and t_hi is not None:
+            inside = [x for x in lines if t_lo <= x[0] <= t_hi + 0.1]
+            if not inside and lines:                   # nearest samples around a short region
+                inside = sorted(lines, key=lambda x: min(abs(x[0] - t_lo), abs(x[0] - t_hi)))[:2]
+            lines = inside
+        for _, ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -468,6 +477,8 @@ def run_ours(args):
         sl = slice(k * Bl, (k + 1) * Bl)
         ctx.critic_step(s_all[sl], a_all[sl], g_all[sl], loss, stream=stream)
 
+    clk = ClockSampler(local)                      # nvidia-smi up before the timed region
+    clk.start()
     for i in range(max(args.warmup, nb)):          # every slice's graph captured before timing
         step(i)
     launches_per_step = 1.0 / nb + ctx.launch_count()
@@ -477,8 +488,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    clk = ClockSampler(local)
-    clk.start()
+    t_lo = time.monotonic()
     t0 = -(-max(args.warmup, nb) // nb) * nb       # timed steps start on a bulk boundary
     n_bulk = sum(1 for i in range(args.steps) if nb > 1 and (t0 + i) % nb == 0)
     with torch.cuda.stream(stream):
@@ -488,7 +498,7 @@ def run_ours(args):
             step(t0 + i)
             ev1[i].record(stream)
     torch.cuda.synchronize()
-    clocks = clk.stop()
+    clocks = clk.stop(t_lo, time.monotonic())
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
