@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4 * NWG);
       mbar_init(&e_full[i], 4 * NWG); mbar_init(&e_empty[i], 1);
-      mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 1);
+      mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 4);
       mbar_init(&st_full[i], 1); mbar_init(&st_empty[i], 4 * NWG);
     }
     fence_mbar_init();
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tm_s[2] = {tmem, tmem + 128};
-  const uint32_t tm_c[2] = {tmem + 256, tmem + 384};
+  const uint32_t tm_c[2] = {tmem + 256, tmem + 272};   // [128 columns j (lanes)] x 16 (column 0 used)
   pdl_wait();
   pdl_launch();
   __shared__ long long s_tr[4][16];
@@ -234,7 +234,10 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
   } else if (warp == 1 && lane == 0) {
     // ------------------------------------------------------------------ MMA issuer
     const uint32_t id_s = idesc_bf16_f32(128, BNT, false, false);
-    const uint32_t id_c = idesc_bf16_f32(128, BNT, false, true);     // B = E is MN-major
+    // column sums as C^T = E^T 1: A = E^T (MN-major: M = the 128 columns j), B = ones (K-major,
+    // N = 16): per tile 8 N = 16 MMAs reading 36 KB of SMEM (the 1 E form read 64 KB into a
+    // 128-column accumulator whose rows were all equal)
+    const uint32_t id_c = idesc_bf16_f32(128, 16, true, false);
     const uint32_t ones = smem_u32(sOnes);
     auto issue_c = [&](int g) {
       const int b = g & 1, eb = g % NE;
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
       // 64-column halves of E are 16 KB apart (LBO); the ones chunk serves both K halves
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks)
-        mma_bf16(tm_c[b], smem_desc_sw128(ones + (ks & 3) * 32, 16, 1024), smem_desc_sw128(e_base + ks * 2048, 16384, 1024),
+        mma_bf16(tm_c[b], smem_desc_sw128(e_base + ks * 2048, 16384, 1024), smem_desc_sw128(ones + (ks & 3) * 32, 16, 1024),
                  id_c, ks != 0);
       mma_commit(&c_full[b]);
       mma_commit(&e_empty[eb]);
@@ -282,35 +285,6 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
       }
     }
     if (g > 0) issue_c(g - 1);
-  } else if (warp == 3) {
-    // ------------------------------------------------------------------ column-sum readout
-    // every TMEM row of C holds the same 128 column sums; this warp reads its lane quarter
-    int g = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += G) {
-      float* out = p.colpart + (size_t)unit_rb(u) * p.ldc;
-      const int nt = unit_ntiles(u), j00 = unit_j0(u);
-      const int jend = min(p.Nb, j00 + p.tiles_per_chunk * BNT);
-      for (int t = 0; t < nt; ++t, ++g) {
-        const int b = g & 1;
-        const int j0 = j00 + t * BNT;
-        mbar_wait(&c_full[b], (g >> 1) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t v[32];
-          tmem_ld32_nowait(tm_c[b] + (96u << 16) + 32 * c, v);
-          tmem_ld_wait();
-          uint32_t mine = 0;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) mine = (i == lane) ? v[i] : mine;
-          const int j = j0 + 32 * c + lane;
-          if (j < jend) out[j] = __uint_as_float(mine);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&c_empty[b]);
-      }
-    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
     // NWG warpgroups split the 128 columns of a tile (CW each): 4 warps per SMSP hide the
@@ -321,6 +295,22 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
     constexpr float L2e2 = fs::kLog2e * fs::kLog2e;
     const uint32_t e_row = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
     const int cg0 = wg * CW;                              // first column of this group
+    // column sums of tile x (C(x) in TMEM lane j = column j): read by warpgroup x % NWG two
+    // tiles later (C(x) is long complete by then), one 32x32b.x1 TMEM load per warp
+    int cs_rb[2] = {0, 0}, cs_j0[2] = {0, 0}, cs_jend[2] = {0, 0};   // tile x's unit, by x & 1
+    auto read_cs = [&](int x) {
+      const int bx = x & 1;
+      mbar_wait(&c_full[bx], (x >> 1) & 1);
+      tc_fence_after();
+      uint32_t v;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tm_c[bx] + ((uint32_t)(q * 32) << 16)));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c_empty[bx]);
+      const int j = cs_j0[bx] + q * 32 + lane;
+      if (j < cs_jend[bx]) p.colpart[(size_t)cs_rb[bx] * p.ldc + j] = __uint_as_float(v);
+    };
     int g = 0;
     for (int u = blockIdx.x; u < p.n_units; u += G) {
       const int row = unit_rb(u) * 128 + r;
@@ -342,6 +332,8 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
       for (int t = 0; t < nt; ++t, ++g) {
         const int b = g & 1, eb = g % NE;
         const int nval = jend - (j00 + t * BNT);
+        if (g >= 2 && wg == (g - 2) % NWG) read_cs(g - 2);
+        cs_rb[b] = unit_rb(u); cs_j0[b] = j00 + t * BNT; cs_jend[b] = jend;   // (tile g - 2's slot is read)
         mbar_wait(&st_full[b], (g >> 1) & 1);
         mbar_wait(&s_full[b], (g >> 1) & 1);
         if (trace && threadIdx.x == 128 && g < 15) s_tr[2][g + 1] = clock64();
@@ -440,6 +432,8 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
       }
       asm volatile("bar.sync 1, %0;" ::"n"(128 * NWG) : "memory");   // sM reusable
     }
+    for (int x = g - 2 < 0 ? 0 : g - 2; x < g; ++x)
+      if (wg == x % NWG) read_cs(x);
   }
   tc_fence_before();
   __syncthreads();
