@@ -96,6 +96,10 @@ struct TcStatsArgs {
 };
 
 constexpr int kStNWG = 4;          // epilogue warpgroups
+#ifndef CRL_ST_NS
+#define CRL_ST_NS 2
+#endif
+constexpr int kNS = CRL_ST_NS;     // S accumulators in TMEM (2 or 3: 128 columns each; 3 measured equal at netscale)
 #ifndef CRL_ST_EMU
 #define CRL_ST_EMU 0
 #endif
@@ -151,9 +155,9 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
   uint64_t* a_empty = a_full + 2;         // [2]
   uint64_t* b_full = a_empty + 2;         // [STAGES]
   uint64_t* b_empty = b_full + STAGES;    // [STAGES]
-  uint64_t* s_full = b_empty + STAGES;    // [2]
-  uint64_t* s_empty = s_full + 2;         // [2]
-  uint64_t* e_full = s_empty + 2;         // [2]
+  uint64_t* s_full = b_empty + STAGES;    // [kNS]
+  uint64_t* s_empty = s_full + kNS;       // [kNS]
+  uint64_t* e_full = s_empty + kNS;       // [2]
   uint64_t* e_empty = e_full + 2;         // [2]
   uint64_t* c_full = e_empty + 2;         // [2]
   uint64_t* c_empty = c_full + 2;         // [2]
@@ -179,8 +183,9 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
     // a B piece is free once the S MMAs that read it completed; the column statistics of a
     // tile have their own 2-slot ring, freed by the epilogue warps
     for (int s = 0; s < STAGES; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
+    for (int i = 0; i < kNS; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4 * NWG); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4 * NWG);
+
       mbar_init(&e_full[i], 4 * NWG); mbar_init(&e_empty[i], 1);
       mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 4);
       mbar_init(&st_full[i], 1); mbar_init(&st_empty[i], 4 * NWG);
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tm_s[2] = {tmem, tmem + 128};
+  const uint32_t tm_s[3] = {tmem, tmem + 128, tmem + 384};   // kNS S accumulators (C sits at 256..287)
   const uint32_t tm_c[2] = {tmem + 256, tmem + 272};   // [128 columns j (lanes)] x 16 (column 0 used)
   pdl_wait();
   pdl_launch();
@@ -262,8 +267,8 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
       const int nt = unit_ntiles(u);
       if (nt == 0) mma_commit(&a_empty[ua]);                // empty chunk: hand the A buffer back
       for (int t = 0; t < nt; ++t, ++g) {
-        const int b = g & 1;
-        mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+        const int b = g % kNS;
+        mbar_wait(&s_empty[b], ((g / kNS) & 1) ^ 1);
         if (trace && g < 15) s_tr[1][g + 1] = clock64();
 #pragma unroll
         for (int pp = 0; pp < NP; ++pp, ++pc) {
@@ -334,18 +339,19 @@ __global__ void __launch_bounds__(128 + 128 * kStNWG, 1) tc_stats_kernel(const _
         const int nval = jend - (j00 + t * BNT);
         if (g >= 2 && wg == (g - 2) % NWG) read_cs(g - 2);
         cs_rb[b] = unit_rb(u); cs_j0[b] = j00 + t * BNT; cs_jend[b] = jend;   // (tile g - 2's slot is read)
+        const int sb = g % kNS;
         mbar_wait(&st_full[b], (g >> 1) & 1);
-        mbar_wait(&s_full[b], (g >> 1) & 1);
+        mbar_wait(&s_full[sb], (g / kNS) & 1);
         if (trace && threadIdx.x == 128 && g < 15) s_tr[2][g + 1] = clock64();
         tc_fence_after();
         uint32_t raw[NCH][32];
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
-          tmem_ld32_nowait(tm_s[b] + ((uint32_t)(q * 32) << 16) + cg0 + 32 * c, raw[c]);
+          tmem_ld32_nowait(tm_s[sb] + ((uint32_t)(q * 32) << 16) + cg0 + 32 * c, raw[c]);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[b]);
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
         const uint32_t st_a = smem_u32(sStat + b * BNT + cg0);
         const uint32_t e_a = smem_u32(sE + eb * C::E_BYTES + (cg0 >> 6) * 16384) + e_row;
         // two instantiations: full tiles carry no per-element column mask (a uniform `if`
