@@ -59,19 +59,11 @@ __global__ void __launch_bounds__(256) loss_partial_kernel(
     const float* a = phi + (size_t)i * D;
     const float* b = psi + (size_t)i * D;
     float x = 0.f, na = 0.f, nb = 0.f;
-    auto term = [&](float av, float bv) {
+    for (int k = lane; k < D; k += 32) {
+      const float av = a[k], bv = b[k];
       if (energy == CRL_ENERGY_L2 || energy == CRL_ENERGY_L2SQ) { const float d = av - bv; x = fmaf(d, d, x); }
       else if (energy == CRL_ENERGY_L1) x += fabsf(av - bv);
       else { x = fmaf(av, bv, x); na = fmaf(av, av, na); nb = fmaf(bv, bv, nb); }
-    };
-    if ((D & 127) == 0) {                        // 16 B per lane, every load of the row in flight
-#pragma unroll 4
-      for (int k = 4 * lane; k < D; k += 128) {
-        const float4 av = *reinterpret_cast<const float4*>(a + k), bv = *reinterpret_cast<const float4*>(b + k);
-        term(av.x, bv.x); term(av.y, bv.y); term(av.z, bv.z); term(av.w, bv.w);
-      }
-    } else {
-      for (int k = lane; k < D; k += 32) term(a[k], b[k]);
     }
     x = warp_sum(x);
     float l;
