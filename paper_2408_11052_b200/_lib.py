@@ -12,7 +12,9 @@ import os
 from dataclasses import dataclass, field
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcrl.so")
+# CRL_LIB_PATH: an alternative build of the same library (A/B measurements of compile-time
+# variants, e.g. `make OUT=... BUILD=... NVFLAGS_EXTRA=-D...`); the in-tree build by default
+LIB_PATH = os.environ.get("CRL_LIB_PATH") or os.path.join(_HERE, "libcrl.so")
 
 CRL_OK, CRL_EINVAL, CRL_ESTATE, CRL_ECUDA, CRL_ENCCL, CRL_ENONFINITE, CRL_ESAMPLER, CRL_EUNSUPPORTED = range(8)
 STATUS_NAMES = ["CRL_OK", "CRL_EINVAL", "CRL_ESTATE", "CRL_ECUDA", "CRL_ENCCL", "CRL_ENONFINITE",
