@@ -240,7 +240,8 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
     c->pair_R = s.take<float>((size_t)Bl + kStatPad);
     c->pair_L = s.take<float>((size_t)Bl + kStatPad);
   }
-  c->loss_part = s.take<float>((size_t)4 * loss_partial_blocks(Bl));
+  // loss partials: the loss kernel's CTAs (16 rows each) or the merge's row-side CTAs (8 rows)
+  c->loss_part = s.take<float>((size_t)4 * std::max(loss_partial_blocks(Bl), (Bl + 7) / 8));
   c->loss_ticket = s.take<unsigned>(1);
   c->loss_dev = s.take<float>(4);
   c->status = s.take<int>(1);

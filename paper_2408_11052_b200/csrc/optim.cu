@@ -8,6 +8,7 @@
 // decoupled weight decay; step counter t lives in device memory so the step can be replayed
 // from a CUDA graph.
 #include "common.cuh"
+#include "loss_common.cuh"
 #include <math_constants.h>
 
 namespace crl {
@@ -18,27 +19,6 @@ namespace crl {
 // loss_out[0..3], sets *skip when the loss is non-finite and advances the Adam step counter.
 constexpr int kLossRowsPerCta = 16;    // 2 rows per warp: one DRAM round trip per CTA
 
-__device__ __forceinline__ void loss_finalize_dev(const float* acc, float invN, float c_f,
-                                                  float c_b, float beta, float* loss_out,
-                                                  int* skip, int* adam_t, int* status) {
-  // negative coefficients mark the FlatNCE losses (F3, reading A-24): same InfoNCE sums and
-  // gradient, but the reported value of log(S / sg[S]) is 0 (the finiteness test keeps the sums)
-  const bool flat = c_f < 0.f || c_b < 0.f;
-  c_f = fabsf(c_f); c_b = fabsf(c_b);
-  const float Lf = acc[0] * invN, Lb = acc[1] * invN, P = beta * acc[2] * invN;
-  const float tot = c_f * Lf + c_b * Lb + P;
-  if (loss_out) {
-    loss_out[0] = flat ? 0.f : Lf; loss_out[1] = flat ? 0.f : Lb; loss_out[2] = P;
-    loss_out[3] = flat ? P : tot;
-  }
-  const bool bad = !isfinite(tot);
-  *skip = bad ? 1 : 0;
-  if (bad) {
-    set_status(status, CRL_ENONFINITE);
-  } else {
-    *adam_t += 1;
-  }
-}
 
 __global__ void __launch_bounds__(256) loss_partial_kernel(
     const float* __restrict__ phi, const float* __restrict__ psi, int Bl, int D, int energy,

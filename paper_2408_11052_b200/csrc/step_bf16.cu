@@ -56,6 +56,8 @@ cudaError_t tc_logits_grad(int, int, const CUtensorMap&, const CUtensorMap&, int
                            __nv_bfloat16*, const int*, cudaStream_t);
 cudaError_t launch_rowstat_bf16(const __nv_bfloat16*, int, int, int, float*, int*, int, cudaStream_t);
 cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st);
+cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st,
+                               const MergeLoss* loss);
 }  // namespace tc
 }  // namespace crl
 
@@ -717,12 +719,13 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     gl.phi32 = ctx->phi_out; gl.psi32 = ctx->psi_out; gl.part = ctx->loss_part; gl.ticket = ctx->loss_ticket;
     gl.acc = ctx->loss_acc; gl.out = loss_out; gl.skip = ctx->skip; gl.adam_t = ctx->adam_t; gl.status = ctx->status;
     gl.c_f = lsgn * c_f; gl.c_b = lsgn * c_b; gl.beta = k.beta_lse;
-  } else { Stage sg(ctx, st, "loss");
+  } else if (!ctx->use_grad2) { Stage sg(ctx, st, "loss");
     CU(launch_loss_partial(ctx->phi_out, ctx->psi_out, Bl, D, k.energy, ctx->lse_row, ctx->lse_col,
                            ctx->loss_acc, ctx->loss_part, ctx->loss_ticket, !ctx->dist, invN, lsgn * c_f, lsgn * c_b,
                            k.beta_lse, loss_out, ctx->skip, ctx->adam_t, ctx->status, st));
     ++nl; }
-  if (ctx->dist) {
+  // (the D = 256 pair gradient path reduces the loss in its merge launch, below)
+  if (ctx->dist && !ctx->use_grad2) {
     NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
     CU(launch_loss_finalize(ctx->loss_acc, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip, ctx->adam_t,
                             ctx->status, st));
@@ -766,8 +769,19 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     m0.valid1 = ctx->g2_flags;
     m1.valid1 = ctx->g2_flags + (Bl + 127) / 128;
     m0.prs_sub = m1.prs_sub = prs_sub;
-    CU(tc::launch_grad_merge2(k.energy, m0, m1, st));
+    // the loss rides on the row-side merge: l_ii from the bf16 rows the logits used
+    tc::MergeLoss ml;
+    ml.lr = ctx->lse_row; ml.lc = ctx->lse_col; ml.part = ctx->loss_part; ml.ticket = ctx->loss_ticket;
+    ml.acc = ctx->loss_acc; ml.out = loss_out; ml.skip = ctx->skip; ml.adam_t = ctx->adam_t; ml.status = ctx->status;
+    ml.invN = invN; ml.c_f = lsgn * c_f; ml.c_b = lsgn * c_b; ml.beta = k.beta_lse; ml.finalize = !ctx->dist;
+    CU(tc::launch_grad_merge2(k.energy, m0, m1, st, &ml));
     nl += 2;
+    if (ctx->dist) {
+      NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
+      CU(launch_loss_finalize(ctx->loss_acc, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip,
+                              ctx->adam_t, ctx->status, st));
+      ++nl;
+    }
   }
   fork2(ctx, st, st2);
   if (!ctx->use_gradf && !ctx->use_grad2) { Stage sg(ctx, st2, "grad_psi");

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tc_merge.cuh"
+#include "loss_common.cuh"
 #include "tc_gradf.h"
 
 namespace crl {
@@ -480,12 +481,57 @@ __global__ void grad_merge_kernel(const GradMergeArgs g) {
   pdl_launch();
   grad_merge_row<ENERGY>(g, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31);
 }
-// both sides of the fused gradient pass in one launch: blockIdx.y picks the row / column side
+// both sides of the fused gradient pass in one launch: blockIdx.y picks the row / column side;
+// the row side's CTAs also reduce the loss when L.part is set (MergeLoss)
 template <int ENERGY>
-__global__ void grad_merge2_kernel(const GradMergeArgs g0, const GradMergeArgs g1) {
+__global__ void grad_merge2_kernel(const GradMergeArgs g0, const GradMergeArgs g1, const MergeLoss L) {
   pdl_wait();
   pdl_launch();
-  grad_merge_row<ENERGY>(blockIdx.y ? g1 : g0, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31);
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  grad_merge_row<ENERGY>(blockIdx.y ? g1 : g0, w, lane);
+  if (blockIdx.y != 0 || L.part == nullptr) return;
+  __shared__ float red[3][8];
+  __shared__ bool last;
+  float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (w < g0.Na) {
+    float l;
+    if (g0.D == 256) l = merge_diag_logit<ENERGY, 8>(g0, w, lane);
+    else if (g0.D == 128) l = merge_diag_logit<ENERGY, 4>(g0, w, lane);
+    else l = merge_diag_logit<ENERGY, 2>(g0, w, lane);
+    const float lr = L.lr[w], lc = L.lc[w];
+    s1 = lr - l; s2 = lc - l; s3 = lr * lr;
+  }
+  const int wi = threadIdx.x >> 5;
+  if (lane == 0) { red[0][wi] = s1; red[1][wi] = s2; red[2][wi] = s3; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) { t1 += red[0][j]; t2 += red[1][j]; t3 += red[2][j]; }
+    L.part[blockIdx.x * 4 + 0] = t1; L.part[blockIdx.x * 4 + 1] = t2; L.part[blockIdx.x * 4 + 2] = t3;
+    __threadfence();
+    last = atomicAdd(L.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  // last row-side CTA: the CTA partials in a fixed order (strided, then a tree): deterministic
+  __threadfence();
+  __shared__ float tr[3][256];
+  float t1 = 0.f, t2 = 0.f, t3 = 0.f;
+  for (unsigned j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
+    t1 += __ldcg(L.part + j * 4 + 0); t2 += __ldcg(L.part + j * 4 + 1); t3 += __ldcg(L.part + j * 4 + 2);
+  }
+  tr[0][threadIdx.x] = t1; tr[1][threadIdx.x] = t2; tr[2][threadIdx.x] = t3;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h)
+      for (int c = 0; c < 3; ++c) tr[c][threadIdx.x] += tr[c][threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    L.acc[0] = tr[0][0]; L.acc[1] = tr[1][0]; L.acc[2] = tr[2][0];
+    *L.ticket = 0u;                               // re-armed for the next (graph) replay
+    if (L.finalize) loss_finalize_dev(L.acc, L.invN, L.c_f, L.c_b, L.beta, L.out, L.skip, L.adam_t, L.status);
+  }
 }
 
 // ------------------------------------------------------------------------------- host side
@@ -634,13 +680,20 @@ cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, c
   if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g);
   return launch_pdl(grad_merge_kernel<CRL_ENERGY_DOT>, grid, dim3(256), 0, st, g);
 }
-// row side (g0) and column side (g1) of the fused gradient pass, one launch
-cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st) {
+// row side (g0) and column side (g1) of the fused gradient pass, one launch (+ the loss when
+// loss != nullptr: grad2 path)
+cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st,
+                               const MergeLoss* loss) {
   const dim3 grid((max(g0.Na, g1.Na) * 32 + 255) / 256, 2);
-  if (energy == CRL_ENERGY_L2) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_L2>, grid, dim3(256), 0, st, g0, g1);
-  if (energy == CRL_ENERGY_L2SQ) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_L2SQ>, grid, dim3(256), 0, st, g0, g1);
-  if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g0, g1);
-  return launch_pdl(grad_merge2_kernel<CRL_ENERGY_DOT>, grid, dim3(256), 0, st, g0, g1);
+  const MergeLoss L = loss ? *loss : MergeLoss{};
+  if (energy == CRL_ENERGY_L2) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_L2>, grid, dim3(256), 0, st, g0, g1, L);
+  if (energy == CRL_ENERGY_L2SQ)
+    return launch_pdl(grad_merge2_kernel<CRL_ENERGY_L2SQ>, grid, dim3(256), 0, st, g0, g1, L);
+  if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g0, g1, L);
+  return launch_pdl(grad_merge2_kernel<CRL_ENERGY_DOT>, grid, dim3(256), 0, st, g0, g1, L);
+}
+cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st) {
+  return launch_grad_merge2(energy, g0, g1, st, nullptr);
 }
 
 cudaError_t launch_rowstat_bf16(const __nv_bfloat16* x, int N, int D, int energy, float* out, int* fac_ok,

@@ -23,6 +23,24 @@ struct GradMergeArgs {
   int prs_sub = 1;                         // row-sum sub-partials per slot (tc_grad2: 2 warpgroups)
 };
 
+// The loss reduced by the row-side merge (the D = 256 pair gradient path: one launch less):
+// per row i the positive-pair logit l_ii from the same bf16 rows the logits used, and
+// (LSE_i - l_ii, LSE'_i - l_ii, LSE_i^2); per-CTA partials, the last CTA (ticket) adds them in
+// CTA order and finalises as the loss kernel does.  part == nullptr: off.
+struct MergeLoss {
+  const float* lr = nullptr;               // [Na] LSE_i of this rank's rows
+  const float* lc = nullptr;               // [Na] LSE'_i of this rank's columns
+  float* part = nullptr;                   // [CTAs][4]
+  unsigned* ticket = nullptr;              // zero on entry, re-armed by the last CTA
+  float* acc = nullptr;                    // [3] the sums (all-reduced by the caller at W > 1)
+  float* out = nullptr;                    // [4] L_fwd, L_bwd, penalty, total (or null)
+  int* skip = nullptr; int* adam_t = nullptr; int* status = nullptr;
+  float invN = 0.f, c_f = 1.f, c_b = 1.f, beta = 0.f;
+  int finalize = 1;                        // W = 1: finalise here; W > 1: the caller does
+};
+
+
+
 // V consecutive floats / bf16 of a row from lane-contiguous addresses (16 B vector accesses)
 template <int V>
 __device__ __forceinline__ void ld_f32v(const float* __restrict__ p, float (&v)[V]) {
@@ -140,6 +158,26 @@ __device__ __forceinline__ void grad_merge_row(const GradMergeArgs& g, int w, in
   if (g.D == 256) grad_merge_row_v<ENERGY, 8>(g, w, lane);
   else if (g.D == 128) grad_merge_row_v<ENERGY, 4>(g, w, lane);
   else grad_merge_row_v<ENERGY, 2>(g, w, lane);
+}
+
+// l_ii of row w (warp-uniform): the energy of (A_w, B_{row_offset + w}) on the bf16 rows
+template <int ENERGY, int V>
+__device__ __forceinline__ float merge_diag_logit(const GradMergeArgs& g, int w, int lane) {
+  constexpr int D = 32 * V;
+  float av[V], bv[V];
+  ld_bf16v<V>(g.A + (size_t)w * D + V * lane, av);
+  ld_bf16v<V>(g.Bg + (size_t)(g.row_offset + w) * D + V * lane, bv);
+  float x = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    if (ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) { const float d = av[i] - bv[i]; x = fmaf(d, d, x); }
+    else x = fmaf(av[i], bv[i], x);
+  }
+  x = warp_sum(x);
+  if (ENERGY == CRL_ENERGY_L2) return -sqrtf(x + kEpsL2);
+  if (ENERGY == CRL_ENERGY_L2SQ) return -x;
+  if (ENERGY == CRL_ENERGY_COS) return x * g.a_stat[w] * g.b_stat[g.row_offset + w];   // 1/|A_i|, 1/|B_i|
+  return x;
 }
 
 }  // namespace tc
