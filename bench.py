@@ -552,7 +552,9 @@ def run_ours(args):
                "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in hb[0])),
                "d2h_bytes_per_step": 16, "steps": K,
                "note": "host wall clock over K back-to-back crl_critic_step calls with page-locked host "
-                       "s/a/g (H2D inside each call) and a page-locked host loss written every step; "
+                       "s/a/g (H2D inside each call: one DMA copy on the copy engine into the staging "
+                       "set the previous call does not read, so it overlaps that call's kernels) and "
+                       "a page-locked host loss written every step; no L2 flush between calls; "
                        "max over ranks"}
 
     # ---- per-stage profile (eager, event-bracketed) for the roofline

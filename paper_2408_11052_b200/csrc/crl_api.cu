@@ -250,6 +250,11 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
   c->stage_s = s.take<float>((size_t)Bl * k.obs_dim);
   c->stage_a = s.take<float>((size_t)Bl * k.act_dim);
   c->stage_g = s.take<float>((size_t)Bl * k.goal_dim + 64);   // + 256 B: the host ring's slot pitch
+  // the second staging set: the same three takes, so the same layout (offsets of a and g from s;
+  // pointer differences would be 0 in the sizing pass, where the carver has no base)
+  c->stage2 = s.take<float>((size_t)Bl * k.obs_dim);
+  s.take<float>((size_t)Bl * k.act_dim);
+  s.take<float>((size_t)Bl * k.goal_dim + 64);
   // actor objective (fp32): actor activations, the frozen critic's activations on [s||a'],
   // head buffers, gradient partials
   c->has_actor = k.actor_depth > 0 && k.actor_width > 0;
@@ -497,6 +502,11 @@ crl_status crl_destroy(crl_ctx* ctx) {
   for (int i = 0; i < crl_ctx::kHostSlots; ++i)
     if (ctx->h_ev[i]) cudaEventDestroy(ctx->h_ev[i]);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (int d = 0; d < 2; ++d) {
+    if (ctx->ev_dcopied[d]) cudaEventDestroy(ctx->ev_dcopied[d]);
+    if (ctx->ev_dfree[d]) cudaEventDestroy(ctx->ev_dfree[d]);
+  }
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
   return CRL_OK;
@@ -845,6 +855,11 @@ static bool make_host_ring(crl_ctx* ctx) {
     return false;
   for (int i = 0; i < crl_ctx::kHostSlots; ++i)
     if (cudaEventCreateWithFlags(&ctx->h_ev[i], cudaEventDisableTiming) != cudaSuccess) return false;
+  if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return false;
+  for (int d = 0; d < 2; ++d)
+    if (cudaEventCreateWithFlags(&ctx->ev_dcopied[d], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_dfree[d], cudaEventDisableTiming) != cudaSuccess)
+      return false;
   return true;
 }
 
@@ -881,6 +896,7 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
   // steps/s, the per-element host-link latency); a page-locked host loss is written in place
   // by the loss kernel (CRL_NO_ZERO_COPY: a device-to-host copy instead)
   const bool zc = !std::getenv("CRL_NO_ZERO_COPY");
+  int dset = -1;                                          // device staging set of a host batch
   if (ctx->h_stage && !is_device_ptr(s) && !is_device_ptr(a) && !is_device_ptr(g)) {
     // host batch: gathered into a page-locked ring slot laid out like the device staging, then
     // ONE host-to-device copy (three small copies cost three DMA latencies on the timeline)
@@ -889,22 +905,41 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
     CU(cudaEventSynchronize(ctx->h_ev[slot]));            // the slot's previous copy is done
     char* hb = ctx->h_stage + (size_t)slot * ctx->h_stage_bytes;
     char* d0 = reinterpret_cast<char*>(ctx->stage_s);
+    const size_t off_a = reinterpret_cast<char*>(ctx->stage_a) - d0, off_g = reinterpret_cast<char*>(ctx->stage_g) - d0;
     std::memcpy(hb, s, Bl * k.obs_dim * 4);
-    std::memcpy(hb + (reinterpret_cast<char*>(ctx->stage_a) - d0), a, Bl * k.act_dim * 4);
-    std::memcpy(hb + (reinterpret_cast<char*>(ctx->stage_g) - d0), g, Bl * k.goal_dim * 4);
-    // the device pulls the slot over the host link with 16 B loads (one small kernel: measured
-    // ahead of a DMA copy for this size, Ant e2e 11.25k -> 11.7k steps/s; CRL_DMA_COPY = copy)
-    if (!std::getenv("CRL_DMA_COPY")) {
+    std::memcpy(hb + off_a, a, Bl * k.act_dim * 4);
+    std::memcpy(hb + off_g, g, Bl * k.goal_dim * 4);
+    if (std::getenv("CRL_E2E_PULL")) {
+      // the device pulls the slot over the host link with 16 B loads (one small kernel on st,
+      // in line with the step; the round-1 design)
       const size_t n16 = (ctx->h_stage_bytes + 15) / 16;
       pull_host_kernel<<<(unsigned)std::min<size_t>((n16 + 255) / 256, (size_t)ctx->num_sms), 256, 0, st>>>(
           reinterpret_cast<uint4*>(ctx->stage_s), reinterpret_cast<const uint4*>(hb), n16);
       CU(cudaGetLastError());
+      CU(cudaEventRecord(ctx->h_ev[slot], st));
+      s = ctx->stage_s; a = ctx->stage_a; g = ctx->stage_g;
     } else {
-      CU(cudaMemcpyAsync(ctx->stage_s, hb, ctx->h_stage_bytes, cudaMemcpyHostToDevice, st));
+      // one DMA copy on the copy engine into the staging set the previous step does NOT read:
+      // it overlaps that step's kernels (it waits only for the step two calls back, the last
+      // reader of this set); the step waits for its copy
+      dset = ctx->d_slot;
+      ctx->d_slot ^= 1;
+      char* db = dset ? reinterpret_cast<char*>(ctx->stage2) : d0;
+      CU(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_dfree[dset], 0));
+      CU(cudaMemcpyAsync(db, hb, ctx->h_stage_bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+      CU(cudaEventRecord(ctx->h_ev[slot], ctx->copy_stream));
+      CU(cudaEventRecord(ctx->ev_dcopied[dset], ctx->copy_stream));
+      CU(cudaStreamWaitEvent(st, ctx->ev_dcopied[dset], 0));
+      s = reinterpret_cast<const float*>(db);
+      a = reinterpret_cast<const float*>(db + off_a);
+      g = reinterpret_cast<const float*>(db + off_g);
     }
-    CU(cudaEventRecord(ctx->h_ev[slot], st));
-    s = ctx->stage_s; a = ctx->stage_a; g = ctx->stage_g;
   }
+  // the staging set d is free again once this step (its only reader) has run
+  auto release_set = [&]() -> crl_status {
+    if (dset >= 0) CU(cudaEventRecord(ctx->ev_dfree[dset], st));
+    return CRL_OK;
+  };
   auto stage_in = [&](const float*& p, float* stage, size_t n) -> crl_status {
     if (is_device_ptr(p)) return CRL_OK;
     CU(cudaMemcpyAsync(stage, p, n * 4, cudaMemcpyHostToDevice, st));
@@ -930,7 +965,7 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
                               : enqueue_critic(ctx, s, a, g, loss_dev, grads_out, st, st);
     if (rs != CRL_OK) return rs;
     if (loss_host) CU(cudaMemcpyAsync(loss_out, loss_dev, 16, cudaMemcpyDeviceToHost, st));
-    return CRL_OK;
+    return release_set();
   }
   GraphKey key{s, a, g, loss_dev, grads_out};
   auto it = ctx->graphs.find(key);
@@ -968,7 +1003,7 @@ extern "C" crl_status crl_critic_step(crl_ctx* ctx, const float* s, const float*
   ctx->graph_use[key] = ++ctx->use_clock;
   ctx->launches = ctx->graph_launches[key];
   if (loss_host) CU(cudaMemcpyAsync(loss_out, loss_dev, 16, cudaMemcpyDeviceToHost, st));
-  return CRL_OK;
+  return release_set();
 }
 
 extern "C" crl_status crl_profile_enable(crl_ctx* ctx, int on) {

@@ -157,6 +157,13 @@ struct crl_ctx {
   size_t h_stage_bytes = 0;
   int h_slot = 0;
   cudaEvent_t h_ev[kHostSlots] = {};
+  // two device staging sets (stage_s.. and stage2 with the same layout) alternate between host
+  // batches: step i + 1's host-to-device copy runs on the copy engine (copy_stream) while step i
+  // computes; ev_dcopied[d]: set d landed, ev_dfree[d]: the step that read set d finished
+  float* stage2 = nullptr;
+  int d_slot = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_dcopied[2] = {}, ev_dfree[2] = {};
   // runtime
   cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr, cap_stream3 = nullptr, cap_stream4 = nullptr;
   cudaStream_t cap_body = nullptr;        // captures the bodies of conditional graph nodes
