@@ -200,9 +200,18 @@ static void carve(crl_ctx* c, char* buf_base, char* scr_base, size_t* buf_bytes,
         // CTA pairs (tc_grad2p) once a pair has two full row blocks to share the B tile over
         c->g2_pair = Bl >= 256 && !std::getenv("CRL_NO_GRAD2P");
         c->g2_grid = c->g2_pair ? tc::tc_grad2p_grid(Bl, device_sms()) : tc::tc_grad2_grid(Bl, device_sms());
-        c->g2_part_da = s.take<float>((size_t)4 * Bl * D);
-        c->g2_part_rs = s.take<float>((size_t)16 * Bl);   // 2 sides x 2 slots x <= 4 warpgroup sub-slots
+        // W = 1 and a symmetric energy: side 1 as W^T Phi from the stored W (CRL_NO_G2_WSYM: off)
+        c->g2_wsym = c->g2_pair && !dist && N == Bl && k.energy != CRL_ENERGY_COS && tc::pdw_supported(Bl, 2) &&
+                     !std::getenv("CRL_NO_G2_WSYM");
+        // partial slots: both sides x 2, or (stored W) side 0 x 3 (a pair covers >= half a row-block
+        // pair, so a row block is cut into at most 3 pieces) + the 2 K slices of W^T Phi
+        c->g2_part_da = s.take<float>((size_t)(c->g2_wsym ? 5 : 4) * Bl * D);
+        c->g2_part_rs = s.take<float>((size_t)16 * Bl);   // 2 sides x 2 slots (or 3 slots) x <= 4 sub-slots
         c->g2_flags = s.take<unsigned char>((size_t)2 * ((Bl + 127) / 128));
+        if (c->g2_wsym) {
+          c->g2_W = s.take<__nv_bfloat16>((size_t)Bl * ((N + 63) / 64 * 64));   // rows padded to 128 B
+          c->g2_cs = s.take<float>((size_t)2 * N);
+        }
       }
     }
   }

@@ -259,6 +259,13 @@ struct crl_ctx {
   bool g2_pair = false;                                 // CTA-pair variant (tc_grad2p)
   CUtensorMap g2_S0, g2_S1;                             // pair: S parts (box {64, 64}): Psi_g, Phi_g
   CUtensorMap g2_A0, g2_A1;        // CTA-pair gradient pass: local Phi / Psi rows, box {64, 128}
+  // W = 1, symmetric energies (L2, L2^2, dot): the pair pass does side 0 only and stores W;
+  // dPsi = W^T Phi and the column sums of W come from one pair GEMM (tc_pdw.cu pdw_add_gemm)
+  bool g2_wsym = false;
+  __nv_bfloat16* g2_W = nullptr;   // [B_l][N] bf16
+  float* g2_cs = nullptr;          // [2 slices][N] column sums of W
+  CUtensorMap g2_Wmap;             // W, box {64, 128} (the pass's TMA stores)
+  tc::PdwParams pdw_g;             // the W^T Phi GEMM
   // all weight / bias gradients of both encoders in one grouped launch (tc_dwg.cu)
   bool use_dwg = false;
   tc::DwgParams dwg;

@@ -189,7 +189,20 @@ crl_status bf16_prepare(crl_ctx* ctx) {
             !tc::make_map_bf16(&ctx->g2_A0, ctx->phi_outb, k.repr_dim, k.batch_local, k.repr_dim, 64, 128) ||
             !tc::make_map_bf16(&ctx->g2_A1, ctx->psi_outb, k.repr_dim, k.batch_local, k.repr_dim, 64, 128))
           return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the gradient operands");
-        tc::tc_grad2p_split_flags(k.batch_local, ctx->N, ctx->g2_grid, fl.data());
+        const int pieces = tc::tc_grad2p_split_flags(k.batch_local, ctx->N, ctx->g2_grid, fl.data(),
+                                                     ctx->g2_wsym ? 1 : 2);
+        if (pieces > (ctx->g2_wsym ? 3 : 2))
+          return fail(ctx, CRL_EUNSUPPORTED, "gradient pass: a row block cut into more pieces than partial slots");
+        if (ctx->g2_wsym) {
+          // W (bf16 [B_l][N]) and dPsi slots 0 / 1 = the two K halves of W^T Phi, column sums beside
+          const int Bl = k.batch_local, D = k.repr_dim, ldw = (ctx->N + 63) / 64 * 64;
+          tc::pdw_init(ctx->pdw_g, Bl, 2, 0);
+          tc::pdw_set_nh(ctx->pdw_g, 1);
+          if (!tc::make_map_bf16(&ctx->g2_Wmap, ctx->g2_W, ctx->N, Bl, ldw, 64, 128) ||
+              !tc::pdw_add_gemm(ctx->pdw_g, ctx->g2_W, ldw, ctx->phi_outb, ctx->N, D,
+                                ctx->g2_part_da + (size_t)3 * Bl * D, (long long)Bl * D, ctx->g2_cs, ctx->N))
+            return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the stored gradient weights");
+        }
       } else {
         tc::tc_grad2_split_flags(k.batch_local, ctx->N, ctx->g2_grid, fl.data());
       }
@@ -756,11 +769,14 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     s1.lcf = ctx->fac_row_g; s1.c_r = c_b; s1.c_c = c_f; s1.beta_r = 0.f; s1.beta_c = k.beta_lse;
     // row-sum sub-slots per partial slot: one per epilogue warpgroup of the launched variant
     const int prs_sub = ctx->g2_pair ? tc::tc_grad2p_warpgroups() : 2;
-    s1.part_da = ctx->g2_part_da + (size_t)2 * Bl * D; s1.part_rs = ctx->g2_part_rs + (size_t)2 * prs_sub * Bl;
+    s1.part_da = ctx->g2_part_da + (size_t)(ctx->g2_wsym ? 3 : 2) * Bl * D; s1.part_rs = ctx->g2_part_rs + (size_t)2 * prs_sub * Bl;
     s1.A = ctx->psi_outb;
+    if (ctx->g2_wsym) { ga.nsides = 1; ga.w_store = 1; }
     if (ctx->g2_pair) CU(tc::tc_grad2p(k.energy, ctx->g2_B0, ctx->g2_B1, ctx->g2_S0, ctx->g2_S1, ctx->g2_A0,
-                                           ctx->g2_A1, ga, ctx->g2_grid, st));
+                                           ctx->g2_A1, ga, ctx->g2_grid, st, ctx->g2_wsym ? &ctx->g2_Wmap : nullptr));
     else CU(tc::tc_grad2(k.energy, ctx->g2_B0, ctx->g2_B1, ga, ctx->g2_grid, st));
+    // symmetric energies at W = 1: side 1's weights are W^T -> dPsi = W^T Phi (+ column sums of W)
+    if (ctx->g2_wsym) { CU(tc::tc_pdw_launch(ctx->pdw_g, ctx->num_sms, st)); ++nl; }
     const float Cdiag = invN * (c_f + c_b);
     tc::GradMergeArgs m0{s0.part_da, s0.part_rs, ctx->phi_outb, s0.a_stat, ctx->psi_outb_g, ctx->stat_psi, row_off,
                          Cdiag, Bl, D, 2, ctx->dphi, ctx->dphib, 0};
@@ -769,6 +785,7 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     m0.valid1 = ctx->g2_flags;
     m1.valid1 = ctx->g2_flags + (Bl + 127) / 128;
     m0.prs_sub = m1.prs_sub = prs_sub;
+    if (ctx->g2_wsym) { m0.S = 3; m1.valid1 = nullptr; m1.prs = ctx->g2_cs; m1.prs_sub = 1; }
     // the loss rides on the row-side merge: l_ii from the bf16 rows the logits used
     tc::MergeLoss ml;
     ml.lr = ctx->lse_row; ml.lc = ctx->lse_col; ml.part = ctx->loss_part; ml.ticket = ctx->loss_ticket;

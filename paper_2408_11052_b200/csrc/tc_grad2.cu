@@ -93,6 +93,15 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 __device__ __forceinline__ uint32_t sw128_off(int r, int k) {
   return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2);
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
@@ -613,11 +622,11 @@ constexpr size_t SMEM = A_BYTES + NS * SP_BYTES + ND * DP_BYTES + W_BYTES + 2 * 
 }  // namespace g2p
 
 template <int ENERGY, int RQ>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 128 * g2p::kNWG, 1)
     tc_grad2p_kernel(const __grid_constant__ CUtensorMap tmD0, const __grid_constant__ CUtensorMap tmD1,
                      const __grid_constant__ CUtensorMap tmS0, const __grid_constant__ CUtensorMap tmS1,
                      const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
-                     const Grad2Args p) {
+                     const __grid_constant__ CUtensorMap tmW, const Grad2Args p) {
   using namespace g2p;
   using namespace pair;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -641,12 +650,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
   uint64_t* a_empty = a_full + 1;          // both: the unit's last S MMA completed
   uint64_t* da_full = a_empty + 1;         // both: the unit's dA complete
   uint64_t* da_empty = da_full + 1;        // leader: dA read out
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(da_empty + 1);
+  uint64_t* w_loc = da_empty + 1;          // local: every epilogue warp of this CTA wrote W (w_store)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_loc + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-  const long X = 2L * p.RB * p.TPB;                                       // p.RB: row-block PAIRS
+  const long X = (long)(p.nsides == 1 ? 1 : 2) * p.RB * p.TPB;           // p.RB: row-block PAIRS
+  const bool wst = p.w_store != 0;                                        // (host: only with nsides = 1)
   const long x0 = g2::range_start(cid, X, ncl), x1 = g2::range_start(cid + 1, X, ncl);
   auto unit_at = [&](long x, int& side, int& rb, int& tb, int& nt) {
     const long r = x / p.TPB;
@@ -661,13 +672,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
     tma_prefetch_desc(&tmD0); tma_prefetch_desc(&tmD1);
     tma_prefetch_desc(&tmS0); tma_prefetch_desc(&tmS1);
     tma_prefetch_desc(&tmA0); tma_prefetch_desc(&tmA1);
+    if (wst) tma_prefetch_desc(&tmW);
     for (int i = 0; i < NS; ++i) { mbar_init(&sp_full[i], 1); mbar_init(&sp_free[i], 1); }
     for (int i = 0; i < ND; ++i) { mbar_init(&dp_full[i], 1); mbar_init(&dp_free[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&st_full[i], 1); mbar_init(&st_empty[i], 4 * kNWG); }
     for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8 * kNWG); }
-    mbar_init(w_full, 8 * kNWG); mbar_init(w_empty, 1);
+    mbar_init(w_full, 8 * kNWG); mbar_init(w_empty, wst ? 2 : 1);   // dA MMA (+ the W store) read W
     mbar_init(a_full, 1); mbar_init(a_empty, 1);
     mbar_init(da_full, 1); mbar_init(da_empty, 8 * kNWG);
+    mbar_init(w_loc, 4 * kNWG);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
@@ -738,6 +751,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
         }
         x += nt;
       }
+    }
+  } else if (warp == 3 + 4 * kNWG) {
+    if (lane == 0 && wst) {
+      // ------------------------------------------ W store (local): the tile's bf16 W -> global
+      // (side 0 only; rows past Na / columns past Nb are clipped by the map or skipped whole)
+      const int row0 = 128 * (int)rank;
+      int g = 0;
+      for (long x = x0; x < x1;) {
+        int side, rb, tb, nt;
+        unit_at(x, side, rb, tb, nt);
+        const int r0 = rb * 256 + row0;
+        for (int t = 0; t < nt; ++t, ++g) {
+          const int j0 = (tb + t) * BNT;
+          mbar_wait(w_loc, g & 1);
+          if (r0 < p.Na) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              if (j0 + 64 * c < p.Nb) g2::tma_store_2d(&tmW, smem_u32(sW + c * W_CH), j0 + 64 * c, r0);
+            g2::bulk_commit();
+            g2::bulk_wait_read();
+          }
+          mbar_arrive(w_empty);                             // local: the tile may be overwritten
+        }
+        x += nt;
+      }
+      g2::bulk_wait_all();
     }
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
@@ -881,7 +920,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
           g2::w_tile<ENERGY, CW, RQ>(raw, bst, c0, nval, fac_fast && nval >= BNT, fac_fast, kc, sd.lc + j0, pk, wsum);
         }
         if (tl) g2::g2_trace(p.trace, g, 6);
-        if (g >= 1) mbar_wait(w_empty, (g - 1) & 1);        // dA(g - 1) has read W
+        if (g >= 1) mbar_wait(w_empty, (g - 1) & 1);        // dA(g - 1) (and its W store) read W
         const uint32_t wt = smem_u32(sW + (c0 >> 6) * W_CH);  // K-chunk of these columns
 #pragma unroll
         for (int u = 0; u < CW / 8; ++u)
@@ -889,10 +928,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(96 + 128 * g2p::kNWG
                      make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) { arrive_remote(w_full_l); mbar_arrive(&st_empty[sl]); }
+        if (lane == 0) {
+          arrive_remote(w_full_l);
+          mbar_arrive(&st_empty[sl]);
+          if (wst) mbar_arrive(w_loc);
+        }
         if (tl) g2::g2_trace(p.trace, g, 7);
       }
-      const int slot = tb == 0 ? 0 : 1;
+      // partial slot = the piece of the row block: 0 for the piece at its first tile, else the
+      // number of pair ranges that began inside the row block up to this one (<= 2: one side only
+      // gives a pair >= half a row-block pair of tiles)
+      int slot = 0;
+      if (tb != 0) {
+        const long first = x - (long)tb;
+        int pf = cid;
+        while (pf > 0 && g2::range_start(pf, X, ncl) > first) --pf;
+        slot = cid - pf;
+      }
       if ((ENERGY == CRL_ENERGY_L2 || ENERGY == CRL_ENERGY_L2SQ) && rv)
         sd.part_rs[((size_t)(kNWG * slot + wg)) * p.Na + row] = wsum;
       prev_side = side; prev_rb = rb; prev_slot = slot;
@@ -950,25 +1002,28 @@ int tc_grad2p_grid(int Na, int num_sms) {
   return 2 * std::max(1, std::min(num_sms / 2, 2 * RBP));
 }
 // slot-1 flags per 128-row block: a row-block pair cut by a pair boundary flags both its blocks
-void tc_grad2p_split_flags(int Na, int Nb, int grid, unsigned char* flags /*[2][RB]*/) {
+int tc_grad2p_split_flags(int Na, int Nb, int grid, unsigned char* flags /*[2][RB]*/, int nsides) {
   const long RB = (Na + 127) / 128, RBP = (Na + 255) / 256, TPB = (Nb + g2::BNT - 1) / g2::BNT;
-  const long X = 2 * RBP * TPB, P = grid / 2;
+  const long X = (nsides == 1 ? 1 : 2) * RBP * TPB, P = grid / 2;
+  int pieces = 1;
   for (long side = 0; side < 2; ++side)
     for (long rb = 0; rb < RB; ++rb) {
       const long rp = side * RBP + rb / 2, first = rp * TPB, last = first + TPB - 1;
-      bool cut = false;
+      int cuts = 0;                                       // pair ranges beginning inside the row block
       for (long c = 1; c < P; ++c) {
         const long st = g2::range_start(c, X, P);
-        if (st > first && st <= last) { cut = true; break; }
+        if (st > first && st <= last) ++cuts;
       }
-      flags[side * RB + rb] = cut ? 1 : 0;
+      flags[side * RB + rb] = (unsigned char)cuts;
+      if (first < X) pieces = std::max(pieces, 1 + cuts);
     }
+  return pieces;
 }
 
 template <int ENERGY, int RQ>
 static cudaError_t launch_g2p(const CUtensorMap& d0, const CUtensorMap& d1, const CUtensorMap& s0,
-                              const CUtensorMap& s1, const CUtensorMap& a0, const CUtensorMap& a1, const Grad2Args& p,
-                              int grid, cudaStream_t st) {
+                              const CUtensorMap& s1, const CUtensorMap& a0, const CUtensorMap& a1,
+                              const CUtensorMap& w, const Grad2Args& p, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_grad2p_kernel<ENERGY, RQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -976,30 +1031,33 @@ static cudaError_t launch_g2p(const CUtensorMap& d0, const CUtensorMap& d1, cons
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(tc_grad2p_kernel<ENERGY, RQ>, dim3(grid), dim3(96 + 128 * g2p::kNWG), g2p::SMEM, st, d0, d1, s0, s1,
-                    a0, a1, p);
+  return launch_pdl(tc_grad2p_kernel<ENERGY, RQ>, dim3(grid), dim3(128 + 128 * g2p::kNWG), g2p::SMEM, st, d0, d1, s0,
+                    s1, a0, a1, w, p);
 }
 
 cudaError_t tc_grad2p(int energy, const CUtensorMap& mD0, const CUtensorMap& mD1, const CUtensorMap& mS0,
                       const CUtensorMap& mS1, const CUtensorMap& mA0, const CUtensorMap& mA1, const Grad2Args& p0,
-                      int grid, cudaStream_t st) {
+                      int grid, cudaStream_t st, const CUtensorMap* mW) {
   Grad2Args p = p0;
+  static const CUtensorMap kNoMap{};
+  if (p.w_store && (mW == nullptr || p.nsides != 1)) return cudaErrorInvalidValue;
+  const CUtensorMap& w = mW != nullptr ? *mW : kNoMap;
   p.RB = (p.Na + 255) / 256;                              // row-block PAIRS
   p.TPB = (p.Nb + g2p::BNT - 1) / g2p::BNT;
   if (energy == CRL_ENERGY_L2) {
     // L2: of every 4 logit pairs, RQ take rsqrt on the FMA pipe instead of the MUFU
     const int rq = std::getenv("CRL_G2_RSQ") ? std::atoi(std::getenv("CRL_G2_RSQ")) : g2::kG2RsqPairs;
     switch (rq) {
-      case 1: return launch_g2p<CRL_ENERGY_L2, 1>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
-      case 2: return launch_g2p<CRL_ENERGY_L2, 2>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
-      case 3: return launch_g2p<CRL_ENERGY_L2, 3>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
-      case 4: return launch_g2p<CRL_ENERGY_L2, 4>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
-      default: return launch_g2p<CRL_ENERGY_L2, 0>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+      case 1: return launch_g2p<CRL_ENERGY_L2, 1>(mD0, mD1, mS0, mS1, mA0, mA1, w, p, grid, st);
+      case 2: return launch_g2p<CRL_ENERGY_L2, 2>(mD0, mD1, mS0, mS1, mA0, mA1, w, p, grid, st);
+      case 3: return launch_g2p<CRL_ENERGY_L2, 3>(mD0, mD1, mS0, mS1, mA0, mA1, w, p, grid, st);
+      case 4: return launch_g2p<CRL_ENERGY_L2, 4>(mD0, mD1, mS0, mS1, mA0, mA1, w, p, grid, st);
+      default: return launch_g2p<CRL_ENERGY_L2, 0>(mD0, mD1, mS0, mS1, mA0, mA1, w, p, grid, st);
     }
   }
-  if (energy == CRL_ENERGY_L2SQ) return launch_g2p<CRL_ENERGY_L2SQ, 0>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
-  if (energy == CRL_ENERGY_COS) return launch_g2p<CRL_ENERGY_COS, 0>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
-  return launch_g2p<CRL_ENERGY_DOT, 0>(mD0, mD1, mS0, mS1, mA0, mA1, p, grid, st);
+  if (energy == CRL_ENERGY_L2SQ) return launch_g2p<CRL_ENERGY_L2SQ, 0>(mD0, mD1, mS0, mS1, mA0, mA1, w, p, grid, st);
+  if (energy == CRL_ENERGY_COS) return launch_g2p<CRL_ENERGY_COS, 0>(mD0, mD1, mS0, mS1, mA0, mA1, w, p, grid, st);
+  return launch_g2p<CRL_ENERGY_DOT, 0>(mD0, mD1, mS0, mS1, mA0, mA1, w, p, grid, st);
 }
 
 cudaError_t tc_grad2(int energy, const CUtensorMap& mB0, const CUtensorMap& mB1, const Grad2Args& p0, int grid,

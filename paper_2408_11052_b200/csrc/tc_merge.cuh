@@ -19,7 +19,7 @@ struct GradMergeArgs {
   const __nv_bfloat16* Bg; const float* b_stat; int row_offset; float Cdiag; int Na, D, S;
   float* out; __nv_bfloat16* outb;
   int pre;   // cos: part already carries the row's own 1/|A_i| (fused pass, w' = g r_i s_j)
-  const unsigned char* valid1 = nullptr;   // tc_grad2: slot 1 holds data only for cut row blocks
+  const unsigned char* valid1 = nullptr;   // tc_grad2: per 128-row block, the extra slots holding data
   int prs_sub = 1;                         // row-sum sub-partials per slot (tc_grad2: 2 warpgroups)
 };
 
@@ -83,7 +83,7 @@ __device__ __forceinline__ void grad_merge_row_v(const GradMergeArgs& g, int w, 
   if (w >= Na) return;
   const size_t ib = (size_t)(row_offset + w) * D + V * lane;
   // slots that hold data for this row (tc_grad2: the second slot only for cut row blocks)
-  const int Sr = (g.valid1 != nullptr && S > 1 && !g.valid1[w >> 7]) ? 1 : S;
+  const int Sr = g.valid1 != nullptr ? min(S, 1 + (int)g.valid1[w >> 7]) : S;
   float av[V], bv[V], acc[V];
   ld_bf16v<V>(g.A + (size_t)w * D + V * lane, av);
   ld_bf16v<V>(g.Bg + ib, bv);

@@ -219,13 +219,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       const Item w = decode(P, it);
       int kb0, kb1;
       kb_range(w.slice, kb0, kb1);
-      const bool do_db = w.tm == 0 && !(P.dbg & 1);
+      const bool from_a = NH == 1 && P.prob[w.p].db_from_a;
+      const bool do_db = (from_a ? (w.tn == 0 && P.prob[w.p].db != nullptr) : w.tm == 0) && !(P.dbg & 1);
       f32x2 acc[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
       for (int kb = kb0; kb < kb1; ++kb, ++g) {
         const int s = g % kStages;
         mbar_wait(&used[s], (g / kStages) & 1);
         if (do_db) {
-          const uint32_t base = smem_u32(sStage + s * kStage) + kHalf + (uint32_t)box * (kBK * 128);
+          const uint32_t base = smem_u32(sStage + s * kStage) + (from_a ? 0u : kHalf) + (uint32_t)box * (kBK * 128);
 #pragma unroll
           for (int i = 0; i < RW / RPI; ++i) {
             const int r = RW * hw + RPI * i + rsub;
@@ -264,12 +265,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
               const float4 t = *reinterpret_cast<const float4*>(sDb + 128 * NH * x + cl);
               o.x += t.x; o.y += t.y; o.z += t.z; o.w += t.w;
             }
-            const int col = w.tn * kTN + 256 * h + 128 * (int)rank + 4 * lane;
-            float* dst = pr.db + (size_t)w.slice * (size_t)P.split_stride + col;
+            const int col = from_a ? w.tm * 256 + 128 * (int)rank + 4 * lane : w.tn * kTN + 256 * h + 128 * (int)rank + 4 * lane;
+            const int lim = from_a ? pr.M : pr.N;
+            float* dst = pr.db + (size_t)w.slice * (size_t)pr.db_stride + col;
             const float v[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              if (col + i < pr.N) dst[i] = v[i];
+              if (col + i < lim) dst[i] = v[i];
           }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kBiasW) : "memory");    // sDb reusable
@@ -376,6 +378,8 @@ bool pdw_add_problem(PdwParams& P, const __nv_bfloat16* X, int ldx, const __nv_b
     return false;
   }
   pr.db = db;
+  pr.db_stride = P.split_stride;
+  pr.db_from_a = 0;
   pr.M = M;
   pr.N = N;
   pr.tiles_n = (N + 256 * P.nh - 1) / (256 * P.nh);
@@ -384,6 +388,29 @@ bool pdw_add_problem(PdwParams& P, const __nv_bfloat16* X, int ldx, const __nv_b
   ++P.n;
   return true;
 }
+
+bool pdw_add_gemm(PdwParams& P, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, int M, int N, float* out,
+                  long long out_stride, float* colsum_a, long long colsum_stride) {
+  if (P.nh != 1 || P.n >= kPdwMaxProblems || (reinterpret_cast<uintptr_t>(out) % 16) != 0 || N % 4 != 0 ||
+      out_stride % 4 != 0)
+    return false;
+  PdwProblem& pr = P.prob[P.n];
+  if (!make_map_bf16(&pr.a, A, M, P.K, lda, 64, 64) || !make_map_bf16(&pr.b, B, N, P.K, N, 64, 64) ||
+      !make_map_f32_3d(&pr.out, out, N, M, P.splits, N, (uint64_t)out_stride, 32, 32))
+    return false;
+  pr.db = colsum_a;
+  pr.db_stride = colsum_stride;
+  pr.db_from_a = 1;
+  pr.M = M;
+  pr.N = N;
+  pr.tiles_n = (N + 255) / 256;
+  pr.tiles = ((M + 255) / 256) * pr.tiles_n * P.splits;
+  P.total += pr.tiles;
+  ++P.n;
+  return true;
+}
+
+void pdw_set_nh(PdwParams& P, int nh) { P.nh = nh == 1 ? 1 : 2; }
 
 template <int NH>
 static cudaError_t launch_pdw(const PdwParams& P, int num_sms, cudaStream_t st) {

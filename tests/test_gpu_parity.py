@@ -201,7 +201,8 @@ def test_relabel_bulk_65536_rows_bit_exact():
 
 # ------------------------------------------------------------------------- A2-A6
 
-def _critic_parity(cfg, batch_seed=11, check_adam=True, tol_loss=1e-5, tol_grad=1e-4, per_layer=True):
+def _critic_parity(cfg, batch_seed=11, check_adam=True, tol_loss=1e-5, tol_grad=1e-4, per_layer=True,
+                   encoder_grads=True):
     ctx, params = make_ctx(cfg)
     B = cfg["batch"]
     s, a, g = crl_synth.random_batch(cfg, B, seed=batch_seed)
@@ -224,6 +225,8 @@ def _critic_parity(cfg, batch_seed=11, check_adam=True, tol_loss=1e-5, tol_grad=
         got = ctx.debug_tensor(name).cpu().numpy()
         assert rel(got, ref[name]) < tol_grad, name
         assert relmax(got, ref[name]) < EMAX * tol_grad, (name, relmax(got, ref[name]))
+    if not encoder_grads:
+        return
     gr = grads.cpu().numpy()
     assert rel(gr, ref["grads"]) < tol_grad
     # per-tensor (every W, b and LayerNorm gamma / beta: a wrong small tensor can hide in the
@@ -894,6 +897,35 @@ def test_critic_step_bf16_wide_kernel_variants(knobs, monkeypatch):
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
     cfg = crl_synth.preset("ant", batch=1100, width=512, repr_dim=256, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
+
+
+@pytest.mark.parametrize("energy", ["l2", "l2sq", "dot"])
+@pytest.mark.parametrize("loss,beta", [("sym", 0.0), ("fwd", 0.3), ("bwd", 0.0)])
+@pytest.mark.parametrize("wsym", [True, False])
+def test_critic_step_bf16_d256_stored_w(energy, loss, beta, wsym, monkeypatch):
+    """D = 256 gradient at W = 1 for the symmetric energies: the pair pass computes side 0 only,
+    stores W = dL/dS (bf16) and dPsi = W^T Phi plus the column sums of W come from one pair GEMM
+    (tc_pdw.cu); CRL_NO_G2_WSYM keeps both sides in the pass.  Ragged batch (the last row-block
+    pair half empty; one side's 45 tiles over 10 pairs cut row blocks into 3 partial slots), every
+    loss kind, a logsumexp penalty.  Checked: the loss, both LSE vectors and the path's outputs
+    dPhi / dPsi (norm and element-wise).  The encoder gradients behind them are not: at this
+    random-init shape they are ill-conditioned in dPhi (the oracle alone, dPhi perturbed by 0.4 %
+    element-wise noise, moves them by 2-3 %: above the bf16 bar for BOTH paths); the stored-W
+    path's full gradient is checked at the 4 x 1024 shapes (test_critic_step_bf16_repr256_width1024)."""
+    if not wsym:
+        monkeypatch.setenv("CRL_NO_G2_WSYM", "1")
+    cfg = crl_synth.preset("ant", batch=1100, width=128, repr_dim=256, energy=energy, loss=loss,
+                           beta_lse=beta, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL, encoder_grads=False)
+
+
+@pytest.mark.parametrize("energy", ["l2sq", "dot"])
+def test_critic_step_bf16_width1024_stored_w_energies(energy):
+    """The stored-W gradient path's full pre-Adam gradient (every W, b of both encoders) for the
+    other symmetric energies at the configs[4] network shapes (well-conditioned: 0.4 % noise on
+    dPhi moves the encoder gradients by < 0.4 % here)."""
+    cfg = crl_synth.preset("netscale", batch=512, energy=energy)
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL)
 
 
