@@ -196,11 +196,12 @@ crl_status bf16_prepare(crl_ctx* ctx) {
         if (ctx->g2_wsym) {
           // W (bf16 [B_l][N]) and dPsi slots 0 / 1 = the two K halves of W^T Phi, column sums beside
           const int Bl = k.batch_local, D = k.repr_dim, ldw = (ctx->N + 63) / 64 * 64;
+          // (Phi^T W on 256 x 512 items: the Phi K block is shared by 512 columns of W; 2 K slices
+          // give 64 items, one wave of pairs; the result is stored transposed, i.e. [N][256])
           tc::pdw_init(ctx->pdw_g, Bl, 2, 0);
-          tc::pdw_set_nh(ctx->pdw_g, 1);
           if (!tc::make_map_bf16(&ctx->g2_Wmap, ctx->g2_W, ctx->N, Bl, ldw, 64, 128) ||
-              !tc::pdw_add_gemm(ctx->pdw_g, ctx->g2_W, ldw, ctx->phi_outb, ctx->N, D,
-                                ctx->g2_part_da + (size_t)3 * Bl * D, (long long)Bl * D, ctx->g2_cs, ctx->N))
+              !tc::pdw_add_gemm_t(ctx->pdw_g, ctx->phi_outb, D, ctx->g2_W, ldw, D, ctx->N,
+                                  ctx->g2_part_da + (size_t)3 * Bl * D, (long long)Bl * D, ctx->g2_cs, ctx->N))
             return fail(ctx, CRL_ECUDA, "cuTensorMapEncodeTiled failed for the stored gradient weights");
         }
       } else {

@@ -219,14 +219,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       const Item w = decode(P, it);
       int kb0, kb1;
       kb_range(w.slice, kb0, kb1);
-      const bool from_a = NH == 1 && P.prob[w.p].db_from_a;
-      const bool do_db = (from_a ? (w.tn == 0 && P.prob[w.p].db != nullptr) : w.tm == 0) && !(P.dbg & 1);
+      const bool do_db = w.tm == 0 && P.prob[w.p].db != nullptr && !(P.dbg & 1);
       f32x2 acc[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
       for (int kb = kb0; kb < kb1; ++kb, ++g) {
         const int s = g % kStages;
         mbar_wait(&used[s], (g / kStages) & 1);
         if (do_db) {
-          const uint32_t base = smem_u32(sStage + s * kStage) + (from_a ? 0u : kHalf) + (uint32_t)box * (kBK * 128);
+          const uint32_t base = smem_u32(sStage + s * kStage) + kHalf + (uint32_t)box * (kBK * 128);
 #pragma unroll
           for (int i = 0; i < RW / RPI; ++i) {
             const int r = RW * hw + RPI * i + rsub;
@@ -265,13 +264,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
               const float4 t = *reinterpret_cast<const float4*>(sDb + 128 * NH * x + cl);
               o.x += t.x; o.y += t.y; o.z += t.z; o.w += t.w;
             }
-            const int col = from_a ? w.tm * 256 + 128 * (int)rank + 4 * lane : w.tn * kTN + 256 * h + 128 * (int)rank + 4 * lane;
-            const int lim = from_a ? pr.M : pr.N;
+            const int col = w.tn * kTN + 256 * h + 128 * (int)rank + 4 * lane;
             float* dst = pr.db + (size_t)w.slice * (size_t)pr.db_stride + col;
             const float v[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              if (col + i < lim) dst[i] = v[i];
+              if (col + i < pr.N) dst[i] = v[i];
           }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kBiasW) : "memory");    // sDb reusable
@@ -318,16 +316,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         if (lane == 0 && c >= kNStg / 2) bulk_wait_read<kNStg / 2 - 1>();
         __syncwarp();
         const uint32_t b0 = stg0 + ((2 * c) % kNStg) * kStgBuf, b1 = stg0 + ((2 * c + 1) % kNStg) * kStgBuf;
+        if (pr.out_t) {
+          // transposed output out[n][m]: staging row = column n (32 m of this warp, 128 B), lane m
+          // writes element m of every row (a conflict-free 128 B row per store instruction)
+          const uint32_t moff = (uint32_t)((lane & 3) * 4), mch = (uint32_t)(lane >> 2);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t bb = (j < 8 ? b0 : b1) + row_sw + (uint32_t)((((j & 7) ^ (lane & 7))) << 4);
-          sts128(bb, make_uint4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]));
+          for (int i = 0; i < 64; ++i) {
+            const int n = i & 31;
+            const uint32_t a = (i < 32 ? b0 : b1) + (uint32_t)n * 128u + ((mch ^ (uint32_t)(n & 7)) << 4) + moff;
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(f[i]) : "memory");
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t bb = (j < 8 ? b0 : b1) + row_sw + (uint32_t)((((j & 7) ^ (lane & 7))) << 4);
+            sts128(bb, make_uint4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]));
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          tma_store_3d(&pr.out, b0, ncol0 + 64 * c, mrow0, w.slice);
-          tma_store_3d(&pr.out, b1, ncol0 + 64 * c + 32, mrow0, w.slice);
+          if (pr.out_t) {
+            tma_store_3d(&pr.out, b0, mrow0, ncol0 + 64 * c, w.slice);
+            tma_store_3d(&pr.out, b1, mrow0, ncol0 + 64 * c + 32, w.slice);
+          } else {
+            tma_store_3d(&pr.out, b0, ncol0 + 64 * c, mrow0, w.slice);
+            tma_store_3d(&pr.out, b1, ncol0 + 64 * c + 32, mrow0, w.slice);
+          }
           bulk_commit();
         }
       }
@@ -379,7 +394,7 @@ bool pdw_add_problem(PdwParams& P, const __nv_bfloat16* X, int ldx, const __nv_b
   }
   pr.db = db;
   pr.db_stride = P.split_stride;
-  pr.db_from_a = 0;
+  pr.out_t = 0;
   pr.M = M;
   pr.N = N;
   pr.tiles_n = (N + 256 * P.nh - 1) / (256 * P.nh);
@@ -389,21 +404,21 @@ bool pdw_add_problem(PdwParams& P, const __nv_bfloat16* X, int ldx, const __nv_b
   return true;
 }
 
-bool pdw_add_gemm(PdwParams& P, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, int M, int N, float* out,
-                  long long out_stride, float* colsum_a, long long colsum_stride) {
-  if (P.nh != 1 || P.n >= kPdwMaxProblems || (reinterpret_cast<uintptr_t>(out) % 16) != 0 || N % 4 != 0 ||
-      out_stride % 4 != 0)
+bool pdw_add_gemm_t(PdwParams& P, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, int ldb, int M, int N,
+                    float* out_t, long long out_stride, float* colsum_b, long long colsum_stride) {
+  if (P.n >= kPdwMaxProblems || (reinterpret_cast<uintptr_t>(out_t) % 16) != 0 || M % 4 != 0 || out_stride % 4 != 0 ||
+      (colsum_b != nullptr && (reinterpret_cast<uintptr_t>(colsum_b) % 16) != 0))
     return false;
   PdwProblem& pr = P.prob[P.n];
-  if (!make_map_bf16(&pr.a, A, M, P.K, lda, 64, 64) || !make_map_bf16(&pr.b, B, N, P.K, N, 64, 64) ||
-      !make_map_f32_3d(&pr.out, out, N, M, P.splits, N, (uint64_t)out_stride, 32, 32))
+  if (!make_map_bf16(&pr.a, A, M, P.K, lda, 64, 64) || !make_map_bf16(&pr.b, B, N, P.K, ldb, 64, 64) ||
+      !make_map_f32_3d(&pr.out, out_t, M, N, P.splits, M, (uint64_t)out_stride, 32, 32))
     return false;
-  pr.db = colsum_a;
+  pr.db = colsum_b;
   pr.db_stride = colsum_stride;
-  pr.db_from_a = 1;
+  pr.out_t = 1;
   pr.M = M;
   pr.N = N;
-  pr.tiles_n = (N + 255) / 256;
+  pr.tiles_n = (N + 256 * P.nh - 1) / (256 * P.nh);
   pr.tiles = ((M + 255) / 256) * pr.tiles_n * P.splits;
   P.total += pr.tiles;
   ++P.n;

@@ -13,9 +13,9 @@ struct alignas(64) PdwProblem {
   CUtensorMap a;           // X_l  [K][ldx] bf16, box {64, 64}: the MN-major A operand (M = in)
   CUtensorMap b;           // dZ_l [K][N]   bf16, box {64, 64}: the MN-major B operand
   CUtensorMap out;         // dW_l partial slices fp32 [S][M][N], box {32, 32, 1} (TMA stores)
-  float* db;               // db_l slice 0 ([N]; slice s at + s * db_stride)
+  float* db;               // db_l slice 0 ([N]; slice s at + s * db_stride), or null
   long long db_stride;     // floats between the db slices (the parameter count for dW / db)
-  int db_from_a;           // 1: "db" = the K sums of A per M column ([M], nh = 1 only), not of B
+  int out_t;               // 1: out is stored transposed, [S][N][M] (pdw_add_gemm_t)
   int M, N;                // dW_l is [M = in][N = out]
   int tiles_n, tiles;      // 256 x 256 nh tiles per slice along N; work items = tiles_m * tiles_n * S
 };
@@ -34,11 +34,13 @@ void pdw_init(PdwParams& P, int K, int splits, size_t split_stride);
 // buffer.  Returns false when a tensor map cannot be encoded or the table is full.
 bool pdw_add_problem(PdwParams& P, const __nv_bfloat16* X, int ldx, const __nv_bfloat16* dZ, int M, int N,
                      float* dW, float* db);
-// A general MN-major pair GEMM on the same engine: out[M][N] (fp32 slices [S][M][N], out_stride
-// floats apart) = sum_K A[K][M] B[K][N]; when colsum_a != nullptr also colsum_a[M] (slices
-// colsum_stride apart) = sum_K A[K][M].  Used for dPsi = W^T Phi from a stored W (nh must be 1).
-bool pdw_add_gemm(PdwParams& P, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, int M, int N, float* out,
-                  long long out_stride, float* colsum_a, long long colsum_stride);
+// The same engine as a general GEMM with a TRANSPOSED result: out_t[N][M] (fp32 slices
+// [S][N][M], out_stride floats apart) = (sum_K A[K][M] B[K][N])^T, and colsum_b[N] (slices
+// colsum_stride apart, or null) = sum_K B[K][N].  A: [K][lda] bf16, B: [K][ldb] bf16 (M, N
+// contiguous).  Used for dPsi = W^T Phi (A = Phi, B = the stored W: out_t = dPsi partials
+// [N][256], row-major like every other partial).
+bool pdw_add_gemm_t(PdwParams& P, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, int ldb, int M, int N,
+                    float* out_t, long long out_stride, float* colsum_b, long long colsum_stride);
 void pdw_set_nh(PdwParams& P, int nh);
 bool pdw_supported(int K, int splits);
 cudaError_t tc_pdw_launch(const PdwParams& P, int num_sms, cudaStream_t st);
