@@ -768,7 +768,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 128 * g2p::kNW
           if (r0 < p.Na) {
 #pragma unroll
             for (int c = 0; c < 2; ++c)
-              if (j0 + 64 * c < p.Nb) g2::tma_store_2d(&tmW, smem_u32(sW + c * W_CH), j0 + 64 * c, r0);
+              if (j0 + 64 * c < p.Nb && !(p.dbg & 8)) g2::tma_store_2d(&tmW, smem_u32(sW + c * W_CH), j0 + 64 * c, r0);
             g2::bulk_commit();
             g2::bulk_wait_read();
           }
@@ -1039,6 +1039,7 @@ cudaError_t tc_grad2p(int energy, const CUtensorMap& mD0, const CUtensorMap& mD1
                       const CUtensorMap& mS1, const CUtensorMap& mA0, const CUtensorMap& mA1, const Grad2Args& p0,
                       int grid, cudaStream_t st, const CUtensorMap* mW) {
   Grad2Args p = p0;
+  if (const char* d = std::getenv("CRL_G2P_DBG")) p.dbg = std::atoi(d);   // measurement ablations
   static const CUtensorMap kNoMap{};
   if (p.w_store && (mW == nullptr || p.nsides != 1)) return cudaErrorInvalidValue;
   const CUtensorMap& w = mW != nullptr ? *mW : kNoMap;
