@@ -9,8 +9,11 @@ tail -3 $OUT/pytest_gpu.log
 timeout 600 python bench.py > $OUT/bench_netscale.json 2> $OUT/bench_netscale.err; echo "bench rc=$?"
 bash scripts/gpu_r2_configs.sh ${1:-final}/cfg > $OUT/cfg.txt 2>&1
 bash scripts/gpu_r2_launches.sh ${1:-final}/ln > $OUT/launches.txt 2>&1
-for k in tc_grad2p_kernel tc_stats_kernel tc_pdw_kernel; do
+for k in tc_grad2p_kernel tc_stats_kernel; do
   bash scripts/gpu_r2_ncufull.sh ${1:-final}/ncu_$k "$k" 0 1 > /dev/null 2>&1
 done
+# tc_pdw_kernel runs twice per step: the stored-W column GEMM (first) and the dW / db launch
+bash scripts/gpu_r2_ncufull.sh ${1:-final}/ncu_tc_pdw_gemm "tc_pdw_kernel" 0 1 > /dev/null 2>&1
+bash scripts/gpu_r2_ncufull.sh ${1:-final}/ncu_tc_pdw_kernel "tc_pdw_kernel" 1 1 > /dev/null 2>&1
 bash scripts/gpu_r2_ncufull.sh ${1:-final}/ncu_pg "tc_pgemm_kernel" 1 2 > /dev/null 2>&1
 ls $OUT
