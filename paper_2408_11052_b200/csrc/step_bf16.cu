@@ -58,6 +58,8 @@ cudaError_t launch_rowstat_bf16(const __nv_bfloat16*, int, int, int, float*, int
 cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st);
 cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st,
                                const MergeLoss* loss);
+cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st,
+                               const MergeLoss* loss, int nsides);
 }  // namespace tc
 }  // namespace crl
 
@@ -777,6 +779,9 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
                                            ctx->g2_A1, ga, ctx->g2_grid, st, ctx->g2_wsym ? &ctx->g2_Wmap : nullptr));
     else CU(tc::tc_grad2(k.energy, ctx->g2_B0, ctx->g2_B1, ga, ctx->g2_grid, st));
     // symmetric energies at W = 1: side 1's weights are W^T -> dPsi = W^T Phi (+ column sums of W)
+    // on the pair engine (64 items: 10 pairs idle), the row-side merge (+ loss) beside it on st2
+    const bool wsym_split = ctx->g2_wsym && st != st2 && !std::getenv("CRL_NO_G2_MERGE_SPLIT");
+    if (wsym_split) fork2(ctx, st, st2);
     if (ctx->g2_wsym) { CU(tc::tc_pdw_launch(ctx->pdw_g, ctx->num_sms, st)); ++nl; }
     const float Cdiag = invN * (c_f + c_b);
     tc::GradMergeArgs m0{s0.part_da, s0.part_rs, ctx->phi_outb, s0.a_stat, ctx->psi_outb_g, ctx->stat_psi, row_off,
@@ -792,8 +797,15 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
     ml.lr = ctx->lse_row; ml.lc = ctx->lse_col; ml.part = ctx->loss_part; ml.ticket = ctx->loss_ticket;
     ml.acc = ctx->loss_acc; ml.out = loss_out; ml.skip = ctx->skip; ml.adam_t = ctx->adam_t; ml.status = ctx->status;
     ml.invN = invN; ml.c_f = lsgn * c_f; ml.c_b = lsgn * c_b; ml.beta = k.beta_lse; ml.finalize = !ctx->dist;
-    CU(tc::launch_grad_merge2(k.energy, m0, m1, st, &ml));
-    nl += 2;
+    if (wsym_split) {
+      CU(tc::launch_grad_merge2(k.energy, m0, m0, st2, &ml, 1));
+      CU(tc::launch_grad_merge2(k.energy, m1, m1, st, nullptr, 1));
+      join2(ctx, st, st2);
+      nl += 3;
+    } else {
+      CU(tc::launch_grad_merge2(k.energy, m0, m1, st, &ml));
+      nl += 2;
+    }
     if (ctx->dist) {
       NC(ncclAllReduce(ctx->loss_acc, ctx->loss_acc, 3, ncclFloat32, ncclSum, ctx->comm, st));
       CU(launch_loss_finalize(ctx->loss_acc, invN, lsgn * c_f, lsgn * c_b, k.beta_lse, loss_out, ctx->skip,

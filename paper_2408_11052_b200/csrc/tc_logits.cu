@@ -683,8 +683,9 @@ cudaError_t launch_grad_merge(int energy, const float* part, const float* prs, c
 // row side (g0) and column side (g1) of the fused gradient pass, one launch (+ the loss when
 // loss != nullptr: grad2 path)
 cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st,
-                               const MergeLoss* loss) {
-  const dim3 grid((max(g0.Na, g1.Na) * 32 + 255) / 256, 2);
+                               const MergeLoss* loss, int nsides) {
+  // nsides = 1: g0 only (the caller runs the other side as its own launch, e.g. on another stream)
+  const dim3 grid(((nsides == 1 ? g0.Na : max(g0.Na, g1.Na)) * 32 + 255) / 256, nsides == 1 ? 1 : 2);
   const MergeLoss L = loss ? *loss : MergeLoss{};
   if (energy == CRL_ENERGY_L2) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_L2>, grid, dim3(256), 0, st, g0, g1, L);
   if (energy == CRL_ENERGY_L2SQ)
@@ -692,8 +693,12 @@ cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMe
   if (energy == CRL_ENERGY_COS) return launch_pdl(grad_merge2_kernel<CRL_ENERGY_COS>, grid, dim3(256), 0, st, g0, g1, L);
   return launch_pdl(grad_merge2_kernel<CRL_ENERGY_DOT>, grid, dim3(256), 0, st, g0, g1, L);
 }
+cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st,
+                               const MergeLoss* loss) {
+  return launch_grad_merge2(energy, g0, g1, st, loss, 2);
+}
 cudaError_t launch_grad_merge2(int energy, const GradMergeArgs& g0, const GradMergeArgs& g1, cudaStream_t st) {
-  return launch_grad_merge2(energy, g0, g1, st, nullptr);
+  return launch_grad_merge2(energy, g0, g1, st, nullptr, 2);
 }
 
 cudaError_t launch_rowstat_bf16(const __nv_bfloat16* x, int N, int D, int energy, float* out, int* fac_ok,
