@@ -920,6 +920,16 @@ def test_critic_step_bf16_d256_stored_w(energy, loss, beta, wsym, monkeypatch):
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL, encoder_grads=False)
 
 
+@pytest.mark.parametrize("batch", [256, 300, 640])
+def test_critic_step_bf16_d256_stored_w_small(batch, monkeypatch):
+    """The stored-W path at its smallest batches: one row-block pair (256), a half-empty second
+    pair whose rank-1 rows are all past the batch (300: its W stores are skipped, its columns
+    clipped) and 2.5 pairs (640), each with the row-side merge on the second stream; outputs
+    dPhi / dPsi and the loss against the oracle (encoder gradients: see stored_w above)."""
+    cfg = crl_synth.preset("ant", batch=batch, width=128, repr_dim=256, precision="bf16")
+    _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL, encoder_grads=False)
+
+
 @pytest.mark.parametrize("energy", ["l2sq", "dot"])
 def test_critic_step_bf16_width1024_stored_w_energies(energy):
     """The stored-W gradient path's full pre-Adam gradient (every W, b of both encoders) for the
