@@ -920,6 +920,28 @@ def test_critic_step_bf16_d256_stored_w(energy, loss, beta, wsym, monkeypatch):
     _critic_parity(cfg, tol_loss=BF16_TOL, tol_grad=BF16_TOL, encoder_grads=False)
 
 
+def test_critic_step_bf16_netscale_shapes_bitwise_deterministic():
+    """Two fresh contexts, same parameters and batch, at the 4 x 1024 / D = 256 shapes: the loss,
+    dPhi, dPsi and the whole pre-Adam gradient agree bit for bit -- the stored-W pass and its
+    column GEMM (fixed K slices), the row-side merge on the second stream, the ticketed loss and
+    the dW slices summed in a fixed order are deterministic (no float atomics on this path)."""
+    cfg = crl_synth.preset("netscale", batch=1024)
+    s, a, g = crl_synth.random_batch(cfg, 1024, seed=21)
+    outs = []
+    for _ in range(2):
+        ctx, _p = make_ctx(cfg)
+        loss = torch.zeros(4, device="cuda")
+        grads = torch.zeros(ctx.n_params, device="cuda")
+        ctx.critic_step(*(torch.from_numpy(x).cuda() for x in (s, a, g)), loss, grads)
+        torch.cuda.synchronize()
+        assert ctx.status() == 0
+        outs.append([loss.cpu().numpy(), ctx.debug_tensor("dphi").cpu().numpy(),
+                     ctx.debug_tensor("dpsi").cpu().numpy(), grads.cpu().numpy()])
+        del ctx
+    for x, y in zip(*outs):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
 @pytest.mark.parametrize("batch", [256, 300, 640])
 def test_critic_step_bf16_d256_stored_w_small(batch, monkeypatch):
     """The stored-W path at its smallest batches: one row-block pair (256), a half-empty second
