@@ -3,7 +3,7 @@
 set -u
 OUT=gpurun_out/${1:-pdwabl}
 mkdir -p $OUT
-for d in 0 1 2 4 6; do
+for d in ${DBGS:-0 1 2 4 5 6 7}; do
   C="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --bulk-updates 0 --profile-steps 0"
   CRL_PDW_DBG=$d ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tc_pdw --csv \
       --log-file $OUT/l$d.csv $C > /dev/null 2>&1
