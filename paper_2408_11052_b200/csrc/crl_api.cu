@@ -694,6 +694,30 @@ crl_status crl::enqueue_allreduce_adam(crl_ctx* ctx, cudaStream_t st, cudaStream
                                   int* nl) {
   const crl_config& k = ctx->cfg;
   const size_t n = ctx->sizes.n_params;
+  if (!ctx->dist && ctx->pdw_split) {
+    // phi's parameters [0, lo) after phi's dW launch (st), the rest after psi's (st2, which also
+    // waits for st: [lo, n_phi) is phi's when n_phi is not a multiple of 256)
+    const size_t lo = (size_t)ctx->phi_plan.n_params / 256 * 256;
+    cudaEventRecord(ctx->ev_side, st);
+    if (st2 != st) cudaStreamWaitEvent(st2, ctx->ev_side, 0);
+    {
+      Stage sg(ctx, st, "adam");
+      CU(launch_adam_range(ctx->mem.params, ctx->grads, ctx->dw_splits, n, ctx->mem.adam_m, ctx->mem.adam_v, lo,
+                           k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay, ctx->adam_t, ctx->skip,
+                           ctx->status, shadow, ctx->num_sms, keep_sum, st));
+    }
+    CU(launch_adam_range(ctx->mem.params + lo, ctx->grads + lo, ctx->dw_splits, n, ctx->mem.adam_m + lo,
+                         ctx->mem.adam_v + lo, n - lo, k.lr, k.adam_b1, k.adam_b2, k.adam_eps, k.weight_decay,
+                         ctx->adam_t, ctx->skip, ctx->status,
+                         shadow ? static_cast<void*>(static_cast<__nv_bfloat16*>(shadow) + lo) : nullptr,
+                         ctx->num_sms, keep_sum, st2));
+    if (st2 != st) {
+      cudaEventRecord(ctx->ev_join, st2);
+      cudaStreamWaitEvent(st, ctx->ev_join, 0);
+    }
+    *nl += 2;
+    return CRL_OK;
+  }
   if (!ctx->dist) {
     Stage sg(ctx, st, "adam");
     CU(launch_adam_ex(ctx->mem.params, ctx->grads, ctx->dw_splits, ctx->mem.adam_m, ctx->mem.adam_v, n, k.lr,

@@ -72,6 +72,9 @@ cudaError_t launch_adam(float*, float*, int, float*, float*, size_t, float, floa
                         float, const int*, const int*, int*, void*, int, cudaStream_t);
 cudaError_t launch_adam_ex(float*, float*, int, float*, float*, size_t, float, float, float, float,
                            float, const int*, const int*, int*, void*, int, int, cudaStream_t);
+cudaError_t launch_adam_range(float* p, float* g, int S, size_t gs, float* m, float* v, size_t n, float lr,
+                              float b1, float b2, float eps, float wd, const int* adam_t, const int* skip,
+                              int* status, void* shadow_bf16, int num_sms, int keep_sum, cudaStream_t st);
 namespace tc {
 bool tc_logits_supports(int D);
 int tc_logits_splits(int Na, int Nb, int D, int num_sms);
@@ -271,6 +274,10 @@ struct crl_ctx {
   tc::DwgParams dwg;
   bool use_pdw = false;            // wide encoders: dW / db on CTA pairs (tc_pdw.cu) instead of tc_dwg
   tc::PdwParams pdw;
+  // W = 1: phi's dW / db (pdw) and psi's (pdw_psi) as two launches on two streams, each
+  // followed by Adam over its encoder's parameters (the first Adam overlaps the other dW tail)
+  bool pdw_split = false;
+  tc::PdwParams pdw_psi;
   // cluster-split MLP chains for small batches (tc_cchain.cu): one launch per direction
   bool use_cchain = false;
   tc::CChainMaps cchain_fwd[2], cchain_bwd[2];

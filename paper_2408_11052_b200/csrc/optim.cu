@@ -105,7 +105,9 @@ __global__ void __launch_bounds__(256) adam_kernel(
     float* __restrict__ p, float* __restrict__ g, int S, float* __restrict__ m,
     float* __restrict__ v, size_t n, float lr, float b1, float b2, float eps, float wd,
     const int* __restrict__ adam_t, const int* __restrict__ skip, int* __restrict__ status,
-    __nv_bfloat16_raw* __restrict__ shadow, int keep_sum) {
+    __nv_bfloat16_raw* __restrict__ shadow, int keep_sum, size_t gs) {
+  // gs: floats between the split-K slices of g (the whole gradient's size when this launch
+  // updates a sub-range of it)
   pdl_wait();
   pdl_launch();
   if (*skip) return;
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(256) adam_kernel(
        i += (size_t)gridDim.x * blockDim.x) {
     float4 gv = reinterpret_cast<const float4*>(g)[i];
     for (int sl = 1; sl < S; ++sl) {                       // deterministic split-K sum
-      const float4 h = reinterpret_cast<const float4*>(g + (size_t)sl * n)[i];
+      const float4 h = reinterpret_cast<const float4*>(g + (size_t)sl * gs)[i];
       gv.x += h.x; gv.y += h.y; gv.z += h.z; gv.w += h.w;
     }
     if (S > 1 && keep_sum) reinterpret_cast<float4*>(g)[i] = gv;   // the reduced gradient, for grads_out
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(256) adam_kernel(
   for (size_t i = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {                // scalar path (n % 4 != 0)
     float gi = g[i];
-    for (int sl = 1; sl < S; ++sl) gi += g[(size_t)sl * n + i];
+    for (int sl = 1; sl < S; ++sl) gi += g[(size_t)sl * gs + i];
     if (S > 1) g[i] = gi;
     float mi = m[i], vi = v[i];
     const float pn = upd(p[i], gi, mi, vi);
@@ -290,7 +292,18 @@ cudaError_t launch_adam_ex(float* p, float* g, int S, float* m, float* v, size_t
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   return launch_pdl(adam_kernel, dim3((unsigned)blocks), dim3(256), 0, st, p, g, S, m, v, n, lr, b1, b2, eps,
-                    wd, adam_t, skip, status, reinterpret_cast<__nv_bfloat16_raw*>(shadow_bf16), keep_sum);
+                    wd, adam_t, skip, status, reinterpret_cast<__nv_bfloat16_raw*>(shadow_bf16), keep_sum, n);
+}
+// a sub-range [off, off + n) of the parameters whose gradient slices are gs floats apart
+cudaError_t launch_adam_range(float* p, float* g, int S, size_t gs, float* m, float* v, size_t n, float lr,
+                              float b1, float b2, float eps, float wd, const int* adam_t, const int* skip,
+                              int* status, void* shadow_bf16, int num_sms, int keep_sum, cudaStream_t st) {
+  size_t blocks = (n / 4 + 255) / 256 + 1;
+  size_t cap = (size_t)num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  return launch_pdl(adam_kernel, dim3((unsigned)blocks), dim3(256), 0, st, p, g, S, m, v, n, lr, b1, b2, eps,
+                    wd, adam_t, skip, status, reinterpret_cast<__nv_bfloat16_raw*>(shadow_bf16), keep_sum, gs);
 }
 
 }  // namespace crl

@@ -133,6 +133,8 @@ crl_status bf16_prepare(crl_ctx* ctx) {
   ctx->use_pdw = k.width >= 512 && tc::pdw_supported(k.batch_local, ctx->dw_splits);
   if (ctx->use_pdw) {
     tc::pdw_init(ctx->pdw, k.batch_local, ctx->dw_splits, ctx->sizes.n_params);
+    ctx->pdw_split = !ctx->dist && !std::getenv("CRL_NO_PDW_SPLIT");
+    if (ctx->pdw_split) tc::pdw_init(ctx->pdw_psi, k.batch_local, ctx->dw_splits, ctx->sizes.n_params);
     const EncoderPlan* plans[2] = {&ctx->phi_plan, &ctx->psi_plan};
     std::vector<crl_ctx::TcLayer>* tcs[2] = {&ctx->tc_phi, &ctx->tc_psi};
     __nv_bfloat16** Xb[2] = {ctx->phiXb, ctx->psiXb};
@@ -148,8 +150,9 @@ crl_status bf16_prepare(crl_ctx* ctx) {
     for (int e = 0; e < 2 && ctx->use_pdw; ++e)
       for (int l = natural ? 0 : (pass == 0 ? 1 : 0); l < (natural || pass == 0 ? L : 1); ++l) {
         const LayerPlan& Lp = plans[e]->layer[l];
-        if (!tc::pdw_add_problem(ctx->pdw, l == 0 ? x0[e] : Xb[e][l], l == 0 ? ld0[e] : k.width, (*tcs[e])[l].dz,
-                                 Lp.in, Lp.out, ctx->grads + Lp.w_off, ctx->grads + Lp.b_off)) {
+        if (!tc::pdw_add_problem(e == 1 && ctx->pdw_split ? ctx->pdw_psi : ctx->pdw, l == 0 ? x0[e] : Xb[e][l],
+                                 l == 0 ? ld0[e] : k.width, (*tcs[e])[l].dz, Lp.in, Lp.out, ctx->grads + Lp.w_off,
+                                 ctx->grads + Lp.b_off)) {
           ctx->use_pdw = false;                 // (alignment / table size): the grouped kernel
           break;
         }
@@ -869,7 +872,15 @@ crl_status enqueue_critic_bf16(crl_ctx* ctx, const float* s, const float* a, con
       CU(tc::tc_cchain_backward(ctx->cchain_bwd[0], ctx->cchain_bwd[1], ctx->cchain_bwd_p, st));
       ++nl; }
   }
-  if (ctx->use_pdw) {
+  if (ctx->use_pdw && ctx->pdw_split) {
+    // phi's dW / db on st, psi's on st2 (both persistent: psi's pairs start as phi's finish);
+    // Adam of each encoder follows its own launch (enqueue_allreduce_adam)
+    Stage sg(ctx, st, "dw_db_pairs");
+    fork2(ctx, st, st2);
+    CU(tc::tc_pdw_launch(ctx->pdw, ctx->num_sms, st));
+    CU(tc::tc_pdw_launch(ctx->pdw_psi, ctx->num_sms, st2));
+    nl += 2;
+  } else if (ctx->use_pdw) {
     // every dW_l and db_l of both encoders on CTA pairs (tc_pdw.cu)
     Stage sg(ctx, st, "dw_db_pairs");
     CU(tc::tc_pdw_launch(ctx->pdw, ctx->num_sms, st));
